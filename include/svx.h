@@ -1,0 +1,244 @@
+/*
+ * svx.h — C-ABI of the B200-native semvox voxel-integration hot path.
+ *
+ * This is the drop-in boundary: plain C types, plain pointers and sizes, no
+ * torch / Eigen / STL in any signature. The C++ mirror of the reference API
+ * (paper_2412_00291_b200/cpp/semvox_b200.hpp) and the Python host mirror
+ * (paper_2412_00291_b200/__init__.py) are thin layers over these entry points.
+ * Every function names the reference interface it replaces (paths relative to
+ * the reference repo, proj/...).
+ *
+ * Conventions
+ *   - Every entry point returns svx_status. 0 = ok; otherwise the matching
+ *     reference exception class (std::invalid_argument, CapacityError,
+ *     DataError; proj/include/semvox/types.hpp:20-27) or a CUDA failure.
+ *     svx_last_error() returns the message of the last failure on this thread.
+ *   - Poses are double R[9] (row-major) + t[3], sensor->world (semvox::Pose,
+ *     proj/include/semvox/types.hpp:16).
+ *   - One map = one CUDA device + one stream. Calls on a map are serialised
+ *     (the reference integrators are single-caller). Calls are
+ *     synchronous unless the name ends in _async.
+ *   - Host pointers are borrowed for the duration of the call.
+ */
+#ifndef SVX_H_
+#define SVX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SVX_OK = 0,
+    SVX_INVALID_ARGUMENT = 1, /* std::invalid_argument                          */
+    SVX_CAPACITY = 2,         /* semvox::CapacityError (types.hpp:20-22)        */
+    SVX_DATA = 3,             /* semvox::DataError (types.hpp:25-27)            */
+    SVX_CUDA = 4,             /* CUDA / NCCL runtime failure (no reference analogue) */
+    SVX_NOT_FOUND = 5         /* lookup of an unallocated block (find_block == nullptr) */
+} svx_status;
+
+/* semvox::MapConfig (proj/include/semvox/types.hpp:97-112); validated like
+ * MapConfig::validate(). */
+typedef struct {
+    float voxel_size;
+    float truncation;
+    int32_t num_labels;
+    uint32_t max_blocks;
+} svx_map_cfg;
+
+/* semvox::ProjectionModel (proj/include/semvox/scan_projection.hpp:16-38). */
+typedef struct {
+    int32_t width;
+    int32_t height_px;
+    double delta_phi;
+    double delta_theta;
+    double theta0;
+    double scale_f;
+    double offset_o;
+    double min_range;
+} svx_lidar_model;
+
+/* semvox::Pose = Eigen::Isometry3d: R row-major, then translation. */
+typedef struct {
+    double R[9];
+    double t[3];
+} svx_pose;
+
+/* semvox::IntegratorConfig (proj/include/semvox/tsdf_integrator.hpp:14-23). */
+enum { SVX_PROJECTIVE = 0, SVX_NON_PROJECTIVE = 1 };
+typedef struct {
+    int32_t mode;            /* SVX_NON_PROJECTIVE by default */
+    float truncation;        /* <= 0: use the map's truncation */
+    double max_range;        /* 70 */
+    double alpha_epsilon;    /* 1e-2 */
+    float min_weight_clamp;  /* 0.01 */
+    int32_t drop_unreliable; /* 0 */
+} svx_integrator_cfg;
+
+/* semvox::SemanticConfig (proj/include/semvox/semantic_integrator.hpp:31-38). */
+enum { SVX_OCCLUSION_SURROGATE = 0, SVX_OCCLUSION_RAYCAST = 1 };
+typedef struct {
+    int32_t use_bayes;          /* 1 */
+    float likelihood_floor;     /* 1e-3 */
+    float default_confidence;   /* 0.9 */
+    int32_t occlusion;          /* SVX_OCCLUSION_SURROGATE */
+} svx_semantic_cfg;
+
+/* semvox::FrameReport (proj/include/semvox/tsdf_integrator.hpp:25-32). */
+typedef struct {
+    int32_t frame;
+    uint64_t updated_voxels;
+    uint64_t new_blocks;
+    double elapsed_ms;
+} svx_frame_report;
+
+/* semvox::LabelImage (proj/include/semvox/semantic_integrator.hpp:14-26).
+ * confidence and prob_tensor may be NULL (absent). prob_tensor is [v][u][k]. */
+typedef struct {
+    int32_t width;
+    int32_t height;
+    const uint16_t* labels;
+    const float* confidence;
+    const float* prob_tensor;
+    double fx, fy, cx, cy;
+    svx_pose pose; /* camera -> world */
+    double max_depth;
+} svx_label_image;
+
+/* semvox::StoreStats (proj/include/semvox/voxel_store.hpp:40-44). */
+typedef struct {
+    uint64_t allocated_blocks;
+    uint64_t observed_voxels;
+    uint64_t memory_bytes;
+} svx_stats;
+
+/* One voxel as stored (semvox::TsdfVoxel, types.hpp:115-121): 20 bytes. */
+typedef struct {
+    float distance;
+    float weight;
+    float gradient[3];
+} svx_tsdf_voxel;
+
+typedef struct svx_map svx_map;
+typedef struct svx_scan svx_scan;
+
+/* ------------------------------------------------------------------ errors */
+/* Copies the last error message of this thread; returns its full length. */
+size_t svx_last_error(char* buf, size_t cap);
+const char* svx_status_name(svx_status s);
+/* Number of hot-path kernel launches issued by this process so far (all maps). */
+uint64_t svx_kernel_launches(void);
+
+/* ------------------------------------------------------------- storage */
+/* VoxelStore::VoxelStore(const MapConfig&) — voxel_store.hpp:51. */
+svx_status svx_map_create(const svx_map_cfg* cfg, int device, svx_map** out);
+svx_status svx_map_destroy(svx_map* map);
+svx_status svx_map_config(const svx_map* map, svx_map_cfg* out);
+/* The map's CUDA stream (cudaStream_t), for callers that time or order work
+ * around svx calls (e.g. torch.cuda.ExternalStream). */
+svx_status svx_map_get_stream(svx_map* map, void** stream);
+
+/* VoxelStore::get_or_allocate_block — voxel_store.cpp:9-23. *was_new may be NULL. */
+svx_status svx_get_or_allocate_block(svx_map* map, const int32_t bxyz[3], int32_t* was_new);
+/* VoxelStore::find_block != nullptr — voxel_store.cpp:25-35. *found = 0/1. */
+svx_status svx_has_block(svx_map* map, const int32_t bxyz[3], int32_t* found);
+/* VoxelStore::block_count — voxel_store.hpp:76-79. */
+svx_status svx_block_count(svx_map* map, uint64_t* n);
+/* VoxelStore::block_coords_sorted — voxel_store.cpp:71-80. out = n*3 int32 (x,y,z),
+ * sorted lexicographically. Pass out=NULL to query n. */
+svx_status svx_block_keys_sorted(svx_map* map, int32_t* out, uint64_t cap, uint64_t* n);
+/* Host mirror of one VoxelBlock (voxel_store.hpp:17-38): tsdf = 512 voxels
+ * (10240 B), sem = 512*K floats (only when *has_sem). Returns SVX_NOT_FOUND for an
+ * unallocated block. sem may be NULL. */
+svx_status svx_block_read(svx_map* map, const int32_t bxyz[3], svx_tsdf_voxel* tsdf,
+                          float* sem, int32_t* has_sem);
+/* Write-back of a host-mirrored block. has_sem=1 allocates the semantic layer if
+ * needed and writes sem (VoxelBlock::ensure_semantics + direct mutation). */
+svx_status svx_block_write(svx_map* map, const int32_t bxyz[3], const svx_tsdf_voxel* tsdf,
+                           const float* sem, int32_t has_sem);
+/* VoxelStore::lookup_voxel / tsdf_at — voxel_store.cpp:37-56. Batched: vxyz = n*3
+ * voxel coords; found[i] = 0 when the block is absent. probs (n*K) may be NULL; a
+ * block without a semantic layer yields the uniform distribution 1/K. */
+svx_status svx_lookup(svx_map* map, const int32_t* vxyz, uint64_t n, svx_tsdf_voxel* tsdf,
+                      float* probs, uint8_t* found);
+/* VoxelStore::stats — voxel_store.cpp:58-69 (memory_bytes is the GPU footprint). */
+svx_status svx_stats_get(svx_map* map, svx_stats* out);
+/* VoxelStore::save / load (SVOX1) — voxel_store.cpp:101-168. Byte-identical to
+ * the reference's snapshot of the same map. */
+svx_status svx_save(svx_map* map, const char* path);
+/* In-memory SVOX1 image; buf=NULL queries the size. */
+svx_status svx_save_mem(svx_map* map, uint8_t* buf, uint64_t cap, uint64_t* size);
+/* VoxelStore::load: creates a new map (max_blocks = cfg default 2^20 unless
+ * max_blocks > 0 is given, mirroring voxel_store.cpp:139-152). */
+svx_status svx_load(const char* path, int device, uint32_t max_blocks, svx_map** out);
+/* TsdfIntegrator / SemanticIntegrator::take_dirty_blocks — tsdf_integrator.cpp:260-264,
+ * semantic_integrator.cpp:167-171. which: 0 = TSDF pass, 1 = semantic pass.
+ * Sorted, unique; the list is cleared. out=NULL queries n without clearing. */
+svx_status svx_take_dirty_blocks(svx_map* map, int32_t which, int32_t* out, uint64_t cap,
+                                 uint64_t* n);
+
+/* --------------------------------------------------------- preprocessing */
+/* ScanImages on the device for one ProjectionModel (scan_projection.hpp:44-58).
+ * Validates the model like ProjectionModel::validate. The scan is bound to the
+ * map's device and stream. */
+svx_status svx_scan_create(svx_map* map, const svx_lidar_model* model, svx_scan** out);
+svx_status svx_scan_destroy(svx_scan* scan);
+/* project_cloud — scan_projection.cpp:39-76. points: n rows of `stride` floats
+ * (3 = xyz, 4 = KITTI xyzi), sensor frame. ptr_is_device: points already in HBM.
+ * Validates the pose (PosedCloud::validate_pose, scan_projection.hpp:65-69). */
+svx_status svx_project(svx_scan* scan, const float* points, uint64_t n, int32_t stride,
+                       int32_t ptr_is_device, const svx_pose* pose);
+/* compute_normal_image — scan_projection.cpp:86-109. */
+svx_status svx_compute_normals(svx_scan* scan);
+/* Upload host ScanImages (depth, and optionally normals n*3 + valid) — the
+ * integrate_frame(const ScanImages&) entry when the caller built images on host. */
+svx_status svx_scan_upload(svx_scan* scan, const float* depth, const float* height,
+                           const float* normals, const uint8_t* normal_valid);
+/* Download ScanImages; any output pointer may be NULL. */
+svx_status svx_scan_download(svx_scan* scan, float* depth, float* height, float* normals,
+                             uint8_t* normal_valid, uint64_t* dropped, int32_t* has_normals);
+
+/* ------------------------------------------------------------ integration */
+/* TsdfIntegrator::integrate_frame — tsdf_integrator.cpp:97-258 (band-limited
+ * DDA, own-pixel rule, accumulate-then-merge fold). The frame counter lives in
+ * the map (one TSDF integrator per map, as in cmd_integrate). */
+svx_status svx_integrate_scan(svx_map* map, svx_scan* scan, const svx_pose* pose,
+                              const svx_integrator_cfg* cfg, svx_frame_report* report);
+/* project_cloud + compute_normal_image + integrate_frame for one posed cloud —
+ * the per-frame body of cmd_integrate (semvox_main.cpp:122-124) in one call. */
+svx_status svx_integrate_cloud(svx_map* map, svx_scan* scan, const float* points, uint64_t n,
+                               int32_t stride, int32_t ptr_is_device, const svx_pose* pose,
+                               const svx_integrator_cfg* cfg, svx_frame_report* report);
+/* A sequence of posed clouds already resident in HBM: frame f uses points
+ * [offsets[f], offsets[f+1]) and poses[f]. No host synchronisation between
+ * frames unless pool growth is needed; reports[f] filled at the end. */
+svx_status svx_integrate_clouds_device(svx_map* map, svx_scan* scan, const float* d_points,
+                                       const uint64_t* offsets, int32_t stride,
+                                       const svx_pose* poses, int32_t n_frames,
+                                       const svx_integrator_cfg* cfg, svx_frame_report* reports);
+/* SemanticIntegrator::integrate_labels — semantic_integrator.cpp:91-165, with
+ * exact block-level frustum culling (results identical to the O(map) sweep). */
+svx_status svx_integrate_labels(svx_map* map, const svx_label_image* img,
+                                const svx_semantic_cfg* cfg, svx_frame_report* report);
+
+/* ------------------------------------------------------------- defaults */
+void svx_default_integrator_cfg(svx_integrator_cfg* cfg);
+void svx_default_semantic_cfg(svx_semantic_cfg* cfg);
+/* ProjectionModel::spinning — scan_projection.cpp:9-19. */
+svx_status svx_lidar_spinning(int32_t width, int32_t height_px, double fov_up_deg,
+                              double fov_down_deg, svx_lidar_model* out);
+
+/* ------------------------------------------------------------- sharding */
+/* Key sharding for multi-GPU: this map owns only blocks with
+ * owner(b) == rank among world ranks. world=1 owns everything. */
+svx_status svx_map_set_shard(svx_map* map, int32_t rank, int32_t world);
+/* owner(bxyz) under the same hash, for host-side routing and tests. */
+int32_t svx_block_owner(const int32_t bxyz[3], int32_t world);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SVX_H_ */

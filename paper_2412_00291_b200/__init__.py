@@ -1,0 +1,639 @@
+"""B200-native semvox voxel-integration hot path (arXiv 2412.00291).
+
+Python host mirror of the reference C++ API (proj/include/semvox/*.hpp) over the
+C-ABI in include/svx.h, backed by lib/libsvx_b200.so (sm_100a kernels). Same
+names, argument meaning and error behaviour as the reference:
+
+  reference (C++)                         here
+  ------------------------------------   -------------------------------------
+  MapConfig / VoxelStore                  MapConfig / VoxelStore
+  ProjectionModel::spinning               ProjectionModel.spinning
+  project_cloud / compute_normal_image    project_cloud / compute_normal_image
+  TsdfIntegrator::integrate_frame         TsdfIntegrator.integrate_frame
+  SemanticIntegrator::integrate_labels    SemanticIntegrator.integrate_labels
+  CapacityError / DataError /             CapacityError / DataError /
+  std::invalid_argument                   InvalidArgument (a ValueError)
+
+There is no CPU fallback: importing works without a GPU (so the library can be
+inspected), but every compute call goes to the CUDA library and fails loudly if
+it is missing or no device is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libsvx_b200.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "svx.h")
+
+# ----------------------------------------------------------------- errors
+
+
+class SvxError(RuntimeError):
+    pass
+
+
+class InvalidArgument(SvxError, ValueError):
+    """std::invalid_argument"""
+
+
+class CapacityError(SvxError):
+    """semvox::CapacityError (types.hpp:20-22)"""
+
+
+class DataError(SvxError):
+    """semvox::DataError (types.hpp:25-27)"""
+
+
+class CudaError(SvxError):
+    pass
+
+
+class NotFound(SvxError, KeyError):
+    pass
+
+
+_STATUS = {1: InvalidArgument, 2: CapacityError, 3: DataError, 4: CudaError, 5: NotFound}
+
+# ---------------------------------------------------------------- structs
+
+
+class MapCfg(C.Structure):
+    _fields_ = [("voxel_size", C.c_float), ("truncation", C.c_float),
+                ("num_labels", C.c_int32), ("max_blocks", C.c_uint32)]
+
+
+class LidarModel(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height_px", C.c_int32), ("delta_phi", C.c_double),
+                ("delta_theta", C.c_double), ("theta0", C.c_double), ("scale_f", C.c_double),
+                ("offset_o", C.c_double), ("min_range", C.c_double)]
+
+
+class PoseC(C.Structure):
+    _fields_ = [("R", C.c_double * 9), ("t", C.c_double * 3)]
+
+
+class IntegratorCfg(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("truncation", C.c_float), ("max_range", C.c_double),
+                ("alpha_epsilon", C.c_double), ("min_weight_clamp", C.c_float),
+                ("drop_unreliable", C.c_int32)]
+
+
+class SemanticCfg(C.Structure):
+    _fields_ = [("use_bayes", C.c_int32), ("likelihood_floor", C.c_float),
+                ("default_confidence", C.c_float), ("occlusion", C.c_int32)]
+
+
+class FrameReportC(C.Structure):
+    _fields_ = [("frame", C.c_int32), ("updated_voxels", C.c_uint64),
+                ("new_blocks", C.c_uint64), ("elapsed_ms", C.c_double)]
+
+
+class LabelImageC(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32),
+                ("labels", C.POINTER(C.c_uint16)), ("confidence", C.POINTER(C.c_float)),
+                ("prob_tensor", C.POINTER(C.c_float)), ("fx", C.c_double), ("fy", C.c_double),
+                ("cx", C.c_double), ("cy", C.c_double), ("pose", PoseC),
+                ("max_depth", C.c_double)]
+
+
+class StatsC(C.Structure):
+    _fields_ = [("allocated_blocks", C.c_uint64), ("observed_voxels", C.c_uint64),
+                ("memory_bytes", C.c_uint64)]
+
+
+TSDF_DTYPE = np.dtype([("distance", "<f4"), ("weight", "<f4"), ("gradient", "<f4", (3,))])
+BLOCK_VOXELS = 512
+
+# ------------------------------------------------------------------ loading
+
+_lib: Optional[C.CDLL] = None
+
+
+def _sig(lib: C.CDLL) -> None:
+    P = C.c_void_p
+    S = C.c_int
+    f = {
+        "svx_last_error": (C.c_size_t, [C.c_char_p, C.c_size_t]),
+        "svx_status_name": (C.c_char_p, [C.c_int]),
+        "svx_kernel_launches": (C.c_uint64, []),
+        "svx_map_create": (S, [C.POINTER(MapCfg), C.c_int, C.POINTER(P)]),
+        "svx_map_destroy": (S, [P]),
+        "svx_map_config": (S, [P, C.POINTER(MapCfg)]),
+        "svx_map_get_stream": (S, [P, C.POINTER(P)]),
+        "svx_get_or_allocate_block": (S, [P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+        "svx_has_block": (S, [P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+        "svx_block_count": (S, [P, C.POINTER(C.c_uint64)]),
+        "svx_block_keys_sorted": (S, [P, P, C.c_uint64, C.POINTER(C.c_uint64)]),
+        "svx_block_read": (S, [P, C.POINTER(C.c_int32), P, P, C.POINTER(C.c_int32)]),
+        "svx_block_write": (S, [P, C.POINTER(C.c_int32), P, P, C.c_int32]),
+        "svx_lookup": (S, [P, P, C.c_uint64, P, P, P]),
+        "svx_stats_get": (S, [P, C.POINTER(StatsC)]),
+        "svx_save": (S, [P, C.c_char_p]),
+        "svx_save_mem": (S, [P, P, C.c_uint64, C.POINTER(C.c_uint64)]),
+        "svx_load": (S, [C.c_char_p, C.c_int, C.c_uint32, C.POINTER(P)]),
+        "svx_take_dirty_blocks": (S, [P, C.c_int32, P, C.c_uint64, C.POINTER(C.c_uint64)]),
+        "svx_scan_create": (S, [P, C.POINTER(LidarModel), C.POINTER(P)]),
+        "svx_scan_destroy": (S, [P]),
+        "svx_project": (S, [P, P, C.c_uint64, C.c_int32, C.c_int32, C.POINTER(PoseC)]),
+        "svx_compute_normals": (S, [P]),
+        "svx_scan_upload": (S, [P, P, P, P, P]),
+        "svx_scan_download": (S, [P, P, P, P, P, C.POINTER(C.c_uint64), C.POINTER(C.c_int32)]),
+        "svx_integrate_scan": (S, [P, P, C.POINTER(PoseC), C.POINTER(IntegratorCfg),
+                                   C.POINTER(FrameReportC)]),
+        "svx_integrate_cloud": (S, [P, P, P, C.c_uint64, C.c_int32, C.c_int32, C.POINTER(PoseC),
+                                    C.POINTER(IntegratorCfg), C.POINTER(FrameReportC)]),
+        "svx_integrate_clouds_device": (S, [P, P, P, P, C.c_int32, P, C.c_int32,
+                                            C.POINTER(IntegratorCfg), P]),
+        "svx_integrate_labels": (S, [P, C.POINTER(LabelImageC), C.POINTER(SemanticCfg),
+                                     C.POINTER(FrameReportC)]),
+        "svx_default_integrator_cfg": (None, [C.POINTER(IntegratorCfg)]),
+        "svx_default_semantic_cfg": (None, [C.POINTER(SemanticCfg)]),
+        "svx_lidar_spinning": (S, [C.c_int32, C.c_int32, C.c_double, C.c_double,
+                                   C.POINTER(LidarModel)]),
+        "svx_map_set_shard": (S, [P, C.c_int32, C.c_int32]),
+        "svx_block_owner": (C.c_int32, [C.POINTER(C.c_int32), C.c_int32]),
+    }
+    for name, (res, args) in f.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+
+
+def lib() -> C.CDLL:
+    """The CUDA library. Raises if it was not built (no CPU fallback exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(make -C paper_2412_00291_b200/csrc)")
+        _lib = C.CDLL(LIB_PATH)
+        _sig(_lib)
+    return _lib
+
+
+def declared_symbols() -> list[str]:
+    """Function names declared in include/svx.h (the drop-in boundary)."""
+    import re
+    text = open(HEADER_PATH).read()
+    return sorted(set(re.findall(r"^\s*(?:svx_status|size_t|const char\*|uint64_t|void|int32_t)"
+                                 r"\s+(svx_\w+)\s*\(", text, re.M)))
+
+
+def _check(status: int) -> None:
+    if status == 0:
+        return
+    buf = C.create_string_buffer(1024)
+    lib().svx_last_error(buf, 1024)
+    raise _STATUS.get(status, SvxError)(buf.value.decode(errors="replace"))
+
+
+def kernel_launches() -> int:
+    return int(lib().svx_kernel_launches())
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _i3(b) -> C.Array:
+    return (C.c_int32 * 3)(*[int(x) for x in b])
+
+# ------------------------------------------------------------------ config
+
+
+@dataclass
+class MapConfig:
+    """semvox::MapConfig (types.hpp:97-112)."""
+    voxel_size: float = 0.25
+    truncation: float = 1.25
+    num_labels: int = 2
+    max_blocks: int = 1 << 20
+
+    def c(self) -> MapCfg:
+        return MapCfg(self.voxel_size, self.truncation, self.num_labels, self.max_blocks)
+
+
+@dataclass
+class ProjectionModel:
+    """semvox::ProjectionModel (scan_projection.hpp:16-38)."""
+    width: int = 1024
+    height_px: int = 64
+    delta_phi: float = 2.0 * np.pi / 1024
+    delta_theta: float = 0.0
+    theta0: float = 0.0
+    scale_f: float = 256.0
+    offset_o: float = 0.0
+    min_range: float = 0.3
+
+    @staticmethod
+    def spinning(width: int, height_px: int, fov_up_deg: float, fov_down_deg: float
+                 ) -> "ProjectionModel":
+        # ProjectionModel::spinning (scan_projection.cpp:9-19), same double arithmetic
+        pi = 3.141592653589793
+        m = ProjectionModel(width=width, height_px=height_px)
+        m.delta_phi = 2.0 * pi / width
+        m.theta0 = (90.0 - fov_up_deg) * pi / 180.0
+        m.delta_theta = (fov_up_deg + fov_down_deg) * pi / 180.0 / height_px
+        m.validate()
+        return m
+
+    def validate(self) -> None:
+        if self.width <= 0 or self.height_px <= 0:
+            raise InvalidArgument("projection model: empty image")
+        if abs(self.width * self.delta_phi - 2.0 * np.pi) > 1e-6:
+            raise InvalidArgument("projection model: width * delta_phi must equal 2*pi")
+        if not self.delta_theta > 0.0:
+            raise InvalidArgument("projection model: delta_theta must be > 0")
+
+    def c(self) -> LidarModel:
+        return LidarModel(self.width, self.height_px, self.delta_phi, self.delta_theta,
+                          self.theta0, self.scale_f, self.offset_o, self.min_range)
+
+    def key(self) -> tuple:
+        return (self.width, self.height_px, self.delta_phi, self.delta_theta, self.theta0,
+                self.min_range)
+
+
+PROJECTIVE, NON_PROJECTIVE = 0, 1
+SURROGATE, RAYCAST = 0, 1
+
+
+@dataclass
+class IntegratorConfig:
+    """semvox::IntegratorConfig (tsdf_integrator.hpp:14-23)."""
+    mode: int = NON_PROJECTIVE
+    truncation: float = 0.0
+    max_range: float = 70.0
+    alpha_epsilon: float = 1e-2
+    min_weight_clamp: float = 0.01
+    drop_unreliable: bool = False
+
+    def c(self) -> IntegratorCfg:
+        return IntegratorCfg(self.mode, self.truncation, self.max_range, self.alpha_epsilon,
+                             self.min_weight_clamp, int(self.drop_unreliable))
+
+
+@dataclass
+class SemanticConfig:
+    """semvox::SemanticConfig (semantic_integrator.hpp:31-38)."""
+    use_bayes: bool = True
+    likelihood_floor: float = 1e-3
+    default_confidence: float = 0.9
+    occlusion: int = SURROGATE
+
+    def c(self) -> SemanticCfg:
+        return SemanticCfg(int(self.use_bayes), self.likelihood_floor, self.default_confidence,
+                           self.occlusion)
+
+
+@dataclass
+class FrameReport:
+    """semvox::FrameReport (tsdf_integrator.hpp:25-32)."""
+    frame: int = -1
+    updated_voxels: int = 0
+    new_blocks: int = 0
+    elapsed_ms: float = 0.0
+
+    def json_line(self) -> str:
+        # FrameReport::json_line (tsdf_integrator.cpp:12-18)
+        return ('{"frame":%d,"updated_voxels":%d,"new_blocks":%d,"elapsed_ms":%.3f}'
+                % (self.frame, self.updated_voxels, self.new_blocks, self.elapsed_ms))
+
+    @staticmethod
+    def of(r: FrameReportC) -> "FrameReport":
+        return FrameReport(r.frame, r.updated_voxels, r.new_blocks, r.elapsed_ms)
+
+
+def pose_c(R=None, t=None) -> PoseC:
+    """(R 3x3, t 3) -> svx_pose. A 4x4 matrix may be passed as R."""
+    R = np.eye(3) if R is None else np.asarray(R, dtype=np.float64)
+    if R.shape == (4, 4):
+        R, t = R[:3, :3], R[:3, 3]
+    t = np.zeros(3) if t is None else np.asarray(t, dtype=np.float64)
+    p = PoseC()
+    p.R[:] = [float(x) for x in R.reshape(9)]
+    p.t[:] = [float(x) for x in t.reshape(3)]
+    return p
+
+
+@dataclass
+class Pose:
+    R: np.ndarray = field(default_factory=lambda: np.eye(3))
+    t: np.ndarray = field(default_factory=lambda: np.zeros(3))
+
+    def c(self) -> PoseC:
+        return pose_c(self.R, self.t)
+
+# -------------------------------------------------------------- the store
+
+
+class VoxelStore:
+    """semvox::VoxelStore (voxel_store.hpp:49-103), resident in HBM on `device`."""
+
+    def __init__(self, cfg: MapConfig = None, device: int = 0, _handle=None):
+        self._h = C.c_void_p()
+        if _handle is not None:
+            self._h = _handle
+            c = MapCfg()
+            _check(lib().svx_map_config(self._h, C.byref(c)))
+            self.cfg = MapConfig(c.voxel_size, c.truncation, c.num_labels, c.max_blocks)
+        else:
+            self.cfg = cfg or MapConfig()
+            _check(lib().svx_map_create(C.byref(self.cfg.c()), device, C.byref(self._h)))
+        self.device = device
+        self._scans: dict = {}
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) and self._h.value:
+            for s in self._scans.values():
+                lib().svx_scan_destroy(s)
+            self._scans.clear()
+            _check(lib().svx_map_destroy(self._h))
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def config(self) -> MapConfig:
+        return self.cfg
+
+    @property
+    def handle(self):
+        return self._h
+
+    def stream_ptr(self) -> int:
+        s = C.c_void_p()
+        _check(lib().svx_map_get_stream(self._h, C.byref(s)))
+        return int(s.value or 0)
+
+    def scan(self, model: ProjectionModel):
+        """Device ScanImages buffers for `model` (cached per model)."""
+        k = model.key()
+        if k not in self._scans:
+            s = C.c_void_p()
+            _check(lib().svx_scan_create(self._h, C.byref(model.c()), C.byref(s)))
+            self._scans[k] = s
+        return self._scans[k]
+
+    def set_shard(self, rank: int, world: int) -> None:
+        _check(lib().svx_map_set_shard(self._h, rank, world))
+
+    def get_or_allocate_block(self, bc) -> bool:
+        nw = C.c_int32()
+        _check(lib().svx_get_or_allocate_block(self._h, _i3(bc), C.byref(nw)))
+        return bool(nw.value)
+
+    def find_block(self, bc) -> bool:
+        f = C.c_int32()
+        _check(lib().svx_has_block(self._h, _i3(bc), C.byref(f)))
+        return bool(f.value)
+
+    def block_count(self) -> int:
+        n = C.c_uint64()
+        _check(lib().svx_block_count(self._h, C.byref(n)))
+        return int(n.value)
+
+    def block_coords_sorted(self) -> np.ndarray:
+        n = C.c_uint64()
+        _check(lib().svx_block_keys_sorted(self._h, None, 0, C.byref(n)))
+        out = np.zeros((n.value, 3), dtype=np.int32)
+        _check(lib().svx_block_keys_sorted(self._h, _ptr(out), n.value, C.byref(n)))
+        return out
+
+    def read_block(self, bc):
+        """(tsdf[512] structured array, semantics [512,K] or None)."""
+        t = np.zeros(BLOCK_VOXELS, dtype=TSDF_DTYPE)
+        s = np.zeros((BLOCK_VOXELS, self.cfg.num_labels), dtype=np.float32)
+        hs = C.c_int32()
+        _check(lib().svx_block_read(self._h, _i3(bc), _ptr(t), _ptr(s), C.byref(hs)))
+        return t, (s if hs.value else None)
+
+    def write_block(self, bc, tsdf: np.ndarray, semantics: Optional[np.ndarray] = None,
+                    ensure_semantics: bool = False) -> None:
+        t = np.ascontiguousarray(tsdf, dtype=TSDF_DTYPE)
+        s = None if semantics is None else np.ascontiguousarray(semantics, dtype=np.float32)
+        hs = int(ensure_semantics or semantics is not None)
+        _check(lib().svx_block_write(self._h, _i3(bc), _ptr(t), _ptr(s), hs))
+
+    def lookup_voxels(self, coords, with_probs: bool = True):
+        """Batched VoxelStore::lookup_voxel: (found[n], tsdf[n], probs[n,K])."""
+        v = np.ascontiguousarray(np.asarray(coords, dtype=np.int32).reshape(-1, 3))
+        n = v.shape[0]
+        t = np.zeros(n, dtype=TSDF_DTYPE)
+        p = np.zeros((n, self.cfg.num_labels), dtype=np.float32) if with_probs else None
+        f = np.zeros(n, dtype=np.uint8)
+        if n:
+            _check(lib().svx_lookup(self._h, _ptr(v), n, _ptr(t), _ptr(p), _ptr(f)))
+        return f.astype(bool), t, p
+
+    def lookup_voxel(self, vc):
+        f, t, p = self.lookup_voxels([vc])
+        if not f[0]:
+            return None
+        return t[0], p[0]
+
+    def stats(self) -> StatsC:
+        s = StatsC()
+        _check(lib().svx_stats_get(self._h, C.byref(s)))
+        return s
+
+    def save(self, path: str) -> None:
+        _check(lib().svx_save(self._h, str(path).encode()))
+
+    def save_bytes(self) -> bytes:
+        n = C.c_uint64()
+        _check(lib().svx_save_mem(self._h, None, 0, C.byref(n)))
+        buf = np.zeros(n.value, dtype=np.uint8)
+        _check(lib().svx_save_mem(self._h, _ptr(buf), n.value, C.byref(n)))
+        return buf.tobytes()
+
+    @staticmethod
+    def load(path: str, device: int = 0, max_blocks: int = 0) -> "VoxelStore":
+        h = C.c_void_p()
+        _check(lib().svx_load(str(path).encode(), device, max_blocks, C.byref(h)))
+        return VoxelStore(device=device, _handle=h)
+
+    def take_dirty_blocks(self, which: int) -> np.ndarray:
+        n = C.c_uint64()
+        _check(lib().svx_take_dirty_blocks(self._h, which, None, 0, C.byref(n)))
+        out = np.zeros((n.value, 3), dtype=np.int32)
+        _check(lib().svx_take_dirty_blocks(self._h, which, _ptr(out), n.value, C.byref(n)))
+        return out
+
+# ----------------------------------------------------------- preprocessing
+
+
+@dataclass
+class ScanImages:
+    """semvox::ScanImages (scan_projection.hpp:44-58) mirrored to host."""
+    model: ProjectionModel
+    depth: np.ndarray
+    height: np.ndarray
+    normals: Optional[np.ndarray] = None
+    normal_valid: Optional[np.ndarray] = None
+    dropped: int = 0
+
+    @property
+    def width(self):
+        return self.model.width
+
+    @property
+    def height_px(self):
+        return self.model.height_px
+
+    def has_normals(self) -> bool:
+        return self.normals is not None
+
+
+def _as_points(points) -> tuple[np.ndarray, int]:
+    a = np.ascontiguousarray(np.asarray(points, dtype=np.float32))
+    if a.ndim != 2 or a.shape[1] not in (3, 4):
+        raise InvalidArgument("points must be (n, 3) or (n, 4) float32")
+    return a, a.shape[1]
+
+
+def _download(store: VoxelStore, model: ProjectionModel, normals: bool = True) -> ScanImages:
+    s = store.scan(model)
+    P = model.width * model.height_px
+    d = np.zeros(P, np.float32)
+    h = np.zeros(P, np.float32)
+    n = np.zeros((P, 3), np.float32)
+    v = np.zeros(P, np.uint8)
+    dropped = C.c_uint64()
+    hn = C.c_int32()
+    _check(lib().svx_scan_download(s, _ptr(d), _ptr(h), _ptr(n), _ptr(v), C.byref(dropped),
+                                   C.byref(hn)))
+    img = ScanImages(model, d, h, None, None, int(dropped.value))
+    if normals and hn.value:
+        img.normals, img.normal_valid = n, v
+    return img
+
+
+def project_cloud(points, pose, model: ProjectionModel, store: VoxelStore,
+                  with_normals: bool = True) -> ScanImages:
+    """project_cloud (+ compute_normal_image) on the device of `store`."""
+    a, stride = _as_points(points)
+    pc = pose if isinstance(pose, PoseC) else (pose.c() if isinstance(pose, Pose) else pose_c(pose))
+    s = store.scan(model)
+    _check(lib().svx_project(s, _ptr(a), a.shape[0], stride, 0, C.byref(pc)))
+    return _download(store, model, normals=with_normals)
+
+
+def compute_normal_image(img: ScanImages, store: VoxelStore) -> ScanImages:
+    s = store.scan(img.model)
+    _check(lib().svx_scan_upload(s, _ptr(np.ascontiguousarray(img.depth, np.float32)),
+                                 _ptr(np.ascontiguousarray(img.height, np.float32)), None, None))
+    _check(lib().svx_compute_normals(s))
+    out = _download(store, img.model)
+    img.normals, img.normal_valid = out.normals, out.normal_valid
+    return img
+
+# -------------------------------------------------------------- integrators
+
+
+class TsdfIntegrator:
+    """semvox::TsdfIntegrator (tsdf_integrator.hpp:75-91)."""
+
+    def __init__(self, store: VoxelStore, cfg: IntegratorConfig = None):
+        self.store = store
+        self.cfg = cfg or IntegratorConfig()
+        if not self.cfg.alpha_epsilon > 0.0:
+            raise InvalidArgument("alpha_epsilon must be > 0")
+
+    def integrate_frame(self, images: ScanImages, pose) -> FrameReport:
+        s = self.store.scan(images.model)
+        nrm = None if images.normals is None else np.ascontiguousarray(images.normals, np.float32)
+        val = None if images.normal_valid is None else np.ascontiguousarray(images.normal_valid,
+                                                                           np.uint8)
+        _check(lib().svx_scan_upload(s, _ptr(np.ascontiguousarray(images.depth, np.float32)),
+                                     None, _ptr(nrm), _ptr(val)))
+        rep = FrameReportC()
+        pc = pose if isinstance(pose, PoseC) else (pose.c() if isinstance(pose, Pose) else pose_c(pose))
+        _check(lib().svx_integrate_scan(self.store.handle, s, C.byref(pc), C.byref(self.cfg.c()),
+                                        C.byref(rep)))
+        return FrameReport.of(rep)
+
+    def integrate_cloud(self, points, pose, model: ProjectionModel) -> FrameReport:
+        """project_cloud + compute_normal_image + integrate_frame in one device call."""
+        a, stride = _as_points(points)
+        pc = pose if isinstance(pose, PoseC) else (pose.c() if isinstance(pose, Pose) else pose_c(pose))
+        s = self.store.scan(model)
+        rep = FrameReportC()
+        _check(lib().svx_integrate_cloud(self.store.handle, s, _ptr(a), a.shape[0], stride, 0,
+                                         C.byref(pc), C.byref(self.cfg.c()), C.byref(rep)))
+        return FrameReport.of(rep)
+
+    def take_dirty_blocks(self) -> np.ndarray:
+        return self.store.take_dirty_blocks(0)
+
+
+@dataclass
+class LabelImage:
+    """semvox::LabelImage (semantic_integrator.hpp:14-26)."""
+    width: int
+    height: int
+    labels: np.ndarray
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    pose: object = None
+    confidence: Optional[np.ndarray] = None
+    prob_tensor: Optional[np.ndarray] = None
+    max_depth: float = 30.0
+
+
+class SemanticIntegrator:
+    """semvox::SemanticIntegrator (semantic_integrator.hpp:50-63)."""
+
+    def __init__(self, store: VoxelStore, cfg: SemanticConfig = None):
+        self.store = store
+        self.cfg = cfg or SemanticConfig()
+
+    def integrate_labels(self, img: LabelImage) -> FrameReport:
+        K = self.store.cfg.num_labels
+        P = img.width * img.height
+        lbl = np.ascontiguousarray(np.asarray(img.labels, np.uint16).reshape(-1))
+        if lbl.size != P:
+            raise InvalidArgument("labels size mismatch")
+        conf = None
+        if img.confidence is not None and np.asarray(img.confidence).size == P:
+            conf = np.ascontiguousarray(np.asarray(img.confidence, np.float32).reshape(-1))
+        ten = None
+        if img.prob_tensor is not None and np.asarray(img.prob_tensor).size == P * K:
+            ten = np.ascontiguousarray(np.asarray(img.prob_tensor, np.float32).reshape(-1))
+        pc = img.pose if isinstance(img.pose, PoseC) else (
+            img.pose.c() if isinstance(img.pose, Pose) else pose_c(img.pose))
+        li = LabelImageC(img.width, img.height, lbl.ctypes.data_as(C.POINTER(C.c_uint16)),
+                         None if conf is None else conf.ctypes.data_as(C.POINTER(C.c_float)),
+                         None if ten is None else ten.ctypes.data_as(C.POINTER(C.c_float)),
+                         img.fx, img.fy, img.cx, img.cy, pc, img.max_depth)
+        rep = FrameReportC()
+        _check(lib().svx_integrate_labels(self.store.handle, C.byref(li), C.byref(self.cfg.c()),
+                                          C.byref(rep)))
+        return FrameReport.of(rep)
+
+    def take_dirty_blocks(self) -> np.ndarray:
+        return self.store.take_dirty_blocks(1)
+
+
+def block_owner(bc, world: int) -> int:
+    return int(lib().svx_block_owner(_i3(bc), world))
+
+
+__all__ = [
+    "MapConfig", "ProjectionModel", "IntegratorConfig", "SemanticConfig", "FrameReport",
+    "VoxelStore", "ScanImages", "project_cloud", "compute_normal_image", "TsdfIntegrator",
+    "SemanticIntegrator", "LabelImage", "Pose", "pose_c", "CapacityError", "DataError",
+    "InvalidArgument", "CudaError", "NotFound", "PROJECTIVE", "NON_PROJECTIVE", "SURROGATE",
+    "RAYCAST", "TSDF_DTYPE", "lib", "declared_symbols", "kernel_launches", "block_owner",
+]

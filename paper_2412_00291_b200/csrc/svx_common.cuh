@@ -1,0 +1,242 @@
+// Shared device-side definitions of the B200 semvox hot path.
+//
+// Arithmetic contract: this code is compiled with --fmad=false, so every
+// double/float expression below rounds exactly like the reference's Release
+// build (-O3, no -march => no FMA contraction). Reductions follow Eigen's order:
+// 3-term dot products are (a0*b0 + a1*b1) + a2*b2; Isometry*p = t + R p;
+// normalized() divides by sqrt(squaredNorm). Transcendentals on the integer
+// decision paths (pixel of a point / of a voxel centre) run in FP32 with a
+// proven error margin and fall back to FP64 near a pixel boundary.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/svx.h"
+
+namespace svx {
+
+constexpr int kBlockSide = 8;
+constexpr int kBlockVoxels = 512;
+constexpr double kPi = 3.14159265358979323846;
+
+// Packed block key: 21 bits per axis, biased by 2^20 so that unsigned order of
+// the packed value equals the lexicographic (x, y, z) order of BlockCoord
+// (types.hpp:59-68). Valid block coordinates: [-2^20, 2^20).
+constexpr int kKeyBits = 21;
+constexpr int32_t kKeyBias = 1 << 20;
+constexpr uint64_t kEmptyKey = ~0ull;
+constexpr uint32_t kInvalid = 0xFFFFFFFFu;
+
+__host__ __device__ inline bool key_in_range(int32_t b) {
+    return b >= -kKeyBias && b < kKeyBias;
+}
+__host__ __device__ inline uint64_t pack_key(int32_t bx, int32_t by, int32_t bz) {
+    return (uint64_t(uint32_t(bx + kKeyBias)) << (2 * kKeyBits)) |
+           (uint64_t(uint32_t(by + kKeyBias)) << kKeyBits) | uint64_t(uint32_t(bz + kKeyBias));
+}
+__host__ __device__ inline void unpack_key(uint64_t k, int32_t& bx, int32_t& by, int32_t& bz) {
+    const uint64_t m = (1ull << kKeyBits) - 1;
+    bx = int32_t((k >> (2 * kKeyBits)) & m) - kKeyBias;
+    by = int32_t((k >> kKeyBits) & m) - kKeyBias;
+    bz = int32_t(k & m) - kKeyBias;
+}
+// Fibonacci hashing into a power-of-two table.
+__host__ __device__ inline uint32_t hash_slot(uint64_t key, int log2cap) {
+    return uint32_t((key * 0x9E3779B97F4A7C15ull) >> (64 - log2cap));
+}
+// Shard owner of a block: a mixed hash, uniform over ranks.
+__host__ __device__ inline int32_t owner_of(uint64_t key, int32_t world) {
+    uint64_t h = key ^ (key >> 31);
+    h *= 0xD6E8FEB86659FD93ull;
+    h ^= h >> 32;
+    return world <= 1 ? 0 : int32_t(h % uint64_t(world));
+}
+
+struct d3 {
+    double x, y, z;
+};
+
+__host__ __device__ inline d3 mk(double x, double y, double z) { return d3{x, y, z}; }
+__host__ __device__ inline double dot3(d3 a, d3 b) { return (a.x * b.x + a.y * b.y) + a.z * b.z; }
+__host__ __device__ inline d3 sub3(d3 a, d3 b) { return d3{a.x - b.x, a.y - b.y, a.z - b.z}; }
+__host__ __device__ inline d3 add3(d3 a, d3 b) { return d3{a.x + b.x, a.y + b.y, a.z + b.z}; }
+__host__ __device__ inline d3 scale3(double s, d3 a) { return d3{s * a.x, s * a.y, s * a.z}; }
+__host__ __device__ inline d3 div3(d3 a, double s) { return d3{a.x / s, a.y / s, a.z / s}; }
+__host__ __device__ inline d3 neg3(d3 a) { return d3{-a.x, -a.y, -a.z}; }
+
+// Rigid transform, row-major R; inverse precomputed on the host exactly like
+// Eigen's Isometry::inverse(): (R^T, (-R^T) t).
+struct Pose {
+    double R[9];
+    double t[3];
+};
+
+__host__ __device__ inline d3 matvec(const double* R, d3 p) {
+    return d3{(R[0] * p.x + R[1] * p.y) + R[2] * p.z, (R[3] * p.x + R[4] * p.y) + R[5] * p.z,
+              (R[6] * p.x + R[7] * p.y) + R[8] * p.z};
+}
+// Isometry * p = t + (R p)   (Eigen transform_right_product_impl)
+__host__ __device__ inline d3 xform(const Pose& T, d3 p) {
+    const d3 rp = matvec(T.R, p);
+    return d3{T.t[0] + rp.x, T.t[1] + rp.y, T.t[2] + rp.z};
+}
+__host__ __device__ inline Pose inverse_pose(const Pose& T) {
+    Pose inv;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) inv.R[3 * i + j] = T.R[3 * j + i];
+    double negRt[9];
+    for (int k = 0; k < 9; ++k) negRt[k] = -inv.R[k];
+    const d3 ti = matvec(negRt, d3{T.t[0], T.t[1], T.t[2]});
+    inv.t[0] = ti.x;
+    inv.t[1] = ti.y;
+    inv.t[2] = ti.z;
+    return inv;
+}
+
+// ProjectionModel plus derived constants for the FP32 fast path.
+struct Model {
+    int32_t W, H;
+    double dphi, dtheta, theta0, min_range;
+    float inv_dphi_f, inv_dtheta_f, theta0_f;
+    float margin_u, margin_v;  // pixel-coordinate error bound of the FP32 path
+};
+
+// project_point (scan_projection.cpp:21-37). Returns 1 with (u, v) on success.
+// Pixel indices are computed in FP32 (atan2f/acosf) when the FP32 value is
+// provably on the same side of every pixel boundary as the exact value; near a
+// boundary (|frac| < margin) the FP64 formula of the reference is evaluated.
+__device__ inline int project_point(d3 p, const Model& m, int& u, int& v, double& range) {
+    range = sqrt(dot3(p, p));
+    if (!isfinite(range) || range < m.min_range) return 0;
+    const float xf = float(p.x), yf = float(p.y);
+    const float cz = float(p.z / range);
+    const float uf = (float(kPi) - atan2f(yf, xf)) * m.inv_dphi_f;
+    const float vf = (acosf(fminf(fmaxf(cz, -1.f), 1.f)) - m.theta0_f) * m.inv_dtheta_f;
+    const float fu = uf - floorf(uf), fv = vf - floorf(vf);
+    int ui, vi;
+    if (fabsf(cz) < 0.9f && fu > m.margin_u && fu < 1.f - m.margin_u && fv > m.margin_v &&
+        fv < 1.f - m.margin_v && isfinite(uf) && isfinite(vf)) {
+        ui = int(floorf(uf));
+        vi = int(floorf(vf));
+    } else {
+        const double az = atan2(p.y, p.x);
+        ui = int(floor((kPi - az) / m.dphi));
+        double c = p.z / range;
+        c = c < -1.0 ? -1.0 : (1.0 < c ? 1.0 : c);
+        vi = int(floor((acos(c) - m.theta0) / m.dtheta));
+    }
+    ui %= m.W;
+    if (ui < 0) ui += m.W;
+    if (vi < 0 || vi >= m.H) return 0;
+    u = ui;
+    v = vi;
+    return 1;
+}
+
+// world_to_voxel (types.hpp:168-173)
+__device__ inline void world_to_voxel(d3 p, double inv, int32_t c[3]) {
+    c[0] = int32_t(floor(p.x * inv + 0.5));
+    c[1] = int32_t(floor(p.y * inv + 0.5));
+    c[2] = int32_t(floor(p.z * inv + 0.5));
+}
+
+// block_of / local_index for kBlockSide = 8: floor_div == arithmetic shift,
+// nonneg_mod == & 7 on two's complement (types.hpp:35-44, 81-89).
+__host__ __device__ inline int32_t block_coord(int32_t c) { return c >> 3; }
+__host__ __device__ inline int local_linear(int32_t x, int32_t y, int32_t z) {
+    return (x & 7) + 8 * (y & 7) + 64 * (z & 7);
+}
+
+// ----------------------------------------------------------------- hash
+struct HashView {
+    uint64_t* keys;  // kEmptyKey = free
+    uint32_t* vals;  // pool index of the block in the slot
+    int log2cap;
+    uint32_t mask;
+};
+
+__device__ inline uint32_t hash_find(const HashView& h, uint64_t key) {
+    uint32_t s = hash_slot(key, h.log2cap);
+    for (uint32_t probe = 0; probe <= h.mask; ++probe) {
+        const uint64_t k = __ldcg(&h.keys[s]);
+        if (k == key) return s;
+        if (k == kEmptyKey) return kInvalid;
+        s = (s + 1) & h.mask;
+    }
+    return kInvalid;
+}
+
+// Returns the slot; *inserted = 1 when this thread claimed it.
+__device__ inline uint32_t hash_insert(const HashView& h, uint64_t key, int* inserted) {
+    uint32_t s = hash_slot(key, h.log2cap);
+    *inserted = 0;
+    for (uint32_t probe = 0; probe <= h.mask; ++probe) {
+        uint64_t k = __ldcg(&h.keys[s]);
+        if (k == key) return s;
+        if (k == kEmptyKey) {
+            const unsigned long long old =
+                atomicCAS(reinterpret_cast<unsigned long long*>(&h.keys[s]), kEmptyKey, key);
+            if (old == kEmptyKey) {
+                *inserted = 1;
+                return s;
+            }
+            if (old == key) return s;
+        }
+        s = (s + 1) & h.mask;
+    }
+    return kInvalid;
+}
+
+// ------------------------------------------------------------ counters
+// Per-map device counters (one 64-byte line each group).
+enum Counter : int {
+    C_BLOCKS = 0,       // allocated blocks (pool high-water mark)
+    C_SEM = 1,          // allocated semantic layers
+    C_TOUCHED = 2,      // blocks touched by the current frame
+    C_UPDATED = 3,      // voxels updated by the current pass
+    C_FALLBACK = 4,     // voxels that need the multi-ray fallback
+    C_RECORDS = 5,      // fallback visit records
+    C_ERR_KEY = 6,      // block coordinate out of key range
+    C_ERR_HASH = 7,     // hash table full
+    C_TIES = 8,         // pixels with a possible exact range tie
+    C_DROPPED = 9,      // points dropped by project_point
+    C_CAND = 10,        // semantic candidate blocks
+    C_ERR_CONF = 11,    // confidence outside [0, 1]
+    C_SEM_UPDATED = 12,
+    C_FRAME = 13,       // frame serial (stamp for touched detection)
+    C_REC_OVERFLOW = 14,
+    kNumCounters = 16
+};
+
+__device__ inline uint32_t warp_agg_add(uint32_t* ctr, uint32_t n) {
+    // warp-aggregated atomicAdd; returns this lane's base offset
+    const unsigned active = __activemask();
+    const int lane = threadIdx.x & 31;
+    uint32_t base = 0;
+    const int leader = __ffs(active) - 1;
+    // exclusive prefix over the active lanes, in lane order
+    uint32_t prefix = 0, total = 0;
+    for (int l = 0; l < 32; ++l) {
+        if (!((active >> l) & 1u)) continue;
+        const uint32_t nl = __shfl_sync(active, n, l);
+        if (l < lane) prefix += nl;
+        total += nl;
+    }
+    if (lane == leader && total) base = atomicAdd(ctr, total);
+    base = __shfl_sync(active, base, leader);
+    return base + prefix;
+}
+
+// Single-item variant: one atomic per warp (count of active lanes with pred).
+__device__ inline uint32_t warp_agg_inc(uint32_t* ctr) {
+    const unsigned active = __activemask();
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(active) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(ctr, uint32_t(__popc(active)));
+    base = __shfl_sync(active, base, leader);
+    return base + __popc(active & ((1u << lane) - 1u));
+}
+
+}  // namespace svx

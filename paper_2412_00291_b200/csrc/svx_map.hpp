@@ -1,0 +1,170 @@
+// Host-side objects behind the C-ABI: svx_map (one voxel map on one device)
+// and svx_scan (device ScanImages for one ProjectionModel).
+//
+// HBM layout of a map:
+//   keys[cap] u64 / vals[cap] u32      open-addressing block hash (linear probing,
+//                                      cap = pow2 >= 2*max_blocks), key = packed (x,y,z)
+//   tsdf pool   [max_blocks][512] x 20 B  AoS TsdfVoxel, exactly the SVOX1 block body;
+//                                      virtual range reserved once, physical memory
+//                                      mapped on demand (CUDA VMM) so addresses are stable
+//   sem pool    [layers][512][K] f32   lazily allocated semantic layers (VMM as above)
+//   block_keys[idx], sem_idx[idx], dirty flags[idx]   per pool block
+//   frame scratch: stamp[cap] u32, touched[cap] u32 (slots touched by this frame),
+//                  vmask[cap][32] u32 (16 words touched-voxel bits + 16 words fallback bits)
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/svx.h"
+#include "svx_common.cuh"
+
+namespace svx {
+
+struct Error : std::runtime_error {
+    svx_status status;
+    Error(svx_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+void cuda_check(cudaError_t e, const char* what);
+#define SVX_CUDA(call) ::svx::cuda_check((call), #call)
+
+// Growable device array with a stable base address (CUDA virtual memory
+// management): reserve once, map physical chunks as the high-water mark grows.
+class VmmArray {
+public:
+    VmmArray() = default;
+    ~VmmArray();
+    VmmArray(const VmmArray&) = delete;
+    VmmArray& operator=(const VmmArray&) = delete;
+
+    void reserve(int device, size_t max_bytes);
+    // Ensures [0, bytes) is mapped. Never shrinks.
+    void ensure(size_t bytes);
+    void* base() const { return reinterpret_cast<void*>(base_); }
+    size_t mapped() const { return mapped_; }
+
+private:
+    int device_ = 0;
+    CUdeviceptr base_ = 0;
+    size_t reserved_ = 0, mapped_ = 0, gran_ = 0;
+    std::vector<std::pair<CUmemGenericAllocationHandle, size_t>> chunks_;
+};
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        if (count <= n) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        SVX_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+}  // namespace svx
+
+struct svx_scan {
+    svx_map* map = nullptr;
+    svx_lidar_model model{};
+    svx::Model dm{};
+    int P = 0;
+    svx::DevBuf<double> dirs;     // P x 3 back_project directions (host libm, bit-exact)
+    svx::DevBuf<float> depth;     // P
+    svx::DevBuf<float> height;    // P
+    svx::DevBuf<float> normals;   // 3P (sensor frame)
+    svx::DevBuf<uint8_t> valid;   // P
+    svx::DevBuf<unsigned long long> pixkey;  // P: (range bits << 32) | point index
+    svx::DevBuf<unsigned long long> lexkey;  // P: tie-break scratch
+    svx::DevBuf<uint8_t> tie;     // P: possible exact-range tie
+    svx::DevBuf<uint32_t> pix_of_pt;  // per input point: pixel index or kInvalid
+    svx::DevBuf<float> points;    // staging for host points
+    bool has_normals = false;
+    uint64_t dropped = 0;
+    uint64_t n_points = 0;
+};
+
+struct svx_map {
+    svx_map_cfg cfg{};
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = true;
+    int32_t shard_rank = 0, shard_world = 1;
+
+    // hash
+    int log2cap = 0;
+    uint32_t cap = 0;
+    uint64_t* keys = nullptr;
+    uint32_t* vals = nullptr;
+    // pool
+    svx::VmmArray tsdf_pool;   // svx_tsdf_voxel[blocks][512]
+    svx::VmmArray sem_pool;    // float[layers][512*K]
+    size_t block_bytes = 0, layer_bytes = 0;
+    uint64_t* block_keys = nullptr;  // [max_blocks]
+    uint32_t* sem_idx = nullptr;     // [max_blocks]
+    uint8_t* dirty = nullptr;        // [2][max_blocks]
+    // frame scratch
+    uint32_t* stamp = nullptr;
+    uint32_t* touched = nullptr;
+    uint32_t* vmask = nullptr;       // [cap][32]
+    svx::DevBuf<unsigned long long> records, records_alt;
+    svx::DevBuf<uint8_t> sort_tmp;
+    svx::DevBuf<uint32_t> cand;      // semantic candidate blocks
+    svx::DevBuf<uint16_t> lbl;
+    svx::DevBuf<float> conf, tensor;
+    svx::DevBuf<float> like_table;   // [K+1][K] label -> likelihood at default confidence
+    // counters
+    uint32_t* d_ctr = nullptr;       // device
+    uint32_t* h_ctr = nullptr;       // pinned mirror
+    uint32_t frame_serial = 0;
+    int32_t tsdf_frames = 0, sem_frames = 0;
+    uint64_t n_blocks = 0;           // host copy of C_BLOCKS after the last sync
+    uint64_t n_layers = 0;
+};
+
+namespace svx {
+
+// Pool growth policy: keep at least `blocks` blocks of TSDF mapped.
+void ensure_blocks(svx_map* m, uint64_t blocks);
+void ensure_layers(svx_map* m, uint64_t layers);
+// Copies counters to the pinned mirror and synchronises the map stream.
+void sync_counters(svx_map* m);
+void count_launch(uint64_t n = 1);
+
+inline svx_tsdf_voxel* tsdf_base(svx_map* m) {
+    return static_cast<svx_tsdf_voxel*>(m->tsdf_pool.base());
+}
+inline float* sem_base(svx_map* m) { return static_cast<float*>(m->sem_pool.base()); }
+inline HashView hash_view(svx_map* m) { return HashView{m->keys, m->vals, m->log2cap, m->cap - 1}; }
+
+Model make_model(const svx_lidar_model& lm);
+Pose to_pose(const svx_pose& p);
+void validate_pose(const svx_pose& p);
+
+// kernels' host launchers (svx_project.cu, svx_tsdf.cu, svx_semantic.cu, svx_store.cu)
+void launch_project(svx_scan* s, const float* d_pts, uint64_t n, int stride, const Pose& pose);
+void launch_normals(svx_scan* s);
+void run_integrate(svx_map* m, svx_scan* s, const Pose& pose, const svx_integrator_cfg& cfg,
+                   svx_frame_report* rep);
+void run_integrate_labels(svx_map* m, const svx_label_image& img, const svx_semantic_cfg& cfg,
+                          svx_frame_report* rep);
+uint64_t count_observed(svx_map* m);
+void launch_zero_blocks(svx_map* m, uint64_t first, uint64_t count);
+void rebuild_hash(svx_map* m);
+void gather_blocks(svx_map* m, const uint32_t* d_idx, uint64_t n, svx_tsdf_voxel* d_out);
+void lookup_voxels(svx_map* m, const int32_t* d_v, uint64_t n, svx_tsdf_voxel* d_out,
+                   float* d_probs, uint8_t* d_found);
+
+}  // namespace svx

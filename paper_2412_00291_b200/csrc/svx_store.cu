@@ -1,0 +1,310 @@
+// K7 and the block store: VMM-backed pools, hash maintenance, batched lookup,
+// observed-voxel count, dirty-block compaction (voxel_store.cpp:9-80).
+#include <cuda.h>
+
+#include <mutex>
+#include <string>
+
+#include "svx_map.hpp"
+
+namespace svx {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw Error(SVX_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+namespace {
+
+// Driver entry points fetched through the runtime, so the library does not
+// link libcuda (it loads on hosts without a driver; the GPU box has one).
+struct Drv {
+    decltype(&cuMemAddressReserve) reserve = nullptr;
+    decltype(&cuMemAddressFree) addr_free = nullptr;
+    decltype(&cuMemCreate) create = nullptr;
+    decltype(&cuMemRelease) release = nullptr;
+    decltype(&cuMemMap) map = nullptr;
+    decltype(&cuMemUnmap) unmap = nullptr;
+    decltype(&cuMemSetAccess) set_access = nullptr;
+    decltype(&cuMemGetAllocationGranularity) gran = nullptr;
+};
+
+const Drv& drv() {
+    static Drv d;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        auto get = [](const char* name, void** fn) {
+            cudaDriverEntryPointQueryResult q;
+            SVX_CUDA(cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q));
+            if (q != cudaDriverEntryPointSuccess)
+                throw Error(SVX_CUDA, std::string("driver entry point missing: ") + name);
+        };
+        get("cuMemAddressReserve", reinterpret_cast<void**>(&d.reserve));
+        get("cuMemAddressFree", reinterpret_cast<void**>(&d.addr_free));
+        get("cuMemCreate", reinterpret_cast<void**>(&d.create));
+        get("cuMemRelease", reinterpret_cast<void**>(&d.release));
+        get("cuMemMap", reinterpret_cast<void**>(&d.map));
+        get("cuMemUnmap", reinterpret_cast<void**>(&d.unmap));
+        get("cuMemSetAccess", reinterpret_cast<void**>(&d.set_access));
+        get("cuMemGetAllocationGranularity", reinterpret_cast<void**>(&d.gran));
+    });
+    return d;
+}
+
+void cu_check(CUresult r, const char* what) {
+    if (r != CUDA_SUCCESS) throw Error(SVX_CUDA, std::string(what) + " failed (CUresult " + std::to_string(int(r)) + ")");
+}
+
+CUmemAllocationProp prop_for(int device) {
+    CUmemAllocationProp p{};
+    p.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    p.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    p.location.id = device;
+    return p;
+}
+
+}  // namespace
+
+void VmmArray::reserve(int device, size_t max_bytes) {
+    device_ = device;
+    const CUmemAllocationProp p = prop_for(device);
+    cu_check(drv().gran(&gran_, &p, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED), "cuMemGetAllocationGranularity");
+    reserved_ = ((max_bytes + gran_ - 1) / gran_) * gran_;
+    if (reserved_ == 0) reserved_ = gran_;
+    cu_check(drv().reserve(&base_, reserved_, gran_, 0, 0), "cuMemAddressReserve");
+}
+
+void VmmArray::ensure(size_t bytes) {
+    if (bytes <= mapped_) return;
+    if (bytes > reserved_) throw Error(SVX_CAPACITY, "device pool reservation exceeded");
+    // grow geometrically (>= 1/4 of the mapped size) to keep mapping calls rare
+    size_t want = std::max(bytes, mapped_ + mapped_ / 4);
+    want = ((want + gran_ - 1) / gran_) * gran_;
+    if (want > reserved_) want = reserved_;
+    const size_t add = want - mapped_;
+    const CUmemAllocationProp p = prop_for(device_);
+    CUmemGenericAllocationHandle h;
+    cu_check(drv().create(&h, add, &p, 0), "cuMemCreate");
+    cu_check(drv().map(base_ + mapped_, add, 0, h, 0), "cuMemMap");
+    CUmemAccessDesc acc{};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = device_;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    cu_check(drv().set_access(base_ + mapped_, add, &acc, 1), "cuMemSetAccess");
+    chunks_.push_back({h, add});
+    mapped_ = want;
+}
+
+VmmArray::~VmmArray() {
+    if (!base_) return;
+    cudaDeviceSynchronize();
+    size_t off = 0;
+    for (auto& [h, sz] : chunks_) {
+        drv().unmap(base_ + off, sz);
+        drv().release(h);
+        off += sz;
+    }
+    drv().addr_free(base_, reserved_);
+}
+
+void ensure_blocks(svx_map* m, uint64_t blocks) {
+    if (blocks > m->cfg.max_blocks) blocks = m->cfg.max_blocks;
+    m->tsdf_pool.ensure(blocks * m->block_bytes);
+}
+
+void ensure_layers(svx_map* m, uint64_t layers) {
+    if (layers > m->cfg.max_blocks) layers = m->cfg.max_blocks;
+    m->sem_pool.ensure(layers * m->layer_bytes);
+}
+
+void sync_counters(svx_map* m) {
+    SVX_CUDA(cudaMemcpyAsync(m->h_ctr, m->d_ctr, sizeof(uint32_t) * kNumCounters,
+                             cudaMemcpyDeviceToHost, m->stream));
+    SVX_CUDA(cudaStreamSynchronize(m->stream));
+}
+
+namespace {
+
+constexpr int kThreads = 256;
+inline unsigned grid_for(uint64_t n) { return unsigned((n + kThreads - 1) / kThreads); }
+
+__global__ void k_rebuild(HashView h, const uint64_t* __restrict__ block_keys, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int ins = 0;
+    const uint32_t s = hash_insert(h, block_keys[i], &ins);
+    if (s != kInvalid) h.vals[s] = i;
+}
+
+__global__ void k_count_observed(const svx_tsdf_voxel* __restrict__ pool, uint64_t n_vox,
+                                 unsigned long long* __restrict__ out) {
+    uint32_t c = 0;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n_vox;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        c += pool[i].weight > 0.f ? 1u : 0u;
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, static_cast<unsigned long long>(c));
+}
+
+__global__ void k_find(HashView h, const uint64_t* __restrict__ q, uint32_t n,
+                       uint32_t* __restrict__ idx) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t s = hash_find(h, q[i]);
+    idx[i] = s == kInvalid ? kInvalid : h.vals[s];
+}
+
+__global__ void k_insert_one(HashView h, uint64_t key, uint64_t* __restrict__ block_keys,
+                             uint32_t* __restrict__ ctr, uint32_t* __restrict__ out) {
+    int ins = 0;
+    const uint32_t s = hash_insert(h, key, &ins);
+    if (s == kInvalid) {
+        *out = kInvalid;
+        return;
+    }
+    if (ins) {
+        const uint32_t idx = ctr[C_BLOCKS]++;
+        h.vals[s] = idx;
+        block_keys[idx] = key;
+    }
+    *out = h.vals[s];
+}
+
+__global__ void k_lookup(HashView h, const int32_t* __restrict__ v, uint64_t n,
+                         const svx_tsdf_voxel* __restrict__ pool, const float* __restrict__ sem,
+                         const uint32_t* __restrict__ sem_idx, int K,
+                         svx_tsdf_voxel* __restrict__ out, float* __restrict__ probs,
+                         uint8_t* __restrict__ found) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t x = v[3 * i], y = v[3 * i + 1], z = v[3 * i + 2];
+    const int32_t bx = block_coord(x), by = block_coord(y), bz = block_coord(z);
+    uint32_t s = kInvalid;
+    if (key_in_range(bx) && key_in_range(by) && key_in_range(bz)) s = hash_find(h, pack_key(bx, by, bz));
+    if (s == kInvalid) {
+        found[i] = 0;
+        return;
+    }
+    found[i] = 1;
+    const uint32_t idx = h.vals[s];
+    const int lin = local_linear(x, y, z);
+    out[i] = pool[uint64_t(idx) * kBlockVoxels + lin];
+    if (probs) {
+        const uint32_t sid = sem_idx[idx];
+        for (int k = 0; k < K; ++k)
+            probs[i * K + k] = sid == kInvalid ? 1.f / float(K)
+                                               : sem[(uint64_t(sid) * kBlockVoxels + lin) * K + k];
+    }
+}
+
+__global__ void k_fill_layer(float* __restrict__ layer, uint64_t n, float v) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        layer[i] = v;
+}
+
+}  // namespace
+
+void rebuild_hash(svx_map* m) {
+    SVX_CUDA(cudaMemsetAsync(m->keys, 0xFF, sizeof(uint64_t) * m->cap, m->stream));
+    if (m->n_blocks)
+        k_rebuild<<<grid_for(m->n_blocks), kThreads, 0, m->stream>>>(hash_view(m), m->block_keys,
+                                                                     uint32_t(m->n_blocks));
+    count_launch();
+    SVX_CUDA(cudaGetLastError());
+}
+
+void launch_zero_blocks(svx_map* m, uint64_t first, uint64_t count) {
+    if (!count) return;
+    SVX_CUDA(cudaMemsetAsync(tsdf_base(m) + first * kBlockVoxels, 0, count * m->block_bytes,
+                             m->stream));
+}
+
+uint64_t count_observed(svx_map* m) {
+    DevBuf<unsigned long long> acc;
+    acc.alloc(1);
+    SVX_CUDA(cudaMemsetAsync(acc.p, 0, 8, m->stream));
+    const uint64_t nv = m->n_blocks * kBlockVoxels;
+    if (nv)
+        k_count_observed<<<std::min<unsigned>(grid_for(nv), 148 * 16), kThreads, 0, m->stream>>>(
+            tsdf_base(m), nv, acc.p);
+    count_launch();
+    unsigned long long h = 0;
+    SVX_CUDA(cudaMemcpyAsync(&h, acc.p, 8, cudaMemcpyDeviceToHost, m->stream));
+    SVX_CUDA(cudaStreamSynchronize(m->stream));
+    acc.release();
+    return h;
+}
+
+// Pool indices of the given packed keys (kInvalid when absent).
+void find_blocks(svx_map* m, const uint64_t* h_keys, uint32_t n, uint32_t* h_idx) {
+    DevBuf<uint64_t> dk;
+    DevBuf<uint32_t> di;
+    dk.alloc(n);
+    di.alloc(n);
+    SVX_CUDA(cudaMemcpyAsync(dk.p, h_keys, 8ull * n, cudaMemcpyHostToDevice, m->stream));
+    k_find<<<grid_for(n), kThreads, 0, m->stream>>>(hash_view(m), dk.p, n, di.p);
+    count_launch();
+    SVX_CUDA(cudaMemcpyAsync(h_idx, di.p, 4ull * n, cudaMemcpyDeviceToHost, m->stream));
+    SVX_CUDA(cudaStreamSynchronize(m->stream));
+    dk.release();
+    di.release();
+}
+
+// get_or_allocate_block (voxel_store.cpp:9-23). Returns the pool index.
+uint32_t get_or_alloc_block(svx_map* m, uint64_t key, bool* was_new) {
+    uint32_t idx = kInvalid;
+    find_blocks(m, &key, 1, &idx);
+    if (was_new) *was_new = false;
+    if (idx != kInvalid) return idx;
+    if (m->n_blocks >= m->cfg.max_blocks)
+        throw Error(SVX_CAPACITY,
+                    "block budget exhausted (max_blocks = " + std::to_string(m->cfg.max_blocks) + ")");
+    ensure_blocks(m, m->n_blocks + 1);
+    DevBuf<uint32_t> out;
+    out.alloc(1);
+    k_insert_one<<<1, 1, 0, m->stream>>>(hash_view(m), key, m->block_keys, m->d_ctr, out.p);
+    count_launch();
+    SVX_CUDA(cudaMemcpyAsync(&idx, out.p, 4, cudaMemcpyDeviceToHost, m->stream));
+    SVX_CUDA(cudaStreamSynchronize(m->stream));
+    out.release();
+    if (idx == kInvalid) throw Error(SVX_CAPACITY, "block hash table full");
+    launch_zero_blocks(m, idx, 1);
+    m->n_blocks = uint64_t(idx) + 1;
+    if (was_new) *was_new = true;
+    return idx;
+}
+
+// Ensures a semantic layer exists for pool block idx (VoxelBlock::ensure_semantics).
+uint32_t ensure_layer(svx_map* m, uint32_t idx) {
+    uint32_t sid = kInvalid;
+    SVX_CUDA(cudaMemcpyAsync(&sid, m->sem_idx + idx, 4, cudaMemcpyDeviceToHost, m->stream));
+    SVX_CUDA(cudaStreamSynchronize(m->stream));
+    if (sid != kInvalid) return sid;
+    sid = uint32_t(m->n_layers);
+    ensure_layers(m, m->n_layers + 1);
+    const int K = m->cfg.num_labels;
+    const uint64_t nf = uint64_t(kBlockVoxels) * K;
+    k_fill_layer<<<64, kThreads, 0, m->stream>>>(sem_base(m) + uint64_t(sid) * nf, nf, 1.f / float(K));
+    count_launch();
+    SVX_CUDA(cudaMemcpyAsync(m->sem_idx + idx, &sid, 4, cudaMemcpyHostToDevice, m->stream));
+    m->n_layers++;
+    m->h_ctr[C_SEM] = uint32_t(m->n_layers);
+    SVX_CUDA(cudaMemcpyAsync(m->d_ctr + C_SEM, &m->h_ctr[C_SEM], 4, cudaMemcpyHostToDevice, m->stream));
+    SVX_CUDA(cudaStreamSynchronize(m->stream));
+    return sid;
+}
+
+void lookup_voxels(svx_map* m, const int32_t* d_v, uint64_t n, svx_tsdf_voxel* d_out,
+                   float* d_probs, uint8_t* d_found) {
+    if (!n) return;
+    k_lookup<<<grid_for(n), kThreads, 0, m->stream>>>(hash_view(m), d_v, n, tsdf_base(m),
+                                                      sem_base(m), m->sem_idx, m->cfg.num_labels,
+                                                      d_out, d_probs, d_found);
+    count_launch();
+    SVX_CUDA(cudaGetLastError());
+}
+
+}  // namespace svx
