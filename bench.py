@@ -1,0 +1,411 @@
+#!/usr/bin/env python
+"""Benchmark: points integrated/sec on BASELINE.json configs[1] (cfg2).
+
+cfg2 = synthetic 128-beam LiDAR (1024 x 128, +-22.5 deg, OS1-128 geometry),
+0.1 m voxels, tau = 0.5 m, 20 classes, 1000 scans along a 500 m street canyon.
+One STEP = one pass of the hot path (project_cloud + compute_normal_image +
+TsdfIntegrator::integrate_frame, i.e. the per-frame body of cmd_integrate,
+proj/tools/semvox_main.cpp:122-124) over `--scans-per-step` consecutive scans
+(default 100, so W=3 + K=7 steps = the 1000-scan sequence). Every step consumes
+fresh scans (157 MB of points per step > 126 MB L2) on a map that keeps growing
+(> 1 GB), so no step is served from L2.
+
+Legs (one JSON line, printed by rank 0):
+  value        device-resident scans, svx_integrate_clouds_device, CUDA events on
+               the map stream, max over ranks
+  e2e          the C-ABI call a user makes (svx_integrate_cloud) with HOST pinned
+               points, H2D + per-frame report D2H inside the timed region
+  roofline     dominant kernel group, algorithmic bytes / event time
+  cpu_baseline the reference's own code (oracle/_ref/libsemvox_ref.so, built from
+               /root/reference) on the host cores, on a bounded sample of cfg2
+--impl reference   only the reference CPU arm (rank 0), same metric and config.
+
+Multi-GPU (torchrun): the map is key-sharded (owner = hash(block) mod N); rank 0
+holds the scans and broadcasts each one with NCCL; every rank integrates the
+blocks it owns. `value` counts each input point once.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "points integrated/sec (and voxel updates/sec) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "points/s"
+WORKLOAD = ("cfg2: synthetic 128-beam LiDAR (1024x128, +-22.5 deg), 0.1 m voxels, tau 0.5 m, "
+            "20 classes, 1000 scans at 0.5 m spacing (street canyon), band-only TSDF "
+            "(non-projective, the reference's default)")
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms (recipe's clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.lines: list[str] = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------ reference arm
+
+def run_reference(args, world, rank):
+    """The reference's own CPU implementation (oracle/_ref/libsemvox_ref.so)."""
+    if rank != 0:
+        return 0
+    nproc = os.cpu_count() or 1
+    os.environ["SEMVOX_THREADS"] = str(nproc)  # read once by worker_count()
+    import paper_2412_00291_b200 as svx
+    from paper_2412_00291_b200 import workload as W
+    from oracle.bindings import RefMap, ref_available
+    if not ref_available():
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref/libsemvox_ref.so not built"}))
+        return 0
+    spp = args.ref_scans_per_step
+    n = (args.warmup + args.steps) * spp
+    wl = W.make(args.workload, max(n + args.ref_offset, 10))
+    frames = list(range(args.ref_offset, args.ref_offset + n))
+    scans = {i: p.numpy() for p, i in wl.scans(device="cpu", frames=frames)}
+    cfg = svx.MapConfig(wl.voxel_size, wl.truncation, wl.num_labels, 1 << 22)
+    icfg = svx.IntegratorConfig()
+    ref = RefMap(cfg)
+    pts = wall = upd = 0.0
+    step_ms = []
+    for s in range(args.warmup + args.steps):
+        sp = sw = su = 0.0
+        for i in frames[s * spp:(s + 1) * spp]:
+            rep, ms = ref.integrate_cloud(wl.model, scans[i], wl.pose(i), icfg)
+            sp += len(scans[i])
+            sw += ms
+            su += rep.updated_voxels
+        if s >= args.warmup:
+            pts += sp
+            wall += sw
+            upd += su
+            step_ms.append(sw)
+    value = pts / (wall / 1e3)
+    sample = (f"{args.steps} steps x {spp} scans of {args.workload} (frames "
+              f"{frames[args.warmup * spp]}..{frames[-1]} after {args.warmup * spp} warm-up "
+              f"scans), project_cloud + compute_normal_image + integrate_frame, "
+              f"SEMVOX_THREADS={nproc}")
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": float(np.mean(step_ms)),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "impl": "reference",
+           "config": {"workload": WORKLOAD, "scans_per_step": spp, "parallelism": "cpu threads"},
+           "voxel_updates_per_s": upd / (wall / 1e3),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": nproc, "kind": "reference",
+                            "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return 0
+
+
+def cpu_baseline(args, wl, scans_host):
+    """Reference CPU path on the box's host cores on a bounded sample (rank 0, N=1)."""
+    nproc = os.cpu_count() or 1
+    os.environ["SEMVOX_THREADS"] = str(nproc)
+    import paper_2412_00291_b200 as svx
+    from oracle.bindings import RefMap, ref_available
+    if not ref_available():
+        return {"value": None, "unit": UNIT, "cores": nproc, "kind": "reference",
+                "sample": "unavailable: oracle/_ref/libsemvox_ref.so not built"}
+    cfg = svx.MapConfig(wl.voxel_size, wl.truncation, wl.num_labels, 1 << 22)
+    ref = RefMap(cfg)
+    icfg = svx.IntegratorConfig()
+    keys = sorted(scans_host)
+    pts = wall = 0.0
+    used = []
+    t_start = time.time()
+    for j, i in enumerate(keys):
+        rep, ms = ref.integrate_cloud(wl.model, scans_host[i], wl.pose(i), icfg)
+        if j == 0:
+            continue  # first frame on an empty map: warm start, not timed
+        pts += len(scans_host[i])
+        wall += ms
+        used.append(i)
+        if time.time() - t_start > args.cpu_seconds or len(used) >= args.cpu_max_scans:
+            break
+    return {"value": pts / (wall / 1e3), "unit": UNIT, "cores": nproc, "kind": "reference",
+            "sample": (f"{len(used)} consecutive {args.workload} scans (frames {used[0]}..{used[-1]}, "
+                       f"{int(pts)} points, {wall / 1e3:.1f} s) after 1 untimed warm-start scan, "
+                       f"project_cloud + compute_normal_image + integrate_frame, reference's own "
+                       f"code at -O3, SEMVOX_THREADS={nproc}")}
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=7)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--scans-per-step", type=int, default=100)
+    ap.add_argument("--ref-scans-per-step", type=int, default=2)
+    ap.add_argument("--ref-offset", type=int, default=300)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--cpu-max-scans", type=int, default=40)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile-json", default="")
+    args = ap.parse_args()
+    world, rank, local = dist_env()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2412_00291_b200 as svx
+    from paper_2412_00291_b200 import workload as W
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    spp = args.scans_per_step
+    n_frames = (args.warmup + args.steps) * spp
+    wl = W.make(args.workload, n_frames)
+    if wl.scene is not None and n_frames * 0.5 + 60 > 560:
+        wl.scene = W.street_canyon(length=n_frames * 0.5 + 60)
+    dev = torch.device("cuda", local)
+
+    # scans: generated on the GPU (rank 0 only when sharded: it is the ingest GPU)
+    counts, chunks = [], []
+    if rank == 0:
+        for p, i in wl.scans(device=dev):
+            chunks.append(p)
+            counts.append(p.shape[0])
+    if world > 1:
+        ct = torch.tensor(counts if rank == 0 else [0] * n_frames, dtype=torch.int64, device=dev)
+        dist.broadcast(ct, 0)
+        counts = ct.cpu().tolist()
+    offsets = np.zeros(n_frames + 1, np.uint64)
+    offsets[1:] = np.cumsum(counts)
+    if rank == 0:
+        pts_all = torch.cat(chunks).contiguous()
+        del chunks
+    else:
+        pts_all = torch.empty((int(offsets[-1]), 3), dtype=torch.float32, device=dev)
+    torch.cuda.synchronize()
+
+    cfg = svx.MapConfig(wl.voxel_size, wl.truncation, wl.num_labels, 1 << 21)
+    icfg = svx.IntegratorConfig()
+    poses = [wl.pose(i) for i in range(n_frames)]
+
+    def make_store():
+        st = svx.VoxelStore(cfg, device=local)
+        st.set_shard(rank, world)
+        return st
+
+    def run_leg(store, host_pts=None, clocks=None):
+        """Returns (per-step ms (max over ranks), points, updates, launches, profile)."""
+        ext = torch.cuda.ExternalStream(store.stream_ptr(), device=dev)
+        step_ms, pts_t, upd_t = [], 0, 0
+        launches0 = None
+        for s in range(args.warmup + args.steps):
+            if s == args.warmup:
+                store.profile_enable(True)
+                launches0 = svx.kernel_launches()
+                if clocks:
+                    clocks.start()
+            f0, f1 = s * spp, (s + 1) * spp
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(ext)
+            upd = 0
+            if world == 1 and host_pts is None:
+                reps = store.integrate_clouds_device(
+                    wl.model, pts_all.data_ptr() + int(offsets[f0]) * 12,
+                    offsets[f0:f1 + 1] - offsets[f0], 3, poses[f0:f1], icfg)
+                upd = sum(r.updated_voxels for r in reps)
+            else:
+                ti = svx.TsdfIntegrator(store, icfg)
+                for f in range(f0, f1):
+                    a, b = int(offsets[f]), int(offsets[f + 1])
+                    if host_pts is not None:
+                        if world > 1:
+                            if rank == 0:
+                                pts_all[a:b].copy_(host_pts[a:b], non_blocking=True)
+                            dist.broadcast(pts_all[a:b], 0)
+                            torch.cuda.current_stream().synchronize()
+                            r = ti.integrate_cloud_device(pts_all[a:b], poses[f], wl.model)
+                        else:
+                            r = ti.integrate_cloud(host_pts[a:b].numpy(), poses[f], wl.model)
+                    else:
+                        dist.broadcast(pts_all[a:b], 0)
+                        torch.cuda.current_stream().synchronize()
+                        r = ti.integrate_cloud_device(pts_all[a:b], poses[f], wl.model)
+                    upd += r.updated_voxels
+            e1.record(ext)
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            if world > 1:
+                t = torch.tensor([ms, float(upd)], dtype=torch.float64, device=dev)
+                tm = t.clone()
+                dist.all_reduce(tm[:1], op=dist.ReduceOp.MAX)
+                dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+                ms, upd = float(tm[0]), float(t[1])
+            if s >= args.warmup:
+                step_ms.append(ms)
+                pts_t += int(offsets[f1] - offsets[f0])
+                upd_t += upd
+        launches = svx.kernel_launches() - launches0
+        prof = store.profile_read()
+        return step_ms, pts_t, upd_t, launches, prof
+
+    # ---- leg 1: device-resident scans
+    store = make_store()
+    clocks = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
+    step_ms, pts_t, upd_t, launches, prof = run_leg(store, clocks=clocks)
+    clk = clocks.stop() if clocks else None
+    total_s = sum(step_ms) / 1e3
+    value = pts_t / total_s
+    pd = prof.as_dict()
+    blocks_final = store.block_count()
+    store.close()
+
+    # ---- roofline: algorithmic bytes per kernel group
+    peak, peak_src = peaks()
+    alg = {
+        "project": 12.0 * prof.points,
+        "raycast": 16.0 * prof.touched_blocks,
+        "fold": 40.0 * prof.updated_voxels + 10240.0 * prof.new_blocks,
+    }
+    ms_k = {k: v for k, v in pd["ms"].items()}
+    dom = max(ms_k, key=ms_k.get) if ms_k else "fold"
+    dom_ms = ms_k.get(dom, 0.0)
+    dom_launches = pd["launches"].get(dom, 1)
+    achieved = (alg.get(dom, 0.0) / (dom_ms / 1e3) / 1e9) if dom_ms else 0.0
+    B_total = alg["project"] + alg["raycast"] + alg["fold"]
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "kernel": dom,
+                "kernel_ms_per_launch": dom_ms / max(dom_launches, 1),
+                "alg_bytes_per_launch": alg.get(dom, 0.0) / max(dom_launches, 1),
+                "peak_source": peak_src,
+                "pipeline": {"alg_bytes_per_frame": B_total / max(prof.frames, 1),
+                             "achieved": B_total / total_s / 1e9,
+                             "frac": B_total / total_s / 1e9 / peak},
+                "kernel_ms": ms_k}
+
+    # ---- leg 2: end to end through the C-ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        host_pts = None
+        if rank == 0:
+            host_pts = pts_all.cpu().pin_memory()
+        store = make_store()
+        s2, p2, u2, _, prof2 = run_leg(store, host_pts=host_pts if rank == 0 else torch.empty(0))
+        store.close()
+        e2e = {"value": p2 / (sum(s2) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(12 * p2 / args.steps),
+               "d2h_bytes_per_step": int(64 * 3 * spp + 32 * spp)}
+
+    # ---- CPU baseline (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        off = min(args.ref_offset, n_frames // 2)
+        sample = list(range(off, min(off + args.cpu_max_scans + 1, n_frames)))
+        scans_host = {i: pts_all[int(offsets[i]):int(offsets[i + 1])].cpu().numpy() for i in sample}
+        cpu = cpu_baseline(args, wl, scans_host)
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": float(np.mean(step_ms)), "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic",
+               "config": {"workload": WORKLOAD, "scans_per_step": spp,
+                          "points_per_step": pts_t / args.steps,
+                          "l2": "inputs > L2: ~157 MB of fresh scans per step; map state > 1 GB",
+                          "parallelism": f"key-sharded map x{world}" if world > 1 else "1 GPU",
+                          "map_blocks": blocks_final},
+               "voxel_updates_per_s": upd_t / total_s,
+               "rays_per_s": prof.rays / total_s,
+               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+               "gpu_launches": int(launches), "clocks": clk, "profile": pd}
+        print(json.dumps(out))
+        if args.profile_json:
+            json.dump(out, open(args.profile_json, "w"), indent=1)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -223,6 +223,29 @@ svx_status svx_integrate_clouds_device(svx_map* map, svx_scan* scan, const float
 svx_status svx_integrate_labels(svx_map* map, const svx_label_image* img,
                                 const svx_semantic_cfg* cfg, svx_frame_report* report);
 
+/* ------------------------------------------------------------ profiling */
+/* Per-kernel device time measured with CUDA events on the map's stream (the
+ * launching stream), plus the algorithmic counters the roofline needs
+ * (SURVEY.md 8(d)). Enabling resets the accumulators. */
+enum {
+    SVX_K_PROJECT = 0,   /* project_cloud + normals (K1/K2)            */
+    SVX_K_RAYCAST = 1,   /* band DDA + block hash (K3/K4)              */
+    SVX_K_FOLD = 2,      /* own-pixel measure + fold (K5)              */
+    SVX_K_FALLBACK = 3,  /* fallback collect + sort + fold             */
+    SVX_K_SEM_CULL = 4,  /* semantic frustum cull                      */
+    SVX_K_SEM_UPDATE = 5,/* semantic Bayes update (K6)                 */
+    SVX_K_COUNT = 8
+};
+typedef struct {
+    double ms[SVX_K_COUNT];         /* summed event time per kernel group */
+    uint64_t launches[SVX_K_COUNT];
+    uint64_t frames, points, rays;  /* TSDF frames, input points, band rays */
+    uint64_t touched_blocks, new_blocks, updated_voxels, fallback_voxels;
+    uint64_t sem_images, sem_candidates, sem_updated, sem_new_layers;
+} svx_profile;
+svx_status svx_profile_enable(svx_map* map, int32_t on);
+svx_status svx_profile_read(svx_map* map, svx_profile* out);
+
 /* ------------------------------------------------------------- defaults */
 void svx_default_integrator_cfg(svx_integrator_cfg* cfg);
 void svx_default_semantic_cfg(svx_semantic_cfg* cfg);

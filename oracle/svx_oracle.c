@@ -800,3 +800,56 @@ int svxo_integrate_labels(svxo_map* m, const svx_label_image* img, const svx_sem
     free(like);
     return st;
 }
+
+/* ------------------------------------------------- known-answer-test exports */
+int svxo_project_point(const double p[3], const svx_lidar_model* m, int* u, int* v, double* r) {
+    d3 q = {{p[0], p[1], p[2]}};
+    return project_point(q, m, u, v, r);
+}
+void svxo_back_project(int u, int v, double depth, const svx_lidar_model* m, double out[3]) {
+    const d3 q = back_project(u, v, depth, m);
+    out[0] = q.v[0];
+    out[1] = q.v[1];
+    out[2] = q.v[2];
+}
+double svxo_nonprojective_distance(double psi, double theta, double alpha, double eps) {
+    return nonprojective_distance(psi, theta, alpha, eps);
+}
+float svxo_observation_weight(double psi, double tau, float min_clamp) {
+    return observation_weight(psi, tau, min_clamp);
+}
+float svxo_truncate_distance(double d, double tau) { return truncate_distance(d, tau); }
+void svxo_world_to_voxel(const double p[3], float voxel_size, int32_t out[3]) {
+    d3 q = {{p[0], p[1], p[2]}};
+    world_to_voxel(q, voxel_size, out);
+}
+/* traverse_segment: writes up to cap voxel coords (x,y,z); returns the count. */
+uint64_t svxo_traverse(const double a[3], const double b[3], float voxel_size, int32_t* out,
+                       uint64_t cap) {
+    visit_vec vv = {0};
+    d3 A = {{a[0], a[1], a[2]}}, B = {{b[0], b[1], b[2]}};
+    traverse_segment(A, B, voxel_size, &vv, 0);
+    for (size_t i = 0; i < vv.n && i < cap; ++i) {
+        const visit* r = &vv.v[i];
+        out[3 * i] = r->b[0] * KB + (r->linear % KB);
+        out[3 * i + 1] = r->b[1] * KB + (r->linear / KB) % KB;
+        out[3 * i + 2] = r->b[2] * KB + r->linear / (KB * KB);
+    }
+    const uint64_t n = vv.n;
+    free(vv.v);
+    return n;
+}
+/* label_to_likelihood; returns 0 or 1 (invalid confidence). */
+int svxo_label_to_likelihood(int label, float conf, int K, float floor_v, float* like) {
+    return label_to_likelihood(label, conf, K, floor_v, like);
+}
+/* apply_likelihood (Bayes step) in place. */
+void svxo_bayes(float* probs, const float* like, int K) {
+    double z = 0.0;
+    for (int k = 0; k < K; ++k) {
+        probs[k] *= like[k];
+        z += probs[k];
+    }
+    const float inv = (float)(1.0 / z);
+    for (int k = 0; k < K; ++k) probs[k] *= inv;
+}

@@ -107,6 +107,24 @@ class StatsC(C.Structure):
                 ("memory_bytes", C.c_uint64)]
 
 
+K_NAMES = ["project", "raycast", "fold", "fallback", "sem_cull", "sem_update", "k6", "k7"]
+
+
+class ProfileC(C.Structure):
+    _fields_ = [("ms", C.c_double * 8), ("launches", C.c_uint64 * 8), ("frames", C.c_uint64),
+                ("points", C.c_uint64), ("rays", C.c_uint64), ("touched_blocks", C.c_uint64),
+                ("new_blocks", C.c_uint64), ("updated_voxels", C.c_uint64),
+                ("fallback_voxels", C.c_uint64), ("sem_images", C.c_uint64),
+                ("sem_candidates", C.c_uint64), ("sem_updated", C.c_uint64),
+                ("sem_new_layers", C.c_uint64)]
+
+    def as_dict(self) -> dict:
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("ms", "launches")}
+        d["ms"] = {K_NAMES[i]: self.ms[i] for i in range(8) if self.launches[i]}
+        d["launches"] = {K_NAMES[i]: self.launches[i] for i in range(8) if self.launches[i]}
+        return d
+
+
 TSDF_DTYPE = np.dtype([("distance", "<f4"), ("weight", "<f4"), ("gradient", "<f4", (3,))])
 BLOCK_VOXELS = 512
 
@@ -157,6 +175,8 @@ def _sig(lib: C.CDLL) -> None:
         "svx_lidar_spinning": (S, [C.c_int32, C.c_int32, C.c_double, C.c_double,
                                    C.POINTER(LidarModel)]),
         "svx_map_set_shard": (S, [P, C.c_int32, C.c_int32]),
+        "svx_profile_enable": (S, [P, C.c_int32]),
+        "svx_profile_read": (S, [P, C.POINTER(ProfileC)]),
         "svx_block_owner": (C.c_int32, [C.POINTER(C.c_int32), C.c_int32]),
     }
     for name, (res, args) in f.items():
@@ -387,6 +407,27 @@ class VoxelStore:
     def set_shard(self, rank: int, world: int) -> None:
         _check(lib().svx_map_set_shard(self._h, rank, world))
 
+    def profile_enable(self, on: bool = True) -> None:
+        _check(lib().svx_profile_enable(self._h, int(on)))
+
+    def profile_read(self) -> ProfileC:
+        p = ProfileC()
+        _check(lib().svx_profile_read(self._h, C.byref(p)))
+        return p
+
+    def integrate_clouds_device(self, model: ProjectionModel, d_points_ptr: int,
+                                offsets: np.ndarray, stride: int, poses: list,
+                                cfg: "IntegratorConfig") -> list:
+        """A sequence of clouds already in HBM (device pointer), one call."""
+        n = len(poses)
+        offs = np.ascontiguousarray(np.asarray(offsets, np.uint64))
+        parr = (PoseC * n)(*poses)
+        reps = (FrameReportC * n)()
+        _check(lib().svx_integrate_clouds_device(self._h, self.scan(model), C.c_void_p(d_points_ptr),
+                                                 _ptr(offs), stride, C.cast(parr, C.c_void_p), n,
+                                                 C.byref(cfg.c()), C.cast(reps, C.c_void_p)))
+        return [FrameReport.of(r) for r in reps]
+
     def get_or_allocate_block(self, bc) -> bool:
         nw = C.c_int32()
         _check(lib().svx_get_or_allocate_block(self._h, _i3(bc), C.byref(nw)))
@@ -570,6 +611,18 @@ class TsdfIntegrator:
         rep = FrameReportC()
         _check(lib().svx_integrate_cloud(self.store.handle, s, _ptr(a), a.shape[0], stride, 0,
                                          C.byref(pc), C.byref(self.cfg.c()), C.byref(rep)))
+        return FrameReport.of(rep)
+
+    def integrate_cloud_device(self, points, pose, model: ProjectionModel) -> FrameReport:
+        """Same as integrate_cloud for a CUDA tensor (n, 3|4) float32 already in HBM.
+        The caller orders the tensor's producer before this call (synchronous API)."""
+        n, stride = int(points.shape[0]), int(points.shape[1])
+        pc = pose if isinstance(pose, PoseC) else (pose.c() if isinstance(pose, Pose) else pose_c(pose))
+        s = self.store.scan(model)
+        rep = FrameReportC()
+        _check(lib().svx_integrate_cloud(self.store.handle, s, C.c_void_p(points.data_ptr()), n,
+                                         stride, 1, C.byref(pc), C.byref(self.cfg.c()),
+                                         C.byref(rep)))
         return FrameReport.of(rep)
 
     def take_dirty_blocks(self) -> np.ndarray:

@@ -401,6 +401,25 @@ svx_status svx_map_get_stream(svx_map* m, void** stream) {
     return guarded([&] { *stream = m->stream; });
 }
 
+svx_status svx_profile_enable(svx_map* m, int32_t on) {
+    return guarded([&] {
+        DeviceGuard g(m->device);
+        SVX_CUDA(cudaStreamSynchronize(m->stream));
+        prof_resolve(m);
+        m->prof = on != 0;
+        m->prof_acc = svx_profile{};
+    });
+}
+
+svx_status svx_profile_read(svx_map* m, svx_profile* out) {
+    return guarded([&] {
+        DeviceGuard g(m->device);
+        SVX_CUDA(cudaStreamSynchronize(m->stream));
+        prof_resolve(m);
+        *out = m->prof_acc;
+    });
+}
+
 svx_status svx_map_set_shard(svx_map* m, int32_t rank, int32_t world) {
     return guarded([&] {
         require(world >= 1 && rank >= 0 && rank < world, SVX_INVALID_ARGUMENT, "bad shard");

@@ -206,6 +206,7 @@ enum Counter : int {
     C_SEM_UPDATED = 12,
     C_FRAME = 13,       // frame serial (stamp for touched detection)
     C_REC_OVERFLOW = 14,
+    C_RAYS = 15,        // band rays cast this frame
     kNumCounters = 16
 };
 

@@ -132,6 +132,16 @@ struct svx_map {
     int32_t tsdf_frames = 0, sem_frames = 0;
     uint64_t n_blocks = 0;           // host copy of C_BLOCKS after the last sync
     uint64_t n_layers = 0;
+    // profiling: event pairs recorded around kernel groups on `stream`,
+    // resolved at the next host synchronisation point
+    bool prof = false;
+    svx_profile prof_acc{};
+    struct PendingEv {
+        int kid;
+        cudaEvent_t a, b;
+    };
+    std::vector<PendingEv> prof_pending;
+    std::vector<cudaEvent_t> prof_free;
 };
 
 namespace svx {
@@ -142,6 +152,15 @@ void ensure_layers(svx_map* m, uint64_t layers);
 // Copies counters to the pinned mirror and synchronises the map stream.
 void sync_counters(svx_map* m);
 void count_launch(uint64_t n = 1);
+// Profiling marks (no-ops unless svx_profile_enable(map, 1)).
+struct ProfMark {
+    svx_map* m;
+    int kid;
+    cudaEvent_t a = nullptr;
+    ProfMark(svx_map* map, int k);
+    ~ProfMark();
+};
+void prof_resolve(svx_map* m);
 
 inline svx_tsdf_voxel* tsdf_base(svx_map* m) {
     return static_cast<svx_tsdf_voxel*>(m->tsdf_pool.base());

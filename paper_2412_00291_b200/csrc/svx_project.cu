@@ -189,6 +189,8 @@ void launch_project(svx_scan* s, const float* d_pts, uint64_t n, int stride, con
     s->tie.alloc(P);
     DevBuf<uint32_t>& pix_of_pt = s->pix_of_pt;
     pix_of_pt.alloc(n ? n : 1);
+    ProfMark pm(m, SVX_K_PROJECT);
+    m->prof_acc.points += n;
     SVX_CUDA(cudaMemsetAsync(s->pixkey.p, 0xFF, sizeof(unsigned long long) * P, m->stream));
     SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_TIES, 0, sizeof(uint32_t), m->stream));
     SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_DROPPED, 0, sizeof(uint32_t), m->stream));
@@ -217,6 +219,7 @@ void launch_project(svx_scan* s, const float* d_pts, uint64_t n, int stride, con
 
 void launch_normals(svx_scan* s) {
     svx_map* m = s->map;
+    ProfMark pm(m, SVX_K_PROJECT);
     k_normals<<<grid_for(uint64_t(s->P)), kThreads, 0, m->stream>>>(
         s->depth.p, s->dirs.p, s->dm.W, s->dm.H, s->normals.p, s->valid.p);
     count_launch(1);

@@ -314,6 +314,7 @@ void run_integrate_labels(svx_map* m, const svx_label_image& img, const svx_sema
     }
     m->cand.alloc(std::max<uint64_t>(m->n_blocks, 1));
     if (m->n_blocks) {
+        ProfMark pm(m, SVX_K_SEM_CULL);
         k_sem_cull<<<grid_for(m->n_blocks), kThreads, 0, m->stream>>>(sp, m->block_keys, m->cand.p,
                                                                       m->d_ctr);
         count_launch();
@@ -323,15 +324,22 @@ void run_integrate_labels(svx_map* m, const svx_label_image& img, const svx_sema
     const uint32_t n_cand = m->h_ctr[C_CAND];
     if (n_cand) {
         ensure_layers(m, m->n_layers + n_cand);
-        k_sem_update<<<persistent_grid(m->device), kThreads, 0, m->stream>>>(
-            sp, hash_view(m), m->block_keys, tsdf_base(m), sem_base(m), m->sem_idx, m->cand.p,
-            m->lbl.p, sp.has_conf ? m->conf.p : nullptr, sp.has_tensor ? m->tensor.p : nullptr,
-            m->dirty + m->cfg.max_blocks, m->d_ctr);
-        count_launch();
+        {
+            ProfMark pm(m, SVX_K_SEM_UPDATE);
+            k_sem_update<<<persistent_grid(m->device), kThreads, 0, m->stream>>>(
+                sp, hash_view(m), m->block_keys, tsdf_base(m), sem_base(m), m->sem_idx, m->cand.p,
+                m->lbl.p, sp.has_conf ? m->conf.p : nullptr, sp.has_tensor ? m->tensor.p : nullptr,
+                m->dirty + m->cfg.max_blocks, m->d_ctr);
+            count_launch();
+        }
         SVX_CUDA(cudaGetLastError());
         sync_counters(m);
     }
     rep->updated_voxels = m->h_ctr[C_SEM_UPDATED];
+    m->prof_acc.sem_images += 1;
+    m->prof_acc.sem_candidates += n_cand;
+    m->prof_acc.sem_updated += m->h_ctr[C_SEM_UPDATED];
+    m->prof_acc.sem_new_layers += m->h_ctr[C_SEM] - m->n_layers;
     m->n_layers = m->h_ctr[C_SEM];
 }
 

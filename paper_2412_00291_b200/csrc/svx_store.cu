@@ -123,6 +123,46 @@ void sync_counters(svx_map* m) {
     SVX_CUDA(cudaMemcpyAsync(m->h_ctr, m->d_ctr, sizeof(uint32_t) * kNumCounters,
                              cudaMemcpyDeviceToHost, m->stream));
     SVX_CUDA(cudaStreamSynchronize(m->stream));
+    if (m->prof) prof_resolve(m);
+}
+
+namespace {
+cudaEvent_t take_event(svx_map* m) {
+    if (!m->prof_free.empty()) {
+        cudaEvent_t e = m->prof_free.back();
+        m->prof_free.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    SVX_CUDA(cudaEventCreate(&e));
+    return e;
+}
+}  // namespace
+
+ProfMark::ProfMark(svx_map* map, int k) : m(map), kid(k) {
+    if (!m->prof) return;
+    a = take_event(m);
+    SVX_CUDA(cudaEventRecord(a, m->stream));
+}
+
+ProfMark::~ProfMark() {
+    if (!a) return;
+    cudaEvent_t b = take_event(m);
+    cudaEventRecord(b, m->stream);
+    m->prof_pending.push_back({kid, a, b});
+    m->prof_acc.launches[kid] += 1;
+}
+
+void prof_resolve(svx_map* m) {
+    for (auto& p : m->prof_pending) {
+        float ms = 0.f;
+        cudaEventSynchronize(p.b);
+        cudaEventElapsedTime(&ms, p.a, p.b);
+        m->prof_acc.ms[p.kid] += ms;
+        m->prof_free.push_back(p.a);
+        m->prof_free.push_back(p.b);
+    }
+    m->prof_pending.clear();
 }
 
 namespace {

@@ -122,6 +122,7 @@ k_raycast_band(FrameParams f, const float* __restrict__ depth, const uint8_t* __
     if (p >= uint32_t(f.m.W) * uint32_t(f.m.H)) return;
     d3 a, b;
     if (!band_of(f, depth, valid, dirs, p, a, b)) return;
+    warp_agg_inc(&ctr[C_RAYS]);
 
     uint64_t cur_key = kEmptyKey;
     uint32_t cur_slot = kInvalid;
@@ -560,11 +561,14 @@ void run_integrate(svx_map* m, svx_scan* s, const Pose& pose, const svx_integrat
     const uint32_t P = uint32_t(s->P);
     SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_TOUCHED, 0, sizeof(uint32_t) * (C_ERR_HASH - C_TOUCHED + 1),
                              m->stream));
+    SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_RAYS, 0, sizeof(uint32_t), m->stream));
     HashView hv = hash_view(m);
+    ProfMark* pm = new ProfMark(m, SVX_K_RAYCAST);
     k_raycast_band<<<grid_for(P), kThreads, 0, m->stream>>>(f, s->depth.p, s->valid.p, s->dirs.p,
                                                             hv, m->block_keys, m->stamp,
                                                             m->touched, m->vmask, m->d_ctr);
     count_launch();
+    delete pm;
     SVX_CUDA(cudaGetLastError());
     sync_counters(m);
     const uint32_t* c = m->h_ctr;
@@ -573,13 +577,17 @@ void run_integrate(svx_map* m, svx_scan* s, const Pose& pose, const svx_integrat
     if (c[C_BLOCKS] > m->cfg.max_blocks || c[C_ERR_HASH]) capacity_path(m, f, s);
     ensure_blocks(m, c[C_BLOCKS]);
 
-    k_fold<<<persistent_grid(m->device), kThreads, 0, m->stream>>>(
-        f, s->depth.p, s->normals.p, s->valid.p, s->dirs.p, hv, tsdf_base(m), m->touched, m->vmask,
-        m->dirty, m->d_ctr);
-    count_launch();
+    {
+        ProfMark pf(m, SVX_K_FOLD);
+        k_fold<<<persistent_grid(m->device), kThreads, 0, m->stream>>>(
+            f, s->depth.p, s->normals.p, s->valid.p, s->dirs.p, hv, tsdf_base(m), m->touched,
+            m->vmask, m->dirty, m->d_ctr);
+        count_launch();
+    }
     SVX_CUDA(cudaGetLastError());
     sync_counters(m);
     if (c[C_FALLBACK]) {
+        ProfMark pb(m, SVX_K_FALLBACK);
         uint32_t cap = std::max<uint32_t>(c[C_FALLBACK] * 16u, 1u << 16);
         for (;;) {
             m->records.alloc(cap);
@@ -606,6 +614,12 @@ void run_integrate(svx_map* m, svx_scan* s, const Pose& pose, const svx_integrat
             sync_counters(m);
         }
     }
+    m->prof_acc.frames += 1;
+    m->prof_acc.rays += c[C_RAYS];
+    m->prof_acc.touched_blocks += c[C_TOUCHED];
+    m->prof_acc.new_blocks += c[C_BLOCKS] - f.blocks_before;
+    m->prof_acc.updated_voxels += c[C_UPDATED];
+    m->prof_acc.fallback_voxels += c[C_FALLBACK];
     rep->updated_voxels = c[C_UPDATED];
     rep->new_blocks = c[C_BLOCKS] - f.blocks_before;
     m->n_blocks = c[C_BLOCKS];

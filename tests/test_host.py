@@ -1,0 +1,102 @@
+"""CPU: workload generator sanity and the multi-process (gloo, world 2) key
+sharding logic used by bench.py's multi-GPU path."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_2412_00291_b200 as svx
+from paper_2412_00291_b200 import workload as W
+
+
+def test_workload_scan_shape_and_range():
+    wl = W.make("tiny", 2)
+    scans = list(wl.scans())
+    assert len(scans) == 2
+    for p, i in scans:
+        assert p.dtype == torch.float32 and p.shape[1] == 3
+        r = p.double().norm(dim=1)
+        assert float(r.min()) >= wl.model.min_range
+        assert 0.5 * wl.model.width * wl.model.height_px < p.shape[0] <= wl.model.width * wl.model.height_px
+
+
+def test_workload_points_sit_on_pixel_centres():
+    # one return per pixel-centre ray (synthetic.cpp:113-139): projecting the
+    # points back hits distinct pixels far from pixel boundaries
+    wl = W.make("tiny", 1)
+    p, _ = next(iter(wl.scans()))
+    p = p.double().numpy()
+    az = np.arctan2(p[:, 1], p[:, 0])
+    uf = (np.pi - az) / wl.model.delta_phi
+    frac = uf - np.floor(uf)
+    assert np.all(np.abs(frac - 0.5) < 0.01)
+
+
+def test_workload_configs_exist():
+    for name in ("cfg1", "cfg2", "cfg3", "cfg5-320"):
+        wl = W.make(name, 2)
+        assert len(wl.poses) == 2 and wl.num_labels == 20
+    assert W.make("cfg2", 3).model.width == 1024 and W.make("cfg2", 3).model.height_px == 128
+    assert W.make("cfg3", 1).voxel_size == 0.05 and len(W.make("cfg3", 1).cams) == 6
+
+
+def test_label_images_render():
+    wl = W.make("tiny", 1)
+    (li,) = wl.label_images(0)
+    assert li.labels.shape == (li.height, li.width) and li.labels.dtype == np.uint16
+    assert li.labels.max() < 20
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _shard_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # rank 0 is the ingest: it broadcasts the scan (bench.py's multi-GPU path)
+    wl = W.make("tiny", 1)
+    if rank == 0:
+        p, _ = next(iter(wl.scans()))
+        n = torch.tensor([p.shape[0]])
+    else:
+        n = torch.tensor([0])
+    dist.broadcast(n, 0)
+    buf = p if rank == 0 else torch.empty((int(n), 3), dtype=torch.float32)
+    dist.broadcast(buf, 0)
+    # every rank sees the same block set and keeps only the blocks it owns
+    rng = np.random.default_rng(11)
+    keys = rng.integers(-3000, 3000, size=(5000, 3))
+    mine = [tuple(k) for k in keys if svx.block_owner(k, world) == rank]
+    out = [None] * world
+    dist.all_gather_object(out, (mine, float(buf.sum())))
+    if rank == 0:
+        q.put(out)
+    dist.destroy_process_group()
+
+
+def test_key_sharding_gloo_world2():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+    shards = [set(o[0]) for o in out]
+    assert shards[0].isdisjoint(shards[1])
+    rng = np.random.default_rng(11)
+    keys = {tuple(k) for k in rng.integers(-3000, 3000, size=(5000, 3))}
+    assert shards[0] | shards[1] == keys
+    assert out[0][1] == out[1][1]  # both ranks received the identical scan
