@@ -107,7 +107,7 @@ class StatsC(C.Structure):
                 ("memory_bytes", C.c_uint64)]
 
 
-K_NAMES = ["project", "raycast", "fold", "fallback", "sem_cull", "sem_update", "k6", "k7"]
+K_NAMES = ["project", "raycast", "fold", "fallback", "sem_cull", "sem_update", "compact", "k7"]
 
 
 class ProfileC(C.Structure):

@@ -94,9 +94,17 @@ void free_map(svx_map* m) {
     if (m->stream) cudaStreamSynchronize(m->stream);
     for (void* p : {(void*)m->keys, (void*)m->vals, (void*)m->block_keys, (void*)m->sem_idx,
                     (void*)m->dirty, (void*)m->stamp, (void*)m->touched, (void*)m->vmask,
-                    (void*)m->d_ctr})
+                    (void*)m->d_ctr, (void*)m->fbcnt, (void*)m->fbstart, (void*)m->fbfill,
+                    (void*)m->fbslots, (void*)m->bigslots})
         if (p) cudaFree(p);
     if (m->h_ctr) cudaFreeHost(m->h_ctr);
+    if (m->h_outs) cudaFreeHost(m->h_outs);
+    m->outs.release();
+    m->bucket.release();
+    m->terms.release();
+    m->vlist.release();
+    prof_resolve(m);
+    for (cudaEvent_t e : m->prof_free) cudaEventDestroy(e);
     m->records.release();
     m->records_alt.release();
     m->sort_tmp.release();
@@ -135,11 +143,21 @@ svx_map* create_map(const svx_map_cfg& cfg, int device) {
         m->sem_idx = dmalloc<uint32_t>(cfg.max_blocks);
         m->dirty = dmalloc<uint8_t>(2ull * cfg.max_blocks);
         m->d_ctr = dmalloc<uint32_t>(kNumCounters);
+        m->fbcnt = dmalloc<uint32_t>(m->cap);
+        m->fbstart = dmalloc<uint32_t>(m->cap);
+        m->fbfill = dmalloc<uint32_t>(m->cap);
+        m->fbslots = dmalloc<uint32_t>(m->cap);
+        m->bigslots = dmalloc<uint32_t>(m->cap);
+        m->rec_cap = 1u << 20;
+        m->records.alloc(m->rec_cap);
+        m->bucket.alloc(m->rec_cap);
+        m->terms.alloc(size_t(m->rec_cap) * 24);
         SVX_CUDA(cudaMallocHost(&m->h_ctr, sizeof(uint32_t) * kNumCounters));
         std::memset(m->h_ctr, 0, sizeof(uint32_t) * kNumCounters);
         SVX_CUDA(cudaMemsetAsync(m->keys, 0xFF, 8ull * m->cap, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->stamp, 0, 4ull * m->cap, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->vmask, 0, 128ull * m->cap, m->stream));
+        SVX_CUDA(cudaMemsetAsync(m->fbcnt, 0, 4ull * m->cap, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->sem_idx, 0xFF, 4ull * cfg.max_blocks, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->dirty, 0, 2ull * cfg.max_blocks, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->d_ctr, 0, sizeof(uint32_t) * kNumCounters, m->stream));
@@ -265,9 +283,7 @@ svx_map* load_svox1(const std::vector<uint8_t>& buf, int device, uint32_t max_bl
             SVX_CUDA(cudaMemcpy(sem_base(m), sem.data(), sem.size() * 4, cudaMemcpyHostToDevice));
         m->n_blocks = n;
         m->n_layers = layers;
-        m->h_ctr[C_BLOCKS] = uint32_t(n);
-        m->h_ctr[C_SEM] = layers;
-        SVX_CUDA(cudaMemcpy(m->d_ctr, m->h_ctr, 8, cudaMemcpyHostToDevice));
+        push_block_counters(m);
         rebuild_hash(m);
         SVX_CUDA(cudaStreamSynchronize(m->stream));
     } catch (...) {
@@ -292,11 +308,14 @@ Model make_model(const svx_lidar_model& lm) {
     m.inv_dphi_f = float(1.0 / lm.delta_phi);
     m.inv_dtheta_f = float(1.0 / lm.delta_theta);
     m.theta0_f = float(lm.theta0);
-    // FP32 pixel-coordinate error bound ("pixel decisions"): angle error
-    // of atan2f/acosf + input rounding <= 4e-6 rad, plus relative rounding of the
-    // scaled coordinate.
-    m.margin_u = float(4e-6 / lm.delta_phi + 1e-6 * lm.width + 1e-4);
-    m.margin_v = float(4e-6 / lm.delta_theta + 1e-6 * lm.height_px + 1e-4);
+    // FP32 pixel-coordinate error bound ("pixel decisions"): angle error of
+    // fast_atan2f (<= 1.2e-7 + 2 ulp) + FP32 geometry (<= 2e-6 relative) is < 3e-6 rad;
+    // budget 8e-6 rad, plus the relative rounding of the scaled coordinate.
+    m.margin_u = float(8e-6 / lm.delta_phi + 5e-7 * lm.width + 1e-4);
+    m.margin_v = float(8e-6 / lm.delta_theta + 5e-7 * lm.height_px + 1e-4);
+    const double lo = lm.min_range * (1.0 - 1e-5), hi = lm.min_range * (1.0 + 1e-5);
+    m.r2_lo = float(lo * lo);
+    m.r2_hi = float(hi * hi);
     return m;
 }
 
@@ -636,6 +655,11 @@ svx_status svx_scan_create(svx_map* m, const svx_lidar_model* model, svx_scan** 
             s->normals.alloc(3 * P);
             s->valid.alloc(P);
             s->tie.alloc(P);
+            s->pixkey.alloc(2 * P);
+            s->lexkey.alloc(3 * P);
+            s->pixcache.alloc(48 * P);
+            SVX_CUDA(cudaMemset(s->pixkey.p, 0xFF, 16 * P));
+            SVX_CUDA(cudaMemset(s->pixcache.p, 0, 48 * P));
             SVX_CUDA(cudaMemset(s->depth.p, 0, 4 * P));
             SVX_CUDA(cudaMemset(s->height.p, 0, 4 * P));
             SVX_CUDA(cudaMemset(s->normals.p, 0, 12 * P));
@@ -661,6 +685,7 @@ svx_status svx_scan_destroy(svx_scan* s) {
         s->valid.release();
         s->pixkey.release();
         s->lexkey.release();
+        s->pixcache.release();
         s->tie.release();
         s->pix_of_pt.release();
         s->points.release();
@@ -689,6 +714,9 @@ svx_status svx_project(svx_scan* s, const float* pts, uint64_t n, int32_t stride
         launch_project(s, d, n, stride, to_pose(*pose));
         sync_counters(s->map);
         s->dropped = s->map->h_ctr[C_DROPPED];
+        SVX_CUDA(cudaMemsetAsync(s->map->d_ctr + C_TIES, 0, 4, s->map->stream));
+        SVX_CUDA(cudaMemsetAsync(s->map->d_ctr + C_DROPPED, 0, 4, s->map->stream));
+        SVX_CUDA(cudaStreamSynchronize(s->map->stream));
     });
 }
 
@@ -739,7 +767,8 @@ svx_status svx_integrate_scan(svx_map* m, svx_scan* s, const svx_pose* pose,
         require(s->map == m, SVX_INVALID_ARGUMENT, "scan belongs to another map");
         DeviceGuard g(m->device);
         const auto t0 = std::chrono::steady_clock::now();
-        run_integrate(m, s, to_pose(*pose), *cfg, rep);
+        const FrameJob job{s, to_pose(*pose), nullptr, 0, 3, false};
+        run_frames(m, &job, 1, *cfg, rep);
         rep->elapsed_ms =
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     });
@@ -755,10 +784,8 @@ svx_status svx_integrate_cloud(svx_map* m, svx_scan* s, const float* pts, uint64
         const auto t0 = std::chrono::steady_clock::now();
         validate_pose(*pose);
         const float* d = stage_points(s, pts, n, stride, is_dev);
-        const Pose P = to_pose(*pose);
-        launch_project(s, d, n, stride, P);
-        run_integrate(m, s, P, *cfg, rep);
-        s->dropped = m->h_ctr[C_DROPPED];
+        const FrameJob job{s, to_pose(*pose), d, n, stride, true};
+        run_frames(m, &job, 1, *cfg, rep);
         rep->elapsed_ms =
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     });
@@ -771,15 +798,18 @@ svx_status svx_integrate_clouds_device(svx_map* m, svx_scan* s, const float* d_p
     return guarded([&] {
         require(s->map == m, SVX_INVALID_ARGUMENT, "scan belongs to another map");
         DeviceGuard g(m->device);
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<FrameJob> jobs(size_t(std::max(n_frames, 0)));
         for (int32_t f = 0; f < n_frames; ++f) {
-            const auto t0 = std::chrono::steady_clock::now();
             validate_pose(poses[f]);
-            const Pose P = to_pose(poses[f]);
-            launch_project(s, d_points + offsets[f] * stride, offsets[f + 1] - offsets[f], stride, P);
-            run_integrate(m, s, P, *cfg, &reports[f]);
-            reports[f].elapsed_ms =
-                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            require(offsets[f + 1] >= offsets[f], SVX_INVALID_ARGUMENT, "offsets must not decrease");
+            jobs[f] = FrameJob{s, to_pose(poses[f]), d_points + offsets[f] * stride,
+                               offsets[f + 1] - offsets[f], stride, true};
         }
+        run_frames(m, jobs.data(), n_frames, *cfg, reports);
+        const double ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        for (int32_t f = 0; f < n_frames; ++f) reports[f].elapsed_ms = ms / n_frames;
     });
 }
 

@@ -86,7 +86,9 @@ struct svx_scan {
     svx::DevBuf<float> height;    // P
     svx::DevBuf<float> normals;   // 3P (sensor frame)
     svx::DevBuf<uint8_t> valid;   // P
-    svx::DevBuf<unsigned long long> pixkey;  // P: (range bits << 32) | point index
+    svx::DevBuf<unsigned long long> pixkey;  // 2P: double-buffered (range bits << 32) | point index
+    int parity = 0;                           // which pixkey half the next projection uses
+    svx::DevBuf<uint8_t> pixcache;           // P x 48 B: ray, range, world normal, flags
     svx::DevBuf<unsigned long long> lexkey;  // P: tie-break scratch
     svx::DevBuf<uint8_t> tie;     // P: possible exact-range tie
     svx::DevBuf<uint32_t> pix_of_pt;  // per input point: pixel index or kInvalid
@@ -121,6 +123,24 @@ struct svx_map {
     uint32_t* vmask = nullptr;       // [cap][32]
     svx::DevBuf<unsigned long long> records, records_alt;
     svx::DevBuf<uint8_t> sort_tmp;
+    // fallback stage (voxels whose own pixel has no return): per-slot record
+    // counts / bucket offsets, the frame's record list and the bucketed keys
+    uint32_t* fbcnt = nullptr;       // [cap]
+    uint32_t* fbstart = nullptr;     // [cap]
+    uint32_t* fbfill = nullptr;      // [cap]
+    uint32_t* fbslots = nullptr;     // [cap]
+    uint32_t* bigslots = nullptr;    // [cap] buckets too large for the warp sort
+    svx::DevBuf<uint32_t> bucket;    // [rec_cap]
+    svx::DevBuf<uint8_t> terms;      // [rec_cap] x 24 B measurement terms
+    uint32_t rec_cap = 0;
+    svx::DevBuf<uint32_t> vlist;     // touched voxels of the frame: (touched idx << 9) | linear
+    uint32_t vox_cap = 0;
+    // per-frame results of a batch
+    svx::DevBuf<svx::FrameOut> outs;
+    svx::FrameOut* h_outs = nullptr;
+    size_t h_outs_n = 0;
+    uint64_t mapped_blocks = 0;      // host mirror of C_MAPPED
+    uint64_t max_new_seen = 0;       // largest new-block count of one frame so far
     svx::DevBuf<uint32_t> cand;      // semantic candidate blocks
     svx::DevBuf<uint16_t> lbl;
     svx::DevBuf<float> conf, tensor;
@@ -175,8 +195,23 @@ void validate_pose(const svx_pose& p);
 // kernels' host launchers (svx_project.cu, svx_tsdf.cu, svx_semantic.cu, svx_store.cu)
 void launch_project(svx_scan* s, const float* d_pts, uint64_t n, int stride, const Pose& pose);
 void launch_normals(svx_scan* s);
-void run_integrate(svx_map* m, svx_scan* s, const Pose& pose, const svx_integrator_cfg& cfg,
-                   svx_frame_report* rep);
+// One TSDF frame of a batch: project (optional) + integrate_frame.
+struct FrameJob {
+    svx_scan* scan;
+    Pose pose;
+    const float* pts;  // device pointer (when project)
+    uint64_t n;
+    int stride;
+    bool project;
+};
+// Runs the frames back to back on the map stream, synchronising once at the end
+// (plus once per abort/resume, rare). Fills one report per frame.
+void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cfg& cfg,
+                svx_frame_report* reps);
+void reset_frame_state(svx_map* m);
+// Writes the host's block/layer/mapping counts into the device counters.
+void push_block_counters(svx_map* m);
+unsigned persistent_grid(int device);
 void run_integrate_labels(svx_map* m, const svx_label_image& img, const svx_semantic_cfg& cfg,
                           svx_frame_report* rep);
 uint64_t count_observed(svx_map* m);

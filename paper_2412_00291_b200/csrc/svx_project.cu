@@ -1,17 +1,23 @@
 // K1/K2: project_cloud + compute_normal_image on the device.
 //
 // project_cloud (scan_projection.cpp:39-76) is a serial nearer-wins scatter with
-// a lexicographic tie-break. Here it is order-independent by construction:
-//   k_project_points  one thread per point: pixel (FP32 fast path, FP64 near
-//                     boundaries), then atomicMin of (f32 range bits << 32 | index)
-//                     on the pixel. A pixel where two equal ranges met is flagged.
-//   k_tie_*           only for flagged pixels (gated on a device counter): the
-//                     lexicographically smallest (x, y, z) among equal-range points
-//                     wins, exactly as std::tie in the reference.
-//   k_finish_pixels   one thread per pixel: depth, height = (pose * p).z of the
-//                     winner, and (optionally) the normal of compute_normal_image
-//                     (scan_projection.cpp:86-109) from the three neighbour depths,
-//                     with back_project directions from a host-libm table (bit-exact).
+// a lexicographic tie-break. Here it is order-independent by construction, in two
+// kernels per scan:
+//   k_project_points  one thread per point: pixel (FP32 polynomial atan2 with an
+//                     error margin, FP64 reference formula near a boundary), then
+//                     atomicMin of (f32 range bits << 32 | point index) on the pixel.
+//                     When two equal ranges meet, both points are appended to a tie
+//                     list and the pixel is flagged (every point with the pixel's
+//                     final range ends up in the list).
+//   k_finish_pixels   one thread per pixel: flagged pixels pick the lexicographically
+//                     smallest (x, y, z) among their equal-range points (std::tie in
+//                     the reference); depth, height = (pose * p).z of the winner, and
+//                     the normal of compute_normal_image (scan_projection.cpp:86-109)
+//                     from the three neighbour depths, with back_project directions
+//                     from a host-libm table (bit-exact). It also resets the other half
+//                     of the double-buffered pixel keys for the next scan.
+#include <algorithm>
+
 #include "svx_map.hpp"
 
 namespace svx {
@@ -20,88 +26,45 @@ namespace {
 
 constexpr int kThreads = 256;
 
-__device__ inline unsigned long long ord_key(double x) {
-    if (x == 0.0) x = 0.0;  // -0.0 and +0.0 compare equal in std::tie
-    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
-    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+__device__ inline bool lex_less(d3 a, d3 b) {
+    if (a.x < b.x) return true;
+    if (b.x < a.x) return false;
+    if (a.y < b.y) return true;
+    if (b.y < a.y) return false;
+    return a.z < b.z;
 }
 
-__global__ void k_project_points(const float* __restrict__ pts, uint64_t n, int stride, Model m,
-                                 unsigned long long* __restrict__ pixkey,
-                                 uint8_t* __restrict__ tie, uint32_t* __restrict__ pix_of_pt,
-                                 uint32_t* __restrict__ ctr) {
+__global__ void __launch_bounds__(kThreads)
+k_project_points(const float* __restrict__ pts, uint64_t n, int stride, Model m,
+                 unsigned long long* __restrict__ pixkey, uint8_t* __restrict__ tie,
+                 unsigned long long* __restrict__ ties, uint32_t tie_cap,
+                 uint32_t* __restrict__ ctr) {
+    if (ctr[C_ABORT]) return;
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const d3 p = mk(pts[i * stride], pts[i * stride + 1], pts[i * stride + 2]);
-    int u, v;
-    double r;
-    if (!project_point(p, m, u, v, r)) {
-        pix_of_pt[i] = kInvalid;
+    const float x = pts[i * stride], y = pts[i * stride + 1], z = pts[i * stride + 2];
+    const d3 p = mk(x, y, z);
+    const double r = sqrt(dot3(p, p));
+    uint32_t pix = kInvalid;
+    if (isfinite(r) && !(r < m.min_range)) {
+        pix = pixel_fast(x, y, z, m, m.r2_lo, m.r2_hi);  // float inputs: exact geometry
+        if (pix == kNeedFp64) pix = pixel_fp64(p, m);
+    }
+    if (pix == kInvalid) {
         warp_agg_inc(&ctr[C_DROPPED]);
         return;
     }
-    const uint32_t pix = uint32_t(v) * uint32_t(m.W) + uint32_t(u);
-    pix_of_pt[i] = pix;
-    const float rf = float(r);
     const unsigned long long key =
-        (static_cast<unsigned long long>(__float_as_uint(rf)) << 32) | static_cast<uint32_t>(i);
+        (static_cast<unsigned long long>(__float_as_uint(float(r))) << 32) | uint32_t(i);
     const unsigned long long old = atomicMin(&pixkey[pix], key);
     if (old != ~0ull && (old >> 32) == (key >> 32)) {
-        if (tie[pix] == 0) {
-            tie[pix] = 1;
-            atomicAdd(&ctr[C_TIES], 1u);
+        tie[pix] = 1;
+        const uint32_t pos = atomicAdd(&ctr[C_TIES], 2u);
+        if (pos + 1 < tie_cap) {
+            ties[pos] = (static_cast<unsigned long long>(pix) << 32) | uint32_t(old);
+            ties[pos + 1] = (static_cast<unsigned long long>(pix) << 32) | uint32_t(i);
         }
     }
-}
-
-// Tie resolution, pass `axis` (0 = x, 1 = y, 2 = z): among points of a flagged
-// pixel whose range equals the minimum and whose earlier coordinates equal the
-// running lexicographic minimum, take the minimum of this coordinate.
-__global__ void k_tie_axis(const float* __restrict__ pts, uint64_t n, int stride,
-                           const uint32_t* __restrict__ pix_of_pt,
-                           const unsigned long long* __restrict__ pixkey,
-                           const uint8_t* __restrict__ tie, unsigned long long* __restrict__ lex,
-                           uint32_t P, int axis, const uint32_t* __restrict__ ctr) {
-    if (ctr[C_TIES] == 0) return;
-    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t pix = pix_of_pt[i];
-    if (pix == kInvalid || !tie[pix]) return;
-    const double c[3] = {pts[i * stride], pts[i * stride + 1], pts[i * stride + 2]};
-    const float rf = float(sqrt(dot3(mk(c[0], c[1], c[2]), mk(c[0], c[1], c[2]))));
-    if (__float_as_uint(rf) != uint32_t(pixkey[pix] >> 32)) return;
-    for (int a = 0; a < axis; ++a)
-        if (ord_key(c[a]) != lex[uint64_t(a) * P + pix]) return;
-    atomicMin(&lex[uint64_t(axis) * P + pix], ord_key(c[axis]));
-}
-
-__global__ void k_tie_reset(const uint8_t* __restrict__ tie, unsigned long long* __restrict__ lex,
-                            uint32_t P, const uint32_t* __restrict__ ctr) {
-    if (ctr[C_TIES] == 0) return;
-    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= P || !tie[p]) return;
-    lex[p] = lex[uint64_t(P) + p] = lex[2ull * P + p] = ~0ull;
-}
-
-__global__ void k_tie_winner(const float* __restrict__ pts, uint64_t n, int stride,
-                             const uint32_t* __restrict__ pix_of_pt,
-                             unsigned long long* __restrict__ pixkey,
-                             const uint8_t* __restrict__ tie,
-                             const unsigned long long* __restrict__ lex, uint32_t P,
-                             const uint32_t* __restrict__ ctr) {
-    if (ctr[C_TIES] == 0) return;
-    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t pix = pix_of_pt[i];
-    if (pix == kInvalid || !tie[pix]) return;
-    const double c[3] = {pts[i * stride], pts[i * stride + 1], pts[i * stride + 2]};
-    const unsigned long long cur = pixkey[pix];
-    const float rf = float(sqrt(dot3(mk(c[0], c[1], c[2]), mk(c[0], c[1], c[2]))));
-    if (__float_as_uint(rf) != uint32_t(cur >> 32)) return;
-    for (int a = 0; a < 3; ++a)
-        if (ord_key(c[a]) != lex[uint64_t(a) * P + pix]) return;
-    // all winners have identical coordinates: any of them gives the same height
-    pixkey[pix] = (cur & 0xFFFFFFFF00000000ull) | static_cast<uint32_t>(i);
 }
 
 __device__ inline float key_depth(unsigned long long k) {
@@ -131,26 +94,49 @@ __device__ inline bool normal_at(const double* __restrict__ dirs, int W, int u, 
     return true;
 }
 
-__global__ void k_finish_pixels(const float* __restrict__ pts, int stride,
-                                const unsigned long long* __restrict__ pixkey,
-                                const double* __restrict__ dirs, Pose pose, int W, int H,
-                                int with_normals, float* __restrict__ depth,
-                                float* __restrict__ height, float* __restrict__ normals,
-                                uint8_t* __restrict__ valid, uint8_t* __restrict__ tie) {
+__device__ inline d3 point_at(const float* __restrict__ pts, int stride, uint32_t i) {
+    return mk(pts[uint64_t(i) * stride], pts[uint64_t(i) * stride + 1],
+              pts[uint64_t(i) * stride + 2]);
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_finish_pixels(const float* __restrict__ pts, int stride, const unsigned long long* __restrict__ pixkey,
+                unsigned long long* __restrict__ next_pixkey, const double* __restrict__ dirs,
+                Pose pose, int W, int H, int with_normals, float* __restrict__ depth,
+                float* __restrict__ height, float* __restrict__ normals,
+                uint8_t* __restrict__ valid, uint8_t* __restrict__ tie,
+                const unsigned long long* __restrict__ ties, uint32_t tie_cap,
+                const uint32_t* __restrict__ ctr) {
+    if (ctr[C_ABORT]) return;
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= uint32_t(W) * H) return;
     const unsigned long long k = pixkey[p];
+    next_pixkey[p] = ~0ull;  // the other half is clean for the next projection
     const float d0 = key_depth(k);
     depth[p] = d0;
     float h = 0.f;
     if (k != ~0ull) {
-        const uint32_t i = uint32_t(k);
-        const d3 q = mk(pts[uint64_t(i) * stride], pts[uint64_t(i) * stride + 1],
-                        pts[uint64_t(i) * stride + 2]);
-        h = float(xform(pose, q).z);
+        uint32_t win = uint32_t(k);
+        if (tie[p]) {
+            // lexicographic minimum among the points of this pixel with its range
+            d3 best = point_at(pts, stride, win);
+            const uint32_t nt = min(ctr[C_TIES], tie_cap);
+            for (uint32_t t = 0; t < nt; ++t) {
+                const unsigned long long e = ties[t];
+                if (uint32_t(e >> 32) != p) continue;
+                const uint32_t i = uint32_t(e);
+                const d3 q = point_at(pts, stride, i);
+                if (__float_as_uint(float(sqrt(dot3(q, q)))) != uint32_t(k >> 32)) continue;
+                if (lex_less(q, best)) {
+                    best = q;
+                    win = i;
+                }
+            }
+            tie[p] = 0;
+        }
+        h = float(xform(pose, point_at(pts, stride, win)).z);
     }
     height[p] = h;
-    tie[p] = 0;
     if (!with_normals) return;
     const int u = int(p % W), v = int(p / W);
     float n[3] = {0.f, 0.f, 0.f};
@@ -181,38 +167,29 @@ inline unsigned grid_for(uint64_t n) { return unsigned((n + kThreads - 1) / kThr
 
 }  // namespace
 
+// Gated on the abort word and double-buffered (no memsets), so a batch of
+// frames can be queued without host synchronisation.
 void launch_project(svx_scan* s, const float* d_pts, uint64_t n, int stride, const Pose& pose) {
     svx_map* m = s->map;
     const uint32_t P = uint32_t(s->P);
-    s->pixkey.alloc(P);
-    s->lexkey.alloc(3ull * P);
-    s->tie.alloc(P);
-    DevBuf<uint32_t>& pix_of_pt = s->pix_of_pt;
-    pix_of_pt.alloc(n ? n : 1);
+    unsigned long long* cur = s->pixkey.p + uint64_t(s->parity) * P;
+    unsigned long long* nxt = s->pixkey.p + uint64_t(s->parity ^ 1) * P;
+    const uint32_t tie_cap = uint32_t(std::min<uint64_t>(2 * n + 2, 0xFFFFFFF0ull));
+    s->lexkey.alloc(tie_cap);  // tie list: (pixel << 32) | point index
     ProfMark pm(m, SVX_K_PROJECT);
     m->prof_acc.points += n;
-    SVX_CUDA(cudaMemsetAsync(s->pixkey.p, 0xFF, sizeof(unsigned long long) * P, m->stream));
-    SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_TIES, 0, sizeof(uint32_t), m->stream));
-    SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_DROPPED, 0, sizeof(uint32_t), m->stream));
     if (n) {
-        k_project_points<<<grid_for(n), kThreads, 0, m->stream>>>(d_pts, n, stride, s->dm,
-                                                                    s->pixkey.p, s->tie.p,
-                                                                    pix_of_pt.p, m->d_ctr);
-        k_tie_reset<<<grid_for(P), kThreads, 0, m->stream>>>(s->tie.p, s->lexkey.p, P, m->d_ctr);
-        for (int axis = 0; axis < 3; ++axis)
-            k_tie_axis<<<grid_for(n), kThreads, 0, m->stream>>>(d_pts, n, stride, pix_of_pt.p,
-                                                                  s->pixkey.p, s->tie.p,
-                                                                  s->lexkey.p, P, axis, m->d_ctr);
-        k_tie_winner<<<grid_for(n), kThreads, 0, m->stream>>>(d_pts, n, stride, pix_of_pt.p,
-                                                                s->pixkey.p, s->tie.p,
-                                                                s->lexkey.p, P, m->d_ctr);
-        count_launch(6);
+        k_project_points<<<grid_for(n), kThreads, 0, m->stream>>>(d_pts, n, stride, s->dm, cur,
+                                                                    s->tie.p, s->lexkey.p,
+                                                                    tie_cap, m->d_ctr);
+        count_launch();
     }
     k_finish_pixels<<<grid_for(P), kThreads, 0, m->stream>>>(
-        d_pts, stride, s->pixkey.p, s->dirs.p, pose, s->dm.W, s->dm.H, 1, s->depth.p,
-        s->height.p, s->normals.p, s->valid.p, s->tie.p);
-    count_launch(1);
+        d_pts, stride, cur, nxt, s->dirs.p, pose, s->dm.W, s->dm.H, 1, s->depth.p, s->height.p,
+        s->normals.p, s->valid.p, s->tie.p, s->lexkey.p, tie_cap, m->d_ctr);
+    count_launch();
     SVX_CUDA(cudaGetLastError());
+    s->parity ^= 1;
     s->has_normals = true;
     s->n_points = n;
 }

@@ -133,6 +133,7 @@ k_sem_update(SemParams sp, HashView h, const uint64_t* __restrict__ block_keys,
     const int lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    if (ctr[C_ERR_CONF]) return;  // invalid confidence: no voxel is touched
     const uint32_t n_cand = ctr[C_CAND];
     const int K = sp.K;
     uint32_t n_upd = 0;
@@ -251,12 +252,6 @@ __global__ void k_check_conf(const float* __restrict__ conf, uint64_t n, uint32_
     if (c < 0.f || c > 1.f) atomicAdd(&ctr[C_ERR_CONF], 1u);
 }
 
-unsigned persistent_grid(int device) {
-    static int sms[64] = {0};
-    if (!sms[device]) cudaDeviceGetAttribute(&sms[device], cudaDevAttrMultiProcessorCount, device);
-    return unsigned(sms[device] * 8);
-}
-
 }  // namespace
 
 void run_integrate_labels(svx_map* m, const svx_label_image& img, const svx_semantic_cfg& cfg,
@@ -313,17 +308,16 @@ void run_integrate_labels(svx_map* m, const svx_label_image& img, const svx_sema
                                  m->stream));
     }
     m->cand.alloc(std::max<uint64_t>(m->n_blocks, 1));
+    // a block owns at most one layer: map as many layers as there are blocks, so the
+    // update kernel never outgrows the pool and no mid-pass synchronisation is needed
+    ensure_layers(m, m->n_blocks);
     if (m->n_blocks) {
-        ProfMark pm(m, SVX_K_SEM_CULL);
-        k_sem_cull<<<grid_for(m->n_blocks), kThreads, 0, m->stream>>>(sp, m->block_keys, m->cand.p,
-                                                                      m->d_ctr);
-        count_launch();
-    }
-    sync_counters(m);
-    if (m->h_ctr[C_ERR_CONF]) throw Error(SVX_INVALID_ARGUMENT, "confidence must be in [0, 1]");
-    const uint32_t n_cand = m->h_ctr[C_CAND];
-    if (n_cand) {
-        ensure_layers(m, m->n_layers + n_cand);
+        {
+            ProfMark pm(m, SVX_K_SEM_CULL);
+            k_sem_cull<<<grid_for(m->n_blocks), kThreads, 0, m->stream>>>(sp, m->block_keys,
+                                                                          m->cand.p, m->d_ctr);
+            count_launch();
+        }
         {
             ProfMark pm(m, SVX_K_SEM_UPDATE);
             k_sem_update<<<persistent_grid(m->device), kThreads, 0, m->stream>>>(
@@ -333,8 +327,10 @@ void run_integrate_labels(svx_map* m, const svx_label_image& img, const svx_sema
             count_launch();
         }
         SVX_CUDA(cudaGetLastError());
-        sync_counters(m);
     }
+    sync_counters(m);
+    if (m->h_ctr[C_ERR_CONF]) throw Error(SVX_INVALID_ARGUMENT, "confidence must be in [0, 1]");
+    const uint32_t n_cand = m->h_ctr[C_CAND];
     rep->updated_voxels = m->h_ctr[C_SEM_UPDATED];
     m->prof_acc.sem_images += 1;
     m->prof_acc.sem_candidates += n_cand;

@@ -2,6 +2,7 @@
 // observed-voxel count, dirty-block compaction (voxel_store.cpp:9-80).
 #include <cuda.h>
 
+#include <algorithm>
 #include <mutex>
 #include <string>
 
@@ -112,6 +113,22 @@ VmmArray::~VmmArray() {
 void ensure_blocks(svx_map* m, uint64_t blocks) {
     if (blocks > m->cfg.max_blocks) blocks = m->cfg.max_blocks;
     m->tsdf_pool.ensure(blocks * m->block_bytes);
+    const uint64_t mapped = std::min<uint64_t>(m->tsdf_pool.mapped() / m->block_bytes, m->cfg.max_blocks);
+    if (mapped != m->mapped_blocks) {
+        m->mapped_blocks = mapped;
+        m->h_ctr[C_MAPPED] = uint32_t(mapped);
+        SVX_CUDA(cudaMemcpyAsync(m->d_ctr + C_MAPPED, &m->h_ctr[C_MAPPED], 4,
+                                 cudaMemcpyHostToDevice, m->stream));
+    }
+}
+
+void push_block_counters(svx_map* m) {
+    m->h_ctr[C_BLOCKS] = m->h_ctr[C_BLOCKS_BEFORE] = uint32_t(m->n_blocks);
+    m->h_ctr[C_SEM] = uint32_t(m->n_layers);
+    m->h_ctr[C_MAPPED] = uint32_t(m->mapped_blocks);
+    for (int c : {C_BLOCKS, C_SEM, C_BLOCKS_BEFORE, C_MAPPED})
+        SVX_CUDA(cudaMemcpyAsync(m->d_ctr + c, &m->h_ctr[c], 4, cudaMemcpyHostToDevice, m->stream));
+    SVX_CUDA(cudaStreamSynchronize(m->stream));
 }
 
 void ensure_layers(svx_map* m, uint64_t layers) {
@@ -313,6 +330,7 @@ uint32_t get_or_alloc_block(svx_map* m, uint64_t key, bool* was_new) {
     if (idx == kInvalid) throw Error(SVX_CAPACITY, "block hash table full");
     launch_zero_blocks(m, idx, 1);
     m->n_blocks = uint64_t(idx) + 1;
+    push_block_counters(m);
     if (was_new) *was_new = true;
     return idx;
 }

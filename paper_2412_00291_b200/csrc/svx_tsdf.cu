@@ -1,24 +1,34 @@
 // K3-K5: TsdfIntegrator::integrate_frame on the device (tsdf_integrator.cpp:97-258).
 //
-//   k_raycast_band   K3+K4. One thread per pixel: q = pose * back_project(u,v,r)
-//                    (direction table => bit-exact), band [q - tau r^, q + tau r^],
-//                    amortised DDA (tsdf_integrator.hpp:93-135). Per block crossing:
-//                    find-or-insert in the open-addressing hash (new block => pool
-//                    index from a bump counter), first touch this frame => append
-//                    the slot to the frame's touched list. Per visit: set the voxel
-//                    bit in the slot's 512-bit mask (RED.OR, consecutive visits in
-//                    one 32-voxel word are merged in registers first). This is the
-//                    per-scan dedup: visits collapse onto distinct voxels in L2.
-//   k_fold           K5. Persistent warps, one touched block per warp iteration,
-//                    lane = voxel (coalesced AoS access). For every touched voxel:
-//                    own pixel = project_point(T_ws * centre); if it holds a return,
-//                    measure that pixel only and fold (Eq. 4-5 accumulate-then-merge,
-//                    .cpp:170-248); otherwise flag the voxel for the fallback. New
-//                    blocks are written in full (zero-fill fused with the update).
-//   k_collect_fb     Fallback voxels only: re-walk the rays, emit (slot, linear,
-//   + radix sort     pixel) records for flagged voxels, sort => per-voxel visits in
-//   k_fold_fb        ascending (v, u) pixel order, exactly the reference's order
-//                    after its chunk-order merge + stable_sort; sequential fold.
+// Four kernels per frame on the map stream, no host synchronisation (a batch of
+// frames is synchronised once at its end):
+//   k_raycast_band  K3+K4. One thread per pixel. Writes the pixel cache (ray, range,
+//                   world normal: the measurement inputs of tsdf_integrator.cpp:178-186,
+//                   computed once per pixel instead of once per (pixel, voxel)).
+//                   Band [q - tau r^, q + tau r^], amortised DDA
+//                   (tsdf_integrator.hpp:93-135). Per block crossing: find-or-insert
+//                   in the open-addressing hash (new block => pool index from a bump
+//                   counter); first touch this frame => slot appended to the touched
+//                   list. Per visit: the voxel bit in the slot's 512-bit mask (RED.OR,
+//                   visits of one 32-voxel word merged in registers) and the own-pixel
+//                   test of the voxel (FP32, sensor-frame offset updated incrementally
+//                   along the DDA, exact decision via error margins): a voxel whose own
+//                   pixel has no return is measured by every visiting ray in the
+//                   reference (.cpp:232-238), so the visit becomes a fallback record.
+//   k_compact       warp per touched block: touched-voxel list (compaction of the mask
+//                   bits), zero-fill of new blocks, mask reset, dirty flag, bucket
+//                   allocation for the block's fallback records.
+//   k_fold          K5, one thread per touched voxel (flat, load-balanced): own pixel,
+//                   measure, accumulate-then-merge fold (Eq. 4-5, .cpp:170-248); then
+//                   scatters the fallback records into per-block buckets.
+//   k_fb_fold       warp per block with fallback records: bitonic sort of its bucket
+//                   (keys = linear << 23 | pixel) => per-voxel visits in ascending
+//                   (v, u) order, exactly the reference's order after its chunk-order
+//                   merge + stable_sort; measurements in parallel, then the per-voxel
+//                   sums strictly in that order; fold. Its last CTA writes the frame
+//                   report and resets the per-frame counters.
+// Every kernel first checks the abort word: after an abort (pool growth, buffer
+// growth, capacity) the rest of the batch no-ops and the host resumes it.
 #include <cub/device/device_radix_sort.cuh>
 #include <math_constants.h>
 
@@ -34,19 +44,33 @@ struct FrameParams {
     Model m;
     Pose pose, w2s;
     d3 origin;
+    float col[3][3];  // nu * (R^T e_m): sensor-frame step of +1 voxel along world axis m
     double tau, max_range, alpha_eps, nu, inv_nu;
     float min_clamp;
     int nonproj, drop_unreliable, has_normals;
     int32_t shard_rank, shard_world;
     uint32_t frame_serial;
-    uint32_t blocks_before;
     uint32_t max_blocks;
-    uint32_t rec_cap;
+    uint32_t rec_cap, vox_cap;
+};
+
+struct PixCache {
+    double ray[3];
+    double range;
+    float n[3];
+    uint32_t flags;  // bit0: measurable, bit1: has normal
+};
+static_assert(sizeof(PixCache) == 48, "PixCache layout");
+
+struct Term {  // one (pixel, voxel) measurement of the fallback path
+    float wg, w, nx, ny, nz;
+    uint32_t flags;  // bit0: measured, bit1: has normal
 };
 
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kWarpSort = 1024;  // max fallback keys per block sorted in one warp
 
 __device__ inline d3 dir_at(const double* __restrict__ dirs, uint32_t p) {
     return mk(__ldg(&dirs[3 * p]), __ldg(&dirs[3 * p + 1]), __ldg(&dirs[3 * p + 2]));
@@ -95,43 +119,77 @@ __device__ inline void traverse_segment(d3 a, d3 b, double nu, double inv, Visit
     }
 }
 
-// Ray of pixel p through the band (tsdf_integrator.cpp:123-131). Returns false
-// when the pixel is skipped.
-__device__ inline bool band_of(const FrameParams& f, const float* __restrict__ depth,
-                               const uint8_t* __restrict__ valid,
-                               const double* __restrict__ dirs, uint32_t p, d3& a, d3& b) {
-    const float r = depth[p];
-    if (r == 0.f || double(r) > f.max_range) return false;
-    if (f.drop_unreliable && f.has_normals && !valid[p]) return false;
-    const d3 q = xform(f.pose, scale3(double(r), dir_at(dirs, p)));
-    const d3 dq = sub3(q, f.origin);
-    const double z = dot3(dq, dq);
-    const d3 ray = z > 0.0 ? div3(dq, sqrt(z)) : dq;
-    const d3 tr = scale3(f.tau, ray);
-    a = sub3(q, tr);
-    b = add3(q, tr);
-    return true;
+__device__ inline d3 voxel_center(int32_t x, int32_t y, int32_t z, double nu) {
+    return mk(nu * x, nu * y, nu * z);
+}
+
+__device__ inline d3 center_of(uint64_t key, int linear, double nu) {
+    int32_t bx, by, bz;
+    unpack_key(key, bx, by, bz);
+    return voxel_center(bx * kBlockSide + linear % kBlockSide,
+                        by * kBlockSide + (linear / kBlockSide) % kBlockSide,
+                        bz * kBlockSide + linear / (kBlockSide * kBlockSide), nu);
+}
+
+// Own pixel of a voxel centre c: project_point(world_to_sensor * c)
+// (tsdf_integrator.cpp:232). pc is world_to_sensor * c in FP64 (reference formula).
+__device__ inline uint32_t own_pixel(const FrameParams& f, d3 pc) {
+    const uint32_t q = pixel_fast(float(pc.x), float(pc.y), float(pc.z), f.m, f.m.r2_lo, f.m.r2_hi);
+    return q == kNeedFp64 ? pixel_fp64(pc, f.m) : q;
 }
 
 __global__ void __launch_bounds__(kThreads)
-k_raycast_band(FrameParams f, const float* __restrict__ depth, const uint8_t* __restrict__ valid,
-               const double* __restrict__ dirs, HashView h, uint64_t* __restrict__ block_keys,
+k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __restrict__ normals,
+               const uint8_t* __restrict__ valid, const double* __restrict__ dirs,
+               PixCache* __restrict__ cache, HashView h, uint64_t* __restrict__ block_keys,
                uint32_t* __restrict__ stamp, uint32_t* __restrict__ touched,
-               uint32_t* __restrict__ vmask, uint32_t* __restrict__ ctr) {
+               uint32_t* __restrict__ vmask, uint32_t* __restrict__ fbcnt,
+               unsigned long long* __restrict__ rec, uint32_t* __restrict__ ctr) {
+    if (ctr[C_ABORT]) return;
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= uint32_t(f.m.W) * uint32_t(f.m.H)) return;
-    d3 a, b;
-    if (!band_of(f, depth, valid, dirs, p, a, b)) return;
+    const float r = depth[p];
+    const bool in_range = !(r == 0.f || double(r) > f.max_range);
+    const bool have_normal = f.has_normals && valid[p];
+    // pixel cache (measure lambda inputs, tsdf_integrator.cpp:173-186)
+    PixCache pc{};
+    d3 q = mk(0, 0, 0), ray = mk(0, 0, 0);
+    if (in_range) {
+        q = xform(f.pose, scale3(double(r), dir_at(dirs, p)));
+        const d3 dq = sub3(q, f.origin);
+        const double range = sqrt(dot3(dq, dq));
+        ray = div3(dq, range);
+        pc.ray[0] = ray.x;
+        pc.ray[1] = ray.y;
+        pc.ray[2] = ray.z;
+        pc.range = range;
+        if (have_normal) {
+            const d3 n = matvec(f.pose.R, mk(normals[3 * p], normals[3 * p + 1], normals[3 * p + 2]));
+            pc.n[0] = float(n.x);
+            pc.n[1] = float(n.y);
+            pc.n[2] = float(n.z);
+        }
+        pc.flags = ((have_normal || !f.drop_unreliable) ? 1u : 0u) | (have_normal ? 2u : 0u);
+    }
+    cache[p] = pc;
+    // band ray (tsdf_integrator.cpp:123-131)
+    if (!in_range) return;
+    if (f.drop_unreliable && f.has_normals && !valid[p]) return;
     warp_agg_inc(&ctr[C_RAYS]);
+    const d3 tr = scale3(f.tau, ray);  // (q - o).normalized() == (q - o) / range
+    const d3 a = sub3(q, tr), b = add3(q, tr);
 
     uint64_t cur_key = kEmptyKey;
     uint32_t cur_slot = kInvalid;
     uint32_t pend_word = kInvalid, pend_bits = 0;
-
+    // own-pixel state: FP32 sensor-frame offset of the current voxel centre
+    int32_t x0 = 0, y0 = 0, z0 = 0;
+    float p0x = 0.f, p0y = 0.f, p0z = 0.f;
+    bool first = true;
     traverse_segment(a, b, f.nu, f.inv_nu, [&](int32_t x, int32_t y, int32_t z) {
         const int32_t bx = block_coord(x), by = block_coord(y), bz = block_coord(z);
         if (!key_in_range(bx) || !key_in_range(by) || !key_in_range(bz)) {
-            atomicAdd(&ctr[C_ERR_KEY], 1u);
+            atomicOr(&ctr[C_ABORT], kAbortKey);
             return;
         }
         const uint64_t key = pack_key(bx, by, bz);
@@ -143,12 +201,14 @@ k_raycast_band(FrameParams f, const float* __restrict__ depth, const uint8_t* __
                 int ins = 0;
                 cur_slot = hash_insert(h, key, &ins);
                 if (cur_slot == kInvalid) {
-                    atomicAdd(&ctr[C_ERR_HASH], 1u);
+                    atomicOr(&ctr[C_ABORT], kAbortHash | kAbortCapacity);
                 } else {
                     if (ins) {
                         const uint32_t idx = atomicAdd(&ctr[C_BLOCKS], 1u);
                         h.vals[cur_slot] = idx;
                         if (idx < f.max_blocks) block_keys[idx] = key;
+                        if (idx >= f.max_blocks) atomicOr(&ctr[C_ABORT], kAbortCapacity);
+                        else if (idx >= ctr[C_MAPPED]) atomicOr(&ctr[C_ABORT], kAbortPool);
                     }
                     if (atomicExch(&stamp[cur_slot], f.frame_serial) != f.frame_serial) {
                         const uint32_t t = atomicAdd(&ctr[C_TOUCHED], 1u);
@@ -168,6 +228,32 @@ k_raycast_band(FrameParams f, const float* __restrict__ depth, const uint8_t* __
             pend_word = word;
             pend_bits = bit;
         }
+        // own-pixel test of the visited voxel
+        if (first) {
+            const d3 pc0 = xform(f.w2s, voxel_center(x, y, z, f.nu));
+            p0x = float(pc0.x);
+            p0y = float(pc0.y);
+            p0z = float(pc0.z);
+            x0 = x;
+            y0 = y;
+            z0 = z;
+            first = false;
+        }
+        const float kx = float(x - x0), ky = float(y - y0), kz = float(z - z0);
+        const float px = p0x + kx * f.col[0][0] + ky * f.col[1][0] + kz * f.col[2][0];
+        const float py = p0y + kx * f.col[0][1] + ky * f.col[1][1] + kz * f.col[2][1];
+        const float pz = p0z + kx * f.col[0][2] + ky * f.col[1][2] + kz * f.col[2][2];
+        uint32_t own = pixel_fast(px, py, pz, f.m, f.m.r2_lo, f.m.r2_hi);
+        if (own == kNeedFp64) own = pixel_fp64(xform(f.w2s, voxel_center(x, y, z, f.nu)), f.m);
+        if (own == kInvalid || depth[own] == 0.f) {
+            atomicAdd(&fbcnt[cur_slot], 1u);
+            const uint32_t pos = atomicAdd(&ctr[C_RECORDS], 1u);
+            if (pos < f.rec_cap)
+                rec[pos] = (static_cast<unsigned long long>(cur_slot) << 32) |
+                           (static_cast<unsigned long long>(lin) << 23) | p;
+            else
+                atomicOr(&ctr[C_ABORT], kAbortRecords);
+        }
     });
     if (pend_word != kInvalid) atomicOr(&vmask[pend_word], pend_bits);
 }
@@ -185,28 +271,19 @@ __device__ inline double nonprojective_distance(double psi, double theta, double
     return psi >= 0.0 ? mag : -mag;
 }
 
-// measure lambda (tsdf_integrator.cpp:172-205) for pixel p.
-__device__ inline bool measure(const FrameParams& f, const float* __restrict__ depth,
-                               const float* __restrict__ normals,
-                               const uint8_t* __restrict__ valid, const double* __restrict__ dirs,
-                               uint32_t p, d3 center, const svx_tsdf_voxel& vox, Accum& acc) {
-    const float dep = depth[p];
-    if (dep == 0.f || double(dep) > f.max_range) return false;
-    const bool have_normal = f.has_normals && valid[p];
-    if (!have_normal && f.drop_unreliable) return false;
-    const d3 q = xform(f.pose, scale3(double(dep), dir_at(dirs, p)));
-    const d3 qo = sub3(q, f.origin);
-    const double range = sqrt(dot3(qo, qo));
-    const d3 ray = div3(qo, range);
-    const double psi = range - dot3(sub3(center, f.origin), ray);
-    if (fabs(psi) > f.tau) return false;
-    float nw[3] = {0.f, 0.f, 0.f};
-    if (have_normal) {
-        const d3 r = matvec(f.pose.R, mk(normals[3 * p], normals[3 * p + 1], normals[3 * p + 2]));
-        nw[0] = float(r.x);
-        nw[1] = float(r.y);
-        nw[2] = float(r.z);
-    }
+// measure lambda (tsdf_integrator.cpp:172-205) for pixel p, from the pixel cache:
+// the contribution (w * Gamma(d), w, w * n) as the reference forms it, in f32.
+__device__ inline Term measure_term(const FrameParams& f, const PixCache* __restrict__ cache,
+                                    uint32_t p, d3 center, const svx_tsdf_voxel& vox) {
+    Term t{0.f, 0.f, 0.f, 0.f, 0.f, 0u};
+    const PixCache& pc = cache[p];
+    const uint32_t flags = pc.flags;
+    if (!(flags & 1u)) return t;
+    const bool have_normal = flags & 2u;
+    const d3 ray = mk(pc.ray[0], pc.ray[1], pc.ray[2]);
+    const double psi = pc.range - dot3(sub3(center, f.origin), ray);
+    if (fabs(psi) > f.tau) return t;
+    const float nw[3] = {pc.n[0], pc.n[1], pc.n[2]};
     double d = psi;
     if (f.nonproj && have_normal) {
         float g[3] = {nw[0], nw[1], nw[2]};
@@ -233,14 +310,26 @@ __device__ inline bool measure(const FrameParams& f, const float* __restrict__ d
     const float w_obs = float(wr);
     // truncate_distance (tsdf_integrator.hpp:57-59)
     const float gamma = float(d >= 0.0 ? (f.tau < d ? f.tau : d) : (d < -f.tau ? -f.tau : d));
-    acc.wd += double(w_obs * gamma);
-    acc.w += double(w_obs);
+    t.wg = w_obs * gamma;
+    t.w = w_obs;
     if (have_normal) {
-        acc.wx += double(w_obs * nw[0]);
-        acc.wy += double(w_obs * nw[1]);
-        acc.wz += double(w_obs * nw[2]);
+        t.nx = w_obs * nw[0];
+        t.ny = w_obs * nw[1];
+        t.nz = w_obs * nw[2];
     }
-    return true;
+    t.flags = 1u | (have_normal ? 2u : 0u);
+    return t;
+}
+
+// acc += term, in the reference's operation order (tsdf_integrator.cpp:201-203)
+__device__ inline void accumulate(Accum& acc, const Term& t) {
+    acc.wd += double(t.wg);
+    acc.w += double(t.w);
+    if (t.flags & 2u) {
+        acc.wx += double(t.nx);
+        acc.wy += double(t.ny);
+        acc.wz += double(t.nz);
+    }
 }
 
 // accumulate-then-merge fold (tsdf_integrator.cpp:239-247)
@@ -256,15 +345,6 @@ __device__ inline void fold(svx_tsdf_voxel& vox, const Accum& acc) {
         vox.gradient[1] = float(bl.y / nrm);
         vox.gradient[2] = float(bl.z / nrm);
     }
-}
-
-__device__ inline d3 center_of(uint64_t key, int linear, double nu) {
-    int32_t bx, by, bz;
-    unpack_key(key, bx, by, bz);
-    const int32_t x = bx * kBlockSide + linear % kBlockSide;
-    const int32_t y = by * kBlockSide + (linear / kBlockSide) % kBlockSide;
-    const int32_t z = bz * kBlockSide + linear / (kBlockSide * kBlockSide);
-    return mk(nu * x, nu * y, nu * z);
 }
 
 __device__ inline svx_tsdf_voxel load_voxel(const svx_tsdf_voxel* p) {
@@ -286,131 +366,260 @@ __device__ inline void store_voxel(svx_tsdf_voxel* p, const svx_tsdf_voxel& v) {
     d[4] = v.gradient[2];
 }
 
+// Touched-voxel list, new-block zero fill, mask reset, dirty flag, fallback
+// bucket allocation. Warp per touched block.
 __global__ void __launch_bounds__(kThreads)
-k_fold(FrameParams f, const float* __restrict__ depth, const float* __restrict__ normals,
-       const uint8_t* __restrict__ valid, const double* __restrict__ dirs, HashView h,
-       svx_tsdf_voxel* __restrict__ pool, const uint32_t* __restrict__ touched,
-       uint32_t* __restrict__ vmask, uint8_t* __restrict__ dirty, uint32_t* __restrict__ ctr) {
+k_compact(FrameParams f, HashView h, svx_tsdf_voxel* __restrict__ pool,
+          const uint32_t* __restrict__ touched, uint32_t* __restrict__ vmask,
+          uint8_t* __restrict__ dirty, uint32_t* __restrict__ vlist,
+          const uint32_t* __restrict__ fbcnt, uint32_t* __restrict__ fbstart,
+          uint32_t* __restrict__ fbfill, uint32_t* __restrict__ fbslots,
+          uint32_t* __restrict__ ctr) {
+    if (ctr[C_ABORT]) return;
     const int lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     const uint32_t n_touched = ctr[C_TOUCHED];
-    uint32_t n_upd = 0, n_fb = 0;
+    const uint32_t blocks_before = ctr[C_BLOCKS_BEFORE];
     for (uint32_t t = warp; t < n_touched; t += nwarps) {
         const uint32_t slot = touched[t];
         const uint32_t idx = h.vals[slot];
-        const uint64_t key = h.keys[slot];
-        const bool is_new = idx >= f.blocks_before;
-        svx_tsdf_voxel* blk = pool + uint64_t(idx) * kBlockVoxels;
         uint32_t* mw = vmask + uint64_t(slot) * 32;
-        for (int j = 0; j < 16; ++j) {
-            const uint32_t word = mw[j];
-            const int linear = j * 32 + lane;
-            const bool hit = (word >> lane) & 1u;
-            svx_tsdf_voxel vox;
-            if (is_new) {
-                vox = svx_tsdf_voxel{0.f, 0.f, {0.f, 0.f, 0.f}};
-            } else if (word) {
-                vox = load_voxel(blk + linear);
+        const uint32_t w = lane < 16 ? mw[lane] : 0u;
+        uint32_t incl = __popc(w);
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 15);
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&ctr[C_VOXLIST], total);
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        if (lane < 16) {
+            uint32_t pos = base + incl - __popc(w);
+            for (uint32_t bits = w; bits; bits &= bits - 1) {
+                const uint32_t linear = uint32_t(lane) * 32u + uint32_t(__ffs(bits) - 1);
+                if (pos < f.vox_cap) vlist[pos] = (t << 9) | linear;
+                ++pos;
             }
-            bool write = is_new, fb = false;
-            if (hit) {
-                const d3 c = center_of(key, linear, f.nu);
-                int ou, ov;
-                double orr;
-                if (project_point(xform(f.w2s, c), f.m, ou, ov, orr) &&
-                    depth[uint32_t(ov) * f.m.W + ou] != 0.f) {
-                    Accum acc{0.0, 0.0, 0.0, 0.0, 0.0};
-                    if (measure(f, depth, normals, valid, dirs, uint32_t(ov) * f.m.W + ou, c, vox,
-                                acc)) {
-                        fold(vox, acc);
-                        write = true;
-                        ++n_upd;
-                    }
-                } else {
-                    fb = true;
-                }
-            }
-            const uint32_t fbw = __ballot_sync(0xFFFFFFFFu, fb);
-            n_fb += fb ? 1 : 0;
-            if (write) store_voxel(blk + linear, vox);
-            if (lane == 0) {
-                mw[j] = 0u;
-                mw[16 + j] = fbw;
+            mw[lane] = 0u;
+        }
+        if (lane == 0) {
+            if (base + total > f.vox_cap) atomicOr(&ctr[C_ABORT], kAbortVoxList);
+            dirty[idx] = 1;
+            const uint32_t c = fbcnt[slot];
+            if (c) {
+                const uint32_t b = atomicAdd(&ctr[C_BUCKET_TOP], c);
+                fbstart[slot] = b;
+                fbfill[slot] = b;
+                fbslots[atomicAdd(&ctr[C_FB_BLOCKS], 1u)] = slot;
             }
         }
-        if (lane == 0) dirty[idx] = 1;
-    }
-    for (int o = 16; o; o >>= 1) {
-        n_upd += __shfl_xor_sync(0xFFFFFFFFu, n_upd, o);
-        n_fb += __shfl_xor_sync(0xFFFFFFFFu, n_fb, o);
-    }
-    if (lane == 0) {
-        if (n_upd) atomicAdd(&ctr[C_UPDATED], n_upd);
-        if (n_fb) atomicAdd(&ctr[C_FALLBACK], n_fb);
+        if (idx >= blocks_before) {  // zero-fill the fresh block (coalesced)
+            float4* z = reinterpret_cast<float4*>(pool + uint64_t(idx) * kBlockVoxels);
+            for (int i = lane; i < kBlockVoxels * 5 / 4; i += 32) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
     }
 }
 
-// Fallback visit records: (slot << 32) | (linear << 23) | pixel.
+// One thread per touched voxel; then the fallback record scatter.
 __global__ void __launch_bounds__(kThreads)
-k_collect_fb(FrameParams f, const float* __restrict__ depth, const uint8_t* __restrict__ valid,
-             const double* __restrict__ dirs, HashView h, const uint32_t* __restrict__ vmask,
-             unsigned long long* __restrict__ rec, uint32_t* __restrict__ ctr) {
-    if (ctr[C_FALLBACK] == 0) return;
-    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= uint32_t(f.m.W) * uint32_t(f.m.H)) return;
-    d3 a, b;
-    if (!band_of(f, depth, valid, dirs, p, a, b)) return;
-    uint64_t cur_key = kEmptyKey;
-    uint32_t cur_slot = kInvalid;
-    traverse_segment(a, b, f.nu, f.inv_nu, [&](int32_t x, int32_t y, int32_t z) {
-        const int32_t bx = block_coord(x), by = block_coord(y), bz = block_coord(z);
-        if (!key_in_range(bx) || !key_in_range(by) || !key_in_range(bz)) return;
-        const uint64_t key = pack_key(bx, by, bz);
-        if (key != cur_key) {
-            cur_key = key;
-            cur_slot = (f.shard_world > 1 && owner_of(key, f.shard_world) != f.shard_rank)
-                           ? kInvalid
-                           : hash_find(h, key);
-        }
-        if (cur_slot == kInvalid) return;
-        const int lin = local_linear(x, y, z);
-        if (!((vmask[uint64_t(cur_slot) * 32 + 16 + (lin >> 5)] >> (lin & 31)) & 1u)) return;
-        const uint32_t pos = atomicAdd(&ctr[C_RECORDS], 1u);
-        if (pos < f.rec_cap)
-            rec[pos] = (static_cast<unsigned long long>(cur_slot) << 32) |
-                       (static_cast<unsigned long long>(lin) << 23) | p;
-    });
-}
-
-__global__ void __launch_bounds__(kThreads)
-k_fold_fb(FrameParams f, const float* __restrict__ depth, const float* __restrict__ normals,
-          const uint8_t* __restrict__ valid, const double* __restrict__ dirs, HashView h,
-          svx_tsdf_voxel* __restrict__ pool, const unsigned long long* __restrict__ rec,
-          uint32_t n, uint32_t* __restrict__ ctr) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t upd = 0;
-    if (i < n && (i == 0 || (rec[i - 1] >> 23) != (rec[i] >> 23))) {
-        const unsigned long long head = rec[i] >> 23;
-        const uint32_t slot = uint32_t(head >> 9);
-        const int linear = int(head & 511);
-        const uint32_t idx = h.vals[slot];
+k_fold(FrameParams f, const float* __restrict__ depth, const PixCache* __restrict__ cache,
+       HashView h, svx_tsdf_voxel* __restrict__ pool, const uint32_t* __restrict__ touched,
+       const uint32_t* __restrict__ vlist, const unsigned long long* __restrict__ rec,
+       uint32_t* __restrict__ fbfill, uint32_t* __restrict__ bucket, uint32_t* __restrict__ ctr) {
+    if (ctr[C_ABORT]) return;
+    const uint32_t nv = ctr[C_VOXLIST];
+    const uint32_t stride = gridDim.x * blockDim.x;
+    uint32_t n_upd = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+        const uint32_t v = vlist[i];
+        const uint32_t slot = touched[v >> 9];
+        const int linear = int(v & 511u);
         const d3 c = center_of(h.keys[slot], linear, f.nu);
-        svx_tsdf_voxel* vp = pool + uint64_t(idx) * kBlockVoxels + linear;
+        const uint32_t own = own_pixel(f, xform(f.w2s, c));
+        if (own == kInvalid || depth[own] == 0.f) continue;  // fallback path
+        svx_tsdf_voxel* vp = pool + uint64_t(h.vals[slot]) * kBlockVoxels + linear;
         svx_tsdf_voxel vox = load_voxel(vp);
-        Accum acc{0.0, 0.0, 0.0, 0.0, 0.0};
-        bool measured = false;
-        for (uint32_t j = i; j < n && (rec[j] >> 23) == head; ++j)
-            measured |= measure(f, depth, normals, valid, dirs, uint32_t(rec[j] & 0x7FFFFF), c,
-                                vox, acc);
-        if (measured) {
+        const Term t = measure_term(f, cache, own, c, vox);
+        if (t.flags & 1u) {
+            Accum acc{0.0, 0.0, 0.0, 0.0, 0.0};
+            accumulate(acc, t);
             fold(vox, acc);
             store_voxel(vp, vox);
-            upd = 1;
+            ++n_upd;
         }
     }
-    const unsigned any = __ballot_sync(0xFFFFFFFFu, upd);
-    if ((threadIdx.x & 31) == 0 && any) atomicAdd(&ctr[C_UPDATED], uint32_t(__popc(any)));
+    const uint32_t nr = min(ctr[C_RECORDS], f.rec_cap);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += stride) {
+        const unsigned long long r = rec[i];
+        const uint32_t pos = atomicAdd(&fbfill[uint32_t(r >> 32)], 1u);
+        bucket[pos] = uint32_t(r);
+    }
+    for (int o = 16; o; o >>= 1) n_upd += __shfl_xor_sync(0xFFFFFFFFu, n_upd, o);
+    if ((threadIdx.x & 31) == 0 && n_upd) atomicAdd(&ctr[C_UPDATED], n_upd);
+}
+
+__device__ void write_frame_end(FrameOut* __restrict__ out, uint32_t* __restrict__ ctr) {
+    FrameOut o;
+    o.updated = ctr[C_UPDATED];
+    o.new_blocks = ctr[C_BLOCKS] - ctr[C_BLOCKS_BEFORE];
+    o.touched = ctr[C_TOUCHED];
+    o.records = ctr[C_RECORDS];
+    o.rays = ctr[C_RAYS];
+    o.dropped = ctr[C_DROPPED];
+    o.fb_voxels = ctr[C_FB_VOXELS];
+    o.ok = 1;
+    *out = o;
+    ctr[C_TOUCHED] = ctr[C_UPDATED] = ctr[C_RECORDS] = ctr[C_RAYS] = 0;
+    ctr[C_DROPPED] = ctr[C_TIES] = ctr[C_FB_BLOCKS] = ctr[C_FB_VOXELS] = ctr[C_FB_BIG] = 0;
+    ctr[C_VOXLIST] = ctr[C_BUCKET_TOP] = 0;
+    ctr[C_BLOCKS_BEFORE] = ctr[C_BLOCKS];
+}
+
+// Ordered fold of one fallback voxel from its measured terms [i, end).
+__device__ inline bool fold_terms(svx_tsdf_voxel* vp, const Term* __restrict__ terms, uint32_t i,
+                                  uint32_t end) {
+    Accum acc{0.0, 0.0, 0.0, 0.0, 0.0};
+    bool measured = false;
+    for (uint32_t j = i; j < end; ++j) {
+        const Term t = terms[j];
+        if (t.flags & 1u) {
+            accumulate(acc, t);
+            measured = true;
+        }
+    }
+    if (!measured) return false;
+    svx_tsdf_voxel vox = load_voxel(vp);
+    fold(vox, acc);
+    store_voxel(vp, vox);
+    return true;
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_fb_fold(FrameParams f, const PixCache* __restrict__ cache, HashView h,
+          svx_tsdf_voxel* __restrict__ pool, const uint32_t* __restrict__ fbslots,
+          uint32_t* __restrict__ fbcnt, const uint32_t* __restrict__ fbstart,
+          const uint32_t* __restrict__ bucket, Term* __restrict__ terms,
+          uint32_t* __restrict__ bigslots, FrameOut* __restrict__ out, uint32_t* __restrict__ ctr) {
+    if (ctr[C_ABORT]) return;
+    __shared__ uint32_t sk[kThreads / 32][kWarpSort];
+    __shared__ bool last;
+    const int lane = threadIdx.x & 31;
+    uint32_t* keys = sk[threadIdx.x >> 5];
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t nb = ctr[C_FB_BLOCKS];
+    uint32_t n_upd = 0;
+    for (uint32_t t = warp; t < nb; t += nwarps) {
+        const uint32_t slot = fbslots[t];
+        const uint32_t cnt = fbcnt[slot];
+        const uint32_t start = fbstart[slot];
+        if (cnt > kWarpSort) {
+            if (lane == 0) {
+                bigslots[atomicAdd(&ctr[C_FB_BIG], 1u)] = slot;
+                atomicOr(&ctr[C_ABORT], kAbortBigBucket);
+            }
+            continue;
+        }
+        uint32_t n2 = 32;
+        while (n2 < cnt) n2 <<= 1;
+        for (uint32_t i = lane; i < n2; i += 32) keys[i] = i < cnt ? bucket[start + i] : 0xFFFFFFFFu;
+        __syncwarp();
+        for (uint32_t k = 2; k <= n2; k <<= 1) {  // bitonic sort, ascending
+            for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+                for (uint32_t i = lane; i < n2; i += 32) {
+                    const uint32_t l = i ^ jj;
+                    if (l > i) {
+                        const uint32_t a = keys[i], b = keys[l];
+                        if ((a > b) == ((i & k) == 0)) {
+                            keys[i] = b;
+                            keys[l] = a;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        const uint64_t key = h.keys[slot];
+        svx_tsdf_voxel* blk = pool + uint64_t(h.vals[slot]) * kBlockVoxels;
+        Term* tb = terms + start;
+        // measurements in parallel (pre-update voxel state, read-only here)
+        for (uint32_t i = lane; i < cnt; i += 32) {
+            const uint32_t kv = keys[i];
+            const int linear = int(kv >> 23);
+            tb[i] = measure_term(f, cache, kv & 0x7FFFFFu, center_of(key, linear, f.nu),
+                                 load_voxel(blk + linear));
+        }
+        __syncwarp();
+        // per-voxel sums strictly in pixel order, one lane per voxel segment
+        for (uint32_t i = lane; i < cnt; i += 32) {
+            if (i != 0 && (keys[i] >> 23) == (keys[i - 1] >> 23)) continue;
+            uint32_t end = i + 1;
+            while (end < cnt && (keys[end] >> 23) == (keys[i] >> 23)) ++end;
+            n_upd += fold_terms(blk + (keys[i] >> 23), tb, i, end) ? 1u : 0u;
+        }
+        __syncwarp();
+        if (lane == 0) fbcnt[slot] = 0u;
+    }
+    for (int o = 16; o; o >>= 1) n_upd += __shfl_xor_sync(0xFFFFFFFFu, n_upd, o);
+    if (lane == 0 && n_upd) {
+        atomicAdd(&ctr[C_UPDATED], n_upd);
+        atomicAdd(&ctr[C_FB_VOXELS], n_upd);
+    }
+    // the last CTA to finish writes the frame report
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&ctr[C_DONE], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        ctr[C_DONE] = 0;
+        if (!atomicAdd(&ctr[C_ABORT], 0u)) write_frame_end(out, ctr);
+    }
+}
+
+// Host-sorted bucket of one big block: terms in parallel, then ordered sums.
+__global__ void k_fb_terms_sorted(FrameParams f, const PixCache* __restrict__ cache, HashView h,
+                                  svx_tsdf_voxel* __restrict__ pool, uint32_t slot,
+                                  const uint32_t* __restrict__ keys, uint32_t cnt,
+                                  Term* __restrict__ terms) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cnt) return;
+    const int linear = int(keys[i] >> 23);
+    svx_tsdf_voxel* blk = pool + uint64_t(h.vals[slot]) * kBlockVoxels;
+    terms[i] = measure_term(f, cache, keys[i] & 0x7FFFFFu, center_of(h.keys[slot], linear, f.nu),
+                            load_voxel(blk + linear));
+}
+
+__global__ void k_fb_fold_sorted(HashView h, svx_tsdf_voxel* __restrict__ pool, uint32_t slot,
+                                 const uint32_t* __restrict__ keys, uint32_t cnt,
+                                 const Term* __restrict__ terms, uint32_t* __restrict__ ctr) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cnt || !(i == 0 || (keys[i] >> 23) != (keys[i - 1] >> 23))) return;
+    uint32_t end = i + 1;
+    while (end < cnt && (keys[end] >> 23) == (keys[i] >> 23)) ++end;
+    svx_tsdf_voxel* blk = pool + uint64_t(h.vals[slot]) * kBlockVoxels;
+    if (fold_terms(blk + (keys[i] >> 23), terms, i, end)) {
+        atomicAdd(&ctr[C_UPDATED], 1u);
+        atomicAdd(&ctr[C_FB_VOXELS], 1u);
+    }
+}
+
+__global__ void k_frame_end(FrameOut* __restrict__ out, uint32_t* __restrict__ ctr) {
+    if (ctr[C_ABORT]) return;
+    write_frame_end(out, ctr);
+}
+
+// Undo the per-frame record state before re-running the band kernel of a frame.
+__global__ void k_reset_fb(const uint32_t* __restrict__ touched, uint32_t* __restrict__ fbcnt,
+                           uint32_t* __restrict__ ctr) {
+    const uint32_t n = ctr[C_TOUCHED];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        fbcnt[touched[i]] = 0;
 }
 
 // Capacity path: every visited block key of the frame (duplicates allowed).
@@ -420,10 +629,15 @@ k_collect_keys(FrameParams f, const float* __restrict__ depth, const uint8_t* __
                uint32_t cap, uint32_t* __restrict__ ctr) {
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= uint32_t(f.m.W) * uint32_t(f.m.H)) return;
-    d3 a, b;
-    if (!band_of(f, depth, valid, dirs, p, a, b)) return;
+    const float r = depth[p];
+    if (r == 0.f || double(r) > f.max_range) return;
+    if (f.drop_unreliable && f.has_normals && !valid[p]) return;
+    const d3 q = xform(f.pose, scale3(double(r), dir_at(dirs, p)));
+    const d3 dq = sub3(q, f.origin);
+    const d3 ray = div3(dq, sqrt(dot3(dq, dq)));
+    const d3 tr = scale3(f.tau, ray);
     uint64_t cur_key = kEmptyKey;
-    traverse_segment(a, b, f.nu, f.inv_nu, [&](int32_t x, int32_t y, int32_t z) {
+    traverse_segment(sub3(q, tr), add3(q, tr), f.nu, f.inv_nu, [&](int32_t x, int32_t y, int32_t z) {
         const int32_t bx = block_coord(x), by = block_coord(y), bz = block_coord(z);
         if (!key_in_range(bx) || !key_in_range(by) || !key_in_range(bz)) return;
         const uint64_t key = pack_key(bx, by, bz);
@@ -445,33 +659,94 @@ __global__ void k_mark_dirty(const uint64_t* __restrict__ keys_sorted, uint32_t 
 
 inline unsigned grid_for(uint64_t n) { return unsigned((n + kThreads - 1) / kThreads); }
 
-unsigned persistent_grid(int device) {
-    static int sms[64] = {0};
-    if (!sms[device]) cudaDeviceGetAttribute(&sms[device], cudaDevAttrMultiProcessorCount, device);
-    return unsigned(sms[device] * 8);  // 8 CTAs x 8 warps per SM
+FrameParams make_params(svx_map* m, svx_scan* s, const Pose& pose, const svx_integrator_cfg& cfg) {
+    FrameParams f{};
+    f.m = s->dm;
+    f.pose = pose;
+    f.w2s = inverse_pose(pose);
+    f.origin = mk(pose.t[0], pose.t[1], pose.t[2]);
+    const double nu = double(m->cfg.voxel_size);
+    for (int a = 0; a < 3; ++a)        // world axis
+        for (int i = 0; i < 3; ++i)    // sensor component: (R^T)_{i a} = R_{a i}
+            f.col[a][i] = float(nu * pose.R[3 * a + i]);
+    f.tau = cfg.truncation > 0.f ? double(cfg.truncation) : double(m->cfg.truncation);
+    f.max_range = cfg.max_range;
+    f.alpha_eps = cfg.alpha_epsilon;
+    f.min_clamp = cfg.min_weight_clamp;
+    f.nonproj = cfg.mode == SVX_NON_PROJECTIVE;
+    f.drop_unreliable = cfg.drop_unreliable != 0;
+    f.has_normals = s->has_normals;
+    f.nu = nu;
+    f.inv_nu = 1.0 / nu;
+    f.shard_rank = m->shard_rank;
+    f.shard_world = m->shard_world;
+    f.frame_serial = ++m->frame_serial;
+    f.max_blocks = m->cfg.max_blocks;
+    f.rec_cap = m->rec_cap;
+    f.vox_cap = m->vox_cap;
+    return f;
 }
 
-void sort_u64(svx_map* m, unsigned long long* in, unsigned long long* out, uint32_t n) {
+// Stages of one frame: 0 band, 1 compact, 2 fold, 3 fallback (+ report), 4 report only.
+void launch_stages(svx_map* m, svx_scan* s, const FrameParams& f, int from, FrameOut* out) {
+    const uint32_t P = uint32_t(s->P);
+    HashView hv = hash_view(m);
+    const PixCache* cache = reinterpret_cast<const PixCache*>(s->pixcache.p);
+    const unsigned pg = persistent_grid(m->device);
+    if (from <= 0) {
+        ProfMark pm(m, SVX_K_RAYCAST);
+        k_raycast_band<<<grid_for(P), kThreads, 0, m->stream>>>(
+            f, s->depth.p, s->normals.p, s->valid.p, s->dirs.p,
+            reinterpret_cast<PixCache*>(s->pixcache.p), hv, m->block_keys, m->stamp, m->touched,
+            m->vmask, m->fbcnt, m->records.p, m->d_ctr);
+        count_launch();
+    }
+    if (from <= 1) {
+        ProfMark pm(m, SVX_K_COMPACT);
+        k_compact<<<pg, kThreads, 0, m->stream>>>(f, hv, tsdf_base(m), m->touched, m->vmask,
+                                                  m->dirty, m->vlist.p, m->fbcnt, m->fbstart,
+                                                  m->fbfill, m->fbslots, m->d_ctr);
+        count_launch();
+    }
+    if (from <= 2) {
+        ProfMark pm(m, SVX_K_FOLD);
+        k_fold<<<pg, kThreads, 0, m->stream>>>(f, s->depth.p, cache, hv, tsdf_base(m), m->touched,
+                                               m->vlist.p, m->records.p, m->fbfill, m->bucket.p,
+                                               m->d_ctr);
+        count_launch();
+    }
+    if (from <= 3) {
+        ProfMark pm(m, SVX_K_FALLBACK);
+        k_fb_fold<<<pg, kThreads, 0, m->stream>>>(f, cache, hv, tsdf_base(m), m->fbslots, m->fbcnt,
+                                                  m->fbstart, m->bucket.p,
+                                                  reinterpret_cast<Term*>(m->terms.p), m->bigslots,
+                                                  out, m->d_ctr);
+        count_launch();
+    } else {
+        k_frame_end<<<1, 1, 0, m->stream>>>(out, m->d_ctr);
+        count_launch();
+    }
+    SVX_CUDA(cudaGetLastError());
+}
+
+void sort_u32(svx_map* m, uint32_t* in, uint32_t* out, uint32_t n) {
     size_t bytes = 0;
-    SVX_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, in, out, int(n), 0, 64, m->stream));
+    SVX_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, in, out, int(n), 0, 32, m->stream));
     m->sort_tmp.alloc(bytes ? bytes : 1);
-    SVX_CUDA(cub::DeviceRadixSort::SortKeys(m->sort_tmp.p, bytes, in, out, int(n), 0, 64, m->stream));
+    SVX_CUDA(cub::DeviceRadixSort::SortKeys(m->sort_tmp.p, bytes, in, out, int(n), 0, 32, m->stream));
 }
 
 // CapacityError path (tsdf_integrator.cpp:160-168 + voxel_store.cpp:18-20):
 // blocks are allocated in sorted key order until max_blocks is reached; every
 // block before the failing one is marked dirty; no voxel is updated.
-void capacity_path(svx_map* m, const FrameParams& f0, svx_scan* s) {
-    FrameParams f = f0;
-    const uint32_t before = f.blocks_before;
-    // 1. all visited keys of the frame
+[[noreturn]] void capacity_path(svx_map* m, const FrameParams& f, svx_scan* s, uint32_t before) {
     uint32_t cap = uint32_t(std::min<uint64_t>(uint64_t(s->P) * 64, 1u << 30));
     for (;;) {
-        m->records.alloc(cap);
+        m->records_alt.alloc(cap);
         SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_RECORDS, 0, 4, m->stream));
         k_collect_keys<<<grid_for(s->P), kThreads, 0, m->stream>>>(f, s->depth.p, s->valid.p,
-                                                                   s->dirs.p, m->records.p, cap,
-                                                                   m->d_ctr);
+                                                                   s->dirs.p, m->records_alt.p,
+                                                                   cap, m->d_ctr);
         count_launch();
         sync_counters(m);
         if (m->h_ctr[C_RECORDS] <= cap) break;
@@ -479,46 +754,40 @@ void capacity_path(svx_map* m, const FrameParams& f0, svx_scan* s) {
     }
     const uint32_t n = m->h_ctr[C_RECORDS];
     std::vector<unsigned long long> keys(n);
-    SVX_CUDA(cudaMemcpy(keys.data(), m->records.p, sizeof(unsigned long long) * n,
+    SVX_CUDA(cudaMemcpy(keys.data(), m->records_alt.p, sizeof(unsigned long long) * n,
                         cudaMemcpyDeviceToHost));
     std::sort(keys.begin(), keys.end());
     keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
-    // 2. existing blocks (pool [0, before)) keep their indices
     std::vector<unsigned long long> existing(before);
     if (before)
         SVX_CUDA(cudaMemcpy(existing.data(), m->block_keys, sizeof(unsigned long long) * before,
                             cudaMemcpyDeviceToHost));
-    std::vector<unsigned long long> ex_sorted = existing;
-    std::sort(ex_sorted.begin(), ex_sorted.end());
+    std::sort(existing.begin(), existing.end());
     std::vector<unsigned long long> alloc_new, dirty_keys;
     uint64_t room = m->cfg.max_blocks > before ? m->cfg.max_blocks - before : 0;
     for (unsigned long long k : keys) {
-        const bool exists = std::binary_search(ex_sorted.begin(), ex_sorted.end(), k);
-        if (!exists) {
+        if (!std::binary_search(existing.begin(), existing.end(), k)) {
             if (room == 0) break;  // get_or_allocate_block throws here
             alloc_new.push_back(k);
             --room;
         }
         dirty_keys.push_back(k);
     }
-    // 3. rebuild the hash from the surviving key set
     const uint64_t total = before + alloc_new.size();
     ensure_blocks(m, total);
     if (!alloc_new.empty())
         SVX_CUDA(cudaMemcpy(m->block_keys + before, alloc_new.data(),
                             sizeof(unsigned long long) * alloc_new.size(), cudaMemcpyHostToDevice));
-    m->h_ctr[C_BLOCKS] = uint32_t(total);
-    SVX_CUDA(cudaMemcpy(m->d_ctr + C_BLOCKS, &m->h_ctr[C_BLOCKS], 4, cudaMemcpyHostToDevice));
     m->n_blocks = total;
     rebuild_hash(m);
     launch_zero_blocks(m, before, alloc_new.size());
-    SVX_CUDA(cudaMemsetAsync(m->vmask, 0, sizeof(uint32_t) * 32ull * m->cap, m->stream));
+    reset_frame_state(m);
     if (!dirty_keys.empty()) {
-        m->records.alloc(dirty_keys.size());
-        SVX_CUDA(cudaMemcpy(m->records.p, dirty_keys.data(),
+        m->records_alt.alloc(dirty_keys.size());
+        SVX_CUDA(cudaMemcpy(m->records_alt.p, dirty_keys.data(),
                             sizeof(unsigned long long) * dirty_keys.size(), cudaMemcpyHostToDevice));
         k_mark_dirty<<<grid_for(dirty_keys.size()), kThreads, 0, m->stream>>>(
-            reinterpret_cast<const uint64_t*>(m->records.p), uint32_t(dirty_keys.size()),
+            reinterpret_cast<const uint64_t*>(m->records_alt.p), uint32_t(dirty_keys.size()),
             hash_view(m), m->dirty);
         count_launch();
     }
@@ -527,102 +796,191 @@ void capacity_path(svx_map* m, const FrameParams& f0, svx_scan* s) {
                                   std::to_string(m->cfg.max_blocks) + ")");
 }
 
+// Host side of kAbortBigBucket: sort each oversized bucket with CUB, fold it.
+void big_buckets(svx_map* m, svx_scan* s, const FrameParams& f) {
+    const uint32_t nbig = m->h_ctr[C_FB_BIG];
+    std::vector<uint32_t> slots(nbig), cnt(nbig), start(nbig);
+    SVX_CUDA(cudaMemcpy(slots.data(), m->bigslots, 4 * nbig, cudaMemcpyDeviceToHost));
+    for (uint32_t i = 0; i < nbig; ++i) {
+        SVX_CUDA(cudaMemcpy(&cnt[i], m->fbcnt + slots[i], 4, cudaMemcpyDeviceToHost));
+        SVX_CUDA(cudaMemcpy(&start[i], m->fbstart + slots[i], 4, cudaMemcpyDeviceToHost));
+    }
+    const PixCache* cache = reinterpret_cast<const PixCache*>(s->pixcache.p);
+    Term* terms = reinterpret_cast<Term*>(m->terms.p);
+    DevBuf<uint32_t> tmp;
+    for (uint32_t i = 0; i < nbig; ++i) {
+        tmp.alloc(cnt[i]);
+        sort_u32(m, m->bucket.p + start[i], tmp.p, cnt[i]);
+        k_fb_terms_sorted<<<grid_for(cnt[i]), kThreads, 0, m->stream>>>(
+            f, cache, hash_view(m), tsdf_base(m), slots[i], tmp.p, cnt[i], terms + start[i]);
+        k_fb_fold_sorted<<<grid_for(cnt[i]), kThreads, 0, m->stream>>>(
+            hash_view(m), tsdf_base(m), slots[i], tmp.p, cnt[i], terms + start[i], m->d_ctr);
+        count_launch(2);
+        SVX_CUDA(cudaMemsetAsync(m->fbcnt + slots[i], 0, 4, m->stream));
+        SVX_CUDA(cudaStreamSynchronize(m->stream));
+    }
+    tmp.release();
+}
+
 }  // namespace
 
-void run_integrate(svx_map* m, svx_scan* s, const Pose& pose, const svx_integrator_cfg& cfg,
-                   svx_frame_report* rep) {
-    rep->frame = m->tsdf_frames++;
-    rep->updated_voxels = 0;
-    rep->new_blocks = 0;
+unsigned persistent_grid(int device) {
+    static int sms[64] = {0};
+    if (!sms[device]) cudaDeviceGetAttribute(&sms[device], cudaDevAttrMultiProcessorCount, device);
+    return unsigned(sms[device] * 8);  // 8 CTAs x 8 warps per SM
+}
+
+// Clears the frame scratch (masks, fallback counts, per-frame counters) after a
+// host-side intervention, and re-arms the device block counters.
+void reset_frame_state(svx_map* m) {
+    SVX_CUDA(cudaMemsetAsync(m->vmask, 0, sizeof(uint32_t) * 32ull * m->cap, m->stream));
+    SVX_CUDA(cudaMemsetAsync(m->fbcnt, 0, sizeof(uint32_t) * m->cap, m->stream));
+    for (int c : {C_TOUCHED, C_UPDATED, C_RECORDS, C_RAYS, C_DROPPED, C_TIES, C_FB_BLOCKS,
+                  C_FB_VOXELS, C_FB_BIG, C_ABORT, C_VOXLIST, C_BUCKET_TOP, C_DONE})
+        m->h_ctr[c] = 0;
+    m->h_ctr[C_BLOCKS] = m->h_ctr[C_BLOCKS_BEFORE] = uint32_t(m->n_blocks);
+    m->h_ctr[C_MAPPED] = uint32_t(m->mapped_blocks);
+    SVX_CUDA(cudaMemcpyAsync(m->d_ctr, m->h_ctr, sizeof(uint32_t) * kNumCounters,
+                             cudaMemcpyHostToDevice, m->stream));
+    SVX_CUDA(cudaStreamSynchronize(m->stream));
+}
+
+namespace {
+void put_ctr(svx_map* m, int c, uint32_t v) {
+    m->h_ctr[c] = v;
+    SVX_CUDA(cudaMemcpyAsync(m->d_ctr + c, &m->h_ctr[c], 4, cudaMemcpyHostToDevice, m->stream));
+}
+}  // namespace
+
+void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cfg& cfg,
+                svx_frame_report* reps) {
     if (!(cfg.alpha_epsilon > 0.0)) throw Error(SVX_INVALID_ARGUMENT, "alpha_epsilon must be > 0");
-    if (cfg.mode == SVX_NON_PROJECTIVE && !s->has_normals)
-        throw Error(SVX_INVALID_ARGUMENT, "non-projective mode needs a normal image");
-
-    FrameParams f{};
-    f.m = s->dm;
-    f.pose = pose;
-    f.w2s = inverse_pose(pose);
-    f.origin = mk(pose.t[0], pose.t[1], pose.t[2]);
-    f.tau = cfg.truncation > 0.f ? double(cfg.truncation) : double(m->cfg.truncation);
-    f.max_range = cfg.max_range;
-    f.alpha_eps = cfg.alpha_epsilon;
-    f.min_clamp = cfg.min_weight_clamp;
-    f.nonproj = cfg.mode == SVX_NON_PROJECTIVE;
-    f.drop_unreliable = cfg.drop_unreliable != 0;
-    f.has_normals = s->has_normals;
-    f.nu = double(m->cfg.voxel_size);
-    f.inv_nu = 1.0 / double(m->cfg.voxel_size);
-    f.shard_rank = m->shard_rank;
-    f.shard_world = m->shard_world;
-    f.frame_serial = ++m->frame_serial;
-    f.blocks_before = uint32_t(m->n_blocks);
-    f.max_blocks = m->cfg.max_blocks;
-
-    const uint32_t P = uint32_t(s->P);
-    SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_TOUCHED, 0, sizeof(uint32_t) * (C_ERR_HASH - C_TOUCHED + 1),
-                             m->stream));
-    SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_RAYS, 0, sizeof(uint32_t), m->stream));
-    HashView hv = hash_view(m);
-    ProfMark* pm = new ProfMark(m, SVX_K_RAYCAST);
-    k_raycast_band<<<grid_for(P), kThreads, 0, m->stream>>>(f, s->depth.p, s->valid.p, s->dirs.p,
-                                                            hv, m->block_keys, m->stamp,
-                                                            m->touched, m->vmask, m->d_ctr);
-    count_launch();
-    delete pm;
-    SVX_CUDA(cudaGetLastError());
-    sync_counters(m);
-    const uint32_t* c = m->h_ctr;
-    if (c[C_ERR_KEY])
-        throw Error(SVX_INVALID_ARGUMENT, "block coordinate outside the device key range [-2^20, 2^20)");
-    if (c[C_BLOCKS] > m->cfg.max_blocks || c[C_ERR_HASH]) capacity_path(m, f, s);
-    ensure_blocks(m, c[C_BLOCKS]);
-
-    {
-        ProfMark pf(m, SVX_K_FOLD);
-        k_fold<<<persistent_grid(m->device), kThreads, 0, m->stream>>>(
-            f, s->depth.p, s->normals.p, s->valid.p, s->dirs.p, hv, tsdf_base(m), m->touched,
-            m->vmask, m->dirty, m->d_ctr);
-        count_launch();
+    if (n <= 0) return;
+    for (int i = 0; i < n; ++i) {
+        reps[i].frame = -1;
+        reps[i].updated_voxels = reps[i].new_blocks = 0;
+        if (!jobs[i].project && !jobs[i].scan->has_normals && cfg.mode == SVX_NON_PROJECTIVE)
+            throw Error(SVX_INVALID_ARGUMENT, "non-projective mode needs a normal image");
     }
-    SVX_CUDA(cudaGetLastError());
-    sync_counters(m);
-    if (c[C_FALLBACK]) {
-        ProfMark pb(m, SVX_K_FALLBACK);
-        uint32_t cap = std::max<uint32_t>(c[C_FALLBACK] * 16u, 1u << 16);
-        for (;;) {
-            m->records.alloc(cap);
-            f.rec_cap = cap;
-            SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_RECORDS, 0, 4, m->stream));
-            k_collect_fb<<<grid_for(P), kThreads, 0, m->stream>>>(f, s->depth.p, s->valid.p,
-                                                                  s->dirs.p, hv, m->vmask,
-                                                                  m->records.p, m->d_ctr);
-            count_launch();
-            sync_counters(m);
-            if (c[C_RECORDS] <= cap) break;
-            cap = c[C_RECORDS];
-        }
-        const uint32_t n = c[C_RECORDS];
-        if (n) {
-            m->records_alt.alloc(n);
-            sort_u64(m, m->records.p, m->records_alt.p, n);
-            k_fold_fb<<<grid_for(n), kThreads, 0, m->stream>>>(f, s->depth.p, s->normals.p,
-                                                               s->valid.p, s->dirs.p, hv,
-                                                               tsdf_base(m), m->records_alt.p, n,
-                                                               m->d_ctr);
-            count_launch();
-            SVX_CUDA(cudaGetLastError());
-            sync_counters(m);
-        }
+    m->outs.alloc(size_t(n));
+    if (m->h_outs_n < size_t(n)) {
+        if (m->h_outs) cudaFreeHost(m->h_outs);
+        SVX_CUDA(cudaMallocHost(&m->h_outs, sizeof(FrameOut) * n));
+        m->h_outs_n = size_t(n);
     }
-    m->prof_acc.frames += 1;
-    m->prof_acc.rays += c[C_RAYS];
-    m->prof_acc.touched_blocks += c[C_TOUCHED];
-    m->prof_acc.new_blocks += c[C_BLOCKS] - f.blocks_before;
-    m->prof_acc.updated_voxels += c[C_UPDATED];
-    m->prof_acc.fallback_voxels += c[C_FALLBACK];
-    rep->updated_voxels = c[C_UPDATED];
-    rep->new_blocks = c[C_BLOCKS] - f.blocks_before;
-    m->n_blocks = c[C_BLOCKS];
+    // per-frame buffers sized for the largest scan of the batch
+    uint64_t pmax = 0, nmax = 0;
+    for (int i = 0; i < n; ++i) {
+        pmax = std::max<uint64_t>(pmax, uint64_t(jobs[i].scan->P));
+        nmax = std::max<uint64_t>(nmax, jobs[i].n);
+        if (jobs[i].project) jobs[i].scan->lexkey.alloc(std::min<uint64_t>(2 * jobs[i].n + 2, 0xFFFFFFF0ull));
+    }
+    if (m->vox_cap < 16 * pmax) {
+        m->vox_cap = uint32_t(std::min<uint64_t>(16 * pmax, 0xFFFFFFF0ull));
+        m->vlist.alloc(m->vox_cap);
+    }
+    // pool headroom for the whole batch (an overflow aborts and resumes below)
+    const uint64_t head = std::max<uint64_t>(65536, 2 * m->max_new_seen * uint64_t(n));
+    ensure_blocks(m, m->n_blocks + head);
+    std::vector<FrameParams> fps(n);
+    std::vector<int> parity(n, 0);
+    std::vector<char> launched(n, 0);
+    int f0 = 0, stage0 = 0;
+    for (;;) {
+        for (int i = f0; i < n; ++i) {
+            const FrameJob& j = jobs[i];
+            const int from = i == f0 ? stage0 : 0;
+            if (!launched[i] || (i > f0)) {
+                if (j.project) {
+                    if (launched[i]) j.scan->parity = parity[i];
+                    parity[i] = j.scan->parity;
+                    launch_project(j.scan, j.pts, j.n, j.stride, j.pose);
+                }
+                fps[i] = make_params(m, j.scan, j.pose, cfg);
+                launched[i] = 1;
+            }
+            launch_stages(m, j.scan, fps[i], from, m->outs.p + i);
+        }
+        SVX_CUDA(cudaMemcpyAsync(m->h_outs, m->outs.p, sizeof(FrameOut) * n,
+                                 cudaMemcpyDeviceToHost, m->stream));
+        sync_counters(m);
+        const uint32_t abort = m->h_ctr[C_ABORT];
+        if (!abort) break;
+        // the first frame of this pass without a report is the one that aborted
+        int fa = f0;
+        while (fa < n && m->h_outs[fa].ok) ++fa;
+        if (fa >= n) fa = n - 1;
+        svx_scan* s = jobs[fa].scan;
+        const uint32_t before = m->h_ctr[C_BLOCKS_BEFORE];
+        if (abort & kAbortKey) {
+            m->n_blocks = std::min<uint64_t>(m->h_ctr[C_BLOCKS], m->cfg.max_blocks);
+            rebuild_hash(m);
+            reset_frame_state(m);
+            throw Error(SVX_INVALID_ARGUMENT,
+                        "block coordinate outside the device key range [-2^20, 2^20)");
+        }
+        if (abort & (kAbortCapacity | kAbortHash)) {
+            for (int i = 0; i < fa; ++i) reps[i].frame = m->tsdf_frames++;
+            m->tsdf_frames++;
+            m->n_blocks = before;
+            capacity_path(m, fps[fa], s, before);
+        }
+        int stage = 4;
+        if (abort & kAbortRecords) {
+            // grow the record buffer and re-run the band kernel of this frame with a
+            // fresh stamp: masks are idempotent (OR), inserted keys are found again
+            ensure_blocks(m, uint64_t(m->h_ctr[C_BLOCKS]) + head);
+            m->rec_cap = std::max<uint32_t>(m->h_ctr[C_RECORDS] + (m->h_ctr[C_RECORDS] >> 1),
+                                            m->rec_cap * 2);
+            m->records.alloc(m->rec_cap);
+            m->bucket.alloc(m->rec_cap);
+            m->terms.alloc(size_t(m->rec_cap) * sizeof(Term));
+            fps[fa].rec_cap = m->rec_cap;
+            k_reset_fb<<<64, kThreads, 0, m->stream>>>(m->touched, m->fbcnt, m->d_ctr);
+            count_launch();
+            fps[fa].frame_serial = ++m->frame_serial;
+            put_ctr(m, C_RECORDS, 0);
+            put_ctr(m, C_TOUCHED, 0);
+            stage = 0;
+        } else if (abort & kAbortPool) {
+            ensure_blocks(m, uint64_t(m->h_ctr[C_BLOCKS]) + head);
+            stage = 1;
+        } else if (abort & kAbortVoxList) {
+            // the compaction re-runs from the (untouched) masks... which it already
+            // cleared: rebuild the list by re-running the band kernel instead
+            m->vox_cap = uint32_t(std::min<uint64_t>(uint64_t(m->h_ctr[C_VOXLIST]) * 2, 0xFFFFFFF0ull));
+            m->vlist.alloc(m->vox_cap);
+            fps[fa].vox_cap = m->vox_cap;
+            k_reset_fb<<<64, kThreads, 0, m->stream>>>(m->touched, m->fbcnt, m->d_ctr);
+            count_launch();
+            fps[fa].frame_serial = ++m->frame_serial;
+            for (int c : {C_RECORDS, C_TOUCHED, C_VOXLIST, C_BUCKET_TOP, C_FB_BLOCKS}) put_ctr(m, c, 0);
+            stage = 0;
+        } else if (abort & kAbortBigBucket) {
+            big_buckets(m, s, fps[fa]);
+            put_ctr(m, C_DONE, 0);
+            stage = 4;
+        }
+        put_ctr(m, C_ABORT, 0);
+        put_ctr(m, C_MAPPED, uint32_t(m->mapped_blocks));
+        f0 = fa;
+        stage0 = stage;
+    }
+    for (int i = 0; i < n; ++i) {
+        const FrameOut& o = m->h_outs[i];
+        reps[i].frame = m->tsdf_frames++;
+        reps[i].updated_voxels = o.updated;
+        reps[i].new_blocks = o.new_blocks;
+        m->max_new_seen = std::max<uint64_t>(m->max_new_seen, o.new_blocks);
+        jobs[i].scan->dropped = o.dropped;
+        m->prof_acc.frames += 1;
+        m->prof_acc.rays += o.rays;
+        m->prof_acc.touched_blocks += o.touched;
+        m->prof_acc.new_blocks += o.new_blocks;
+        m->prof_acc.updated_voxels += o.updated;
+        m->prof_acc.fallback_voxels += o.fb_voxels;
+    }
+    m->n_blocks = m->h_ctr[C_BLOCKS];
 }
 
 }  // namespace svx
