@@ -686,6 +686,7 @@ svx_status svx_scan_destroy(svx_scan* s) {
         s->pixkey.release();
         s->lexkey.release();
         s->pixcache.release();
+        s->rowdist.release();
         s->tie.release();
         s->pix_of_pt.release();
         s->points.release();

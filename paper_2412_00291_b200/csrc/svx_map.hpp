@@ -89,6 +89,7 @@ struct svx_scan {
     svx::DevBuf<unsigned long long> pixkey;  // 2P: double-buffered (range bits << 32) | point index
     int parity = 0;                           // which pixkey half the next projection uses
     svx::DevBuf<uint8_t> pixcache;           // P x 48 B: ray, range, world normal, flags
+    svx::DevBuf<uint8_t> rowdist;            // P: row distance to the nearest empty pixel
     svx::DevBuf<unsigned long long> lexkey;  // P: tie-break scratch
     svx::DevBuf<uint8_t> tie;     // P: possible exact-range tie
     svx::DevBuf<uint32_t> pix_of_pt;  // per input point: pixel index or kInvalid
@@ -140,7 +141,7 @@ struct svx_map {
     svx::FrameOut* h_outs = nullptr;
     size_t h_outs_n = 0;
     uint64_t mapped_blocks = 0;      // host mirror of C_MAPPED
-    uint64_t max_new_seen = 0;       // largest new-block count of one frame so far
+    double new_ema = 0.0;            // moving average of new blocks per frame
     svx::DevBuf<uint32_t> cand;      // semantic candidate blocks
     svx::DevBuf<uint16_t> lbl;
     svx::DevBuf<float> conf, tensor;

@@ -29,6 +29,7 @@
 //                   report and resets the per-frame counters.
 // Every kernel first checks the abort word: after an abort (pool growth, buffer
 // growth, capacity) the rest of the batch no-ops and the host resumes it.
+#include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <math_constants.h>
 
@@ -47,6 +48,9 @@ struct FrameParams {
     float col[3][3];  // nu * (R^T e_m): sensor-frame step of +1 voxel along world axis m
     double tau, max_range, alpha_eps, nu, inv_nu;
     float min_clamp;
+    // band_all_own(): half voxel diagonal, safe min range, min sin(polar) over the
+    // vertical field of view, pixel pitches
+    float delta, min_range_safe, sin_min, dphi_f, dtheta_f;
     int nonproj, drop_unreliable, has_normals;
     int32_t shard_rank, shard_world;
     uint32_t frame_serial;
@@ -70,7 +74,8 @@ struct Term {  // one (pixel, voxel) measurement of the fallback path
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kWarpSort = 1024;  // max fallback keys per block sorted in one warp
+constexpr int kFbThreads = 512, kFbItems = 8;
+constexpr int kFbMax = kFbThreads * kFbItems;  // fallback keys per block sorted in one CTA
 
 __device__ inline d3 dir_at(const double* __restrict__ dirs, uint32_t p) {
     return mk(__ldg(&dirs[3 * p]), __ldg(&dirs[3 * p + 1]), __ldg(&dirs[3 * p + 2]));
@@ -138,124 +143,287 @@ __device__ inline uint32_t own_pixel(const FrameParams& f, d3 pc) {
     return q == kNeedFp64 ? pixel_fp64(pc, f.m) : q;
 }
 
+// Row distance (columns, azimuth wraps) from each pixel to the nearest pixel of
+// its row without a return, capped at kRmax + 1.
+constexpr int kRmax = 11;
 __global__ void __launch_bounds__(kThreads)
-k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __restrict__ normals,
-               const uint8_t* __restrict__ valid, const double* __restrict__ dirs,
-               PixCache* __restrict__ cache, HashView h, uint64_t* __restrict__ block_keys,
-               uint32_t* __restrict__ stamp, uint32_t* __restrict__ touched,
-               uint32_t* __restrict__ vmask, uint32_t* __restrict__ fbcnt,
-               unsigned long long* __restrict__ rec, uint32_t* __restrict__ ctr) {
+k_row_dist(const float* __restrict__ depth, int W, int H, uint8_t* __restrict__ hd,
+           const uint32_t* __restrict__ ctr) {
     if (ctr[C_ABORT]) return;
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= uint32_t(f.m.W) * uint32_t(f.m.H)) return;
-    const float r = depth[p];
-    const bool in_range = !(r == 0.f || double(r) > f.max_range);
-    const bool have_normal = f.has_normals && valid[p];
-    // pixel cache (measure lambda inputs, tsdf_integrator.cpp:173-186)
-    PixCache pc{};
-    d3 q = mk(0, 0, 0), ray = mk(0, 0, 0);
-    if (in_range) {
-        q = xform(f.pose, scale3(double(r), dir_at(dirs, p)));
-        const d3 dq = sub3(q, f.origin);
-        const double range = sqrt(dot3(dq, dq));
-        ray = div3(dq, range);
-        pc.ray[0] = ray.x;
-        pc.ray[1] = ray.y;
-        pc.ray[2] = ray.z;
-        pc.range = range;
-        if (have_normal) {
-            const d3 n = matvec(f.pose.R, mk(normals[3 * p], normals[3 * p + 1], normals[3 * p + 2]));
-            pc.n[0] = float(n.x);
-            pc.n[1] = float(n.y);
-            pc.n[2] = float(n.z);
-        }
-        pc.flags = ((have_normal || !f.drop_unreliable) ? 1u : 0u) | (have_normal ? 2u : 0u);
+    if (p >= uint32_t(W) * H) return;
+    const int u = int(p % W);
+    const float* row = depth + (p - u);
+    int d = 0;
+    for (; d <= kRmax; ++d) {
+        int a = u + d, b = u - d;
+        a -= a >= W ? W : 0;
+        b += b < 0 ? W : 0;
+        if (row[a] == 0.f || row[b] == 0.f) break;
     }
-    cache[p] = pc;
-    // band ray (tsdf_integrator.cpp:123-131)
-    if (!in_range) return;
-    if (f.drop_unreliable && f.has_normals && !valid[p]) return;
-    warp_agg_inc(&ctr[C_RAYS]);
-    const d3 tr = scale3(f.tau, ray);  // (q - o).normalized() == (q - o) / range
-    const d3 a = sub3(q, tr), b = add3(q, tr);
+    hd[p] = uint8_t(d);
+}
 
-    uint64_t cur_key = kEmptyKey;
-    uint32_t cur_slot = kInvalid;
-    uint32_t pend_word = kInvalid, pend_bits = 0;
-    // own-pixel state: FP32 sensor-frame offset of the current voxel centre
-    int32_t x0 = 0, y0 = 0, z0 = 0;
-    float p0x = 0.f, p0y = 0.f, p0z = 0.f;
-    bool first = true;
-    traverse_segment(a, b, f.nu, f.inv_nu, [&](int32_t x, int32_t y, int32_t z) {
-        const int32_t bx = block_coord(x), by = block_coord(y), bz = block_coord(z);
-        if (!key_in_range(bx) || !key_in_range(by) || !key_in_range(bz)) {
-            atomicOr(&ctr[C_ABORT], kAbortKey);
-            return;
+// Chebyshev distance from pixel p to the nearest pixel without a return or to
+// the top/bottom image edge, capped at kRmax + 1: every pixel closer than that
+// holds a return.
+__device__ inline int valid_radius(const uint8_t* __restrict__ hd, int W, int H, uint32_t p) {
+    const int u = int(p % W), v = int(p / W);
+    int r = kRmax + 1;
+    for (int dy = -kRmax; dy <= kRmax; ++dy) {
+        const int ady = dy < 0 ? -dy : dy;
+        if (ady >= r) continue;
+        const int v2 = v + dy;
+        const int h = (v2 < 0 || v2 >= H) ? 0 : int(hd[uint32_t(v2) * W + u]);
+        r = min(r, max(ady, h));
+    }
+    return r;
+}
+
+// True when no voxel visited by the band of this ray can have its own pixel
+// without a return: the voxel centre lies within delta = sqrt(3)/2 nu of the ray,
+// so its direction is within angle a <= 1.1 delta / d_min of the pixel-centre
+// direction, i.e. within k pixels; every pixel within k of p holds a return.
+__device__ inline bool band_all_own(const FrameParams& f, const uint8_t* __restrict__ hd,
+                                    uint32_t p, float r) {
+    const float dmin = r - float(f.tau) - f.delta;
+    if (!(dmin > f.min_range_safe)) return false;
+    const float x = f.delta / dmin;
+    if (x > 0.3f) return false;
+    const float a = 1.1f * x;  // asin(x) <= 1.1 x for x <= 0.3
+    const float s = f.sin_min - a;
+    if (s < 0.1f || a > s * (1.f / 3.f)) return false;
+    // azimuth offset <= 2 asin(sin(a/2) / s) <= 1.05 a / s for a / s <= 1/3
+    const int ku = int(floorf(1.05f * a / (s * f.dphi_f) + 0.5f)) + 1;
+    const int kv = int(floorf(a / f.dtheta_f + 0.5f)) + 1;
+    const int k = max(ku, kv);
+    if (k > kRmax) return false;
+    return valid_radius(hd, f.m.W, f.m.H, p) > k;
+}
+
+// Per-visit work on global state (no tile staging): the path a visit takes when
+// its tile's shared tables are full. Same effect as the staged path.
+__device__ void visit_global(const FrameParams& f, HashView h, uint64_t* __restrict__ block_keys,
+                             uint32_t* __restrict__ stamp, uint32_t* __restrict__ touched,
+                             uint32_t* __restrict__ vmask, uint32_t* __restrict__ fbcnt,
+                             unsigned long long* __restrict__ rec, uint32_t* __restrict__ ctr,
+                             uint64_t key, int lin, bool fb, uint32_t p);
+
+__device__ inline uint32_t global_slot(const FrameParams& f, HashView h,
+                                       uint64_t* __restrict__ block_keys,
+                                       uint32_t* __restrict__ stamp,
+                                       uint32_t* __restrict__ touched, uint32_t* __restrict__ ctr,
+                                       uint64_t key) {
+    int ins = 0;
+    const uint32_t slot = hash_insert(h, key, &ins);
+    if (slot == kInvalid) {
+        atomicOr(&ctr[C_ABORT], kAbortHash | kAbortCapacity);
+        return kInvalid;
+    }
+    if (ins) {
+        const uint32_t idx = atomicAdd(&ctr[C_BLOCKS], 1u);
+        h.vals[slot] = idx;
+        if (idx < f.max_blocks) block_keys[idx] = key;
+        if (idx >= f.max_blocks) atomicOr(&ctr[C_ABORT], kAbortCapacity);
+        else if (idx >= ctr[C_MAPPED]) atomicOr(&ctr[C_ABORT], kAbortPool);
+    }
+    if (atomicExch(&stamp[slot], f.frame_serial) != f.frame_serial) {
+        const uint32_t t = atomicAdd(&ctr[C_TOUCHED], 1u);
+        touched[t] = slot;
+    }
+    return slot;
+}
+
+__device__ inline void emit_fallback(const FrameParams& f, uint32_t* __restrict__ fbcnt,
+                                     unsigned long long* __restrict__ rec,
+                                     uint32_t* __restrict__ ctr, uint32_t slot, int lin,
+                                     uint32_t p) {
+    atomicAdd(&fbcnt[slot], 1u);
+    const uint32_t pos = atomicAdd(&ctr[C_RECORDS], 1u);
+    if (pos < f.rec_cap)
+        rec[pos] = (static_cast<unsigned long long>(slot) << 32) |
+                   (static_cast<unsigned long long>(lin) << 23) | p;
+    else
+        atomicOr(&ctr[C_ABORT], kAbortRecords);
+}
+
+__device__ void visit_global(const FrameParams& f, HashView h, uint64_t* __restrict__ block_keys,
+                             uint32_t* __restrict__ stamp, uint32_t* __restrict__ touched,
+                             uint32_t* __restrict__ vmask, uint32_t* __restrict__ fbcnt,
+                             unsigned long long* __restrict__ rec, uint32_t* __restrict__ ctr,
+                             uint64_t key, int lin, bool fb, uint32_t p) {
+    const uint32_t slot = global_slot(f, h, block_keys, stamp, touched, ctr, key);
+    if (slot == kInvalid) return;
+    atomicOr(&vmask[uint64_t(slot) * 32 + (lin >> 5)], 1u << (lin & 31));
+    if (fb) emit_fallback(f, fbcnt, rec, ctr, slot, lin, p);
+}
+
+// CTA = 32 x 8 pixel tile. The tile's rays run their DDA into shared memory: a
+// local table of the distinct blocks they visit, the visit records and per-block
+// voxel masks (smem atomics). Global work is then one hash find-or-insert per
+// distinct block (in parallel across threads) and one RED.OR per non-empty mask
+// word, instead of serialized global round trips per ray.
+constexpr int kTileU = 32, kTileV = 8;
+constexpr int kLocalKeys = 256;
+constexpr int kTileFb = 1024;  // staged fallback visits per tile
+
+__global__ void __launch_bounds__(kTileU * kTileV)
+k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __restrict__ normals,
+               const uint8_t* __restrict__ valid, const double* __restrict__ dirs,
+               const uint8_t* __restrict__ hd, PixCache* __restrict__ cache, HashView h,
+               uint64_t* __restrict__ block_keys, uint32_t* __restrict__ stamp,
+               uint32_t* __restrict__ touched, uint32_t* __restrict__ vmask,
+               uint32_t* __restrict__ fbcnt, unsigned long long* __restrict__ rec,
+               uint32_t* __restrict__ ctr) {
+    if (ctr[C_ABORT]) return;
+    __shared__ unsigned long long lkey[kLocalKeys];
+    __shared__ uint32_t lslot[kLocalKeys];
+    __shared__ uint32_t lmask[kLocalKeys][16];
+    __shared__ uint32_t lfb[kTileFb];
+    __shared__ uint32_t nfb;
+    const int tid = threadIdx.x;
+    lkey[tid] = kEmptyKey;
+#pragma unroll
+    for (int w = 0; w < 16; ++w) lmask[tid][w] = 0u;
+    if (tid == 0) nfb = 0;
+    __syncthreads();
+
+    const int tiles_u = (f.m.W + kTileU - 1) / kTileU;
+    const int tu = int(blockIdx.x) % tiles_u, tv = int(blockIdx.x) / tiles_u;
+    const int u = tu * kTileU + (tid % kTileU);
+    const int v = tv * kTileV + (tid / kTileU);
+    const uint32_t tile_p0 = uint32_t(tv * kTileV) * uint32_t(f.m.W) + uint32_t(tu * kTileU);
+    const bool has_pix = u < f.m.W && v < f.m.H;
+    const uint32_t p = has_pix ? uint32_t(v) * uint32_t(f.m.W) + uint32_t(u) : 0u;
+    const float r = has_pix ? depth[p] : 0.f;
+    const bool in_range = has_pix && !(r == 0.f || double(r) > f.max_range);
+    const bool have_normal = has_pix && f.has_normals && valid[p];
+    // pixel cache (measure lambda inputs, tsdf_integrator.cpp:173-186)
+    d3 q = mk(0, 0, 0), ray = mk(0, 0, 0);
+    if (has_pix) {
+        PixCache pc{};
+        if (in_range) {
+            q = xform(f.pose, scale3(double(r), dir_at(dirs, p)));
+            const d3 dq = sub3(q, f.origin);
+            const double range = sqrt(dot3(dq, dq));
+            ray = div3(dq, range);
+            pc.ray[0] = ray.x;
+            pc.ray[1] = ray.y;
+            pc.ray[2] = ray.z;
+            pc.range = range;
+            if (have_normal) {
+                const d3 n = matvec(f.pose.R, mk(normals[3 * p], normals[3 * p + 1], normals[3 * p + 2]));
+                pc.n[0] = float(n.x);
+                pc.n[1] = float(n.y);
+                pc.n[2] = float(n.z);
+            }
+            pc.flags = ((have_normal || !f.drop_unreliable) ? 1u : 0u) | (have_normal ? 2u : 0u);
         }
-        const uint64_t key = pack_key(bx, by, bz);
-        if (key != cur_key) {
-            cur_key = key;
-            if (f.shard_world > 1 && owner_of(key, f.shard_world) != f.shard_rank) {
-                cur_slot = kInvalid;
-            } else {
-                int ins = 0;
-                cur_slot = hash_insert(h, key, &ins);
-                if (cur_slot == kInvalid) {
-                    atomicOr(&ctr[C_ABORT], kAbortHash | kAbortCapacity);
-                } else {
-                    if (ins) {
-                        const uint32_t idx = atomicAdd(&ctr[C_BLOCKS], 1u);
-                        h.vals[cur_slot] = idx;
-                        if (idx < f.max_blocks) block_keys[idx] = key;
-                        if (idx >= f.max_blocks) atomicOr(&ctr[C_ABORT], kAbortCapacity);
-                        else if (idx >= ctr[C_MAPPED]) atomicOr(&ctr[C_ABORT], kAbortPool);
-                    }
-                    if (atomicExch(&stamp[cur_slot], f.frame_serial) != f.frame_serial) {
-                        const uint32_t t = atomicAdd(&ctr[C_TOUCHED], 1u);
-                        touched[t] = cur_slot;
+        cache[p] = pc;
+    }
+    // band ray (tsdf_integrator.cpp:123-131)
+    const bool cast = in_range && !(f.drop_unreliable && f.has_normals && !valid[p]);
+    if (cast) {
+        warp_agg_inc(&ctr[C_RAYS]);
+        const d3 tr = scale3(f.tau, ray);  // (q - o).normalized() == (q - o) / range
+        const d3 a = sub3(q, tr), b = add3(q, tr);
+        uint64_t cur_key = kEmptyKey;
+        int cur_li = -1;
+        bool cur_own = true;
+        int pend_word = -1;
+        uint32_t pend_bits = 0;
+        int32_t x0 = 0, y0 = 0, z0 = 0;
+        float p0x = 0.f, p0y = 0.f, p0z = 0.f;
+        bool first = true;
+        const bool all_own = band_all_own(f, hd, p, r);
+        traverse_segment(a, b, f.nu, f.inv_nu, [&](int32_t x, int32_t y, int32_t z) {
+            const int32_t bx = block_coord(x), by = block_coord(y), bz = block_coord(z);
+            if (!key_in_range(bx) || !key_in_range(by) || !key_in_range(bz)) {
+                atomicOr(&ctr[C_ABORT], kAbortKey);
+                return;
+            }
+            const uint64_t key = pack_key(bx, by, bz);
+            if (key != cur_key) {
+                cur_key = key;
+                cur_own = !(f.shard_world > 1 && owner_of(key, f.shard_world) != f.shard_rank);
+                cur_li = -1;
+                if (cur_own) {  // local table insert (open addressing in smem)
+                    uint32_t s = hash_slot(key, 8);
+                    for (int probe = 0; probe < kLocalKeys; ++probe) {
+                        const unsigned long long old = atomicCAS(&lkey[s], kEmptyKey, key);
+                        if (old == kEmptyKey || old == key) {
+                            cur_li = int(s);
+                            break;
+                        }
+                        s = (s + 1) & (kLocalKeys - 1);
                     }
                 }
             }
-        }
-        if (cur_slot == kInvalid) return;
-        const int lin = local_linear(x, y, z);
-        const uint32_t word = cur_slot * 32u + uint32_t(lin >> 5);
-        const uint32_t bit = 1u << (lin & 31);
-        if (word == pend_word) {
-            pend_bits |= bit;
-        } else {
-            if (pend_word != kInvalid) atomicOr(&vmask[pend_word], pend_bits);
-            pend_word = word;
-            pend_bits = bit;
-        }
-        // own-pixel test of the visited voxel
-        if (first) {
-            const d3 pc0 = xform(f.w2s, voxel_center(x, y, z, f.nu));
-            p0x = float(pc0.x);
-            p0y = float(pc0.y);
-            p0z = float(pc0.z);
-            x0 = x;
-            y0 = y;
-            z0 = z;
-            first = false;
-        }
-        const float kx = float(x - x0), ky = float(y - y0), kz = float(z - z0);
-        const float px = p0x + kx * f.col[0][0] + ky * f.col[1][0] + kz * f.col[2][0];
-        const float py = p0y + kx * f.col[0][1] + ky * f.col[1][1] + kz * f.col[2][1];
-        const float pz = p0z + kx * f.col[0][2] + ky * f.col[1][2] + kz * f.col[2][2];
-        uint32_t own = pixel_fast(px, py, pz, f.m, f.m.r2_lo, f.m.r2_hi);
-        if (own == kNeedFp64) own = pixel_fp64(xform(f.w2s, voxel_center(x, y, z, f.nu)), f.m);
-        if (own == kInvalid || depth[own] == 0.f) {
-            atomicAdd(&fbcnt[cur_slot], 1u);
-            const uint32_t pos = atomicAdd(&ctr[C_RECORDS], 1u);
-            if (pos < f.rec_cap)
-                rec[pos] = (static_cast<unsigned long long>(cur_slot) << 32) |
-                           (static_cast<unsigned long long>(lin) << 23) | p;
-            else
-                atomicOr(&ctr[C_ABORT], kAbortRecords);
-        }
-    });
-    if (pend_word != kInvalid) atomicOr(&vmask[pend_word], pend_bits);
+            if (!cur_own) return;
+            const int lin = local_linear(x, y, z);
+            // own-pixel test of the visited voxel
+            bool fb = false;
+            if (!all_own) {
+                if (first) {
+                    const d3 pc0 = xform(f.w2s, voxel_center(x, y, z, f.nu));
+                    p0x = float(pc0.x);
+                    p0y = float(pc0.y);
+                    p0z = float(pc0.z);
+                    x0 = x;
+                    y0 = y;
+                    z0 = z;
+                    first = false;
+                }
+                const float kx = float(x - x0), ky = float(y - y0), kz = float(z - z0);
+                const float px = p0x + kx * f.col[0][0] + ky * f.col[1][0] + kz * f.col[2][0];
+                const float py = p0y + kx * f.col[0][1] + ky * f.col[1][1] + kz * f.col[2][1];
+                const float pz = p0z + kx * f.col[0][2] + ky * f.col[1][2] + kz * f.col[2][2];
+                uint32_t own = pixel_fast(px, py, pz, f.m, f.m.r2_lo, f.m.r2_hi);
+                if (own == kNeedFp64) own = pixel_fp64(xform(f.w2s, voxel_center(x, y, z, f.nu)), f.m);
+                fb = own == kInvalid || depth[own] == 0.f;
+            }
+            if (cur_li < 0) {  // local table full: straight to global state
+                visit_global(f, h, block_keys, stamp, touched, vmask, fbcnt, rec, ctr, key, lin, fb, p);
+                return;
+            }
+            const int word = cur_li * 16 + (lin >> 5);
+            if (word != pend_word) {
+                if (pend_word >= 0) atomicOr(&lmask[0][0] + pend_word, pend_bits);
+                pend_word = word;
+                pend_bits = 0u;
+            }
+            pend_bits |= 1u << (lin & 31);
+            if (fb) {
+                const uint32_t pos = atomicAdd(&nfb, 1u);
+                if (pos < uint32_t(kTileFb))
+                    lfb[pos] = (uint32_t(cur_li) << 24) | (uint32_t(lin) << 15) | uint32_t(tid);
+                else
+                    visit_global(f, h, block_keys, stamp, touched, vmask, fbcnt, rec, ctr, key, lin,
+                                 true, p);
+            }
+        });
+        if (pend_word >= 0) atomicOr(&lmask[0][0] + pend_word, pend_bits);
+    }
+    __syncthreads();
+    // one global hash operation per distinct block of the tile
+    if (lkey[tid] != kEmptyKey)
+        lslot[tid] = global_slot(f, h, block_keys, stamp, touched, ctr, lkey[tid]);
+    __syncthreads();
+    const uint32_t nf = min(nfb, uint32_t(kTileFb));
+    for (uint32_t i = tid; i < nf; i += kTileU * kTileV) {
+        const uint32_t e = lfb[i];
+        const uint32_t slot = lslot[e >> 24];
+        if (slot == kInvalid) continue;
+        const uint32_t t = e & 255u;
+        emit_fallback(f, fbcnt, rec, ctr, slot, int((e >> 15) & 511u),
+                      tile_p0 + (t / kTileU) * uint32_t(f.m.W) + (t % kTileU));
+    }
+    for (int i = tid; i < kLocalKeys * 16; i += kTileU * kTileV) {
+        const int li = i >> 4, w = i & 15;
+        const uint32_t bits = lmask[li][w];
+        if (bits && lkey[li] != kEmptyKey && lslot[li] != kInvalid)
+            atomicOr(&vmask[uint64_t(lslot[li]) * 32 + w], bits);
+    }
 }
 
 struct Accum {
@@ -265,9 +433,12 @@ struct Accum {
 // nonprojective_distance (tsdf_integrator.cpp:39-46)
 __device__ inline double nonprojective_distance(double psi, double theta, double alpha,
                                                 double eps) {
-    const double ct = cos(theta);
+    double st, ct;
+    sincos(theta, &st, &ct);  // same values as sin()/cos(), one shared range reduction
     if (alpha < eps) return fabs(ct) * psi;
-    const double mag = fabs((cos(alpha) - 1.0) * sin(theta) / sin(alpha)) + fabs(ct * psi);
+    double sa, ca;
+    sincos(alpha, &sa, &ca);
+    const double mag = fabs((ca - 1.0) * st / sa) + fabs(ct * psi);
     return psi >= 0.0 ? mag : -mag;
 }
 
@@ -497,74 +668,69 @@ __device__ inline bool fold_terms(svx_tsdf_voxel* vp, const Term* __restrict__ t
     return true;
 }
 
-__global__ void __launch_bounds__(kThreads)
+// CTA per block with fallback records (the records cluster on few blocks, e.g. on
+// the ring where the lowest beam meets the ground: ~1000 keys per block).
+__global__ void __launch_bounds__(kFbThreads)
 k_fb_fold(FrameParams f, const PixCache* __restrict__ cache, HashView h,
           svx_tsdf_voxel* __restrict__ pool, const uint32_t* __restrict__ fbslots,
           uint32_t* __restrict__ fbcnt, const uint32_t* __restrict__ fbstart,
           const uint32_t* __restrict__ bucket, Term* __restrict__ terms,
           uint32_t* __restrict__ bigslots, FrameOut* __restrict__ out, uint32_t* __restrict__ ctr) {
     if (ctr[C_ABORT]) return;
-    __shared__ uint32_t sk[kThreads / 32][kWarpSort];
+    using Sort = cub::BlockRadixSort<uint32_t, kFbThreads, kFbItems>;
+    __shared__ union {
+        typename Sort::TempStorage sort;
+        uint32_t keys[kFbMax];
+    } sm;
     __shared__ bool last;
-    const int lane = threadIdx.x & 31;
-    uint32_t* keys = sk[threadIdx.x >> 5];
-    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     const uint32_t nb = ctr[C_FB_BLOCKS];
     uint32_t n_upd = 0;
-    for (uint32_t t = warp; t < nb; t += nwarps) {
+    for (uint32_t t = blockIdx.x; t < nb; t += gridDim.x) {
         const uint32_t slot = fbslots[t];
         const uint32_t cnt = fbcnt[slot];
         const uint32_t start = fbstart[slot];
-        if (cnt > kWarpSort) {
-            if (lane == 0) {
+        if (cnt > uint32_t(kFbMax)) {
+            if (threadIdx.x == 0) {
                 bigslots[atomicAdd(&ctr[C_FB_BIG], 1u)] = slot;
                 atomicOr(&ctr[C_ABORT], kAbortBigBucket);
             }
             continue;
         }
-        uint32_t n2 = 32;
-        while (n2 < cnt) n2 <<= 1;
-        for (uint32_t i = lane; i < n2; i += 32) keys[i] = i < cnt ? bucket[start + i] : 0xFFFFFFFFu;
-        __syncwarp();
-        for (uint32_t k = 2; k <= n2; k <<= 1) {  // bitonic sort, ascending
-            for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
-                for (uint32_t i = lane; i < n2; i += 32) {
-                    const uint32_t l = i ^ jj;
-                    if (l > i) {
-                        const uint32_t a = keys[i], b = keys[l];
-                        if ((a > b) == ((i & k) == 0)) {
-                            keys[i] = b;
-                            keys[l] = a;
-                        }
-                    }
-                }
-                __syncwarp();
-            }
+        // sort the bucket: keys = linear << 23 | pixel, ascending
+        uint32_t k[kFbItems];
+#pragma unroll
+        for (int j = 0; j < kFbItems; ++j) {
+            const uint32_t i = threadIdx.x * kFbItems + j;
+            k[j] = i < cnt ? bucket[start + i] : 0xFFFFFFFFu;
         }
+        __syncthreads();  // smem reuse across iterations
+        Sort(sm.sort).Sort(k, 0, 32);
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kFbItems; ++j) sm.keys[threadIdx.x * kFbItems + j] = k[j];
+        __syncthreads();
         const uint64_t key = h.keys[slot];
         svx_tsdf_voxel* blk = pool + uint64_t(h.vals[slot]) * kBlockVoxels;
         Term* tb = terms + start;
         // measurements in parallel (pre-update voxel state, read-only here)
-        for (uint32_t i = lane; i < cnt; i += 32) {
-            const uint32_t kv = keys[i];
+        for (uint32_t i = threadIdx.x; i < cnt; i += kFbThreads) {
+            const uint32_t kv = sm.keys[i];
             const int linear = int(kv >> 23);
             tb[i] = measure_term(f, cache, kv & 0x7FFFFFu, center_of(key, linear, f.nu),
                                  load_voxel(blk + linear));
         }
-        __syncwarp();
-        // per-voxel sums strictly in pixel order, one lane per voxel segment
-        for (uint32_t i = lane; i < cnt; i += 32) {
-            if (i != 0 && (keys[i] >> 23) == (keys[i - 1] >> 23)) continue;
+        __syncthreads();
+        // per-voxel sums strictly in pixel order, one thread per voxel segment
+        for (uint32_t i = threadIdx.x; i < cnt; i += kFbThreads) {
+            if (i != 0 && (sm.keys[i] >> 23) == (sm.keys[i - 1] >> 23)) continue;
             uint32_t end = i + 1;
-            while (end < cnt && (keys[end] >> 23) == (keys[i] >> 23)) ++end;
-            n_upd += fold_terms(blk + (keys[i] >> 23), tb, i, end) ? 1u : 0u;
+            while (end < cnt && (sm.keys[end] >> 23) == (sm.keys[i] >> 23)) ++end;
+            n_upd += fold_terms(blk + (sm.keys[i] >> 23), tb, i, end) ? 1u : 0u;
         }
-        __syncwarp();
-        if (lane == 0) fbcnt[slot] = 0u;
+        if (threadIdx.x == 0) fbcnt[slot] = 0u;
     }
     for (int o = 16; o; o >>= 1) n_upd += __shfl_xor_sync(0xFFFFFFFFu, n_upd, o);
-    if (lane == 0 && n_upd) {
+    if ((threadIdx.x & 31) == 0 && n_upd) {
         atomicAdd(&ctr[C_UPDATED], n_upd);
         atomicAdd(&ctr[C_FB_VOXELS], n_upd);
     }
@@ -678,6 +844,15 @@ FrameParams make_params(svx_map* m, svx_scan* s, const Pose& pose, const svx_int
     f.has_normals = s->has_normals;
     f.nu = nu;
     f.inv_nu = 1.0 / nu;
+    f.delta = float(0.8660254037844386 * nu * (1.0 + 1e-6)) + 1e-6f;
+    f.min_range_safe = float(s->model.min_range * (1.0 + 1e-4)) + 1e-4f;
+    {
+        const double t0 = s->model.theta0, t1 = s->model.theta0 + s->model.height_px * s->model.delta_theta;
+        // polar range inside (0, pi): sin is smallest at an end of the range
+        f.sin_min = (t0 > 0.0 && t1 < kPi) ? float(std::min(std::sin(t0), std::sin(t1)) - 1e-6) : 0.f;
+    }
+    f.dphi_f = float(s->model.delta_phi * (1.0 - 1e-6));
+    f.dtheta_f = float(s->model.delta_theta * (1.0 - 1e-6));
     f.shard_rank = m->shard_rank;
     f.shard_world = m->shard_world;
     f.frame_serial = ++m->frame_serial;
@@ -695,11 +870,15 @@ void launch_stages(svx_map* m, svx_scan* s, const FrameParams& f, int from, Fram
     const unsigned pg = persistent_grid(m->device);
     if (from <= 0) {
         ProfMark pm(m, SVX_K_RAYCAST);
-        k_raycast_band<<<grid_for(P), kThreads, 0, m->stream>>>(
-            f, s->depth.p, s->normals.p, s->valid.p, s->dirs.p,
+        s->rowdist.alloc(P);
+        k_row_dist<<<grid_for(P), kThreads, 0, m->stream>>>(s->depth.p, s->dm.W, s->dm.H,
+                                                            s->rowdist.p, m->d_ctr);
+        const unsigned tiles = unsigned(((s->dm.W + 31) / 32) * ((s->dm.H + 7) / 8));
+        k_raycast_band<<<tiles, 256, 0, m->stream>>>(
+            f, s->depth.p, s->normals.p, s->valid.p, s->dirs.p, s->rowdist.p,
             reinterpret_cast<PixCache*>(s->pixcache.p), hv, m->block_keys, m->stamp, m->touched,
             m->vmask, m->fbcnt, m->records.p, m->d_ctr);
-        count_launch();
+        count_launch(2);
     }
     if (from <= 1) {
         ProfMark pm(m, SVX_K_COMPACT);
@@ -717,7 +896,7 @@ void launch_stages(svx_map* m, svx_scan* s, const FrameParams& f, int from, Fram
     }
     if (from <= 3) {
         ProfMark pm(m, SVX_K_FALLBACK);
-        k_fb_fold<<<pg, kThreads, 0, m->stream>>>(f, cache, hv, tsdf_base(m), m->fbslots, m->fbcnt,
+        k_fb_fold<<<pg / 4, kFbThreads, 0, m->stream>>>(f, cache, hv, tsdf_base(m), m->fbslots, m->fbcnt,
                                                   m->fbstart, m->bucket.p,
                                                   reinterpret_cast<Term*>(m->terms.p), m->bigslots,
                                                   out, m->d_ctr);
@@ -880,7 +1059,9 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
         m->vlist.alloc(m->vox_cap);
     }
     // pool headroom for the whole batch (an overflow aborts and resumes below)
-    const uint64_t head = std::max<uint64_t>(65536, 2 * m->max_new_seen * uint64_t(n));
+    // (an exhausted headroom costs one abort + resume; over-mapping costs physical
+    // memory and cuMemCreate time, so size it from the recent new-block rate)
+    const uint64_t head = std::max<uint64_t>(32768, uint64_t(2.0 * m->new_ema * n));
     ensure_blocks(m, m->n_blocks + head);
     std::vector<FrameParams> fps(n);
     std::vector<int> parity(n, 0);
@@ -971,7 +1152,8 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
         reps[i].frame = m->tsdf_frames++;
         reps[i].updated_voxels = o.updated;
         reps[i].new_blocks = o.new_blocks;
-        m->max_new_seen = std::max<uint64_t>(m->max_new_seen, o.new_blocks);
+        m->new_ema = m->new_ema == 0.0 ? double(o.new_blocks)
+                                       : 0.9 * m->new_ema + 0.1 * double(o.new_blocks);
         jobs[i].scan->dropped = o.dropped;
         m->prof_acc.frames += 1;
         m->prof_acc.rays += o.rays;

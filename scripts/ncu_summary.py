@@ -1,0 +1,44 @@
+"""Summarise an ncu report: per-kernel duration, throughput, occupancy, pipes, stalls, DRAM bytes."""
+import csv
+import subprocess
+import sys
+
+rep = sys.argv[1]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(raw.splitlines()))
+hdr, units = rows[0], rows[1]
+want = {
+    "gpu__time_duration.sum": "dur",
+    "dram__bytes_read.sum": "dram_rd",
+    "dram__bytes_write.sum": "dram_wr",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm%",
+    "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed": "mem%",
+    "sm__warps_active.avg.pct_of_peak_sustained_active": "occ%",
+    "smsp__inst_executed.sum": "inst",
+    "launch__registers_per_thread": "regs",
+    "lts__t_sector_hit_rate.pct": "l2hit%",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active": "fp64%",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active": "xu%",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active": "fma%",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active": "alu%",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active": "lsu%",
+    "smsp__thread_inst_executed_per_inst_executed.ratio": "thr/warp",
+}
+stall = "smsp__average_warp_latency_issue_stalled_"
+for r in rows[2:]:
+    d = dict(zip(hdr, r))
+    name = d["Kernel Name"].split("(")[0].split("::")[-1]
+    out = []
+    for k, lab in want.items():
+        if k in d:
+            out.append(f"{lab}={d[k]}{units[hdr.index(k)]}")
+    st = []
+    for h, v in d.items():
+        if h.startswith(stall) and h.endswith(".ratio"):
+            try:
+                st.append((float(v), h[len(stall):-len(".ratio")]))
+            except ValueError:
+                pass
+    st.sort(reverse=True)
+    print(f"== {name}: " + " ".join(out))
+    print("   stalls(top): " + ", ".join(f"{n}={v:.1f}" for v, n in st[:6]))
