@@ -57,53 +57,46 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms (recipe's clocks line)."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks + throttle reasons via NVML, sampled between timed steps.
 
-    def __init__(self, index: int):
-        self.index = index
-        self.lines: list[str] = []
-        self.proc = None
+    (A background `nvidia-smi -lms 200` stalls the launch stream for milliseconds
+    per poll on these hosts, so sampling is done in-process at step boundaries:
+    inside the overall timed region, outside each step's CUDA-event bracket.)"""
 
-    def start(self):
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap"}
+
+    def __init__(self, torch_device):
+        self.sm, self.mx, self.reasons = [], None, set()
+        self.h = None
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            threading.Thread(target=self._read, daemon=True).start()
-        except Exception:
-            self.proc = None
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            pr = torch.cuda.get_device_properties(torch_device)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        except Exception as e:  # noqa: BLE001
+            self.err = repr(e)
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def sample(self):
+        if self.h is None:
+            return
+        try:
+            self.sm.append(float(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)))
+            bits = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for b, n in self.REASONS.items():
+                if bits & b:
+                    self.reasons.add(n)
+        except Exception:  # noqa: BLE001
+            pass
 
-    def stop(self) -> dict:
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
-            except ValueError:
-                continue
-            for n, v in zip(names, f[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+    def result(self) -> dict:
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.mx,
+                "reasons": sorted(self.reasons), "samples": len(self.sm),
+                "method": "NVML at step boundaries inside the timed region"}
 
 
 def dist_env():
@@ -275,12 +268,18 @@ def main():
         ext = torch.cuda.ExternalStream(store.stream_ptr(), device=dev)
         step_ms, pts_t, upd_t = [], 0, 0
         launches0 = None
+        warm_prof = None
         for s in range(args.warmup + args.steps):
+            if s == 0:
+                store.profile_enable(True)  # all kernel groups during warm-up
             if s == args.warmup:
-                store.profile_enable(True)
+                # time only the dominant group inside the timed region (2 events/frame)
+                warm_prof = store.profile_read().as_dict()
+                dom = max(warm_prof["ms"], key=warm_prof["ms"].get) if warm_prof["ms"] else "fold"
+                store.profile_enable(1 << svx.K_NAMES.index(dom))
                 launches0 = svx.kernel_launches()
                 if clocks:
-                    clocks.start()
+                    clocks.sample()
             f0, f1 = s * spp, (s + 1) * spp
             if world > 1:
                 dist.barrier()
@@ -315,6 +314,8 @@ def main():
             e1.record(ext)
             e1.synchronize()
             ms = e0.elapsed_time(e1)
+            if clocks and s >= args.warmup:
+                clocks.sample()
             if world > 1:
                 t = torch.tensor([ms, float(upd)], dtype=torch.float64, device=dev)
                 tm = t.clone()
@@ -327,13 +328,13 @@ def main():
                 upd_t += upd
         launches = svx.kernel_launches() - launches0
         prof = store.profile_read()
-        return step_ms, pts_t, upd_t, launches, prof
+        return step_ms, pts_t, upd_t, launches, prof, warm_prof
 
     # ---- leg 1: device-resident scans
     store = make_store()
-    clocks = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
-    step_ms, pts_t, upd_t, launches, prof = run_leg(store, clocks=clocks)
-    clk = clocks.stop() if clocks else None
+    clocks = ClockSampler(dev) if rank == 0 else None
+    step_ms, pts_t, upd_t, launches, prof, warm_prof = run_leg(store, clocks=clocks)
+    clk = clocks.result() if clocks else None
     total_s = sum(step_ms) / 1e3
     value = pts_t / total_s
     pd = prof.as_dict()
@@ -342,17 +343,20 @@ def main():
 
     # ---- roofline: algorithmic bytes per kernel group
     peak, peak_src = peaks()
+    # compulsory traffic per kernel group (per-scan intermediates excluded, L2-resident)
     alg = {
-        "project": 12.0 * prof.points,
-        "raycast": 16.0 * prof.touched_blocks,
-        "fold": 40.0 * prof.updated_voxels + 10240.0 * prof.new_blocks,
+        "project": 12.0 * prof.points,                   # f32 xyz in
+        "raycast": 16.0 * prof.touched_blocks,           # hash key + value + touched list
+        "compact": 10240.0 * prof.new_blocks,            # zero-fill of new blocks
+        "fold": 40.0 * prof.updated_voxels,              # voxel read + write (20 B each)
+        "fallback": 0.0,                                 # counted in fold's updated voxels
     }
     ms_k = {k: v for k, v in pd["ms"].items()}
     dom = max(ms_k, key=ms_k.get) if ms_k else "fold"
     dom_ms = ms_k.get(dom, 0.0)
     dom_launches = pd["launches"].get(dom, 1)
     achieved = (alg.get(dom, 0.0) / (dom_ms / 1e3) / 1e9) if dom_ms else 0.0
-    B_total = alg["project"] + alg["raycast"] + alg["fold"]
+    B_total = sum(alg.values())
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": None, "kernel": dom,
                 "kernel_ms_per_launch": dom_ms / max(dom_launches, 1),
@@ -361,7 +365,10 @@ def main():
                 "pipeline": {"alg_bytes_per_frame": B_total / max(prof.frames, 1),
                              "achieved": B_total / total_s / 1e9,
                              "frac": B_total / total_s / 1e9 / peak},
-                "kernel_ms": ms_k}
+                "timed_kernel_ms": ms_k,
+                "warmup_kernel_us_per_frame": {
+                    k: 1e3 * v / max(warm_prof["frames"], 1) for k, v in warm_prof["ms"].items()}
+                if warm_prof else None}
 
     # ---- leg 2: end to end through the C-ABI with host buffers
     e2e = None
@@ -370,7 +377,7 @@ def main():
         if rank == 0:
             host_pts = pts_all.cpu().pin_memory()
         store = make_store()
-        s2, p2, u2, _, prof2 = run_leg(store, host_pts=host_pts if rank == 0 else torch.empty(0))
+        s2, p2, u2, _, prof2, _ = run_leg(store, host_pts=host_pts if rank == 0 else torch.empty(0))
         store.close()
         e2e = {"value": p2 / (sum(s2) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(12 * p2 / args.steps),

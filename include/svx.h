@@ -244,6 +244,9 @@ typedef struct {
     uint64_t touched_blocks, new_blocks, updated_voxels, fallback_voxels;
     uint64_t sem_images, sem_candidates, sem_updated, sem_new_layers;
 } svx_profile;
+/* on: 0 off, 1 all kernel groups, otherwise a bitmask (1 << SVX_K_*) of the groups
+ * to time (each timed group costs two event records per launch). Counters are
+ * always accumulated while profiling is on. */
 svx_status svx_profile_enable(svx_map* map, int32_t on);
 svx_status svx_profile_read(svx_map* map, svx_profile* out);
 

@@ -426,6 +426,7 @@ svx_status svx_profile_enable(svx_map* m, int32_t on) {
         SVX_CUDA(cudaStreamSynchronize(m->stream));
         prof_resolve(m);
         m->prof = on != 0;
+        m->prof_mask = on == 1 ? 0xFFFFFFFFu : uint32_t(on);
         m->prof_acc = svx_profile{};
     });
 }
@@ -658,6 +659,7 @@ svx_status svx_scan_create(svx_map* m, const svx_lidar_model* model, svx_scan** 
             s->pixkey.alloc(2 * P);
             s->lexkey.alloc(3 * P);
             s->pixcache.alloc(48 * P);
+            s->rowdist.alloc(P);
             SVX_CUDA(cudaMemset(s->pixkey.p, 0xFF, 16 * P));
             SVX_CUDA(cudaMemset(s->pixcache.p, 0, 48 * P));
             SVX_CUDA(cudaMemset(s->depth.p, 0, 4 * P));
@@ -738,6 +740,7 @@ svx_status svx_scan_upload(svx_scan* s, const float* depth, const float* height,
         SVX_CUDA(cudaMemcpy(s->depth.p, depth, 4 * P, cudaMemcpyHostToDevice));
         if (height) SVX_CUDA(cudaMemcpy(s->height.p, height, 4 * P, cudaMemcpyHostToDevice));
         s->has_normals = normals != nullptr;
+        s->rowdist_fresh = false;
         if (normals) {
             require(valid != nullptr, SVX_INVALID_ARGUMENT, "normal_valid required with normals");
             SVX_CUDA(cudaMemcpy(s->normals.p, normals, 12 * P, cudaMemcpyHostToDevice));

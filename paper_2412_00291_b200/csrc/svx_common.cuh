@@ -127,6 +127,7 @@ __device__ inline float fast_atan2f(float y, float x) {
 }
 
 constexpr uint32_t kNeedFp64 = 0xFFFFFFFEu;
+constexpr int kRowDistMax = 11;  // cap of the row-distance map (valid-radius skip)
 
 // Pixel of a sensor-frame vector p given in FP32 with |error| <= ~2e-6 |p|.
 // Returns the pixel index, kInvalid (no pixel), or kNeedFp64 when the FP32

@@ -90,6 +90,7 @@ struct svx_scan {
     int parity = 0;                           // which pixkey half the next projection uses
     svx::DevBuf<uint8_t> pixcache;           // P x 48 B: ray, range, world normal, flags
     svx::DevBuf<uint8_t> rowdist;            // P: row distance to the nearest empty pixel
+    bool rowdist_fresh = false;              // rowdist matches depth (set by projection)
     svx::DevBuf<unsigned long long> lexkey;  // P: tie-break scratch
     svx::DevBuf<uint8_t> tie;     // P: possible exact-range tie
     svx::DevBuf<uint32_t> pix_of_pt;  // per input point: pixel index or kInvalid
@@ -156,6 +157,7 @@ struct svx_map {
     // profiling: event pairs recorded around kernel groups on `stream`,
     // resolved at the next host synchronisation point
     bool prof = false;
+    uint32_t prof_mask = 0;  // kernel groups (bit = SVX_K_*) timed with events
     svx_profile prof_acc{};
     struct PendingEv {
         int kid;

@@ -106,7 +106,7 @@ k_finish_pixels(const float* __restrict__ pts, int stride, const unsigned long l
                 float* __restrict__ height, float* __restrict__ normals,
                 uint8_t* __restrict__ valid, uint8_t* __restrict__ tie,
                 const unsigned long long* __restrict__ ties, uint32_t tie_cap,
-                const uint32_t* __restrict__ ctr) {
+                uint8_t* __restrict__ rowdist, const uint32_t* __restrict__ ctr) {
     if (ctr[C_ABORT]) return;
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= uint32_t(W) * H) return;
@@ -114,6 +114,18 @@ k_finish_pixels(const float* __restrict__ pts, int stride, const unsigned long l
     next_pixkey[p] = ~0ull;  // the other half is clean for the next projection
     const float d0 = key_depth(k);
     depth[p] = d0;
+    {   // row distance to the nearest pixel without a return (k_row_dist, from the keys)
+        const int u = int(p % W);
+        const unsigned long long* row = pixkey + (p - u);
+        int d = 0;
+        for (; d <= kRowDistMax; ++d) {
+            int a = u + d, b = u - d;
+            a -= a >= W ? W : 0;
+            b += b < 0 ? W : 0;
+            if (row[a] == ~0ull || row[b] == ~0ull) break;
+        }
+        rowdist[p] = uint8_t(d);
+    }
     float h = 0.f;
     if (k != ~0ull) {
         uint32_t win = uint32_t(k);
@@ -186,9 +198,10 @@ void launch_project(svx_scan* s, const float* d_pts, uint64_t n, int stride, con
     }
     k_finish_pixels<<<grid_for(P), kThreads, 0, m->stream>>>(
         d_pts, stride, cur, nxt, s->dirs.p, pose, s->dm.W, s->dm.H, 1, s->depth.p, s->height.p,
-        s->normals.p, s->valid.p, s->tie.p, s->lexkey.p, tie_cap, m->d_ctr);
+        s->normals.p, s->valid.p, s->tie.p, s->lexkey.p, tie_cap, s->rowdist.p, m->d_ctr);
     count_launch();
     SVX_CUDA(cudaGetLastError());
+    s->rowdist_fresh = true;
     s->parity ^= 1;
     s->has_normals = true;
     s->n_points = n;

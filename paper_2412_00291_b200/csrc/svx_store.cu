@@ -157,7 +157,7 @@ cudaEvent_t take_event(svx_map* m) {
 }  // namespace
 
 ProfMark::ProfMark(svx_map* map, int k) : m(map), kid(k) {
-    if (!m->prof) return;
+    if (!m->prof || !((m->prof_mask >> k) & 1u)) return;
     a = take_event(m);
     SVX_CUDA(cudaEventRecord(a, m->stream));
 }

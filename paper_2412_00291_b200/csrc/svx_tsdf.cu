@@ -145,7 +145,7 @@ __device__ inline uint32_t own_pixel(const FrameParams& f, d3 pc) {
 
 // Row distance (columns, azimuth wraps) from each pixel to the nearest pixel of
 // its row without a return, capped at kRmax + 1.
-constexpr int kRmax = 11;
+constexpr int kRmax = kRowDistMax;
 __global__ void __launch_bounds__(kThreads)
 k_row_dist(const float* __restrict__ depth, int W, int H, uint8_t* __restrict__ hd,
            const uint32_t* __restrict__ ctr) {
@@ -870,15 +870,18 @@ void launch_stages(svx_map* m, svx_scan* s, const FrameParams& f, int from, Fram
     const unsigned pg = persistent_grid(m->device);
     if (from <= 0) {
         ProfMark pm(m, SVX_K_RAYCAST);
-        s->rowdist.alloc(P);
-        k_row_dist<<<grid_for(P), kThreads, 0, m->stream>>>(s->depth.p, s->dm.W, s->dm.H,
-                                                            s->rowdist.p, m->d_ctr);
+        if (!s->rowdist_fresh) {  // host-provided depth: the projection did not build it
+            k_row_dist<<<grid_for(P), kThreads, 0, m->stream>>>(s->depth.p, s->dm.W, s->dm.H,
+                                                                s->rowdist.p, m->d_ctr);
+            count_launch();
+            s->rowdist_fresh = true;
+        }
         const unsigned tiles = unsigned(((s->dm.W + 31) / 32) * ((s->dm.H + 7) / 8));
         k_raycast_band<<<tiles, 256, 0, m->stream>>>(
             f, s->depth.p, s->normals.p, s->valid.p, s->dirs.p, s->rowdist.p,
             reinterpret_cast<PixCache*>(s->pixcache.p), hv, m->block_keys, m->stamp, m->touched,
             m->vmask, m->fbcnt, m->records.p, m->d_ctr);
-        count_launch(2);
+        count_launch();
     }
     if (from <= 1) {
         ProfMark pm(m, SVX_K_COMPACT);
