@@ -154,6 +154,13 @@ svx_status svx_block_keys_sorted(svx_map* map, int32_t* out, uint64_t cap, uint6
  * unallocated block. sem may be NULL. */
 svx_status svx_block_read(svx_map* map, const int32_t bxyz[3], svx_tsdf_voxel* tsdf,
                           float* sem, int32_t* has_sem);
+/* Batched svx_block_read for n blocks (bxyz = n*3): tsdf = n*512 voxels, sem (may be
+ * NULL) = n*512*K floats, has_sem[i] = 0 for blocks without a semantic layer (their
+ * sem rows are left untouched). SVX_NOT_FOUND if any block is unallocated. Used by
+ * host mirrors that materialise many blocks at once (VoxelStore::for_each_block,
+ * voxel_store.hpp:82-91). */
+svx_status svx_blocks_read(svx_map* map, const int32_t* bxyz, uint64_t n, svx_tsdf_voxel* tsdf,
+                           float* sem, uint8_t* has_sem);
 /* Write-back of a host-mirrored block. has_sem=1 allocates the semantic layer if
  * needed and writes sem (VoxelBlock::ensure_semantics + direct mutation). */
 svx_status svx_block_write(svx_map* map, const int32_t bxyz[3], const svx_tsdf_voxel* tsdf,
@@ -190,6 +197,10 @@ svx_status svx_scan_destroy(svx_scan* scan);
  * Validates the pose (PosedCloud::validate_pose, scan_projection.hpp:65-69). */
 svx_status svx_project(svx_scan* scan, const float* points, uint64_t n, int32_t stride,
                        int32_t ptr_is_device, const svx_pose* pose);
+/* project_cloud for FP64 points (PosedCloud holds Eigen::Vector3d,
+ * scan_projection.hpp:60-63): same semantics, n rows of `stride` doubles. */
+svx_status svx_project_f64(svx_scan* scan, const double* points, uint64_t n, int32_t stride,
+                           int32_t ptr_is_device, const svx_pose* pose);
 /* compute_normal_image — scan_projection.cpp:86-109. */
 svx_status svx_compute_normals(svx_scan* scan);
 /* Upload host ScanImages (depth, and optionally normals n*3 + valid) — the

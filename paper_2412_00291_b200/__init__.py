@@ -149,6 +149,7 @@ def _sig(lib: C.CDLL) -> None:
         "svx_block_count": (S, [P, C.POINTER(C.c_uint64)]),
         "svx_block_keys_sorted": (S, [P, P, C.c_uint64, C.POINTER(C.c_uint64)]),
         "svx_block_read": (S, [P, C.POINTER(C.c_int32), P, P, C.POINTER(C.c_int32)]),
+        "svx_blocks_read": (S, [P, P, C.c_uint64, P, P, P]),
         "svx_block_write": (S, [P, C.POINTER(C.c_int32), P, P, C.c_int32]),
         "svx_lookup": (S, [P, P, C.c_uint64, P, P, P]),
         "svx_stats_get": (S, [P, C.POINTER(StatsC)]),
@@ -159,6 +160,7 @@ def _sig(lib: C.CDLL) -> None:
         "svx_scan_create": (S, [P, C.POINTER(LidarModel), C.POINTER(P)]),
         "svx_scan_destroy": (S, [P]),
         "svx_project": (S, [P, P, C.c_uint64, C.c_int32, C.c_int32, C.POINTER(PoseC)]),
+        "svx_project_f64": (S, [P, P, C.c_uint64, C.c_int32, C.c_int32, C.POINTER(PoseC)]),
         "svx_compute_normals": (S, [P]),
         "svx_scan_upload": (S, [P, P, P, P, P]),
         "svx_scan_download": (S, [P, P, P, P, P, C.POINTER(C.c_uint64), C.POINTER(C.c_int32)]),

@@ -113,6 +113,8 @@ void free_map(svx_map* m) {
     m->conf.release();
     m->tensor.release();
     m->like_table.release();
+    m->q_keys.release();
+    m->q_idx.release();
     if (m->stream && m->own_stream) cudaStreamDestroy(m->stream);
     delete m;
 }
@@ -513,6 +515,51 @@ svx_status svx_block_read(svx_map* m, const int32_t b[3], svx_tsdf_voxel* tsdf, 
     });
 }
 
+svx_status svx_blocks_read(svx_map* m, const int32_t* bxyz, uint64_t n, svx_tsdf_voxel* tsdf,
+                           float* sem, uint8_t* has_sem) {
+    return guarded([&] {
+        require(m && (bxyz || !n) && tsdf, SVX_INVALID_ARGUMENT, "null argument");
+        require(!sem || has_sem, SVX_INVALID_ARGUMENT, "has_sem required with sem");
+        require(n < (1ull << 31), SVX_INVALID_ARGUMENT, "too many blocks in one read");
+        if (!n) return;
+        DeviceGuard g(m->device);
+        std::vector<uint64_t> keys(n);
+        for (uint64_t i = 0; i < n; ++i) {
+            const int32_t* b = bxyz + 3 * i;
+            if (!(key_in_range(b[0]) && key_in_range(b[1]) && key_in_range(b[2])))
+                throw Error(SVX_NOT_FOUND, "block not allocated");
+            keys[i] = pack_key(b[0], b[1], b[2]);
+        }
+        std::vector<uint32_t> idx(n);
+        find_blocks(m, keys.data(), uint32_t(n), idx.data());
+        for (uint32_t i : idx)
+            if (i == kInvalid) throw Error(SVX_NOT_FOUND, "block not allocated");
+        const uint64_t nf = uint64_t(kBlockVoxels) * m->cfg.num_labels;
+        DevBuf<uint32_t> di;
+        DevBuf<svx_tsdf_voxel> dt;
+        DevBuf<float> ds;
+        DevBuf<uint8_t> dh;
+        di.alloc(n);
+        dt.alloc(n * kBlockVoxels);
+        if (sem) {
+            ds.alloc(n * nf);
+            dh.alloc(n);
+        }
+        SVX_CUDA(cudaMemcpyAsync(di.p, idx.data(), 4 * n, cudaMemcpyHostToDevice, m->stream));
+        gather_blocks(m, di.p, n, dt.p, sem ? ds.p : nullptr, sem ? dh.p : nullptr);
+        SVX_CUDA(cudaMemcpyAsync(tsdf, dt.p, n * m->block_bytes, cudaMemcpyDeviceToHost, m->stream));
+        if (sem) {
+            SVX_CUDA(cudaMemcpyAsync(has_sem, dh.p, n, cudaMemcpyDeviceToHost, m->stream));
+            SVX_CUDA(cudaMemcpyAsync(sem, ds.p, 4 * n * nf, cudaMemcpyDeviceToHost, m->stream));
+        }
+        SVX_CUDA(cudaStreamSynchronize(m->stream));
+        di.release();
+        dt.release();
+        ds.release();
+        dh.release();
+    });
+}
+
 svx_status svx_block_write(svx_map* m, const int32_t b[3], const svx_tsdf_voxel* tsdf,
                            const float* sem, int32_t has_sem) {
     return guarded([&] {
@@ -689,6 +736,7 @@ svx_status svx_scan_destroy(svx_scan* s) {
         s->lexkey.release();
         s->pixcache.release();
         s->rowdist.release();
+        s->points64.release();
         s->tie.release();
         s->pix_of_pt.release();
         s->points.release();
@@ -714,6 +762,29 @@ svx_status svx_project(svx_scan* s, const float* pts, uint64_t n, int32_t stride
         DeviceGuard g(s->map->device);
         validate_pose(*pose);
         const float* d = stage_points(s, pts, n, stride, is_dev);
+        launch_project(s, d, n, stride, to_pose(*pose));
+        sync_counters(s->map);
+        s->dropped = s->map->h_ctr[C_DROPPED];
+        SVX_CUDA(cudaMemsetAsync(s->map->d_ctr + C_TIES, 0, 4, s->map->stream));
+        SVX_CUDA(cudaMemsetAsync(s->map->d_ctr + C_DROPPED, 0, 4, s->map->stream));
+        SVX_CUDA(cudaStreamSynchronize(s->map->stream));
+    });
+}
+
+svx_status svx_project_f64(svx_scan* s, const double* pts, uint64_t n, int32_t stride,
+                           int32_t is_dev, const svx_pose* pose) {
+    return guarded([&] {
+        DeviceGuard g(s->map->device);
+        validate_pose(*pose);
+        require(stride >= 3, SVX_INVALID_ARGUMENT, "point stride must be >= 3");
+        require(n < (1ull << 32), SVX_INVALID_ARGUMENT, "too many points in one cloud");
+        const double* d = pts;
+        if (!is_dev && n) {
+            s->points64.alloc(n * stride);
+            SVX_CUDA(cudaMemcpyAsync(s->points64.p, pts, 8ull * n * stride, cudaMemcpyHostToDevice,
+                                     s->map->stream));
+            d = s->points64.p;
+        }
         launch_project(s, d, n, stride, to_pose(*pose));
         sync_counters(s->map);
         s->dropped = s->map->h_ctr[C_DROPPED];

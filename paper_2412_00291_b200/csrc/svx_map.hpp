@@ -95,6 +95,7 @@ struct svx_scan {
     svx::DevBuf<uint8_t> tie;     // P: possible exact-range tie
     svx::DevBuf<uint32_t> pix_of_pt;  // per input point: pixel index or kInvalid
     svx::DevBuf<float> points;    // staging for host points
+    svx::DevBuf<double> points64; // staging for host FP64 points
     bool has_normals = false;
     uint64_t dropped = 0;
     uint64_t n_points = 0;
@@ -143,6 +144,8 @@ struct svx_map {
     size_t h_outs_n = 0;
     uint64_t mapped_blocks = 0;      // host mirror of C_MAPPED
     double new_ema = 0.0;            // moving average of new blocks per frame
+    svx::DevBuf<uint64_t> q_keys;    // scratch of host block queries (find / insert)
+    svx::DevBuf<uint32_t> q_idx;
     svx::DevBuf<uint32_t> cand;      // semantic candidate blocks
     svx::DevBuf<uint16_t> lbl;
     svx::DevBuf<float> conf, tensor;
@@ -197,6 +200,7 @@ void validate_pose(const svx_pose& p);
 
 // kernels' host launchers (svx_project.cu, svx_tsdf.cu, svx_semantic.cu, svx_store.cu)
 void launch_project(svx_scan* s, const float* d_pts, uint64_t n, int stride, const Pose& pose);
+void launch_project(svx_scan* s, const double* d_pts, uint64_t n, int stride, const Pose& pose);
 void launch_normals(svx_scan* s);
 // One TSDF frame of a batch: project (optional) + integrate_frame.
 struct FrameJob {
@@ -220,7 +224,10 @@ void run_integrate_labels(svx_map* m, const svx_label_image& img, const svx_sema
 uint64_t count_observed(svx_map* m);
 void launch_zero_blocks(svx_map* m, uint64_t first, uint64_t count);
 void rebuild_hash(svx_map* m);
-void gather_blocks(svx_map* m, const uint32_t* d_idx, uint64_t n, svx_tsdf_voxel* d_out);
+// Copies pool blocks d_idx[0..n) to d_out (n x 512 voxels); with d_sem, also their
+// semantic layers (n x 512*K, has_sem[i] = 0 when block i has none).
+void gather_blocks(svx_map* m, const uint32_t* d_idx, uint64_t n, svx_tsdf_voxel* d_out,
+                   float* d_sem, uint8_t* d_has_sem);
 void lookup_voxels(svx_map* m, const int32_t* d_v, uint64_t n, svx_tsdf_voxel* d_out,
                    float* d_probs, uint8_t* d_found);
 

@@ -34,20 +34,21 @@ __device__ inline bool lex_less(d3 a, d3 b) {
     return a.z < b.z;
 }
 
+template <typename T>
 __global__ void __launch_bounds__(kThreads)
-k_project_points(const float* __restrict__ pts, uint64_t n, int stride, Model m,
+k_project_points(const T* __restrict__ pts, uint64_t n, int stride, Model m,
                  unsigned long long* __restrict__ pixkey, uint8_t* __restrict__ tie,
                  unsigned long long* __restrict__ ties, uint32_t tie_cap,
                  uint32_t* __restrict__ ctr) {
     if (ctr[C_ABORT]) return;
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const float x = pts[i * stride], y = pts[i * stride + 1], z = pts[i * stride + 2];
+    const double x = pts[i * stride], y = pts[i * stride + 1], z = pts[i * stride + 2];
     const d3 p = mk(x, y, z);
     const double r = sqrt(dot3(p, p));
     uint32_t pix = kInvalid;
     if (isfinite(r) && !(r < m.min_range)) {
-        pix = pixel_fast(x, y, z, m, m.r2_lo, m.r2_hi);  // float inputs: exact geometry
+        pix = pixel_fast(float(x), float(y), float(z), m, m.r2_lo, m.r2_hi);
         if (pix == kNeedFp64) pix = pixel_fp64(p, m);
     }
     if (pix == kInvalid) {
@@ -94,13 +95,15 @@ __device__ inline bool normal_at(const double* __restrict__ dirs, int W, int u, 
     return true;
 }
 
-__device__ inline d3 point_at(const float* __restrict__ pts, int stride, uint32_t i) {
+template <typename T>
+__device__ inline d3 point_at(const T* __restrict__ pts, int stride, uint32_t i) {
     return mk(pts[uint64_t(i) * stride], pts[uint64_t(i) * stride + 1],
               pts[uint64_t(i) * stride + 2]);
 }
 
+template <typename T>
 __global__ void __launch_bounds__(kThreads)
-k_finish_pixels(const float* __restrict__ pts, int stride, const unsigned long long* __restrict__ pixkey,
+k_finish_pixels(const T* __restrict__ pts, int stride, const unsigned long long* __restrict__ pixkey,
                 unsigned long long* __restrict__ next_pixkey, const double* __restrict__ dirs,
                 Pose pose, int W, int H, int with_normals, float* __restrict__ depth,
                 float* __restrict__ height, float* __restrict__ normals,
@@ -181,7 +184,8 @@ inline unsigned grid_for(uint64_t n) { return unsigned((n + kThreads - 1) / kThr
 
 // Gated on the abort word and double-buffered (no memsets), so a batch of
 // frames can be queued without host synchronisation.
-void launch_project(svx_scan* s, const float* d_pts, uint64_t n, int stride, const Pose& pose) {
+template <typename T>
+void launch_project_t(svx_scan* s, const T* d_pts, uint64_t n, int stride, const Pose& pose) {
     svx_map* m = s->map;
     const uint32_t P = uint32_t(s->P);
     unsigned long long* cur = s->pixkey.p + uint64_t(s->parity) * P;
@@ -205,6 +209,13 @@ void launch_project(svx_scan* s, const float* d_pts, uint64_t n, int stride, con
     s->parity ^= 1;
     s->has_normals = true;
     s->n_points = n;
+}
+
+void launch_project(svx_scan* s, const float* d_pts, uint64_t n, int stride, const Pose& pose) {
+    launch_project_t(s, d_pts, n, stride, pose);
+}
+void launch_project(svx_scan* s, const double* d_pts, uint64_t n, int stride, const Pose& pose) {
+    launch_project_t(s, d_pts, n, stride, pose);
 }
 
 void launch_normals(svx_scan* s) {

@@ -262,7 +262,41 @@ __global__ void k_fill_layer(float* __restrict__ layer, uint64_t n, float v) {
         layer[i] = v;
 }
 
+// One CTA per requested block: 16-byte copies of the TSDF body (10240 B) and,
+// when the block has a semantic layer, of its 512*K floats.
+__global__ void k_gather_blocks(const uint4* __restrict__ pool, const float* __restrict__ sem_pool,
+                                const uint32_t* __restrict__ sem_idx,
+                                const uint32_t* __restrict__ idx, uint64_t n, int K,
+                                uint4* __restrict__ out, float* __restrict__ sem_out,
+                                uint8_t* __restrict__ has_sem) {
+    constexpr int kVec = kBlockVoxels * int(sizeof(svx_tsdf_voxel)) / 16;  // 640
+    for (uint64_t b = blockIdx.x; b < n; b += gridDim.x) {
+        const uint32_t i = idx[b];
+        const uint4* src = pool + uint64_t(i) * kVec;
+        uint4* dst = out + b * kVec;
+        for (int t = threadIdx.x; t < kVec; t += blockDim.x) dst[t] = src[t];
+        if (!sem_out) continue;
+        const uint32_t s = sem_idx[i];
+        if (threadIdx.x == 0) has_sem[b] = s != kInvalid;
+        if (s == kInvalid) continue;
+        const uint64_t nf = uint64_t(kBlockVoxels) * K;
+        const float* ss = sem_pool + uint64_t(s) * nf;
+        float* sd = sem_out + b * nf;
+        for (uint64_t t = threadIdx.x; t < nf; t += blockDim.x) sd[t] = ss[t];
+    }
+}
+
 }  // namespace
+
+void gather_blocks(svx_map* m, const uint32_t* d_idx, uint64_t n, svx_tsdf_voxel* d_out,
+                   float* d_sem, uint8_t* d_has_sem) {
+    if (!n) return;
+    k_gather_blocks<<<unsigned(std::min<uint64_t>(n, 148 * 8)), kThreads, 0, m->stream>>>(
+        reinterpret_cast<const uint4*>(tsdf_base(m)), sem_base(m), m->sem_idx, d_idx, n,
+        m->cfg.num_labels, reinterpret_cast<uint4*>(d_out), d_sem, d_has_sem);
+    count_launch();
+    SVX_CUDA(cudaGetLastError());
+}
 
 void rebuild_hash(svx_map* m) {
     SVX_CUDA(cudaMemsetAsync(m->keys, 0xFF, sizeof(uint64_t) * m->cap, m->stream));
@@ -297,17 +331,14 @@ uint64_t count_observed(svx_map* m) {
 
 // Pool indices of the given packed keys (kInvalid when absent).
 void find_blocks(svx_map* m, const uint64_t* h_keys, uint32_t n, uint32_t* h_idx) {
-    DevBuf<uint64_t> dk;
-    DevBuf<uint32_t> di;
-    dk.alloc(n);
-    di.alloc(n);
-    SVX_CUDA(cudaMemcpyAsync(dk.p, h_keys, 8ull * n, cudaMemcpyHostToDevice, m->stream));
-    k_find<<<grid_for(n), kThreads, 0, m->stream>>>(hash_view(m), dk.p, n, di.p);
+    if (!n) return;
+    m->q_keys.alloc(std::max<uint32_t>(n, 64));
+    m->q_idx.alloc(std::max<uint32_t>(n, 64));
+    SVX_CUDA(cudaMemcpyAsync(m->q_keys.p, h_keys, 8ull * n, cudaMemcpyHostToDevice, m->stream));
+    k_find<<<grid_for(n), kThreads, 0, m->stream>>>(hash_view(m), m->q_keys.p, n, m->q_idx.p);
     count_launch();
-    SVX_CUDA(cudaMemcpyAsync(h_idx, di.p, 4ull * n, cudaMemcpyDeviceToHost, m->stream));
+    SVX_CUDA(cudaMemcpyAsync(h_idx, m->q_idx.p, 4ull * n, cudaMemcpyDeviceToHost, m->stream));
     SVX_CUDA(cudaStreamSynchronize(m->stream));
-    dk.release();
-    di.release();
 }
 
 // get_or_allocate_block (voxel_store.cpp:9-23). Returns the pool index.
@@ -320,13 +351,11 @@ uint32_t get_or_alloc_block(svx_map* m, uint64_t key, bool* was_new) {
         throw Error(SVX_CAPACITY,
                     "block budget exhausted (max_blocks = " + std::to_string(m->cfg.max_blocks) + ")");
     ensure_blocks(m, m->n_blocks + 1);
-    DevBuf<uint32_t> out;
-    out.alloc(1);
-    k_insert_one<<<1, 1, 0, m->stream>>>(hash_view(m), key, m->block_keys, m->d_ctr, out.p);
+    m->q_idx.alloc(64);
+    k_insert_one<<<1, 1, 0, m->stream>>>(hash_view(m), key, m->block_keys, m->d_ctr, m->q_idx.p);
     count_launch();
-    SVX_CUDA(cudaMemcpyAsync(&idx, out.p, 4, cudaMemcpyDeviceToHost, m->stream));
+    SVX_CUDA(cudaMemcpyAsync(&idx, m->q_idx.p, 4, cudaMemcpyDeviceToHost, m->stream));
     SVX_CUDA(cudaStreamSynchronize(m->stream));
-    out.release();
     if (idx == kInvalid) throw Error(SVX_CAPACITY, "block hash table full");
     launch_zero_blocks(m, idx, 1);
     m->n_blocks = uint64_t(idx) + 1;
