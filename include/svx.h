@@ -3,7 +3,7 @@
  *
  * This is the drop-in boundary: plain C types, plain pointers and sizes, no
  * torch / Eigen / STL in any signature. The C++ mirror of the reference API
- * (paper_2412_00291_b200/cpp/semvox_b200.hpp) and the Python host mirror
+ * (the semvox headers under paper_2412_00291_b200/cpp/include) and the Python host mirror
  * (paper_2412_00291_b200/__init__.py) are thin layers over these entry points.
  * Every function names the reference interface it replaces (paths relative to
  * the reference repo, proj/...).
@@ -254,6 +254,11 @@ typedef struct {
     uint64_t frames, points, rays;  /* TSDF frames, input points, band rays */
     uint64_t touched_blocks, new_blocks, updated_voxels, fallback_voxels;
     uint64_t sem_images, sem_candidates, sem_updated, sem_new_layers;
+    double host_enqueue_ms; /* host time spent issuing the TSDF frame kernels (batched path) */
+    double host_resume_ms;  /* host time spent handling aborts (pool growth, buffer growth) */
+    double host_map_ms;     /* host time spent mapping pool memory (CUDA VMM) */
+    uint64_t aborts[8];     /* batch aborts by reason bit: pool, capacity, key, hash, records,
+                               big bucket, voxel list */
 } svx_profile;
 /* on: 0 off, 1 all kernel groups, otherwise a bitmask (1 << SVX_K_*) of the groups
  * to time (each timed group costs two event records per launch). Counters are

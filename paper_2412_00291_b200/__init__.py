@@ -116,10 +116,14 @@ class ProfileC(C.Structure):
                 ("new_blocks", C.c_uint64), ("updated_voxels", C.c_uint64),
                 ("fallback_voxels", C.c_uint64), ("sem_images", C.c_uint64),
                 ("sem_candidates", C.c_uint64), ("sem_updated", C.c_uint64),
-                ("sem_new_layers", C.c_uint64)]
+                ("sem_new_layers", C.c_uint64), ("host_enqueue_ms", C.c_double),
+                ("host_resume_ms", C.c_double), ("host_map_ms", C.c_double),
+                ("aborts", C.c_uint64 * 8)]
 
     def as_dict(self) -> dict:
-        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("ms", "launches")}
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("ms", "launches", "aborts")}
+        names = ["pool", "capacity", "key", "hash", "records", "big_bucket", "voxel_list", "b7"]
+        d["aborts"] = {names[i]: self.aborts[i] for i in range(8) if self.aborts[i]}
         d["ms"] = {K_NAMES[i]: self.ms[i] for i in range(8) if self.launches[i]}
         d["launches"] = {K_NAMES[i]: self.launches[i] for i in range(8) if self.launches[i]}
         return d

@@ -16,8 +16,11 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
+#include <exception>
 #include <stdexcept>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -36,6 +39,9 @@ void cuda_check(cudaError_t e, const char* what);
 
 // Growable device array with a stable base address (CUDA virtual memory
 // management): reserve once, map physical chunks as the high-water mark grows.
+// Mapping physical memory costs milliseconds per call, so growth can also run
+// ahead of need on a helper thread (prefetch); kernels only ever touch the
+// published mapped() prefix.
 class VmmArray {
 public:
     VmmArray() = default;
@@ -44,15 +50,23 @@ public:
     VmmArray& operator=(const VmmArray&) = delete;
 
     void reserve(int device, size_t max_bytes);
-    // Ensures [0, bytes) is mapped. Never shrinks.
+    // Ensures [0, bytes) is mapped (waits for a pending prefetch). Never shrinks.
     void ensure(size_t bytes);
+    // Starts mapping up to >= bytes in the background (no-op if already mapped or a
+    // growth is in flight). The caller learns about it through mapped().
+    void prefetch(size_t bytes);
     void* base() const { return reinterpret_cast<void*>(base_); }
-    size_t mapped() const { return mapped_; }
+    size_t mapped() const { return mapped_.load(std::memory_order_acquire); }
 
 private:
+    void grow(size_t bytes);  // maps [mapped_, >= bytes); caller holds no worker
+    void join();
     int device_ = 0;
     CUdeviceptr base_ = 0;
-    size_t reserved_ = 0, mapped_ = 0, gran_ = 0;
+    size_t reserved_ = 0, gran_ = 0;
+    std::atomic<size_t> mapped_{0};
+    std::thread worker_;
+    std::exception_ptr worker_err_;
     std::vector<std::pair<CUmemGenericAllocationHandle, size_t>> chunks_;
 };
 
@@ -136,7 +150,7 @@ struct svx_map {
     svx::DevBuf<uint32_t> bucket;    // [rec_cap]
     svx::DevBuf<uint8_t> terms;      // [rec_cap] x 24 B measurement terms
     uint32_t rec_cap = 0;
-    svx::DevBuf<uint32_t> vlist;     // touched voxels of the frame: (touched idx << 9) | linear
+    svx::DevBuf<unsigned long long> vlist;  // touched voxels of the frame: (pool idx << 9) | linear
     uint32_t vox_cap = 0;
     // per-frame results of a batch
     svx::DevBuf<svx::FrameOut> outs;

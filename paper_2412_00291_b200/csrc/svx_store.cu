@@ -6,6 +6,8 @@
 #include <mutex>
 #include <string>
 
+#include <chrono>
+
 #include "svx_map.hpp"
 
 namespace svx {
@@ -77,28 +79,62 @@ void VmmArray::reserve(int device, size_t max_bytes) {
     cu_check(drv().reserve(&base_, reserved_, gran_, 0, 0), "cuMemAddressReserve");
 }
 
-void VmmArray::ensure(size_t bytes) {
-    if (bytes <= mapped_) return;
+void VmmArray::grow(size_t bytes) {
+    const size_t cur = mapped_.load(std::memory_order_relaxed);
+    if (bytes <= cur) return;
     if (bytes > reserved_) throw Error(SVX_CAPACITY, "device pool reservation exceeded");
-    // grow geometrically (>= 1/4 of the mapped size) to keep mapping calls rare
-    size_t want = std::max(bytes, mapped_ + mapped_ / 4);
+    // grow geometrically (>= 1/2 of the mapped size) to keep mapping calls rare
+    size_t want = std::max(bytes, cur + cur / 2);
     want = ((want + gran_ - 1) / gran_) * gran_;
     if (want > reserved_) want = reserved_;
-    const size_t add = want - mapped_;
+    const size_t add = want - cur;
     const CUmemAllocationProp p = prop_for(device_);
     CUmemGenericAllocationHandle h;
     cu_check(drv().create(&h, add, &p, 0), "cuMemCreate");
-    cu_check(drv().map(base_ + mapped_, add, 0, h, 0), "cuMemMap");
+    cu_check(drv().map(base_ + cur, add, 0, h, 0), "cuMemMap");
     CUmemAccessDesc acc{};
     acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     acc.location.id = device_;
     acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-    cu_check(drv().set_access(base_ + mapped_, add, &acc, 1), "cuMemSetAccess");
+    cu_check(drv().set_access(base_ + cur, add, &acc, 1), "cuMemSetAccess");
     chunks_.push_back({h, add});
-    mapped_ = want;
+    mapped_.store(want, std::memory_order_release);
+}
+
+void VmmArray::join() {
+    if (worker_.joinable()) worker_.join();
+    if (worker_err_) {
+        std::exception_ptr e = worker_err_;
+        worker_err_ = nullptr;
+        std::rethrow_exception(e);
+    }
+}
+
+void VmmArray::ensure(size_t bytes) {
+    if (bytes <= mapped()) return;
+    join();
+    grow(bytes);
+}
+
+void VmmArray::prefetch(size_t bytes) {
+    if (bytes > reserved_) bytes = reserved_;
+    if (worker_.joinable()) {
+        if (mapped() >= bytes) join();  // the growth in flight is done: reap it
+        return;
+    }
+    if (bytes <= mapped()) return;
+    worker_ = std::thread([this, bytes] {
+        try {
+            cudaSetDevice(device_);  // primary context current on this thread
+            grow(bytes);
+        } catch (...) {
+            worker_err_ = std::current_exception();
+        }
+    });
 }
 
 VmmArray::~VmmArray() {
+    if (worker_.joinable()) worker_.join();
     if (!base_) return;
     cudaDeviceSynchronize();
     size_t off = 0;
@@ -112,7 +148,14 @@ VmmArray::~VmmArray() {
 
 void ensure_blocks(svx_map* m, uint64_t blocks) {
     if (blocks > m->cfg.max_blocks) blocks = m->cfg.max_blocks;
-    m->tsdf_pool.ensure(blocks * m->block_bytes);
+    if (blocks * m->block_bytes > m->tsdf_pool.mapped()) {
+        const auto t0 = std::chrono::steady_clock::now();
+        m->tsdf_pool.ensure(blocks * m->block_bytes);
+        m->prof_acc.host_map_ms +=
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+    // keep the next growth off the critical path: map ahead in the background
+    m->tsdf_pool.prefetch(std::min<uint64_t>(m->cfg.max_blocks, blocks + blocks / 2) * m->block_bytes);
     const uint64_t mapped = std::min<uint64_t>(m->tsdf_pool.mapped() / m->block_bytes, m->cfg.max_blocks);
     if (mapped != m->mapped_blocks) {
         m->mapped_blocks = mapped;
@@ -134,6 +177,7 @@ void push_block_counters(svx_map* m) {
 void ensure_layers(svx_map* m, uint64_t layers) {
     if (layers > m->cfg.max_blocks) layers = m->cfg.max_blocks;
     m->sem_pool.ensure(layers * m->layer_bytes);
+    m->sem_pool.prefetch(std::min<uint64_t>(m->cfg.max_blocks, layers + layers / 2) * m->layer_bytes);
 }
 
 void sync_counters(svx_map* m) {

@@ -29,7 +29,7 @@
 //                   report and resets the per-frame counters.
 // Every kernel first checks the abort word: after an abort (pool growth, buffer
 // growth, capacity) the rest of the batch no-ops and the host resumes it.
-#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <math_constants.h>
 
@@ -47,6 +47,7 @@ struct FrameParams {
     d3 origin;
     float col[3][3];  // nu * (R^T e_m): sensor-frame step of +1 voxel along world axis m
     double tau, max_range, alpha_eps, nu, inv_nu;
+    double ca_hi, ca_lo;  // cos(alpha_eps) +- 1e-12: margins of the alpha < eps branch
     float min_clamp;
     // band_all_own(): half voxel diagonal, safe min range, min sin(polar) over the
     // vertical field of view, pixel pitches
@@ -74,8 +75,8 @@ struct Term {  // one (pixel, voxel) measurement of the fallback path
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kFbThreads = 512, kFbItems = 8;
-constexpr int kFbMax = kFbThreads * kFbItems;  // fallback keys per block sorted in one CTA
+constexpr int kFbThreads = 256;
+constexpr int kFbMax = 8192;  // fallback records of one block ordered in shared memory
 
 __device__ inline d3 dir_at(const double* __restrict__ dirs, uint32_t p) {
     return mk(__ldg(&dirs[3 * p]), __ldg(&dirs[3 * p + 1]), __ldg(&dirs[3 * p + 2]));
@@ -442,6 +443,52 @@ __device__ inline double nonprojective_distance(double psi, double theta, double
     return psi >= 0.0 ? mag : -mag;
 }
 
+// truncate_distance (tsdf_integrator.hpp:57-59)
+__device__ inline float truncate_f(double d, double tau) {
+    return float(d >= 0.0 ? (tau < d ? tau : d) : (d < -tau ? -tau : d));
+}
+
+// Gamma(d) of the non-projective distance from the clamped cosines ct = cos(theta)
+// and ca = cos(alpha). The reference evaluates theta = acos(ct), alpha = acos(ca)
+// and then cos/sin of both with libm (tsdf_integrator.cpp:39-46,195-196).
+// Fast path without transcendentals: cos(acos(x)) = x and sin(acos(x)) =
+// sqrt((1-x)(1+x)) up to |err| <= 2e-15 (1-ulp libm acos/cos/sin: pi * 2^-52 + 2^-52),
+// an absolute bound E on the resulting d, and the f32 value the reference stores,
+// float(clamp(d, +-tau)), accepted only when all of [d - E, d + E] rounds to it.
+// The branch alpha < eps is decided on ca against cos(eps) with a 1e-12 margin
+// (acos is strictly decreasing). Otherwise (ca near cos(eps), sin(alpha) < 1e-6,
+// or an interval straddling a float boundary: ~1e-4 of the voxels) the reference
+// formula is evaluated with CUDA's FP64 acos/sincos.
+__device__ inline float gamma_nonprojective(const FrameParams& f, double psi, double ct, double ca) {
+    constexpr double kAbs = 2e-15, kRel = 2e-15;
+    bool fast = false;
+    double d = 0.0, e = 0.0;
+    if (ca > f.ca_hi) {  // alpha < eps: |cos theta| * psi
+        d = fabs(ct) * psi;
+        e = fabs(psi) * (kAbs + kRel * fabs(ct)) + 1e-15 * fabs(d);
+        fast = true;
+    } else if (ca < f.ca_lo) {
+        const double st = sqrt((1.0 - ct) * (1.0 + ct));
+        const double sa = sqrt((1.0 - ca) * (1.0 + ca));
+        if (sa > 1e-6) {
+            const double a = ca - 1.0;
+            const double t1 = fabs(a * st / sa), t2 = fabs(ct * psi);
+            const double mag = t1 + t2;
+            d = psi >= 0.0 ? mag : -mag;
+            const double da = kAbs + kRel * fabs(a), dst = kAbs + kRel * st, dsa = kAbs + kRel * sa;
+            e = 1.01 * ((fabs(a) * dst + st * da) / sa + t1 * dsa / sa +
+                        fabs(psi) * (kAbs + kRel * fabs(ct))) +
+                1e-15 * mag;
+            fast = true;
+        }
+    }
+    if (fast) {
+        const float lo = truncate_f(d - e, f.tau), hi = truncate_f(d + e, f.tau);
+        if (lo == hi && __float_as_uint(lo) == __float_as_uint(hi)) return lo;
+    }
+    return truncate_f(nonprojective_distance(psi, acos(ct), acos(ca), f.alpha_eps), f.tau);
+}
+
 // measure lambda (tsdf_integrator.cpp:172-205) for pixel p, from the pixel cache:
 // the contribution (w * Gamma(d), w, w * n) as the reference forms it, in f32.
 __device__ inline Term measure_term(const FrameParams& f, const PixCache* __restrict__ cache,
@@ -455,7 +502,7 @@ __device__ inline Term measure_term(const FrameParams& f, const PixCache* __rest
     const double psi = pc.range - dot3(sub3(center, f.origin), ray);
     if (fabs(psi) > f.tau) return t;
     const float nw[3] = {pc.n[0], pc.n[1], pc.n[2]};
-    double d = psi;
+    float gamma;
     if (f.nonproj && have_normal) {
         float g[3] = {nw[0], nw[1], nw[2]};
         const float gsq = (vox.gradient[0] * vox.gradient[0] + vox.gradient[1] * vox.gradient[1]) +
@@ -472,15 +519,15 @@ __device__ inline Term measure_term(const FrameParams& f, const PixCache* __rest
         ct = ct < -1.0 ? -1.0 : (1.0 < ct ? 1.0 : ct);
         double ca = dot3(gd, mk(nw[0], nw[1], nw[2]));
         ca = ca < -1.0 ? -1.0 : (1.0 < ca ? 1.0 : ca);
-        d = nonprojective_distance(psi, acos(ct), acos(ca), f.alpha_eps);
+        gamma = gamma_nonprojective(f, psi, ct, ca);
+    } else {
+        gamma = truncate_f(psi, f.tau);
     }
     // observation_weight (tsdf_integrator.cpp:48-51)
     double wr = (psi + f.tau) / (2.0 * f.tau);
     const double lo = double(f.min_clamp);
     wr = wr < lo ? lo : (1.0 < wr ? 1.0 : wr);
     const float w_obs = float(wr);
-    // truncate_distance (tsdf_integrator.hpp:57-59)
-    const float gamma = float(d >= 0.0 ? (f.tau < d ? f.tau : d) : (d < -f.tau ? -f.tau : d));
     t.wg = w_obs * gamma;
     t.w = w_obs;
     if (have_normal) {
@@ -542,21 +589,25 @@ __device__ inline void store_voxel(svx_tsdf_voxel* p, const svx_tsdf_voxel& v) {
 __global__ void __launch_bounds__(kThreads)
 k_compact(FrameParams f, HashView h, svx_tsdf_voxel* __restrict__ pool,
           const uint32_t* __restrict__ touched, uint32_t* __restrict__ vmask,
-          uint8_t* __restrict__ dirty, uint32_t* __restrict__ vlist,
+          uint8_t* __restrict__ dirty, unsigned long long* __restrict__ vlist,
           const uint32_t* __restrict__ fbcnt, uint32_t* __restrict__ fbstart,
           uint32_t* __restrict__ fbfill, uint32_t* __restrict__ fbslots,
           uint32_t* __restrict__ ctr) {
     if (ctr[C_ABORT]) return;
-    const int lane = threadIdx.x & 31;
-    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    constexpr int kWarps = kThreads / 32;
+    __shared__ uint32_t wtot[kWarps], wbase[kWarps];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t n_touched = ctr[C_TOUCHED];
     const uint32_t blocks_before = ctr[C_BLOCKS_BEFORE];
-    for (uint32_t t = warp; t < n_touched; t += nwarps) {
-        const uint32_t slot = touched[t];
-        const uint32_t idx = h.vals[slot];
+    // CTA-uniform loop: one list-counter atomic per CTA and iteration (the counter is
+    // a single address; per-warp atomics serialise at L2)
+    for (uint32_t t0 = blockIdx.x * kWarps; t0 < n_touched; t0 += gridDim.x * kWarps) {
+        const uint32_t t = t0 + uint32_t(wid);
+        const bool live = t < n_touched;
+        const uint32_t slot = live ? touched[t] : 0u;
+        const uint32_t idx = live ? h.vals[slot] : 0u;
         uint32_t* mw = vmask + uint64_t(slot) * 32;
-        const uint32_t w = lane < 16 ? mw[lane] : 0u;
+        const uint32_t w = (live && lane < 16) ? mw[lane] : 0u;
         uint32_t incl = __popc(w);
 #pragma unroll
         for (int o = 1; o < 16; o <<= 1) {
@@ -564,14 +615,25 @@ k_compact(FrameParams f, HashView h, svx_tsdf_voxel* __restrict__ pool,
             if (lane >= o) incl += y;
         }
         const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 15);
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(&ctr[C_VOXLIST], total);
-        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        if (lane == 0) wtot[wid] = total;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t s = 0;
+            for (int i = 0; i < kWarps; ++i) {
+                wbase[i] = s;
+                s += wtot[i];
+            }
+            const uint32_t b = s ? atomicAdd(&ctr[C_VOXLIST], s) : 0u;
+            for (int i = 0; i < kWarps; ++i) wbase[i] += b;
+        }
+        __syncthreads();
+        const uint32_t base = wbase[wid];
+        if (!live) continue;
         if (lane < 16) {
             uint32_t pos = base + incl - __popc(w);
             for (uint32_t bits = w; bits; bits &= bits - 1) {
                 const uint32_t linear = uint32_t(lane) * 32u + uint32_t(__ffs(bits) - 1);
-                if (pos < f.vox_cap) vlist[pos] = (t << 9) | linear;
+                if (pos < f.vox_cap) vlist[pos] = (static_cast<unsigned long long>(idx) << 9) | linear;
                 ++pos;
             }
             mw[lane] = 0u;
@@ -594,25 +656,28 @@ k_compact(FrameParams f, HashView h, svx_tsdf_voxel* __restrict__ pool,
     }
 }
 
-// One thread per touched voxel; then the fallback record scatter.
+// One thread per touched voxel; then the fallback record scatter. A list entry
+// holds the pool index and the voxel, so the voxel and its block key load in
+// parallel, and the own pixel's depth and cache entry load together.
 __global__ void __launch_bounds__(kThreads)
 k_fold(FrameParams f, const float* __restrict__ depth, const PixCache* __restrict__ cache,
-       HashView h, svx_tsdf_voxel* __restrict__ pool, const uint32_t* __restrict__ touched,
-       const uint32_t* __restrict__ vlist, const unsigned long long* __restrict__ rec,
+       const uint64_t* __restrict__ block_keys, svx_tsdf_voxel* __restrict__ pool,
+       const unsigned long long* __restrict__ vlist, const unsigned long long* __restrict__ rec,
        uint32_t* __restrict__ fbfill, uint32_t* __restrict__ bucket, uint32_t* __restrict__ ctr) {
     if (ctr[C_ABORT]) return;
     const uint32_t nv = ctr[C_VOXLIST];
     const uint32_t stride = gridDim.x * blockDim.x;
     uint32_t n_upd = 0;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
-        const uint32_t v = vlist[i];
-        const uint32_t slot = touched[v >> 9];
+        const unsigned long long v = vlist[i];
+        const uint64_t idx = v >> 9;
         const int linear = int(v & 511u);
-        const d3 c = center_of(h.keys[slot], linear, f.nu);
+        svx_tsdf_voxel* vp = pool + idx * kBlockVoxels + linear;
+        const uint64_t key = block_keys[idx];
+        svx_tsdf_voxel vox = load_voxel(vp);
+        const d3 c = center_of(key, linear, f.nu);
         const uint32_t own = own_pixel(f, xform(f.w2s, c));
         if (own == kInvalid || depth[own] == 0.f) continue;  // fallback path
-        svx_tsdf_voxel* vp = pool + uint64_t(h.vals[slot]) * kBlockVoxels + linear;
-        svx_tsdf_voxel vox = load_voxel(vp);
         const Term t = measure_term(f, cache, own, c, vox);
         if (t.flags & 1u) {
             Accum acc{0.0, 0.0, 0.0, 0.0, 0.0};
@@ -669,7 +734,11 @@ __device__ inline bool fold_terms(svx_tsdf_voxel* vp, const Term* __restrict__ t
 }
 
 // CTA per block with fallback records (the records cluster on few blocks, e.g. on
-// the ring where the lowest beam meets the ground: ~1000 keys per block).
+// the ring where the lowest beam meets the ground). The bucket is ordered by
+// (voxel, pixel) without a full sort: counting sort by voxel in shared memory
+// (histogram, scan, scatter), then each voxel's short segment is insertion-sorted
+// by pixel by one thread. Terms are measured in parallel and summed per voxel
+// strictly in that order.
 __global__ void __launch_bounds__(kFbThreads)
 k_fb_fold(FrameParams f, const PixCache* __restrict__ cache, HashView h,
           svx_tsdf_voxel* __restrict__ pool, const uint32_t* __restrict__ fbslots,
@@ -677,11 +746,12 @@ k_fb_fold(FrameParams f, const PixCache* __restrict__ cache, HashView h,
           const uint32_t* __restrict__ bucket, Term* __restrict__ terms,
           uint32_t* __restrict__ bigslots, FrameOut* __restrict__ out, uint32_t* __restrict__ ctr) {
     if (ctr[C_ABORT]) return;
-    using Sort = cub::BlockRadixSort<uint32_t, kFbThreads, kFbItems>;
-    __shared__ union {
-        typename Sort::TempStorage sort;
-        uint32_t keys[kFbMax];
-    } sm;
+    using Scan = cub::BlockScan<uint32_t, kFbThreads>;
+    constexpr int kPer = kBlockVoxels / kFbThreads;  // voxels per thread in the scan
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ uint32_t keys[kFbMax];
+    __shared__ uint32_t seg_end[kBlockVoxels];  // per voxel: end of its segment after scatter
+    __shared__ uint32_t seg_cnt[kBlockVoxels];
     __shared__ bool last;
     const uint32_t nb = ctr[C_FB_BLOCKS];
     uint32_t n_upd = 0;
@@ -696,38 +766,54 @@ k_fb_fold(FrameParams f, const PixCache* __restrict__ cache, HashView h,
             }
             continue;
         }
-        // sort the bucket: keys = linear << 23 | pixel, ascending
-        uint32_t k[kFbItems];
-#pragma unroll
-        for (int j = 0; j < kFbItems; ++j) {
-            const uint32_t i = threadIdx.x * kFbItems + j;
-            k[j] = i < cnt ? bucket[start + i] : 0xFFFFFFFFu;
-        }
-        __syncthreads();  // smem reuse across iterations
-        Sort(sm.sort).Sort(k, 0, 32);
+        for (int v = threadIdx.x; v < kBlockVoxels; v += kFbThreads) seg_cnt[v] = 0u;
         __syncthreads();
+        for (uint32_t i = threadIdx.x; i < cnt; i += kFbThreads)
+            atomicAdd(&seg_cnt[bucket[start + i] >> 23], 1u);
+        __syncthreads();
+        {   // exclusive scan of the per-voxel counts -> segment starts
+            uint32_t c[kPer];
 #pragma unroll
-        for (int j = 0; j < kFbItems; ++j) sm.keys[threadIdx.x * kFbItems + j] = k[j];
+            for (int j = 0; j < kPer; ++j) c[j] = seg_cnt[threadIdx.x * kPer + j];
+            Scan(scan_tmp).ExclusiveSum(c, c);
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) seg_end[threadIdx.x * kPer + j] = c[j];
+        }
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < cnt; i += kFbThreads) {
+            const uint32_t k = bucket[start + i];
+            keys[atomicAdd(&seg_end[k >> 23], 1u)] = k;
+        }
+        __syncthreads();
+        // pixel order inside each voxel segment (segments are short)
+        for (int v = threadIdx.x; v < kBlockVoxels; v += kFbThreads) {
+            const uint32_t e = seg_end[v], b = e - seg_cnt[v];
+            for (uint32_t i = b + 1; i < e; ++i) {
+                const uint32_t k = keys[i];
+                uint32_t j = i;
+                for (; j > b && keys[j - 1] > k; --j) keys[j] = keys[j - 1];
+                keys[j] = k;
+            }
+        }
         __syncthreads();
         const uint64_t key = h.keys[slot];
         svx_tsdf_voxel* blk = pool + uint64_t(h.vals[slot]) * kBlockVoxels;
         Term* tb = terms + start;
         // measurements in parallel (pre-update voxel state, read-only here)
         for (uint32_t i = threadIdx.x; i < cnt; i += kFbThreads) {
-            const uint32_t kv = sm.keys[i];
+            const uint32_t kv = keys[i];
             const int linear = int(kv >> 23);
             tb[i] = measure_term(f, cache, kv & 0x7FFFFFu, center_of(key, linear, f.nu),
                                  load_voxel(blk + linear));
         }
         __syncthreads();
-        // per-voxel sums strictly in pixel order, one thread per voxel segment
-        for (uint32_t i = threadIdx.x; i < cnt; i += kFbThreads) {
-            if (i != 0 && (sm.keys[i] >> 23) == (sm.keys[i - 1] >> 23)) continue;
-            uint32_t end = i + 1;
-            while (end < cnt && (sm.keys[end] >> 23) == (sm.keys[i] >> 23)) ++end;
-            n_upd += fold_terms(blk + (sm.keys[i] >> 23), tb, i, end) ? 1u : 0u;
+        // per-voxel sums strictly in pixel order
+        for (int v = threadIdx.x; v < kBlockVoxels; v += kFbThreads) {
+            const uint32_t n = seg_cnt[v];
+            if (n) n_upd += fold_terms(blk + v, tb, seg_end[v] - n, seg_end[v]) ? 1u : 0u;
         }
         if (threadIdx.x == 0) fbcnt[slot] = 0u;
+        __syncthreads();  // shared arrays are reused by the next bucket
     }
     for (int o = 16; o; o >>= 1) n_upd += __shfl_xor_sync(0xFFFFFFFFu, n_upd, o);
     if ((threadIdx.x & 31) == 0 && n_upd) {
@@ -838,6 +924,14 @@ FrameParams make_params(svx_map* m, svx_scan* s, const Pose& pose, const svx_int
     f.tau = cfg.truncation > 0.f ? double(cfg.truncation) : double(m->cfg.truncation);
     f.max_range = cfg.max_range;
     f.alpha_eps = cfg.alpha_epsilon;
+    if (!(cfg.alpha_epsilon > 0.0)) {  // alpha < eps never holds
+        f.ca_hi = f.ca_lo = 2.0;
+    } else if (cfg.alpha_epsilon > kPi) {  // always holds (alpha <= pi)
+        f.ca_hi = f.ca_lo = -2.0;
+    } else {
+        f.ca_hi = std::cos(cfg.alpha_epsilon) + 1e-12;
+        f.ca_lo = std::cos(cfg.alpha_epsilon) - 1e-12;
+    }
     f.min_clamp = cfg.min_weight_clamp;
     f.nonproj = cfg.mode == SVX_NON_PROJECTIVE;
     f.drop_unreliable = cfg.drop_unreliable != 0;
@@ -892,14 +986,14 @@ void launch_stages(svx_map* m, svx_scan* s, const FrameParams& f, int from, Fram
     }
     if (from <= 2) {
         ProfMark pm(m, SVX_K_FOLD);
-        k_fold<<<pg, kThreads, 0, m->stream>>>(f, s->depth.p, cache, hv, tsdf_base(m), m->touched,
+        k_fold<<<pg, kThreads, 0, m->stream>>>(f, s->depth.p, cache, m->block_keys, tsdf_base(m),
                                                m->vlist.p, m->records.p, m->fbfill, m->bucket.p,
                                                m->d_ctr);
         count_launch();
     }
     if (from <= 3) {
         ProfMark pm(m, SVX_K_FALLBACK);
-        k_fb_fold<<<pg / 4, kFbThreads, 0, m->stream>>>(f, cache, hv, tsdf_base(m), m->fbslots, m->fbcnt,
+        k_fb_fold<<<pg / 2, kFbThreads, 0, m->stream>>>(f, cache, hv, tsdf_base(m), m->fbslots, m->fbcnt,
                                                   m->fbstart, m->bucket.p,
                                                   reinterpret_cast<Term*>(m->terms.p), m->bigslots,
                                                   out, m->d_ctr);
@@ -1071,6 +1165,7 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
     std::vector<char> launched(n, 0);
     int f0 = 0, stage0 = 0;
     for (;;) {
+        const auto te0 = std::chrono::steady_clock::now();
         for (int i = f0; i < n; ++i) {
             const FrameJob& j = jobs[i];
             const int from = i == f0 ? stage0 : 0;
@@ -1085,11 +1180,16 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
             }
             launch_stages(m, j.scan, fps[i], from, m->outs.p + i);
         }
+        if (m->prof)
+            m->prof_acc.host_enqueue_ms +=
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - te0).count();
         SVX_CUDA(cudaMemcpyAsync(m->h_outs, m->outs.p, sizeof(FrameOut) * n,
                                  cudaMemcpyDeviceToHost, m->stream));
         sync_counters(m);
         const uint32_t abort = m->h_ctr[C_ABORT];
         if (!abort) break;
+        const auto tr0 = std::chrono::steady_clock::now();
+        for (int b = 0; b < 8; ++b) m->prof_acc.aborts[b] += (abort >> b) & 1u;
         // the first frame of this pass without a report is the one that aborted
         int fa = f0;
         while (fa < n && m->h_outs[fa].ok) ++fa;
@@ -1149,6 +1249,8 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
         put_ctr(m, C_MAPPED, uint32_t(m->mapped_blocks));
         f0 = fa;
         stage0 = stage;
+        m->prof_acc.host_resume_ms +=
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tr0).count();
     }
     for (int i = 0; i < n; ++i) {
         const FrameOut& o = m->h_outs[i];

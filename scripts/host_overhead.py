@@ -24,7 +24,7 @@ icfg = svx.IntegratorConfig()
 s = svx.VoxelStore(cfg, 0)
 ext = torch.cuda.ExternalStream(s.stream_ptr())
 f = 0
-for prof in (False, True) * 5:
+for prof in (True,) * 10:
     s.profile_enable(prof)
     for batch in (100,):
         a, b = f, f + batch
@@ -41,5 +41,6 @@ for prof in (False, True) * 5:
         ksum = sum(p["ms"].values())
         print(f"prof={prof} frames {a}-{b}: call {1e6 * (t1 - t0) / batch:.1f} us/frame, events "
               f"{1e3 * e0.elapsed_time(e1) / batch:.1f} us/frame, kernel groups {1e3 * ksum / batch:.1f}"
-              f" us/frame, blocks {s.block_count()}")
+              f" us/frame, host enqueue {1e3 * p.get('host_enqueue_ms', 0) / batch:.1f} us/frame,"
+              f" blocks {s.block_count()} aborts {p.get('aborts')} resume {p.get('host_resume_ms', 0):.1f} ms map {p.get('host_map_ms', 0):.1f} ms")
         f = b

@@ -24,7 +24,7 @@ want = {
     "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active": "lsu%",
     "smsp__thread_inst_executed_per_inst_executed.ratio": "thr/warp",
 }
-stall = "smsp__average_warp_latency_issue_stalled_"
+stall = "smsp__average_warps_issue_stalled_"
 for r in rows[2:]:
     d = dict(zip(hdr, r))
     name = d["Kernel Name"].split("(")[0].split("::")[-1]
@@ -34,9 +34,9 @@ for r in rows[2:]:
             out.append(f"{lab}={d[k]}{units[hdr.index(k)]}")
     st = []
     for h, v in d.items():
-        if h.startswith(stall) and h.endswith(".ratio"):
+        if h.startswith(stall) and h.endswith("_per_issue_active.ratio"):
             try:
-                st.append((float(v), h[len(stall):-len(".ratio")]))
+                st.append((float(v), h[len(stall):-len("_per_issue_active.ratio")]))
             except ValueError:
                 pass
     st.sort(reverse=True)
