@@ -346,8 +346,9 @@ def main():
     # compulsory traffic per kernel group (per-scan intermediates excluded, L2-resident)
     alg = {
         "project": 12.0 * prof.points,                   # f32 xyz in
-        "raycast": 16.0 * prof.touched_blocks,           # hash key + value + touched list
-        "compact": 10240.0 * prof.new_blocks,            # zero-fill of new blocks
+        # hash key + value + touched list per touched block, zero-fill of new blocks,
+        # touched-voxel list entry (8 B) per updated voxel
+        "raycast": 16.0 * prof.touched_blocks + 10240.0 * prof.new_blocks + 8.0 * prof.updated_voxels,
         "fold": 40.0 * prof.updated_voxels,              # voxel read + write (20 B each)
         "fallback": 0.0,                                 # counted in fold's updated voxels
     }

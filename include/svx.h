@@ -245,7 +245,7 @@ enum {
     SVX_K_FALLBACK = 3,  /* fallback collect + sort + fold             */
     SVX_K_SEM_CULL = 4,  /* semantic frustum cull                      */
     SVX_K_SEM_UPDATE = 5,/* semantic Bayes update (K6)                 */
-    SVX_K_COMPACT = 6,   /* touched-voxel compaction + new-block fill  */
+    SVX_K_COMPACT = 6,   /* reserved (the compaction is part of K3 now) */
     SVX_K_COUNT = 8
 };
 typedef struct {

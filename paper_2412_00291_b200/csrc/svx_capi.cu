@@ -95,13 +95,12 @@ void free_map(svx_map* m) {
     for (void* p : {(void*)m->keys, (void*)m->vals, (void*)m->block_keys, (void*)m->sem_idx,
                     (void*)m->dirty, (void*)m->stamp, (void*)m->touched, (void*)m->vmask,
                     (void*)m->d_ctr, (void*)m->fbcnt, (void*)m->fbstart, (void*)m->fbfill,
-                    (void*)m->fbslots, (void*)m->bigslots})
+                    (void*)m->fbslots, (void*)m->bigslots, (void*)m->fbclaim})
         if (p) cudaFree(p);
     if (m->h_ctr) cudaFreeHost(m->h_ctr);
     if (m->h_outs) cudaFreeHost(m->h_outs);
     m->outs.release();
     m->bucket.release();
-    m->terms.release();
     m->vlist.release();
     prof_resolve(m);
     for (cudaEvent_t e : m->prof_free) cudaEventDestroy(e);
@@ -139,7 +138,7 @@ svx_map* create_map(const svx_map_cfg& cfg, int device) {
         m->keys = dmalloc<uint64_t>(m->cap);
         m->vals = dmalloc<uint32_t>(m->cap);
         m->stamp = dmalloc<uint32_t>(m->cap);
-        m->touched = dmalloc<uint32_t>(m->cap);
+        m->touched = dmalloc<uint32_t>(2ull * m->cap);
         m->vmask = dmalloc<uint32_t>(32ull * m->cap);
         m->block_keys = dmalloc<uint64_t>(cfg.max_blocks);
         m->sem_idx = dmalloc<uint32_t>(cfg.max_blocks);
@@ -148,18 +147,22 @@ svx_map* create_map(const svx_map_cfg& cfg, int device) {
         m->fbcnt = dmalloc<uint32_t>(m->cap);
         m->fbstart = dmalloc<uint32_t>(m->cap);
         m->fbfill = dmalloc<uint32_t>(m->cap);
+        m->fbclaim = dmalloc<uint32_t>(m->cap);
         m->fbslots = dmalloc<uint32_t>(m->cap);
         m->bigslots = dmalloc<uint32_t>(m->cap);
         m->rec_cap = 1u << 20;
-        m->records.alloc(m->rec_cap);
-        m->bucket.alloc(m->rec_cap);
-        m->terms.alloc(size_t(m->rec_cap) * 24);
+        m->records.alloc(2ull * m->rec_cap);  // 32-byte records: 2 x uint4
+        m->bucket.alloc(2ull * m->rec_cap);
         SVX_CUDA(cudaMallocHost(&m->h_ctr, sizeof(uint32_t) * kNumCounters));
         std::memset(m->h_ctr, 0, sizeof(uint32_t) * kNumCounters);
         SVX_CUDA(cudaMemsetAsync(m->keys, 0xFF, 8ull * m->cap, m->stream));
+        SVX_CUDA(cudaMemsetAsync(m->vals, 0xFF, 4ull * m->cap, m->stream));  // kInvalid: no block yet
         SVX_CUDA(cudaMemsetAsync(m->stamp, 0, 4ull * m->cap, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->vmask, 0, 128ull * m->cap, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->fbcnt, 0, 4ull * m->cap, m->stream));
+        SVX_CUDA(cudaMemsetAsync(m->fbfill, 0, 4ull * m->cap, m->stream));
+        SVX_CUDA(cudaMemsetAsync(m->fbclaim, 0, 4ull * m->cap, m->stream));
+        SVX_CUDA(cudaMemsetAsync(m->fbstart, 0xFF, 4ull * m->cap, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->sem_idx, 0xFF, 4ull * cfg.max_blocks, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->dirty, 0, 2ull * cfg.max_blocks, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->d_ctr, 0, sizeof(uint32_t) * kNumCounters, m->stream));

@@ -251,9 +251,10 @@ enum Counter : int {
     C_FB_BLOCKS = 19,   // blocks holding fallback records this frame
     C_FB_VOXELS = 20,   // voxels folded by the fallback path
     C_FB_BIG = 21,      // blocks whose fallback bucket exceeds the warp sort
-    C_VOXLIST = 22,     // touched voxels listed by k_compact
+    C_VOXLIST = 22,     // touched voxels listed by the band kernel
     C_BUCKET_TOP = 23,  // fallback bucket space handed out this frame
     C_DONE = 24,        // CTAs of k_fb_fold finished (last one writes the report)
+    C_TOUCHED_PREV = 25,  // blocks touched by the previous frame (their mask words get cleared)
     kNumCounters = 32
 };
 
@@ -300,6 +301,67 @@ __device__ inline uint32_t warp_agg_inc(uint32_t* ctr) {
     if (lane == leader) base = atomicAdd(ctr, uint32_t(__popc(active)));
     base = __shfl_sync(active, base, leader);
     return base + __popc(active & ((1u << lane) - 1u));
+}
+
+// CTA-uniform read of the abort word (bits in `mask`): kernels with barriers must
+// not let their threads disagree about it (another CTA may set it meanwhile).
+__device__ inline bool cta_aborted(const uint32_t* ctr, uint32_t mask = 0xFFFFFFFFu) {
+    return __syncthreads_or(threadIdx.x == 0 ? int((ctr[C_ABORT] & mask) != 0) : 0) != 0;
+}
+
+// CTA-wide reservation of n entries per thread in a list whose length lives in
+// *counter: one atomic per CTA (a single global counter serialises per-thread or
+// per-warp atomics at L2). Returns this thread's first position. Every thread of
+// the CTA must call it; s_w is shared scratch of 2 * kWarps words.
+template <int kWarps>
+__device__ inline uint32_t cta_reserve(uint32_t n, uint32_t* counter, uint32_t* s_w) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_w[wid] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t s = 0;
+        for (int i = 0; i < kWarps; ++i) {
+            const uint32_t c = s_w[i];
+            s_w[kWarps + i] = s;
+            s += c;
+        }
+        const uint32_t b = s ? atomicAdd(counter, s) : 0u;
+        for (int i = 0; i < kWarps; ++i) s_w[kWarps + i] += b;
+    }
+    __syncthreads();
+    const uint32_t pos = s_w[kWarps + wid] + incl - n;
+    __syncthreads();  // s_w may be reused after return
+    return pos;
+}
+
+// cta_reserve of one entry for the threads with take set.
+template <int kWarps>
+__device__ inline uint32_t cta_append(bool take, uint32_t* counter, uint32_t* s_w) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, take);
+    const uint32_t rank = __popc(m & ((1u << lane) - 1u));
+    if (lane == 0) s_w[wid] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t s = 0;
+        for (int i = 0; i < kWarps; ++i) {
+            const uint32_t c = s_w[i];
+            s_w[kWarps + i] = s;
+            s += c;
+        }
+        const uint32_t b = s ? atomicAdd(counter, s) : 0u;
+        for (int i = 0; i < kWarps; ++i) s_w[kWarps + i] += b;
+    }
+    __syncthreads();
+    const uint32_t pos = s_w[kWarps + wid] + rank;
+    __syncthreads();  // s_w may be reused after return
+    return pos;
 }
 
 }  // namespace svx

@@ -9,8 +9,9 @@
 //                                      mapped on demand (CUDA VMM) so addresses are stable
 //   sem pool    [layers][512][K] f32   lazily allocated semantic layers (VMM as above)
 //   block_keys[idx], sem_idx[idx], dirty flags[idx]   per pool block
-//   frame scratch: stamp[cap] u32, touched[cap] u32 (slots touched by this frame),
-//                  vmask[cap][32] u32 (16 words touched-voxel bits + 16 words fallback bits)
+//   frame scratch: stamp[cap] u32, touched[2][cap] u32 (slots touched by a frame),
+//                  vmask[cap][2][16] u32 (touched-voxel bits, two halves used by
+//                  alternate frames so each frame's half is cleared by the next one)
 #pragma once
 
 #include <cuda.h>
@@ -136,19 +137,20 @@ struct svx_map {
     uint8_t* dirty = nullptr;        // [2][max_blocks]
     // frame scratch
     uint32_t* stamp = nullptr;
-    uint32_t* touched = nullptr;
+    uint32_t* touched = nullptr;     // [2][cap]: blocks touched by the frame, per mask parity
     uint32_t* vmask = nullptr;       // [cap][32]
-    svx::DevBuf<unsigned long long> records, records_alt;
+    svx::DevBuf<uint4> records;      // fallback records of the frame (32 B each: 2 x uint4)
+    svx::DevBuf<unsigned long long> records_alt;  // capacity path: visited block keys
     svx::DevBuf<uint8_t> sort_tmp;
     // fallback stage (voxels whose own pixel has no return): per-slot record
     // counts / bucket offsets, the frame's record list and the bucketed keys
     uint32_t* fbcnt = nullptr;       // [cap]
     uint32_t* fbstart = nullptr;     // [cap]
     uint32_t* fbfill = nullptr;      // [cap]
+    uint32_t* fbclaim = nullptr;     // [cap] bucket allocation claim flags
     uint32_t* fbslots = nullptr;     // [cap]
     uint32_t* bigslots = nullptr;    // [cap] buckets too large for the warp sort
-    svx::DevBuf<uint32_t> bucket;    // [rec_cap]
-    svx::DevBuf<uint8_t> terms;      // [rec_cap] x 24 B measurement terms
+    svx::DevBuf<uint4> bucket;       // the records grouped by block (32 B each)
     uint32_t rec_cap = 0;
     svx::DevBuf<unsigned long long> vlist;  // touched voxels of the frame: (pool idx << 9) | linear
     uint32_t vox_cap = 0;
@@ -187,7 +189,8 @@ struct svx_map {
 namespace svx {
 
 // Pool growth policy: keep at least `blocks` blocks of TSDF mapped.
-void ensure_blocks(svx_map* m, uint64_t blocks);
+// Maps at least `blocks` blocks now and starts mapping `ahead` more in the background.
+void ensure_blocks(svx_map* m, uint64_t blocks, uint64_t ahead = 65536);
 void ensure_layers(svx_map* m, uint64_t layers);
 // Copies counters to the pinned mirror and synchronises the map stream.
 void sync_counters(svx_map* m);

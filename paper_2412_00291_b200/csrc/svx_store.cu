@@ -83,8 +83,9 @@ void VmmArray::grow(size_t bytes) {
     const size_t cur = mapped_.load(std::memory_order_relaxed);
     if (bytes <= cur) return;
     if (bytes > reserved_) throw Error(SVX_CAPACITY, "device pool reservation exceeded");
-    // grow geometrically (>= 1/2 of the mapped size) to keep mapping calls rare
-    size_t want = std::max(bytes, cur + cur / 2);
+    // grow by >= 1/4 of the mapped size: mapping time is proportional to the size,
+    // and growth normally runs ahead of need on the helper thread (prefetch)
+    size_t want = std::max(bytes, cur + cur / 4);
     want = ((want + gran_ - 1) / gran_) * gran_;
     if (want > reserved_) want = reserved_;
     const size_t add = want - cur;
@@ -146,7 +147,7 @@ VmmArray::~VmmArray() {
     drv().addr_free(base_, reserved_);
 }
 
-void ensure_blocks(svx_map* m, uint64_t blocks) {
+void ensure_blocks(svx_map* m, uint64_t blocks, uint64_t ahead) {
     if (blocks > m->cfg.max_blocks) blocks = m->cfg.max_blocks;
     if (blocks * m->block_bytes > m->tsdf_pool.mapped()) {
         const auto t0 = std::chrono::steady_clock::now();
@@ -155,7 +156,7 @@ void ensure_blocks(svx_map* m, uint64_t blocks) {
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     }
     // keep the next growth off the critical path: map ahead in the background
-    m->tsdf_pool.prefetch(std::min<uint64_t>(m->cfg.max_blocks, blocks + blocks / 2) * m->block_bytes);
+    m->tsdf_pool.prefetch(std::min<uint64_t>(m->cfg.max_blocks, blocks + ahead) * m->block_bytes);
     const uint64_t mapped = std::min<uint64_t>(m->tsdf_pool.mapped() / m->block_bytes, m->cfg.max_blocks);
     if (mapped != m->mapped_blocks) {
         m->mapped_blocks = mapped;
@@ -344,6 +345,7 @@ void gather_blocks(svx_map* m, const uint32_t* d_idx, uint64_t n, svx_tsdf_voxel
 
 void rebuild_hash(svx_map* m) {
     SVX_CUDA(cudaMemsetAsync(m->keys, 0xFF, sizeof(uint64_t) * m->cap, m->stream));
+    SVX_CUDA(cudaMemsetAsync(m->vals, 0xFF, sizeof(uint32_t) * m->cap, m->stream));
     if (m->n_blocks)
         k_rebuild<<<grid_for(m->n_blocks), kThreads, 0, m->stream>>>(hash_view(m), m->block_keys,
                                                                      uint32_t(m->n_blocks));

@@ -1,32 +1,32 @@
 // K3-K5: TsdfIntegrator::integrate_frame on the device (tsdf_integrator.cpp:97-258).
 //
-// Four kernels per frame on the map stream, no host synchronisation (a batch of
+// Three kernels per frame on the map stream, no host synchronisation (a batch of
 // frames is synchronised once at its end):
-//   k_raycast_band  K3+K4. One thread per pixel. Writes the pixel cache (ray, range,
-//                   world normal: the measurement inputs of tsdf_integrator.cpp:178-186,
-//                   computed once per pixel instead of once per (pixel, voxel)).
-//                   Band [q - tau r^, q + tau r^], amortised DDA
-//                   (tsdf_integrator.hpp:93-135). Per block crossing: find-or-insert
-//                   in the open-addressing hash (new block => pool index from a bump
-//                   counter); first touch this frame => slot appended to the touched
-//                   list. Per visit: the voxel bit in the slot's 512-bit mask (RED.OR,
-//                   visits of one 32-voxel word merged in registers) and the own-pixel
-//                   test of the voxel (FP32, sensor-frame offset updated incrementally
-//                   along the DDA, exact decision via error margins): a voxel whose own
-//                   pixel has no return is measured by every visiting ray in the
-//                   reference (.cpp:232-238), so the visit becomes a fallback record.
-//   k_compact       warp per touched block: touched-voxel list (compaction of the mask
-//                   bits), zero-fill of new blocks, mask reset, dirty flag, bucket
-//                   allocation for the block's fallback records.
+//   k_raycast_band  K3+K4. CTA = 32 x 8 pixel tile, one thread per pixel. Writes the
+//                   pixel cache (ray, range, world normal: the measurement inputs of
+//                   tsdf_integrator.cpp:178-186, once per pixel instead of once per
+//                   (pixel, voxel)). Band [q - tau r^, q + tau r^], amortised DDA
+//                   (tsdf_integrator.hpp:93-135) into a shared-memory table of the
+//                   tile's blocks and their 512-bit voxel masks. Per visit, the
+//                   own-pixel test of the voxel (FP32, sensor-frame offset updated
+//                   incrementally along the DDA, exact decision via error margins): a
+//                   voxel whose own pixel has no return is measured by every visiting
+//                   ray in the reference (.cpp:232-238), so the visit becomes a
+//                   fallback record, measured right away. Tile epilogue: one hash
+//                   find-or-insert per distinct block (new block => next pool index,
+//                   zero-filled by the tile), dirty flag, touched list; the masks are
+//                   ORed into the frame's half of the global mask words and the bits a
+//                   tile sets first become the frame's touched-voxel list (each voxel
+//                   exactly once).
 //   k_fold          K5, one thread per touched voxel (flat, load-balanced): own pixel,
-//                   measure, accumulate-then-merge fold (Eq. 4-5, .cpp:170-248); then
-//                   scatters the fallback records into per-block buckets.
-//   k_fb_fold       warp per block with fallback records: bitonic sort of its bucket
-//                   (keys = linear << 23 | pixel) => per-voxel visits in ascending
-//                   (v, u) order, exactly the reference's order after its chunk-order
-//                   merge + stable_sort; measurements in parallel, then the per-voxel
-//                   sums strictly in that order; fold. Its last CTA writes the frame
-//                   report and resets the per-frame counters.
+//                   measure, accumulate-then-merge fold (Eq. 4-5, .cpp:170-248). Also
+//                   clears the previous frame's half of the mask words and moves the
+//                   fallback records into per-block buckets.
+//   k_fb_fold       CTA per block with fallback records: orders its bucket by (voxel,
+//                   pixel) => per-voxel visits in ascending (v, u) order, exactly the
+//                   reference's order after its chunk-order merge + stable_sort; sums
+//                   the terms strictly in that order; fold. Its last CTA writes the
+//                   frame report and resets the per-frame counters.
 // Every kernel first checks the abort word: after an abort (pool growth, buffer
 // growth, capacity) the rest of the batch no-ops and the host resumes it.
 #include <cub/block/block_scan.cuh>
@@ -55,6 +55,7 @@ struct FrameParams {
     int nonproj, drop_unreliable, has_normals;
     int32_t shard_rank, shard_world;
     uint32_t frame_serial;
+    uint32_t parity;  // which half of each block's 32 mask words this frame uses
     uint32_t max_blocks;
     uint32_t rec_cap, vox_cap;
 };
@@ -76,7 +77,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kFbThreads = 256;
-constexpr int kFbMax = 8192;  // fallback records of one block ordered in shared memory
+constexpr int kFbMax = 4096;  // fallback records of one block ordered in shared memory
 
 __device__ inline d3 dir_at(const double* __restrict__ dirs, uint32_t p) {
     return mk(__ldg(&dirs[3 * p]), __ldg(&dirs[3 * p + 1]), __ldg(&dirs[3 * p + 2]));
@@ -200,231 +201,6 @@ __device__ inline bool band_all_own(const FrameParams& f, const uint8_t* __restr
     const int k = max(ku, kv);
     if (k > kRmax) return false;
     return valid_radius(hd, f.m.W, f.m.H, p) > k;
-}
-
-// Per-visit work on global state (no tile staging): the path a visit takes when
-// its tile's shared tables are full. Same effect as the staged path.
-__device__ void visit_global(const FrameParams& f, HashView h, uint64_t* __restrict__ block_keys,
-                             uint32_t* __restrict__ stamp, uint32_t* __restrict__ touched,
-                             uint32_t* __restrict__ vmask, uint32_t* __restrict__ fbcnt,
-                             unsigned long long* __restrict__ rec, uint32_t* __restrict__ ctr,
-                             uint64_t key, int lin, bool fb, uint32_t p);
-
-__device__ inline uint32_t global_slot(const FrameParams& f, HashView h,
-                                       uint64_t* __restrict__ block_keys,
-                                       uint32_t* __restrict__ stamp,
-                                       uint32_t* __restrict__ touched, uint32_t* __restrict__ ctr,
-                                       uint64_t key) {
-    int ins = 0;
-    const uint32_t slot = hash_insert(h, key, &ins);
-    if (slot == kInvalid) {
-        atomicOr(&ctr[C_ABORT], kAbortHash | kAbortCapacity);
-        return kInvalid;
-    }
-    if (ins) {
-        const uint32_t idx = atomicAdd(&ctr[C_BLOCKS], 1u);
-        h.vals[slot] = idx;
-        if (idx < f.max_blocks) block_keys[idx] = key;
-        if (idx >= f.max_blocks) atomicOr(&ctr[C_ABORT], kAbortCapacity);
-        else if (idx >= ctr[C_MAPPED]) atomicOr(&ctr[C_ABORT], kAbortPool);
-    }
-    if (atomicExch(&stamp[slot], f.frame_serial) != f.frame_serial) {
-        const uint32_t t = atomicAdd(&ctr[C_TOUCHED], 1u);
-        touched[t] = slot;
-    }
-    return slot;
-}
-
-__device__ inline void emit_fallback(const FrameParams& f, uint32_t* __restrict__ fbcnt,
-                                     unsigned long long* __restrict__ rec,
-                                     uint32_t* __restrict__ ctr, uint32_t slot, int lin,
-                                     uint32_t p) {
-    atomicAdd(&fbcnt[slot], 1u);
-    const uint32_t pos = atomicAdd(&ctr[C_RECORDS], 1u);
-    if (pos < f.rec_cap)
-        rec[pos] = (static_cast<unsigned long long>(slot) << 32) |
-                   (static_cast<unsigned long long>(lin) << 23) | p;
-    else
-        atomicOr(&ctr[C_ABORT], kAbortRecords);
-}
-
-__device__ void visit_global(const FrameParams& f, HashView h, uint64_t* __restrict__ block_keys,
-                             uint32_t* __restrict__ stamp, uint32_t* __restrict__ touched,
-                             uint32_t* __restrict__ vmask, uint32_t* __restrict__ fbcnt,
-                             unsigned long long* __restrict__ rec, uint32_t* __restrict__ ctr,
-                             uint64_t key, int lin, bool fb, uint32_t p) {
-    const uint32_t slot = global_slot(f, h, block_keys, stamp, touched, ctr, key);
-    if (slot == kInvalid) return;
-    atomicOr(&vmask[uint64_t(slot) * 32 + (lin >> 5)], 1u << (lin & 31));
-    if (fb) emit_fallback(f, fbcnt, rec, ctr, slot, lin, p);
-}
-
-// CTA = 32 x 8 pixel tile. The tile's rays run their DDA into shared memory: a
-// local table of the distinct blocks they visit, the visit records and per-block
-// voxel masks (smem atomics). Global work is then one hash find-or-insert per
-// distinct block (in parallel across threads) and one RED.OR per non-empty mask
-// word, instead of serialized global round trips per ray.
-constexpr int kTileU = 32, kTileV = 8;
-constexpr int kLocalKeys = 256;
-constexpr int kTileFb = 1024;  // staged fallback visits per tile
-
-__global__ void __launch_bounds__(kTileU * kTileV)
-k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __restrict__ normals,
-               const uint8_t* __restrict__ valid, const double* __restrict__ dirs,
-               const uint8_t* __restrict__ hd, PixCache* __restrict__ cache, HashView h,
-               uint64_t* __restrict__ block_keys, uint32_t* __restrict__ stamp,
-               uint32_t* __restrict__ touched, uint32_t* __restrict__ vmask,
-               uint32_t* __restrict__ fbcnt, unsigned long long* __restrict__ rec,
-               uint32_t* __restrict__ ctr) {
-    if (ctr[C_ABORT]) return;
-    __shared__ unsigned long long lkey[kLocalKeys];
-    __shared__ uint32_t lslot[kLocalKeys];
-    __shared__ uint32_t lmask[kLocalKeys][16];
-    __shared__ uint32_t lfb[kTileFb];
-    __shared__ uint32_t nfb;
-    const int tid = threadIdx.x;
-    lkey[tid] = kEmptyKey;
-#pragma unroll
-    for (int w = 0; w < 16; ++w) lmask[tid][w] = 0u;
-    if (tid == 0) nfb = 0;
-    __syncthreads();
-
-    const int tiles_u = (f.m.W + kTileU - 1) / kTileU;
-    const int tu = int(blockIdx.x) % tiles_u, tv = int(blockIdx.x) / tiles_u;
-    const int u = tu * kTileU + (tid % kTileU);
-    const int v = tv * kTileV + (tid / kTileU);
-    const uint32_t tile_p0 = uint32_t(tv * kTileV) * uint32_t(f.m.W) + uint32_t(tu * kTileU);
-    const bool has_pix = u < f.m.W && v < f.m.H;
-    const uint32_t p = has_pix ? uint32_t(v) * uint32_t(f.m.W) + uint32_t(u) : 0u;
-    const float r = has_pix ? depth[p] : 0.f;
-    const bool in_range = has_pix && !(r == 0.f || double(r) > f.max_range);
-    const bool have_normal = has_pix && f.has_normals && valid[p];
-    // pixel cache (measure lambda inputs, tsdf_integrator.cpp:173-186)
-    d3 q = mk(0, 0, 0), ray = mk(0, 0, 0);
-    if (has_pix) {
-        PixCache pc{};
-        if (in_range) {
-            q = xform(f.pose, scale3(double(r), dir_at(dirs, p)));
-            const d3 dq = sub3(q, f.origin);
-            const double range = sqrt(dot3(dq, dq));
-            ray = div3(dq, range);
-            pc.ray[0] = ray.x;
-            pc.ray[1] = ray.y;
-            pc.ray[2] = ray.z;
-            pc.range = range;
-            if (have_normal) {
-                const d3 n = matvec(f.pose.R, mk(normals[3 * p], normals[3 * p + 1], normals[3 * p + 2]));
-                pc.n[0] = float(n.x);
-                pc.n[1] = float(n.y);
-                pc.n[2] = float(n.z);
-            }
-            pc.flags = ((have_normal || !f.drop_unreliable) ? 1u : 0u) | (have_normal ? 2u : 0u);
-        }
-        cache[p] = pc;
-    }
-    // band ray (tsdf_integrator.cpp:123-131)
-    const bool cast = in_range && !(f.drop_unreliable && f.has_normals && !valid[p]);
-    if (cast) {
-        warp_agg_inc(&ctr[C_RAYS]);
-        const d3 tr = scale3(f.tau, ray);  // (q - o).normalized() == (q - o) / range
-        const d3 a = sub3(q, tr), b = add3(q, tr);
-        uint64_t cur_key = kEmptyKey;
-        int cur_li = -1;
-        bool cur_own = true;
-        int pend_word = -1;
-        uint32_t pend_bits = 0;
-        int32_t x0 = 0, y0 = 0, z0 = 0;
-        float p0x = 0.f, p0y = 0.f, p0z = 0.f;
-        bool first = true;
-        const bool all_own = band_all_own(f, hd, p, r);
-        traverse_segment(a, b, f.nu, f.inv_nu, [&](int32_t x, int32_t y, int32_t z) {
-            const int32_t bx = block_coord(x), by = block_coord(y), bz = block_coord(z);
-            if (!key_in_range(bx) || !key_in_range(by) || !key_in_range(bz)) {
-                atomicOr(&ctr[C_ABORT], kAbortKey);
-                return;
-            }
-            const uint64_t key = pack_key(bx, by, bz);
-            if (key != cur_key) {
-                cur_key = key;
-                cur_own = !(f.shard_world > 1 && owner_of(key, f.shard_world) != f.shard_rank);
-                cur_li = -1;
-                if (cur_own) {  // local table insert (open addressing in smem)
-                    uint32_t s = hash_slot(key, 8);
-                    for (int probe = 0; probe < kLocalKeys; ++probe) {
-                        const unsigned long long old = atomicCAS(&lkey[s], kEmptyKey, key);
-                        if (old == kEmptyKey || old == key) {
-                            cur_li = int(s);
-                            break;
-                        }
-                        s = (s + 1) & (kLocalKeys - 1);
-                    }
-                }
-            }
-            if (!cur_own) return;
-            const int lin = local_linear(x, y, z);
-            // own-pixel test of the visited voxel
-            bool fb = false;
-            if (!all_own) {
-                if (first) {
-                    const d3 pc0 = xform(f.w2s, voxel_center(x, y, z, f.nu));
-                    p0x = float(pc0.x);
-                    p0y = float(pc0.y);
-                    p0z = float(pc0.z);
-                    x0 = x;
-                    y0 = y;
-                    z0 = z;
-                    first = false;
-                }
-                const float kx = float(x - x0), ky = float(y - y0), kz = float(z - z0);
-                const float px = p0x + kx * f.col[0][0] + ky * f.col[1][0] + kz * f.col[2][0];
-                const float py = p0y + kx * f.col[0][1] + ky * f.col[1][1] + kz * f.col[2][1];
-                const float pz = p0z + kx * f.col[0][2] + ky * f.col[1][2] + kz * f.col[2][2];
-                uint32_t own = pixel_fast(px, py, pz, f.m, f.m.r2_lo, f.m.r2_hi);
-                if (own == kNeedFp64) own = pixel_fp64(xform(f.w2s, voxel_center(x, y, z, f.nu)), f.m);
-                fb = own == kInvalid || depth[own] == 0.f;
-            }
-            if (cur_li < 0) {  // local table full: straight to global state
-                visit_global(f, h, block_keys, stamp, touched, vmask, fbcnt, rec, ctr, key, lin, fb, p);
-                return;
-            }
-            const int word = cur_li * 16 + (lin >> 5);
-            if (word != pend_word) {
-                if (pend_word >= 0) atomicOr(&lmask[0][0] + pend_word, pend_bits);
-                pend_word = word;
-                pend_bits = 0u;
-            }
-            pend_bits |= 1u << (lin & 31);
-            if (fb) {
-                const uint32_t pos = atomicAdd(&nfb, 1u);
-                if (pos < uint32_t(kTileFb))
-                    lfb[pos] = (uint32_t(cur_li) << 24) | (uint32_t(lin) << 15) | uint32_t(tid);
-                else
-                    visit_global(f, h, block_keys, stamp, touched, vmask, fbcnt, rec, ctr, key, lin,
-                                 true, p);
-            }
-        });
-        if (pend_word >= 0) atomicOr(&lmask[0][0] + pend_word, pend_bits);
-    }
-    __syncthreads();
-    // one global hash operation per distinct block of the tile
-    if (lkey[tid] != kEmptyKey)
-        lslot[tid] = global_slot(f, h, block_keys, stamp, touched, ctr, lkey[tid]);
-    __syncthreads();
-    const uint32_t nf = min(nfb, uint32_t(kTileFb));
-    for (uint32_t i = tid; i < nf; i += kTileU * kTileV) {
-        const uint32_t e = lfb[i];
-        const uint32_t slot = lslot[e >> 24];
-        if (slot == kInvalid) continue;
-        const uint32_t t = e & 255u;
-        emit_fallback(f, fbcnt, rec, ctr, slot, int((e >> 15) & 511u),
-                      tile_p0 + (t / kTileU) * uint32_t(f.m.W) + (t % kTileU));
-    }
-    for (int i = tid; i < kLocalKeys * 16; i += kTileU * kTileV) {
-        const int li = i >> 4, w = i & 15;
-        const uint32_t bits = lmask[li][w];
-        if (bits && lkey[li] != kEmptyKey && lslot[li] != kInvalid)
-            atomicOr(&vmask[uint64_t(lslot[li]) * 32 + w], bits);
-    }
 }
 
 struct Accum {
@@ -584,91 +360,379 @@ __device__ inline void store_voxel(svx_tsdf_voxel* p, const svx_tsdf_voxel& v) {
     d[4] = v.gradient[2];
 }
 
-// Touched-voxel list, new-block zero fill, mask reset, dirty flag, fallback
-// bucket allocation. Warp per touched block.
-__global__ void __launch_bounds__(kThreads)
-k_compact(FrameParams f, HashView h, svx_tsdf_voxel* __restrict__ pool,
-          const uint32_t* __restrict__ touched, uint32_t* __restrict__ vmask,
-          uint8_t* __restrict__ dirty, unsigned long long* __restrict__ vlist,
-          const uint32_t* __restrict__ fbcnt, uint32_t* __restrict__ fbstart,
-          uint32_t* __restrict__ fbfill, uint32_t* __restrict__ fbslots,
-          uint32_t* __restrict__ ctr) {
-    if (ctr[C_ABORT]) return;
-    constexpr int kWarps = kThreads / 32;
-    __shared__ uint32_t wtot[kWarps], wbase[kWarps];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const uint32_t n_touched = ctr[C_TOUCHED];
-    const uint32_t blocks_before = ctr[C_BLOCKS_BEFORE];
-    // CTA-uniform loop: one list-counter atomic per CTA and iteration (the counter is
-    // a single address; per-warp atomics serialise at L2)
-    for (uint32_t t0 = blockIdx.x * kWarps; t0 < n_touched; t0 += gridDim.x * kWarps) {
-        const uint32_t t = t0 + uint32_t(wid);
-        const bool live = t < n_touched;
-        const uint32_t slot = live ? touched[t] : 0u;
-        const uint32_t idx = live ? h.vals[slot] : 0u;
-        uint32_t* mw = vmask + uint64_t(slot) * 32;
-        const uint32_t w = (live && lane < 16) ? mw[lane] : 0u;
-        uint32_t incl = __popc(w);
-#pragma unroll
-        for (int o = 1; o < 16; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 15);
-        if (lane == 0) wtot[wid] = total;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t s = 0;
-            for (int i = 0; i < kWarps; ++i) {
-                wbase[i] = s;
-                s += wtot[i];
-            }
-            const uint32_t b = s ? atomicAdd(&ctr[C_VOXLIST], s) : 0u;
-            for (int i = 0; i < kWarps; ++i) wbase[i] += b;
-        }
-        __syncthreads();
-        const uint32_t base = wbase[wid];
-        if (!live) continue;
-        if (lane < 16) {
-            uint32_t pos = base + incl - __popc(w);
-            for (uint32_t bits = w; bits; bits &= bits - 1) {
-                const uint32_t linear = uint32_t(lane) * 32u + uint32_t(__ffs(bits) - 1);
-                if (pos < f.vox_cap) vlist[pos] = (static_cast<unsigned long long>(idx) << 9) | linear;
-                ++pos;
-            }
-            mw[lane] = 0u;
-        }
-        if (lane == 0) {
-            if (base + total > f.vox_cap) atomicOr(&ctr[C_ABORT], kAbortVoxList);
-            dirty[idx] = 1;
-            const uint32_t c = fbcnt[slot];
-            if (c) {
-                const uint32_t b = atomicAdd(&ctr[C_BUCKET_TOP], c);
-                fbstart[slot] = b;
-                fbfill[slot] = b;
-                fbslots[atomicAdd(&ctr[C_FB_BLOCKS], 1u)] = slot;
-            }
-        }
-        if (idx >= blocks_before) {  // zero-fill the fresh block (coalesced)
-            float4* z = reinterpret_cast<float4*>(pool + uint64_t(idx) * kBlockVoxels);
-            for (int i = lane; i < kBlockVoxels * 5 / 4; i += 32) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+// A fallback record: one (visiting ray, voxel) measurement of a voxel whose own
+// pixel has no return, measured where the visit is found (band kernel) and
+// summed later in pixel order (k_fb_fold). The voxel's state cannot change in
+// between: fallback voxels are only written by k_fb_fold.
+struct FbRec {
+    uint32_t key;   // linear << 23 | pixel
+    uint32_t slot;  // hash slot of the block
+    Term t;
+};
+static_assert(sizeof(FbRec) == 32, "FbRec layout");
+
+// Hash find-or-insert of a block key; a new block takes the next pool index.
+struct SlotRef {
+    uint32_t slot, idx;
+    bool inserted;
+};
+
+// Pool index of an existing slot. A slot inserted concurrently by another CTA
+// gets its index right after the key (find_or_insert): wait for it.
+__device__ inline uint32_t block_index(HashView h, uint32_t slot) {
+    uint32_t idx = __ldcg(&h.vals[slot]);
+    while (idx == kInvalid) {
+        __nanosleep(64);
+        idx = *reinterpret_cast<volatile uint32_t*>(&h.vals[slot]);
     }
+    return idx;
 }
 
-// One thread per touched voxel; then the fallback record scatter. A list entry
-// holds the pool index and the voxel, so the voxel and its block key load in
-// parallel, and the own pixel's depth and cache entry load together.
+__device__ inline SlotRef find_or_insert(const FrameParams& f, HashView h,
+                                         uint64_t* __restrict__ block_keys,
+                                         uint32_t* __restrict__ ctr, uint64_t key) {
+    SlotRef r{kInvalid, kInvalid, false};
+    int ins = 0;
+    r.slot = hash_insert(h, key, &ins);
+    if (r.slot == kInvalid) {
+        atomicOr(&ctr[C_ABORT], kAbortHash | kAbortCapacity);
+        return r;
+    }
+    if (ins) {
+        r.inserted = true;
+        r.idx = atomicAdd(&ctr[C_BLOCKS], 1u);
+        if (r.idx < f.max_blocks) block_keys[r.idx] = key;
+        __threadfence();
+        atomicExch(&h.vals[r.slot], r.idx);
+        if (r.idx >= f.max_blocks) atomicOr(&ctr[C_ABORT], kAbortCapacity);
+        else if (r.idx >= ctr[C_MAPPED]) atomicOr(&ctr[C_ABORT], kAbortPool);
+    } else {
+        r.idx = block_index(h, r.slot);
+    }
+    return r;
+}
+
+__device__ inline void zero_block(svx_tsdf_voxel* __restrict__ pool, uint32_t idx, int lane, int lanes) {
+    float4* z = reinterpret_cast<float4*>(pool + uint64_t(idx) * kBlockVoxels);
+    for (int i = lane; i < kBlockVoxels * 5 / 4; i += lanes) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// Measurement of fallback visit (slot, lin) by the ray of pixel p. A block
+// created in this frame (pool index unset yet or >= the frame's first new index)
+// is all-zero; its pool memory may not be zero-filled yet (tile epilogues).
+__device__ inline Term fallback_term(const FrameParams& f, HashView h,
+                                     const svx_tsdf_voxel* __restrict__ pool,
+                                     const PixCache* __restrict__ cache, uint32_t blocks_before,
+                                     uint32_t slot, uint64_t key, int lin, uint32_t p) {
+    const uint32_t idx = __ldcg(&h.vals[slot]);
+    svx_tsdf_voxel vox{0.f, 0.f, {0.f, 0.f, 0.f}};
+    if (idx != kInvalid && idx < blocks_before) vox = load_voxel(pool + uint64_t(idx) * kBlockVoxels + lin);
+    return measure_term(f, cache, p, center_of(key, lin, f.nu), vox);
+}
+
+__device__ inline void store_record(FbRec* __restrict__ rec, uint32_t pos, const FbRec& r) {
+    uint4* d = reinterpret_cast<uint4*>(rec + pos);
+    const uint4* s = reinterpret_cast<const uint4*>(&r);
+    d[0] = s[0];
+    d[1] = s[1];
+}
+
+// Per-visit work on global state (no tile staging): the path a visit takes when
+// its tile's shared tables are full. Same effect as the staged path.
+__device__ void visit_global(const FrameParams& f, HashView h, uint64_t* __restrict__ block_keys,
+                             uint32_t* __restrict__ stamp, uint32_t* __restrict__ touched,
+                             uint32_t* __restrict__ vmask, uint32_t* __restrict__ fbcnt,
+                             FbRec* __restrict__ rec, svx_tsdf_voxel* __restrict__ pool,
+                             const PixCache* __restrict__ cache, uint8_t* __restrict__ dirty,
+                             unsigned long long* __restrict__ vlist, uint32_t blocks_before,
+                             uint32_t* __restrict__ ctr, uint64_t key, int lin, bool fb, uint32_t p) {
+    const SlotRef r = find_or_insert(f, h, block_keys, ctr, key);
+    if (r.slot == kInvalid) return;
+    if (atomicExch(&stamp[r.slot], f.frame_serial) != f.frame_serial)
+        touched[atomicAdd(&ctr[C_TOUCHED], 1u)] = r.slot;
+    if (r.idx >= f.max_blocks) return;
+    if (r.inserted && r.idx < ctr[C_MAPPED]) zero_block(pool, r.idx, 0, 1);
+    dirty[r.idx] = 1;
+    const uint32_t bit = 1u << (lin & 31);
+    if (!(atomicOr(&vmask[uint64_t(r.slot) * 32 + f.parity * 16 + (lin >> 5)], bit) & bit)) {
+        const uint32_t pos = atomicAdd(&ctr[C_VOXLIST], 1u);
+        if (pos < f.vox_cap) vlist[pos] = (static_cast<unsigned long long>(r.idx) << 9) | uint32_t(lin);
+        else atomicOr(&ctr[C_ABORT], kAbortVoxList);
+    }
+    if (!fb) return;
+    const Term t = fallback_term(f, h, pool, cache, blocks_before, r.slot, key, lin, p);
+    if (!(t.flags & 1u)) return;  // no contribution
+    atomicAdd(&fbcnt[r.slot], 1u);
+    const uint32_t pos = atomicAdd(&ctr[C_RECORDS], 1u);
+    if (pos < f.rec_cap)
+        store_record(rec, pos, FbRec{(uint32_t(lin) << 23) | p, r.slot, t});
+    else
+        atomicOr(&ctr[C_ABORT], kAbortRecords);
+}
+
+// CTA = 32 x 8 pixel tile. The tile's rays run their DDA into shared memory: a
+// local table of the distinct blocks they visit, the visit records and per-block
+// voxel masks (smem atomics). Global work is then one hash find-or-insert per
+// distinct block (in parallel across threads) and one RED.OR per non-empty mask
+// word, instead of serialized global round trips per ray.
+constexpr int kTileU = 32, kTileV = 8;
+constexpr int kLocalKeys = 256;
+constexpr int kTileFb = 1024;  // staged fallback visits per tile
+
+__global__ void __launch_bounds__(kTileU * kTileV, 4)
+k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __restrict__ normals,
+               const uint8_t* __restrict__ valid, const double* __restrict__ dirs,
+               const uint8_t* __restrict__ hd, PixCache* __restrict__ cache, HashView h,
+               uint64_t* __restrict__ block_keys, uint32_t* __restrict__ stamp,
+               uint32_t* __restrict__ touched, uint32_t* __restrict__ vmask,
+               uint32_t* __restrict__ fbcnt, FbRec* __restrict__ rec,
+               svx_tsdf_voxel* __restrict__ pool, uint8_t* __restrict__ dirty,
+               unsigned long long* __restrict__ vlist, uint32_t* __restrict__ ctr) {
+    // pool exhaustion does not stop the band: the frame resumes after its band
+    if (cta_aborted(ctr, ~uint32_t(kAbortPool))) return;
+    __shared__ unsigned long long lkey[kLocalKeys];
+    __shared__ uint32_t lslot[kLocalKeys];
+    __shared__ uint32_t lidx[kLocalKeys];
+    __shared__ uint32_t lmask[kLocalKeys][16];
+    __shared__ uint32_t lfb[kTileFb];
+    __shared__ uint32_t lcnt[kLocalKeys];  // kept fallback records per local block
+    __shared__ uint32_t lnew[kLocalKeys];  // pool indices of blocks this tile created
+    __shared__ uint32_t nfb, nnew;
+    const int tid = threadIdx.x;
+    const uint32_t blocks_before = ctr[C_BLOCKS_BEFORE];
+    lkey[tid] = kEmptyKey;
+    lcnt[tid] = 0u;
+#pragma unroll
+    for (int w = 0; w < 16; ++w) lmask[tid][w] = 0u;
+    if (tid == 0) nfb = nnew = 0;
+    __syncthreads();
+
+    const int tiles_u = (f.m.W + kTileU - 1) / kTileU;
+    const int tu = int(blockIdx.x) % tiles_u, tv = int(blockIdx.x) / tiles_u;
+    const int u = tu * kTileU + (tid % kTileU);
+    const int v = tv * kTileV + (tid / kTileU);
+    const uint32_t tile_p0 = uint32_t(tv * kTileV) * uint32_t(f.m.W) + uint32_t(tu * kTileU);
+    const bool has_pix = u < f.m.W && v < f.m.H;
+    const uint32_t p = has_pix ? uint32_t(v) * uint32_t(f.m.W) + uint32_t(u) : 0u;
+    const float r = has_pix ? depth[p] : 0.f;
+    const bool in_range = has_pix && !(r == 0.f || double(r) > f.max_range);
+    const bool have_normal = has_pix && f.has_normals && valid[p];
+    // pixel cache (measure lambda inputs, tsdf_integrator.cpp:173-186)
+    d3 q = mk(0, 0, 0), ray = mk(0, 0, 0);
+    if (has_pix) {
+        PixCache pc{};
+        if (in_range) {
+            q = xform(f.pose, scale3(double(r), dir_at(dirs, p)));
+            const d3 dq = sub3(q, f.origin);
+            const double range = sqrt(dot3(dq, dq));
+            ray = div3(dq, range);
+            pc.ray[0] = ray.x;
+            pc.ray[1] = ray.y;
+            pc.ray[2] = ray.z;
+            pc.range = range;
+            if (have_normal) {
+                const d3 n = matvec(f.pose.R, mk(normals[3 * p], normals[3 * p + 1], normals[3 * p + 2]));
+                pc.n[0] = float(n.x);
+                pc.n[1] = float(n.y);
+                pc.n[2] = float(n.z);
+            }
+            pc.flags = ((have_normal || !f.drop_unreliable) ? 1u : 0u) | (have_normal ? 2u : 0u);
+        }
+        cache[p] = pc;
+    }
+    // band ray (tsdf_integrator.cpp:123-131)
+    const bool cast = in_range && !(f.drop_unreliable && f.has_normals && !valid[p]);
+    if (cast) {
+        warp_agg_inc(&ctr[C_RAYS]);
+        const d3 tr = scale3(f.tau, ray);  // (q - o).normalized() == (q - o) / range
+        const d3 a = sub3(q, tr), b = add3(q, tr);
+        uint64_t cur_key = kEmptyKey;
+        int cur_li = -1;
+        bool cur_own = true;
+        int pend_word = -1;
+        uint32_t pend_bits = 0;
+        int32_t x0 = 0, y0 = 0, z0 = 0;
+        float p0x = 0.f, p0y = 0.f, p0z = 0.f;
+        bool first = true;
+        const bool all_own = band_all_own(f, hd, p, r);
+        traverse_segment(a, b, f.nu, f.inv_nu, [&](int32_t x, int32_t y, int32_t z) {
+            const int32_t bx = block_coord(x), by = block_coord(y), bz = block_coord(z);
+            if (!key_in_range(bx) || !key_in_range(by) || !key_in_range(bz)) {
+                atomicOr(&ctr[C_ABORT], kAbortKey);
+                return;
+            }
+            const uint64_t key = pack_key(bx, by, bz);
+            if (key != cur_key) {
+                cur_key = key;
+                cur_own = !(f.shard_world > 1 && owner_of(key, f.shard_world) != f.shard_rank);
+                cur_li = -1;
+                if (cur_own) {  // local table insert (open addressing in smem)
+                    uint32_t s = hash_slot(key, 8);
+                    for (int probe = 0; probe < kLocalKeys; ++probe) {
+                        const unsigned long long old = atomicCAS(&lkey[s], kEmptyKey, key);
+                        if (old == kEmptyKey || old == key) {
+                            cur_li = int(s);
+                            break;
+                        }
+                        s = (s + 1) & (kLocalKeys - 1);
+                    }
+                }
+            }
+            if (!cur_own) return;
+            const int lin = local_linear(x, y, z);
+            // own-pixel test of the visited voxel
+            bool fb = false;
+            if (!all_own) {
+                if (first) {
+                    const d3 pc0 = xform(f.w2s, voxel_center(x, y, z, f.nu));
+                    p0x = float(pc0.x);
+                    p0y = float(pc0.y);
+                    p0z = float(pc0.z);
+                    x0 = x;
+                    y0 = y;
+                    z0 = z;
+                    first = false;
+                }
+                const float kx = float(x - x0), ky = float(y - y0), kz = float(z - z0);
+                const float px = p0x + kx * f.col[0][0] + ky * f.col[1][0] + kz * f.col[2][0];
+                const float py = p0y + kx * f.col[0][1] + ky * f.col[1][1] + kz * f.col[2][1];
+                const float pz = p0z + kx * f.col[0][2] + ky * f.col[1][2] + kz * f.col[2][2];
+                uint32_t own = pixel_fast(px, py, pz, f.m, f.m.r2_lo, f.m.r2_hi);
+                if (own == kNeedFp64) own = pixel_fp64(xform(f.w2s, voxel_center(x, y, z, f.nu)), f.m);
+                fb = own == kInvalid || depth[own] == 0.f;
+            }
+            if (cur_li < 0) {  // local table full: straight to global state
+                visit_global(f, h, block_keys, stamp, touched, vmask, fbcnt, rec, pool, cache, dirty,
+                             vlist, blocks_before, ctr, key, lin, fb, p);
+                return;
+            }
+            const int word = cur_li * 16 + (lin >> 5);
+            if (word != pend_word) {
+                if (pend_word >= 0) atomicOr(&lmask[0][0] + pend_word, pend_bits);
+                pend_word = word;
+                pend_bits = 0u;
+            }
+            pend_bits |= 1u << (lin & 31);
+            if (fb) {
+                const uint32_t pos = atomicAdd(&nfb, 1u);
+                if (pos < uint32_t(kTileFb))
+                    lfb[pos] = (uint32_t(cur_li) << 24) | (uint32_t(lin) << 15) | uint32_t(tid);
+                else
+                    visit_global(f, h, block_keys, stamp, touched, vmask, fbcnt, rec, pool, cache,
+                                 dirty, vlist, blocks_before, ctr, key, lin, true, p);
+            }
+        });
+        if (pend_word >= 0) atomicOr(&lmask[0][0] + pend_word, pend_bits);
+    }
+    __syncthreads();
+    // one global hash operation per distinct block of the tile; first touches of
+    // the frame are appended to the touched list with one atomic per tile
+    constexpr int kW = kTileU * kTileV / 32;
+    __shared__ uint32_t s_w[2 * kW];
+    uint32_t slot = kInvalid;
+    bool first_touch = false;
+    if (lkey[tid] != kEmptyKey) {
+        const SlotRef r = find_or_insert(f, h, block_keys, ctr, lkey[tid]);
+        slot = r.slot;
+        if (slot != kInvalid) {
+            first_touch = atomicExch(&stamp[slot], f.frame_serial) != f.frame_serial;
+            lidx[tid] = r.idx;
+            if (r.idx < f.max_blocks) {
+                dirty[r.idx] = 1;
+                if (r.inserted && r.idx < ctr[C_MAPPED]) lnew[atomicAdd(&nnew, 1u)] = r.idx;
+            } else {
+                slot = kInvalid;  // capacity abort is set; nothing below may touch the pool
+                first_touch = false;
+            }
+        }
+    }
+    lslot[tid] = slot;
+    const uint32_t tpos = cta_append<kW>(first_touch, &ctr[C_TOUCHED], s_w);
+    if (first_touch) touched[tpos] = slot;
+    // zero-fill the blocks this tile created (read from the next kernel on)
+    for (uint32_t j = 0; j < nnew; ++j) zero_block(pool, lnew[j], tid, kTileU * kTileV);
+    // fallback visits: measured here (the rays' pixel cache entries were written
+    // above by this CTA); records that contribute are appended with one atomic per
+    // round, and counted per block with one atomic per block
+    const uint32_t nf = min(nfb, uint32_t(kTileFb));
+    for (uint32_t i0 = 0; i0 < nf; i0 += kTileU * kTileV) {
+        const uint32_t i = i0 + uint32_t(tid);
+        FbRec r{};
+        bool keep = false;
+        uint32_t li = 0;
+        if (i < nf) {
+            const uint32_t e = lfb[i];
+            li = e >> 24;
+            r.slot = lslot[li];
+            if (r.slot != kInvalid) {
+                const uint32_t t = e & 255u;
+                const uint32_t px = tile_p0 + (t / kTileU) * uint32_t(f.m.W) + (t % kTileU);
+                const int lin = int((e >> 15) & 511u);
+                r.t = fallback_term(f, h, pool, cache, blocks_before, r.slot, lkey[li], lin, px);
+                r.key = (uint32_t(lin) << 23) | px;
+                keep = r.t.flags & 1u;
+            }
+        }
+        const uint32_t pos = cta_append<kW>(keep, &ctr[C_RECORDS], s_w);
+        if (keep) {
+            atomicAdd(&lcnt[li], 1u);
+            if (pos < f.rec_cap) store_record(rec, pos, r);
+            else atomicOr(&ctr[C_ABORT], kAbortRecords);
+        }
+    }
+    // voxel masks -> this frame's half of the global mask words; the bits a tile
+    // sets first (atomicOr returns them clear) are its voxels' single entries in
+    // the frame's touched-voxel list
+    uint32_t nv = 0;
+    for (int i = tid; i < kLocalKeys * 16; i += kTileU * kTileV) {
+        const int li = i >> 4, w = i & 15;
+        uint32_t bits = lmask[li][w];
+        if (bits && lslot[li] != kInvalid) {
+            const uint32_t old = atomicOr(&vmask[uint64_t(lslot[li]) * 32 + f.parity * 16 + w], bits);
+            bits &= ~old;
+        } else {
+            bits = 0u;
+        }
+        lmask[li][w] = bits;
+        nv += __popc(bits);
+    }
+    uint32_t pos = cta_reserve<kW>(nv, &ctr[C_VOXLIST], s_w);
+    if (nv && pos + nv > f.vox_cap) atomicOr(&ctr[C_ABORT], kAbortVoxList);
+    for (int i = tid; i < kLocalKeys * 16 && nv; i += kTileU * kTileV) {
+        const int li = i >> 4, w = i & 15;
+        const unsigned long long hi = static_cast<unsigned long long>(lidx[li]) << 9;
+        for (uint32_t bits = lmask[li][w]; bits; bits &= bits - 1, ++pos)
+            if (pos < f.vox_cap) vlist[pos] = hi | (uint32_t(w) * 32u + uint32_t(__ffs(bits) - 1));
+    }
+    __syncthreads();  // lcnt complete
+    if (lcnt[tid]) atomicAdd(&fbcnt[lslot[tid]], lcnt[tid]);
+}
+
+// One thread per touched voxel: own pixel, measure, fold. A list entry holds the
+// pool index and the voxel, so the voxel and its block key load in parallel.
+// The same kernel clears the previous frame's half of the mask words (the next
+// frame uses it) and moves the fallback records into per-block buckets; a
+// block's bucket is allocated by the first of its records to arrive.
 __global__ void __launch_bounds__(kThreads)
 k_fold(FrameParams f, const float* __restrict__ depth, const PixCache* __restrict__ cache,
        const uint64_t* __restrict__ block_keys, svx_tsdf_voxel* __restrict__ pool,
-       const unsigned long long* __restrict__ vlist, const unsigned long long* __restrict__ rec,
-       uint32_t* __restrict__ fbfill, uint32_t* __restrict__ bucket, uint32_t* __restrict__ ctr) {
+       const unsigned long long* __restrict__ vlist, const uint32_t* __restrict__ touched_prev,
+       uint32_t* __restrict__ vmask, const FbRec* __restrict__ rec,
+       const uint32_t* __restrict__ fbcnt, uint32_t* __restrict__ fbstart,
+       uint32_t* __restrict__ fbclaim, uint32_t* __restrict__ fbfill,
+       uint32_t* __restrict__ fbslots, FbRec* __restrict__ bucket, uint32_t* __restrict__ ctr) {
     if (ctr[C_ABORT]) return;
-    const uint32_t nv = ctr[C_VOXLIST];
+    const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t stride = gridDim.x * blockDim.x;
+    {
+        const uint32_t n_prev = ctr[C_TOUCHED_PREV];
+        const uint32_t other = (f.parity ^ 1u) * 16u;
+        for (uint32_t i = gtid; i < n_prev * 16u; i += stride)
+            vmask[uint64_t(touched_prev[i >> 4]) * 32 + other + (i & 15u)] = 0u;
+    }
+    const uint32_t nv = min(ctr[C_VOXLIST], f.vox_cap);
     uint32_t n_upd = 0;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+    for (uint32_t i = gtid; i < nv; i += stride) {
         const unsigned long long v = vlist[i];
         const uint64_t idx = v >> 9;
         const int linear = int(v & 511u);
@@ -688,10 +752,25 @@ k_fold(FrameParams f, const float* __restrict__ depth, const PixCache* __restric
         }
     }
     const uint32_t nr = min(ctr[C_RECORDS], f.rec_cap);
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += stride) {
-        const unsigned long long r = rec[i];
-        const uint32_t pos = atomicAdd(&fbfill[uint32_t(r >> 32)], 1u);
-        bucket[pos] = uint32_t(r);
+    for (uint32_t i = gtid; i < nr; i += stride) {
+        const uint4* src = reinterpret_cast<const uint4*>(rec + i);
+        const uint4 a = src[0], b = src[1];
+        const uint32_t slot = a.y;
+        uint32_t start = __ldcg(&fbstart[slot]);
+        if (start == kInvalid) {
+            if (atomicCAS(&fbclaim[slot], 0u, 1u) == 0u) {  // this record allocates the bucket
+                start = atomicAdd(&ctr[C_BUCKET_TOP], fbcnt[slot]);
+                fbslots[atomicAdd(&ctr[C_FB_BLOCKS], 1u)] = slot;
+                atomicExch(&fbstart[slot], start);
+            } else {
+                while ((start = *reinterpret_cast<volatile uint32_t*>(&fbstart[slot])) == kInvalid)
+                    __nanosleep(32);
+            }
+        }
+        const uint32_t pos = start + atomicAdd(&fbfill[slot], 1u);
+        uint4* dst = reinterpret_cast<uint4*>(bucket + pos);
+        dst[0] = a;
+        dst[1] = b;
     }
     for (int o = 16; o; o >>= 1) n_upd += __shfl_xor_sync(0xFFFFFFFFu, n_upd, o);
     if ((threadIdx.x & 31) == 0 && n_upd) atomicAdd(&ctr[C_UPDATED], n_upd);
@@ -708,25 +787,44 @@ __device__ void write_frame_end(FrameOut* __restrict__ out, uint32_t* __restrict
     o.fb_voxels = ctr[C_FB_VOXELS];
     o.ok = 1;
     *out = o;
+    ctr[C_TOUCHED_PREV] = ctr[C_TOUCHED];
     ctr[C_TOUCHED] = ctr[C_UPDATED] = ctr[C_RECORDS] = ctr[C_RAYS] = 0;
     ctr[C_DROPPED] = ctr[C_TIES] = ctr[C_FB_BLOCKS] = ctr[C_FB_VOXELS] = ctr[C_FB_BIG] = 0;
     ctr[C_VOXLIST] = ctr[C_BUCKET_TOP] = 0;
     ctr[C_BLOCKS_BEFORE] = ctr[C_BLOCKS];
 }
 
-// Ordered fold of one fallback voxel from its measured terms [i, end).
-__device__ inline bool fold_terms(svx_tsdf_voxel* vp, const Term* __restrict__ terms, uint32_t i,
-                                  uint32_t end) {
+__device__ inline Term record_term(const FbRec* __restrict__ r) {
+    const uint4* q = reinterpret_cast<const uint4*>(r);
+    const uint4 a = q[0], b = q[1];
+    Term t;
+    t.wg = __uint_as_float(a.z);
+    t.w = __uint_as_float(a.w);
+    t.nx = __uint_as_float(b.x);
+    t.ny = __uint_as_float(b.y);
+    t.nz = __uint_as_float(b.z);
+    t.flags = b.w;
+    return t;
+}
+
+// Ordered fold of one fallback voxel: the terms of records bucket[src[i..end)],
+// summed in that order (ascending pixel). Loads are issued four at a time so the
+// sequential sum does not pay one L2 round trip per record.
+template <typename Src>
+__device__ inline bool fold_records(svx_tsdf_voxel* vp, const FbRec* __restrict__ bucket,
+                                    const Src* __restrict__ src, uint32_t i, uint32_t end) {
+    if (i == end) return false;
     Accum acc{0.0, 0.0, 0.0, 0.0, 0.0};
-    bool measured = false;
-    for (uint32_t j = i; j < end; ++j) {
-        const Term t = terms[j];
-        if (t.flags & 1u) {
-            accumulate(acc, t);
-            measured = true;
-        }
+    uint32_t j = i;
+    for (; j + 4 <= end; j += 4) {
+        const Term t0 = record_term(bucket + src[j]), t1 = record_term(bucket + src[j + 1]);
+        const Term t2 = record_term(bucket + src[j + 2]), t3 = record_term(bucket + src[j + 3]);
+        accumulate(acc, t0);
+        accumulate(acc, t1);
+        accumulate(acc, t2);
+        accumulate(acc, t3);
     }
-    if (!measured) return false;
+    for (; j < end; ++j) accumulate(acc, record_term(bucket + src[j]));
     svx_tsdf_voxel vox = load_voxel(vp);
     fold(vox, acc);
     store_voxel(vp, vox);
@@ -734,24 +832,27 @@ __device__ inline bool fold_terms(svx_tsdf_voxel* vp, const Term* __restrict__ t
 }
 
 // CTA per block with fallback records (the records cluster on few blocks, e.g. on
-// the ring where the lowest beam meets the ground). The bucket is ordered by
-// (voxel, pixel) without a full sort: counting sort by voxel in shared memory
-// (histogram, scan, scatter), then each voxel's short segment is insertion-sorted
-// by pixel by one thread. Terms are measured in parallel and summed per voxel
-// strictly in that order.
+// the ring where the lowest beam meets the ground). Records arrive measured; the
+// bucket is ordered by (voxel, pixel) in shared memory: counting sort by voxel
+// (histogram, scan, scatter), then inside each voxel's segment a rank sort (the
+// rank of a record is the number of smaller keys in its segment; keys are unique,
+// a ray visits a voxel once), all in parallel. One thread per voxel then folds it
+// with the terms summed strictly in that order.
 __global__ void __launch_bounds__(kFbThreads)
-k_fb_fold(FrameParams f, const PixCache* __restrict__ cache, HashView h,
-          svx_tsdf_voxel* __restrict__ pool, const uint32_t* __restrict__ fbslots,
-          uint32_t* __restrict__ fbcnt, const uint32_t* __restrict__ fbstart,
-          const uint32_t* __restrict__ bucket, Term* __restrict__ terms,
-          uint32_t* __restrict__ bigslots, FrameOut* __restrict__ out, uint32_t* __restrict__ ctr) {
-    if (ctr[C_ABORT]) return;
+k_fb_fold(HashView h, svx_tsdf_voxel* __restrict__ pool, const uint32_t* __restrict__ fbslots,
+          uint32_t* __restrict__ fbcnt, uint32_t* __restrict__ fbstart,
+          uint32_t* __restrict__ fbclaim, uint32_t* __restrict__ fbfill,
+          const FbRec* __restrict__ bucket, uint32_t* __restrict__ bigslots,
+          FrameOut* __restrict__ out, uint32_t* __restrict__ ctr) {
+    // a big bucket (host-sorted afterwards) must not stop the other buckets
+    if (cta_aborted(ctr, ~uint32_t(kAbortBigBucket))) return;
     using Scan = cub::BlockScan<uint32_t, kFbThreads>;
     constexpr int kPer = kBlockVoxels / kFbThreads;  // voxels per thread in the scan
     __shared__ typename Scan::TempStorage scan_tmp;
-    __shared__ uint32_t keys[kFbMax];
-    __shared__ uint32_t seg_end[kBlockVoxels];  // per voxel: end of its segment after scatter
-    __shared__ uint32_t seg_cnt[kBlockVoxels];
+    __shared__ uint32_t keys[kFbMax];   // grouped by voxel
+    __shared__ uint16_t src1[kFbMax];   // record index of keys[i]
+    __shared__ uint16_t src2[kFbMax];   // record indices in (voxel, pixel) order
+    __shared__ uint32_t seg_start[kBlockVoxels], seg_cnt[kBlockVoxels], cursor[kBlockVoxels];
     __shared__ bool last;
     const uint32_t nb = ctr[C_FB_BLOCKS];
     uint32_t n_upd = 0;
@@ -766,10 +867,10 @@ k_fb_fold(FrameParams f, const PixCache* __restrict__ cache, HashView h,
             }
             continue;
         }
+        const FbRec* bk = bucket + start;
         for (int v = threadIdx.x; v < kBlockVoxels; v += kFbThreads) seg_cnt[v] = 0u;
         __syncthreads();
-        for (uint32_t i = threadIdx.x; i < cnt; i += kFbThreads)
-            atomicAdd(&seg_cnt[bucket[start + i] >> 23], 1u);
+        for (uint32_t i = threadIdx.x; i < cnt; i += kFbThreads) atomicAdd(&seg_cnt[bk[i].key >> 23], 1u);
         __syncthreads();
         {   // exclusive scan of the per-voxel counts -> segment starts
             uint32_t c[kPer];
@@ -777,42 +878,38 @@ k_fb_fold(FrameParams f, const PixCache* __restrict__ cache, HashView h,
             for (int j = 0; j < kPer; ++j) c[j] = seg_cnt[threadIdx.x * kPer + j];
             Scan(scan_tmp).ExclusiveSum(c, c);
 #pragma unroll
-            for (int j = 0; j < kPer; ++j) seg_end[threadIdx.x * kPer + j] = c[j];
-        }
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < cnt; i += kFbThreads) {
-            const uint32_t k = bucket[start + i];
-            keys[atomicAdd(&seg_end[k >> 23], 1u)] = k;
-        }
-        __syncthreads();
-        // pixel order inside each voxel segment (segments are short)
-        for (int v = threadIdx.x; v < kBlockVoxels; v += kFbThreads) {
-            const uint32_t e = seg_end[v], b = e - seg_cnt[v];
-            for (uint32_t i = b + 1; i < e; ++i) {
-                const uint32_t k = keys[i];
-                uint32_t j = i;
-                for (; j > b && keys[j - 1] > k; --j) keys[j] = keys[j - 1];
-                keys[j] = k;
+            for (int j = 0; j < kPer; ++j) {
+                seg_start[threadIdx.x * kPer + j] = c[j];
+                cursor[threadIdx.x * kPer + j] = c[j];
             }
         }
         __syncthreads();
-        const uint64_t key = h.keys[slot];
-        svx_tsdf_voxel* blk = pool + uint64_t(h.vals[slot]) * kBlockVoxels;
-        Term* tb = terms + start;
-        // measurements in parallel (pre-update voxel state, read-only here)
         for (uint32_t i = threadIdx.x; i < cnt; i += kFbThreads) {
-            const uint32_t kv = keys[i];
-            const int linear = int(kv >> 23);
-            tb[i] = measure_term(f, cache, kv & 0x7FFFFFu, center_of(key, linear, f.nu),
-                                 load_voxel(blk + linear));
+            const uint32_t k = bk[i].key;
+            const uint32_t d = atomicAdd(&cursor[k >> 23], 1u);
+            keys[d] = k;
+            src1[d] = uint16_t(i);
         }
         __syncthreads();
-        // per-voxel sums strictly in pixel order
-        for (int v = threadIdx.x; v < kBlockVoxels; v += kFbThreads) {
-            const uint32_t n = seg_cnt[v];
-            if (n) n_upd += fold_terms(blk + v, tb, seg_end[v] - n, seg_end[v]) ? 1u : 0u;
+        for (uint32_t i = threadIdx.x; i < cnt; i += kFbThreads) {
+            const uint32_t k = keys[i], v = k >> 23;
+            const uint32_t b = seg_start[v], e = b + seg_cnt[v];
+            uint32_t r = 0;
+            for (uint32_t j = b; j < e; ++j) r += keys[j] < k ? 1u : 0u;
+            src2[b + r] = src1[i];
         }
-        if (threadIdx.x == 0) fbcnt[slot] = 0u;
+        __syncthreads();
+        svx_tsdf_voxel* blk = pool + uint64_t(h.vals[slot]) * kBlockVoxels;
+        for (int v = threadIdx.x; v < kBlockVoxels; v += kFbThreads) {
+            const uint32_t b = seg_start[v];
+            n_upd += fold_records(blk + v, bk, src2, b, b + seg_cnt[v]) ? 1u : 0u;
+        }
+        if (threadIdx.x == 0) {  // per-slot fallback state, clean for the next frame
+            fbcnt[slot] = 0u;
+            fbstart[slot] = kInvalid;
+            fbclaim[slot] = 0u;
+            fbfill[slot] = 0u;
+        }
         __syncthreads();  // shared arrays are reused by the next bucket
     }
     for (int o = 16; o; o >>= 1) n_upd += __shfl_xor_sync(0xFFFFFFFFu, n_upd, o);
@@ -834,28 +931,26 @@ k_fb_fold(FrameParams f, const PixCache* __restrict__ cache, HashView h,
     }
 }
 
-// Host-sorted bucket of one big block: terms in parallel, then ordered sums.
-__global__ void k_fb_terms_sorted(FrameParams f, const PixCache* __restrict__ cache, HashView h,
-                                  svx_tsdf_voxel* __restrict__ pool, uint32_t slot,
-                                  const uint32_t* __restrict__ keys, uint32_t cnt,
-                                  Term* __restrict__ terms) {
+// Big buckets (more records than k_fb_fold orders in shared memory): keys and
+// record indices sorted by CUB on the device, then one thread per voxel segment.
+__global__ void k_fb_extract(const FbRec* __restrict__ bk, uint32_t cnt, uint32_t* __restrict__ keys,
+                             uint32_t* __restrict__ idx) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= cnt) return;
-    const int linear = int(keys[i] >> 23);
-    svx_tsdf_voxel* blk = pool + uint64_t(h.vals[slot]) * kBlockVoxels;
-    terms[i] = measure_term(f, cache, keys[i] & 0x7FFFFFu, center_of(h.keys[slot], linear, f.nu),
-                            load_voxel(blk + linear));
+    keys[i] = bk[i].key;
+    idx[i] = i;
 }
 
 __global__ void k_fb_fold_sorted(HashView h, svx_tsdf_voxel* __restrict__ pool, uint32_t slot,
-                                 const uint32_t* __restrict__ keys, uint32_t cnt,
-                                 const Term* __restrict__ terms, uint32_t* __restrict__ ctr) {
+                                 const FbRec* __restrict__ bk, const uint32_t* __restrict__ keys,
+                                 const uint32_t* __restrict__ idx, uint32_t cnt,
+                                 uint32_t* __restrict__ ctr) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= cnt || !(i == 0 || (keys[i] >> 23) != (keys[i - 1] >> 23))) return;
     uint32_t end = i + 1;
     while (end < cnt && (keys[end] >> 23) == (keys[i] >> 23)) ++end;
     svx_tsdf_voxel* blk = pool + uint64_t(h.vals[slot]) * kBlockVoxels;
-    if (fold_terms(blk + (keys[i] >> 23), terms, i, end)) {
+    if (fold_records(blk + (keys[i] >> 23), bk, idx, i, end)) {
         atomicAdd(&ctr[C_UPDATED], 1u);
         atomicAdd(&ctr[C_FB_VOXELS], 1u);
     }
@@ -867,11 +962,15 @@ __global__ void k_frame_end(FrameOut* __restrict__ out, uint32_t* __restrict__ c
 }
 
 // Undo the per-frame record state before re-running the band kernel of a frame.
+// (fallback counts and this frame's half of the mask words of its touched blocks)
 __global__ void k_reset_fb(const uint32_t* __restrict__ touched, uint32_t* __restrict__ fbcnt,
-                           uint32_t* __restrict__ ctr) {
+                           uint32_t* __restrict__ vmask, uint32_t parity, uint32_t* __restrict__ ctr) {
     const uint32_t n = ctr[C_TOUCHED];
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        fbcnt[touched[i]] = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n * 16u; i += gridDim.x * blockDim.x) {
+        const uint32_t slot = touched[i >> 4];
+        if ((i & 15u) == 0) fbcnt[slot] = 0;
+        vmask[uint64_t(slot) * 32 + parity * 16 + (i & 15u)] = 0u;
+    }
 }
 
 // Capacity path: every visited block key of the frame (duplicates allowed).
@@ -911,8 +1010,10 @@ __global__ void k_mark_dirty(const uint64_t* __restrict__ keys_sorted, uint32_t 
 
 inline unsigned grid_for(uint64_t n) { return unsigned((n + kThreads - 1) / kThreads); }
 
-FrameParams make_params(svx_map* m, svx_scan* s, const Pose& pose, const svx_integrator_cfg& cfg) {
+FrameParams make_params(svx_map* m, svx_scan* s, const Pose& pose, const svx_integrator_cfg& cfg,
+                        uint32_t parity) {
     FrameParams f{};
+    f.parity = parity & 1u;
     f.m = s->dm;
     f.pose = pose;
     f.w2s = inverse_pose(pose);
@@ -956,13 +1057,17 @@ FrameParams make_params(svx_map* m, svx_scan* s, const Pose& pose, const svx_int
     return f;
 }
 
-// Stages of one frame: 0 band, 1 compact, 2 fold, 3 fallback (+ report), 4 report only.
+// Stages of one frame: 0 band, 1 fold, 2 fallback (+ report), 3 report only.
+enum { kStageBand = 0, kStageFold = 1, kStageFallback = 2, kStageReport = 3 };
+
 void launch_stages(svx_map* m, svx_scan* s, const FrameParams& f, int from, FrameOut* out) {
     const uint32_t P = uint32_t(s->P);
     HashView hv = hash_view(m);
     const PixCache* cache = reinterpret_cast<const PixCache*>(s->pixcache.p);
     const unsigned pg = persistent_grid(m->device);
-    if (from <= 0) {
+    uint32_t* touched_cur = m->touched + uint64_t(f.parity) * m->cap;
+    uint32_t* touched_prev = m->touched + uint64_t(f.parity ^ 1u) * m->cap;
+    if (from <= kStageBand) {
         ProfMark pm(m, SVX_K_RAYCAST);
         if (!s->rowdist_fresh) {  // host-provided depth: the projection did not build it
             k_row_dist<<<grid_for(P), kThreads, 0, m->stream>>>(s->depth.p, s->dm.W, s->dm.H,
@@ -973,43 +1078,31 @@ void launch_stages(svx_map* m, svx_scan* s, const FrameParams& f, int from, Fram
         const unsigned tiles = unsigned(((s->dm.W + 31) / 32) * ((s->dm.H + 7) / 8));
         k_raycast_band<<<tiles, 256, 0, m->stream>>>(
             f, s->depth.p, s->normals.p, s->valid.p, s->dirs.p, s->rowdist.p,
-            reinterpret_cast<PixCache*>(s->pixcache.p), hv, m->block_keys, m->stamp, m->touched,
-            m->vmask, m->fbcnt, m->records.p, m->d_ctr);
+            reinterpret_cast<PixCache*>(s->pixcache.p), hv, m->block_keys, m->stamp, touched_cur,
+            m->vmask, m->fbcnt, reinterpret_cast<FbRec*>(m->records.p), tsdf_base(m), m->dirty,
+            m->vlist.p, m->d_ctr);
         count_launch();
     }
-    if (from <= 1) {
-        ProfMark pm(m, SVX_K_COMPACT);
-        k_compact<<<pg, kThreads, 0, m->stream>>>(f, hv, tsdf_base(m), m->touched, m->vmask,
-                                                  m->dirty, m->vlist.p, m->fbcnt, m->fbstart,
-                                                  m->fbfill, m->fbslots, m->d_ctr);
-        count_launch();
-    }
-    if (from <= 2) {
+    if (from <= kStageFold) {
         ProfMark pm(m, SVX_K_FOLD);
         k_fold<<<pg, kThreads, 0, m->stream>>>(f, s->depth.p, cache, m->block_keys, tsdf_base(m),
-                                               m->vlist.p, m->records.p, m->fbfill, m->bucket.p,
-                                               m->d_ctr);
+                                               m->vlist.p, touched_prev, m->vmask,
+                                               reinterpret_cast<const FbRec*>(m->records.p), m->fbcnt,
+                                               m->fbstart, m->fbclaim, m->fbfill, m->fbslots,
+                                               reinterpret_cast<FbRec*>(m->bucket.p), m->d_ctr);
         count_launch();
     }
-    if (from <= 3) {
+    if (from <= kStageFallback) {
         ProfMark pm(m, SVX_K_FALLBACK);
-        k_fb_fold<<<pg / 2, kFbThreads, 0, m->stream>>>(f, cache, hv, tsdf_base(m), m->fbslots, m->fbcnt,
-                                                  m->fbstart, m->bucket.p,
-                                                  reinterpret_cast<Term*>(m->terms.p), m->bigslots,
-                                                  out, m->d_ctr);
+        k_fb_fold<<<pg / 2, kFbThreads, 0, m->stream>>>(
+            hv, tsdf_base(m), m->fbslots, m->fbcnt, m->fbstart, m->fbclaim, m->fbfill,
+            reinterpret_cast<const FbRec*>(m->bucket.p), m->bigslots, out, m->d_ctr);
         count_launch();
     } else {
         k_frame_end<<<1, 1, 0, m->stream>>>(out, m->d_ctr);
         count_launch();
     }
     SVX_CUDA(cudaGetLastError());
-}
-
-void sort_u32(svx_map* m, uint32_t* in, uint32_t* out, uint32_t n) {
-    size_t bytes = 0;
-    SVX_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, in, out, int(n), 0, 32, m->stream));
-    m->sort_tmp.alloc(bytes ? bytes : 1);
-    SVX_CUDA(cub::DeviceRadixSort::SortKeys(m->sort_tmp.p, bytes, in, out, int(n), 0, 32, m->stream));
 }
 
 // CapacityError path (tsdf_integrator.cpp:160-168 + voxel_store.cpp:18-20):
@@ -1072,8 +1165,9 @@ void sort_u32(svx_map* m, uint32_t* in, uint32_t* out, uint32_t n) {
                                   std::to_string(m->cfg.max_blocks) + ")");
 }
 
-// Host side of kAbortBigBucket: sort each oversized bucket with CUB, fold it.
-void big_buckets(svx_map* m, svx_scan* s, const FrameParams& f) {
+// Host side of kAbortBigBucket: each oversized bucket is ordered by a CUB pair
+// sort (key, record index) on the device and folded per voxel segment.
+void big_buckets(svx_map* m) {
     const uint32_t nbig = m->h_ctr[C_FB_BIG];
     std::vector<uint32_t> slots(nbig), cnt(nbig), start(nbig);
     SVX_CUDA(cudaMemcpy(slots.data(), m->bigslots, 4 * nbig, cudaMemcpyDeviceToHost));
@@ -1081,21 +1175,29 @@ void big_buckets(svx_map* m, svx_scan* s, const FrameParams& f) {
         SVX_CUDA(cudaMemcpy(&cnt[i], m->fbcnt + slots[i], 4, cudaMemcpyDeviceToHost));
         SVX_CUDA(cudaMemcpy(&start[i], m->fbstart + slots[i], 4, cudaMemcpyDeviceToHost));
     }
-    const PixCache* cache = reinterpret_cast<const PixCache*>(s->pixcache.p);
-    Term* terms = reinterpret_cast<Term*>(m->terms.p);
-    DevBuf<uint32_t> tmp;
+    const FbRec* bucket = reinterpret_cast<const FbRec*>(m->bucket.p);
+    DevBuf<uint32_t> buf;
     for (uint32_t i = 0; i < nbig; ++i) {
-        tmp.alloc(cnt[i]);
-        sort_u32(m, m->bucket.p + start[i], tmp.p, cnt[i]);
-        k_fb_terms_sorted<<<grid_for(cnt[i]), kThreads, 0, m->stream>>>(
-            f, cache, hash_view(m), tsdf_base(m), slots[i], tmp.p, cnt[i], terms + start[i]);
-        k_fb_fold_sorted<<<grid_for(cnt[i]), kThreads, 0, m->stream>>>(
-            hash_view(m), tsdf_base(m), slots[i], tmp.p, cnt[i], terms + start[i], m->d_ctr);
+        const uint32_t n = cnt[i];
+        buf.alloc(4ull * n);
+        uint32_t *k_in = buf.p, *k_out = buf.p + n, *i_in = buf.p + 2ull * n, *i_out = buf.p + 3ull * n;
+        k_fb_extract<<<grid_for(n), kThreads, 0, m->stream>>>(bucket + start[i], n, k_in, i_in);
+        size_t bytes = 0;
+        SVX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k_in, k_out, i_in, i_out, int(n), 0, 32,
+                                                 m->stream));
+        m->sort_tmp.alloc(bytes ? bytes : 1);
+        SVX_CUDA(cub::DeviceRadixSort::SortPairs(m->sort_tmp.p, bytes, k_in, k_out, i_in, i_out, int(n),
+                                                 0, 32, m->stream));
+        k_fb_fold_sorted<<<grid_for(n), kThreads, 0, m->stream>>>(
+            hash_view(m), tsdf_base(m), slots[i], bucket + start[i], k_out, i_out, n, m->d_ctr);
         count_launch(2);
         SVX_CUDA(cudaMemsetAsync(m->fbcnt + slots[i], 0, 4, m->stream));
-        SVX_CUDA(cudaStreamSynchronize(m->stream));
+        SVX_CUDA(cudaMemsetAsync(m->fbclaim + slots[i], 0, 4, m->stream));
+        SVX_CUDA(cudaMemsetAsync(m->fbfill + slots[i], 0, 4, m->stream));
+        SVX_CUDA(cudaMemsetAsync(m->fbstart + slots[i], 0xFF, 4, m->stream));
     }
-    tmp.release();
+    SVX_CUDA(cudaStreamSynchronize(m->stream));
+    buf.release();
 }
 
 }  // namespace
@@ -1111,8 +1213,11 @@ unsigned persistent_grid(int device) {
 void reset_frame_state(svx_map* m) {
     SVX_CUDA(cudaMemsetAsync(m->vmask, 0, sizeof(uint32_t) * 32ull * m->cap, m->stream));
     SVX_CUDA(cudaMemsetAsync(m->fbcnt, 0, sizeof(uint32_t) * m->cap, m->stream));
+    SVX_CUDA(cudaMemsetAsync(m->fbclaim, 0, sizeof(uint32_t) * m->cap, m->stream));
+    SVX_CUDA(cudaMemsetAsync(m->fbfill, 0, sizeof(uint32_t) * m->cap, m->stream));
+    SVX_CUDA(cudaMemsetAsync(m->fbstart, 0xFF, sizeof(uint32_t) * m->cap, m->stream));
     for (int c : {C_TOUCHED, C_UPDATED, C_RECORDS, C_RAYS, C_DROPPED, C_TIES, C_FB_BLOCKS,
-                  C_FB_VOXELS, C_FB_BIG, C_ABORT, C_VOXLIST, C_BUCKET_TOP, C_DONE})
+                  C_FB_VOXELS, C_FB_BIG, C_ABORT, C_VOXLIST, C_BUCKET_TOP, C_DONE, C_TOUCHED_PREV})
         m->h_ctr[c] = 0;
     m->h_ctr[C_BLOCKS] = m->h_ctr[C_BLOCKS_BEFORE] = uint32_t(m->n_blocks);
     m->h_ctr[C_MAPPED] = uint32_t(m->mapped_blocks);
@@ -1159,7 +1264,7 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
     // (an exhausted headroom costs one abort + resume; over-mapping costs physical
     // memory and cuMemCreate time, so size it from the recent new-block rate)
     const uint64_t head = std::max<uint64_t>(32768, uint64_t(2.0 * m->new_ema * n));
-    ensure_blocks(m, m->n_blocks + head);
+    ensure_blocks(m, m->n_blocks + head, 4 * head);
     std::vector<FrameParams> fps(n);
     std::vector<int> parity(n, 0);
     std::vector<char> launched(n, 0);
@@ -1175,7 +1280,7 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
                     parity[i] = j.scan->parity;
                     launch_project(j.scan, j.pts, j.n, j.stride, j.pose);
                 }
-                fps[i] = make_params(m, j.scan, j.pose, cfg);
+                fps[i] = make_params(m, j.scan, j.pose, cfg, uint32_t(m->tsdf_frames + i));
                 launched[i] = 1;
             }
             launch_stages(m, j.scan, fps[i], from, m->outs.p + i);
@@ -1209,41 +1314,43 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
             m->n_blocks = before;
             capacity_path(m, fps[fa], s, before);
         }
-        int stage = 4;
-        if (abort & kAbortRecords) {
-            // grow the record buffer and re-run the band kernel of this frame with a
-            // fresh stamp: masks are idempotent (OR), inserted keys are found again
+        int stage = kStageReport;
+        const uint32_t par = fps[fa].parity;
+        if (abort & (kAbortRecords | kAbortVoxList)) {
+            // grow the buffer and re-run the band kernel of this frame with a fresh
+            // stamp, after clearing what its first run left: this frame's mask
+            // words (so every voxel is listed again), fallback counts, counters
             ensure_blocks(m, uint64_t(m->h_ctr[C_BLOCKS]) + head);
-            m->rec_cap = std::max<uint32_t>(m->h_ctr[C_RECORDS] + (m->h_ctr[C_RECORDS] >> 1),
-                                            m->rec_cap * 2);
-            m->records.alloc(m->rec_cap);
-            m->bucket.alloc(m->rec_cap);
-            m->terms.alloc(size_t(m->rec_cap) * sizeof(Term));
-            fps[fa].rec_cap = m->rec_cap;
-            k_reset_fb<<<64, kThreads, 0, m->stream>>>(m->touched, m->fbcnt, m->d_ctr);
+            if (abort & kAbortRecords) {
+                m->rec_cap = std::max<uint32_t>(m->h_ctr[C_RECORDS] + (m->h_ctr[C_RECORDS] >> 1),
+                                                m->rec_cap * 2);
+                m->records.alloc(2ull * m->rec_cap);
+                m->bucket.alloc(2ull * m->rec_cap);
+                fps[fa].rec_cap = m->rec_cap;
+            }
+            if (abort & kAbortVoxList) {
+                m->vox_cap = uint32_t(std::min<uint64_t>(uint64_t(m->h_ctr[C_VOXLIST]) * 2, 0xFFFFFFF0ull));
+                m->vlist.alloc(m->vox_cap);
+                fps[fa].vox_cap = m->vox_cap;
+            }
+            k_reset_fb<<<256, kThreads, 0, m->stream>>>(m->touched + uint64_t(par) * m->cap, m->fbcnt,
+                                                        m->vmask, par, m->d_ctr);
             count_launch();
+            // blocks created by the first run are found again (not created): zero them all here
+            launch_zero_blocks(m, before, uint64_t(m->h_ctr[C_BLOCKS]) - before);
             fps[fa].frame_serial = ++m->frame_serial;
-            put_ctr(m, C_RECORDS, 0);
-            put_ctr(m, C_TOUCHED, 0);
-            stage = 0;
+            for (int c : {C_RECORDS, C_TOUCHED, C_VOXLIST}) put_ctr(m, c, 0);
+            stage = kStageBand;
         } else if (abort & kAbortPool) {
+            // the band ran to completion; blocks beyond the mapped pool were not
+            // zero-filled: map more, zero all of the frame's new blocks, fold
             ensure_blocks(m, uint64_t(m->h_ctr[C_BLOCKS]) + head);
-            stage = 1;
-        } else if (abort & kAbortVoxList) {
-            // the compaction re-runs from the (untouched) masks... which it already
-            // cleared: rebuild the list by re-running the band kernel instead
-            m->vox_cap = uint32_t(std::min<uint64_t>(uint64_t(m->h_ctr[C_VOXLIST]) * 2, 0xFFFFFFF0ull));
-            m->vlist.alloc(m->vox_cap);
-            fps[fa].vox_cap = m->vox_cap;
-            k_reset_fb<<<64, kThreads, 0, m->stream>>>(m->touched, m->fbcnt, m->d_ctr);
-            count_launch();
-            fps[fa].frame_serial = ++m->frame_serial;
-            for (int c : {C_RECORDS, C_TOUCHED, C_VOXLIST, C_BUCKET_TOP, C_FB_BLOCKS}) put_ctr(m, c, 0);
-            stage = 0;
+            launch_zero_blocks(m, before, uint64_t(m->h_ctr[C_BLOCKS]) - before);
+            stage = kStageFold;
         } else if (abort & kAbortBigBucket) {
-            big_buckets(m, s, fps[fa]);
+            big_buckets(m);
             put_ctr(m, C_DONE, 0);
-            stage = 4;
+            stage = kStageReport;
         }
         put_ctr(m, C_ABORT, 0);
         put_ctr(m, C_MAPPED, uint32_t(m->mapped_blocks));

@@ -39,8 +39,9 @@ for prof in (True,) * 10:
         e1.synchronize()
         p = s.profile_read().as_dict() if prof else {"ms": {}}
         ksum = sum(p["ms"].values())
+        groups = " ".join(f"{k}={1e3 * v / batch:.1f}" for k, v in p["ms"].items())
         print(f"prof={prof} frames {a}-{b}: call {1e6 * (t1 - t0) / batch:.1f} us/frame, events "
               f"{1e3 * e0.elapsed_time(e1) / batch:.1f} us/frame, kernel groups {1e3 * ksum / batch:.1f}"
-              f" us/frame, host enqueue {1e3 * p.get('host_enqueue_ms', 0) / batch:.1f} us/frame,"
+              f" us/frame [{groups}], host enqueue {1e3 * p.get('host_enqueue_ms', 0) / batch:.1f} us/frame,"
               f" blocks {s.block_count()} aborts {p.get('aborts')} resume {p.get('host_resume_ms', 0):.1f} ms map {p.get('host_map_ms', 0):.1f} ms")
         f = b
