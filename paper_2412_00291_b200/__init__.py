@@ -28,7 +28,8 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libsvx_b200.so")
+# SVX_LIB: an alternative build of the same library (kernel-variant experiments)
+LIB_PATH = os.environ.get("SVX_LIB") or os.path.join(_HERE, "lib", "libsvx_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "svx.h")
 
 # ----------------------------------------------------------------- errors

@@ -303,6 +303,14 @@ __device__ inline uint32_t warp_agg_inc(uint32_t* ctr) {
     return base + __popc(active & ((1u << lane) - 1u));
 }
 
+// Programmatic dependent launch (PDL): frame kernels are launched so that the
+// next one can be scheduled while the previous one drains. pdl_wait() blocks
+// until the previous grid has completed and its writes are visible (a no-op for
+// a normal launch); pdl_trigger() lets the next grid start launching once every
+// CTA of this grid has passed it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // CTA-uniform read of the abort word (bits in `mask`): kernels with barriers must
 // not let their threads disagree about it (another CTA may set it meanwhile).
 __device__ inline bool cta_aborted(const uint32_t* ctr, uint32_t mask = 0xFFFFFFFFu) {

@@ -205,6 +205,23 @@ struct ProfMark {
 };
 void prof_resolve(svx_map* m);
 
+// Launch with programmatic stream serialization (see pdl_wait in svx_common.cuh).
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t stream,
+                       Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SVX_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
 inline svx_tsdf_voxel* tsdf_base(svx_map* m) {
     return static_cast<svx_tsdf_voxel*>(m->tsdf_pool.base());
 }

@@ -40,6 +40,8 @@ k_project_points(const T* __restrict__ pts, uint64_t n, int stride, Model m,
                  unsigned long long* __restrict__ pixkey, uint8_t* __restrict__ tie,
                  unsigned long long* __restrict__ ties, uint32_t tie_cap,
                  uint32_t* __restrict__ ctr) {
+    pdl_wait();
+    pdl_trigger();
     if (ctr[C_ABORT]) return;
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -110,6 +112,8 @@ k_finish_pixels(const T* __restrict__ pts, int stride, const unsigned long long*
                 uint8_t* __restrict__ valid, uint8_t* __restrict__ tie,
                 const unsigned long long* __restrict__ ties, uint32_t tie_cap,
                 uint8_t* __restrict__ rowdist, const uint32_t* __restrict__ ctr) {
+    pdl_wait();
+    pdl_trigger();
     if (ctr[C_ABORT]) return;
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= uint32_t(W) * H) return;
@@ -195,14 +199,13 @@ void launch_project_t(svx_scan* s, const T* d_pts, uint64_t n, int stride, const
     ProfMark pm(m, SVX_K_PROJECT);
     m->prof_acc.points += n;
     if (n) {
-        k_project_points<<<grid_for(n), kThreads, 0, m->stream>>>(d_pts, n, stride, s->dm, cur,
-                                                                    s->tie.p, s->lexkey.p,
-                                                                    tie_cap, m->d_ctr);
+        launch_pdl(k_project_points<T>, grid_for(n), kThreads, m->stream, d_pts, n, stride, s->dm, cur,
+                   s->tie.p, s->lexkey.p, tie_cap, m->d_ctr);
         count_launch();
     }
-    k_finish_pixels<<<grid_for(P), kThreads, 0, m->stream>>>(
-        d_pts, stride, cur, nxt, s->dirs.p, pose, s->dm.W, s->dm.H, 1, s->depth.p, s->height.p,
-        s->normals.p, s->valid.p, s->tie.p, s->lexkey.p, tie_cap, s->rowdist.p, m->d_ctr);
+    launch_pdl(k_finish_pixels<T>, grid_for(P), kThreads, m->stream, d_pts, stride, cur, nxt, s->dirs.p,
+               pose, s->dm.W, s->dm.H, 1, s->depth.p, s->height.p, s->normals.p, s->valid.p, s->tie.p,
+               s->lexkey.p, tie_cap, s->rowdist.p, m->d_ctr);
     count_launch();
     SVX_CUDA(cudaGetLastError());
     s->rowdist_fresh = true;

@@ -151,6 +151,8 @@ constexpr int kRmax = kRowDistMax;
 __global__ void __launch_bounds__(kThreads)
 k_row_dist(const float* __restrict__ depth, int W, int H, uint8_t* __restrict__ hd,
            const uint32_t* __restrict__ ctr) {
+    pdl_wait();
+    pdl_trigger();
     if (ctr[C_ABORT]) return;
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= uint32_t(W) * H) return;
@@ -488,6 +490,8 @@ k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __re
                uint32_t* __restrict__ fbcnt, FbRec* __restrict__ rec,
                svx_tsdf_voxel* __restrict__ pool, uint8_t* __restrict__ dirty,
                unsigned long long* __restrict__ vlist, uint32_t* __restrict__ ctr) {
+    pdl_wait();
+    pdl_trigger();
     // pool exhaustion does not stop the band: the frame resumes after its band
     if (cta_aborted(ctr, ~uint32_t(kAbortPool))) return;
     __shared__ unsigned long long lkey[kLocalKeys];
@@ -721,6 +725,8 @@ k_fold(FrameParams f, const float* __restrict__ depth, const PixCache* __restric
        const uint32_t* __restrict__ fbcnt, uint32_t* __restrict__ fbstart,
        uint32_t* __restrict__ fbclaim, uint32_t* __restrict__ fbfill,
        uint32_t* __restrict__ fbslots, FbRec* __restrict__ bucket, uint32_t* __restrict__ ctr) {
+    pdl_wait();
+    pdl_trigger();
     if (ctr[C_ABORT]) return;
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t stride = gridDim.x * blockDim.x;
@@ -844,6 +850,8 @@ k_fb_fold(HashView h, svx_tsdf_voxel* __restrict__ pool, const uint32_t* __restr
           uint32_t* __restrict__ fbclaim, uint32_t* __restrict__ fbfill,
           const FbRec* __restrict__ bucket, uint32_t* __restrict__ bigslots,
           FrameOut* __restrict__ out, uint32_t* __restrict__ ctr) {
+    pdl_wait();
+    pdl_trigger();
     // a big bucket (host-sorted afterwards) must not stop the other buckets
     if (cta_aborted(ctr, ~uint32_t(kAbortBigBucket))) return;
     using Scan = cub::BlockScan<uint32_t, kFbThreads>;
@@ -957,6 +965,8 @@ __global__ void k_fb_fold_sorted(HashView h, svx_tsdf_voxel* __restrict__ pool, 
 }
 
 __global__ void k_frame_end(FrameOut* __restrict__ out, uint32_t* __restrict__ ctr) {
+    pdl_wait();
+    pdl_trigger();
     if (ctr[C_ABORT]) return;
     write_frame_end(out, ctr);
 }
@@ -1070,36 +1080,34 @@ void launch_stages(svx_map* m, svx_scan* s, const FrameParams& f, int from, Fram
     if (from <= kStageBand) {
         ProfMark pm(m, SVX_K_RAYCAST);
         if (!s->rowdist_fresh) {  // host-provided depth: the projection did not build it
-            k_row_dist<<<grid_for(P), kThreads, 0, m->stream>>>(s->depth.p, s->dm.W, s->dm.H,
-                                                                s->rowdist.p, m->d_ctr);
+            launch_pdl(k_row_dist, grid_for(P), kThreads, m->stream, s->depth.p, s->dm.W, s->dm.H,
+                       s->rowdist.p, m->d_ctr);
             count_launch();
             s->rowdist_fresh = true;
         }
         const unsigned tiles = unsigned(((s->dm.W + 31) / 32) * ((s->dm.H + 7) / 8));
-        k_raycast_band<<<tiles, 256, 0, m->stream>>>(
-            f, s->depth.p, s->normals.p, s->valid.p, s->dirs.p, s->rowdist.p,
-            reinterpret_cast<PixCache*>(s->pixcache.p), hv, m->block_keys, m->stamp, touched_cur,
-            m->vmask, m->fbcnt, reinterpret_cast<FbRec*>(m->records.p), tsdf_base(m), m->dirty,
-            m->vlist.p, m->d_ctr);
+        launch_pdl(k_raycast_band, tiles, 256, m->stream, f, s->depth.p, s->normals.p, s->valid.p,
+                   s->dirs.p, s->rowdist.p, reinterpret_cast<PixCache*>(s->pixcache.p), hv, m->block_keys,
+                   m->stamp, touched_cur, m->vmask, m->fbcnt, reinterpret_cast<FbRec*>(m->records.p),
+                   tsdf_base(m), m->dirty, m->vlist.p, m->d_ctr);
         count_launch();
     }
     if (from <= kStageFold) {
         ProfMark pm(m, SVX_K_FOLD);
-        k_fold<<<pg, kThreads, 0, m->stream>>>(f, s->depth.p, cache, m->block_keys, tsdf_base(m),
-                                               m->vlist.p, touched_prev, m->vmask,
-                                               reinterpret_cast<const FbRec*>(m->records.p), m->fbcnt,
-                                               m->fbstart, m->fbclaim, m->fbfill, m->fbslots,
-                                               reinterpret_cast<FbRec*>(m->bucket.p), m->d_ctr);
+        launch_pdl(k_fold, pg, kThreads, m->stream, f, s->depth.p, cache, m->block_keys, tsdf_base(m),
+                   m->vlist.p, touched_prev, m->vmask, reinterpret_cast<const FbRec*>(m->records.p),
+                   m->fbcnt, m->fbstart, m->fbclaim, m->fbfill, m->fbslots,
+                   reinterpret_cast<FbRec*>(m->bucket.p), m->d_ctr);
         count_launch();
     }
     if (from <= kStageFallback) {
         ProfMark pm(m, SVX_K_FALLBACK);
-        k_fb_fold<<<pg / 2, kFbThreads, 0, m->stream>>>(
-            hv, tsdf_base(m), m->fbslots, m->fbcnt, m->fbstart, m->fbclaim, m->fbfill,
-            reinterpret_cast<const FbRec*>(m->bucket.p), m->bigslots, out, m->d_ctr);
+        launch_pdl(k_fb_fold, pg / 2, kFbThreads, m->stream, hv, tsdf_base(m), m->fbslots, m->fbcnt,
+                   m->fbstart, m->fbclaim, m->fbfill, reinterpret_cast<const FbRec*>(m->bucket.p),
+                   m->bigslots, out, m->d_ctr);
         count_launch();
     } else {
-        k_frame_end<<<1, 1, 0, m->stream>>>(out, m->d_ctr);
+        launch_pdl(k_frame_end, 1, 1, m->stream, out, m->d_ctr);
         count_launch();
     }
     SVX_CUDA(cudaGetLastError());
