@@ -229,6 +229,14 @@ svx_status svx_integrate_clouds_device(svx_map* map, svx_scan* scan, const float
                                        const uint64_t* offsets, int32_t stride,
                                        const svx_pose* poses, int32_t n_frames,
                                        const svx_integrator_cfg* cfg, svx_frame_report* reports);
+/* The same sequence with the points in HOST memory (pinned for full overlap): the
+ * points of the next frames are copied to the device on a copy stream while the
+ * current frame integrates (a ring of 4 staged frames) — the per-frame body of
+ * cmd_integrate with its prefetcher (semvox_main.cpp:30-76,121-124) in one call. */
+svx_status svx_integrate_clouds(svx_map* map, svx_scan* scan, const float* points,
+                                const uint64_t* offsets, int32_t stride, const svx_pose* poses,
+                                int32_t n_frames, const svx_integrator_cfg* cfg,
+                                svx_frame_report* reports);
 /* SemanticIntegrator::integrate_labels — semantic_integrator.cpp:91-165, with
  * exact block-level frustum culling (results identical to the O(map) sweep). */
 svx_status svx_integrate_labels(svx_map* map, const svx_label_image* img,

@@ -175,6 +175,8 @@ def _sig(lib: C.CDLL) -> None:
                                     C.POINTER(IntegratorCfg), C.POINTER(FrameReportC)]),
         "svx_integrate_clouds_device": (S, [P, P, P, P, C.c_int32, P, C.c_int32,
                                             C.POINTER(IntegratorCfg), P]),
+        "svx_integrate_clouds": (S, [P, P, P, P, C.c_int32, P, C.c_int32,
+                                     C.POINTER(IntegratorCfg), P]),
         "svx_integrate_labels": (S, [P, C.POINTER(LabelImageC), C.POINTER(SemanticCfg),
                                      C.POINTER(FrameReportC)]),
         "svx_default_integrator_cfg": (None, [C.POINTER(IntegratorCfg)]),
@@ -433,6 +435,19 @@ class VoxelStore:
         _check(lib().svx_integrate_clouds_device(self._h, self.scan(model), C.c_void_p(d_points_ptr),
                                                  _ptr(offs), stride, C.cast(parr, C.c_void_p), n,
                                                  C.byref(cfg.c()), C.cast(reps, C.c_void_p)))
+        return [FrameReport.of(r) for r in reps]
+
+    def integrate_clouds_host(self, model: ProjectionModel, points_ptr: int, offsets: np.ndarray,
+                              stride: int, poses: list, cfg: "IntegratorConfig") -> list:
+        """A sequence of clouds in host memory (pointer; pinned memory overlaps the
+        copies with the integration), one call."""
+        n = len(poses)
+        offs = np.ascontiguousarray(np.asarray(offsets, np.uint64))
+        parr = (PoseC * n)(*poses)
+        reps = (FrameReportC * n)()
+        _check(lib().svx_integrate_clouds(self._h, self.scan(model), C.c_void_p(points_ptr), _ptr(offs),
+                                          stride, C.cast(parr, C.c_void_p), n, C.byref(cfg.c()),
+                                          C.cast(reps, C.c_void_p)))
         return [FrameReport.of(r) for r in reps]
 
     def get_or_allocate_block(self, bc) -> bool:

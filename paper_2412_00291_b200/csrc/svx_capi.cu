@@ -6,6 +6,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <numeric>
@@ -114,6 +115,13 @@ void free_map(svx_map* m) {
     m->like_table.release();
     m->q_keys.release();
     m->q_idx.release();
+    if (m->copy_stream) cudaStreamSynchronize(m->copy_stream);
+    for (int i = 0; i < svx_map::kIngestSlots; ++i) {
+        if (m->ingest_ready[i]) cudaEventDestroy(m->ingest_ready[i]);
+        if (m->ingest_used[i]) cudaEventDestroy(m->ingest_used[i]);
+        m->ingest[i].release();
+    }
+    if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
     if (m->stream && m->own_stream) cudaStreamDestroy(m->stream);
     delete m;
 }
@@ -151,6 +159,9 @@ svx_map* create_map(const svx_map_cfg& cfg, int device) {
         m->fbslots = dmalloc<uint32_t>(m->cap);
         m->bigslots = dmalloc<uint32_t>(m->cap);
         m->rec_cap = 1u << 20;
+        // test hook: tiny buffers exercise the abort-and-resume paths
+        if (const char* e = std::getenv("SVX_TEST_REC_CAP")) m->rec_cap = uint32_t(std::max(1L, std::atol(e)));
+        if (const char* e = std::getenv("SVX_TEST_POOL_HEAD")) m->test_pool_head = uint64_t(std::max(1L, std::atol(e)));
         m->records.alloc(2ull * m->rec_cap);  // 32-byte records: 2 x uint4
         m->bucket.alloc(2ull * m->rec_cap);
         SVX_CUDA(cudaMallocHost(&m->h_ctr, sizeof(uint32_t) * kNumCounters));
@@ -883,6 +894,32 @@ svx_status svx_integrate_clouds_device(svx_map* m, svx_scan* s, const float* d_p
             require(offsets[f + 1] >= offsets[f], SVX_INVALID_ARGUMENT, "offsets must not decrease");
             jobs[f] = FrameJob{s, to_pose(poses[f]), d_points + offsets[f] * stride,
                                offsets[f + 1] - offsets[f], stride, true};
+        }
+        run_frames(m, jobs.data(), n_frames, *cfg, reports);
+        const double ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        for (int32_t f = 0; f < n_frames; ++f) reports[f].elapsed_ms = ms / n_frames;
+    });
+}
+
+svx_status svx_integrate_clouds(svx_map* m, svx_scan* s, const float* points, const uint64_t* offsets,
+                                int32_t stride, const svx_pose* poses, int32_t n_frames,
+                                const svx_integrator_cfg* cfg, svx_frame_report* reports) {
+    return guarded([&] {
+        require(m && s && cfg && reports && (points || n_frames <= 0), SVX_INVALID_ARGUMENT,
+                "null argument");
+        require(s->map == m, SVX_INVALID_ARGUMENT, "scan belongs to another map");
+        require(stride >= 3, SVX_INVALID_ARGUMENT, "point stride must be >= 3");
+        DeviceGuard g(m->device);
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<FrameJob> jobs(size_t(std::max(n_frames, 0)));
+        for (int32_t f = 0; f < n_frames; ++f) {
+            validate_pose(poses[f]);
+            require(offsets[f + 1] >= offsets[f], SVX_INVALID_ARGUMENT, "offsets must not decrease");
+            require(offsets[f + 1] - offsets[f] < (1ull << 32), SVX_INVALID_ARGUMENT,
+                    "too many points in one cloud");
+            jobs[f] = FrameJob{s, to_pose(poses[f]), points + offsets[f] * stride,
+                               offsets[f + 1] - offsets[f], stride, true, true};
         }
         run_frames(m, jobs.data(), n_frames, *cfg, reports);
         const double ms =

@@ -255,6 +255,7 @@ enum Counter : int {
     C_BUCKET_TOP = 23,  // fallback bucket space handed out this frame
     C_DONE = 24,        // CTAs of k_fb_fold finished (last one writes the report)
     C_TOUCHED_PREV = 25,  // blocks touched by the previous frame (their mask words get cleared)
+    C_ABORT_FRAME = 26, // frame serial that raised a pool / big-bucket abort (set before the bit)
     kNumCounters = 32
 };
 
@@ -315,6 +316,25 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // not let their threads disagree about it (another CTA may set it meanwhile).
 __device__ inline bool cta_aborted(const uint32_t* ctr, uint32_t mask = 0xFFFFFFFFu) {
     return __syncthreads_or(threadIdx.x == 0 ? int((ctr[C_ABORT] & mask) != 0) : 0) != 0;
+}
+
+// Raises abort `bit` for the frame `serial` (the frame itself may finish the kernel
+// that raised it; later frames must not run): the frame id is published first.
+__device__ inline void raise_frame_abort(uint32_t* ctr, uint32_t bit, uint32_t serial) {
+    atomicExch(&ctr[C_ABORT_FRAME], serial);
+    __threadfence();
+    atomicOr(&ctr[C_ABORT], bit);
+}
+
+// CTA-uniform abort test that lets the frame that raised `own_bit` continue.
+__device__ inline bool cta_aborted_for(const uint32_t* ctr, uint32_t own_bit, uint32_t serial) {
+    int stop = 0;
+    if (threadIdx.x == 0) {
+        const uint32_t a = __ldcg(&ctr[C_ABORT]);
+        __threadfence();
+        stop = (a & ~own_bit) != 0 || ((a & own_bit) && __ldcg(&ctr[C_ABORT_FRAME]) != serial);
+    }
+    return __syncthreads_or(stop) != 0;
 }
 
 // CTA-wide reservation of n entries per thread in a list whose length lives in

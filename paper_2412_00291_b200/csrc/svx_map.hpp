@@ -19,6 +19,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <exception>
 #include <stdexcept>
 #include <thread>
@@ -160,6 +161,13 @@ struct svx_map {
     size_t h_outs_n = 0;
     uint64_t mapped_blocks = 0;      // host mirror of C_MAPPED
     double new_ema = 0.0;            // moving average of new blocks per frame
+    uint64_t test_pool_head = 0;     // test hook (SVX_TEST_POOL_HEAD): fixed pool headroom
+    // host ingest ring (svx_integrate_clouds): the points of the next frames are
+    // copied on `copy_stream` while the current frame integrates
+    static constexpr int kIngestSlots = 4;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ingest_ready[kIngestSlots] = {}, ingest_used[kIngestSlots] = {};
+    svx::DevBuf<float> ingest[kIngestSlots];
     svx::DevBuf<uint64_t> q_keys;    // scratch of host block queries (find / insert)
     svx::DevBuf<uint32_t> q_idx;
     svx::DevBuf<uint32_t> cand;      // semantic candidate blocks
@@ -220,6 +228,15 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStre
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     SVX_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+    static const bool debug_sync = std::getenv("SVX_DEBUG_SYNC") != nullptr;
+    if (debug_sync) {  // debugging aid: attribute a device fault to its kernel
+        const cudaError_t e = cudaStreamSynchronize(stream);
+        if (e != cudaSuccess) {
+            const char* name = "?";
+            cudaFuncGetName(&name, reinterpret_cast<const void*>(kernel));
+            throw Error(SVX_CUDA, std::string("kernel ") + name + ": " + cudaGetErrorString(e));
+        }
+    }
 }
 
 inline svx_tsdf_voxel* tsdf_base(svx_map* m) {
@@ -240,10 +257,11 @@ void launch_normals(svx_scan* s);
 struct FrameJob {
     svx_scan* scan;
     Pose pose;
-    const float* pts;  // device pointer (when project)
+    const float* pts;  // device pointer (when project); HOST pointer when host_ingest
     uint64_t n;
     int stride;
     bool project;
+    bool host_ingest = false;  // pts are in host memory: staged through the ingest ring
 };
 // Runs the frames back to back on the map stream, synchronising once at the end
 // (plus once per abort/resume, rare). Fills one report per frame.

@@ -34,6 +34,7 @@
 #include <math_constants.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <chrono>
 #include <vector>
 
@@ -407,7 +408,7 @@ __device__ inline SlotRef find_or_insert(const FrameParams& f, HashView h,
         __threadfence();
         atomicExch(&h.vals[r.slot], r.idx);
         if (r.idx >= f.max_blocks) atomicOr(&ctr[C_ABORT], kAbortCapacity);
-        else if (r.idx >= ctr[C_MAPPED]) atomicOr(&ctr[C_ABORT], kAbortPool);
+        else if (r.idx >= ctr[C_MAPPED]) raise_frame_abort(ctr, kAbortPool, f.frame_serial);
     } else {
         r.idx = block_index(h, r.slot);
     }
@@ -492,8 +493,9 @@ k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __re
                unsigned long long* __restrict__ vlist, uint32_t* __restrict__ ctr) {
     pdl_wait();
     pdl_trigger();
-    // pool exhaustion does not stop the band: the frame resumes after its band
-    if (cta_aborted(ctr, ~uint32_t(kAbortPool))) return;
+    // pool exhaustion raised by this frame does not stop its band: the frame
+    // resumes after its band
+    if (cta_aborted_for(ctr, kAbortPool, f.frame_serial)) return;
     __shared__ unsigned long long lkey[kLocalKeys];
     __shared__ uint32_t lslot[kLocalKeys];
     __shared__ uint32_t lidx[kLocalKeys];
@@ -849,11 +851,11 @@ k_fb_fold(HashView h, svx_tsdf_voxel* __restrict__ pool, const uint32_t* __restr
           uint32_t* __restrict__ fbcnt, uint32_t* __restrict__ fbstart,
           uint32_t* __restrict__ fbclaim, uint32_t* __restrict__ fbfill,
           const FbRec* __restrict__ bucket, uint32_t* __restrict__ bigslots,
-          FrameOut* __restrict__ out, uint32_t* __restrict__ ctr) {
+          FrameOut* __restrict__ out, uint32_t serial, uint32_t* __restrict__ ctr) {
     pdl_wait();
     pdl_trigger();
-    // a big bucket (host-sorted afterwards) must not stop the other buckets
-    if (cta_aborted(ctr, ~uint32_t(kAbortBigBucket))) return;
+    // a big bucket (host-sorted afterwards) of this frame must not stop its other buckets
+    if (cta_aborted_for(ctr, kAbortBigBucket, serial)) return;
     using Scan = cub::BlockScan<uint32_t, kFbThreads>;
     constexpr int kPer = kBlockVoxels / kFbThreads;  // voxels per thread in the scan
     __shared__ typename Scan::TempStorage scan_tmp;
@@ -871,10 +873,18 @@ k_fb_fold(HashView h, svx_tsdf_voxel* __restrict__ pool, const uint32_t* __restr
         if (cnt > uint32_t(kFbMax)) {
             if (threadIdx.x == 0) {
                 bigslots[atomicAdd(&ctr[C_FB_BIG], 1u)] = slot;
-                atomicOr(&ctr[C_ABORT], kAbortBigBucket);
+                raise_frame_abort(ctr, kAbortBigBucket, serial);
             }
             continue;
         }
+#ifdef SVX_DEBUG_CHECKS
+        if (threadIdx.x == 0 && (start == kInvalid || slot > h.mask || start + cnt > ctr[C_BUCKET_TOP] ||
+                                 h.vals[slot] == kInvalid)) {
+            printf("k_fb_fold: t %u/%u slot %u cnt %u start %u top %u val %u serial %u\n", t, nb, slot, cnt,
+                   start, ctr[C_BUCKET_TOP], h.vals[slot], serial);
+            __trap();
+        }
+#endif
         const FbRec* bk = bucket + start;
         for (int v = threadIdx.x; v < kBlockVoxels; v += kFbThreads) seg_cnt[v] = 0u;
         __syncthreads();
@@ -1104,7 +1114,7 @@ void launch_stages(svx_map* m, svx_scan* s, const FrameParams& f, int from, Fram
         ProfMark pm(m, SVX_K_FALLBACK);
         launch_pdl(k_fb_fold, pg / 2, kFbThreads, m->stream, hv, tsdf_base(m), m->fbslots, m->fbcnt,
                    m->fbstart, m->fbclaim, m->fbfill, reinterpret_cast<const FbRec*>(m->bucket.p),
-                   m->bigslots, out, m->d_ctr);
+                   m->bigslots, out, f.frame_serial, m->d_ctr);
         count_launch();
     } else {
         launch_pdl(k_frame_end, 1, 1, m->stream, out, m->d_ctr);
@@ -1252,6 +1262,9 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
             throw Error(SVX_INVALID_ARGUMENT, "non-projective mode needs a normal image");
     }
     m->outs.alloc(size_t(n));
+    // frame reports start "not done": the resume logic finds the aborted frame as the
+    // first report without ok (stale reports of an earlier batch must not count)
+    SVX_CUDA(cudaMemsetAsync(m->outs.p, 0, sizeof(FrameOut) * size_t(n), m->stream));
     if (m->h_outs_n < size_t(n)) {
         if (m->h_outs) cudaFreeHost(m->h_outs);
         SVX_CUDA(cudaMallocHost(&m->h_outs, sizeof(FrameOut) * n));
@@ -1271,22 +1284,59 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
     // pool headroom for the whole batch (an overflow aborts and resumes below)
     // (an exhausted headroom costs one abort + resume; over-mapping costs physical
     // memory and cuMemCreate time, so size it from the recent new-block rate)
-    const uint64_t head = std::max<uint64_t>(32768, uint64_t(2.0 * m->new_ema * n));
+    const uint64_t head = m->test_pool_head ? m->test_pool_head
+                                            : std::max<uint64_t>(32768, uint64_t(2.0 * m->new_ema * n));
     ensure_blocks(m, m->n_blocks + head, 4 * head);
     std::vector<FrameParams> fps(n);
     std::vector<int> parity(n, 0);
     std::vector<char> launched(n, 0);
+    // host ingest ring: frame i's points go to slot i % R on the copy stream, at most
+    // R - 1 frames ahead of the frame being launched; a slot is refilled only after
+    // the projection of the frame that used it (event ingest_used)
+    constexpr int R = svx_map::kIngestSlots;
+    const bool ingest = jobs[0].host_ingest;
+    if (ingest) {
+        if (!m->copy_stream) {
+            SVX_CUDA(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking));
+            for (int r = 0; r < R; ++r) {
+                SVX_CUDA(cudaEventCreateWithFlags(&m->ingest_ready[r], cudaEventDisableTiming));
+                SVX_CUDA(cudaEventCreateWithFlags(&m->ingest_used[r], cudaEventDisableTiming));
+            }
+        }
+        uint64_t most = 1;
+        for (int i = 0; i < n; ++i) most = std::max<uint64_t>(most, jobs[i].n * uint64_t(jobs[i].stride));
+        for (int r = 0; r < R; ++r) {
+            m->ingest[r].alloc(most);
+            SVX_CUDA(cudaEventRecord(m->ingest_used[r], m->stream));
+        }
+    }
     int f0 = 0, stage0 = 0;
     for (;;) {
         const auto te0 = std::chrono::steady_clock::now();
+        int next_copy = f0;
         for (int i = f0; i < n; ++i) {
             const FrameJob& j = jobs[i];
             const int from = i == f0 ? stage0 : 0;
+            const float* pts = j.pts;
+            if (ingest) {
+                for (; next_copy < n && next_copy < i + R; ++next_copy) {
+                    const FrameJob& c = jobs[next_copy];
+                    const int r = next_copy % R;
+                    SVX_CUDA(cudaStreamWaitEvent(m->copy_stream, m->ingest_used[r], 0));
+                    if (c.n)
+                        SVX_CUDA(cudaMemcpyAsync(m->ingest[r].p, c.pts, 4ull * c.n * c.stride,
+                                                 cudaMemcpyHostToDevice, m->copy_stream));
+                    SVX_CUDA(cudaEventRecord(m->ingest_ready[r], m->copy_stream));
+                }
+                SVX_CUDA(cudaStreamWaitEvent(m->stream, m->ingest_ready[i % R], 0));
+                pts = m->ingest[i % R].p;
+            }
             if (!launched[i] || (i > f0)) {
                 if (j.project) {
                     if (launched[i]) j.scan->parity = parity[i];
                     parity[i] = j.scan->parity;
-                    launch_project(j.scan, j.pts, j.n, j.stride, j.pose);
+                    launch_project(j.scan, pts, j.n, j.stride, j.pose);
+                    if (ingest) SVX_CUDA(cudaEventRecord(m->ingest_used[i % R], m->stream));
                 }
                 fps[i] = make_params(m, j.scan, j.pose, cfg, uint32_t(m->tsdf_frames + i));
                 launched[i] = 1;
@@ -1299,10 +1349,17 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
         SVX_CUDA(cudaMemcpyAsync(m->h_outs, m->outs.p, sizeof(FrameOut) * n,
                                  cudaMemcpyDeviceToHost, m->stream));
         sync_counters(m);
+        if (ingest) SVX_CUDA(cudaStreamSynchronize(m->copy_stream));
         const uint32_t abort = m->h_ctr[C_ABORT];
         if (!abort) break;
         const auto tr0 = std::chrono::steady_clock::now();
         for (int b = 0; b < 8; ++b) m->prof_acc.aborts[b] += (abort >> b) & 1u;
+#ifdef SVX_DEBUG_CHECKS
+        std::fprintf(stderr, "abort %#x f0 %d blocks %u before %u mapped %u records %u rec_cap %u touched %u fbb %u top %u\n",
+                     abort, f0, m->h_ctr[C_BLOCKS], m->h_ctr[C_BLOCKS_BEFORE], m->h_ctr[C_MAPPED],
+                     m->h_ctr[C_RECORDS], m->rec_cap, m->h_ctr[C_TOUCHED], m->h_ctr[C_FB_BLOCKS],
+                     m->h_ctr[C_BUCKET_TOP]);
+#endif
         // the first frame of this pass without a report is the one that aborted
         int fa = f0;
         while (fa < n && m->h_outs[fa].ok) ++fa;
