@@ -242,6 +242,14 @@ svx_status svx_integrate_clouds(svx_map* map, svx_scan* scan, const float* point
 svx_status svx_integrate_labels(svx_map* map, const svx_label_image* img,
                                 const svx_semantic_cfg* cfg, svx_frame_report* report);
 
+/* n label images applied in order (as n integrate_labels calls) with one
+ * synchronisation: labels / confidence / prob_tensor of every image are read from
+ * DEVICE memory when ptr_is_device, else copied from the host asynchronously.
+ * An invalid confidence stops the batch with SVX_INVALID_ARGUMENT. */
+svx_status svx_integrate_labels_batch(svx_map* map, const svx_label_image* imgs, int32_t n,
+                                      int32_t ptr_is_device, const svx_semantic_cfg* cfg,
+                                      svx_frame_report* reports);
+
 /* ------------------------------------------------------------ profiling */
 /* Per-kernel device time measured with CUDA events on the map's stream (the
  * launching stream), plus the algorithmic counters the roofline needs

@@ -177,6 +177,7 @@ def _sig(lib: C.CDLL) -> None:
                                             C.POINTER(IntegratorCfg), P]),
         "svx_integrate_clouds": (S, [P, P, P, P, C.c_int32, P, C.c_int32,
                                      C.POINTER(IntegratorCfg), P]),
+        "svx_integrate_labels_batch": (S, [P, P, C.c_int32, C.c_int32, C.POINTER(SemanticCfg), P]),
         "svx_integrate_labels": (S, [P, C.POINTER(LabelImageC), C.POINTER(SemanticCfg),
                                      C.POINTER(FrameReportC)]),
         "svx_default_integrator_cfg": (None, [C.POINTER(IntegratorCfg)]),
@@ -696,6 +697,43 @@ class SemanticIntegrator:
         _check(lib().svx_integrate_labels(self.store.handle, C.byref(li), C.byref(self.cfg.c()),
                                           C.byref(rep)))
         return FrameReport.of(rep)
+
+    def integrate_labels_batch(self, imgs: list, on_device: bool = False) -> list:
+        """Several label images in order with one synchronisation
+        (svx_integrate_labels_batch). With on_device, labels / confidence /
+        prob_tensor are CUDA tensors (or device pointers) holding the same bytes."""
+        K = self.store.cfg.num_labels
+        n = len(imgs)
+        arr = (LabelImageC * n)()
+        keep = []
+
+        def addr(x, dtype):
+            if x is None:
+                return None
+            if on_device:
+                return C.c_void_p(x if isinstance(x, int) else x.data_ptr())
+            a = np.ascontiguousarray(np.asarray(x, dtype).reshape(-1))
+            keep.append(a)
+            return C.c_void_p(a.ctypes.data)
+
+        for i, img in enumerate(imgs):
+            P = img.width * img.height
+            conf = img.confidence if (img.confidence is not None and (
+                on_device or np.asarray(img.confidence).size == P)) else None
+            ten = img.prob_tensor if (img.prob_tensor is not None and (
+                on_device or np.asarray(img.prob_tensor).size == P * K)) else None
+            pc = img.pose if isinstance(img.pose, PoseC) else (
+                img.pose.c() if isinstance(img.pose, Pose) else pose_c(img.pose))
+            arr[i] = LabelImageC(img.width, img.height,
+                                 C.cast(addr(img.labels, np.uint16), C.POINTER(C.c_uint16)),
+                                 C.cast(addr(conf, np.float32), C.POINTER(C.c_float)),
+                                 C.cast(addr(ten, np.float32), C.POINTER(C.c_float)),
+                                 img.fx, img.fy, img.cx, img.cy, pc, img.max_depth)
+        reps = (FrameReportC * n)()
+        _check(lib().svx_integrate_labels_batch(self.store.handle, C.cast(arr, C.c_void_p), n,
+                                                int(on_device), C.byref(self.cfg.c()),
+                                                C.cast(reps, C.c_void_p)))
+        return [FrameReport.of(r) for r in reps]
 
     def take_dirty_blocks(self) -> np.ndarray:
         return self.store.take_dirty_blocks(1)

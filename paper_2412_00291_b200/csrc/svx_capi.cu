@@ -113,6 +113,7 @@ void free_map(svx_map* m) {
     m->conf.release();
     m->tensor.release();
     m->like_table.release();
+    m->sem_out.release();
     m->q_keys.release();
     m->q_idx.release();
     if (m->copy_stream) cudaStreamSynchronize(m->copy_stream);
@@ -937,6 +938,20 @@ svx_status svx_integrate_labels(svx_map* m, const svx_label_image* img,
         run_integrate_labels(m, *img, *cfg, rep);
         rep->elapsed_ms =
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
+svx_status svx_integrate_labels_batch(svx_map* m, const svx_label_image* imgs, int32_t n,
+                                      int32_t ptr_is_device, const svx_semantic_cfg* cfg,
+                                      svx_frame_report* reps) {
+    return guarded([&] {
+        require(m && cfg && reps && (imgs || n <= 0), SVX_INVALID_ARGUMENT, "null argument");
+        DeviceGuard g(m->device);
+        const auto t0 = std::chrono::steady_clock::now();
+        run_integrate_labels_batch(m, imgs, n, ptr_is_device != 0, *cfg, reps);
+        const double ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        for (int32_t i = 0; i < n; ++i) reps[i].elapsed_ms = ms / n;
     });
 }
 

@@ -17,6 +17,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <cstdlib>
@@ -68,6 +69,7 @@ private:
     size_t reserved_ = 0, gran_ = 0;
     std::atomic<size_t> mapped_{0};
     std::thread worker_;
+    std::atomic<bool> worker_done_{true};
     std::exception_ptr worker_err_;
     std::vector<std::pair<CUmemGenericAllocationHandle, size_t>> chunks_;
 };
@@ -76,8 +78,11 @@ template <typename T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
+    // Grows geometrically (x1.5): regrowing frees the old buffer, and cudaFree
+    // synchronises the device, so per-frame growth must stay rare.
     void alloc(size_t count) {
         if (count <= n) return;
+        if (n) count = std::max(count, n + n / 2);
         if (p) cudaFree(p);
         p = nullptr;
         SVX_CUDA(cudaMalloc(&p, count * sizeof(T)));
@@ -174,6 +179,7 @@ struct svx_map {
     svx::DevBuf<uint16_t> lbl;
     svx::DevBuf<float> conf, tensor;
     svx::DevBuf<float> like_table;   // [K+1][K] label -> likelihood at default confidence
+    svx::DevBuf<uint32_t> sem_out;   // per image of a label batch: candidates, updated voxels
     // counters
     uint32_t* d_ctr = nullptr;       // device
     uint32_t* h_ctr = nullptr;       // pinned mirror
@@ -273,6 +279,8 @@ void push_block_counters(svx_map* m);
 unsigned persistent_grid(int device);
 void run_integrate_labels(svx_map* m, const svx_label_image& img, const svx_semantic_cfg& cfg,
                           svx_frame_report* rep);
+void run_integrate_labels_batch(svx_map* m, const svx_label_image* imgs, int n, bool on_device,
+                                const svx_semantic_cfg& cfg, svx_frame_report* reps);
 uint64_t count_observed(svx_map* m);
 void launch_zero_blocks(svx_map* m, uint64_t first, uint64_t count);
 void rebuild_hash(svx_map* m);

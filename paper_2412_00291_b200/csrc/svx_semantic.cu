@@ -123,6 +123,120 @@ __device__ bool occluded_along_ray(const SemParams& sp, HashView h,
     return false;
 }
 
+// The voxel's K class probabilities in registers (compile-time K) or in place.
+template <int KC>
+struct Probs {
+    float v[KC];
+    __device__ inline void load(const float* p) {
+        if constexpr (KC % 4 == 0) {
+#pragma unroll
+            for (int i = 0; i < KC / 4; ++i) {
+                const float4 q = reinterpret_cast<const float4*>(p)[i];
+                v[4 * i] = q.x;
+                v[4 * i + 1] = q.y;
+                v[4 * i + 2] = q.z;
+                v[4 * i + 3] = q.w;
+            }
+        } else if constexpr (KC % 2 == 0) {
+#pragma unroll
+            for (int i = 0; i < KC / 2; ++i) {
+                const float2 q = reinterpret_cast<const float2*>(p)[i];
+                v[2 * i] = q.x;
+                v[2 * i + 1] = q.y;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < KC; ++i) v[i] = p[i];
+        }
+    }
+    __device__ inline void store(float* p) const {
+        if constexpr (KC % 4 == 0) {
+#pragma unroll
+            for (int i = 0; i < KC / 4; ++i)
+                reinterpret_cast<float4*>(p)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        } else if constexpr (KC % 2 == 0) {
+#pragma unroll
+            for (int i = 0; i < KC / 2; ++i) reinterpret_cast<float2*>(p)[i] = make_float2(v[2 * i], v[2 * i + 1]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < KC; ++i) p[i] = v[i];
+        }
+    }
+};
+
+// Likelihood of class k for one pixel (label_to_likelihood / the floored tensor,
+// semantic_integrator.cpp:24-39,130-145), divided by its f32 sum as the
+// reference does. A label likelihood has two distinct values, so two divisions
+// replace K (same quotients).
+struct Like {
+    const float* tp;  // tensor row or nullptr
+    float floor_v, inv_src, lb, lt;
+    int label;
+    float sum;
+    __device__ inline float operator()(int k) const {
+        if (tp) {
+            const float tk = tp[k];
+            return (tk < floor_v ? floor_v : tk) / sum;
+        }
+        return k == label ? lt : lb;
+    }
+};
+
+template <int KC>
+__device__ inline void bayes_step(float* probs, const Like& like, int K, bool use_bayes) {
+    if constexpr (KC > 0) {
+        Probs<KC> p;
+        p.load(probs);
+        if (use_bayes) {  // apply_likelihood (semantic_integrator.cpp:44-52)
+            double z = 0.0;
+#pragma unroll
+            for (int k = 0; k < KC; ++k) {
+                p.v[k] = p.v[k] * like(k);
+                z += double(p.v[k]);
+            }
+            const float inv = float(1.0 / z);
+#pragma unroll
+            for (int k = 0; k < KC; ++k) p.v[k] = p.v[k] * inv;
+        } else {  // apply_latest_argmax (semantic_integrator.cpp:54-59)
+            int best = 0;
+            float bl = like(0);
+            for (int k = 1; k < KC; ++k) {
+                const float lk = like(k);
+                if (lk > bl) {  // tie -> lower id
+                    best = k;
+                    bl = lk;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < KC; ++k) p.v[k] = k == best ? 1.f : 0.f;
+        }
+        p.store(probs);
+    } else {
+        if (use_bayes) {
+            double z = 0.0;
+            for (int k = 0; k < K; ++k) {
+                const float pk = probs[k] * like(k);
+                probs[k] = pk;
+                z += double(pk);
+            }
+            const float inv = float(1.0 / z);
+            for (int k = 0; k < K; ++k) probs[k] = probs[k] * inv;
+        } else {
+            int best = 0;
+            float bl = like(0);
+            for (int k = 1; k < K; ++k) {
+                const float lk = like(k);
+                if (lk > bl) {
+                    best = k;
+                    bl = lk;
+                }
+            }
+            for (int k = 0; k < K; ++k) probs[k] = k == best ? 1.f : 0.f;
+        }
+    }
+}
+
+template <int KC>
 __global__ void __launch_bounds__(kThreads)
 k_sem_update(SemParams sp, HashView h, const uint64_t* __restrict__ block_keys,
              const svx_tsdf_voxel* __restrict__ pool, float* __restrict__ sem,
@@ -135,7 +249,7 @@ k_sem_update(SemParams sp, HashView h, const uint64_t* __restrict__ block_keys,
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     if (ctr[C_ERR_CONF]) return;  // invalid confidence: no voxel is touched
     const uint32_t n_cand = ctr[C_CAND];
-    const int K = sp.K;
+    const int K = KC > 0 ? KC : sp.K;
     uint32_t n_upd = 0;
     for (uint32_t t = warp; t < n_cand; t += nwarps) {
         const uint32_t idx = cand[t];
@@ -174,69 +288,33 @@ k_sem_update(SemParams sp, HashView h, const uint64_t* __restrict__ block_keys,
             for (int i = lane; i < kBlockVoxels * K; i += 32) layer[i] = u0;
             __syncwarp();
         }
-#pragma unroll
+#pragma unroll 1
         for (int j = 0; j < 16; ++j) {
             if (!((pass >> j) & 1u)) continue;
             const int linear = j * 32 + lane;
-            float* probs = sem + (uint64_t(sid) * kBlockVoxels + linear) * K;
             const uint32_t px = pix[j];
-            // likelihood: two closed forms so no K-array lives in registers
-            float base = 0.f, top = 0.f, sum = 0.f;
-            int label = -1;
-            const float* tp = nullptr;
+            Like like{nullptr, sp.floor_v, 0.f, 0.f, 0.f, -1, 0.f};
             if (sp.has_tensor) {
-                tp = tensor + uint64_t(px) * K;
+                like.tp = tensor + uint64_t(px) * K;
                 for (int k = 0; k < K; ++k) {
-                    const float tk = tp[k];
-                    sum += tk < sp.floor_v ? sp.floor_v : tk;
+                    const float tk = like.tp[k];
+                    like.sum += tk < sp.floor_v ? sp.floor_v : tk;
                 }
             } else {
-                // label_to_likelihood (semantic_integrator.cpp:24-39)
+                // label_to_likelihood (semantic_integrator.cpp:24-39): floored, f32 sum in k order
                 const float cf = sp.has_conf ? conf[px] : sp.default_conf;
-                label = int(labels[px]);
-                base = K > 1 ? (1.f - cf) / float(K - 1) : 1.f;
-                top = K > 1 ? cf : 1.f;
+                int label = int(labels[px]);
+                float base = K > 1 ? (1.f - cf) / float(K - 1) : 1.f;
+                float top = K > 1 ? cf : 1.f;
                 if (!(label >= 0 && label < K)) label = -1;
                 base = base < sp.floor_v ? sp.floor_v : base;
                 top = top < sp.floor_v ? sp.floor_v : top;
-                for (int k = 0; k < K; ++k) sum += (k == label) ? top : base;
+                for (int k = 0; k < K; ++k) like.sum += (k == label) ? top : base;
+                like.label = label;
+                like.lb = base / like.sum;
+                like.lt = top / like.sum;
             }
-            if (sp.use_bayes) {
-                // apply_likelihood (semantic_integrator.cpp:44-52)
-                double z = 0.0;
-                for (int k = 0; k < K; ++k) {
-                    float lk;
-                    if (tp) {
-                        const float tk = tp[k];
-                        lk = (tk < sp.floor_v ? sp.floor_v : tk) / sum;
-                    } else {
-                        lk = ((k == label) ? top : base) / sum;
-                    }
-                    const float pk = probs[k] * lk;
-                    probs[k] = pk;
-                    z += double(pk);
-                }
-                const float inv = float(1.0 / z);
-                for (int k = 0; k < K; ++k) probs[k] = probs[k] * inv;
-            } else {
-                // apply_latest_argmax (semantic_integrator.cpp:54-59)
-                int best = 0;
-                float bl = 0.f;
-                for (int k = 0; k < K; ++k) {
-                    float lk;
-                    if (tp) {
-                        const float tk = tp[k];
-                        lk = (tk < sp.floor_v ? sp.floor_v : tk) / sum;
-                    } else {
-                        lk = ((k == label) ? top : base) / sum;
-                    }
-                    if (k == 0 || lk > bl) {  // tie -> lower id
-                        best = k;
-                        bl = lk;
-                    }
-                }
-                for (int k = 0; k < K; ++k) probs[k] = k == best ? 1.f : 0.f;
-            }
+            bayes_step<KC>(sem + (uint64_t(sid) * kBlockVoxels + linear) * K, like, K, sp.use_bayes != 0);
             ++n_upd;
         }
         if (lane == 0) dirty_sem[idx] = 1;
@@ -254,89 +332,153 @@ __global__ void k_check_conf(const float* __restrict__ conf, uint64_t n, uint32_
 
 }  // namespace
 
-void run_integrate_labels(svx_map* m, const svx_label_image& img, const svx_semantic_cfg& cfg,
-                          svx_frame_report* rep) {
-    rep->frame = m->sem_frames++;
-    rep->updated_voxels = 0;
-    rep->new_blocks = 0;
+// A sequence of label images, enqueued back to back on the map stream with one
+// synchronisation at the end (images are applied in order, each seeing the
+// previous ones' updates, exactly as successive integrate_labels calls).
+// Labels / confidences / tensors are read from device memory when on_device,
+// else copied from the host (asynchronously; pinned memory overlaps).
+void run_integrate_labels_batch(svx_map* m, const svx_label_image* imgs, int n, bool on_device,
+                                const svx_semantic_cfg& cfg, svx_frame_report* reps) {
     const int K = m->cfg.num_labels;
-    if (img.width <= 0 || img.height <= 0 || !img.labels)
-        throw Error(SVX_INVALID_ARGUMENT, "label image is empty");
-    const uint64_t P = uint64_t(img.width) * uint64_t(img.height);
-    SemParams sp{};
-    const Pose cp = to_pose(img.pose);
-    sp.w2c = inverse_pose(cp);
-    sp.cam_o = mk(cp.t[0], cp.t[1], cp.t[2]);
-    sp.fx = img.fx;
-    sp.fy = img.fy;
-    sp.cx = img.cx;
-    sp.cy = img.cy;
-    sp.max_depth = img.max_depth;
-    sp.W = img.width;
-    sp.H = img.height;
-    sp.K = K;
-    sp.nu = double(m->cfg.voxel_size);
-    sp.inv_nu = 1.0 / double(m->cfg.voxel_size);
-    sp.occ_floor = -0.5 * double(m->cfg.truncation);
-    sp.use_bayes = cfg.use_bayes != 0;
-    sp.raycast = cfg.occlusion == SVX_OCCLUSION_RAYCAST;
-    sp.has_tensor = img.prob_tensor != nullptr;
-    sp.has_conf = img.confidence != nullptr;
-    sp.floor_v = cfg.likelihood_floor;
-    sp.default_conf = cfg.default_confidence;
-    sp.n_blocks = uint32_t(m->n_blocks);
-    if (!sp.has_tensor && !sp.has_conf &&
-        (cfg.default_confidence < 0.f || cfg.default_confidence > 1.f))
-        throw Error(SVX_INVALID_ARGUMENT, "confidence must be in [0, 1]");
-
-    SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_CAND, 0, 4, m->stream));
-    SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_ERR_CONF, 0, 4, m->stream));
-    SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_SEM_UPDATED, 0, 4, m->stream));
-    m->lbl.alloc(P);
-    SVX_CUDA(cudaMemcpyAsync(m->lbl.p, img.labels, 2 * P, cudaMemcpyHostToDevice, m->stream));
-    if (sp.has_conf) {
-        m->conf.alloc(P);
-        SVX_CUDA(cudaMemcpyAsync(m->conf.p, img.confidence, 4 * P, cudaMemcpyHostToDevice, m->stream));
-        if (!sp.has_tensor) {
-            k_check_conf<<<grid_for(P), kThreads, 0, m->stream>>>(m->conf.p, P, m->d_ctr);
-            count_launch();
-        }
+    for (int i = 0; i < n; ++i) {
+        reps[i].frame = -1;
+        reps[i].updated_voxels = reps[i].new_blocks = 0;
+        if (imgs[i].width <= 0 || imgs[i].height <= 0 || !imgs[i].labels)
+            throw Error(SVX_INVALID_ARGUMENT, "label image is empty");
+        if (!imgs[i].prob_tensor && !imgs[i].confidence &&
+            (cfg.default_confidence < 0.f || cfg.default_confidence > 1.f))
+            throw Error(SVX_INVALID_ARGUMENT, "confidence must be in [0, 1]");
     }
-    if (sp.has_tensor) {
-        m->tensor.alloc(P * K);
-        SVX_CUDA(cudaMemcpyAsync(m->tensor.p, img.prob_tensor, 4 * P * K, cudaMemcpyHostToDevice,
-                                 m->stream));
+    if (n <= 0) return;
+    // staging for host images: every image of the batch gets its own slice
+    uint64_t lbl_n = 0, conf_n = 0, ten_n = 0;
+    for (int i = 0; i < n; ++i) {
+        const uint64_t P = uint64_t(imgs[i].width) * uint64_t(imgs[i].height);
+        lbl_n += P;
+        if (imgs[i].confidence) conf_n += P;
+        if (imgs[i].prob_tensor) ten_n += P * K;
+    }
+    if (!on_device) {
+        m->lbl.alloc(lbl_n);
+        if (conf_n) m->conf.alloc(conf_n);
+        if (ten_n) m->tensor.alloc(ten_n);
     }
     m->cand.alloc(std::max<uint64_t>(m->n_blocks, 1));
+    m->sem_out.alloc(2ull * n);
     // a block owns at most one layer: map as many layers as there are blocks, so the
     // update kernel never outgrows the pool and no mid-pass synchronisation is needed
     ensure_layers(m, m->n_blocks);
-    if (m->n_blocks) {
-        {
-            ProfMark pm(m, SVX_K_SEM_CULL);
-            k_sem_cull<<<grid_for(m->n_blocks), kThreads, 0, m->stream>>>(sp, m->block_keys,
-                                                                          m->cand.p, m->d_ctr);
+    SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_ERR_CONF, 0, 4, m->stream));
+    uint64_t lo = 0, co = 0, to = 0;
+    for (int i = 0; i < n; ++i) {
+        const svx_label_image& img = imgs[i];
+        const uint64_t P = uint64_t(img.width) * uint64_t(img.height);
+        SemParams sp{};
+        const Pose cp = to_pose(img.pose);
+        sp.w2c = inverse_pose(cp);
+        sp.cam_o = mk(cp.t[0], cp.t[1], cp.t[2]);
+        sp.fx = img.fx;
+        sp.fy = img.fy;
+        sp.cx = img.cx;
+        sp.cy = img.cy;
+        sp.max_depth = img.max_depth;
+        sp.W = img.width;
+        sp.H = img.height;
+        sp.K = K;
+        sp.nu = double(m->cfg.voxel_size);
+        sp.inv_nu = 1.0 / double(m->cfg.voxel_size);
+        sp.occ_floor = -0.5 * double(m->cfg.truncation);
+        sp.use_bayes = cfg.use_bayes != 0;
+        sp.raycast = cfg.occlusion == SVX_OCCLUSION_RAYCAST;
+        sp.has_tensor = img.prob_tensor != nullptr;
+        sp.has_conf = img.confidence != nullptr;
+        sp.floor_v = cfg.likelihood_floor;
+        sp.default_conf = cfg.default_confidence;
+        sp.n_blocks = uint32_t(m->n_blocks);
+        const uint16_t* lbl = img.labels;
+        const float* conf = img.confidence;
+        const float* ten = img.prob_tensor;
+        if (!on_device) {
+            SVX_CUDA(cudaMemcpyAsync(m->lbl.p + lo, img.labels, 2 * P, cudaMemcpyHostToDevice, m->stream));
+            lbl = m->lbl.p + lo;
+            lo += P;
+            if (conf) {
+                SVX_CUDA(cudaMemcpyAsync(m->conf.p + co, img.confidence, 4 * P, cudaMemcpyHostToDevice,
+                                         m->stream));
+                conf = m->conf.p + co;
+                co += P;
+            }
+            if (ten) {
+                SVX_CUDA(cudaMemcpyAsync(m->tensor.p + to, img.prob_tensor, 4 * P * K,
+                                         cudaMemcpyHostToDevice, m->stream));
+                ten = m->tensor.p + to;
+                to += P * K;
+            }
+        }
+        if (conf && !ten) {
+            k_check_conf<<<grid_for(P), kThreads, 0, m->stream>>>(conf, P, m->d_ctr);
             count_launch();
         }
-        {
-            ProfMark pm(m, SVX_K_SEM_UPDATE);
-            k_sem_update<<<persistent_grid(m->device), kThreads, 0, m->stream>>>(
-                sp, hash_view(m), m->block_keys, tsdf_base(m), sem_base(m), m->sem_idx, m->cand.p,
-                m->lbl.p, sp.has_conf ? m->conf.p : nullptr, sp.has_tensor ? m->tensor.p : nullptr,
-                m->dirty + m->cfg.max_blocks, m->d_ctr);
-            count_launch();
+        SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_CAND, 0, 4, m->stream));
+        SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_SEM_UPDATED, 0, 4, m->stream));
+        if (m->n_blocks) {
+            {
+                ProfMark pm(m, SVX_K_SEM_CULL);
+                k_sem_cull<<<grid_for(m->n_blocks), kThreads, 0, m->stream>>>(sp, m->block_keys, m->cand.p,
+                                                                              m->d_ctr);
+                count_launch();
+            }
+            {
+                ProfMark pm(m, SVX_K_SEM_UPDATE);
+                // compile-time class counts keep a voxel's probabilities in registers
+                auto kern = &k_sem_update<0>;
+                switch (K) {
+                    case 2: kern = &k_sem_update<2>; break;
+                    case 4: kern = &k_sem_update<4>; break;
+                    case 8: kern = &k_sem_update<8>; break;
+                    case 10: kern = &k_sem_update<10>; break;
+                    case 16: kern = &k_sem_update<16>; break;
+                    case 19: kern = &k_sem_update<19>; break;
+                    case 20: kern = &k_sem_update<20>; break;
+                    case 32: kern = &k_sem_update<32>; break;
+                    default: break;
+                }
+                kern<<<persistent_grid(m->device), kThreads, 0, m->stream>>>(
+                    sp, hash_view(m), m->block_keys, tsdf_base(m), sem_base(m), m->sem_idx, m->cand.p, lbl,
+                    conf, ten, m->dirty + m->cfg.max_blocks, m->d_ctr);
+                count_launch();
+            }
+            SVX_CUDA(cudaGetLastError());
         }
-        SVX_CUDA(cudaGetLastError());
+        // per-image results: candidates and updated voxels
+        SVX_CUDA(cudaMemcpyAsync(m->sem_out.p + 2 * i, m->d_ctr + C_CAND, 4, cudaMemcpyDeviceToDevice,
+                                 m->stream));
+        SVX_CUDA(cudaMemcpyAsync(m->sem_out.p + 2 * i + 1, m->d_ctr + C_SEM_UPDATED, 4,
+                                 cudaMemcpyDeviceToDevice, m->stream));
     }
+    std::vector<uint32_t> outs(2ull * n);
+    SVX_CUDA(cudaMemcpyAsync(outs.data(), m->sem_out.p, 8ull * n, cudaMemcpyDeviceToHost, m->stream));
     sync_counters(m);
-    if (m->h_ctr[C_ERR_CONF]) throw Error(SVX_INVALID_ARGUMENT, "confidence must be in [0, 1]");
-    const uint32_t n_cand = m->h_ctr[C_CAND];
-    rep->updated_voxels = m->h_ctr[C_SEM_UPDATED];
-    m->prof_acc.sem_images += 1;
-    m->prof_acc.sem_candidates += n_cand;
-    m->prof_acc.sem_updated += m->h_ctr[C_SEM_UPDATED];
+    if (m->h_ctr[C_ERR_CONF]) {
+        // the reference numbers a frame before it can throw (semantic_integrator.cpp:93-94)
+        m->sem_frames += n;
+        m->n_layers = m->h_ctr[C_SEM];
+        throw Error(SVX_INVALID_ARGUMENT, "confidence must be in [0, 1]");
+    }
+    for (int i = 0; i < n; ++i) {
+        reps[i].frame = m->sem_frames++;
+        reps[i].updated_voxels = outs[2 * i + 1];
+        m->prof_acc.sem_images += 1;
+        m->prof_acc.sem_candidates += outs[2 * i];
+        m->prof_acc.sem_updated += outs[2 * i + 1];
+    }
     m->prof_acc.sem_new_layers += m->h_ctr[C_SEM] - m->n_layers;
     m->n_layers = m->h_ctr[C_SEM];
+}
+
+void run_integrate_labels(svx_map* m, const svx_label_image& img, const svx_semantic_cfg& cfg,
+                          svx_frame_report* rep) {
+    run_integrate_labels_batch(m, &img, 1, false, cfg, rep);
 }
 
 }  // namespace svx

@@ -79,27 +79,33 @@ void VmmArray::reserve(int device, size_t max_bytes) {
     cu_check(drv().reserve(&base_, reserved_, gran_, 0, 0), "cuMemAddressReserve");
 }
 
+// Maps [mapped_, >= bytes) in chunks of at most kVmmChunk, publishing each chunk
+// as soon as it is mapped (a waiting ensure() can proceed early).
+static constexpr size_t kVmmChunk = size_t(256) << 20;
+
 void VmmArray::grow(size_t bytes) {
-    const size_t cur = mapped_.load(std::memory_order_relaxed);
+    size_t cur = mapped_.load(std::memory_order_relaxed);
     if (bytes <= cur) return;
     if (bytes > reserved_) throw Error(SVX_CAPACITY, "device pool reservation exceeded");
-    // grow by >= 1/4 of the mapped size: mapping time is proportional to the size,
-    // and growth normally runs ahead of need on the helper thread (prefetch)
+    // grow by >= 1/4 of the mapped size: keeps the number of mappings logarithmic
     size_t want = std::max(bytes, cur + cur / 4);
     want = ((want + gran_ - 1) / gran_) * gran_;
     if (want > reserved_) want = reserved_;
-    const size_t add = want - cur;
     const CUmemAllocationProp p = prop_for(device_);
-    CUmemGenericAllocationHandle h;
-    cu_check(drv().create(&h, add, &p, 0), "cuMemCreate");
-    cu_check(drv().map(base_ + cur, add, 0, h, 0), "cuMemMap");
     CUmemAccessDesc acc{};
     acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     acc.location.id = device_;
     acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-    cu_check(drv().set_access(base_ + cur, add, &acc, 1), "cuMemSetAccess");
-    chunks_.push_back({h, add});
-    mapped_.store(want, std::memory_order_release);
+    while (cur < want) {
+        const size_t add = std::min(want - cur, std::max(kVmmChunk, gran_));
+        CUmemGenericAllocationHandle h;
+        cu_check(drv().create(&h, add, &p, 0), "cuMemCreate");
+        cu_check(drv().map(base_ + cur, add, 0, h, 0), "cuMemMap");
+        cu_check(drv().set_access(base_ + cur, add, &acc, 1), "cuMemSetAccess");
+        chunks_.push_back({h, add});
+        cur += add;
+        mapped_.store(cur, std::memory_order_release);
+    }
 }
 
 void VmmArray::join() {
@@ -113,6 +119,10 @@ void VmmArray::join() {
 
 void VmmArray::ensure(size_t bytes) {
     if (bytes <= mapped()) return;
+    // a background growth may already cover it: wait for its chunks, not its end
+    while (worker_.joinable() && !worker_done_.load(std::memory_order_acquire) && mapped() < bytes)
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+    if (bytes <= mapped()) return;
     join();
     grow(bytes);
 }
@@ -120,10 +130,11 @@ void VmmArray::ensure(size_t bytes) {
 void VmmArray::prefetch(size_t bytes) {
     if (bytes > reserved_) bytes = reserved_;
     if (worker_.joinable()) {
-        if (mapped() >= bytes) join();  // the growth in flight is done: reap it
-        return;
+        if (!worker_done_.load(std::memory_order_acquire)) return;  // still mapping
+        join();
     }
     if (bytes <= mapped()) return;
+    worker_done_.store(false, std::memory_order_relaxed);
     worker_ = std::thread([this, bytes] {
         try {
             cudaSetDevice(device_);  // primary context current on this thread
@@ -131,6 +142,7 @@ void VmmArray::prefetch(size_t bytes) {
         } catch (...) {
             worker_err_ = std::current_exception();
         }
+        worker_done_.store(true, std::memory_order_release);
     });
 }
 
@@ -177,7 +189,12 @@ void push_block_counters(svx_map* m) {
 
 void ensure_layers(svx_map* m, uint64_t layers) {
     if (layers > m->cfg.max_blocks) layers = m->cfg.max_blocks;
-    m->sem_pool.ensure(layers * m->layer_bytes);
+    if (layers * m->layer_bytes > m->sem_pool.mapped()) {
+        const auto t0 = std::chrono::steady_clock::now();
+        m->sem_pool.ensure(layers * m->layer_bytes);
+        m->prof_acc.host_map_ms +=
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
     m->sem_pool.prefetch(std::min<uint64_t>(m->cfg.max_blocks, layers + layers / 2) * m->layer_bytes);
 }
 

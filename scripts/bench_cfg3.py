@@ -1,0 +1,131 @@
+"""cfg3 (BASELINE.json configs[2]): cfg2 LiDAR geometry at 0.05 m plus 6 x 1280x720
+semantic label images per frame. Per frame: one TSDF frame + the 6
+label images (svx_integrate_labels_batch) through the C-ABI, timed with CUDA events
+on the map stream, with inputs resident in HBM (gpu) and in pinned host memory
+(e2e: points and label images copied inside the timed region); kernel groups from the map's profiling events; the
+reference's own code (oracle/_ref) on a bounded sample of the same frames.
+Prints one JSON line."""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2412_00291_b200 as svx  # noqa: E402
+from paper_2412_00291_b200 import workload as W  # noqa: E402
+
+n_warm, n_timed = int(os.environ.get("WARM", "5")), int(os.environ.get("FRAMES", "20"))
+n_cpu = int(os.environ.get("CPU_FRAMES", "3"))
+wl = W.make("cfg3", n_warm + n_timed)
+frames = list(range(n_warm + n_timed))
+scans = {i: p.numpy() for p, i in wl.scans()}
+labels = {i: wl.label_images(i) for i in frames}
+cfg = svx.MapConfig(wl.voxel_size, wl.truncation, wl.num_labels, 1 << 22)
+offs = np.zeros(len(frames) + 1, np.uint64)
+offs[1:] = np.cumsum([len(scans[i]) for i in frames])
+flat = np.ascontiguousarray(np.concatenate([scans[i] for i in frames]).astype(np.float32))
+pts_dev = torch.from_numpy(flat).cuda()
+pts_host = torch.from_numpy(flat).pin_memory()
+
+
+def dev_images(i):
+    out = []
+    for li in labels[i]:
+        out.append(svx.LabelImage(li.width, li.height,
+                                  torch.from_numpy(np.asarray(li.labels).view(np.int16).copy()).cuda(),
+                                  li.fx, li.fy, li.cx, li.cy, li.pose, max_depth=li.max_depth))
+    return out
+
+
+def pinned_images(i):
+    out = []
+    for li in labels[i]:
+        t = torch.from_numpy(np.asarray(li.labels).view(np.int16).copy()).pin_memory()
+        out.append(svx.LabelImage(li.width, li.height, t.numpy().view(np.uint16), li.fx, li.fy, li.cx,
+                                  li.cy, li.pose, max_depth=li.max_depth))
+    return out
+
+
+labels_dev = {i: dev_images(i) for i in frames}
+labels_pin = {i: pinned_images(i) for i in frames}
+torch.cuda.synchronize()
+
+
+def leg(device_resident):
+    st = svx.VoxelStore(cfg, 0)
+    si = svx.SemanticIntegrator(st)
+    icfg = svx.IntegratorConfig()
+    ext = torch.cuda.ExternalStream(st.stream_ptr())
+    pts = upd_t = upd_s = 0
+    ms_tot = 0.0
+    for i in frames:
+        if i == n_warm:
+            torch.cuda.synchronize()
+            st.profile_enable(True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ext)
+        a = int(offs[i])
+        rel = offs[i:i + 2] - offs[i]
+        if device_resident:
+            r = st.integrate_clouds_device(wl.model, pts_dev.data_ptr() + 12 * a, rel, 3, [wl.pose(i)], icfg)
+            us = sum(x.updated_voxels for x in si.integrate_labels_batch(labels_dev[i], on_device=True))
+        else:
+            t0 = time.perf_counter()
+            r = st.integrate_clouds_host(wl.model, pts_host.data_ptr() + 12 * a, rel, 3, [wl.pose(i)], icfg)
+            t1 = time.perf_counter()
+            us = sum(x.updated_voxels for x in si.integrate_labels_batch(labels_pin[i]))
+            t2 = time.perf_counter()
+            if os.environ.get("TRACE"):
+                print(f"frame {i}: tsdf {1e3 * (t1 - t0):.2f} ms labels {1e3 * (t2 - t1):.2f} ms", file=sys.stderr)
+        e1.record(ext)
+        e1.synchronize()
+        if i >= n_warm:
+            ms_tot += e0.elapsed_time(e1)
+            pts += len(scans[i])
+            upd_t += r[0].updated_voxels
+            upd_s += us
+    prof = st.profile_read().as_dict()
+    out = {"points_per_s": pts / (ms_tot / 1e3), "voxel_updates_per_s": (upd_t + upd_s) / (ms_tot / 1e3),
+           "ms_per_frame": ms_tot / n_timed, "tsdf_updates_per_frame": upd_t / n_timed,
+           "semantic_updates_per_frame": upd_s / n_timed, "blocks": st.block_count(),
+           "kernel_us_per_frame": {k: 1e3 * v / n_timed for k, v in prof["ms"].items()},
+           "sem_candidates_per_image": prof["sem_candidates"] / max(prof["sem_images"], 1),
+           "host_map_ms_per_frame": prof["host_map_ms"] / n_timed,
+           "host_enqueue_us_per_frame": 1e3 * prof["host_enqueue_ms"] / n_timed}
+    st.close()
+    return out
+
+
+gpu = leg(True)
+e2e = leg(False)
+e2e["h2d_bytes_per_frame"] = int(12 * np.mean(np.diff(offs)) + sum(2 * li.width * li.height
+                                                                   for li in labels[frames[0]]))
+
+cpu = None
+from oracle.bindings import RefMap, ref_available  # noqa: E402  (checker / CPU baseline only)
+if ref_available() and n_cpu:
+    nproc = os.cpu_count() or 1
+    os.environ["SEMVOX_THREADS"] = str(nproc)
+    ref = RefMap(cfg)
+    scfg, icfg = svx.SemanticConfig(), svx.IntegratorConfig()
+    wall = cpts = 0.0
+    used = 0
+    for i in frames[:n_warm + n_cpu]:
+        t0 = time.perf_counter()
+        ref.integrate_cloud(wl.model, scans[i], wl.pose(i), icfg)
+        for li in labels[i]:
+            ref.integrate_labels(li, scfg)
+        dt = time.perf_counter() - t0
+        if i >= n_warm:
+            wall += dt
+            cpts += len(scans[i])
+            used += 1
+    cpu = {"points_per_s": cpts / wall, "cores": nproc, "kind": "reference",
+           "sample": f"{used} cfg3 frames after {n_warm} warm-up frames (map grown identically), "
+                     f"integrate_cloud + 6 x integrate_labels, SEMVOX_THREADS={nproc}"}
+print(json.dumps({"workload": wl.name, "frames_timed": n_timed, "gpu": gpu, "e2e": e2e, "cpu_baseline": cpu,
+                  "speedup_e2e": (e2e["points_per_s"] / cpu["points_per_s"]) if cpu else None}))

@@ -209,3 +209,56 @@ def test_batched_paths_match_per_frame():
             assert aborts.get("records", 0) >= 1, aborts
         st.close()
     ref.close()
+
+
+@pytest.mark.parametrize("variant", ["plain", "conf", "tensor"])
+def test_label_batches_match_single_calls(variant):
+    """svx_integrate_labels_batch (host and device inputs) == one integrate_labels
+    call per image: same reports, same map bytes."""
+    import torch
+    wl = W.make("tiny", 3)
+    cfg = svx.MapConfig(wl.voxel_size, wl.truncation, wl.num_labels, 1 << 16)
+    rng = np.random.default_rng(5)
+
+    def images(i):
+        out = wl.label_images(i)
+        for li in out:
+            P = li.width * li.height
+            if variant == "conf":
+                li.confidence = rng.uniform(0.3, 1.0, P).astype(np.float32)
+            if variant == "tensor":
+                t = rng.uniform(0.0, 1.0, (P, wl.num_labels)).astype(np.float32)
+                li.prob_tensor = t / t.sum(1, keepdims=True)
+        return out
+
+    imgs = {i: images(i) for i in range(3)}
+    maps, reps = [], []
+    for how in ("single", "host", "device"):
+        st = svx.VoxelStore(cfg, 0)
+        ti, si = svx.TsdfIntegrator(st, svx.IntegratorConfig()), svx.SemanticIntegrator(st)
+        rr = []
+        for p, i in wl.scans():
+            ti.integrate_cloud(p.numpy(), wl.pose(i), wl.model)
+            if how == "single":
+                rr += [si.integrate_labels(li) for li in imgs[i]]
+            elif how == "host":
+                rr += si.integrate_labels_batch(imgs[i])
+            else:
+                dev = []
+                for li in imgs[i]:
+                    d = svx.LabelImage(li.width, li.height,
+                                       torch.from_numpy(np.asarray(li.labels).view(np.int16).copy()).cuda(),
+                                       li.fx, li.fy, li.cx, li.cy, li.pose, max_depth=li.max_depth)
+                    if li.confidence is not None:
+                        d.confidence = torch.from_numpy(li.confidence).cuda()
+                    if li.prob_tensor is not None:
+                        d.prob_tensor = torch.from_numpy(li.prob_tensor).cuda()
+                    dev.append(d)
+                torch.cuda.synchronize()
+                rr += si.integrate_labels_batch(dev, on_device=True)
+        maps.append(st.save_bytes())
+        reps.append([(r.frame, r.updated_voxels) for r in rr])
+        st.close()
+    assert reps[0][-1][1] > 0
+    assert reps[1] == reps[0] and reps[2] == reps[0]
+    assert maps[1] == maps[0] and maps[2] == maps[0]
