@@ -352,8 +352,20 @@ def main():
     dom_launches = pd["launches"].get(dom, 1)
     achieved = (alg.get(dom, 0.0) / (dom_ms / 1e3) / 1e9) if dom_ms else 0.0
     B_total = sum(alg.values())
+    # measured DRAM traffic per launch of the dominant kernel (ncu --set full capture of
+    # this build, committed as profiles/ncu_frame_kernels.json by scripts/ncu_summary.py)
+    traffic, traffic_src = None, None
+    kmap = {"raycast": ["k_raycast_band"], "fold": ["k_fold"], "fallback": ["k_fb_fold"],
+            "project": ["k_project_points<float>", "k_finish_pixels<float>"]}
+    try:
+        nk = json.load(open(os.path.join(ROOT, "profiles", "ncu_frame_kernels.json")))
+        traffic = sum(nk["kernels"][k]["dram_bytes_per_launch"] for k in kmap[dom])
+        traffic_src = "profiles/ncu_frame_kernels.json (" + nk["report"] + ")"
+    except Exception:  # noqa: BLE001
+        pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "kernel": dom,
+                "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                "kernel": dom,
                 "kernel_ms_per_launch": dom_ms / max(dom_launches, 1),
                 "alg_bytes_per_launch": alg.get(dom, 0.0) / max(dom_launches, 1),
                 "peak_source": peak_src,

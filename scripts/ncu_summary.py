@@ -1,9 +1,15 @@
-"""Summarise an ncu report: per-kernel duration, throughput, occupancy, pipes, stalls, DRAM bytes."""
+"""Summarise an ncu report: per-kernel duration, throughput, occupancy, pipes, stalls, DRAM bytes.
+
+usage: ncu_summary.py REPORT [JSON_OUT]   (JSON_OUT: per-kernel mean duration and DRAM
+bytes per launch, read by bench.py for the roofline `traffic` field)"""
 import csv
+import json
 import subprocess
 import sys
+from collections import defaultdict
 
 rep = sys.argv[1]
+json_out = sys.argv[2] if len(sys.argv) > 2 else None
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(raw.splitlines()))
 hdr, units = rows[0], rows[1]
@@ -25,6 +31,16 @@ want = {
     "smsp__thread_inst_executed_per_inst_executed.ratio": "thr/warp",
 }
 stall = "smsp__average_warps_issue_stalled_"
+scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1.0, "ms": 1e3,
+         "usecond": 1.0, "nsecond": 1e-3, "msecond": 1e3}
+agg = defaultdict(lambda: {"launches": 0, "us": 0.0, "dram_bytes": 0.0})
+
+
+def num(d, k):
+    u = units[hdr.index(k)]
+    return float(d[k].replace(",", "")) * scale.get(u, 1.0)
+
+
 for r in rows[2:]:
     d = dict(zip(hdr, r))
     name = d["Kernel Name"].split("(")[0].split("::")[-1]
@@ -40,5 +56,14 @@ for r in rows[2:]:
             except ValueError:
                 pass
     st.sort(reverse=True)
+    a = agg[name]
+    a["launches"] += 1
+    a["us"] += num(d, "gpu__time_duration.sum")
+    a["dram_bytes"] += num(d, "dram__bytes_read.sum") + num(d, "dram__bytes_write.sum")
     print(f"== {name}: " + " ".join(out))
     print("   stalls(top): " + ", ".join(f"{n}={v:.1f}" for v, n in st[:6]))
+
+if json_out:
+    res = {k: {"launches": v["launches"], "us_per_launch": v["us"] / v["launches"],
+               "dram_bytes_per_launch": v["dram_bytes"] / v["launches"]} for k, v in agg.items()}
+    json.dump({"report": rep.split("/")[-1], "kernels": res}, open(json_out, "w"), indent=1)
