@@ -722,6 +722,8 @@ svx_status svx_scan_create(svx_map* m, const svx_lidar_model* model, svx_scan** 
             s->lexkey.alloc(3 * P);
             s->pixcache.alloc(48 * P);
             s->rowdist.alloc(P);
+            s->validbits.alloc((P + 31) / 32);
+            SVX_CUDA(cudaMemset(s->validbits.p, 0, 4 * ((P + 31) / 32)));
             SVX_CUDA(cudaMemset(s->pixkey.p, 0xFF, 16 * P));
             SVX_CUDA(cudaMemset(s->pixcache.p, 0, 48 * P));
             SVX_CUDA(cudaMemset(s->depth.p, 0, 4 * P));
@@ -751,6 +753,7 @@ svx_status svx_scan_destroy(svx_scan* s) {
         s->lexkey.release();
         s->pixcache.release();
         s->rowdist.release();
+        s->validbits.release();
         s->points64.release();
         s->tie.release();
         s->pix_of_pt.release();

@@ -312,6 +312,13 @@ __device__ inline uint32_t warp_agg_inc(uint32_t* ctr) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Whether pixel p has a return (depth != 0): one bit per pixel, built with the
+// depth image (k_finish_pixels / k_row_dist). 16 KB at 131k pixels, so the
+// per-visit own-pixel tests hit L1 instead of reading depth[] from L2.
+__device__ __forceinline__ bool pixel_has_return(const uint32_t* __restrict__ bits, uint32_t p) {
+    return (__ldg(&bits[p >> 5]) >> (p & 31)) & 1u;
+}
+
 // CTA-uniform read of the abort word (bits in `mask`): kernels with barriers must
 // not let their threads disagree about it (another CTA may set it meanwhile).
 __device__ inline bool cta_aborted(const uint32_t* ctr, uint32_t mask = 0xFFFFFFFFu) {

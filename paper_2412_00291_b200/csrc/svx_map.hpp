@@ -111,6 +111,7 @@ struct svx_scan {
     int parity = 0;                           // which pixkey half the next projection uses
     svx::DevBuf<uint8_t> pixcache;           // P x 48 B: ray, range, world normal, flags
     svx::DevBuf<uint8_t> rowdist;            // P: row distance to the nearest empty pixel
+    svx::DevBuf<uint32_t> validbits;         // P/32: pixel has a return (bit per pixel)
     bool rowdist_fresh = false;              // rowdist matches depth (set by projection)
     svx::DevBuf<unsigned long long> lexkey;  // P: tie-break scratch
     svx::DevBuf<uint8_t> tie;     // P: possible exact-range tie

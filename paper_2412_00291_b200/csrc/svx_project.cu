@@ -111,13 +111,17 @@ k_finish_pixels(const T* __restrict__ pts, int stride, const unsigned long long*
                 float* __restrict__ height, float* __restrict__ normals,
                 uint8_t* __restrict__ valid, uint8_t* __restrict__ tie,
                 const unsigned long long* __restrict__ ties, uint32_t tie_cap,
-                uint8_t* __restrict__ rowdist, const uint32_t* __restrict__ ctr) {
+                uint8_t* __restrict__ rowdist, uint32_t* __restrict__ validbits,
+                const uint32_t* __restrict__ ctr) {
     pdl_wait();
     pdl_trigger();
     if (ctr[C_ABORT]) return;
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= uint32_t(W) * H) return;
-    const unsigned long long k = pixkey[p];
+    const bool inside = p < uint32_t(W) * H;
+    const unsigned long long k = inside ? pixkey[p] : ~0ull;
+    const uint32_t bits = __ballot_sync(0xFFFFFFFFu, k != ~0ull);  // pixels with a return
+    if ((threadIdx.x & 31) == 0 && inside) validbits[p >> 5] = bits;
+    if (!inside) return;
     next_pixkey[p] = ~0ull;  // the other half is clean for the next projection
     const float d0 = key_depth(k);
     depth[p] = d0;
@@ -205,7 +209,7 @@ void launch_project_t(svx_scan* s, const T* d_pts, uint64_t n, int stride, const
     }
     launch_pdl(k_finish_pixels<T>, grid_for(P), kThreads, m->stream, d_pts, stride, cur, nxt, s->dirs.p,
                pose, s->dm.W, s->dm.H, 1, s->depth.p, s->height.p, s->normals.p, s->valid.p, s->tie.p,
-               s->lexkey.p, tie_cap, s->rowdist.p, m->d_ctr);
+               s->lexkey.p, tie_cap, s->rowdist.p, s->validbits.p, m->d_ctr);
     count_launch();
     SVX_CUDA(cudaGetLastError());
     s->rowdist_fresh = true;

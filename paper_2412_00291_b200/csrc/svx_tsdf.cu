@@ -151,12 +151,15 @@ __device__ inline uint32_t own_pixel(const FrameParams& f, d3 pc) {
 constexpr int kRmax = kRowDistMax;
 __global__ void __launch_bounds__(kThreads)
 k_row_dist(const float* __restrict__ depth, int W, int H, uint8_t* __restrict__ hd,
-           const uint32_t* __restrict__ ctr) {
+           uint32_t* __restrict__ validbits, const uint32_t* __restrict__ ctr) {
     pdl_wait();
     pdl_trigger();
     if (ctr[C_ABORT]) return;
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= uint32_t(W) * H) return;
+    const bool inside = p < uint32_t(W) * H;
+    const uint32_t bits = __ballot_sync(0xFFFFFFFFu, inside && depth[inside ? p : 0] != 0.f);
+    if ((threadIdx.x & 31) == 0 && p < uint32_t(W) * H) validbits[p >> 5] = bits;
+    if (!inside) return;
     const int u = int(p % W);
     const float* row = depth + (p - u);
     int d = 0;
@@ -485,7 +488,8 @@ constexpr int kTileFb = 1024;  // staged fallback visits per tile
 __global__ void __launch_bounds__(kTileU * kTileV, 4)
 k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __restrict__ normals,
                const uint8_t* __restrict__ valid, const double* __restrict__ dirs,
-               const uint8_t* __restrict__ hd, PixCache* __restrict__ cache, HashView h,
+               const uint8_t* __restrict__ hd, const uint32_t* __restrict__ validbits,
+               PixCache* __restrict__ cache, HashView h,
                uint64_t* __restrict__ block_keys, uint32_t* __restrict__ stamp,
                uint32_t* __restrict__ touched, uint32_t* __restrict__ vmask,
                uint32_t* __restrict__ fbcnt, FbRec* __restrict__ rec,
@@ -605,7 +609,7 @@ k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __re
                 const float pz = p0z + kx * f.col[0][2] + ky * f.col[1][2] + kz * f.col[2][2];
                 uint32_t own = pixel_fast(px, py, pz, f.m, f.m.r2_lo, f.m.r2_hi);
                 if (own == kNeedFp64) own = pixel_fp64(xform(f.w2s, voxel_center(x, y, z, f.nu)), f.m);
-                fb = own == kInvalid || depth[own] == 0.f;
+                fb = own == kInvalid || !pixel_has_return(validbits, own);
             }
             if (cur_li < 0) {  // local table full: straight to global state
                 visit_global(f, h, block_keys, stamp, touched, vmask, fbcnt, rec, pool, cache, dirty,
@@ -720,7 +724,7 @@ k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __re
 // frame uses it) and moves the fallback records into per-block buckets; a
 // block's bucket is allocated by the first of its records to arrive.
 __global__ void __launch_bounds__(kThreads)
-k_fold(FrameParams f, const float* __restrict__ depth, const PixCache* __restrict__ cache,
+k_fold(FrameParams f, const uint32_t* __restrict__ validbits, const PixCache* __restrict__ cache,
        const uint64_t* __restrict__ block_keys, svx_tsdf_voxel* __restrict__ pool,
        const unsigned long long* __restrict__ vlist, const uint32_t* __restrict__ touched_prev,
        uint32_t* __restrict__ vmask, const FbRec* __restrict__ rec,
@@ -749,7 +753,7 @@ k_fold(FrameParams f, const float* __restrict__ depth, const PixCache* __restric
         svx_tsdf_voxel vox = load_voxel(vp);
         const d3 c = center_of(key, linear, f.nu);
         const uint32_t own = own_pixel(f, xform(f.w2s, c));
-        if (own == kInvalid || depth[own] == 0.f) continue;  // fallback path
+        if (own == kInvalid || !pixel_has_return(validbits, own)) continue;  // fallback path
         const Term t = measure_term(f, cache, own, c, vox);
         if (t.flags & 1u) {
             Accum acc{0.0, 0.0, 0.0, 0.0, 0.0};
@@ -1091,20 +1095,21 @@ void launch_stages(svx_map* m, svx_scan* s, const FrameParams& f, int from, Fram
         ProfMark pm(m, SVX_K_RAYCAST);
         if (!s->rowdist_fresh) {  // host-provided depth: the projection did not build it
             launch_pdl(k_row_dist, grid_for(P), kThreads, m->stream, s->depth.p, s->dm.W, s->dm.H,
-                       s->rowdist.p, m->d_ctr);
+                       s->rowdist.p, s->validbits.p, m->d_ctr);
             count_launch();
             s->rowdist_fresh = true;
         }
         const unsigned tiles = unsigned(((s->dm.W + 31) / 32) * ((s->dm.H + 7) / 8));
         launch_pdl(k_raycast_band, tiles, 256, m->stream, f, s->depth.p, s->normals.p, s->valid.p,
-                   s->dirs.p, s->rowdist.p, reinterpret_cast<PixCache*>(s->pixcache.p), hv, m->block_keys,
+                   s->dirs.p, s->rowdist.p, s->validbits.p, reinterpret_cast<PixCache*>(s->pixcache.p), hv,
+                   m->block_keys,
                    m->stamp, touched_cur, m->vmask, m->fbcnt, reinterpret_cast<FbRec*>(m->records.p),
                    tsdf_base(m), m->dirty, m->vlist.p, m->d_ctr);
         count_launch();
     }
     if (from <= kStageFold) {
         ProfMark pm(m, SVX_K_FOLD);
-        launch_pdl(k_fold, pg, kThreads, m->stream, f, s->depth.p, cache, m->block_keys, tsdf_base(m),
+        launch_pdl(k_fold, pg, kThreads, m->stream, f, s->validbits.p, cache, m->block_keys, tsdf_base(m),
                    m->vlist.p, touched_prev, m->vmask, reinterpret_cast<const FbRec*>(m->records.p),
                    m->fbcnt, m->fbstart, m->fbclaim, m->fbfill, m->fbslots,
                    reinterpret_cast<FbRec*>(m->bucket.p), m->d_ctr);
