@@ -160,6 +160,13 @@ def test_sweep_sizes_cfg5():
         compare_maps(g.save_bytes(), o.save_bytes())
 
 
+def test_sweep_max_size_cfg5():
+    """The largest scan of the cfg5 sweep (16384 x 128 = 2.1M pixels, every ray hits)."""
+    g, o = _run_pair(W.make("cfg5-16384", 1), svx.IntegratorConfig(), labels=False, max_blocks=1 << 21)
+    st = compare_maps(g.save_bytes(), o.save_bytes())
+    assert st["blocks"] > 1000
+
+
 def test_batched_paths_match_per_frame():
     """The batched entry points (clouds resident in HBM; clouds in pinned host memory,
     staged through the ingest ring) produce the same map, reports and dirty lists as
