@@ -250,6 +250,32 @@ svx_status svx_integrate_labels_batch(svx_map* map, const svx_label_image* imgs,
                                       int32_t ptr_is_device, const svx_semantic_cfg* cfg,
                                       svx_frame_report* reports);
 
+/* ------------------------------------------------------------------ mesh */
+/* extract_mesh / IncrementalMesher::update's re-mesh — proj/src/mesh.cpp:105-287.
+ * Marching cubes over every cell whose base corner lies in one of the given blocks
+ * (bxyz = n*3 block coords; bxyz = NULL meshes every allocated block, as
+ * extract_mesh does). Blocks absent from the map are skipped; duplicates are
+ * ignored. Corners are read from any allocated block. A cell is meshed when its 8
+ * corners have !(weight < min_weight). reserved_unlabeled: the class id of a
+ * trailing "unlabeled" class (its vertices get label 255), or -1. Output order and
+ * values are those of the reference's stitched mesh: vertices in first-appearance
+ * order, faces (i0, i2, i1) per table triangle. The mesh stays on the device until
+ * the next extraction (svx_mesh_read / svx_mesh_device). */
+svx_status svx_mesh_extract(svx_map* map, float min_weight, int32_t reserved_unlabeled,
+                            const int32_t* bxyz, uint64_t n, uint64_t* n_vertices,
+                            uint64_t* n_faces);
+/* Copies the last extracted mesh to host buffers; any pointer may be NULL.
+ * vertices / normals: 3V floats (LabeledMesh::vertices / vertex_normals), labels: V
+ * bytes (255 = kUnlabeled), faces: 3F uint32. */
+svx_status svx_mesh_read(svx_map* map, float* vertices, float* normals, uint8_t* labels,
+                         uint32_t* faces);
+/* Device pointers of the last extracted mesh (valid until the next extraction or
+ * svx_map_destroy), for consumers that stay on the GPU. */
+svx_status svx_mesh_device(svx_map* map, const float** vertices, const float** normals,
+                           const uint8_t** labels, const uint32_t** faces);
+/* VoxelStore::find_block != nullptr for n blocks at once (bxyz = n*3): found[i] = 0/1. */
+svx_status svx_has_blocks(svx_map* map, const int32_t* bxyz, uint64_t n, uint8_t* found);
+
 /* ------------------------------------------------------------ profiling */
 /* Per-kernel device time measured with CUDA events on the map's stream (the
  * launching stream), plus the algorithmic counters the roofline needs

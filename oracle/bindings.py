@@ -68,6 +68,10 @@ def olib():
         L.svxo_observed.argtypes = [_P]
         L.svxo_take_dirty.restype = C.c_uint64
         L.svxo_take_dirty.argtypes = [_P, C.c_int32, _P, C.c_uint64]
+        L.svxo_mesh_extract.argtypes = [_P, C.c_float, C.c_int32, _P, C.c_uint64,
+                                        C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.svxo_mesh_read.argtypes = [_P, _P, _P, _P, _P]
+        L.svxo_mesh_read.restype = None
         L.svxo_last_error.restype = C.c_char_p
         _olib = L
     return _olib
@@ -79,6 +83,8 @@ def rlib():
         L = C.CDLL(REF_SO)
         L.ref_map_create.restype = _P
         L.ref_map_create.argtypes = [C.POINTER(MapCfg)]
+        L.ref_map_load.argtypes = [C.c_char_p]
+        L.ref_map_load.restype = _P
         L.ref_map_destroy.argtypes = [_P]
         L.ref_project.argtypes = [C.POINTER(LidarModel), _P, C.c_uint64, C.c_int32,
                                   C.POINTER(PoseC), _P, _P, _P, _P, C.POINTER(C.c_uint64)]
@@ -98,6 +104,13 @@ def rlib():
         L.ref_lookup.argtypes = [_P, _P, C.c_uint64, _P, _P, _P]
         L.ref_take_dirty.restype = C.c_uint64
         L.ref_take_dirty.argtypes = [_P, C.c_int32, _P, C.c_uint64]
+        L.ref_mesh_extract.argtypes = [_P, C.c_float, C.c_int32, C.POINTER(C.c_uint64),
+                                       C.POINTER(C.c_uint64)]
+        L.ref_mesh_incremental.argtypes = [_P, C.c_float, C.c_int32, _P, C.c_uint64,
+                                           C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), _P,
+                                           C.c_uint64, C.POINTER(C.c_uint64)]
+        L.ref_mesh_read.argtypes = [_P, _P, _P, _P, _P]
+        L.ref_mesh_read.restype = None
         L.ref_last_error.restype = C.c_char_p
         L.ref_worker_count.restype = C.c_int
         L.ref_lidar_spinning.argtypes = [C.c_int32, C.c_int32, C.c_double, C.c_double,
@@ -227,6 +240,14 @@ class OracleMap(_Base):
         if st:
             raise CheckerError(st, olib().svxo_last_error().decode())
 
+    def extract_mesh(self, min_weight=1e-4, reserved=-1, blocks=None):
+        """extract_mesh restated (svx_oracle.c) -> (vertices, normals, labels, faces)."""
+        nv, nf = C.c_uint64(), C.c_uint64()
+        b = None if blocks is None else np.ascontiguousarray(np.asarray(blocks, np.int32).reshape(-1, 3))
+        olib().svxo_mesh_extract(self.h, min_weight, reserved, _ptr(b), 0 if b is None else b.shape[0],
+                                 C.byref(nv), C.byref(nf))
+        return _mesh_arrays(olib().svxo_mesh_read, self.h, nv.value, nf.value)
+
     def take_dirty(self, which):
         cap = max(self.block_count(), 1)  # unique dirty blocks <= allocated blocks
         out = np.zeros((cap, 3), np.int32)
@@ -244,9 +265,22 @@ class RefMap(_Base):
         if not self.h:
             raise CheckerError(1, rlib().ref_last_error().decode())
 
+    @staticmethod
+    def load(path, cfg):
+        """VoxelStore::load of an SVOX1 file (the reference's own reader)."""
+        m = RefMap.__new__(RefMap)
+        m.cfg, m.K = cfg, cfg.num_labels
+        m.h = rlib().ref_map_load(str(path).encode())
+        if not m.h:
+            raise CheckerError(3, rlib().ref_last_error().decode())
+        return m
+
     def __del__(self):
         if getattr(self, "h", None):
-            rlib().ref_map_destroy(self.h)
+            try:
+                rlib().ref_map_destroy(self.h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self.h = None
 
     @staticmethod
@@ -339,6 +373,35 @@ class RefMap(_Base):
         out = np.zeros((cap, 3), np.int32)
         n = rlib().ref_take_dirty(self.h, which, _ptr(out), cap)
         return out[:n]
+
+    def extract_mesh(self, min_weight=1e-4, reserved=-1):
+        """The reference's extract_mesh -> (vertices, normals, labels, faces)."""
+        nv, nf = C.c_uint64(), C.c_uint64()
+        st = rlib().ref_mesh_extract(self.h, min_weight, reserved, C.byref(nv), C.byref(nf))
+        if st:
+            raise CheckerError(st, rlib().ref_last_error().decode())
+        return _mesh_arrays(rlib().ref_mesh_read, self.h, nv.value, nf.value)
+
+    def mesh_incremental(self, dirty, min_weight=1e-4, reserved=-1):
+        """The reference's IncrementalMesher::update -> (mesh arrays, last_remeshed)."""
+        d = np.ascontiguousarray(np.asarray(dirty, np.int32).reshape(-1, 3))
+        nv, nf, nr = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        cap = 8 * d.shape[0] + 1
+        rem = np.zeros((cap, 3), np.int32)
+        st = rlib().ref_mesh_incremental(self.h, min_weight, reserved, _ptr(d), d.shape[0],
+                                         C.byref(nv), C.byref(nf), _ptr(rem), cap, C.byref(nr))
+        if st:
+            raise CheckerError(st, rlib().ref_last_error().decode())
+        return _mesh_arrays(rlib().ref_mesh_read, self.h, nv.value, nf.value), rem[:nr.value]
+
+
+def _mesh_arrays(read, h, nv, nf):
+    v = np.zeros((nv, 3), np.float32)
+    n = np.zeros((nv, 3), np.float32)
+    lab = np.zeros(nv, np.uint8)
+    f = np.zeros((nf, 3), np.uint32)
+    read(h, _ptr(v), _ptr(n), _ptr(lab), _ptr(f))
+    return v, n, lab, f
 
 
 def parse_svox1(buf: bytes):

@@ -5,6 +5,7 @@
 // path consumes. Structs are the svx.h ones; nothing here is product code.
 #include "../include/svx.h"
 
+#include "semvox/mesh.hpp"
 #include "semvox/scan_projection.hpp"
 #include "semvox/semantic_integrator.hpp"
 #include "semvox/threading.hpp"
@@ -80,7 +81,21 @@ struct RefMap {
     std::unique_ptr<VoxelStore> store;
     std::unique_ptr<TsdfIntegrator> tsdf;
     std::unique_ptr<SemanticIntegrator> sem;
+    std::unique_ptr<IncrementalMesher> mesher;
+    LabelSet mesher_labels;
+    LabeledMesh mesh;
 };
+
+// A LabelSet whose reserved_unlabeled_id (mesh.cpp:218-222) is `reserved` (-1: none).
+LabelSet reserved_labels(int32_t reserved) {
+    LabelSet ls;
+    if (reserved < 0) return ls;
+    for (int i = 0; i <= reserved; ++i) {
+        ls.names.push_back(i == reserved ? "unlabeled" : "c" + std::to_string(i));
+        ls.colors.push_back(Rgb{});
+    }
+    return ls;
+}
 
 void fill_report(const FrameReport& r, svx_frame_report* out) {
     out->frame = r.frame;
@@ -136,6 +151,16 @@ int ref_lidar_spinning(int32_t w, int32_t h, double up, double down, svx_lidar_m
         out->offset_o = m.offset_o;
         out->min_range = m.min_range;
     });
+}
+
+// VoxelStore::load (voxel_store.cpp:132-168) into a new driver map.
+void* ref_map_load(const char* path) {
+    RefMap* m = nullptr;
+    const int st = guarded([&] {
+        auto store = std::make_unique<VoxelStore>(VoxelStore::load(path));
+        m = new RefMap{std::move(store), nullptr, nullptr};
+    });
+    return st == 0 ? m : nullptr;
 }
 
 void* ref_map_create(const svx_map_cfg* cfg) {
@@ -298,6 +323,58 @@ uint64_t ref_take_dirty(void* h, int32_t which, int32_t* out, uint64_t cap) {
         out[3 * i + 2] = d[i].z;
     }
     return d.size();
+}
+
+// extract_mesh (mesh.cpp:224-229); the mesh stays in the map for ref_mesh_read.
+int ref_mesh_extract(void* h, float min_weight, int32_t reserved, uint64_t* nv, uint64_t* nf) {
+    return guarded([&] {
+        RefMap* m = static_cast<RefMap*>(h);
+        const LabelSet ls = reserved_labels(reserved);
+        m->mesh = extract_mesh(*m->store, min_weight, reserved >= 0 ? &ls : nullptr);
+        *nv = m->mesh.vertices.size();
+        *nf = m->mesh.faces.size();
+    });
+}
+
+// IncrementalMesher::update (mesh.cpp:231-287) with a mesher kept in the map;
+// remeshed (cap entries) receives last_remeshed(), *n_remeshed its size.
+int ref_mesh_incremental(void* h, float min_weight, int32_t reserved, const int32_t* dirty,
+                         uint64_t n, uint64_t* nv, uint64_t* nf, int32_t* remeshed, uint64_t cap,
+                         uint64_t* n_remeshed) {
+    return guarded([&] {
+        RefMap* m = static_cast<RefMap*>(h);
+        if (!m->mesher) {
+            m->mesher_labels = reserved_labels(reserved);
+            m->mesher = std::make_unique<IncrementalMesher>(
+                min_weight, reserved >= 0 ? &m->mesher_labels : nullptr);
+        }
+        std::vector<BlockCoord> d(n);
+        for (uint64_t i = 0; i < n; ++i) d[i] = {dirty[3 * i], dirty[3 * i + 1], dirty[3 * i + 2]};
+        m->mesh = m->mesher->update(*m->store, d);
+        *nv = m->mesh.vertices.size();
+        *nf = m->mesh.faces.size();
+        const auto& r = m->mesher->last_remeshed();
+        *n_remeshed = r.size();
+        for (size_t i = 0; i < r.size() && i < cap; ++i) {
+            remeshed[3 * i] = r[i].x;
+            remeshed[3 * i + 1] = r[i].y;
+            remeshed[3 * i + 2] = r[i].z;
+        }
+    });
+}
+
+void ref_mesh_read(void* h, float* vertices, float* normals, uint8_t* labels, uint32_t* faces) {
+    const LabeledMesh& mesh = static_cast<RefMap*>(h)->mesh;
+    for (size_t i = 0; i < mesh.vertices.size(); ++i)
+        for (int c = 0; c < 3; ++c) {
+            if (vertices) vertices[3 * i + c] = mesh.vertices[i][c];
+            if (normals) normals[3 * i + c] = mesh.vertex_normals[i][c];
+        }
+    if (labels && !mesh.vertex_labels.empty())
+        std::memcpy(labels, mesh.vertex_labels.data(), mesh.vertex_labels.size());
+    if (faces)
+        for (size_t i = 0; i < mesh.faces.size(); ++i)
+            for (int c = 0; c < 3; ++c) faces[3 * i + c] = mesh.faces[i][c];
 }
 
 }  // extern "C"

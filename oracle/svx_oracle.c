@@ -100,6 +100,11 @@ struct svxo_map {
     int tsdf_frames, sem_frames;
     int32_t* dirty[2];
     uint64_t ndirty[2], capdirty[2];
+    /* last extract_mesh result (svxo_mesh_extract) */
+    float *mesh_v, *mesh_n;
+    uint8_t* mesh_l;
+    uint32_t* mesh_f;
+    uint64_t mesh_nv, mesh_nf;
 };
 
 static uint64_t hkey(const int32_t k[3]) {
@@ -159,6 +164,10 @@ void svxo_map_destroy(svxo_map* m) {
     free(m->table);
     free(m->dirty[0]);
     free(m->dirty[1]);
+    free(m->mesh_v);
+    free(m->mesh_n);
+    free(m->mesh_l);
+    free(m->mesh_f);
     free(m);
 }
 
@@ -852,4 +861,238 @@ void svxo_bayes(float* probs, const float* like, int K) {
     }
     const float inv = (float)(1.0 / z);
     for (int k = 0; k < K; ++k) probs[k] *= inv;
+}
+
+/* ===================================================================== mesh
+ * extract_mesh (mesh.cpp:105-229): marching cubes per block in sorted block order,
+ * cells in linear (z, y, x) order, a vertex per lattice edge keyed by (lower corner,
+ * axis). The reference dedups edges per block and then stitches blocks in sorted
+ * order through a global edge map (mesh.cpp:192-216); one global edge map visited in
+ * the same order assigns the same first-appearance indices, so that is what this
+ * restatement does. Case tables: the classic Lorensen-Cline/Bourke tabulation, read
+ * from the product header (pinned against the reference's mc_tables.hpp by
+ * tests/test_oracle.py). */
+#include "../paper_2412_00291_b200/csrc/svx_mc_tables.h"
+
+typedef struct { int32_t c[3]; int axis; } edge_key;
+typedef struct { edge_key k; uint32_t idx; int used; } edge_slot;
+typedef struct {
+    const svx_tsdf_voxel* tsdf;
+    const oblock* blk;
+    int linear;
+    int32_t coord[3];
+} cell_corner;
+
+static uint64_t edge_hash(const edge_key* k) {
+    return hkey(k->c) * 31u + (uint64_t)k->axis;
+}
+static float nonzero_distance(float d) { /* mesh.cpp:44-48 */
+    const float eps = 1e-5f;
+    if (d > -eps && d < eps) return d < 0.f ? -eps : eps;
+    return d;
+}
+
+typedef struct {
+    float *v, *n;
+    uint8_t* l;
+    uint32_t* f;
+    uint64_t nv, nf, capv, capf;
+} mesh_buf;
+
+/* make_edge_vertex (mesh.cpp:52-95) */
+static void make_edge_vertex(const svxo_map* m, const cell_corner* lo, const cell_corner* hi,
+                             int reserved, float* pos, float* nrm, uint8_t* label) {
+    const float dl = nonzero_distance(lo->tsdf->distance);
+    const float dh = nonzero_distance(hi->tsdf->distance);
+    const float t = dl / (dl - dh);
+    const d3 cld = voxel_center(lo->coord, m->cfg.voxel_size);
+    const d3 chd = voxel_center(hi->coord, m->cfg.voxel_size);
+    float n[3];
+    for (int c = 0; c < 3; ++c) {
+        const float cl = (float)cld.v[c], ch = (float)chd.v[c];
+        pos[c] = cl + t * (ch - cl);
+        n[c] = (1.f - t) * lo->tsdf->gradient[c] + t * hi->tsdf->gradient[c];
+    }
+    const float norm = sqrtf((n[0] * n[0] + n[1] * n[1]) + n[2] * n[2]);
+    for (int c = 0; c < 3; ++c) nrm[c] = norm > 1e-8f ? n[c] / norm : (c == 2 ? 1.f : 0.f);
+    *label = 255;
+    if (lo->blk->sem && hi->blk->sem) {
+        const int K = m->cfg.num_labels;
+        const float* pl = lo->blk->sem + (size_t)lo->linear * K;
+        const float* ph = hi->blk->sem + (size_t)hi->linear * K;
+        const float prior = 1.f / (float)K;
+        int lp = 1, hp = 1;
+        for (int k = 0; k < K; ++k) {
+            if (pl[k] != prior) lp = 0;
+            if (ph[k] != prior) hp = 0;
+        }
+        if (lp || hp) return;
+        int best = 0;
+        float best_p = -1.f;
+        for (int k = 0; k < K; ++k) {
+            const float p = (1.f - t) * pl[k] + t * ph[k];
+            if (p > best_p) {
+                best_p = p;
+                best = k;
+            }
+        }
+        *label = best == reserved ? 255 : (uint8_t)best;
+    }
+}
+
+int svxo_mesh_extract(svxo_map* m, float min_weight, int32_t reserved, const int32_t* bxyz,
+                      uint64_t n, uint64_t* n_vertices, uint64_t* n_faces) {
+    /* the mesh blocks, sorted unique (block_coords_sorted, or the cached set of an
+     * IncrementalMesher, mesh.cpp:261-285); absent blocks are skipped */
+    oblock** blocks = malloc((m->n + 1) * sizeof(oblock*));
+    uint64_t nb = 0;
+    if (!bxyz) {
+        memcpy(blocks, m->blocks, m->n * sizeof(oblock*));
+        nb = m->n;
+    } else {
+        int32_t* ks = malloc((n + 1) * 12);
+        memcpy(ks, bxyz, n * 12);
+        qsort(ks, n, 12, cmp_key3);
+        for (uint64_t i = 0; i < n; ++i) {
+            if (i && key_cmp(ks + 3 * i, ks + 3 * (i - 1)) == 0) continue;
+            const int64_t bi = find_idx(m, ks + 3 * i);
+            if (bi >= 0) blocks[nb++] = m->blocks[bi];
+        }
+        free(ks);
+    }
+    qsort(blocks, nb, sizeof(oblock*), cmp_blockptr);
+
+    uint8_t tris[256][16];
+    for (int c = 0; c < 256; ++c) {
+        const char* t = kMcTris[c];
+        int k = 0;
+        for (; t[k]; ++k) tris[c][k] = (uint8_t)(t[k] <= '9' ? t[k] - '0' : t[k] - 'a' + 10);
+        tris[c][k] = 0xFF;
+    }
+    uint64_t hcap = 1 << 16;
+    edge_slot* h = calloc(hcap, sizeof(edge_slot));
+    mesh_buf out = {0};
+    for (uint64_t bi = 0; bi < nb; ++bi) {
+        const oblock* blk = blocks[bi];
+        const int32_t o[3] = {blk->key[0] * KB, blk->key[1] * KB, blk->key[2] * KB};
+        /* corner cache of the 9x9x9 voxels the block's cells touch (mesh.cpp:119-133) */
+        const oblock* cb[9][9][9];
+        for (int z = 0; z < 9; ++z)
+            for (int y = 0; y < 9; ++y)
+                for (int x = 0; x < 9; ++x) {
+                    if (x < 8 && y < 8 && z < 8) {
+                        cb[z][y][x] = blk;
+                        continue;
+                    }
+                    const int32_t v[3] = {o[0] + x, o[1] + y, o[2] + z};
+                    const int32_t bk[3] = {floor_div(v[0], KB), floor_div(v[1], KB), floor_div(v[2], KB)};
+                    const int64_t j = find_idx(m, bk);
+                    cb[z][y][x] = j >= 0 ? m->blocks[j] : NULL;
+                }
+        for (int z = 0; z < KB; ++z)
+            for (int y = 0; y < KB; ++y)
+                for (int x = 0; x < KB; ++x) {
+                    cell_corner corners[8];
+                    int usable = 1, cube = 0;
+                    for (int c = 0; c < 8 && usable; ++c) {
+                        const int cx = x + kMcCorner[c][0], cy = y + kMcCorner[c][1],
+                                  cz = z + kMcCorner[c][2];
+                        const oblock* b = cb[cz][cy][cx];
+                        const int32_t vc[3] = {o[0] + cx, o[1] + cy, o[2] + cz};
+                        const int lin = nonneg_mod(vc[0], KB) + KB * nonneg_mod(vc[1], KB) +
+                                        KB * KB * nonneg_mod(vc[2], KB);
+                        if (!b || b->tsdf[lin].weight < min_weight) {
+                            usable = 0;
+                            break;
+                        }
+                        corners[c].tsdf = &b->tsdf[lin];
+                        corners[c].blk = b;
+                        corners[c].linear = lin;
+                        memcpy(corners[c].coord, vc, 12);
+                        if (b->tsdf[lin].distance < 0.f) cube |= 1 << c;
+                    }
+                    const uint16_t emask = mc_edge_mask(cube);
+                    if (!usable || emask == 0) continue;
+                    uint32_t eidx[12];
+                    for (int e = 0; e < 12; ++e) {
+                        if (!(emask >> e & 1)) continue;
+                        const cell_corner* a = &corners[kMcEdge[e][0]];
+                        const cell_corner* b = &corners[kMcEdge[e][1]];
+                        if (key_cmp(b->coord, a->coord) < 0) {
+                            const cell_corner* t = a;
+                            a = b;
+                            b = t;
+                        }
+                        edge_key key;
+                        memcpy(key.c, a->coord, 12);
+                        key.axis = b->coord[1] != a->coord[1] ? 1 : (b->coord[2] != a->coord[2] ? 2 : 0);
+                        if (2 * (out.nv + 1) > hcap) { /* grow the edge map */
+                            edge_slot* nh = calloc(2 * hcap, sizeof(edge_slot));
+                            for (uint64_t q = 0; q < hcap; ++q) {
+                                if (!h[q].used) continue;
+                                uint64_t s2 = edge_hash(&h[q].k) & (2 * hcap - 1);
+                                while (nh[s2].used) s2 = (s2 + 1) & (2 * hcap - 1);
+                                nh[s2] = h[q];
+                            }
+                            free(h);
+                            h = nh;
+                            hcap *= 2;
+                        }
+                        uint64_t sl = edge_hash(&key) & (hcap - 1);
+                        while (h[sl].used && !(h[sl].k.axis == key.axis && key_cmp(h[sl].k.c, key.c) == 0))
+                            sl = (sl + 1) & (hcap - 1);
+                        if (!h[sl].used) {
+                            h[sl].used = 1;
+                            h[sl].k = key;
+                            h[sl].idx = (uint32_t)out.nv;
+                            if (out.nv == out.capv) {
+                                out.capv = out.capv ? 2 * out.capv : 4096;
+                                out.v = realloc(out.v, out.capv * 12);
+                                out.n = realloc(out.n, out.capv * 12);
+                                out.l = realloc(out.l, out.capv);
+                            }
+                            make_edge_vertex(m, a, b, reserved, out.v + 3 * out.nv, out.n + 3 * out.nv,
+                                             out.l + out.nv);
+                            ++out.nv;
+                        }
+                        eidx[e] = h[sl].idx;
+                    }
+                    for (int i = 0; tris[cube][i] != 0xFF; i += 3) { /* mesh.cpp:179-189 */
+                        const uint32_t i0 = eidx[tris[cube][i]], i1 = eidx[tris[cube][i + 1]],
+                                       i2 = eidx[tris[cube][i + 2]];
+                        if (i0 == i1 || i1 == i2 || i0 == i2) continue;
+                        if (out.nf == out.capf) {
+                            out.capf = out.capf ? 2 * out.capf : 4096;
+                            out.f = realloc(out.f, out.capf * 12);
+                        }
+                        out.f[3 * out.nf] = i0;
+                        out.f[3 * out.nf + 1] = i2;
+                        out.f[3 * out.nf + 2] = i1;
+                        ++out.nf;
+                    }
+                }
+    }
+    free(h);
+    free(blocks);
+    free(m->mesh_v);
+    free(m->mesh_n);
+    free(m->mesh_l);
+    free(m->mesh_f);
+    m->mesh_v = out.v;
+    m->mesh_n = out.n;
+    m->mesh_l = out.l;
+    m->mesh_f = out.f;
+    m->mesh_nv = out.nv;
+    m->mesh_nf = out.nf;
+    *n_vertices = out.nv;
+    *n_faces = out.nf;
+    return 0;
+}
+
+void svxo_mesh_read(const svxo_map* m, float* vertices, float* normals, uint8_t* labels,
+                    uint32_t* faces) {
+    if (vertices && m->mesh_nv) memcpy(vertices, m->mesh_v, 12 * m->mesh_nv);
+    if (normals && m->mesh_nv) memcpy(normals, m->mesh_n, 12 * m->mesh_nv);
+    if (labels && m->mesh_nv) memcpy(labels, m->mesh_l, m->mesh_nv);
+    if (faces && m->mesh_nf) memcpy(faces, m->mesh_f, 12 * m->mesh_nf);
 }

@@ -50,6 +50,12 @@ int svxo_lookup(const svxo_map* m, const int32_t v[3], svx_tsdf_voxel* out, floa
 uint64_t svxo_observed(const svxo_map* m);
 /* Sorted unique dirty blocks of pass `which` (0 tsdf, 1 semantic); clears. */
 uint64_t svxo_take_dirty(svxo_map* m, int32_t which, int32_t* out, uint64_t cap);
+/* extract_mesh (mesh.cpp:105-229) over the blocks bxyz (n*3; NULL = all blocks);
+ * reserved: trailing "unlabeled" class id or -1. The result stays in the map. */
+int svxo_mesh_extract(svxo_map* m, float min_weight, int32_t reserved, const int32_t* bxyz,
+                      uint64_t n, uint64_t* n_vertices, uint64_t* n_faces);
+void svxo_mesh_read(const svxo_map* m, float* vertices, float* normals, uint8_t* labels,
+                    uint32_t* faces);
 const char* svxo_last_error(void);
 
 #ifdef __cplusplus

@@ -188,6 +188,11 @@ def _sig(lib: C.CDLL) -> None:
         "svx_profile_enable": (S, [P, C.c_int32]),
         "svx_profile_read": (S, [P, C.POINTER(ProfileC)]),
         "svx_block_owner": (C.c_int32, [C.POINTER(C.c_int32), C.c_int32]),
+        "svx_has_blocks": (S, [P, P, C.c_uint64, P]),
+        "svx_mesh_extract": (S, [P, C.c_float, C.c_int32, P, C.c_uint64, C.POINTER(C.c_uint64),
+                                 C.POINTER(C.c_uint64)]),
+        "svx_mesh_read": (S, [P, P, P, P, P]),
+        "svx_mesh_device": (S, [P, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P)]),
     }
     for name, (res, args) in f.items():
         fn = getattr(lib, name)
@@ -526,6 +531,14 @@ class VoxelStore:
         _check(lib().svx_load(str(path).encode(), device, max_blocks, C.byref(h)))
         return VoxelStore(device=device, _handle=h)
 
+    def has_blocks(self, coords) -> np.ndarray:
+        """find_block(b) != nullptr for many blocks at once."""
+        b = np.ascontiguousarray(np.asarray(coords, dtype=np.int32).reshape(-1, 3))
+        f = np.zeros(b.shape[0], dtype=np.uint8)
+        if b.shape[0]:
+            _check(lib().svx_has_blocks(self._h, _ptr(b), b.shape[0], _ptr(f)))
+        return f.astype(bool)
+
     def take_dirty_blocks(self, which: int) -> np.ndarray:
         n = C.c_uint64()
         _check(lib().svx_take_dirty_blocks(self._h, which, None, 0, C.byref(n)))
@@ -739,6 +752,98 @@ class SemanticIntegrator:
         return self.store.take_dirty_blocks(1)
 
 
+# ------------------------------------------------------------------ mesh
+
+DEFAULT_MESH_MIN_WEIGHT = 1e-4  # kDefaultMeshMinWeight, mesh.hpp:32
+UNLABELED = 255                 # kUnlabeled, types.hpp:32
+
+
+@dataclass
+class LabeledMesh:
+    """semvox::LabeledMesh (mesh.hpp:11-21) as numpy arrays."""
+    vertices: np.ndarray        # [V,3] f32
+    faces: np.ndarray           # [F,3] u32
+    vertex_labels: np.ndarray   # [V] u8, 255 = unlabeled
+    vertex_normals: np.ndarray  # [V,3] f32
+    vertex_colors: Optional[np.ndarray] = None  # [V,3] u8 when a label colour table is given
+
+    def vertex_count(self) -> int:
+        return int(self.vertices.shape[0])
+
+    def empty(self) -> bool:
+        return self.faces.shape[0] == 0
+
+
+def _reserved_unlabeled(label_names) -> int:
+    """reserved_unlabeled_id (mesh.cpp:218-222): a trailing "unlabeled" class."""
+    if label_names and label_names[-1] == "unlabeled":
+        return len(label_names) - 1
+    return -1
+
+
+def _read_mesh(store: "VoxelStore", nv: int, nf: int, colors) -> LabeledMesh:
+    v = np.zeros((nv, 3), np.float32)
+    n = np.zeros((nv, 3), np.float32)
+    lab = np.zeros(nv, np.uint8)
+    f = np.zeros((nf, 3), np.uint32)
+    _check(lib().svx_mesh_read(store.handle, _ptr(v), _ptr(n), _ptr(lab), _ptr(f)))
+    col = None
+    if colors is not None:  # LabelSet::color_of_label; gray (128) for unlabeled
+        table = np.full((256, 3), 128, np.uint8)
+        c = np.asarray(colors, np.uint8).reshape(-1, 3)
+        table[:min(len(c), 255)] = c[:255]
+        col = table[lab]
+    return LabeledMesh(v, f, lab, n, col)
+
+
+def extract_mesh(store: "VoxelStore", min_weight: float = DEFAULT_MESH_MIN_WEIGHT,
+                 label_names=None, label_colors=None, blocks=None) -> LabeledMesh:
+    """extract_mesh (mesh.cpp:224-229) on the device; `blocks` restricts the cells to
+    those based in the given blocks (None = every allocated block)."""
+    nv, nf = C.c_uint64(), C.c_uint64()
+    b = None if blocks is None else np.ascontiguousarray(np.asarray(blocks, np.int32).reshape(-1, 3))
+    _check(lib().svx_mesh_extract(store.handle, float(min_weight), _reserved_unlabeled(label_names),
+                                  _ptr(b), 0 if b is None else b.shape[0], C.byref(nv), C.byref(nf)))
+    return _read_mesh(store, nv.value, nf.value, label_colors)
+
+
+class IncrementalMesher:
+    """IncrementalMesher (mesh.hpp:37-63, mesh.cpp:231-287): keeps the set of meshed
+    blocks; update() adds the blocks a dirty set affects (D - {0,1}^3) that exist and
+    drops those that do not, then re-meshes the set on the device. The stitched mesh
+    equals extract_mesh over the set, which is what the reference guarantees for
+    blocks that were reported dirty whenever they changed."""
+
+    def __init__(self, min_weight: float = DEFAULT_MESH_MIN_WEIGHT, label_names=None,
+                 label_colors=None):
+        self.min_weight = min_weight
+        self.label_names = label_names
+        self.label_colors = label_colors
+        self._cache: set = set()
+        self.last_remeshed = np.zeros((0, 3), np.int32)
+        self.mesh = LabeledMesh(np.zeros((0, 3), np.float32), np.zeros((0, 3), np.uint32),
+                                np.zeros(0, np.uint8), np.zeros((0, 3), np.float32))
+
+    def update(self, store: "VoxelStore", dirty) -> LabeledMesh:
+        d = np.asarray(dirty, np.int32).reshape(-1, 3)
+        off = np.array([(x, y, z) for z in (-1, 0) for y in (-1, 0) for x in (-1, 0)], np.int32)
+        aff = np.unique((d[:, None, :] + off[None]).reshape(-1, 3), axis=0) if len(d) else d
+        present = store.has_blocks(aff)
+        for bc, ok in zip(map(tuple, aff.tolist()), present):
+            if ok:
+                self._cache.add(bc)
+            else:
+                self._cache.discard(bc)
+        self.last_remeshed = aff[present]
+        if not self._cache:
+            self.mesh = LabeledMesh(np.zeros((0, 3), np.float32), np.zeros((0, 3), np.uint32),
+                                    np.zeros(0, np.uint8), np.zeros((0, 3), np.float32))
+            return self.mesh
+        blocks = np.array(sorted(self._cache), np.int32)
+        self.mesh = extract_mesh(store, self.min_weight, self.label_names, self.label_colors, blocks)
+        return self.mesh
+
+
 def block_owner(bc, world: int) -> int:
     return int(lib().svx_block_owner(_i3(bc), world))
 
@@ -749,4 +854,5 @@ __all__ = [
     "SemanticIntegrator", "LabelImage", "Pose", "pose_c", "CapacityError", "DataError",
     "InvalidArgument", "CudaError", "NotFound", "PROJECTIVE", "NON_PROJECTIVE", "SURROGATE",
     "RAYCAST", "TSDF_DTYPE", "lib", "declared_symbols", "kernel_launches", "block_owner",
+    "LabeledMesh", "extract_mesh", "IncrementalMesher", "DEFAULT_MESH_MIN_WEIGHT", "UNLABELED",
 ]

@@ -116,6 +116,7 @@ void free_map(svx_map* m) {
     m->sem_out.release();
     m->q_keys.release();
     m->q_idx.release();
+    m->mesh.release();
     if (m->copy_stream) cudaStreamSynchronize(m->copy_stream);
     for (int i = 0; i < svx_map::kIngestSlots; ++i) {
         if (m->ingest_ready[i]) cudaEventDestroy(m->ingest_ready[i]);
@@ -487,6 +488,73 @@ svx_status svx_has_block(svx_map* m, const int32_t b[3], int32_t* found) {
         uint32_t idx = kInvalid;
         find_blocks(m, &k, 1, &idx);
         *found = idx != kInvalid;
+    });
+}
+
+svx_status svx_has_blocks(svx_map* m, const int32_t* bxyz, uint64_t n, uint8_t* found) {
+    return guarded([&] {
+        require(m && (bxyz || !n) && (found || !n), SVX_INVALID_ARGUMENT, "null argument");
+        require(n < (1ull << 31), SVX_INVALID_ARGUMENT, "too many blocks in one query");
+        if (!n) return;
+        DeviceGuard g(m->device);
+        std::vector<uint64_t> keys(n);
+        std::vector<uint8_t> in_range(n);
+        for (uint64_t i = 0; i < n; ++i) {
+            const int32_t* b = bxyz + 3 * i;
+            in_range[i] = key_in_range(b[0]) && key_in_range(b[1]) && key_in_range(b[2]);
+            keys[i] = in_range[i] ? pack_key(b[0], b[1], b[2]) : 0;
+        }
+        std::vector<uint32_t> idx(n);
+        find_blocks(m, keys.data(), uint32_t(n), idx.data());
+        for (uint64_t i = 0; i < n; ++i) found[i] = in_range[i] && idx[i] != kInvalid;
+    });
+}
+
+svx_status svx_mesh_extract(svx_map* m, float min_weight, int32_t reserved, const int32_t* bxyz,
+                            uint64_t n, uint64_t* n_vertices, uint64_t* n_faces) {
+    return guarded([&] {
+        require(m && n_vertices && n_faces && (bxyz || !n), SVX_INVALID_ARGUMENT, "null argument");
+        DeviceGuard g(m->device);
+        SVX_CUDA(cudaStreamSynchronize(m->stream));
+        if (!bxyz) {
+            run_extract_mesh(m, min_weight, reserved, nullptr, 0, n_vertices, n_faces);
+            return;
+        }
+        std::vector<uint64_t> keys;
+        keys.reserve(n);
+        for (uint64_t i = 0; i < n; ++i) {
+            const int32_t* b = bxyz + 3 * i;
+            if (key_in_range(b[0]) && key_in_range(b[1]) && key_in_range(b[2]))
+                keys.push_back(pack_key(b[0], b[1], b[2]));
+        }
+        std::sort(keys.begin(), keys.end());
+        keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+        run_extract_mesh(m, min_weight, reserved, keys.data(), keys.size(), n_vertices, n_faces);
+    });
+}
+
+svx_status svx_mesh_read(svx_map* m, float* vertices, float* normals, uint8_t* labels,
+                         uint32_t* faces) {
+    return guarded([&] {
+        require(m != nullptr, SVX_INVALID_ARGUMENT, "null map");
+        DeviceGuard g(m->device);
+        const MeshState& ms = m->mesh;
+        const uint64_t V = ms.n_vertices, F = ms.n_faces;
+        if (vertices && V) SVX_CUDA(cudaMemcpy(vertices, ms.verts.p, 12 * V, cudaMemcpyDeviceToHost));
+        if (normals && V) SVX_CUDA(cudaMemcpy(normals, ms.normals.p, 12 * V, cudaMemcpyDeviceToHost));
+        if (labels && V) SVX_CUDA(cudaMemcpy(labels, ms.labels.p, V, cudaMemcpyDeviceToHost));
+        if (faces && F) SVX_CUDA(cudaMemcpy(faces, ms.faces.p, 12 * F, cudaMemcpyDeviceToHost));
+    });
+}
+
+svx_status svx_mesh_device(svx_map* m, const float** vertices, const float** normals,
+                           const uint8_t** labels, const uint32_t** faces) {
+    return guarded([&] {
+        require(m != nullptr, SVX_INVALID_ARGUMENT, "null map");
+        if (vertices) *vertices = m->mesh.verts.p;
+        if (normals) *normals = m->mesh.normals.p;
+        if (labels) *labels = m->mesh.labels.p;
+        if (faces) *faces = m->mesh.faces.p;
     });
 }
 

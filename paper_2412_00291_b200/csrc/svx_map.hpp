@@ -95,6 +95,26 @@ struct DevBuf {
     }
 };
 
+// Device state of the last mesh extraction (svx_mesh.cu): scratch + output.
+struct MeshState {
+    DevBuf<uint64_t> keys;            // mesh blocks, sorted (2R: sort scratch)
+    DevBuf<uint32_t> pidx;            // their pool indices (2R)
+    DevBuf<uint32_t> rank_of_pool;    // [max_blocks] pool index -> mesh rank, kInvalid outside
+    DevBuf<uint32_t> nb_pool, nb_rank;  // [R][27] neighbour blocks
+    DevBuf<uint8_t> cases;            // [R][512] cell case bytes
+    DevBuf<uint32_t> cellinfo;        // [R][512] local vertex offset | owned-edge mask << 12
+    DevBuf<unsigned long long> counts;  // per-block vertex/face counts and their scans
+    DevBuf<float> verts, normals;     // 3V
+    DevBuf<uint8_t> labels;           // V
+    DevBuf<uint32_t> faces;           // 3F
+    uint64_t n_vertices = 0, n_faces = 0;
+    void release() {
+        keys.release(); pidx.release(); rank_of_pool.release(); nb_pool.release();
+        nb_rank.release(); cases.release(); cellinfo.release(); counts.release();
+        verts.release(); normals.release(); labels.release(); faces.release();
+    }
+};
+
 }  // namespace svx
 
 struct svx_scan {
@@ -181,6 +201,7 @@ struct svx_map {
     svx::DevBuf<float> conf, tensor;
     svx::DevBuf<float> like_table;   // [K+1][K] label -> likelihood at default confidence
     svx::DevBuf<uint32_t> sem_out;   // per image of a label batch: candidates, updated voxels
+    svx::MeshState mesh;             // last extract_mesh result (svx_mesh.cu)
     // counters
     uint32_t* d_ctr = nullptr;       // device
     uint32_t* h_ctr = nullptr;       // pinned mirror
@@ -289,6 +310,10 @@ void rebuild_hash(svx_map* m);
 // semantic layers (n x 512*K, has_sem[i] = 0 when block i has none).
 void gather_blocks(svx_map* m, const uint32_t* d_idx, uint64_t n, svx_tsdf_voxel* d_out,
                    float* d_sem, uint8_t* d_has_sem);
+// extract_mesh (mesh.cpp:105-287) over the sorted unique packed keys h_keys[0..n)
+// (every allocated block when h_keys == nullptr); result in m->mesh.
+void run_extract_mesh(svx_map* m, float min_weight, int reserved, const uint64_t* h_keys,
+                      uint64_t n_keys, uint64_t* n_vertices, uint64_t* n_faces);
 void lookup_voxels(svx_map* m, const int32_t* d_v, uint64_t n, svx_tsdf_voxel* d_out,
                    float* d_probs, uint8_t* d_found);
 

@@ -36,7 +36,8 @@ def test_dropin_library_exports_reference_api():
                 "semvox::compute_normal_image", "semvox::TsdfIntegrator::integrate_frame",
                 "semvox::TsdfIntegrator::take_dirty_blocks",
                 "semvox::SemanticIntegrator::integrate_labels", "semvox::fuse_voxel",
-                "semvox::label_to_likelihood", "semvox::bayes_update"):
+                "semvox::label_to_likelihood", "semvox::bayes_update", "semvox::extract_mesh",
+                "semvox::IncrementalMesher::update", "semvox::extract_vertex_cloud"):
         assert sym in out, sym
     # the drop-in resolves the device path from the C-ABI library, never from the oracle
     deps = subprocess.run(["ldd", LIB], capture_output=True, text=True).stdout
@@ -62,3 +63,17 @@ def test_dropin_reference_suites_pass_on_gpu():
     p, (ran, passed, failed) = _run(900)
     assert ran >= 50
     assert failed == 0, p.stderr[-4000:]
+
+
+ACC = os.path.join(ROOT, "oracle", "_ref", "dropin_acceptance")
+
+
+@pytest.mark.skipif(not os.path.exists(ACC), reason="dropin_acceptance not built")
+@pytest.mark.gpu
+def test_dropin_acceptance_passes_on_gpu():
+    """The reference's acceptance criteria A1-A9 (proj/tests/acceptance/acceptance.cpp)
+    through the drop-in: integration, semantics and the mesh export on the device."""
+    p = subprocess.run([ACC], capture_output=True, text=True, timeout=900, cwd=os.path.dirname(ACC))
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    passed = re.findall(r"^\[PASS\] (A\d)", p.stdout, re.M)
+    assert sorted(passed) == [f"A{i}" for i in range(1, 10)], p.stdout[-3000:]
