@@ -276,6 +276,80 @@ svx_status svx_mesh_device(svx_map* map, const float** vertices, const float** n
 /* VoxelStore::find_block != nullptr for n blocks at once (bxyz = n*3): found[i] = 0/1. */
 svx_status svx_has_blocks(svx_map* map, const int32_t* bxyz, uint64_t n, uint8_t* found);
 
+/* ------------------------------------------------- occupancy extension */
+/* Free-space carving + log-odds occupancy + hit/miss counters + integer class
+ * histograms for per-point labelled LiDAR: the north-star extension of BASELINE.json
+ * (SURVEY.md 8(f) row 3). The reference declines carving, so there is
+ * no reference implementation: the contract below is this project's own and the
+ * oracle (oracle/svx_oracle.c, svxo_occ_*) restates it serially ("parity unpinned").
+ *
+ * Per scan, for every point p (sensor frame) with finite coordinates and
+ * r = |p| >= min_range (Eigen order, FP64):
+ *   q = pose * p; o = pose.t; if r <= max_range the ray HITS the voxel of q and its
+ *   end is q, else it is cut at max_range (end = o + (q - o) * (max_range / r), no hit).
+ *   carve: every voxel traverse_segment(o, end) visits (tsdf_integrator.hpp:93-135)
+ *   is a MISS, except the hit voxel. Per scan a voxel is updated once: HIT if any ray
+ *   hit it, else MISS if any ray traversed it (order-independent by construction).
+ *   Update (f32): HIT: L = min(L + l_hit, l_max), hits += 1;
+ *                 MISS: L = max(L + l_miss, l_min), misses += 1.   (L starts at 0)
+ *   Labels: a hitting point with label l < K adds q8(conf) to hist[voxel][l], an
+ *   integer (u32 atomics, exact in any order); q8(c) = (uint32)(clamp(c,0,1)*255 + 0.5f),
+ *   255 without a confidence, 0 for a non-finite one. Label = first argmax of the
+ *   histogram, -1 when it is all zero. */
+typedef struct {
+    float voxel_size;      /* metres */
+    int32_t num_labels;    /* K histogram classes, 1..64 */
+    uint32_t max_blocks;   /* 8x8x8-voxel blocks */
+    float l_hit;           /* 0.85  (OctoMap p_hit 0.7)   */
+    float l_miss;          /* -0.4  (p_miss 0.4)          */
+    float l_min;           /* -2.0  (p 0.12)              */
+    float l_max;           /* 3.5   (p 0.97)              */
+    double min_range;      /* 0.3 */
+    double max_range;      /* 70  */
+    int32_t carve;         /* 1: free-space carving along the ray; 0: endpoints only */
+} svx_occ_cfg;
+
+typedef struct {
+    int32_t frame;
+    uint64_t points;       /* input points */
+    uint64_t rays;         /* points kept (finite, >= min_range) */
+    uint64_t hit_voxels;   /* voxels updated as HIT this scan */
+    uint64_t miss_voxels;  /* voxels updated as MISS this scan */
+    uint64_t new_blocks;
+    double elapsed_ms;
+} svx_occ_report;
+
+typedef struct svx_occ svx_occ;
+
+void svx_default_occ_cfg(svx_occ_cfg* cfg);
+svx_status svx_occ_create(const svx_occ_cfg* cfg, int device, svx_occ** out);
+svx_status svx_occ_destroy(svx_occ* occ);
+svx_status svx_occ_get_stream(svx_occ* occ, void** stream);
+/* Key sharding (as svx_map_set_shard): this map owns blocks with owner(b) == rank. */
+svx_status svx_occ_set_shard(svx_occ* occ, int32_t rank, int32_t world);
+/* One scan: n points of `stride` floats (xyz first), sensor frame; labels (u16 per
+ * point) and conf (f32 per point) may be NULL; ptr_is_device: all three in HBM. */
+svx_status svx_occ_integrate(svx_occ* occ, const float* points, const uint16_t* labels,
+                             const float* conf, uint64_t n, int32_t stride,
+                             int32_t ptr_is_device, const svx_pose* pose,
+                             svx_occ_report* report);
+/* A sequence of scans: scan f is rows [offsets[f], offsets[f+1]) of points / labels /
+ * conf, posed by poses[f]. */
+svx_status svx_occ_integrate_batch(svx_occ* occ, const float* points, const uint16_t* labels,
+                                   const float* conf, const uint64_t* offsets, int32_t stride,
+                                   int32_t ptr_is_device, const svx_pose* poses,
+                                   int32_t n_frames, svx_occ_report* reports);
+/* Point query of n voxels (vxyz = n*3). Any output may be NULL; hist is n*K. label =
+ * histogram argmax (-1: none). found[i] = 0 for a voxel of an unallocated block. */
+svx_status svx_occ_lookup(svx_occ* occ, const int32_t* vxyz, uint64_t n, float* log_odds,
+                          uint32_t* hits, uint32_t* misses, uint32_t* hist, int32_t* label,
+                          uint8_t* found);
+svx_status svx_occ_block_count(svx_occ* occ, uint64_t* n);
+/* Map export "SOCC1": "SOCC1", f32 voxel_size, u32 K, f32 l_hit, l_miss, l_min, l_max,
+ * u64 n_blocks, then per block in sorted key order: i32 x,y,z, f32 log_odds[512],
+ * u32 hits[512], u32 misses[512], u8 has_hist, [u32 hist[512][K]]. buf=NULL -> size. */
+svx_status svx_occ_save_mem(svx_occ* occ, uint8_t* buf, uint64_t cap, uint64_t* size);
+
 /* ------------------------------------------------------------ profiling */
 /* Per-kernel device time measured with CUDA events on the map's stream (the
  * launching stream), plus the algorithmic counters the roofline needs

@@ -17,6 +17,7 @@ import tempfile
 
 import numpy as np
 
+import paper_2412_00291_b200 as svx
 from paper_2412_00291_b200 import (FrameReport, FrameReportC, IntegratorCfg, LabelImageC,
                                    LidarModel, MapCfg, PoseC, SemanticCfg, StatsC, TSDF_DTYPE)
 
@@ -72,6 +73,13 @@ def olib():
                                         C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.svxo_mesh_read.argtypes = [_P, _P, _P, _P, _P]
         L.svxo_mesh_read.restype = None
+        L.svxo_occ_create.argtypes = [C.POINTER(svx.OccCfgC)]
+        L.svxo_occ_create.restype = _P
+        L.svxo_occ_destroy.argtypes = [_P]
+        L.svxo_occ_integrate.argtypes = [_P, _P, _P, _P, C.c_uint64, C.c_int32, C.POINTER(PoseC),
+                                         C.POINTER(svx.OccReportC)]
+        L.svxo_occ_save_mem.argtypes = [_P, _P, C.c_uint64]
+        L.svxo_occ_save_mem.restype = C.c_uint64
         L.svxo_last_error.restype = C.c_char_p
         _olib = L
     return _olib
@@ -393,6 +401,67 @@ class RefMap(_Base):
         if st:
             raise CheckerError(st, rlib().ref_last_error().decode())
         return _mesh_arrays(rlib().ref_mesh_read, self.h, nv.value, nf.value), rem[:nr.value]
+
+
+class OracleOcc:
+    """Serial restatement of the occupancy extension (svx_oracle.c, parity unpinned)."""
+
+    def __init__(self, cfg):
+        self.cfg = cfg
+        self.h = olib().svxo_occ_create(C.byref(cfg.c()))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                olib().svxo_occ_destroy(self.h)
+            except TypeError:
+                pass
+            self.h = None
+
+    def integrate(self, points, pose, labels=None, conf=None):
+        a = np.ascontiguousarray(np.asarray(points, np.float32))
+        lb = None if labels is None else np.ascontiguousarray(labels, np.uint16)
+        cf = None if conf is None else np.ascontiguousarray(conf, np.float32)
+        rep = svx.OccReportC()
+        st = olib().svxo_occ_integrate(self.h, _ptr(a), _ptr(lb), _ptr(cf), a.shape[0], a.shape[1],
+                                       C.byref(pose), C.byref(rep))
+        if st:
+            raise CheckerError(st, olib().svxo_last_error().decode())
+        return rep
+
+    def save_bytes(self) -> bytes:
+        n = olib().svxo_occ_save_mem(self.h, None, 0)
+        buf = np.zeros(n, np.uint8)
+        olib().svxo_occ_save_mem(self.h, _ptr(buf), n)
+        return buf.tobytes()
+
+
+def parse_socc1(buf: bytes):
+    """SOCC1 (include/svx.h svx_occ_save_mem) -> (header, keys[n,3], L[n,512], hits, misses, hist dict)."""
+    import struct
+    if buf[:5] != b"SOCC1":
+        raise ValueError("not SOCC1")
+    vs, K, lh, lm, lmin, lmax = struct.unpack_from("<fIffff", buf, 5)
+    (nb,) = struct.unpack_from("<Q", buf, 29)
+    off = 37
+    keys = np.zeros((nb, 3), np.int32)
+    L = np.zeros((nb, 512), np.float32)
+    hits = np.zeros((nb, 512), np.uint32)
+    misses = np.zeros((nb, 512), np.uint32)
+    hist = {}
+    for i in range(nb):
+        keys[i] = np.frombuffer(buf, np.int32, 3, off)
+        off += 12
+        L[i] = np.frombuffer(buf, np.float32, 512, off)
+        hits[i] = np.frombuffer(buf, np.uint32, 512, off + 2048)
+        misses[i] = np.frombuffer(buf, np.uint32, 512, off + 4096)
+        off += 6144
+        hs = buf[off]
+        off += 1
+        if hs:
+            hist[i] = np.frombuffer(buf, np.uint32, 512 * K, off).reshape(512, K)
+            off += 2048 * K
+    return {"voxel_size": vs, "num_labels": K, "l": (lh, lm, lmin, lmax)}, keys, L, hits, misses, hist
 
 
 def _mesh_arrays(read, h, nv, nf):

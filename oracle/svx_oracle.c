@@ -1096,3 +1096,286 @@ void svxo_mesh_read(const svxo_map* m, float* vertices, float* normals, uint8_t*
     if (labels && m->mesh_nv) memcpy(labels, m->mesh_l, m->mesh_nv);
     if (faces && m->mesh_nf) memcpy(faces, m->mesh_f, 12 * m->mesh_nf);
 }
+
+/* ================================================================ occupancy
+ * The occupancy extension of include/svx.h ("occupancy extension"), restated
+ * serially. PARITY UNPINNED: the reference has no carving / log-odds / histogram
+ * code (SPEC.md:255 declines carving), so this restates the project's own contract;
+ * only the DDA it uses (traverse_segment above, tsdf_integrator.hpp:93-135) and the
+ * key arithmetic are the reference's. */
+typedef struct {
+    int32_t key[3];
+    uint32_t tag[KV];
+    float L[KV];
+    uint32_t hits[KV], misses[KV];
+    uint32_t* hist; /* KV*K, NULL until a labelled hit */
+    uint32_t touched_serial;
+} oocc_block;
+
+struct svxo_occ {
+    svx_occ_cfg cfg;
+    oocc_block** blocks;
+    uint64_t n, cap;
+    int64_t* table;
+    uint64_t tcap;
+    uint32_t serial;
+    int32_t frames;
+};
+
+static int64_t occ_find(const svxo_occ* m, const int32_t k[3]) {
+    uint64_t s = hkey(k) & (m->tcap - 1);
+    for (;;) {
+        const int64_t i = m->table[s];
+        if (i < 0) return -1;
+        if (key_cmp(m->blocks[i]->key, k) == 0) return i;
+        s = (s + 1) & (m->tcap - 1);
+    }
+}
+static void occ_table_insert(svxo_occ* m, int64_t idx) {
+    uint64_t s = hkey(m->blocks[idx]->key) & (m->tcap - 1);
+    while (m->table[s] >= 0) s = (s + 1) & (m->tcap - 1);
+    m->table[s] = idx;
+}
+static int64_t occ_alloc(svxo_occ* m, const int32_t k[3]) {
+    int64_t i = occ_find(m, k);
+    if (i >= 0) return i;
+    if (m->n == m->cap) {
+        m->cap = m->cap ? 2 * m->cap : 256;
+        m->blocks = realloc(m->blocks, m->cap * sizeof(oocc_block*));
+    }
+    oocc_block* b = calloc(1, sizeof *b);
+    memcpy(b->key, k, 12);
+    m->blocks[m->n] = b;
+    i = (int64_t)m->n++;
+    if (2 * m->n > m->tcap) {
+        free(m->table);
+        m->tcap *= 2;
+        m->table = malloc(m->tcap * sizeof(int64_t));
+        memset(m->table, 0xFF, m->tcap * sizeof(int64_t));
+        for (uint64_t j = 0; j < m->n; ++j) occ_table_insert(m, (int64_t)j);
+    } else {
+        occ_table_insert(m, i);
+    }
+    return i;
+}
+
+svxo_occ* svxo_occ_create(const svx_occ_cfg* cfg) {
+    svxo_occ* m = calloc(1, sizeof *m);
+    m->cfg = *cfg;
+    m->tcap = 1024;
+    m->table = malloc(m->tcap * sizeof(int64_t));
+    memset(m->table, 0xFF, m->tcap * sizeof(int64_t));
+    return m;
+}
+
+void svxo_occ_destroy(svxo_occ* m) {
+    if (!m) return;
+    for (uint64_t i = 0; i < m->n; ++i) {
+        free(m->blocks[i]->hist);
+        free(m->blocks[i]);
+    }
+    free(m->blocks);
+    free(m->table);
+    free(m);
+}
+
+typedef struct {
+    int32_t v[3];
+    int kind;        /* 3 hit, 1 miss */
+    uint32_t label;  /* >= K: none */
+    uint32_t q;
+} occ_visit;
+
+typedef struct {
+    occ_visit* v;
+    size_t n, cap;
+} occ_vec;
+
+static void occ_push(occ_vec* o, const int32_t v[3], int kind, uint32_t label, uint32_t q) {
+    if (o->n == o->cap) {
+        o->cap = o->cap ? 2 * o->cap : 1 << 16;
+        o->v = realloc(o->v, o->cap * sizeof(occ_visit));
+    }
+    occ_visit* r = &o->v[o->n++];
+    memcpy(r->v, v, 12);
+    r->kind = kind;
+    r->label = label;
+    r->q = q;
+}
+
+static uint32_t occ_q8(const float* conf, uint64_t i) {
+    if (!conf) return 255u;
+    const float c = conf[i];
+    if (!isfinite(c)) return 0u;
+    const float cc = c < 0.f ? 0.f : (c > 1.f ? 1.f : c);
+    return (uint32_t)(cc * 255.f + 0.5f);
+}
+
+int svxo_occ_integrate(svxo_occ* m, const float* pts, const uint16_t* labels, const float* conf,
+                       uint64_t n, int32_t stride, const svx_pose* pose, svx_occ_report* rep) {
+    const svx_occ_cfg* c = &m->cfg;
+    const int K = c->num_labels;
+    occ_vec vis = {0};
+    visit_vec ray = {0};
+    uint64_t rays = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const float* q = pts + i * (uint64_t)stride;
+        if (!(isfinite(q[0]) && isfinite(q[1]) && isfinite(q[2]))) continue;
+        const d3 ps = {{q[0], q[1], q[2]}};
+        const double r = sqrt(dot3(ps, ps));
+        if (r < c->min_range) continue;
+        ++rays;
+        const d3 pw = xform(pose, ps);
+        const d3 o = origin_of(pose);
+        const int hit = r <= c->max_range;
+        const d3 end = hit ? pw : add3(o, scale3(c->max_range / r, sub3(pw, o)));
+        int32_t ev[3];
+        world_to_voxel(end, c->voxel_size, ev);
+        const uint32_t lab = labels ? labels[i] : 0xFFFFFFFFu;
+        if (c->carve) {
+            ray.n = 0;
+            traverse_segment(o, end, c->voxel_size, &ray, 0);
+            for (size_t k = 0; k < ray.n; ++k) {
+                const visit* t = &ray.v[k];
+                const int32_t vc[3] = {t->b[0] * KB + (t->linear % KB), t->b[1] * KB + (t->linear / KB) % KB,
+                                       t->b[2] * KB + t->linear / (KB * KB)};
+                if (hit && vc[0] == ev[0] && vc[1] == ev[1] && vc[2] == ev[2]) continue;
+                occ_push(&vis, vc, 1, 0xFFFFFFFFu, 0);
+            }
+        }
+        if (hit) occ_push(&vis, ev, 3, lab, occ_q8(conf, i));
+    }
+    free(ray.v);
+    /* capacity: the scan is rejected unchanged if its new blocks do not fit */
+    uint64_t scap = 1024;
+    while (scap < 4 * vis.n) scap *= 2;
+    int32_t* seen = malloc(scap * 12);
+    uint8_t* used = calloc(scap, 1);
+    uint64_t fresh = 0;
+    for (size_t k = 0; k < vis.n; ++k) {
+        int32_t b[3];
+        block_of(vis.v[k].v, b);
+        for (int a = 0; a < 3; ++a)
+            if (b[a] < -(1 << 20) || b[a] >= (1 << 20)) {
+                free(seen), free(used), free(vis.v);
+                return fail(1, "voxel outside the device key range [-2^23, 2^23)");
+            }
+        if (occ_find(m, b) >= 0) continue;
+        uint64_t s = hkey(b) & (scap - 1);
+        while (used[s] && key_cmp(seen + 3 * s, b) != 0) s = (s + 1) & (scap - 1);
+        if (!used[s]) {
+            used[s] = 1;
+            memcpy(seen + 3 * s, b, 12);
+            ++fresh;
+        }
+    }
+    free(seen);
+    free(used);
+    if (m->n + fresh > c->max_blocks) {
+        free(vis.v);
+        return fail(2, "occupancy map: max_blocks reached");
+    }
+    const uint64_t old_n = m->n;
+    m->serial += 1;
+    const uint32_t S = m->serial;
+    oocc_block** touched = malloc((m->n + fresh + 1) * sizeof(oocc_block*));
+    uint64_t nt = 0;
+    for (size_t k = 0; k < vis.n; ++k) {
+        const occ_visit* t = &vis.v[k];
+        int32_t b[3];
+        block_of(t->v, b);
+        const int64_t bi = occ_alloc(m, b); /* may grow m->blocks */
+        oocc_block* blk = m->blocks[bi];
+        if (blk->touched_serial != S) {
+            blk->touched_serial = S;
+            touched[nt++] = blk;
+        }
+        const int li = local_index(t->v);
+        const uint32_t want = 4u * S + (uint32_t)t->kind;
+        if (blk->tag[li] < want) blk->tag[li] = want;
+        if (t->kind == 3 && t->label < (uint32_t)K) {
+            if (!blk->hist) blk->hist = calloc((size_t)KV * K, sizeof(uint32_t));
+            blk->hist[(size_t)li * K + t->label] += t->q;
+        }
+    }
+    free(vis.v);
+    uint64_t nh = 0, nm = 0;
+    for (uint64_t k = 0; k < nt; ++k) {
+        oocc_block* blk = touched[k];
+        for (int v = 0; v < KV; ++v) {
+            if (blk->tag[v] >> 2 != S) continue;
+            if ((blk->tag[v] & 3u) == 3u) {
+                const float t = blk->L[v] + c->l_hit;
+                blk->L[v] = t > c->l_max ? c->l_max : t;
+                blk->hits[v] += 1;
+                ++nh;
+            } else {
+                const float t = blk->L[v] + c->l_miss;
+                blk->L[v] = t < c->l_min ? c->l_min : t;
+                blk->misses[v] += 1;
+                ++nm;
+            }
+        }
+    }
+    free(touched);
+    if (rep) {
+        rep->frame = m->frames;
+        rep->points = n;
+        rep->rays = rays;
+        rep->hit_voxels = nh;
+        rep->miss_voxels = nm;
+        rep->new_blocks = m->n - old_n;
+        rep->elapsed_ms = 0.0;
+    }
+    m->frames += 1;
+    return 0;
+}
+
+static int cmp_occptr(const void* a, const void* b) {
+    return key_cmp((*(oocc_block* const*)a)->key, (*(oocc_block* const*)b)->key);
+}
+
+/* SOCC1 export (include/svx.h svx_occ_save_mem) */
+#define PUT(x) do { memcpy(p, &(x), sizeof(x)); p += sizeof(x); } while (0)
+uint64_t svxo_occ_save_mem(svxo_occ* m, uint8_t* buf, uint64_t cap) {
+    const int K = m->cfg.num_labels;
+    uint64_t size = 5 + 4 + 4 + 16 + 8;
+    for (uint64_t i = 0; i < m->n; ++i)
+        size += 12 + 3 * 4 * KV + 1 + (m->blocks[i]->hist ? (uint64_t)KV * K * 4 : 0);
+    if (!buf) return size;
+    if (cap < size) return 0;
+    oocc_block** sorted = malloc((m->n + 1) * sizeof(oocc_block*));
+    memcpy(sorted, m->blocks, m->n * sizeof(oocc_block*));
+    qsort(sorted, m->n, sizeof(oocc_block*), cmp_occptr);
+    uint8_t* p = buf;
+    memcpy(p, "SOCC1", 5);
+    p += 5;
+    PUT(m->cfg.voxel_size);
+    const uint32_t k32 = (uint32_t)K;
+    PUT(k32);
+    PUT(m->cfg.l_hit);
+    PUT(m->cfg.l_miss);
+    PUT(m->cfg.l_min);
+    PUT(m->cfg.l_max);
+    const uint64_t nb = m->n;
+    PUT(nb);
+    for (uint64_t i = 0; i < m->n; ++i) {
+        const oocc_block* b = sorted[i];
+        memcpy(p, b->key, 12);
+        p += 12;
+        memcpy(p, b->L, 4 * KV);
+        p += 4 * KV;
+        memcpy(p, b->hits, 4 * KV);
+        p += 4 * KV;
+        memcpy(p, b->misses, 4 * KV);
+        p += 4 * KV;
+        *p++ = b->hist != NULL;
+        if (b->hist) {
+            memcpy(p, b->hist, (size_t)KV * K * 4);
+            p += (size_t)KV * K * 4;
+        }
+    }
+    free(sorted);
+    return size;
+}
+#undef PUT

@@ -56,6 +56,13 @@ int svxo_mesh_extract(svxo_map* m, float min_weight, int32_t reserved, const int
                       uint64_t n, uint64_t* n_vertices, uint64_t* n_faces);
 void svxo_mesh_read(const svxo_map* m, float* vertices, float* normals, uint8_t* labels,
                     uint32_t* faces);
+/* Occupancy extension (include/svx.h): PARITY UNPINNED, no reference implementation. */
+typedef struct svxo_occ svxo_occ;
+svxo_occ* svxo_occ_create(const svx_occ_cfg* cfg);
+void svxo_occ_destroy(svxo_occ* m);
+int svxo_occ_integrate(svxo_occ* m, const float* pts, const uint16_t* labels, const float* conf,
+                       uint64_t n, int32_t stride, const svx_pose* pose, svx_occ_report* rep);
+uint64_t svxo_occ_save_mem(svxo_occ* m, uint8_t* buf, uint64_t cap);
 const char* svxo_last_error(void);
 
 #ifdef __cplusplus

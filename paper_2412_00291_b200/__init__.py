@@ -138,6 +138,22 @@ BLOCK_VOXELS = 512
 _lib: Optional[C.CDLL] = None
 
 
+class OccCfgC(C.Structure):
+    _fields_ = [("voxel_size", C.c_float), ("num_labels", C.c_int32), ("max_blocks", C.c_uint32),
+                ("l_hit", C.c_float), ("l_miss", C.c_float), ("l_min", C.c_float),
+                ("l_max", C.c_float), ("min_range", C.c_double), ("max_range", C.c_double),
+                ("carve", C.c_int32)]
+
+
+class OccReportC(C.Structure):
+    _fields_ = [("frame", C.c_int32), ("points", C.c_uint64), ("rays", C.c_uint64),
+                ("hit_voxels", C.c_uint64), ("miss_voxels", C.c_uint64),
+                ("new_blocks", C.c_uint64), ("elapsed_ms", C.c_double)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 def _sig(lib: C.CDLL) -> None:
     P = C.c_void_p
     S = C.c_int
@@ -193,6 +209,17 @@ def _sig(lib: C.CDLL) -> None:
                                  C.POINTER(C.c_uint64)]),
         "svx_mesh_read": (S, [P, P, P, P, P]),
         "svx_mesh_device": (S, [P, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P)]),
+        "svx_default_occ_cfg": (None, [C.POINTER(OccCfgC)]),
+        "svx_occ_create": (S, [C.POINTER(OccCfgC), C.c_int, C.POINTER(P)]),
+        "svx_occ_destroy": (S, [P]),
+        "svx_occ_get_stream": (S, [P, C.POINTER(P)]),
+        "svx_occ_set_shard": (S, [P, C.c_int32, C.c_int32]),
+        "svx_occ_integrate": (S, [P, P, P, P, C.c_uint64, C.c_int32, C.c_int32, C.POINTER(PoseC),
+                                  C.POINTER(OccReportC)]),
+        "svx_occ_integrate_batch": (S, [P, P, P, P, P, C.c_int32, C.c_int32, P, C.c_int32, P]),
+        "svx_occ_lookup": (S, [P, P, C.c_uint64, P, P, P, P, P, P]),
+        "svx_occ_block_count": (S, [P, C.POINTER(C.c_uint64)]),
+        "svx_occ_save_mem": (S, [P, P, C.c_uint64, C.POINTER(C.c_uint64)]),
     }
     for name, (res, args) in f.items():
         fn = getattr(lib, name)
@@ -844,6 +871,106 @@ class IncrementalMesher:
         return self.mesh
 
 
+# ------------------------------------------------------- occupancy extension
+
+
+@dataclass
+class OccupancyConfig:
+    """svx_occ_cfg (include/svx.h): free-space carving + log-odds + hit/miss counters +
+    integer class histograms. No reference implementation (parity unpinned)."""
+    voxel_size: float = 0.1
+    num_labels: int = 20
+    max_blocks: int = 1 << 20
+    l_hit: float = 0.85
+    l_miss: float = -0.4
+    l_min: float = -2.0
+    l_max: float = 3.5
+    min_range: float = 0.3
+    max_range: float = 70.0
+    carve: bool = True
+
+    def c(self) -> OccCfgC:
+        return OccCfgC(self.voxel_size, self.num_labels, self.max_blocks, self.l_hit, self.l_miss,
+                       self.l_min, self.l_max, self.min_range, self.max_range, int(self.carve))
+
+
+class OccupancyMap:
+    """Device occupancy map (svx_occ_*)."""
+
+    def __init__(self, cfg: OccupancyConfig = None, device: int = 0):
+        self.cfg = cfg or OccupancyConfig()
+        self.device = device
+        h = C.c_void_p()
+        _check(lib().svx_occ_create(C.byref(self.cfg.c()), device, C.byref(h)))
+        self._h = h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().svx_occ_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_shard(self, rank: int, world: int) -> None:
+        _check(lib().svx_occ_set_shard(self._h, rank, world))
+
+    def integrate(self, points, pose, labels=None, conf=None) -> OccReportC:
+        p, stride = _as_points(points)
+        n = p.shape[0]
+        lb = None if labels is None else np.ascontiguousarray(labels, np.uint16)
+        cf = None if conf is None else np.ascontiguousarray(conf, np.float32)
+        rep = OccReportC()
+        _check(lib().svx_occ_integrate(self._h, _ptr(p), _ptr(lb), _ptr(cf), n, stride, 0,
+                                       C.byref(pose), C.byref(rep)))
+        return rep
+
+    def integrate_batch_device(self, d_points_ptr: int, offsets: np.ndarray, stride: int, poses,
+                               d_labels_ptr: int = 0, d_conf_ptr: int = 0) -> list:
+        """Scans already in HBM (device pointers, e.g. torch tensor .data_ptr())."""
+        offs = np.ascontiguousarray(offsets, np.uint64)
+        nf = len(offs) - 1
+        pa = (PoseC * nf)(*poses)
+        reps = (OccReportC * nf)()
+        _check(lib().svx_occ_integrate_batch(self._h, C.c_void_p(d_points_ptr),
+                                             C.c_void_p(d_labels_ptr or None),
+                                             C.c_void_p(d_conf_ptr or None), _ptr(offs), stride, 1,
+                                             pa, nf, reps))
+        return list(reps)
+
+    def lookup(self, coords) -> dict:
+        v = np.ascontiguousarray(np.asarray(coords, np.int32).reshape(-1, 3))
+        n, K = v.shape[0], self.cfg.num_labels
+        out = {"log_odds": np.zeros(n, np.float32), "hits": np.zeros(n, np.uint32),
+               "misses": np.zeros(n, np.uint32), "hist": np.zeros((n, K), np.uint32),
+               "label": np.zeros(n, np.int32), "found": np.zeros(n, np.uint8)}
+        if n:
+            _check(lib().svx_occ_lookup(self._h, _ptr(v), n, _ptr(out["log_odds"]), _ptr(out["hits"]),
+                                        _ptr(out["misses"]), _ptr(out["hist"]), _ptr(out["label"]),
+                                        _ptr(out["found"])))
+        out["found"] = out["found"].astype(bool)
+        return out
+
+    def block_count(self) -> int:
+        n = C.c_uint64()
+        _check(lib().svx_occ_block_count(self._h, C.byref(n)))
+        return int(n.value)
+
+    def save_bytes(self) -> bytes:
+        n = C.c_uint64()
+        _check(lib().svx_occ_save_mem(self._h, None, 0, C.byref(n)))
+        buf = np.zeros(n.value, np.uint8)
+        _check(lib().svx_occ_save_mem(self._h, _ptr(buf), n.value, C.byref(n)))
+        return buf.tobytes()
+
+
 def block_owner(bc, world: int) -> int:
     return int(lib().svx_block_owner(_i3(bc), world))
 
@@ -854,5 +981,5 @@ __all__ = [
     "SemanticIntegrator", "LabelImage", "Pose", "pose_c", "CapacityError", "DataError",
     "InvalidArgument", "CudaError", "NotFound", "PROJECTIVE", "NON_PROJECTIVE", "SURROGATE",
     "RAYCAST", "TSDF_DTYPE", "lib", "declared_symbols", "kernel_launches", "block_owner",
-    "LabeledMesh", "extract_mesh", "IncrementalMesher", "DEFAULT_MESH_MIN_WEIGHT", "UNLABELED",
+    "OccupancyConfig", "OccupancyMap", "LabeledMesh", "extract_mesh", "IncrementalMesher", "DEFAULT_MESH_MIN_WEIGHT", "UNLABELED",
 ]

@@ -313,6 +313,8 @@ svx_map* load_svox1(const std::vector<uint8_t>& buf, int device, uint32_t max_bl
 
 }  // namespace
 
+void set_last_error(const char* msg) { g_last_error = msg; }
+
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 Model make_model(const svx_lidar_model& lm) {

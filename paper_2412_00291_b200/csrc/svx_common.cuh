@@ -11,6 +11,7 @@
 
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <math_constants.h>
 
 #include "../../include/svx.h"
 
@@ -182,6 +183,51 @@ __device__ inline void world_to_voxel(d3 p, double inv, int32_t c[3]) {
 // block_of / local_index for kBlockSide = 8: floor_div == arithmetic shift,
 // nonneg_mod == & 7 on two's complement (types.hpp:35-44, 81-89).
 __host__ __device__ inline int32_t block_coord(int32_t c) { return c >> 3; }
+
+// traverse_segment (tsdf_integrator.hpp:93-135); visit(x, y, z) per cell.
+// (shared by the TSDF band and the occupancy carving)
+template <typename Visit>
+__device__ inline void traverse_segment(d3 a, d3 b, double nu, double inv, Visit&& visit) {
+    int32_t cur[3], end[3];
+    world_to_voxel(a, inv, cur);
+    world_to_voxel(b, inv, end);
+    d3 dir = sub3(b, a);
+    const double len = sqrt(dot3(dir, dir));
+    if (len < 1e-12) {
+        visit(cur[0], cur[1], cur[2]);
+        return;
+    }
+    dir = div3(dir, len);
+    const double dv[3] = {dir.x, dir.y, dir.z};
+    const double av[3] = {a.x, a.y, a.z};
+    int32_t step[3];
+    double t_max[3], t_delta[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        if (fabs(dv[i]) < 1e-15) {
+            step[i] = 0;
+            t_max[i] = CUDART_INF;
+            t_delta[i] = CUDART_INF;
+        } else {
+            step[i] = dv[i] > 0 ? 1 : -1;
+            const double boundary = nu * (double(cur[i]) + 0.5 * step[i]);
+            t_max[i] = (boundary - av[i]) / dv[i];
+            t_delta[i] = nu / fabs(dv[i]);
+        }
+    }
+    const uint64_t max_steps = uint64_t(3.0 * len / nu) + 8;
+    for (uint64_t n = 0; n < max_steps; ++n) {
+        visit(cur[0], cur[1], cur[2]);
+        if (cur[0] == end[0] && cur[1] == end[1] && cur[2] == end[2]) return;
+        int m = 0;
+        if (t_max[1] < t_max[m]) m = 1;
+        if (t_max[2] < t_max[m]) m = 2;
+        if (t_max[m] > len) return;
+        cur[m] += step[m];
+        t_max[m] += t_delta[m];
+    }
+}
+
 __host__ __device__ inline int local_linear(int32_t x, int32_t y, int32_t z) {
     return (x & 7) + 8 * (y & 7) + 64 * (z & 7);
 }

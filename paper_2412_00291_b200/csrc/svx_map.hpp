@@ -74,6 +74,27 @@ private:
     std::vector<std::pair<CUmemGenericAllocationHandle, size_t>> chunks_;
 };
 
+// Records the message svx_last_error() returns on this thread (svx_capi.cu).
+void set_last_error(const char* msg);
+
+// Runs fn, mapping exceptions to svx_status + svx_last_error (the C-ABI contract).
+template <typename Fn>
+svx_status api_guard(Fn&& fn) {
+    try {
+        fn();
+        return SVX_OK;
+    } catch (const Error& e) {
+        set_last_error(e.what());
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        set_last_error("host allocation failed");
+        return SVX_DATA;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return SVX_DATA;
+    }
+}
+
 template <typename T>
 struct DevBuf {
     T* p = nullptr;

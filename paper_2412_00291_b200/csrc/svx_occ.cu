@@ -1,0 +1,697 @@
+// Occupancy extension (include/svx.h "occupancy extension"):
+// free-space carving with the reference's 3D-DDA (traverse_segment,
+// tsdf_integrator.hpp:93-135), per-scan HIT/MISS deduplication, f32 log-odds with
+// clamping, hit/miss counters and u32 class histograms for per-point labels.
+//
+// Map: its own open-addressing block hash (the TSDF map's HashView code) and a CUDA
+// VMM pool of 8 KB occupancy blocks, SoA inside a block so the fold is coalesced:
+//     u32 tag[512] | f32 log_odds[512] | u32 hits[512] | u32 misses[512]
+// plus lazily allocated histogram layers [512][K] u32 for blocks that received a
+// labelled hit.
+//
+// Per scan (one host synchronisation, to map pool memory for the scan's new blocks):
+//   k_occ_alloc  thread per point: the ray's DDA at voxel resolution, touching each
+//                block once per run of voxels (hash find-or-insert, pool index from a
+//                counter, first touch this scan -> touched-block list); histogram
+//                layer claimed for the hit block of a labelled point.
+//   k_occ_visit  thread per point: the same DDA; per voxel tag = max(tag, 4*S + kind)
+//                with kind HIT = 3 > MISS = 1, so HIT wins and the result does not
+//                depend on ray order (a plain load skips the atomic once the tag
+//                already holds this scan's value - the voxels near the sensor are
+//                crossed by every ray); labelled hits add q8(conf) to the histogram.
+//   k_occ_fold   CTA per touched block, thread per voxel: voxels whose tag carries
+//                this scan's serial S get their one log-odds / counter update.
+// Deduplication is per-voxel tag based (no sort): tags carry the scan serial, so no
+// clearing pass is needed between scans.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "svx_map.hpp"
+
+namespace svx {
+namespace {
+
+constexpr int kOccWords = 4 * kBlockVoxels;  // u32 words per occupancy block
+constexpr size_t kOccBlockBytes = 4ull * kOccWords;
+constexpr uint32_t kClaim = 0xFFFFFFFEu;     // histogram layer being allocated
+constexpr uint32_t kOverflow = 0xFFFFFFFDu;  // block beyond max_blocks
+constexpr int kHit = 3, kMiss = 1;
+
+enum OccCounter : int {
+    O_BLOCKS = 0, O_LAYERS, O_TOUCHED, O_ERR_CAP, O_ERR_KEY, O_ERR_HASH, O_HITV, O_MISSV,
+    O_RAYS, O_COUNT
+};
+
+struct OccParams {
+    Pose T;
+    double nu, inv_nu, min_r, max_r;
+    const float* pts;
+    const uint16_t* lbl;
+    const float* conf;
+    uint64_t n;
+    int stride, carve, K;
+    uint32_t serial, max_blocks;
+    int32_t shard_rank, shard_world;
+};
+
+struct OccDev {
+    HashView h;
+    uint32_t* pool;       // [blocks][kOccWords]
+    uint32_t* hist;       // [layers][512][K]
+    uint64_t* block_keys;
+    uint32_t* hist_idx;
+    uint32_t* block_tag;
+    uint32_t* touched;
+    uint32_t* ctr;
+};
+
+// The ray of point i (svx.h contract): false when the point is dropped.
+__device__ inline bool point_ray(const OccParams& p, uint64_t i, d3& o, d3& end, bool& hit) {
+    const float* q = p.pts + i * uint64_t(p.stride);
+    const float x = q[0], y = q[1], z = q[2];
+    if (!(isfinite(x) && isfinite(y) && isfinite(z))) return false;
+    const d3 ps = mk(x, y, z);
+    const double r = sqrt(dot3(ps, ps));
+    if (r < p.min_r) return false;
+    const d3 pw = xform(p.T, ps);
+    o = mk(p.T.t[0], p.T.t[1], p.T.t[2]);
+    hit = r <= p.max_r;
+    end = hit ? pw : add3(o, scale3(p.max_r / r, sub3(pw, o)));
+    return true;
+}
+
+__device__ inline uint32_t claim_block(const OccParams& p, const OccDev& d, uint64_t key) {
+    int ins = 0;
+    const uint32_t s = hash_insert(d.h, key, &ins);
+    if (s == kInvalid) {
+        atomicAdd(&d.ctr[O_ERR_HASH], 1u);
+        return kInvalid;
+    }
+    uint32_t idx;
+    if (ins) {
+        idx = atomicAdd(&d.ctr[O_BLOCKS], 1u);
+        if (idx >= p.max_blocks) {
+            atomicAdd(&d.ctr[O_ERR_CAP], 1u);
+            idx = kOverflow;
+        } else {
+            d.block_keys[idx] = key;
+        }
+        __threadfence();
+        atomicExch(&d.h.vals[s], idx);
+    } else {
+        volatile uint32_t* v = d.h.vals + s;
+        while ((idx = *v) == kInvalid) {
+        }
+    }
+    if (idx == kOverflow) return kInvalid;
+    if (__ldcg(&d.block_tag[idx]) != p.serial && atomicExch(&d.block_tag[idx], p.serial) != p.serial)
+        d.touched[atomicAdd(&d.ctr[O_TOUCHED], 1u)] = idx;
+    return idx;
+}
+
+__device__ inline uint32_t find_block(const OccDev& d, uint64_t key) {
+    const uint32_t s = hash_find(d.h, key);
+    return s == kInvalid ? kInvalid : __ldcg(&d.h.vals[s]);
+}
+
+__device__ inline bool owned(const OccParams& p, uint64_t key) {
+    return p.shard_world <= 1 || owner_of(key, p.shard_world) == p.shard_rank;
+}
+
+__device__ inline uint32_t label_of(const OccParams& p, uint64_t i) {
+    return p.lbl ? uint32_t(p.lbl[i]) : 0xFFFFFFFFu;
+}
+
+__device__ inline uint32_t q8(const OccParams& p, uint64_t i) {
+    if (!p.conf) return 255u;
+    const float c = p.conf[i];
+    if (!isfinite(c)) return 0u;
+    const float cc = c < 0.f ? 0.f : (c > 1.f ? 1.f : c);
+    return uint32_t(cc * 255.f + 0.5f);
+}
+
+// Visits the ray's voxels (carving) then the hit voxel; fn(x, y, z, kind).
+template <typename Fn>
+__device__ inline void for_each_ray_voxel(const OccParams& p, d3 o, d3 end, bool hit, Fn&& fn) {
+    int32_t ev[3];
+    world_to_voxel(end, p.inv_nu, ev);
+    if (p.carve)
+        traverse_segment(o, end, p.nu, p.inv_nu, [&](int32_t x, int32_t y, int32_t z) {
+            if (hit && x == ev[0] && y == ev[1] && z == ev[2]) return;
+            fn(x, y, z, kMiss);
+        });
+    if (hit) fn(ev[0], ev[1], ev[2], kHit);
+}
+
+__global__ void __launch_bounds__(256) k_occ_alloc(OccParams p, OccDev d) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= p.n) return;
+    d3 o, end;
+    bool hit;
+    if (!point_ray(p, i, o, end, hit)) return;
+    atomicAdd(&d.ctr[O_RAYS], 1u);
+    uint64_t last = kEmptyKey;
+    uint32_t last_idx = kInvalid;
+    const uint32_t lab = label_of(p, i);
+    for_each_ray_voxel(p, o, end, hit, [&](int32_t x, int32_t y, int32_t z, int kind) {
+        const int32_t bx = block_coord(x), by = block_coord(y), bz = block_coord(z);
+        if (!(key_in_range(bx) && key_in_range(by) && key_in_range(bz))) {
+            atomicAdd(&d.ctr[O_ERR_KEY], 1u);
+            return;
+        }
+        const uint64_t key = pack_key(bx, by, bz);
+        if (key != last) {
+            last = key;
+            last_idx = owned(p, key) ? claim_block(p, d, key) : kInvalid;
+        }
+        if (kind == kHit && last_idx != kInvalid && lab < uint32_t(p.K) &&
+            __ldcg(&d.hist_idx[last_idx]) == kInvalid &&
+            atomicCAS(&d.hist_idx[last_idx], kInvalid, kClaim) == kInvalid)
+            atomicExch(&d.hist_idx[last_idx], atomicAdd(&d.ctr[O_LAYERS], 1u));
+    });
+}
+
+__global__ void __launch_bounds__(256) k_occ_visit(OccParams p, OccDev d) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= p.n) return;
+    d3 o, end;
+    bool hit;
+    if (!point_ray(p, i, o, end, hit)) return;
+    uint64_t last = kEmptyKey;
+    uint32_t* base = nullptr;
+    uint32_t idx = kInvalid;
+    const uint32_t lab = label_of(p, i);
+    const uint32_t tag_base = p.serial * 4u;
+    for_each_ray_voxel(p, o, end, hit, [&](int32_t x, int32_t y, int32_t z, int kind) {
+        const int32_t bx = block_coord(x), by = block_coord(y), bz = block_coord(z);
+        if (!(key_in_range(bx) && key_in_range(by) && key_in_range(bz))) return;
+        const uint64_t key = pack_key(bx, by, bz);
+        if (key != last) {
+            last = key;
+            idx = owned(p, key) ? find_block(d, key) : kInvalid;
+            base = idx < p.max_blocks ? d.pool + uint64_t(idx) * kOccWords : nullptr;
+        }
+        if (!base) return;
+        const int lin = local_linear(x, y, z);
+        const uint32_t want = tag_base + uint32_t(kind);
+        if (__ldcg(&base[lin]) < want) atomicMax(&base[lin], want);
+        if (kind == kHit && lab < uint32_t(p.K)) {
+            const uint32_t layer = __ldcg(&d.hist_idx[idx]);
+            atomicAdd(&d.hist[(uint64_t(layer) * kBlockVoxels + lin) * p.K + lab], q8(p, i));
+        }
+    });
+}
+
+struct FoldParams {
+    uint32_t serial;
+    float l_hit, l_miss, l_min, l_max;
+};
+
+__global__ void __launch_bounds__(kBlockVoxels) k_occ_fold(FoldParams fp, OccDev d) {
+    const uint32_t idx = d.touched[blockIdx.x];
+    uint32_t* base = d.pool + uint64_t(idx) * kOccWords;
+    const int v = threadIdx.x;
+    const uint32_t tag = base[v];
+    uint32_t nh = 0, nm = 0;
+    if ((tag >> 2) == fp.serial) {
+        float* L = reinterpret_cast<float*>(base + kBlockVoxels);
+        float l = L[v];
+        if ((tag & 3u) == uint32_t(kHit)) {
+            const float t = l + fp.l_hit;
+            l = t > fp.l_max ? fp.l_max : t;
+            base[2 * kBlockVoxels + v] += 1u;
+            nh = 1;
+        } else {
+            const float t = l + fp.l_miss;
+            l = t < fp.l_min ? fp.l_min : t;
+            base[3 * kBlockVoxels + v] += 1u;
+            nm = 1;
+        }
+        L[v] = l;
+    }
+    nh = __reduce_add_sync(0xFFFFFFFFu, nh);
+    nm = __reduce_add_sync(0xFFFFFFFFu, nm);
+    if ((threadIdx.x & 31) == 0) {
+        if (nh) atomicAdd(&d.ctr[O_HITV], nh);
+        if (nm) atomicAdd(&d.ctr[O_MISSV], nm);
+    }
+}
+
+// capacity rollback: histogram layers claimed by the rejected scan
+__global__ void k_occ_unclaim(uint32_t* __restrict__ hist_idx, uint32_t n_blocks, uint32_t keep) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n_blocks && hist_idx[i] != kInvalid && hist_idx[i] >= keep) hist_idx[i] = kInvalid;
+}
+
+__global__ void k_occ_rebuild(HashView h, const uint64_t* __restrict__ keys, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int ins = 0;
+    const uint32_t s = hash_insert(h, keys[i], &ins);
+    if (s != kInvalid) h.vals[s] = i;
+}
+
+__global__ void k_occ_lookup(OccDev d, int K, const int32_t* __restrict__ v, uint64_t n,
+                             float* __restrict__ lo, uint32_t* __restrict__ hits,
+                             uint32_t* __restrict__ misses, uint32_t* __restrict__ hist,
+                             int32_t* __restrict__ label, uint8_t* __restrict__ found) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t x = v[3 * i], y = v[3 * i + 1], z = v[3 * i + 2];
+    const int32_t bx = block_coord(x), by = block_coord(y), bz = block_coord(z);
+    uint32_t idx = kInvalid;
+    if (key_in_range(bx) && key_in_range(by) && key_in_range(bz)) idx = find_block(d, pack_key(bx, by, bz));
+    if (idx == kInvalid || idx == kOverflow) {
+        if (found) found[i] = 0;
+        if (label) label[i] = -1;
+        return;
+    }
+    const int lin = local_linear(x, y, z);
+    const uint32_t* b = d.pool + uint64_t(idx) * kOccWords;
+    if (found) found[i] = 1;
+    if (lo) lo[i] = __uint_as_float(b[kBlockVoxels + lin]);
+    if (hits) hits[i] = b[2 * kBlockVoxels + lin];
+    if (misses) misses[i] = b[3 * kBlockVoxels + lin];
+    const uint32_t layer = d.hist_idx[idx];
+    int best = -1;
+    uint32_t best_c = 0;
+    for (int k = 0; k < K; ++k) {
+        const uint32_t c = layer == kInvalid ? 0u : d.hist[(uint64_t(layer) * kBlockVoxels + lin) * K + k];
+        if (hist) hist[i * K + k] = c;
+        if (c > best_c) {
+            best_c = c;
+            best = k;
+        }
+    }
+    if (label) label[i] = best;
+}
+
+inline unsigned grid256(uint64_t n) { return unsigned((n + 255) / 256); }
+
+template <typename T>
+T* dmalloc(size_t n) {
+    T* p = nullptr;
+    SVX_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    return p;
+}
+
+void require(bool ok, svx_status s, const char* msg) {
+    if (!ok) throw Error(s, msg);
+}
+
+struct DevGuard {
+    int prev = 0;
+    explicit DevGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) SVX_CUDA(cudaSetDevice(dev));
+    }
+    ~DevGuard() {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (cur != prev) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace
+}  // namespace svx
+
+struct svx_occ {
+    svx_occ_cfg cfg{};
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int32_t shard_rank = 0, shard_world = 1;
+    int log2cap = 0;
+    uint32_t cap = 0;
+    uint64_t* keys = nullptr;
+    uint32_t* vals = nullptr;
+    svx::VmmArray pool;   // [blocks][4 x 512] u32
+    svx::VmmArray hist;   // [layers][512][K] u32
+    size_t layer_bytes = 0;
+    uint64_t* block_keys = nullptr;
+    uint32_t* hist_idx = nullptr;
+    uint32_t* block_tag = nullptr;
+    uint32_t* touched = nullptr;
+    uint32_t* d_ctr = nullptr;
+    uint32_t* h_ctr = nullptr;
+    uint32_t serial = 0;
+    int32_t frames = 0;
+    uint64_t n_blocks = 0, n_layers = 0;
+    svx::DevBuf<float> pts;
+    svx::DevBuf<uint16_t> lbl;
+    svx::DevBuf<float> conf;
+};
+
+namespace svx {
+namespace {
+
+OccDev occ_dev(svx_occ* m) {
+    return OccDev{HashView{m->keys, m->vals, m->log2cap, m->cap - 1},
+                  static_cast<uint32_t*>(m->pool.base()), static_cast<uint32_t*>(m->hist.base()),
+                  m->block_keys, m->hist_idx, m->block_tag, m->touched, m->d_ctr};
+}
+
+void free_occ(svx_occ* m) {
+    if (!m) return;
+    cudaSetDevice(m->device);
+    if (m->stream) cudaStreamSynchronize(m->stream);
+    for (void* p : {(void*)m->keys, (void*)m->vals, (void*)m->block_keys, (void*)m->hist_idx,
+                    (void*)m->block_tag, (void*)m->touched, (void*)m->d_ctr})
+        if (p) cudaFree(p);
+    if (m->h_ctr) cudaFreeHost(m->h_ctr);
+    m->pts.release();
+    m->lbl.release();
+    m->conf.release();
+    if (m->stream) cudaStreamDestroy(m->stream);
+    delete m;
+}
+
+void validate(const svx_occ_cfg& c) {
+    require(c.voxel_size > 0.f, SVX_INVALID_ARGUMENT, "voxel_size must be > 0");
+    require(c.num_labels >= 1 && c.num_labels <= 64, SVX_INVALID_ARGUMENT, "num_labels must be in [1, 64]");
+    require(c.max_blocks != 0 && c.max_blocks < (1u << 25), SVX_INVALID_ARGUMENT,
+            "max_blocks must be in [1, 2^25)");
+    require(c.l_hit >= 0.f && c.l_miss <= 0.f && c.l_min <= 0.f && c.l_max >= 0.f,
+            SVX_INVALID_ARGUMENT, "log-odds: need l_hit >= 0, l_miss <= 0, l_min <= 0 <= l_max");
+    require(c.min_range >= 0.0 && c.max_range > c.min_range, SVX_INVALID_ARGUMENT,
+            "ranges: need 0 <= min_range < max_range");
+}
+
+// One scan; points / labels / conf already on the device.
+void occ_scan(svx_occ* m, const float* d_pts, const uint16_t* d_lbl, const float* d_conf, uint64_t n,
+              int stride, const svx_pose& pose, svx_occ_report* rep) {
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaStream_t st = m->stream;
+    require(m->serial + 1 < (1u << 30), SVX_INVALID_ARGUMENT, "too many scans for one occupancy map");
+    m->serial += 1;
+    OccParams p{};
+    p.T = to_pose(pose);
+    p.nu = double(m->cfg.voxel_size);
+    p.inv_nu = 1.0 / double(m->cfg.voxel_size);
+    p.min_r = m->cfg.min_range;
+    p.max_r = m->cfg.max_range;
+    p.pts = d_pts;
+    p.lbl = d_lbl;
+    p.conf = d_conf;
+    p.n = n;
+    p.stride = stride;
+    p.carve = m->cfg.carve;
+    p.K = m->cfg.num_labels;
+    p.serial = m->serial;
+    p.max_blocks = m->cfg.max_blocks;
+    p.shard_rank = m->shard_rank;
+    p.shard_world = m->shard_world;
+    // per-scan counters (blocks / layers persist)
+    m->h_ctr[O_BLOCKS] = uint32_t(m->n_blocks);
+    m->h_ctr[O_LAYERS] = uint32_t(m->n_layers);
+    for (int c = O_TOUCHED; c < O_COUNT; ++c) m->h_ctr[c] = 0;
+    SVX_CUDA(cudaMemcpyAsync(m->d_ctr, m->h_ctr, 4 * O_COUNT, cudaMemcpyHostToDevice, st));
+    OccDev d = occ_dev(m);
+    if (n) {
+        k_occ_alloc<<<grid256(n), 256, 0, st>>>(p, d);
+        count_launch();
+    }
+    SVX_CUDA(cudaMemcpyAsync(m->h_ctr, m->d_ctr, 4 * O_COUNT, cudaMemcpyDeviceToHost, st));
+    SVX_CUDA(cudaStreamSynchronize(st));
+    const uint64_t old_blocks = m->n_blocks, old_layers = m->n_layers;
+    if (m->h_ctr[O_ERR_KEY] || m->h_ctr[O_ERR_HASH] || m->h_ctr[O_ERR_CAP]) {
+        // reject the scan: drop its new blocks and histogram claims
+        SVX_CUDA(cudaMemsetAsync(m->keys, 0xFF, 8ull * m->cap, st));
+        SVX_CUDA(cudaMemsetAsync(m->vals, 0xFF, 4ull * m->cap, st));
+        if (old_blocks) {
+            k_occ_rebuild<<<grid256(old_blocks), 256, 0, st>>>(d.h, m->block_keys, uint32_t(old_blocks));
+            k_occ_unclaim<<<grid256(old_blocks), 256, 0, st>>>(m->hist_idx, uint32_t(old_blocks),
+                                                               uint32_t(old_layers));
+            count_launch(2);
+        }
+        const uint64_t over = std::min<uint64_t>(m->h_ctr[O_BLOCKS], m->cfg.max_blocks);
+        if (over > old_blocks)
+            SVX_CUDA(cudaMemsetAsync(m->hist_idx + old_blocks, 0xFF, 4 * (over - old_blocks), st));
+        SVX_CUDA(cudaStreamSynchronize(st));
+        if (m->h_ctr[O_ERR_KEY])
+            throw Error(SVX_INVALID_ARGUMENT, "voxel outside the device key range [-2^23, 2^23)");
+        if (m->h_ctr[O_ERR_HASH]) throw Error(SVX_CAPACITY, "occupancy block hash is full");
+        throw Error(SVX_CAPACITY, "occupancy map: max_blocks reached");
+    }
+    m->n_blocks = m->h_ctr[O_BLOCKS];
+    m->n_layers = m->h_ctr[O_LAYERS];
+    const uint32_t touched = m->h_ctr[O_TOUCHED];
+    const uint64_t rays = m->h_ctr[O_RAYS];
+    if (m->n_blocks > old_blocks) {  // map + zero the new blocks (tags 0 < any serial)
+        m->pool.ensure(m->n_blocks * kOccBlockBytes);
+        SVX_CUDA(cudaMemsetAsync(static_cast<uint8_t*>(m->pool.base()) + old_blocks * kOccBlockBytes, 0,
+                                 (m->n_blocks - old_blocks) * kOccBlockBytes, st));
+        m->pool.prefetch(std::min<uint64_t>(m->cfg.max_blocks, 2 * m->n_blocks + 65536) * kOccBlockBytes);
+    }
+    if (m->n_layers > old_layers) {
+        m->hist.ensure(m->n_layers * m->layer_bytes);
+        SVX_CUDA(cudaMemsetAsync(static_cast<uint8_t*>(m->hist.base()) + old_layers * m->layer_bytes, 0,
+                                 (m->n_layers - old_layers) * m->layer_bytes, st));
+    }
+    d = occ_dev(m);
+    if (n) {
+        k_occ_visit<<<grid256(n), 256, 0, st>>>(p, d);
+        count_launch();
+    }
+    if (touched) {
+        const FoldParams fp{m->serial, m->cfg.l_hit, m->cfg.l_miss, m->cfg.l_min, m->cfg.l_max};
+        k_occ_fold<<<touched, kBlockVoxels, 0, st>>>(fp, d);
+        count_launch();
+    }
+    SVX_CUDA(cudaGetLastError());
+    SVX_CUDA(cudaMemcpyAsync(m->h_ctr + O_HITV, m->d_ctr + O_HITV, 8, cudaMemcpyDeviceToHost, st));
+    SVX_CUDA(cudaStreamSynchronize(st));
+    if (rep) {
+        rep->frame = m->frames;
+        rep->points = n;
+        rep->rays = rays;
+        rep->hit_voxels = m->h_ctr[O_HITV];
+        rep->miss_voxels = m->h_ctr[O_MISSV];
+        rep->new_blocks = m->n_blocks - old_blocks;
+        rep->elapsed_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+    m->frames += 1;
+}
+
+template <typename T>
+const T* stage(svx_occ* m, DevBuf<T>& buf, const T* src, uint64_t count) {
+    if (!src) return nullptr;
+    buf.alloc(std::max<uint64_t>(count, 1));
+    SVX_CUDA(cudaMemcpyAsync(buf.p, src, sizeof(T) * count, cudaMemcpyHostToDevice, m->stream));
+    return buf.p;
+}
+
+}  // namespace
+}  // namespace svx
+
+using namespace svx;
+
+extern "C" {
+
+void svx_default_occ_cfg(svx_occ_cfg* c) {
+    c->voxel_size = 0.1f;
+    c->num_labels = 20;
+    c->max_blocks = 1u << 20;
+    c->l_hit = 0.85f;
+    c->l_miss = -0.4f;
+    c->l_min = -2.0f;
+    c->l_max = 3.5f;
+    c->min_range = 0.3;
+    c->max_range = 70.0;
+    c->carve = 1;
+}
+
+svx_status svx_occ_create(const svx_occ_cfg* cfg, int device, svx_occ** out) {
+    return api_guard([&] {
+        require(cfg && out, SVX_INVALID_ARGUMENT, "null argument");
+        validate(*cfg);
+        int ndev = 0;
+        SVX_CUDA(cudaGetDeviceCount(&ndev));
+        require(device >= 0 && device < ndev, SVX_INVALID_ARGUMENT, "no such CUDA device");
+        DevGuard g(device);
+        svx_occ* m = new svx_occ();
+        try {
+            m->cfg = *cfg;
+            m->device = device;
+            SVX_CUDA(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
+            const uint64_t want = std::max<uint64_t>(2ull * cfg->max_blocks, 1024);
+            while ((1ull << m->log2cap) < want) ++m->log2cap;
+            m->cap = uint32_t(1u << m->log2cap);
+            m->keys = dmalloc<uint64_t>(m->cap);
+            m->vals = dmalloc<uint32_t>(m->cap);
+            m->block_keys = dmalloc<uint64_t>(cfg->max_blocks);
+            m->hist_idx = dmalloc<uint32_t>(cfg->max_blocks);
+            m->block_tag = dmalloc<uint32_t>(cfg->max_blocks);
+            m->touched = dmalloc<uint32_t>(cfg->max_blocks);
+            m->d_ctr = dmalloc<uint32_t>(O_COUNT);
+            SVX_CUDA(cudaMallocHost(&m->h_ctr, 4 * O_COUNT));
+            std::memset(m->h_ctr, 0, 4 * O_COUNT);
+            SVX_CUDA(cudaMemsetAsync(m->keys, 0xFF, 8ull * m->cap, m->stream));
+            SVX_CUDA(cudaMemsetAsync(m->vals, 0xFF, 4ull * m->cap, m->stream));
+            SVX_CUDA(cudaMemsetAsync(m->hist_idx, 0xFF, 4ull * cfg->max_blocks, m->stream));
+            SVX_CUDA(cudaMemsetAsync(m->block_tag, 0, 4ull * cfg->max_blocks, m->stream));
+            m->layer_bytes = 4ull * kBlockVoxels * uint64_t(cfg->num_labels);
+            m->pool.reserve(device, size_t(cfg->max_blocks) * kOccBlockBytes);
+            m->hist.reserve(device, size_t(cfg->max_blocks) * m->layer_bytes);
+            SVX_CUDA(cudaStreamSynchronize(m->stream));
+        } catch (...) {
+            free_occ(m);
+            throw;
+        }
+        *out = m;
+    });
+}
+
+svx_status svx_occ_destroy(svx_occ* m) {
+    return api_guard([&] { free_occ(m); });
+}
+
+svx_status svx_occ_get_stream(svx_occ* m, void** stream) {
+    return api_guard([&] {
+        require(m && stream, SVX_INVALID_ARGUMENT, "null argument");
+        *stream = m->stream;
+    });
+}
+
+svx_status svx_occ_set_shard(svx_occ* m, int32_t rank, int32_t world) {
+    return api_guard([&] {
+        require(m && world >= 1 && rank >= 0 && rank < world, SVX_INVALID_ARGUMENT, "bad shard");
+        require(m->n_blocks == 0, SVX_INVALID_ARGUMENT, "set the shard before the first scan");
+        m->shard_rank = rank;
+        m->shard_world = world;
+    });
+}
+
+svx_status svx_occ_integrate(svx_occ* m, const float* points, const uint16_t* labels,
+                             const float* conf, uint64_t n, int32_t stride, int32_t on_device,
+                             const svx_pose* pose, svx_occ_report* rep) {
+    const uint64_t offs[2] = {0, n};
+    return svx_occ_integrate_batch(m, points, labels, conf, offs, stride, on_device, pose, 1, rep);
+}
+
+svx_status svx_occ_integrate_batch(svx_occ* m, const float* points, const uint16_t* labels,
+                                   const float* conf, const uint64_t* offs, int32_t stride,
+                                   int32_t on_device, const svx_pose* poses, int32_t n_frames,
+                                   svx_occ_report* reps) {
+    return api_guard([&] {
+        require(m && offs && poses && n_frames >= 0, SVX_INVALID_ARGUMENT, "null argument");
+        require(stride >= 3, SVX_INVALID_ARGUMENT, "stride must be >= 3");
+        DevGuard g(m->device);
+        for (int f = 0; f < n_frames; ++f) {
+            require(offs[f + 1] >= offs[f], SVX_INVALID_ARGUMENT, "offsets must be non-decreasing");
+            require(offs[f + 1] == offs[f] || points, SVX_INVALID_ARGUMENT, "null points");
+            validate_pose(poses[f]);
+            const uint64_t a = offs[f], n = offs[f + 1] - a;
+            const float* dp = points ? points + a * uint64_t(stride) : nullptr;
+            const uint16_t* dl = labels ? labels + a : nullptr;
+            const float* dc = conf ? conf + a : nullptr;
+            if (!on_device && n) {
+                dp = stage(m, m->pts, dp, n * uint64_t(stride));
+                dl = stage(m, m->lbl, dl, n);
+                dc = stage(m, m->conf, dc, n);
+            }
+            occ_scan(m, dp, dl, dc, n, stride, poses[f], reps ? reps + f : nullptr);
+        }
+    });
+}
+
+svx_status svx_occ_lookup(svx_occ* m, const int32_t* vxyz, uint64_t n, float* log_odds,
+                          uint32_t* hits, uint32_t* misses, uint32_t* hist, int32_t* label,
+                          uint8_t* found) {
+    return api_guard([&] {
+        require(m && (vxyz || !n), SVX_INVALID_ARGUMENT, "null argument");
+        if (!n) return;
+        DevGuard g(m->device);
+        const int K = m->cfg.num_labels;
+        DevBuf<int32_t> dv;
+        DevBuf<uint8_t> out;
+        dv.alloc(3 * n);
+        // outputs packed in one device buffer: lo | hits | misses | label | hist | found
+        const uint64_t b_lo = 0, b_h = b_lo + 4 * n, b_m = b_h + 4 * n, b_l = b_m + 4 * n,
+                       b_hist = b_l + 4 * n, b_f = b_hist + 4 * n * K, total = b_f + n;
+        out.alloc(total);
+        SVX_CUDA(cudaMemcpyAsync(dv.p, vxyz, 12 * n, cudaMemcpyHostToDevice, m->stream));
+        k_occ_lookup<<<grid256(n), 256, 0, m->stream>>>(
+            occ_dev(m), K, dv.p, n, reinterpret_cast<float*>(out.p + b_lo),
+            reinterpret_cast<uint32_t*>(out.p + b_h), reinterpret_cast<uint32_t*>(out.p + b_m),
+            reinterpret_cast<uint32_t*>(out.p + b_hist), reinterpret_cast<int32_t*>(out.p + b_l),
+            out.p + b_f);
+        count_launch();
+        std::vector<uint8_t> h(total);
+        SVX_CUDA(cudaMemcpyAsync(h.data(), out.p, total, cudaMemcpyDeviceToHost, m->stream));
+        SVX_CUDA(cudaStreamSynchronize(m->stream));
+        if (log_odds) std::memcpy(log_odds, h.data() + b_lo, 4 * n);
+        if (hits) std::memcpy(hits, h.data() + b_h, 4 * n);
+        if (misses) std::memcpy(misses, h.data() + b_m, 4 * n);
+        if (label) std::memcpy(label, h.data() + b_l, 4 * n);
+        if (hist) std::memcpy(hist, h.data() + b_hist, 4 * n * K);
+        if (found) std::memcpy(found, h.data() + b_f, n);
+        dv.release();
+        out.release();
+    });
+}
+
+svx_status svx_occ_block_count(svx_occ* m, uint64_t* n) {
+    return api_guard([&] {
+        require(m && n, SVX_INVALID_ARGUMENT, "null argument");
+        *n = m->n_blocks;
+    });
+}
+
+svx_status svx_occ_save_mem(svx_occ* m, uint8_t* buf, uint64_t cap, uint64_t* size) {
+    return api_guard([&] {
+        require(m && size, SVX_INVALID_ARGUMENT, "null argument");
+        DevGuard g(m->device);
+        SVX_CUDA(cudaStreamSynchronize(m->stream));
+        const uint64_t nb = m->n_blocks;
+        const int K = m->cfg.num_labels;
+        std::vector<uint32_t> hidx(nb);
+        if (nb) SVX_CUDA(cudaMemcpy(hidx.data(), m->hist_idx, 4 * nb, cudaMemcpyDeviceToHost));
+        uint64_t with_hist = 0;
+        for (uint32_t h : hidx) with_hist += h != kInvalid;
+        const uint64_t per_block = 12 + 3 * 4 * kBlockVoxels + 1;
+        const uint64_t total = 5 + 4 + 4 + 16 + 8 + nb * per_block + with_hist * m->layer_bytes;
+        *size = total;
+        if (!buf) return;
+        require(cap >= total, SVX_INVALID_ARGUMENT, "buffer too small");
+        std::vector<uint64_t> keys(nb);
+        std::vector<uint32_t> pool(nb * kOccWords);
+        std::vector<uint32_t> hist(m->n_layers * kBlockVoxels * uint64_t(K));
+        if (nb) {
+            SVX_CUDA(cudaMemcpy(keys.data(), m->block_keys, 8 * nb, cudaMemcpyDeviceToHost));
+            SVX_CUDA(cudaMemcpy(pool.data(), m->pool.base(), nb * kOccBlockBytes, cudaMemcpyDeviceToHost));
+        }
+        if (!hist.empty())
+            SVX_CUDA(cudaMemcpy(hist.data(), m->hist.base(), 4 * hist.size(), cudaMemcpyDeviceToHost));
+        std::vector<uint64_t> order(nb);
+        for (uint64_t i = 0; i < nb; ++i) order[i] = i;
+        std::sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) { return keys[a] < keys[b]; });
+        uint8_t* p = buf;
+        auto put = [&](const void* src, size_t len) {
+            std::memcpy(p, src, len);
+            p += len;
+        };
+        put("SOCC1", 5);
+        put(&m->cfg.voxel_size, 4);
+        const uint32_t k32 = uint32_t(K);
+        put(&k32, 4);
+        put(&m->cfg.l_hit, 4);
+        put(&m->cfg.l_miss, 4);
+        put(&m->cfg.l_min, 4);
+        put(&m->cfg.l_max, 4);
+        put(&nb, 8);
+        for (uint64_t i : order) {
+            int32_t b[3];
+            unpack_key(keys[i], b[0], b[1], b[2]);
+            put(b, 12);
+            put(&pool[i * kOccWords + kBlockVoxels], 3 * 4 * kBlockVoxels);  // L, hits, misses
+            const uint8_t hs = hidx[i] != kInvalid;
+            put(&hs, 1);
+            if (hs) put(&hist[uint64_t(hidx[i]) * kBlockVoxels * K], m->layer_bytes);
+        }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,225 @@
+"""Occupancy extension (include/svx.h "occupancy extension"):
+free-space carving, per-scan HIT/MISS dedup, log-odds, hit/miss counters, integer
+class histograms. The reference has none of this (SPEC.md:255 declines carving), so
+PARITY IS UNPINNED: the oracle (svxo_occ_*) restates the project's own contract and
+is checked here against hand-derived known answers and the contract's properties
+(order independence, hit dominance, clamping, range cut, capacity rejection); the
+GPU must reproduce the oracle's SOCC1 export byte for byte."""
+import numpy as np
+import pytest
+
+import paper_2412_00291_b200 as svx
+from oracle import bindings as ob
+
+needs_oracle = pytest.mark.skipif(not ob.oracle_available(), reason="oracle not built")
+
+
+def occ_cfg(**kw):
+    c = svx.OccupancyConfig(voxel_size=0.1, num_labels=4, max_blocks=1 << 12)
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+def voxel(parsed, v):
+    """(L, hits, misses, hist row | None) of voxel v from a parsed SOCC1."""
+    hdr, keys, L, hits, misses, hist = parsed
+    b = np.floor_divide(np.asarray(v), 8)
+    i = np.where(np.all(keys == b, axis=1))[0]
+    if not len(i):
+        return None
+    i = int(i[0])
+    lin = (v[0] & 7) + 8 * (v[1] & 7) + 64 * (v[2] & 7)
+    return float(L[i, lin]), int(hits[i, lin]), int(misses[i, lin]), (hist[i][lin] if i in hist else None)
+
+
+@needs_oracle
+def test_single_ray_known_answer():
+    o = ob.OracleOcc(occ_cfg())
+    r = o.integrate(np.array([[1.0, 0, 0]], np.float32), svx.pose_c())
+    assert (r.rays, r.hit_voxels, r.miss_voxels, r.new_blocks) == (1, 1, 10, 2)
+    p = ob.parse_socc1(o.save_bytes())
+    for x in range(10):  # world_to_voxel(1.0 / 0.1) = 10 is the hit voxel
+        assert voxel(p, (x, 0, 0))[:3] == (np.float32(-0.4), 0, 1)
+    assert voxel(p, (10, 0, 0))[:3] == (np.float32(0.85), 1, 0)
+    assert voxel(p, (11, 0, 0))[:3] == (0.0, 0, 0)
+
+
+@needs_oracle
+def test_hit_dominates_and_once_per_scan():
+    """Voxel 10 is hit by one ray and crossed by another: one HIT update; the
+    crossed voxels are updated once although two rays cross them."""
+    o = ob.OracleOcc(occ_cfg())
+    pts = np.array([[1.0, 0, 0], [2.0, 0, 0]], np.float32)
+    r = o.integrate(pts, svx.pose_c())
+    assert (r.hit_voxels, r.miss_voxels) == (2, 19)  # misses 0-9, 11-19
+    p = ob.parse_socc1(o.save_bytes())
+    assert voxel(p, (10, 0, 0))[:3] == (np.float32(0.85), 1, 0)
+    assert voxel(p, (5, 0, 0))[:3] == (np.float32(-0.4), 0, 1)
+
+
+@needs_oracle
+def test_clamping_and_counters_over_scans():
+    o = ob.OracleOcc(occ_cfg())
+    for _ in range(6):
+        o.integrate(np.array([[1.0, 0, 0]], np.float32), svx.pose_c())
+    p = ob.parse_socc1(o.save_bytes())
+    L, h, m, _ = voxel(p, (10, 0, 0))
+    assert (h, m) == (6, 0) and L == np.float32(3.5)      # 6 * 0.85 clamps at l_max
+    L, h, m, _ = voxel(p, (3, 0, 0))
+    assert (h, m) == (0, 6) and L == np.float32(-2.0)     # clamps at l_min
+
+
+@needs_oracle
+def test_max_range_cut_and_min_range_drop():
+    o = ob.OracleOcc(occ_cfg(max_range=0.57))
+    r = o.integrate(np.array([[1.0, 0, 0], [0.1, 0, 0], [np.nan, 0, 0]], np.float32), svx.pose_c())
+    assert (r.points, r.rays, r.hit_voxels) == (3, 1, 0)  # 0.1 < min_range, NaN dropped
+    p = ob.parse_socc1(o.save_bytes())
+    assert voxel(p, (6, 0, 0))[:3] == (np.float32(-0.4), 0, 1)  # end cut at 0.57 -> voxel 6
+    assert voxel(p, (7, 0, 0))[:3] == (0.0, 0, 0)
+
+
+@needs_oracle
+def test_histogram_fixed_point_and_argmax():
+    o = ob.OracleOcc(occ_cfg(carve=False))
+    pts = np.array([[1.0, 0, 0]] * 4, np.float32)
+    o.integrate(pts, svx.pose_c(), labels=np.array([2, 1, 1, 9], np.uint16),
+                conf=np.array([0.9, 0.5, 0.3, 1.0], np.float32))
+    p = ob.parse_socc1(o.save_bytes())
+    L, h, m, hist = voxel(p, (10, 0, 0))
+    # q8 = (uint32)(c*255 + 0.5): 0.9 -> 230, 0.5 -> 128, 0.3 -> 77; label 9 >= K ignored
+    assert list(hist) == [0, 128 + 77, 230, 0]
+    assert (h, m) == (1, 0) and p[1].shape[0] == 1   # carve off: only the hit block
+
+
+@needs_oracle
+def test_order_independence():
+    wl = __import__("paper_2412_00291_b200.workload", fromlist=["make"]).make("tiny", 2)
+    cfg = occ_cfg(voxel_size=wl.voxel_size, num_labels=8, max_blocks=1 << 16, max_range=15.0)
+    rng = np.random.default_rng(0)
+    a, b = ob.OracleOcc(cfg), ob.OracleOcc(cfg)
+    for pts, i in wl.scans():
+        pts = pts.numpy()
+        lab = rng.integers(0, 10, len(pts)).astype(np.uint16)
+        conf = rng.uniform(0, 1, len(pts)).astype(np.float32)
+        perm = rng.permutation(len(pts))
+        a.integrate(pts, wl.pose(i), lab, conf)
+        b.integrate(pts[perm], wl.pose(i), lab[perm], conf[perm])
+    assert a.save_bytes() == b.save_bytes()
+
+
+@needs_oracle
+def test_capacity_rejects_scan_unchanged():
+    o = ob.OracleOcc(occ_cfg(max_blocks=2))
+    o.integrate(np.array([[0.5, 0, 0]], np.float32), svx.pose_c())
+    before = o.save_bytes()
+    with pytest.raises(ob.CheckerError) as e:
+        o.integrate(np.array([[3.0, 0, 0]], np.float32), svx.pose_c())
+    assert e.value.code == 2
+    assert o.save_bytes() == before
+
+
+# ------------------------------------------------------------------------ GPU
+
+def _run_both(wl, cfg, n_frames=None, labels=True, seed=0, shard=None):
+    rng = np.random.default_rng(seed)
+    gpu = svx.OccupancyMap(cfg)
+    if shard:
+        gpu.set_shard(*shard)
+    o = ob.OracleOcc(cfg)
+    for pts, i in wl.scans():
+        pts = pts.numpy()
+        lab = rng.integers(0, cfg.num_labels + 2, len(pts)).astype(np.uint16) if labels else None
+        conf = rng.uniform(-0.1, 1.1, len(pts)).astype(np.float32) if labels else None
+        rg = gpu.integrate(pts, wl.pose(i), lab, conf)
+        ro = o.integrate(pts, wl.pose(i), lab, conf)
+        if not shard:
+            assert (rg.rays, rg.hit_voxels, rg.miss_voxels, rg.new_blocks) == \
+                (ro.rays, ro.hit_voxels, ro.miss_voxels, ro.new_blocks)
+    return gpu, o
+
+
+@pytest.mark.gpu
+@needs_oracle
+@pytest.mark.parametrize("variant", ["carve", "endpoints", "range_cut", "unlabelled"])
+def test_gpu_occupancy_equals_oracle(variant):
+    from paper_2412_00291_b200 import workload as W
+    wl = W.make("tiny", 3)
+    cfg = occ_cfg(voxel_size=wl.voxel_size, num_labels=20, max_blocks=1 << 17)
+    if variant == "endpoints":
+        cfg.carve = False
+    if variant == "range_cut":
+        cfg.max_range = 9.0
+    gpu, o = _run_both(wl, cfg, labels=variant != "unlabelled")
+    assert gpu.save_bytes() == o.save_bytes()
+    # point queries agree with the export
+    p = ob.parse_socc1(o.save_bytes())
+    keys = p[1]
+    vs = np.concatenate([keys[:50] * 8 + np.array([[1, 2, 3]]), [[10 ** 6, 0, 0]]]).astype(np.int32)
+    q = gpu.lookup(vs)
+    assert not q["found"][-1] and q["label"][-1] == -1
+    for j in range(50):
+        L, h, m, hist = voxel(p, tuple(vs[j]))
+        assert q["found"][j] and q["log_odds"][j] == L and q["hits"][j] == h and q["misses"][j] == m
+        if hist is not None:
+            assert np.array_equal(q["hist"][j], hist)
+            assert q["label"][j] == (int(np.argmax(hist)) if hist.max() > 0 else -1)
+    gpu.close()
+
+
+@pytest.mark.gpu
+@needs_oracle
+def test_gpu_occupancy_cfg2_scans_equal_oracle():
+    from paper_2412_00291_b200 import workload as W
+    wl = W.make("cfg2", 3)
+    cfg = occ_cfg(voxel_size=wl.voxel_size, num_labels=20, max_blocks=1 << 20)
+    gpu, o = _run_both(wl, cfg)
+    assert gpu.save_bytes() == o.save_bytes()
+    gpu.close()
+
+
+def _merge_socc1(parts):
+    """k-way merge of per-shard SOCC1 exports into one (sorted keys)."""
+    import struct
+    hdr = parts[0][:37]
+    blocks = []
+    for buf in parts:
+        K = struct.unpack_from("<I", buf, 9)[0]
+        (nb,) = struct.unpack_from("<Q", buf, 29)
+        off = 37
+        for _ in range(nb):
+            key = tuple(np.frombuffer(buf, np.int32, 3, off))
+            ln = 12 + 6144 + 1 + (2048 * K if buf[off + 12 + 6144] else 0)
+            blocks.append((key, buf[off:off + ln]))
+            off += ln
+    blocks.sort(key=lambda kb: kb[0])
+    return hdr[:29] + struct.pack("<Q", len(blocks)) + b"".join(b for _, b in blocks)
+
+
+@pytest.mark.gpu
+@needs_oracle
+def test_gpu_occupancy_key_sharded_union_equals_unsharded():
+    """two key shards (world 2) hold disjoint blocks whose union is the
+    unsharded map, byte for byte."""
+    from paper_2412_00291_b200 import workload as W
+    wl = W.make("tiny", 2)
+    cfg = occ_cfg(voxel_size=wl.voxel_size, num_labels=20, max_blocks=1 << 17)
+    g0, o = _run_both(wl, cfg, shard=(0, 2))
+    g1, _ = _run_both(wl, cfg, shard=(1, 2))
+    assert g0.block_count() > 0 and g1.block_count() > 0
+    assert _merge_socc1([g0.save_bytes(), g1.save_bytes()]) == o.save_bytes()
+    g0.close()
+    g1.close()
+
+
+@pytest.mark.gpu
+def test_gpu_occupancy_capacity_rejects_scan():
+    gpu = svx.OccupancyMap(occ_cfg(max_blocks=2))
+    gpu.integrate(np.array([[0.5, 0, 0]], np.float32), svx.pose_c())
+    before = gpu.save_bytes()
+    with pytest.raises(svx.CapacityError):
+        gpu.integrate(np.array([[3.0, 0, 0]], np.float32), svx.pose_c())
+    assert gpu.save_bytes() == before
+    gpu.integrate(np.array([[0.5, 0, 0]], np.float32), svx.pose_c())  # still usable
+    gpu.close()
