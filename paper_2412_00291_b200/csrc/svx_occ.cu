@@ -3,29 +3,32 @@
 // tsdf_integrator.hpp:93-135), per-scan HIT/MISS deduplication, f32 log-odds with
 // clamping, hit/miss counters and u32 class histograms for per-point labels.
 //
-// Map: its own open-addressing block hash (the TSDF map's HashView code) and a CUDA
+// Map: its own open-addressing block hash (16-byte slots: key + pool index) and a CUDA
 // VMM pool of 8 KB occupancy blocks, SoA inside a block so the fold is coalesced:
 //     u32 tag[512] | f32 log_odds[512] | u32 hits[512] | u32 misses[512]
 // plus lazily allocated histogram layers [512][K] u32 for blocks that received a
 // labelled hit.
 //
-// Per scan (one host synchronisation, to map pool memory for the scan's new blocks):
-//   k_occ_alloc  thread per point: the ray's DDA at voxel resolution, touching each
-//                block once per run of voxels (hash find-or-insert, pool index from a
-//                counter, first touch this scan -> touched-block list); histogram
-//                layer claimed for the hit block of a labelled point.
-//   k_occ_visit  thread per point: the same DDA; per voxel tag = max(tag, 4*S + kind)
-//                with kind HIT = 3 > MISS = 1, so HIT wins and the result does not
-//                depend on ray order (a plain load skips the atomic once the tag
-//                already holds this scan's value - the voxels near the sensor are
-//                crossed by every ray); labelled hits add q8(conf) to the histogram.
-//   k_occ_fold   CTA per touched block, thread per voxel: voxels whose tag carries
-//                this scan's serial S get their one log-odds / counter update.
+// Per scan (one host synchronisation, which sizes the fold grid):
+//   k_occ_visit  thread per point, the ray's DDA at voxel resolution: on each change
+//                of block a hash find-or-insert (pool index from a counter, first
+//                touch this scan marks the block); per voxel a RED.MAX (after a load
+//                that skips it when the tag already holds this scan's value: every ray
+//                crosses the voxels near the sensor) of tag = 4*S + kind with
+//                HIT = 3 > MISS = 1, so HIT wins and the result does not depend on ray
+//                order; labelled hits claim the block's histogram layer. Pool blocks
+//                are mapped and zeroed ahead of need; a scan that outruns the mapping
+//                is completed by a second launch for the blocks the first one skipped.
+//   k_occ_touched  compacts the marked blocks into the scan's touched list.
+//   k_occ_hist   labelled hits add to the class histograms (after the capacity check).
+//   k_occ_fold   persistent CTAs over the touched list, thread per voxel: voxels whose
+//                tag carries this scan's serial S get their one log-odds / counter update.
 // Deduplication is per-voxel tag based (no sort): tags carry the scan serial, so no
 // clearing pass is needed between scans.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -41,8 +44,7 @@ constexpr uint32_t kOverflow = 0xFFFFFFFDu;  // block beyond max_blocks
 constexpr int kHit = 3, kMiss = 1;
 
 enum OccCounter : int {
-    O_BLOCKS = 0, O_LAYERS, O_TOUCHED, O_ERR_CAP, O_ERR_KEY, O_ERR_HASH, O_HITV, O_MISSV,
-    O_RAYS, O_COUNT
+    O_BLOCKS = 0, O_LAYERS, O_TOUCHED, O_ERR_CAP, O_ERR_KEY, O_ERR_HASH, O_ERR_MAP, O_RAYS, O_COUNT
 };
 
 struct OccParams {
@@ -55,10 +57,22 @@ struct OccParams {
     int stride, carve, K;
     uint32_t serial, max_blocks;
     int32_t shard_rank, shard_world;
+    uint32_t mapped_blocks;  // pool blocks mapped and zeroed
+    uint32_t prev_blocks;    // redo launch: blocks the first launch already tagged
+    int redo;
+};
+
+// Hash slot: key and pool index side by side, so one 16-byte load resolves a probe.
+struct __align__(16) OccSlot {
+    unsigned long long key;  // kEmptyKey = free
+    uint32_t idx;            // kInvalid until the inserting thread publishes it
+    uint32_t pad;
 };
 
 struct OccDev {
-    HashView h;
+    OccSlot* slots;
+    int log2cap;
+    uint32_t mask;
     uint32_t* pool;       // [blocks][kOccWords]
     uint32_t* hist;       // [layers][512][K]
     uint64_t* block_keys;
@@ -66,6 +80,7 @@ struct OccDev {
     uint32_t* block_tag;
     uint32_t* touched;
     uint32_t* ctr;
+    uint32_t* rep;  // per scan of the batch: HIT voxels, MISS voxels
 };
 
 // The ray of point i (svx.h contract): false when the point is dropped.
@@ -83,38 +98,66 @@ __device__ inline bool point_ray(const OccParams& p, uint64_t i, d3& o, d3& end,
     return true;
 }
 
+__device__ inline uint32_t slot_idx(const OccSlot* sl) {
+    volatile const uint32_t* v = &sl->idx;
+    uint32_t idx;
+    while ((idx = *v) == kInvalid) {  // inserted, index not yet published
+    }
+    return idx;
+}
+
+// Find-or-insert of a block; marks it touched by this scan (plain store: the
+// touched list is compacted from the marks after the visit pass).
 __device__ inline uint32_t claim_block(const OccParams& p, const OccDev& d, uint64_t key) {
-    int ins = 0;
-    const uint32_t s = hash_insert(d.h, key, &ins);
-    if (s == kInvalid) {
+    uint32_t s = hash_slot(key, d.log2cap);
+    uint32_t idx = kInvalid;
+    for (uint32_t probe = 0; probe <= d.mask; ++probe) {
+        const uint4 v = __ldcg(reinterpret_cast<const uint4*>(&d.slots[s]));
+        const uint64_t k = uint64_t(v.x) | (uint64_t(v.y) << 32);
+        if (k == key) {
+            idx = v.z != kInvalid ? v.z : slot_idx(&d.slots[s]);
+            break;
+        }
+        if (k == kEmptyKey) {
+            const unsigned long long old = atomicCAS(&d.slots[s].key, kEmptyKey, key);
+            if (old == kEmptyKey) {
+                idx = atomicAdd(&d.ctr[O_BLOCKS], 1u);
+                if (idx >= p.max_blocks) {
+                    atomicAdd(&d.ctr[O_ERR_CAP], 1u);
+                    idx = kOverflow;
+                } else {
+                    d.block_keys[idx] = key;
+                }
+                __threadfence();
+                atomicExch(&d.slots[s].idx, idx);
+                break;
+            }
+            if (old == key) {
+                idx = slot_idx(&d.slots[s]);
+                break;
+            }
+        }
+        s = (s + 1) & d.mask;
+    }
+    if (idx == kInvalid) {
         atomicAdd(&d.ctr[O_ERR_HASH], 1u);
         return kInvalid;
     }
-    uint32_t idx;
-    if (ins) {
-        idx = atomicAdd(&d.ctr[O_BLOCKS], 1u);
-        if (idx >= p.max_blocks) {
-            atomicAdd(&d.ctr[O_ERR_CAP], 1u);
-            idx = kOverflow;
-        } else {
-            d.block_keys[idx] = key;
-        }
-        __threadfence();
-        atomicExch(&d.h.vals[s], idx);
-    } else {
-        volatile uint32_t* v = d.h.vals + s;
-        while ((idx = *v) == kInvalid) {
-        }
-    }
     if (idx == kOverflow) return kInvalid;
-    if (__ldcg(&d.block_tag[idx]) != p.serial && atomicExch(&d.block_tag[idx], p.serial) != p.serial)
-        d.touched[atomicAdd(&d.ctr[O_TOUCHED], 1u)] = idx;
+    if (__ldcg(&d.block_tag[idx]) != p.serial) d.block_tag[idx] = p.serial;  // hot blocks: read, not write
     return idx;
 }
 
 __device__ inline uint32_t find_block(const OccDev& d, uint64_t key) {
-    const uint32_t s = hash_find(d.h, key);
-    return s == kInvalid ? kInvalid : __ldcg(&d.h.vals[s]);
+    uint32_t s = hash_slot(key, d.log2cap);
+    for (uint32_t probe = 0; probe <= d.mask; ++probe) {
+        const uint4 v = __ldcg(reinterpret_cast<const uint4*>(&d.slots[s]));
+        const uint64_t k = uint64_t(v.x) | (uint64_t(v.y) << 32);
+        if (k == key) return v.z;
+        if (k == kEmptyKey) return kInvalid;
+        s = (s + 1) & d.mask;
+    }
+    return kInvalid;
 }
 
 __device__ inline bool owned(const OccParams& p, uint64_t key) {
@@ -146,16 +189,19 @@ __device__ inline void for_each_ray_voxel(const OccParams& p, d3 o, d3 end, bool
     if (hit) fn(ev[0], ev[1], ev[2], kHit);
 }
 
-__global__ void __launch_bounds__(256) k_occ_alloc(OccParams p, OccDev d) {
+__global__ void __launch_bounds__(256) k_occ_visit(OccParams p, OccDev d) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= p.n) return;
     d3 o, end;
     bool hit;
     if (!point_ray(p, i, o, end, hit)) return;
-    atomicAdd(&d.ctr[O_RAYS], 1u);
+    if (!p.redo) atomicAdd(&d.ctr[O_RAYS], 1u);
     uint64_t last = kEmptyKey;
-    uint32_t last_idx = kInvalid;
+    uint32_t* base = nullptr;
+    uint32_t idx = kInvalid;
+    bool done_before = false;  // redo: this block's updates were applied by the first launch
     const uint32_t lab = label_of(p, i);
+    const uint32_t tag_base = p.serial * 4u;
     for_each_ray_voxel(p, o, end, hit, [&](int32_t x, int32_t y, int32_t z, int kind) {
         const int32_t bx = block_coord(x), by = block_coord(y), bz = block_coord(z);
         if (!(key_in_range(bx) && key_in_range(by) && key_in_range(bz))) {
@@ -165,44 +211,45 @@ __global__ void __launch_bounds__(256) k_occ_alloc(OccParams p, OccDev d) {
         const uint64_t key = pack_key(bx, by, bz);
         if (key != last) {
             last = key;
-            last_idx = owned(p, key) ? claim_block(p, d, key) : kInvalid;
-        }
-        if (kind == kHit && last_idx != kInvalid && lab < uint32_t(p.K) &&
-            __ldcg(&d.hist_idx[last_idx]) == kInvalid &&
-            atomicCAS(&d.hist_idx[last_idx], kInvalid, kClaim) == kInvalid)
-            atomicExch(&d.hist_idx[last_idx], atomicAdd(&d.ctr[O_LAYERS], 1u));
-    });
-}
-
-__global__ void __launch_bounds__(256) k_occ_visit(OccParams p, OccDev d) {
-    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= p.n) return;
-    d3 o, end;
-    bool hit;
-    if (!point_ray(p, i, o, end, hit)) return;
-    uint64_t last = kEmptyKey;
-    uint32_t* base = nullptr;
-    uint32_t idx = kInvalid;
-    const uint32_t lab = label_of(p, i);
-    const uint32_t tag_base = p.serial * 4u;
-    for_each_ray_voxel(p, o, end, hit, [&](int32_t x, int32_t y, int32_t z, int kind) {
-        const int32_t bx = block_coord(x), by = block_coord(y), bz = block_coord(z);
-        if (!(key_in_range(bx) && key_in_range(by) && key_in_range(bz))) return;
-        const uint64_t key = pack_key(bx, by, bz);
-        if (key != last) {
-            last = key;
-            idx = owned(p, key) ? find_block(d, key) : kInvalid;
-            base = idx < p.max_blocks ? d.pool + uint64_t(idx) * kOccWords : nullptr;
+            idx = owned(p, key) ? claim_block(p, d, key) : kInvalid;
+            base = nullptr;
+            if (idx != kInvalid) {
+                if (idx < p.mapped_blocks) base = d.pool + uint64_t(idx) * kOccWords;
+                else atomicOr(&d.ctr[O_ERR_MAP], 1u);
+            }
+            done_before = p.redo && idx < p.prev_blocks;
         }
         if (!base) return;
         const int lin = local_linear(x, y, z);
+        // hot voxels (near the sensor every ray crosses them) are read, not written:
+        // same-address writes serialise in L2
         const uint32_t want = tag_base + uint32_t(kind);
-        if (__ldcg(&base[lin]) < want) atomicMax(&base[lin], want);
-        if (kind == kHit && lab < uint32_t(p.K)) {
-            const uint32_t layer = __ldcg(&d.hist_idx[idx]);
-            atomicAdd(&d.hist[(uint64_t(layer) * kBlockVoxels + lin) * p.K + lab], q8(p, i));
-        }
+        if (!done_before && __ldcg(&base[lin]) < want) atomicMax(&base[lin], want);  // RED
+        if (kind == kHit && lab < uint32_t(p.K) && __ldcg(&d.hist_idx[idx]) == kInvalid &&
+            atomicCAS(&d.hist_idx[idx], kInvalid, kClaim) == kInvalid)  // histogram layer
+            atomicExch(&d.hist_idx[idx], atomicAdd(&d.ctr[O_LAYERS], 1u));
     });
+}
+
+// Labelled hits -> class histograms, once the scan is accepted (the adds cannot be
+// undone, so they wait for the capacity check) and every claimed layer is mapped.
+__global__ void __launch_bounds__(256) k_occ_hist(OccParams p, OccDev d) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= p.n) return;
+    const uint32_t lab = label_of(p, i);
+    if (lab >= uint32_t(p.K)) return;
+    d3 o, end;
+    bool hit;
+    if (!point_ray(p, i, o, end, hit) || !hit) return;
+    int32_t ev[3];
+    world_to_voxel(end, p.inv_nu, ev);
+    const int32_t bx = block_coord(ev[0]), by = block_coord(ev[1]), bz = block_coord(ev[2]);
+    const uint64_t key = pack_key(bx, by, bz);
+    if (!owned(p, key)) return;
+    const uint32_t idx = find_block(d, key);
+    const uint32_t layer = d.hist_idx[idx];
+    atomicAdd(&d.hist[(uint64_t(layer) * kBlockVoxels + local_linear(ev[0], ev[1], ev[2])) * p.K + lab],
+              q8(p, i));
 }
 
 struct FoldParams {
@@ -210,33 +257,50 @@ struct FoldParams {
     float l_hit, l_miss, l_min, l_max;
 };
 
+// Touched-block list of the scan: the blocks whose mark carries its serial.
+__global__ void k_occ_touched(OccDev d, uint32_t n_blocks, uint32_t serial) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool t = i < n_blocks && d.block_tag[i] == serial;
+    const uint32_t ballot = __ballot_sync(0xFFFFFFFFu, t);
+    if (!ballot) return;
+    const int lane = threadIdx.x & 31;
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(&d.ctr[O_TOUCHED], uint32_t(__popc(ballot)));
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    if (t) d.touched[base + __popc(ballot & ((1u << lane) - 1))] = i;
+}
+
+// Persistent CTAs over the touched list, thread per voxel. The tag, log-odds and
+// both counters are loaded together (coalesced, no dependent round trip).
 __global__ void __launch_bounds__(kBlockVoxels) k_occ_fold(FoldParams fp, OccDev d) {
-    const uint32_t idx = d.touched[blockIdx.x];
-    uint32_t* base = d.pool + uint64_t(idx) * kOccWords;
+    const uint32_t n = __ldcg(&d.ctr[O_TOUCHED]);
     const int v = threadIdx.x;
-    const uint32_t tag = base[v];
     uint32_t nh = 0, nm = 0;
-    if ((tag >> 2) == fp.serial) {
-        float* L = reinterpret_cast<float*>(base + kBlockVoxels);
-        float l = L[v];
+    for (uint32_t j = blockIdx.x; j < n; j += gridDim.x) {
+        uint32_t* base = d.pool + uint64_t(d.touched[j]) * kOccWords;
+        const uint32_t tag = __ldcg(&base[v]);
+        float l = __uint_as_float(__ldcg(&base[kBlockVoxels + v]));
+        const uint32_t h = __ldcg(&base[2 * kBlockVoxels + v]);
+        const uint32_t ms = __ldcg(&base[3 * kBlockVoxels + v]);
+        if ((tag >> 2) != fp.serial) continue;
         if ((tag & 3u) == uint32_t(kHit)) {
             const float t = l + fp.l_hit;
             l = t > fp.l_max ? fp.l_max : t;
-            base[2 * kBlockVoxels + v] += 1u;
-            nh = 1;
+            base[2 * kBlockVoxels + v] = h + 1u;
+            ++nh;
         } else {
             const float t = l + fp.l_miss;
             l = t < fp.l_min ? fp.l_min : t;
-            base[3 * kBlockVoxels + v] += 1u;
-            nm = 1;
+            base[3 * kBlockVoxels + v] = ms + 1u;
+            ++nm;
         }
-        L[v] = l;
+        base[kBlockVoxels + v] = __float_as_uint(l);
     }
     nh = __reduce_add_sync(0xFFFFFFFFu, nh);
     nm = __reduce_add_sync(0xFFFFFFFFu, nm);
     if ((threadIdx.x & 31) == 0) {
-        if (nh) atomicAdd(&d.ctr[O_HITV], nh);
-        if (nm) atomicAdd(&d.ctr[O_MISSV], nm);
+        if (nh) atomicAdd(&d.rep[0], nh);
+        if (nm) atomicAdd(&d.rep[1], nm);
     }
 }
 
@@ -246,12 +310,21 @@ __global__ void k_occ_unclaim(uint32_t* __restrict__ hist_idx, uint32_t n_blocks
     if (i < n_blocks && hist_idx[i] != kInvalid && hist_idx[i] >= keep) hist_idx[i] = kInvalid;
 }
 
-__global__ void k_occ_rebuild(HashView h, const uint64_t* __restrict__ keys, uint32_t n) {
+__global__ void k_occ_rebuild(OccDev d, uint32_t n) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    int ins = 0;
-    const uint32_t s = hash_insert(h, keys[i], &ins);
-    if (s != kInvalid) h.vals[s] = i;
+    const uint64_t key = d.block_keys[i];
+    uint32_t s = hash_slot(key, d.log2cap);
+    while (atomicCAS(&d.slots[s].key, kEmptyKey, key) != kEmptyKey) s = (s + 1) & d.mask;
+    d.slots[s].idx = i;
+}
+
+__global__ void k_occ_clear_slots(OccSlot* __restrict__ slots, uint32_t cap) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < cap) {
+        slots[i].key = kEmptyKey;
+        slots[i].idx = kInvalid;
+    }
 }
 
 __global__ void k_occ_lookup(OccDev d, int K, const int32_t* __restrict__ v, uint64_t n,
@@ -325,8 +398,7 @@ struct svx_occ {
     int32_t shard_rank = 0, shard_world = 1;
     int log2cap = 0;
     uint32_t cap = 0;
-    uint64_t* keys = nullptr;
-    uint32_t* vals = nullptr;
+    void* slots = nullptr;  // OccSlot[cap]
     svx::VmmArray pool;   // [blocks][4 x 512] u32
     svx::VmmArray hist;   // [layers][512][K] u32
     size_t layer_bytes = 0;
@@ -339,6 +411,10 @@ struct svx_occ {
     uint32_t serial = 0;
     int32_t frames = 0;
     uint64_t n_blocks = 0, n_layers = 0;
+    uint64_t mapped_blocks = 0, mapped_layers = 0;  // mapped and zeroed
+    uint64_t max_new_blocks = 0;                    // largest per-scan growth seen
+    uint64_t min_headroom = 65536;                  // blocks mapped ahead of a scan
+    svx::DevBuf<uint32_t> rep;                      // per scan of a batch: HIT, MISS voxels
     svx::DevBuf<float> pts;
     svx::DevBuf<uint16_t> lbl;
     svx::DevBuf<float> conf;
@@ -348,19 +424,20 @@ namespace svx {
 namespace {
 
 OccDev occ_dev(svx_occ* m) {
-    return OccDev{HashView{m->keys, m->vals, m->log2cap, m->cap - 1},
+    return OccDev{static_cast<OccSlot*>(m->slots), m->log2cap, m->cap - 1,
                   static_cast<uint32_t*>(m->pool.base()), static_cast<uint32_t*>(m->hist.base()),
-                  m->block_keys, m->hist_idx, m->block_tag, m->touched, m->d_ctr};
+                  m->block_keys, m->hist_idx, m->block_tag, m->touched, m->d_ctr, m->rep.p};
 }
 
 void free_occ(svx_occ* m) {
     if (!m) return;
     cudaSetDevice(m->device);
     if (m->stream) cudaStreamSynchronize(m->stream);
-    for (void* p : {(void*)m->keys, (void*)m->vals, (void*)m->block_keys, (void*)m->hist_idx,
+    for (void* p : {m->slots, (void*)m->block_keys, (void*)m->hist_idx,
                     (void*)m->block_tag, (void*)m->touched, (void*)m->d_ctr})
         if (p) cudaFree(p);
     if (m->h_ctr) cudaFreeHost(m->h_ctr);
+    m->rep.release();
     m->pts.release();
     m->lbl.release();
     m->conf.release();
@@ -379,9 +456,32 @@ void validate(const svx_occ_cfg& c) {
             "ranges: need 0 <= min_range < max_range");
 }
 
-// One scan; points / labels / conf already on the device.
+// Maps and zero-fills the pool so that `blocks` blocks are usable (new blocks must
+// read as zero: tags 0 < every serial), plus headroom mapped in the background.
+void map_blocks(svx_occ* m, uint64_t blocks) {
+    blocks = std::min<uint64_t>(blocks, m->cfg.max_blocks);
+    const uint64_t ready = std::min<uint64_t>(m->pool.mapped() / kOccBlockBytes, m->cfg.max_blocks);
+    const uint64_t target = std::max(blocks, ready);  // adopt a finished prefetch too
+    if (target <= m->mapped_blocks) return;
+    if (target * kOccBlockBytes > m->pool.mapped()) m->pool.ensure(target * kOccBlockBytes);
+    SVX_CUDA(cudaMemsetAsync(static_cast<uint8_t*>(m->pool.base()) + m->mapped_blocks * kOccBlockBytes, 0,
+                             (target - m->mapped_blocks) * kOccBlockBytes, m->stream));
+    m->mapped_blocks = target;
+}
+
+void map_layers(svx_occ* m, uint64_t layers) {
+    if (layers <= m->mapped_layers) return;
+    const uint64_t target = std::min<uint64_t>(m->cfg.max_blocks, std::max(layers, m->mapped_layers * 2));
+    m->hist.ensure(target * m->layer_bytes);
+    SVX_CUDA(cudaMemsetAsync(static_cast<uint8_t*>(m->hist.base()) + m->mapped_layers * m->layer_bytes, 0,
+                             (target - m->mapped_layers) * m->layer_bytes, m->stream));
+    m->mapped_layers = target;
+}
+
+// One scan; points / labels / conf already on the device. rep_slot: this scan's
+// HIT/MISS counters on the device (read at the end of the batch).
 void occ_scan(svx_occ* m, const float* d_pts, const uint16_t* d_lbl, const float* d_conf, uint64_t n,
-              int stride, const svx_pose& pose, svx_occ_report* rep) {
+              int stride, const svx_pose& pose, uint32_t* rep_slot, svx_occ_report* rep) {
     const auto t0 = std::chrono::steady_clock::now();
     cudaStream_t st = m->stream;
     require(m->serial + 1 < (1u << 30), SVX_INVALID_ARGUMENT, "too many scans for one occupancy map");
@@ -403,25 +503,30 @@ void occ_scan(svx_occ* m, const float* d_pts, const uint16_t* d_lbl, const float
     p.max_blocks = m->cfg.max_blocks;
     p.shard_rank = m->shard_rank;
     p.shard_world = m->shard_world;
-    // per-scan counters (blocks / layers persist)
+    // headroom for this scan's new blocks, mapped and zeroed ahead of the launch
+    map_blocks(m, m->n_blocks + std::max<uint64_t>(m->min_headroom, 2 * m->max_new_blocks));
+    m->pool.prefetch(std::min<uint64_t>(m->cfg.max_blocks, 2 * m->mapped_blocks) * kOccBlockBytes);
+    p.mapped_blocks = uint32_t(m->mapped_blocks);
     m->h_ctr[O_BLOCKS] = uint32_t(m->n_blocks);
     m->h_ctr[O_LAYERS] = uint32_t(m->n_layers);
     for (int c = O_TOUCHED; c < O_COUNT; ++c) m->h_ctr[c] = 0;
     SVX_CUDA(cudaMemcpyAsync(m->d_ctr, m->h_ctr, 4 * O_COUNT, cudaMemcpyHostToDevice, st));
     OccDev d = occ_dev(m);
+    d.rep = rep_slot;
     if (n) {
-        k_occ_alloc<<<grid256(n), 256, 0, st>>>(p, d);
+        k_occ_visit<<<grid256(n), 256, 0, st>>>(p, d);
         count_launch();
     }
     SVX_CUDA(cudaMemcpyAsync(m->h_ctr, m->d_ctr, 4 * O_COUNT, cudaMemcpyDeviceToHost, st));
     SVX_CUDA(cudaStreamSynchronize(st));
     const uint64_t old_blocks = m->n_blocks, old_layers = m->n_layers;
     if (m->h_ctr[O_ERR_KEY] || m->h_ctr[O_ERR_HASH] || m->h_ctr[O_ERR_CAP]) {
-        // reject the scan: drop its new blocks and histogram claims
-        SVX_CUDA(cudaMemsetAsync(m->keys, 0xFF, 8ull * m->cap, st));
-        SVX_CUDA(cudaMemsetAsync(m->vals, 0xFF, 4ull * m->cap, st));
+        // reject the scan: drop its new blocks and histogram claims. Its tags carry a
+        // serial no fold will look for; log-odds, counters and histograms are untouched.
+        k_occ_clear_slots<<<grid256(m->cap), 256, 0, st>>>(d.slots, m->cap);
+        count_launch();
         if (old_blocks) {
-            k_occ_rebuild<<<grid256(old_blocks), 256, 0, st>>>(d.h, m->block_keys, uint32_t(old_blocks));
+            k_occ_rebuild<<<grid256(old_blocks), 256, 0, st>>>(d, uint32_t(old_blocks));
             k_occ_unclaim<<<grid256(old_blocks), 256, 0, st>>>(m->hist_idx, uint32_t(old_blocks),
                                                                uint32_t(old_layers));
             count_launch(2);
@@ -437,38 +542,39 @@ void occ_scan(svx_occ* m, const float* d_pts, const uint16_t* d_lbl, const float
     }
     m->n_blocks = m->h_ctr[O_BLOCKS];
     m->n_layers = m->h_ctr[O_LAYERS];
-    const uint32_t touched = m->h_ctr[O_TOUCHED];
+    if (m->min_headroom >= 65536) m->max_new_blocks = std::max(m->max_new_blocks, m->n_blocks - old_blocks);
     const uint64_t rays = m->h_ctr[O_RAYS];
-    if (m->n_blocks > old_blocks) {  // map + zero the new blocks (tags 0 < any serial)
-        m->pool.ensure(m->n_blocks * kOccBlockBytes);
-        SVX_CUDA(cudaMemsetAsync(static_cast<uint8_t*>(m->pool.base()) + old_blocks * kOccBlockBytes, 0,
-                                 (m->n_blocks - old_blocks) * kOccBlockBytes, st));
-        m->pool.prefetch(std::min<uint64_t>(m->cfg.max_blocks, 2 * m->n_blocks + 65536) * kOccBlockBytes);
-    }
-    if (m->n_layers > old_layers) {
-        m->hist.ensure(m->n_layers * m->layer_bytes);
-        SVX_CUDA(cudaMemsetAsync(static_cast<uint8_t*>(m->hist.base()) + old_layers * m->layer_bytes, 0,
-                                 (m->n_layers - old_layers) * m->layer_bytes, st));
-    }
-    d = occ_dev(m);
-    if (n) {
+    if (m->h_ctr[O_ERR_MAP]) {  // the scan outran the mapped pool: finish the skipped blocks
+        map_blocks(m, m->n_blocks);
+        p.redo = 1;
+        p.prev_blocks = p.mapped_blocks;
+        p.mapped_blocks = uint32_t(m->mapped_blocks);
         k_occ_visit<<<grid256(n), 256, 0, st>>>(p, d);
         count_launch();
+        // it may claim histogram layers for the blocks it completes
+        SVX_CUDA(cudaMemcpyAsync(&m->h_ctr[O_LAYERS], &m->d_ctr[O_LAYERS], 4, cudaMemcpyDeviceToHost, st));
+        SVX_CUDA(cudaStreamSynchronize(st));
+        m->n_layers = m->h_ctr[O_LAYERS];
     }
-    if (touched) {
-        const FoldParams fp{m->serial, m->cfg.l_hit, m->cfg.l_miss, m->cfg.l_min, m->cfg.l_max};
-        k_occ_fold<<<touched, kBlockVoxels, 0, st>>>(fp, d);
+    map_layers(m, m->n_layers);
+    d = occ_dev(m);
+    d.rep = rep_slot;
+    if (n && p.lbl) {
+        k_occ_hist<<<grid256(n), 256, 0, st>>>(p, d);
         count_launch();
     }
+    if (m->n_blocks) {
+        k_occ_touched<<<grid256(m->n_blocks), 256, 0, st>>>(d, uint32_t(m->n_blocks), m->serial);
+        const FoldParams fp{m->serial, m->cfg.l_hit, m->cfg.l_miss, m->cfg.l_min, m->cfg.l_max};
+        const unsigned grid = unsigned(std::min<uint64_t>(m->n_blocks, 148ull * 4));
+        k_occ_fold<<<grid, kBlockVoxels, 0, st>>>(fp, d);
+        count_launch(2);
+    }
     SVX_CUDA(cudaGetLastError());
-    SVX_CUDA(cudaMemcpyAsync(m->h_ctr + O_HITV, m->d_ctr + O_HITV, 8, cudaMemcpyDeviceToHost, st));
-    SVX_CUDA(cudaStreamSynchronize(st));
     if (rep) {
         rep->frame = m->frames;
         rep->points = n;
         rep->rays = rays;
-        rep->hit_voxels = m->h_ctr[O_HITV];
-        rep->miss_voxels = m->h_ctr[O_MISSV];
         rep->new_blocks = m->n_blocks - old_blocks;
         rep->elapsed_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     }
@@ -519,8 +625,7 @@ svx_status svx_occ_create(const svx_occ_cfg* cfg, int device, svx_occ** out) {
             const uint64_t want = std::max<uint64_t>(2ull * cfg->max_blocks, 1024);
             while ((1ull << m->log2cap) < want) ++m->log2cap;
             m->cap = uint32_t(1u << m->log2cap);
-            m->keys = dmalloc<uint64_t>(m->cap);
-            m->vals = dmalloc<uint32_t>(m->cap);
+            m->slots = dmalloc<OccSlot>(m->cap);
             m->block_keys = dmalloc<uint64_t>(cfg->max_blocks);
             m->hist_idx = dmalloc<uint32_t>(cfg->max_blocks);
             m->block_tag = dmalloc<uint32_t>(cfg->max_blocks);
@@ -528,11 +633,16 @@ svx_status svx_occ_create(const svx_occ_cfg* cfg, int device, svx_occ** out) {
             m->d_ctr = dmalloc<uint32_t>(O_COUNT);
             SVX_CUDA(cudaMallocHost(&m->h_ctr, 4 * O_COUNT));
             std::memset(m->h_ctr, 0, 4 * O_COUNT);
-            SVX_CUDA(cudaMemsetAsync(m->keys, 0xFF, 8ull * m->cap, m->stream));
-            SVX_CUDA(cudaMemsetAsync(m->vals, 0xFF, 4ull * m->cap, m->stream));
+            k_occ_clear_slots<<<grid256(m->cap), 256, 0, m->stream>>>(static_cast<OccSlot*>(m->slots), m->cap);
+            count_launch();
             SVX_CUDA(cudaMemsetAsync(m->hist_idx, 0xFF, 4ull * cfg->max_blocks, m->stream));
             SVX_CUDA(cudaMemsetAsync(m->block_tag, 0, 4ull * cfg->max_blocks, m->stream));
             m->layer_bytes = 4ull * kBlockVoxels * uint64_t(cfg->num_labels);
+            // test hook: a tiny mapping headroom exercises the scan-completion launch
+            if (const char* e = std::getenv("SVX_TEST_OCC_HEADROOM")) {
+                m->min_headroom = uint64_t(std::max(0L, std::atol(e)));
+                m->max_new_blocks = 0;
+            }
             m->pool.reserve(device, size_t(cfg->max_blocks) * kOccBlockBytes);
             m->hist.reserve(device, size_t(cfg->max_blocks) * m->layer_bytes);
             SVX_CUDA(cudaStreamSynchronize(m->stream));
@@ -579,6 +689,8 @@ svx_status svx_occ_integrate_batch(svx_occ* m, const float* points, const uint16
         require(m && offs && poses && n_frames >= 0, SVX_INVALID_ARGUMENT, "null argument");
         require(stride >= 3, SVX_INVALID_ARGUMENT, "stride must be >= 3");
         DevGuard g(m->device);
+        m->rep.alloc(2ull * std::max(n_frames, 1));
+        SVX_CUDA(cudaMemsetAsync(m->rep.p, 0, 8ull * std::max(n_frames, 1), m->stream));
         for (int f = 0; f < n_frames; ++f) {
             require(offs[f + 1] >= offs[f], SVX_INVALID_ARGUMENT, "offsets must be non-decreasing");
             require(offs[f + 1] == offs[f] || points, SVX_INVALID_ARGUMENT, "null points");
@@ -592,7 +704,14 @@ svx_status svx_occ_integrate_batch(svx_occ* m, const float* points, const uint16
                 dl = stage(m, m->lbl, dl, n);
                 dc = stage(m, m->conf, dc, n);
             }
-            occ_scan(m, dp, dl, dc, n, stride, poses[f], reps ? reps + f : nullptr);
+            occ_scan(m, dp, dl, dc, n, stride, poses[f], m->rep.p + 2 * f, reps ? reps + f : nullptr);
+        }
+        std::vector<uint32_t> hm(2ull * std::max(n_frames, 1));
+        SVX_CUDA(cudaMemcpyAsync(hm.data(), m->rep.p, 4 * hm.size(), cudaMemcpyDeviceToHost, m->stream));
+        SVX_CUDA(cudaStreamSynchronize(m->stream));
+        for (int f = 0; reps && f < n_frames; ++f) {
+            reps[f].hit_voxels = hm[2 * f];
+            reps[f].miss_voxels = hm[2 * f + 1];
         }
     });
 }

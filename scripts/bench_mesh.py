@@ -80,7 +80,7 @@ ach = alg / (out["device_ms"] * 1e-3) / 1e9
 out["roofline"] = {"bound": "hbm", "alg_bytes": alg, "achieved": ach, "peak": peak, "unit": "GB/s",
                    "frac": ach / peak}
 
-if ob.ref_available():
+if ob.ref_available() and REF_REPS > 0:
     with tempfile.TemporaryDirectory() as d:
         path = os.path.join(d, "map.svox")
         st.save(path)

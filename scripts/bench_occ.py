@@ -112,7 +112,7 @@ line = {"metric": "points integrated/sec with free-space carving (occupancy exte
                 "api": "svx_occ_integrate_batch, points/labels/conf in pinned host memory"},
         "roofline": {"bound": "hbm", "alg_bytes_per_scan": alg / SCANS, "achieved": ach, "peak": peak,
                      "unit": "GB/s", "frac": ach / peak, "note": "whole pipeline (3 kernels + 1 sync per scan)"}}
-if ob.oracle_available():
+if ob.oracle_available() and CPU_SCANS > 0:
     o = ob.OracleOcc(cfg)
     pts_n = 0
     t0 = time.perf_counter()

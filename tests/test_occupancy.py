@@ -214,6 +214,20 @@ def test_gpu_occupancy_key_sharded_union_equals_unsharded():
 
 
 @pytest.mark.gpu
+@needs_oracle
+def test_gpu_occupancy_scan_completion_after_mapping(monkeypatch):
+    """A scan that outruns the mapped pool is finished by a second launch that applies
+    exactly the skipped updates (SVX_TEST_OCC_HEADROOM forces it on every scan)."""
+    from paper_2412_00291_b200 import workload as W
+    monkeypatch.setenv("SVX_TEST_OCC_HEADROOM", "3")
+    wl = W.make("tiny", 3)
+    cfg = occ_cfg(voxel_size=wl.voxel_size, num_labels=20, max_blocks=1 << 17)
+    gpu, o = _run_both(wl, cfg)
+    assert gpu.save_bytes() == o.save_bytes()
+    gpu.close()
+
+
+@pytest.mark.gpu
 def test_gpu_occupancy_capacity_rejects_scan():
     gpu = svx.OccupancyMap(occ_cfg(max_blocks=2))
     gpu.integrate(np.array([[0.5, 0, 0]], np.float32), svx.pose_c())
