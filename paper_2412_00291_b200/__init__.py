@@ -809,10 +809,10 @@ def _reserved_unlabeled(label_names) -> int:
 
 
 def _read_mesh(store: "VoxelStore", nv: int, nf: int, colors) -> LabeledMesh:
-    v = np.zeros((nv, 3), np.float32)
-    n = np.zeros((nv, 3), np.float32)
-    lab = np.zeros(nv, np.uint8)
-    f = np.zeros((nf, 3), np.uint32)
+    v = np.empty((nv, 3), np.float32)
+    n = np.empty((nv, 3), np.float32)
+    lab = np.empty(nv, np.uint8)
+    f = np.empty((nf, 3), np.uint32)
     _check(lib().svx_mesh_read(store.handle, _ptr(v), _ptr(n), _ptr(lab), _ptr(f)))
     col = None
     if colors is not None:  # LabelSet::color_of_label; gray (128) for unlabeled

@@ -11,6 +11,7 @@
 #include <fstream>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "svx_map.hpp"
@@ -117,6 +118,7 @@ void free_map(svx_map* m) {
     m->q_keys.release();
     m->q_idx.release();
     m->mesh.release();
+    if (m->mesh.host_stage) cudaFreeHost(m->mesh.host_stage);
     if (m->copy_stream) cudaStreamSynchronize(m->copy_stream);
     for (int i = 0; i < svx_map::kIngestSlots; ++i) {
         if (m->ingest_ready[i]) cudaEventDestroy(m->ingest_ready[i]);
@@ -535,17 +537,63 @@ svx_status svx_mesh_extract(svx_map* m, float min_weight, int32_t reserved, cons
     });
 }
 
+// Mesh read-back: one D2H of every requested array into a pinned staging buffer
+// (full copy-engine bandwidth), then a multi-threaded copy into the caller's
+// (typically pageable) buffers. A pageable cudaMemcpy runs at single-thread memcpy
+// speed and dominated the end-to-end extraction time.
 svx_status svx_mesh_read(svx_map* m, float* vertices, float* normals, uint8_t* labels,
                          uint32_t* faces) {
     return guarded([&] {
         require(m != nullptr, SVX_INVALID_ARGUMENT, "null map");
         DeviceGuard g(m->device);
-        const MeshState& ms = m->mesh;
+        MeshState& ms = m->mesh;
         const uint64_t V = ms.n_vertices, F = ms.n_faces;
-        if (vertices && V) SVX_CUDA(cudaMemcpy(vertices, ms.verts.p, 12 * V, cudaMemcpyDeviceToHost));
-        if (normals && V) SVX_CUDA(cudaMemcpy(normals, ms.normals.p, 12 * V, cudaMemcpyDeviceToHost));
-        if (labels && V) SVX_CUDA(cudaMemcpy(labels, ms.labels.p, V, cudaMemcpyDeviceToHost));
-        if (faces && F) SVX_CUDA(cudaMemcpy(faces, ms.faces.p, 12 * F, cudaMemcpyDeviceToHost));
+        struct Part {
+            void* dst;
+            const void* src;
+            uint64_t bytes;
+        };
+        std::vector<Part> parts;
+        if (vertices && V) parts.push_back({vertices, ms.verts.p, 12 * V});
+        if (normals && V) parts.push_back({normals, ms.normals.p, 12 * V});
+        if (labels && V) parts.push_back({labels, ms.labels.p, V});
+        if (faces && F) parts.push_back({faces, ms.faces.p, 12 * F});
+        uint64_t total = 0;
+        for (const Part& q : parts) total += (q.bytes + 255) & ~uint64_t(255);
+        if (!total) return;
+        if (ms.host_stage_bytes < total) {
+            if (ms.host_stage) cudaFreeHost(ms.host_stage);
+            ms.host_stage = nullptr;
+            ms.host_stage_bytes = 0;
+            SVX_CUDA(cudaMallocHost(&ms.host_stage, total + total / 4));
+            ms.host_stage_bytes = total + total / 4;
+        }
+        uint8_t* stage = static_cast<uint8_t*>(ms.host_stage);
+        std::vector<uint8_t*> at;
+        uint64_t off = 0;
+        for (const Part& q : parts) {
+            at.push_back(stage + off);
+            SVX_CUDA(cudaMemcpyAsync(stage + off, q.src, q.bytes, cudaMemcpyDeviceToHost, m->stream));
+            off += (q.bytes + 255) & ~uint64_t(255);
+        }
+        SVX_CUDA(cudaStreamSynchronize(m->stream));
+        const unsigned nt = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+        const uint64_t chunk = 1ull << 20;
+        std::atomic<uint64_t> next{0};
+        std::vector<std::pair<size_t, uint64_t>> work;  // (part, offset)
+        for (size_t k = 0; k < parts.size(); ++k)
+            for (uint64_t o = 0; o < parts[k].bytes; o += chunk) work.push_back({k, o});
+        auto worker = [&] {
+            for (uint64_t w; (w = next.fetch_add(1)) < work.size();) {
+                const auto [k, o] = work[w];
+                std::memcpy(static_cast<uint8_t*>(parts[k].dst) + o, at[k] + o,
+                            std::min(chunk, parts[k].bytes - o));
+            }
+        };
+        std::vector<std::thread> pool;
+        for (unsigned i = 1; i < nt && i < work.size(); ++i) pool.emplace_back(worker);
+        worker();
+        for (std::thread& th : pool) th.join();
     });
 }
 

@@ -123,15 +123,19 @@ struct MeshState {
     DevBuf<uint32_t> rank_of_pool;    // [max_blocks] pool index -> mesh rank, kInvalid outside
     DevBuf<uint32_t> nb_pool, nb_rank;  // [R][27] neighbour blocks
     DevBuf<uint8_t> cases;            // [R][512] cell case bytes
+    DevBuf<uint8_t> block_active;     // [R] block has a cell with geometry
     DevBuf<uint32_t> cellinfo;        // [R][512] local vertex offset | owned-edge mask << 12
+    DevBuf<uint4> active;             // cells with geometry: rank, lin | case << 9, cellinfo, face offset
     DevBuf<unsigned long long> counts;  // per-block vertex/face counts and their scans
     DevBuf<float> verts, normals;     // 3V
     DevBuf<uint8_t> labels;           // V
     DevBuf<uint32_t> faces;           // 3F
     uint64_t n_vertices = 0, n_faces = 0;
+    void* host_stage = nullptr;       // pinned read-back staging (svx_mesh_read)
+    uint64_t host_stage_bytes = 0;
     void release() {
         keys.release(); pidx.release(); rank_of_pool.release(); nb_pool.release();
-        nb_rank.release(); cases.release(); cellinfo.release(); counts.release();
+        nb_rank.release(); cases.release(); block_active.release(); cellinfo.release(); active.release(); counts.release();
         verts.release(); normals.release(); labels.release(); faces.release();
     }
 };

@@ -146,26 +146,36 @@ __global__ void k_mesh_nbr(HashView h, const uint64_t* __restrict__ keys, uint32
     nb_rank[i] = p == kInvalid ? kInvalid : rank_of_pool[p];
 }
 
-// Case byte of every cell of mesh block blockIdx.x (mesh.cpp:143-160): a cell is
-// usable when all 8 corners exist with !(weight < min_weight); bit c set when
-// corner c has distance < 0. 0 = no geometry (unusable, or edge mask empty).
-__global__ void __launch_bounds__(kCells) k_mesh_case(MeshParams mp, const uint32_t* __restrict__ nb_pool,
-                                                     const svx_tsdf_voxel* __restrict__ pool,
-                                                     uint8_t* __restrict__ cases) {
-    __shared__ float sd[9 * 9 * 9];
-    __shared__ uint8_t sok[9 * 9 * 9];
-    __shared__ uint32_t snb[8];
-    const uint32_t r = blockIdx.x;
-    const int t = threadIdx.x;
-    if (t < 8) snb[t] = nb_pool[uint64_t(r) * 27 + nb27(t & 1, (t >> 1) & 1, t >> 2)];
-    __syncthreads();
-    if (snb[0] == kInvalid) {  // block absent from the map: no cells
-        cases[uint64_t(r) * kCells + t] = 0;
+constexpr int kWarpsPerCta = 8;  // mesh blocks per CTA in the warp-per-block kernels
+
+// Case byte of every cell (mesh.cpp:143-160), one WARP per mesh block: the warp
+// stages the block's 9x9x9 corner lattice (D and the weight test; the block and its
+// 7 upper neighbours) in shared memory, then each lane classifies 16 cells. A cell is
+// usable when all 8 corners exist with !(weight < min_weight); bit c set when corner
+// c has distance < 0; 0 = no geometry (unusable, or edge mask empty). No CTA-wide
+// barrier: blocks are independent, and at ~50k blocks per map the per-CTA cost of a
+// 512-thread block-per-CTA layout dominated.
+__global__ void __launch_bounds__(32 * kWarpsPerCta) k_mesh_case(MeshParams mp, const uint32_t* __restrict__ nb_pool,
+                                                                  const svx_tsdf_voxel* __restrict__ pool,
+                                                                  uint8_t* __restrict__ cases,
+                                                                  uint8_t* __restrict__ block_active) {
+    __shared__ float sd[kWarpsPerCta][9 * 9 * 9];
+    __shared__ uint8_t sok[kWarpsPerCta][9 * 9 * 9 + 7];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t r = blockIdx.x * kWarpsPerCta + w;
+    if (r >= mp.R) return;
+    uint32_t nbp = kInvalid;  // lane c < 8: pool index of upper neighbour c
+    if (lane < 8) nbp = nb_pool[uint64_t(r) * 27 + nb27(lane & 1, (lane >> 1) & 1, lane >> 2)];
+    const uint32_t own = __shfl_sync(0xFFFFFFFFu, nbp, 0);
+    uint8_t* out = cases + uint64_t(r) * kCells;
+    if (own == kInvalid) {  // block absent from the map: no cells
+        reinterpret_cast<uint4*>(out)[lane] = make_uint4(0, 0, 0, 0);
+        if (lane == 0) block_active[r] = 0;
         return;
     }
-    for (int q = t; q < 729; q += kCells) {
+    for (int q = lane; q < 729; q += 32) {
         const int x = q % 9, y = (q / 9) % 9, z = q / 81;
-        const uint32_t p = snb[(x >> 3) | ((y >> 3) << 1) | ((z >> 3) << 2)];
+        const uint32_t p = __shfl_sync(__activemask(), nbp, (x >> 3) | ((y >> 3) << 1) | ((z >> 3) << 2));
         float d = 0.f;
         uint8_t ok = 0;
         if (p != kInvalid) {
@@ -173,20 +183,31 @@ __global__ void __launch_bounds__(kCells) k_mesh_case(MeshParams mp, const uint3
             d = __ldg(&v->distance);  // 20-byte voxels: 4-byte aligned only
             ok = !(__ldg(&v->weight) < mp.min_weight);
         }
-        sd[q] = d;
-        sok[q] = ok;
+        sd[w][q] = d;
+        sok[w][q] = ok;
     }
-    __syncthreads();
-    const int x = t & 7, y = (t >> 3) & 7, z = t >> 6;
-    int cube = 0;
-    bool usable = true;
+    __syncwarp();
+    bool any = false;
+    uint32_t word[4] = {0, 0, 0, 0};
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-        const int q = (x + corner_x(c)) + 9 * (y + corner_y(c)) + 81 * (z + corner_z(c));
-        usable = usable && sok[q];
-        if (sd[q] < 0.f) cube |= 1 << c;
+    for (int j = 0; j < 16; ++j) {  // cells 16*lane .. 16*lane+15
+        const int c = 16 * lane + j;
+        const int x = c & 7, y = (c >> 3) & 7, z = c >> 6;
+        int cube = 0;
+        bool usable = true;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int q = (x + corner_x(k)) + 9 * (y + corner_y(k)) + 81 * (z + corner_z(k));
+            usable = usable && sok[w][q];
+            if (sd[w][q] < 0.f) cube |= 1 << k;
+        }
+        const uint32_t b = (usable && c_edge_mask[cube]) ? uint32_t(cube) : 0u;
+        any = any || b;
+        word[j >> 2] |= b << (8 * (j & 3));
     }
-    cases[uint64_t(r) * kCells + t] = (usable && c_edge_mask[cube]) ? uint8_t(cube) : uint8_t(0);
+    reinterpret_cast<uint4*>(out)[lane] = make_uint4(word[0], word[1], word[2], word[3]);
+    const bool act = __any_sync(0xFFFFFFFFu, any);
+    if (lane == 0) block_active[r] = act;
 }
 
 // Smallest traversal index among the cells referencing cell-local edge e of the cell
@@ -225,19 +246,28 @@ __device__ inline Owner edge_owner(int e, int lx, int ly, int lz, uint32_t r, co
     return best;
 }
 
+// Per cell: owned-edge mask and face count; one CTA scan of (owned << 16 | faces)
+// gives the cell's local vertex and face offsets. Cells with geometry are appended to
+// the active-cell list (any order: an entry carries its own offsets). Blocks without
+// geometry (k_mesh_case's flag) leave at once.
 __global__ void __launch_bounds__(kCells) k_mesh_own(const uint32_t* __restrict__ nb_rank,
                                                     const uint8_t* __restrict__ cases,
+                                                    const uint8_t* __restrict__ block_active,
                                                     uint32_t* __restrict__ cellinfo,
                                                     unsigned long long* __restrict__ vcount,
-                                                    unsigned long long* __restrict__ fcount) {
+                                                    unsigned long long* __restrict__ fcount,
+                                                    uint4* __restrict__ active, uint32_t active_cap,
+                                                    uint32_t* __restrict__ n_active) {
     using Scan = cub::BlockScan<uint32_t, kCells>;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ uint32_t snr[27];
-    __shared__ uint32_t sfaces;
     const uint32_t r = blockIdx.x;
     const int t = threadIdx.x;
+    if (!block_active[r]) {
+        if (t == 0) vcount[r] = fcount[r] = 0;
+        return;
+    }
     if (t < 27) snr[t] = nb_rank[uint64_t(r) * 27 + t];
-    if (t == 0) sfaces = 0;
     __syncthreads();
     const int cube = cases[uint64_t(r) * kCells + t];
     uint32_t mask = 0;
@@ -251,16 +281,24 @@ __global__ void __launch_bounds__(kCells) k_mesh_own(const uint32_t* __restrict_
             if (edge_owner(e, lx, ly, lz, r, snr, cases).t == self) mask |= 1u << e;
         }
     }
+    const uint32_t nf = cube ? c_ntri[cube] : 0u;
     uint32_t off, total;
-    Scan(tmp).ExclusiveSum(uint32_t(__popc(mask)), off, total);
-    cellinfo[uint64_t(r) * kCells + t] = off | (mask << 12);
-    const uint32_t nf = cube ? c_ntri[cube] : 0;
-    if (nf) atomicAdd(&sfaces, nf);
-    __syncthreads();
+    Scan(tmp).ExclusiveSum((uint32_t(__popc(mask)) << 16) | nf, off, total);
     if (t == 0) {
-        vcount[r] = total;
-        fcount[r] = sfaces;
+        vcount[r] = total >> 16;
+        fcount[r] = total & 0xFFFFu;
     }
+    cellinfo[uint64_t(r) * kCells + t] = (off >> 16) | (mask << 12);
+    const bool act = cube != 0;
+    const uint32_t ballot = __ballot_sync(0xFFFFFFFFu, act);
+    if (!ballot) return;
+    const int lane = t & 31;
+    uint32_t pos = 0;
+    if (lane == 0) pos = atomicAdd(n_active, uint32_t(__popc(ballot)));
+    pos = __shfl_sync(0xFFFFFFFFu, pos, 0) + __popc(ballot & ((1u << lane) - 1));
+    if (act && pos < active_cap)
+        active[pos] = make_uint4(r, uint32_t(t) | (uint32_t(cube) << 9), (off >> 16) | (mask << 12),
+                                 off & 0xFFFFu);
 }
 
 struct MeshOut {
@@ -276,36 +314,31 @@ __device__ inline float nonzero_distance(float d) {  // mesh.cpp:44-48
     return d;
 }
 
-__global__ void __launch_bounds__(kCells) k_mesh_emit(
-    MeshParams mp, const uint64_t* __restrict__ keys, const uint32_t* __restrict__ nb_pool,
+// Thread per active cell: its owned vertices (make_edge_vertex, mesh.cpp:52-95:
+// position, normal, label) and its faces (table triangles, each edge resolved to its
+// owner cell's vertex index, emitted i0, i2, i1: mesh.cpp:179-189).
+__global__ void __launch_bounds__(256) k_mesh_emit(
+    MeshParams mp, const uint4* __restrict__ active, uint32_t n_active,
+    const uint64_t* __restrict__ keys, const uint32_t* __restrict__ nb_pool,
     const uint32_t* __restrict__ nb_rank, const uint8_t* __restrict__ cases,
     const uint32_t* __restrict__ cellinfo, const unsigned long long* __restrict__ vbase,
     const unsigned long long* __restrict__ fbase, const svx_tsdf_voxel* __restrict__ pool,
     const float* __restrict__ sem, const uint32_t* __restrict__ sem_idx, MeshOut out) {
-    using Scan = cub::BlockScan<uint32_t, kCells>;
-    __shared__ typename Scan::TempStorage tmp;
-    __shared__ uint32_t snr[27], snp[27];
-    const uint32_t r = blockIdx.x;
-    const int t = threadIdx.x;
-    if (t < 27) {
-        snr[t] = nb_rank[uint64_t(r) * 27 + t];
-        snp[t] = nb_pool[uint64_t(r) * 27 + t];
-    }
-    __syncthreads();
-    const int cube = cases[uint64_t(r) * kCells + t];
-    const uint32_t nf = cube ? c_ntri[cube] : 0;
-    uint32_t foff, ftotal;
-    Scan(tmp).ExclusiveSum(nf, foff, ftotal);
-    if (!cube) return;
-    const uint32_t info = cellinfo[uint64_t(r) * kCells + t];
-    const uint32_t loff = info & 0xFFFu, mask = info >> 12;
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_active) return;
+    const uint4 a = active[i];
+    const uint32_t r = a.x;
+    const int t = int(a.y & 511u), cube = int(a.y >> 9);
+    const uint32_t loff = a.z & 0xFFFu, mask = a.z >> 12, foff = a.w;
+    const uint32_t* snr = nb_rank + uint64_t(r) * 27;
+    const uint32_t* snp = nb_pool + uint64_t(r) * 27;
     const int lx = t & 7, ly = (t >> 3) & 7, lz = t >> 6;
     int32_t kx, ky, kz;
     unpack_key(keys[r], kx, ky, kz);
     const int32_t gx = kx * kBlockSide + lx, gy = ky * kBlockSide + ly, gz = kz * kBlockSide + lz;
     const uint64_t vb = vbase[r] + loff;
 
-    // ---- owned vertices, in edge order (make_edge_vertex, mesh.cpp:52-95)
+    // ---- owned vertices, in edge order
     uint32_t om = mask;
     uint32_t j = 0;
     while (om) {
@@ -316,8 +349,8 @@ __global__ void __launch_bounds__(kCells) k_mesh_emit(
         // lower endpoint a (the edge base) and upper endpoint b, cell-relative in [0, 8]
         const int ax = lx + ox, ay = ly + oy, az = lz + oz;
         const int bx2 = ax + (axis == 0), by2 = ay + (axis == 1), bz2 = az + (axis == 2);
-        const uint32_t pa = snp[nb27(ax >> 3, ay >> 3, az >> 3)];
-        const uint32_t pb = snp[nb27(bx2 >> 3, by2 >> 3, bz2 >> 3)];
+        const uint32_t pa = __ldg(&snp[nb27(ax >> 3, ay >> 3, az >> 3)]);
+        const uint32_t pb = __ldg(&snp[nb27(bx2 >> 3, by2 >> 3, bz2 >> 3)]);
         const int la = (ax & 7) + 8 * (ay & 7) + 64 * (az & 7);
         const int lb = (bx2 & 7) + 8 * (by2 & 7) + 64 * (bz2 & 7);
         const svx_tsdf_voxel va = pool[uint64_t(pa) * kBlockVoxels + la];
@@ -369,7 +402,7 @@ __global__ void __launch_bounds__(kCells) k_mesh_emit(
         ++j;
     }
 
-    // ---- faces (mesh.cpp:179-189): table triangles, emitted (i0, i2, i1)
+    // ---- faces
     uint32_t vid[12];
     uint32_t em = c_edge_mask[cube];
     while (em) {
@@ -384,6 +417,7 @@ __global__ void __launch_bounds__(kCells) k_mesh_emit(
         }
     }
     const uint64_t fb = fbase[r] + foff;
+    const uint32_t nf = c_ntri[cube];
     for (uint32_t k = 0; k < nf; ++k) {
         const uint32_t i0 = vid[c_tris[cube][3 * k]], i1 = vid[c_tris[cube][3 * k + 1]],
                        i2 = vid[c_tris[cube][3 * k + 2]];
@@ -461,14 +495,22 @@ void run_extract_mesh(svx_map* m, float min_weight, int reserved, const uint64_t
     MeshParams mp{R, min_weight, reserved, m->cfg.num_labels, double(m->cfg.voxel_size)};
     ms.cases.alloc(uint64_t(R) * kCells);
     ms.cellinfo.alloc(uint64_t(R) * kCells);
-    ms.counts.alloc(4ull * (R + 1));
+    ms.counts.alloc(4ull * (R + 1) + 1);
     unsigned long long* vcount = ms.counts.p;
     unsigned long long* fcount = vcount + (R + 1);
     unsigned long long* vbase = fcount + (R + 1);
     unsigned long long* fbase = vbase + (R + 1);
-    k_mesh_case<<<R, kCells, 0, st>>>(mp, ms.nb_pool.p, tsdf_base(m), ms.cases.p);
+    ms.block_active.alloc(R);
+    const unsigned wgrid = (R + kWarpsPerCta - 1) / kWarpsPerCta;
+    k_mesh_case<<<wgrid, 32 * kWarpsPerCta, 0, st>>>(mp, ms.nb_pool.p, tsdf_base(m), ms.cases.p,
+                                                     ms.block_active.p);
     count_launch();
-    k_mesh_own<<<R, kCells, 0, st>>>(ms.nb_rank.p, ms.cases.p, ms.cellinfo.p, vcount, fcount);
+    if (!ms.active.p) ms.active.alloc(std::max<uint64_t>(1u << 20, uint64_t(R) * 32));
+    SVX_CUDA(cudaMemsetAsync(ms.counts.p + 4ull * (R + 1), 0, 8, st));  // active-cell counter
+    uint32_t* n_active = reinterpret_cast<uint32_t*>(ms.counts.p + 4ull * (R + 1));
+    k_mesh_own<<<R, kCells, 0, st>>>(ms.nb_rank.p, ms.cases.p, ms.block_active.p, ms.cellinfo.p, vcount,
+                                     fcount, ms.active.p,
+                                     uint32_t(std::min<uint64_t>(ms.active.n, 0xFFFFFFFFu)), n_active);
     count_launch();
     SVX_CUDA(cudaMemsetAsync(vcount + R, 0, 8, st));
     SVX_CUDA(cudaMemsetAsync(fcount + R, 0, 8, st));
@@ -477,18 +519,30 @@ void run_extract_mesh(svx_map* m, float min_weight, int reserved, const uint64_t
     m->sort_tmp.alloc(bytes);
     SVX_CUDA(cub::DeviceScan::ExclusiveSum(m->sort_tmp.p, bytes, vcount, vbase, int(R + 1), st));
     SVX_CUDA(cub::DeviceScan::ExclusiveSum(m->sort_tmp.p, bytes, fcount, fbase, int(R + 1), st));
-    unsigned long long tot[2];
+    unsigned long long tot[3];
     SVX_CUDA(cudaMemcpyAsync(&tot[0], vbase + R, 8, cudaMemcpyDeviceToHost, st));
     SVX_CUDA(cudaMemcpyAsync(&tot[1], fbase + R, 8, cudaMemcpyDeviceToHost, st));
+    SVX_CUDA(cudaMemcpyAsync(&tot[2], n_active, 8, cudaMemcpyDeviceToHost, st));
     SVX_CUDA(cudaStreamSynchronize(st));
     if (tot[0] >= (1ull << 32)) throw Error(SVX_CAPACITY, "mesh has more than 2^32 vertices");
+    const uint32_t na = uint32_t(tot[2] & 0xFFFFFFFFu);
+    if (na > ms.active.n) {  // list too small: grow and redo the (idempotent) ownership pass
+        ms.active.release();
+        ms.active.alloc(na + na / 4);
+        SVX_CUDA(cudaMemsetAsync(n_active, 0, 4, st));
+        k_mesh_own<<<R, kCells, 0, st>>>(ms.nb_rank.p, ms.cases.p, ms.block_active.p, ms.cellinfo.p,
+                                         vcount, fcount, ms.active.p, uint32_t(ms.active.n), n_active);
+        count_launch();
+    }
     ms.verts.alloc(3 * tot[0] + 1);
     ms.normals.alloc(3 * tot[0] + 1);
     ms.labels.alloc(tot[0] + 1);
     ms.faces.alloc(3 * tot[1] + 1);
-    k_mesh_emit<<<R, kCells, 0, st>>>(mp, keys, ms.nb_pool.p, ms.nb_rank.p, ms.cases.p, ms.cellinfo.p,
-                                      vbase, fbase, tsdf_base(m), sem_base(m), m->sem_idx,
-                                      MeshOut{ms.verts.p, ms.normals.p, ms.labels.p, ms.faces.p});
+    if (na)
+        k_mesh_emit<<<(na + 255) / 256, 256, 0, st>>>(
+            mp, ms.active.p, na, keys, ms.nb_pool.p, ms.nb_rank.p, ms.cases.p, ms.cellinfo.p, vbase,
+            fbase, tsdf_base(m), sem_base(m), m->sem_idx,
+            MeshOut{ms.verts.p, ms.normals.p, ms.labels.p, ms.faces.p});
     count_launch();
     SVX_CUDA(cudaStreamSynchronize(st));
     ms.n_vertices = tot[0];
