@@ -262,6 +262,11 @@ def main():
     def make_store():
         st = svx.VoxelStore(cfg, device=local)
         st.set_shard(rank, world)
+        # diagnostic: one rank's share of an N-way key shard on a single GPU
+        # (SVX_SIM_SHARD="r,N"), for per-rank cost estimates without N GPUs
+        sim = os.environ.get("SVX_SIM_SHARD")
+        if sim and world == 1:
+            st.set_shard(*[int(x) for x in sim.split(",")])
         return st
 
     def run_leg(store, host_pts=None, clocks=None):

@@ -269,3 +269,43 @@ def test_label_batches_match_single_calls(variant):
     assert reps[0][-1][1] > 0
     assert reps[1] == reps[0] and reps[2] == reps[0]
     assert maps[1] == maps[0] and maps[2] == maps[0]
+
+
+def test_key_sharded_maps_union_equals_unsharded():
+    """two key shards (svx_map_set_shard, world 2) integrate the same
+    scans and label images; they hold disjoint block sets, their per-frame reports sum
+    to the unsharded map's, and their union is the unsharded map block for block."""
+    from oracle.bindings import parse_svox1
+    wl = W.make("tiny", 3)
+    cfg = svx.MapConfig(wl.voxel_size, wl.truncation, wl.num_labels, 1 << 18)
+    maps = []
+    for shard in (None, (0, 2), (1, 2)):
+        g = svx.VoxelStore(cfg, 0)
+        if shard:
+            g.set_shard(*shard)
+        ti, si = svx.TsdfIntegrator(g, svx.IntegratorConfig()), svx.SemanticIntegrator(g)
+        reps = []
+        for p, i in wl.scans():
+            r = ti.integrate_cloud(p.numpy(), wl.pose(i), wl.model)
+            s = [si.integrate_labels(li).updated_voxels for li in wl.label_images(i)]
+            reps.append((r.updated_voxels, r.new_blocks, sum(s)))
+        maps.append((g, np.array(reps)))
+    full, s0, s1 = maps
+    assert np.array_equal(s0[1] + s1[1], full[1])
+    _, kf, tf, sf = parse_svox1(full[0].save_bytes())
+    parts = [parse_svox1(m.save_bytes()) for m, _ in (s0, s1)]
+    assert len(parts[0][1]) > 0 and len(parts[1][1]) > 0
+    keys = np.concatenate([p[1] for p in parts])
+    tsdf = np.concatenate([p[2] for p in parts])
+    has = np.concatenate([[i in p[3] for i in range(len(p[1]))] for p in parts])
+    order = np.lexsort((keys[:, 2], keys[:, 1], keys[:, 0]))
+    assert np.array_equal(keys[order], kf)
+    assert tsdf[order].tobytes() == tf.tobytes()
+    assert np.array_equal(has[order], np.array([i in sf for i in range(len(kf))]))
+    sems = [p[3][i] for p in parts for i in range(len(p[1])) if i in p[3]]
+    sem_order = [j for j in order if has[j]]
+    idx = {j: n for n, j in enumerate([j for j in range(len(keys)) if has[j]])}
+    for n_full, j in enumerate(sem_order):
+        assert np.array_equal(sems[idx[j]], sf[sorted(sf)[n_full]])
+    for g, _ in maps:
+        g.close()
