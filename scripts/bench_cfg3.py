@@ -22,8 +22,8 @@ n_warm, n_timed = int(os.environ.get("WARM", "5")), int(os.environ.get("FRAMES",
 n_cpu = int(os.environ.get("CPU_FRAMES", "3"))
 wl = W.make("cfg3", n_warm + n_timed)
 frames = list(range(n_warm + n_timed))
-scans = {i: p.numpy() for p, i in wl.scans()}
-labels = {i: wl.label_images(i) for i in frames}
+scans = {i: p.cpu().numpy() for p, i in wl.scans(device="cuda")}  # rendered on the GPU
+labels = {i: wl.label_images(i, device="cuda") for i in frames}
 cfg = svx.MapConfig(wl.voxel_size, wl.truncation, wl.num_labels, 1 << 22)
 offs = np.zeros(len(frames) + 1, np.uint64)
 offs[1:] = np.cumsum([len(scans[i]) for i in frames])
