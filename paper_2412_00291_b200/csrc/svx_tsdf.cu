@@ -508,7 +508,14 @@ k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __re
         cache[p] = pc;
     }
     // band ray (tsdf_integrator.cpp:123-131)
+#ifdef SVX_DIAG_NODDA  // timing diagnostic builds only (results invalid)
+    const bool cast = false;
+#else
     const bool cast = in_range && !(f.drop_unreliable && f.has_normals && !valid[p]);
+#endif
+#ifdef SVX_DIAG_NOVISIT
+    uint32_t diag_sink = 0;
+#endif
     if (cast) {
         warp_agg_inc(&ctr[C_RAYS]);
         const d3 tr = scale3(f.tau, ray);  // (q - o).normalized() == (q - o) / range
@@ -523,6 +530,10 @@ k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __re
         bool first = true;
         const bool all_own = band_all_own(f, hd, p, r);
         traverse_segment(a, b, f.nu, f.inv_nu, [&](int32_t x, int32_t y, int32_t z) {
+#ifdef SVX_DIAG_NOVISIT
+            diag_sink += uint32_t(x ^ y ^ z);
+            return;
+#endif
             const int32_t bx = block_coord(x), by = block_coord(y), bz = block_coord(z);
             if (!key_in_range(bx) || !key_in_range(by) || !key_in_range(bz)) {
                 atomicOr(&ctr[C_ABORT], kAbortKey);
@@ -590,6 +601,9 @@ k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __re
             }
         });
         if (pend_word >= 0) atomicOr(&lmask[0][0] + pend_word, pend_bits);
+#ifdef SVX_DIAG_NOVISIT
+        if (diag_sink == 0xFFFFFFFFu) atomicOr(&ctr[C_ABORT], 0u);
+#endif
     }
     __syncthreads();
     // one global hash operation per distinct block of the tile; first touches of
