@@ -8,8 +8,9 @@
 //                 centre) with a conservative margin. A block is dropped only if
 //                 all 8 corners are outside one half-space, so no voxel the
 //                 reference would update is lost: results are identical.
-//   k_sem_update  persistent warps, one candidate block per iteration, lane =
-//                 voxel. Per voxel exactly the reference test sequence (observed,
+//   k_sem_update  persistent warps (grid = the resident CTAs), one eighth of a
+//                 candidate block per task (2 voxels per lane: short chains of
+//                 dependent loads), lane = voxel. Per voxel exactly the reference test sequence (observed,
 //                 D >= -tau/2, 0 < z <= max_depth, pixel in bounds, optional
 //                 raycast occlusion), then likelihood (tensor or label +
 //                 confidence, floored and renormalised in f32) and the Bayes
@@ -236,6 +237,12 @@ __device__ inline void bayes_step(float* probs, const Like& like, int K, bool us
     }
 }
 
+#ifndef SVX_SEM_PARTS
+#define SVX_SEM_PARTS 8
+#endif
+constexpr int kParts = SVX_SEM_PARTS;  // warp tasks per candidate block
+constexpr uint32_t kLayerClaim = 0xFFFFFFFEu;  // semantic layer being allocated
+
 template <int KC>
 __global__ void __launch_bounds__(kThreads)
 k_sem_update(SemParams sp, HashView h, const uint64_t* __restrict__ block_keys,
@@ -251,16 +258,20 @@ k_sem_update(SemParams sp, HashView h, const uint64_t* __restrict__ block_keys,
     const uint32_t n_cand = ctr[C_CAND];
     const int K = KC > 0 ? KC : sp.K;
     uint32_t n_upd = 0;
-    for (uint32_t t = warp; t < n_cand; t += nwarps) {
-        const uint32_t idx = cand[t];
+    // task = (candidate block, quarter): 4 voxels per lane keeps each warp's chain of
+    // dependent loads short; the grid is sized to the resident CTAs
+    for (uint32_t t = warp; t < kParts * n_cand; t += nwarps) {
+        const uint32_t idx = cand[t / kParts];
+        const int part = int(t % kParts);
         const uint64_t key = block_keys[idx];
         const svx_tsdf_voxel* blk = pool + uint64_t(idx) * kBlockVoxels;
-        uint32_t pix[16];
+        constexpr int kPer = kBlockVoxels / 32 / kParts;
+        uint32_t pix[kPer];
         uint32_t pass = 0;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < kPer; ++j) {
             pix[j] = 0;
-            const int linear = j * 32 + lane;
+            const int linear = (part * kPer + j) * 32 + lane;
             const float w = blk[linear].weight;
             const float dist = blk[linear].distance;
             if (!(w > 0.f)) continue;
@@ -276,22 +287,37 @@ k_sem_update(SemParams sp, HashView h, const uint64_t* __restrict__ block_keys,
             pass |= 1u << j;
         }
         if (!__any_sync(0xFFFFFFFFu, pass != 0)) continue;
-        uint32_t sid = sem_idx[idx];
-        if (sid == kInvalid) {
+        // the block's semantic layer (ensure_semantics): the first part to need it
+        // claims it, fills it with 1/K and publishes its index; other parts wait
+        uint32_t sid = __ldcg(&sem_idx[idx]);
+        if (sid == kInvalid || sid == kLayerClaim) {
+            uint32_t claimed = 0;
             if (lane == 0) {
-                sid = atomicAdd(&ctr[C_SEM], 1u);
-                sem_idx[idx] = sid;
+                const uint32_t old = atomicCAS(&sem_idx[idx], kInvalid, kLayerClaim);
+                if (old == kInvalid) {
+                    sid = atomicAdd(&ctr[C_SEM], 1u);
+                    claimed = 1;
+                } else {
+                    volatile uint32_t* vs = sem_idx + idx;
+                    while ((sid = *vs) == kLayerClaim) {
+                    }
+                }
             }
             sid = __shfl_sync(0xFFFFFFFFu, sid, 0);
-            float* layer = sem + uint64_t(sid) * kBlockVoxels * K;
-            const float u0 = 1.f / float(K);
-            for (int i = lane; i < kBlockVoxels * K; i += 32) layer[i] = u0;
-            __syncwarp();
+            claimed = __shfl_sync(0xFFFFFFFFu, claimed, 0);
+            if (claimed) {
+                float* layer = sem + uint64_t(sid) * kBlockVoxels * K;
+                const float u0 = 1.f / float(K);
+                for (int i = lane; i < kBlockVoxels * K; i += 32) layer[i] = u0;
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) atomicExch(&sem_idx[idx], sid);
+            }
         }
 #pragma unroll 1
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < kPer; ++j) {
             if (!((pass >> j) & 1u)) continue;
-            const int linear = j * 32 + lane;
+            const int linear = (part * kPer + j) * 32 + lane;
             const uint32_t px = pix[j];
             Like like{nullptr, sp.floor_v, 0.f, 0.f, 0.f, -1, 0.f};
             if (sp.has_tensor) {
@@ -443,7 +469,10 @@ void run_integrate_labels_batch(svx_map* m, const svx_label_image* imgs, int n, 
                     case 32: kern = &k_sem_update<32>; break;
                     default: break;
                 }
-                kern<<<persistent_grid(m->device), kThreads, 0, m->stream>>>(
+                int per_sm = 0;
+                SVX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0));
+                const unsigned grid = std::max(1u, unsigned(per_sm)) * (persistent_grid(m->device) / 8);
+                kern<<<grid, kThreads, 0, m->stream>>>(
                     sp, hash_view(m), m->block_keys, tsdf_base(m), sem_base(m), m->sem_idx, m->cand.p, lbl,
                     conf, ten, m->dirty + m->cfg.max_blocks, m->d_ctr);
                 count_launch();
