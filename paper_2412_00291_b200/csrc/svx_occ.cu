@@ -457,16 +457,15 @@ void validate(const svx_occ_cfg& c) {
 }
 
 // Maps and zero-fills the pool so that `blocks` blocks are usable (new blocks must
-// read as zero: tags 0 < every serial), plus headroom mapped in the background.
+// read as zero: tags 0 < every serial). Only the growth is zeroed; mapping ahead of
+// need runs on the pool's background thread.
 void map_blocks(svx_occ* m, uint64_t blocks) {
     blocks = std::min<uint64_t>(blocks, m->cfg.max_blocks);
-    const uint64_t ready = std::min<uint64_t>(m->pool.mapped() / kOccBlockBytes, m->cfg.max_blocks);
-    const uint64_t target = std::max(blocks, ready);  // adopt a finished prefetch too
-    if (target <= m->mapped_blocks) return;
-    if (target * kOccBlockBytes > m->pool.mapped()) m->pool.ensure(target * kOccBlockBytes);
+    if (blocks <= m->mapped_blocks) return;
+    m->pool.ensure(blocks * kOccBlockBytes);  // immediate when a prefetch already covers it
     SVX_CUDA(cudaMemsetAsync(static_cast<uint8_t*>(m->pool.base()) + m->mapped_blocks * kOccBlockBytes, 0,
-                             (target - m->mapped_blocks) * kOccBlockBytes, m->stream));
-    m->mapped_blocks = target;
+                             (blocks - m->mapped_blocks) * kOccBlockBytes, m->stream));
+    m->mapped_blocks = blocks;
 }
 
 void map_layers(svx_occ* m, uint64_t layers) {
@@ -504,8 +503,9 @@ void occ_scan(svx_occ* m, const float* d_pts, const uint16_t* d_lbl, const float
     p.shard_rank = m->shard_rank;
     p.shard_world = m->shard_world;
     // headroom for this scan's new blocks, mapped and zeroed ahead of the launch
-    map_blocks(m, m->n_blocks + std::max<uint64_t>(m->min_headroom, 2 * m->max_new_blocks));
-    m->pool.prefetch(std::min<uint64_t>(m->cfg.max_blocks, 2 * m->mapped_blocks) * kOccBlockBytes);
+    const uint64_t head = std::max<uint64_t>(m->min_headroom, 2 * m->max_new_blocks);
+    map_blocks(m, m->n_blocks + head);
+    m->pool.prefetch(std::min<uint64_t>(m->cfg.max_blocks, m->n_blocks + 4 * head) * kOccBlockBytes);
     p.mapped_blocks = uint32_t(m->mapped_blocks);
     m->h_ctr[O_BLOCKS] = uint32_t(m->n_blocks);
     m->h_ctr[O_LAYERS] = uint32_t(m->n_layers);
