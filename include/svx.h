@@ -393,6 +393,10 @@ svx_status svx_lidar_spinning(int32_t width, int32_t height_px, double fov_up_de
 /* Key sharding for multi-GPU: this map owns only blocks with
  * owner(b) == rank among world ranks. world=1 owns everything. */
 svx_status svx_map_set_shard(svx_map* map, int32_t rank, int32_t world);
+/* Maps physical memory for `blocks` TSDF blocks and `layers` semantic layers now
+ * (CUDA VMM; addresses never move), so that a growing map does not pay the mapping
+ * calls on its critical path. No effect on results. */
+svx_status svx_map_reserve(svx_map* map, uint64_t blocks, uint64_t layers);
 /* owner(bxyz) under the same hash, for host-side routing and tests. */
 int32_t svx_block_owner(const int32_t bxyz[3], int32_t world);
 

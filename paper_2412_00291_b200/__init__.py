@@ -205,6 +205,7 @@ def _sig(lib: C.CDLL) -> None:
         "svx_profile_read": (S, [P, C.POINTER(ProfileC)]),
         "svx_block_owner": (C.c_int32, [C.POINTER(C.c_int32), C.c_int32]),
         "svx_has_blocks": (S, [P, P, C.c_uint64, P]),
+        "svx_map_reserve": (S, [P, C.c_uint64, C.c_uint64]),
         "svx_mesh_extract": (S, [P, C.c_float, C.c_int32, P, C.c_uint64, C.POINTER(C.c_uint64),
                                  C.POINTER(C.c_uint64)]),
         "svx_mesh_read": (S, [P, P, P, P, P]),
@@ -557,6 +558,10 @@ class VoxelStore:
         h = C.c_void_p()
         _check(lib().svx_load(str(path).encode(), device, max_blocks, C.byref(h)))
         return VoxelStore(device=device, _handle=h)
+
+    def reserve(self, blocks: int, layers: int = 0) -> None:
+        """Map pool memory for `blocks` TSDF blocks / `layers` semantic layers up front."""
+        _check(lib().svx_map_reserve(self._h, blocks, layers))
 
     def has_blocks(self, coords) -> np.ndarray:
         """find_block(b) != nullptr for many blocks at once."""

@@ -470,6 +470,16 @@ svx_status svx_map_set_shard(svx_map* m, int32_t rank, int32_t world) {
     });
 }
 
+svx_status svx_map_reserve(svx_map* m, uint64_t blocks, uint64_t layers) {
+    return guarded([&] {
+        require(m != nullptr, SVX_INVALID_ARGUMENT, "null map");
+        DeviceGuard g(m->device);
+        SVX_CUDA(cudaStreamSynchronize(m->stream));
+        ensure_blocks(m, std::max<uint64_t>(blocks, m->n_blocks), 0);
+        ensure_layers(m, std::min<uint64_t>(layers, m->cfg.max_blocks));
+    });
+}
+
 int32_t svx_block_owner(const int32_t b[3], int32_t world) {
     return owner_of(pack_key(b[0], b[1], b[2]), world);
 }
