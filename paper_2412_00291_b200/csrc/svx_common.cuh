@@ -184,9 +184,27 @@ __device__ inline void world_to_voxel(d3 p, double inv, int32_t c[3]) {
 // nonneg_mod == & 7 on two's complement (types.hpp:35-44, 81-89).
 __host__ __device__ inline int32_t block_coord(int32_t c) { return c >> 3; }
 
+// One axis of traverse_segment's set-up (tsdf_integrator.hpp:108-120).
+__device__ inline void dda_axis(double d, double a, int32_t c, double nu, int32_t& step,
+                                double& t_max, double& t_delta) {
+    if (fabs(d) < 1e-15) {
+        step = 0;
+        t_max = CUDART_INF;
+        t_delta = CUDART_INF;
+    } else {
+        step = d > 0 ? 1 : -1;
+        const double boundary = nu * (double(c) + 0.5 * step);
+        t_max = (boundary - a) / d;
+        t_delta = nu / fabs(d);
+    }
+}
+
 // traverse_segment (tsdf_integrator.hpp:93-135); visit(x, y, z) per cell.
 // (shared by the TSDF band and the occupancy carving)
-template <typename Visit>
+// kArrays: the per-axis state in 3-element arrays indexed by the chosen axis (local
+// memory; measured ~1% faster in the register-limited TSDF band kernel), else scalars
+// (the occupancy visit: 1.3x, no stack frame).
+template <bool kArrays = false, typename Visit>
 __device__ inline void traverse_segment(d3 a, d3 b, double nu, double inv, Visit&& visit) {
     int32_t cur[3], end[3];
     world_to_voxel(a, inv, cur);
@@ -198,33 +216,47 @@ __device__ inline void traverse_segment(d3 a, d3 b, double nu, double inv, Visit
         return;
     }
     dir = div3(dir, len);
-    const double dv[3] = {dir.x, dir.y, dir.z};
-    const double av[3] = {a.x, a.y, a.z};
-    int32_t step[3];
-    double t_max[3], t_delta[3];
+    if constexpr (kArrays) {
+        const double dv[3] = {dir.x, dir.y, dir.z};
+        const double av[3] = {a.x, a.y, a.z};
+        int32_t step[3];
+        double t_max[3], t_delta[3];
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        if (fabs(dv[i]) < 1e-15) {
-            step[i] = 0;
-            t_max[i] = CUDART_INF;
-            t_delta[i] = CUDART_INF;
-        } else {
-            step[i] = dv[i] > 0 ? 1 : -1;
-            const double boundary = nu * (double(cur[i]) + 0.5 * step[i]);
-            t_max[i] = (boundary - av[i]) / dv[i];
-            t_delta[i] = nu / fabs(dv[i]);
+        for (int i = 0; i < 3; ++i) dda_axis(dv[i], av[i], cur[i], nu, step[i], t_max[i], t_delta[i]);
+        const uint64_t max_steps = uint64_t(3.0 * len / nu) + 8;
+        for (uint64_t n = 0; n < max_steps; ++n) {
+            visit(cur[0], cur[1], cur[2]);
+            if (cur[0] == end[0] && cur[1] == end[1] && cur[2] == end[2]) return;
+            int m = 0;
+            if (t_max[1] < t_max[m]) m = 1;
+            if (t_max[2] < t_max[m]) m = 2;
+            if (t_max[m] > len) return;
+            cur[m] += step[m];
+            t_max[m] += t_delta[m];
         }
-    }
-    const uint64_t max_steps = uint64_t(3.0 * len / nu) + 8;
-    for (uint64_t n = 0; n < max_steps; ++n) {
-        visit(cur[0], cur[1], cur[2]);
-        if (cur[0] == end[0] && cur[1] == end[1] && cur[2] == end[2]) return;
-        int m = 0;
-        if (t_max[1] < t_max[m]) m = 1;
-        if (t_max[2] < t_max[m]) m = 2;
-        if (t_max[m] > len) return;
-        cur[m] += step[m];
-        t_max[m] += t_delta[m];
+    } else {
+        // Per-axis DDA state in scalars (no dynamically indexed arrays: those live in local
+        // memory); the axis choice and every update are the reference's, in its order.
+        int32_t cx = cur[0], cy = cur[1], cz = cur[2];
+        int32_t sx, sy, sz;
+        double tx, ty, tz, dx, dy, dz;
+        dda_axis(dir.x, a.x, cx, nu, sx, tx, dx);
+        dda_axis(dir.y, a.y, cy, nu, sy, ty, dy);
+        dda_axis(dir.z, a.z, cz, nu, sz, tz, dz);
+        const uint64_t max_steps = uint64_t(3.0 * len / nu) + 8;
+        for (uint64_t n = 0; n < max_steps; ++n) {
+            visit(cx, cy, cz);
+            if (cx == end[0] && cy == end[1] && cz == end[2]) return;
+            // m = argmin with the reference's strict comparisons (ties keep the lower axis)
+            int m = 0;
+            double tm = tx;
+            if (ty < tm) { m = 1; tm = ty; }
+            if (tz < tm) { m = 2; tm = tz; }
+            if (tm > len) return;
+            if (m == 0) { cx += sx; tx += dx; }
+            else if (m == 1) { cy += sy; ty += dy; }
+            else { cz += sz; tz += dz; }
+        }
     }
 }
 

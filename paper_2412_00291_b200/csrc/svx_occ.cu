@@ -189,6 +189,40 @@ __device__ inline void for_each_ray_voxel(const OccParams& p, d3 o, d3 end, bool
     if (hit) fn(ev[0], ev[1], ev[2], kHit);
 }
 
+// Tag updates of one ray, issued kTagBatch at a time: the loads of a batch are in flight
+// together (the DDA does not depend on them), then each RED.MAX is issued only where the
+// tag does not already hold the value. Entries are tag addresses with the HIT flag in
+// bit 1 (tags are 4-byte aligned); the window shifts so every index is static (registers).
+constexpr int kTagBatch = 8;
+struct TagBatch {
+    uintptr_t q[kTagBatch];
+    int n = 0;
+    __device__ TagBatch() {
+#pragma unroll
+        for (int j = 0; j < kTagBatch; ++j) q[j] = 0;
+    }
+    __device__ void flush(uint32_t tag_base) {
+        uint32_t cur[kTagBatch];
+#pragma unroll
+        for (int j = 0; j < kTagBatch; ++j)
+            cur[j] = q[j] ? __ldcg(reinterpret_cast<const uint32_t*>(q[j] & ~uintptr_t(3))) : 0u;
+#pragma unroll
+        for (int j = 0; j < kTagBatch; ++j) {
+            if (!q[j]) continue;
+            const uint32_t want = tag_base + uint32_t((q[j] & 2) ? kHit : kMiss);
+            if (cur[j] < want) atomicMax(reinterpret_cast<uint32_t*>(q[j] & ~uintptr_t(3)), want);
+            q[j] = 0;
+        }
+        n = 0;
+    }
+    __device__ void push(uint32_t* tag, bool is_hit, uint32_t tag_base) {
+#pragma unroll
+        for (int j = 0; j + 1 < kTagBatch; ++j) q[j] = q[j + 1];
+        q[kTagBatch - 1] = reinterpret_cast<uintptr_t>(tag) | (is_hit ? 2u : 0u);
+        if (++n == kTagBatch) flush(tag_base);
+    }
+};
+
 __global__ void __launch_bounds__(256) k_occ_visit(OccParams p, OccDev d) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= p.n) return;
@@ -202,6 +236,7 @@ __global__ void __launch_bounds__(256) k_occ_visit(OccParams p, OccDev d) {
     bool done_before = false;  // redo: this block's updates were applied by the first launch
     const uint32_t lab = label_of(p, i);
     const uint32_t tag_base = p.serial * 4u;
+    TagBatch tb;
     for_each_ray_voxel(p, o, end, hit, [&](int32_t x, int32_t y, int32_t z, int kind) {
         const int32_t bx = block_coord(x), by = block_coord(y), bz = block_coord(z);
         if (!(key_in_range(bx) && key_in_range(by) && key_in_range(bz))) {
@@ -220,15 +255,14 @@ __global__ void __launch_bounds__(256) k_occ_visit(OccParams p, OccDev d) {
             done_before = p.redo && idx < p.prev_blocks;
         }
         if (!base) return;
-        const int lin = local_linear(x, y, z);
         // hot voxels (near the sensor every ray crosses them) are read, not written:
         // same-address writes serialise in L2
-        const uint32_t want = tag_base + uint32_t(kind);
-        if (!done_before && __ldcg(&base[lin]) < want) atomicMax(&base[lin], want);  // RED
+        if (!done_before) tb.push(base + local_linear(x, y, z), kind == kHit, tag_base);
         if (kind == kHit && lab < uint32_t(p.K) && __ldcg(&d.hist_idx[idx]) == kInvalid &&
             atomicCAS(&d.hist_idx[idx], kInvalid, kClaim) == kInvalid)  // histogram layer
             atomicExch(&d.hist_idx[idx], atomicAdd(&d.ctr[O_LAYERS], 1u));
     });
+    tb.flush(tag_base);
 }
 
 // Labelled hits -> class histograms, once the scan is accepted (the adds cannot be

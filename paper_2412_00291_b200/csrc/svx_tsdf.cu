@@ -529,7 +529,7 @@ k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __re
         float p0x = 0.f, p0y = 0.f, p0z = 0.f;
         bool first = true;
         const bool all_own = band_all_own(f, hd, p, r);
-        traverse_segment(a, b, f.nu, f.inv_nu, [&](int32_t x, int32_t y, int32_t z) {
+        traverse_segment<true>(a, b, f.nu, f.inv_nu, [&](int32_t x, int32_t y, int32_t z) {
 #ifdef SVX_DIAG_NOVISIT
             diag_sink += uint32_t(x ^ y ^ z);
             return;
