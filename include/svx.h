@@ -326,6 +326,10 @@ svx_status svx_occ_create(const svx_occ_cfg* cfg, int device, svx_occ** out);
 svx_status svx_occ_destroy(svx_occ* occ);
 svx_status svx_occ_get_stream(svx_occ* occ, void** stream);
 /* Key sharding (as svx_map_set_shard): this map owns blocks with owner(b) == rank. */
+/* Maps and zero-fills pool memory for `blocks` occupancy blocks and `layers` histogram
+ * layers now, so that a growing map does not pay the mapping calls during a scan.
+ * No effect on results. */
+svx_status svx_occ_reserve(svx_occ* occ, uint64_t blocks, uint64_t layers);
 svx_status svx_occ_set_shard(svx_occ* occ, int32_t rank, int32_t world);
 /* One scan: n points of `stride` floats (xyz first), sensor frame; labels (u16 per
  * point) and conf (f32 per point) may be NULL; ptr_is_device: all three in HBM. */

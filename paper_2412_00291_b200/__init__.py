@@ -215,6 +215,7 @@ def _sig(lib: C.CDLL) -> None:
         "svx_occ_destroy": (S, [P]),
         "svx_occ_get_stream": (S, [P, C.POINTER(P)]),
         "svx_occ_set_shard": (S, [P, C.c_int32, C.c_int32]),
+        "svx_occ_reserve": (S, [P, C.c_uint64, C.c_uint64]),
         "svx_occ_integrate": (S, [P, P, P, P, C.c_uint64, C.c_int32, C.c_int32, C.POINTER(PoseC),
                                   C.POINTER(OccReportC)]),
         "svx_occ_integrate_batch": (S, [P, P, P, P, P, C.c_int32, C.c_int32, P, C.c_int32, P]),
@@ -926,6 +927,10 @@ class OccupancyMap:
 
     def set_shard(self, rank: int, world: int) -> None:
         _check(lib().svx_occ_set_shard(self._h, rank, world))
+
+    def reserve(self, blocks: int, layers: int = 0) -> None:
+        """Map pool memory for `blocks` blocks / `layers` histogram layers up front."""
+        _check(lib().svx_occ_reserve(self._h, blocks, layers))
 
     def integrate(self, points, pose, labels=None, conf=None) -> OccReportC:
         p, stride = _as_points(points)

@@ -106,8 +106,7 @@ __device__ inline uint32_t slot_idx(const OccSlot* sl) {
     return idx;
 }
 
-// Find-or-insert of a block; marks it touched by this scan (plain store: the
-// touched list is compacted from the marks after the visit pass).
+// Find-or-insert of a block.
 __device__ inline uint32_t claim_block(const OccParams& p, const OccDev& d, uint64_t key) {
     uint32_t s = hash_slot(key, d.log2cap);
     uint32_t idx = kInvalid;
@@ -144,8 +143,7 @@ __device__ inline uint32_t claim_block(const OccParams& p, const OccDev& d, uint
         return kInvalid;
     }
     if (idx == kOverflow) return kInvalid;
-    if (__ldcg(&d.block_tag[idx]) != p.serial) d.block_tag[idx] = p.serial;  // hot blocks: read, not write
-    return idx;
+    return idx;  // the caller marks the block touched (block_tag = serial)
 }
 
 __device__ inline uint32_t find_block(const OccDev& d, uint64_t key) {
@@ -194,6 +192,13 @@ __device__ inline void for_each_ray_voxel(const OccParams& p, d3 o, d3 end, bool
 // tag does not already hold the value. Entries are tag addresses with the HIT flag in
 // bit 1 (tags are 4-byte aligned); the window shifts so every index is static (registers).
 constexpr int kTagBatch = 8;
+// Only the first kNearVoxels cells of a ray (next to the sensor, where every ray of the
+// scan passes) go through the load-then-RED batch; beyond them few rays share a voxel
+// and the RED.MAX is issued directly (no load, nothing to wait for).
+#ifndef SVX_OCC_NEAR
+#define SVX_OCC_NEAR 32
+#endif
+constexpr uint32_t kNearVoxels = SVX_OCC_NEAR;
 struct TagBatch {
     uintptr_t q[kTagBatch];
     int n = 0;
@@ -223,7 +228,22 @@ struct TagBatch {
     }
 };
 
+// Per-CTA cache of the near blocks' hash lookups (key -> pool index) in shared memory:
+// every ray of the scan starts at the sensor, so the blocks there are looked up by
+// every thread. Direct-mapped, first come keeps the slot: the key is claimed with a
+// CAS, and its index is published (one 32-bit store) after the block has been marked
+// touched, so a hit needs neither the global probe nor the mark; a reader that sees
+// the key before the index falls back to the global path.
+constexpr int kBlockCache = 2048;
+
 __global__ void __launch_bounds__(256) k_occ_visit(OccParams p, OccDev d) {
+    __shared__ unsigned long long ckey[kBlockCache];
+    __shared__ uint32_t cidx[kBlockCache];
+    for (int j = threadIdx.x; j < kBlockCache; j += blockDim.x) {
+        ckey[j] = kEmptyKey;
+        cidx[j] = kInvalid;
+    }
+    __syncthreads();
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= p.n) return;
     d3 o, end;
@@ -237,7 +257,9 @@ __global__ void __launch_bounds__(256) k_occ_visit(OccParams p, OccDev d) {
     const uint32_t lab = label_of(p, i);
     const uint32_t tag_base = p.serial * 4u;
     TagBatch tb;
+    uint32_t nv = 0;  // cells of this ray visited so far
     for_each_ray_voxel(p, o, end, hit, [&](int32_t x, int32_t y, int32_t z, int kind) {
+        ++nv;
         const int32_t bx = block_coord(x), by = block_coord(y), bz = block_coord(z);
         if (!(key_in_range(bx) && key_in_range(by) && key_in_range(bz))) {
             atomicAdd(&d.ctr[O_ERR_KEY], 1u);
@@ -246,7 +268,24 @@ __global__ void __launch_bounds__(256) k_occ_visit(OccParams p, OccDev d) {
         const uint64_t key = pack_key(bx, by, bz);
         if (key != last) {
             last = key;
-            idx = owned(p, key) ? claim_block(p, d, key) : kInvalid;
+            idx = kInvalid;
+            if (owned(p, key)) {
+                const bool near = nv <= kNearVoxels;
+                const uint32_t h = uint32_t((key * 0x9E3779B97F4A7C15ull) >> 53) & (kBlockCache - 1);
+                if (near && ckey[h] == key) idx = *reinterpret_cast<volatile uint32_t*>(&cidx[h]);
+                if (idx == kInvalid) {
+                    idx = claim_block(p, d, key);
+                    if (idx != kInvalid) {
+                        if (near) {  // hot block: read, not write (same-address writes serialise)
+                            if (__ldcg(&d.block_tag[idx]) != p.serial) d.block_tag[idx] = p.serial;
+                            if (ckey[h] == kEmptyKey && atomicCAS(&ckey[h], kEmptyKey, key) == kEmptyKey)
+                                cidx[h] = idx;
+                        } else {
+                            atomicMax(&d.block_tag[idx], p.serial);  // RED: tags only grow
+                        }
+                    }
+                }
+            }
             base = nullptr;
             if (idx != kInvalid) {
                 if (idx < p.mapped_blocks) base = d.pool + uint64_t(idx) * kOccWords;
@@ -257,7 +296,10 @@ __global__ void __launch_bounds__(256) k_occ_visit(OccParams p, OccDev d) {
         if (!base) return;
         // hot voxels (near the sensor every ray crosses them) are read, not written:
         // same-address writes serialise in L2
-        if (!done_before) tb.push(base + local_linear(x, y, z), kind == kHit, tag_base);
+        if (!done_before) {
+            if (nv < kNearVoxels) tb.push(base + local_linear(x, y, z), kind == kHit, tag_base);
+            else atomicMax(base + local_linear(x, y, z), tag_base + uint32_t(kind));  // RED
+        }
         if (kind == kHit && lab < uint32_t(p.K) && __ldcg(&d.hist_idx[idx]) == kInvalid &&
             atomicCAS(&d.hist_idx[idx], kInvalid, kClaim) == kInvalid)  // histogram layer
             atomicExch(&d.hist_idx[idx], atomicAdd(&d.ctr[O_LAYERS], 1u));
@@ -696,6 +738,16 @@ svx_status svx_occ_get_stream(svx_occ* m, void** stream) {
     return api_guard([&] {
         require(m && stream, SVX_INVALID_ARGUMENT, "null argument");
         *stream = m->stream;
+    });
+}
+
+svx_status svx_occ_reserve(svx_occ* m, uint64_t blocks, uint64_t layers) {
+    return api_guard([&] {
+        require(m != nullptr, SVX_INVALID_ARGUMENT, "null map");
+        DevGuard g(m->device);
+        map_blocks(m, blocks);
+        map_layers(m, std::min<uint64_t>(layers, m->cfg.max_blocks));
+        SVX_CUDA(cudaStreamSynchronize(m->stream));
     });
 }
 
