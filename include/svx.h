@@ -343,6 +343,26 @@ svx_status svx_occ_integrate_batch(svx_occ* occ, const float* points, const uint
                                    const float* conf, const uint64_t* offsets, int32_t stride,
                                    int32_t ptr_is_device, const svx_pose* poses,
                                    int32_t n_frames, svx_occ_report* reports);
+/* Pinhole depth images (BASELINE.json configs[2]: multi-camera semantic depth images;
+ * no reference implementation, parity unpinned). Camera frame: x right, y down, z
+ * forward, the reference's LabelImage convention (semantic_integrator.cpp:117-121:
+ * u = floor(fx*x/z + cx)), so pixel (u, v) is back-projected through its centre:
+ *   x = f32((u + 0.5 - cx) * z / fx),  y = f32((v + 0.5 - cy) * z / fy)   (FP64, that
+ *   order), point = (x, y, z) for a finite depth 0 < z <= max_depth (metres, f32),
+ * and the pixel is dropped otherwise. Each image is then one scan of the occupancy
+ * contract above (ray from the camera centre, labels[pixel] / conf[pixel]), exactly as
+ * svx_occ_integrate with that point cloud. */
+typedef struct {
+    int32_t width, height;
+    double fx, fy, cx, cy;
+    double max_depth;
+} svx_pinhole;
+/* n_images images, row-major (v * width + u), concatenated in order in depth / labels /
+ * conf (labels and conf may be NULL); cams[i] and cam_to_world[i] per image. */
+svx_status svx_occ_integrate_depth(svx_occ* occ, const float* depth, const uint16_t* labels,
+                                   const float* conf, const svx_pinhole* cams,
+                                   const svx_pose* cam_to_world, int32_t n_images,
+                                   int32_t ptr_is_device, svx_occ_report* reports);
 /* Point query of n voxels (vxyz = n*3). Any output may be NULL; hist is n*K. label =
  * histogram argmax (-1: none). found[i] = 0 for a voxel of an unallocated block. */
 svx_status svx_occ_lookup(svx_occ* occ, const int32_t* vxyz, uint64_t n, float* log_odds,

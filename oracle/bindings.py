@@ -78,6 +78,8 @@ def olib():
         L.svxo_occ_destroy.argtypes = [_P]
         L.svxo_occ_integrate.argtypes = [_P, _P, _P, _P, C.c_uint64, C.c_int32, C.POINTER(PoseC),
                                          C.POINTER(svx.OccReportC)]
+        L.svxo_occ_integrate_depth.argtypes = [_P, _P, _P, _P, C.POINTER(svx.PinholeC), C.POINTER(PoseC),
+                                               C.POINTER(svx.OccReportC)]
         L.svxo_occ_save_mem.argtypes = [_P, _P, C.c_uint64]
         L.svxo_occ_save_mem.restype = C.c_uint64
         L.svxo_last_error.restype = C.c_char_p
@@ -425,6 +427,17 @@ class OracleOcc:
         rep = svx.OccReportC()
         st = olib().svxo_occ_integrate(self.h, _ptr(a), _ptr(lb), _ptr(cf), a.shape[0], a.shape[1],
                                        C.byref(pose), C.byref(rep))
+        if st:
+            raise CheckerError(st, olib().svxo_last_error().decode())
+        return rep
+
+    def integrate_depth(self, depth, cam, pose, labels=None, conf=None):
+        d = np.ascontiguousarray(np.asarray(depth, np.float32))
+        lb = None if labels is None else np.ascontiguousarray(labels, np.uint16)
+        cf = None if conf is None else np.ascontiguousarray(conf, np.float32)
+        rep = svx.OccReportC()
+        st = olib().svxo_occ_integrate_depth(self.h, _ptr(d), _ptr(lb), _ptr(cf), C.byref(cam),
+                                             C.byref(pose), C.byref(rep))
         if st:
             raise CheckerError(st, olib().svxo_last_error().decode())
         return rep

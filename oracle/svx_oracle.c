@@ -1337,6 +1337,34 @@ static int cmp_occptr(const void* a, const void* b) {
 
 /* SOCC1 export (include/svx.h svx_occ_save_mem) */
 #define PUT(x) do { memcpy(p, &(x), sizeof(x)); p += sizeof(x); } while (0)
+/* Pinhole back-projection through the pixel centre (svx.h "pinhole depth images"; the
+ * pixel convention of the reference's label projection, semantic_integrator.cpp:117-121),
+ * FP64 in the contract's order, NaN for a dropped pixel. */
+int svxo_occ_integrate_depth(svxo_occ* m, const float* depth, const uint16_t* labels,
+                             const float* conf, const svx_pinhole* cam, const svx_pose* pose,
+                             svx_occ_report* rep) {
+    const uint64_t n = (uint64_t)cam->width * (uint64_t)cam->height;
+    float* pts = malloc(sizeof(float) * 3 * (n ? n : 1));
+    if (!pts) return 1;
+    for (uint64_t i = 0; i < n; ++i) {
+        const float z = depth[i];
+        float x = NAN, y = NAN, zz = NAN;
+        if (isfinite(z) && z > 0.f && (double)z <= cam->max_depth) {
+            const uint32_t u = (uint32_t)(i % (uint64_t)cam->width), v = (uint32_t)(i / (uint64_t)cam->width);
+            const double zd = (double)z;
+            x = (float)(((double)u + 0.5 - cam->cx) * zd / cam->fx);
+            y = (float)(((double)v + 0.5 - cam->cy) * zd / cam->fy);
+            zz = z;
+        }
+        pts[3 * i] = x;
+        pts[3 * i + 1] = y;
+        pts[3 * i + 2] = zz;
+    }
+    const int st = svxo_occ_integrate(m, pts, labels, conf, n, 3, pose, rep);
+    free(pts);
+    return st;
+}
+
 uint64_t svxo_occ_save_mem(svxo_occ* m, uint8_t* buf, uint64_t cap) {
     const int K = m->cfg.num_labels;
     uint64_t size = 5 + 4 + 4 + 16 + 8;

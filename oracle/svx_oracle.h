@@ -62,6 +62,11 @@ svxo_occ* svxo_occ_create(const svx_occ_cfg* cfg);
 void svxo_occ_destroy(svxo_occ* m);
 int svxo_occ_integrate(svxo_occ* m, const float* pts, const uint16_t* labels, const float* conf,
                        uint64_t n, int32_t stride, const svx_pose* pose, svx_occ_report* rep);
+/* One pinhole depth image (svx.h svx_occ_integrate_depth): back-projection, then
+ * svxo_occ_integrate of the cloud. */
+int svxo_occ_integrate_depth(svxo_occ* m, const float* depth, const uint16_t* labels,
+                             const float* conf, const svx_pinhole* cam, const svx_pose* pose,
+                             svx_occ_report* rep);
 uint64_t svxo_occ_save_mem(svxo_occ* m, uint8_t* buf, uint64_t cap);
 const char* svxo_last_error(void);
 

@@ -145,6 +145,12 @@ class OccCfgC(C.Structure):
                 ("carve", C.c_int32)]
 
 
+class PinholeC(C.Structure):
+    """svx_pinhole: a pinhole depth camera (x right, y down, z forward)."""
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("fx", C.c_double), ("fy", C.c_double),
+                ("cx", C.c_double), ("cy", C.c_double), ("max_depth", C.c_double)]
+
+
 class OccReportC(C.Structure):
     _fields_ = [("frame", C.c_int32), ("points", C.c_uint64), ("rays", C.c_uint64),
                 ("hit_voxels", C.c_uint64), ("miss_voxels", C.c_uint64),
@@ -216,6 +222,8 @@ def _sig(lib: C.CDLL) -> None:
         "svx_occ_get_stream": (S, [P, C.POINTER(P)]),
         "svx_occ_set_shard": (S, [P, C.c_int32, C.c_int32]),
         "svx_occ_reserve": (S, [P, C.c_uint64, C.c_uint64]),
+        "svx_occ_integrate_depth": (S, [P, P, P, P, C.POINTER(PinholeC), C.POINTER(PoseC), C.c_int32,
+                                        C.c_int32, C.POINTER(OccReportC)]),
         "svx_occ_integrate": (S, [P, P, P, P, C.c_uint64, C.c_int32, C.c_int32, C.POINTER(PoseC),
                                   C.POINTER(OccReportC)]),
         "svx_occ_integrate_batch": (S, [P, P, P, P, P, C.c_int32, C.c_int32, P, C.c_int32, P]),
@@ -941,6 +949,33 @@ class OccupancyMap:
         _check(lib().svx_occ_integrate(self._h, _ptr(p), _ptr(lb), _ptr(cf), n, stride, 0,
                                        C.byref(pose), C.byref(rep)))
         return rep
+
+    def integrate_depth(self, depths, cams, poses, labels=None, conf=None) -> list:
+        """Pinhole depth images (host arrays): depths[i] is (height, width) f32 metres,
+        cams[i] a PinholeC, poses[i] camera->world; labels / conf per pixel or None.
+        Each image is one scan (svx.h svx_occ_integrate_depth)."""
+        if len(depths) != len(cams) or len(depths) != len(poses):
+            raise InvalidArgument("depths, cams and poses must have the same length")
+        for d, c in zip(depths, cams):
+            if np.shape(d) != (c.height, c.width):
+                raise InvalidArgument("depth image shape must be (height, width) of its camera")
+        cat = lambda xs, t: None if xs is None else np.ascontiguousarray(  # noqa: E731
+            np.concatenate([np.asarray(x, t).reshape(-1) for x in xs]))
+        d = cat(depths, np.float32) if len(depths) else np.zeros(0, np.float32)
+        lb, cf = cat(labels, np.uint16), cat(conf, np.float32)
+        n = len(depths)
+        ca, pa, reps = (PinholeC * max(n, 1))(*cams), (PoseC * max(n, 1))(*poses), (OccReportC * max(n, 1))()
+        _check(lib().svx_occ_integrate_depth(self._h, _ptr(d), _ptr(lb), _ptr(cf), ca, pa, n, 0, reps))
+        return list(reps)[:n]
+
+    def integrate_depth_device(self, d_depth_ptr: int, cams, poses, d_labels_ptr: int = 0,
+                               d_conf_ptr: int = 0) -> list:
+        """Depth images already in HBM (concatenated, row-major)."""
+        n = len(cams)
+        ca, pa, reps = (PinholeC * max(n, 1))(*cams), (PoseC * max(n, 1))(*poses), (OccReportC * max(n, 1))()
+        _check(lib().svx_occ_integrate_depth(self._h, C.c_void_p(d_depth_ptr), C.c_void_p(d_labels_ptr or None),
+                                             C.c_void_p(d_conf_ptr or None), ca, pa, n, 1, reps))
+        return list(reps)[:n]
 
     def integrate_batch_device(self, d_points_ptr: int, offsets: np.ndarray, stride: int, poses,
                                d_labels_ptr: int = 0, d_conf_ptr: int = 0) -> list:

@@ -307,6 +307,27 @@ __global__ void __launch_bounds__(256) k_occ_visit(OccParams p, OccDev d) {
     tb.flush(tag_base);
 }
 
+// Pinhole depth image -> camera-frame points (svx.h "pinhole depth images"): thread per
+// pixel, NaN for a dropped pixel (the scan then drops it like any non-finite point).
+__global__ void __launch_bounds__(256) k_depth_points(const float* __restrict__ depth, int32_t w,
+                                                      uint64_t n, svx_pinhole cam,
+                                                      float* __restrict__ out) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float z = depth[i];
+    float x = CUDART_NAN_F, y = CUDART_NAN_F, zz = CUDART_NAN_F;
+    if (isfinite(z) && z > 0.f && double(z) <= cam.max_depth) {
+        const uint32_t u = uint32_t(i % uint64_t(w)), v = uint32_t(i / uint64_t(w));
+        const double zd = double(z);
+        x = float((double(u) + 0.5 - cam.cx) * zd / cam.fx);
+        y = float((double(v) + 0.5 - cam.cy) * zd / cam.fy);
+        zz = z;
+    }
+    out[3 * i] = x;
+    out[3 * i + 1] = y;
+    out[3 * i + 2] = zz;
+}
+
 // Labelled hits -> class histograms, once the scan is accepted (the adds cannot be
 // undone, so they wait for the capacity check) and every claimed layer is mapped.
 __global__ void __launch_bounds__(256) k_occ_hist(OccParams p, OccDev d) {
@@ -494,6 +515,7 @@ struct svx_occ {
     svx::DevBuf<float> pts;
     svx::DevBuf<uint16_t> lbl;
     svx::DevBuf<float> conf;
+    svx::DevBuf<float> dep;  // staged depth images
 };
 
 namespace svx {
@@ -517,6 +539,7 @@ void free_occ(svx_occ* m) {
     m->pts.release();
     m->lbl.release();
     m->conf.release();
+    m->dep.release();
     if (m->stream) cudaStreamDestroy(m->stream);
     delete m;
 }
@@ -796,6 +819,54 @@ svx_status svx_occ_integrate_batch(svx_occ* m, const float* points, const uint16
         SVX_CUDA(cudaMemcpyAsync(hm.data(), m->rep.p, 4 * hm.size(), cudaMemcpyDeviceToHost, m->stream));
         SVX_CUDA(cudaStreamSynchronize(m->stream));
         for (int f = 0; reps && f < n_frames; ++f) {
+            reps[f].hit_voxels = hm[2 * f];
+            reps[f].miss_voxels = hm[2 * f + 1];
+        }
+    });
+}
+
+svx_status svx_occ_integrate_depth(svx_occ* m, const float* depth, const uint16_t* labels,
+                                   const float* conf, const svx_pinhole* cams,
+                                   const svx_pose* poses, int32_t n_images, int32_t on_device,
+                                   svx_occ_report* reps) {
+    return api_guard([&] {
+        require(m && cams && poses && n_images >= 0, SVX_INVALID_ARGUMENT, "null argument");
+        DevGuard g(m->device);
+        uint64_t a = 0;
+        for (int f = 0; f < n_images; ++f) {
+            const svx_pinhole& c = cams[f];
+            require(c.width > 0 && c.height > 0, SVX_INVALID_ARGUMENT, "image size must be positive");
+            require(std::isfinite(c.fx) && std::isfinite(c.fy) && c.fx != 0.0 && c.fy != 0.0 &&
+                        std::isfinite(c.cx) && std::isfinite(c.cy),
+                    SVX_INVALID_ARGUMENT, "bad intrinsics");
+            require(c.max_depth > 0.0, SVX_INVALID_ARGUMENT, "max_depth must be positive");
+            validate_pose(poses[f]);
+            a += uint64_t(c.width) * uint64_t(c.height);
+        }
+        require(a == 0 || depth, SVX_INVALID_ARGUMENT, "null depth");
+        m->rep.alloc(2ull * std::max(n_images, 1));
+        SVX_CUDA(cudaMemsetAsync(m->rep.p, 0, 8ull * std::max(n_images, 1), m->stream));
+        a = 0;
+        for (int f = 0; f < n_images; ++f) {
+            const uint64_t n = uint64_t(cams[f].width) * uint64_t(cams[f].height);
+            const float* dd = depth + a;
+            const uint16_t* dl = labels ? labels + a : nullptr;
+            const float* dc = conf ? conf + a : nullptr;
+            if (!on_device) {
+                dd = stage(m, m->dep, dd, n);
+                dl = stage(m, m->lbl, dl, n);
+                dc = stage(m, m->conf, dc, n);
+            }
+            m->pts.alloc(3 * n);
+            k_depth_points<<<grid256(n), 256, 0, m->stream>>>(dd, cams[f].width, n, cams[f], m->pts.p);
+            count_launch();
+            occ_scan(m, m->pts.p, dl, dc, n, 3, poses[f], m->rep.p + 2 * f, reps ? reps + f : nullptr);
+            a += n;
+        }
+        std::vector<uint32_t> hm(2ull * std::max(n_images, 1));
+        SVX_CUDA(cudaMemcpyAsync(hm.data(), m->rep.p, 4 * hm.size(), cudaMemcpyDeviceToHost, m->stream));
+        SVX_CUDA(cudaStreamSynchronize(m->stream));
+        for (int f = 0; reps && f < n_images; ++f) {
             reps[f].hit_voxels = hm[2 * f];
             reps[f].miss_voxels = hm[2 * f + 1];
         }

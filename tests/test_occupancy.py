@@ -237,3 +237,132 @@ def test_gpu_occupancy_capacity_rejects_scan():
     assert gpu.save_bytes() == before
     gpu.integrate(np.array([[0.5, 0, 0]], np.float32), svx.pose_c())  # still usable
     gpu.close()
+
+
+# ----------------------------------------------------------- pinhole depth images
+# svx.h svx_occ_integrate_depth (BASELINE.json configs[2]; no reference: unpinned).
+
+def pinhole(w, h, f, max_depth=30.0):
+    return svx.PinholeC(w, h, f, f, w / 2.0, h / 2.0, max_depth)
+
+
+def back_project_np(depth, cam):
+    """Independent numpy restatement of the contract's back-projection (FP64, its order)."""
+    h, w = depth.shape
+    v, u = np.meshgrid(np.arange(h, dtype=np.float64), np.arange(w, dtype=np.float64), indexing="ij")
+    z = depth.astype(np.float64)
+    keep = np.isfinite(depth) & (depth > 0) & (z <= cam.max_depth)
+    with np.errstate(invalid="ignore"):
+        x = ((u + 0.5 - cam.cx) * z / cam.fx).astype(np.float32)
+        y = ((v + 0.5 - cam.cy) * z / cam.fy).astype(np.float32)
+    pts = np.stack([x, y, depth.astype(np.float32)], -1).reshape(-1, 3)
+    pts[~keep.reshape(-1)] = np.nan
+    return pts
+
+
+def depth_scene(n_img, w, h, seed=0):
+    """Cameras on a short track looking along +x at a wall and a ground plane (z up in the
+    world; camera z forward, y down), with noise, holes and far pixels."""
+    rng = np.random.default_rng(seed)
+    cam = pinhole(w, h, 0.8 * w, max_depth=12.0)
+    # camera -> world rotation: camera z -> world +x, camera x -> world -y, camera y -> world -z
+    R = np.array([[0, 0, 1], [-1, 0, 0], [0, -1, 0]], np.float64)
+    imgs, poses = [], []
+    for i in range(n_img):
+        t = np.array([0.37 * i, 0.05 * i, 1.6])
+        yaw = 0.2 * (i % 3 - 1)
+        Rz = np.array([[np.cos(yaw), -np.sin(yaw), 0], [np.sin(yaw), np.cos(yaw), 0], [0, 0, 1]])
+        Rw = Rz @ R
+        v, u = np.meshgrid(np.arange(h) + 0.5, np.arange(w) + 0.5, indexing="ij")
+        dcam = np.stack([(u - cam.cx) / cam.fx, (v - cam.cy) / cam.fy, np.ones_like(u)], -1)
+        dw = dcam @ Rw.T
+        t_wall = (9.0 - t[0]) / np.where(dw[..., 0] > 1e-9, dw[..., 0], np.nan)
+        t_gnd = -t[2] / np.where(dw[..., 2] < -1e-9, dw[..., 2], np.nan)
+        tt = np.fmin(np.where(t_wall > 0, t_wall, np.inf), np.where(t_gnd > 0, t_gnd, np.inf))
+        z = (tt * 1.0).astype(np.float32)  # camera-frame z = ray parameter (dcam.z = 1)
+        z += rng.normal(0, 0.01, z.shape).astype(np.float32)
+        z[rng.random(z.shape) < 0.05] = 0.0       # holes
+        z[rng.random(z.shape) < 0.01] = np.nan    # invalid
+        z[~np.isfinite(tt)] = 0.0
+        imgs.append(z.astype(np.float32))
+        poses.append(svx.pose_c(Rw, t))
+    labels = [rng.integers(0, 4, (h, w)).astype(np.uint16) for _ in range(n_img)]
+    conf = [rng.uniform(0.2, 1.0, (h, w)).astype(np.float32) for _ in range(n_img)]
+    return cam, imgs, poses, labels, conf
+
+
+@needs_oracle
+def test_depth_single_pixel_known_answer():
+    """1x1 image, principal point at the pixel centre: depth 2 m -> point (0, 0, 2): one
+    HIT at voxel (0, 0, 20), MISS for the 20 cells from the camera to it."""
+    o = ob.OracleOcc(occ_cfg())
+    cam = svx.PinholeC(1, 1, 100.0, 100.0, 0.5, 0.5, 30.0)
+    r = o.integrate_depth(np.array([[2.0]], np.float32), cam, svx.pose_c())
+    assert (r.points, r.rays, r.hit_voxels, r.miss_voxels) == (1, 1, 1, 20)
+    p = ob.parse_socc1(o.save_bytes())
+    assert voxel(p, (0, 0, 20))[:3] == (np.float32(0.85), 1, 0)
+    assert voxel(p, (0, 0, 7))[:3] == (np.float32(-0.4), 0, 1)
+
+
+@needs_oracle
+def test_depth_dropped_pixels():
+    """0, negative, NaN, inf and beyond-max_depth pixels are not rays."""
+    o = ob.OracleOcc(occ_cfg())
+    cam = svx.PinholeC(6, 1, 10.0, 10.0, 3.0, 0.5, 5.0)
+    d = np.array([[0.0, -1.0, np.nan, np.inf, 5.5, 5.0]], np.float32)
+    r = o.integrate_depth(d, cam, svx.pose_c())
+    assert (r.points, r.rays, r.hit_voxels) == (6, 1, 1)
+
+
+@needs_oracle
+def test_depth_equals_point_cloud_path():
+    """The oracle's depth path == its point path on an independently back-projected
+    cloud (numpy restatement of the contract's arithmetic)."""
+    cam, imgs, poses, labels, conf = depth_scene(3, 40, 30)
+    a, b = ob.OracleOcc(occ_cfg(max_blocks=1 << 14)), ob.OracleOcc(occ_cfg(max_blocks=1 << 14))
+    for d, p, lb, cf in zip(imgs, poses, labels, conf):
+        ra = a.integrate_depth(d, cam, p, lb, cf)
+        rb = b.integrate(back_project_np(d, cam), p, lb.reshape(-1), cf.reshape(-1))
+        assert (ra.rays, ra.hit_voxels, ra.miss_voxels) == (rb.rays, rb.hit_voxels, rb.miss_voxels)
+        assert ra.rays > 0.8 * d.size
+    assert a.save_bytes() == b.save_bytes()
+
+
+def test_depth_api_rejects_bad_arguments():
+    m = svx.OccupancyMap.__new__(svx.OccupancyMap)  # argument checks happen before any GPU call
+    cam = pinhole(4, 3, 3.0)
+    with pytest.raises(svx.InvalidArgument):
+        svx.OccupancyMap.integrate_depth(m, [np.zeros((4, 4), np.float32)], [cam], [svx.pose_c()])
+    with pytest.raises(svx.InvalidArgument):
+        svx.OccupancyMap.integrate_depth(m, [np.zeros((3, 4), np.float32)], [cam], [])
+
+
+@pytest.mark.gpu
+@needs_oracle
+def test_gpu_depth_images_equal_oracle():
+    """Two 'frames' of 3 labelled depth cameras: GPU SOCC1 == oracle SOCC1, host and
+    device-pointer entry points agree."""
+    import torch
+    cam, imgs, poses, labels, conf = depth_scene(6, 96, 64, seed=3)
+    cfg = occ_cfg(max_blocks=1 << 15)
+    o = ob.OracleOcc(cfg)
+    g = svx.OccupancyMap(cfg, 0)
+    g2 = svx.OccupancyMap(cfg, 0)
+    for f in (0, 3):
+        sl = slice(f, f + 3)
+        rg = g.integrate_depth(imgs[sl], [cam] * 3, poses[sl], labels[sl], conf[sl])
+        dd = torch.from_numpy(np.concatenate([x.reshape(-1) for x in imgs[sl]])).cuda()
+        dl = torch.from_numpy(np.concatenate([x.reshape(-1) for x in labels[sl]]).view(np.int16)).cuda()
+        dc = torch.from_numpy(np.concatenate([x.reshape(-1) for x in conf[sl]])).cuda()
+        torch.cuda.synchronize()
+        r2 = g2.integrate_depth_device(dd.data_ptr(), [cam] * 3, poses[sl], dl.data_ptr(), dc.data_ptr())
+        for j in range(3):
+            ro = o.integrate_depth(imgs[f + j], cam, poses[f + j], labels[f + j], conf[f + j])
+            assert (rg[j].rays, rg[j].hit_voxels, rg[j].miss_voxels, rg[j].new_blocks) == \
+                (ro.rays, ro.hit_voxels, ro.miss_voxels, ro.new_blocks)
+            assert (r2[j].hit_voxels, r2[j].miss_voxels) == (ro.hit_voxels, ro.miss_voxels)
+    ref = o.save_bytes()
+    assert g.save_bytes() == ref
+    assert g2.save_bytes() == ref
+    g.close()
+    g2.close()
