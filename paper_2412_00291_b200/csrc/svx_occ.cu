@@ -32,6 +32,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "svx_map.hpp"
 
 namespace svx {
@@ -60,6 +62,7 @@ struct OccParams {
     uint32_t mapped_blocks;  // pool blocks mapped and zeroed
     uint32_t prev_blocks;    // redo launch: blocks the first launch already tagged
     int redo;
+    const uint32_t* order;   // visit order of the points (longest rays first), or null
 };
 
 // Hash slot: key and pool index side by side, so one 16-byte load resolves a probe.
@@ -195,6 +198,9 @@ constexpr int kTagBatch = 8;
 // Only the first kNearVoxels cells of a ray (next to the sensor, where every ray of the
 // scan passes) go through the load-then-RED batch; beyond them few rays share a voxel
 // and the RED.MAX is issued directly (no load, nothing to wait for).
+#ifndef SVX_OCC_SORT
+#define SVX_OCC_SORT 1
+#endif
 #ifndef SVX_OCC_NEAR
 #define SVX_OCC_NEAR 32
 #endif
@@ -244,8 +250,9 @@ __global__ void __launch_bounds__(256) k_occ_visit(OccParams p, OccDev d) {
         cidx[j] = kInvalid;
     }
     __syncthreads();
-    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= p.n) return;
+    const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (tid >= p.n) return;
+    const uint64_t i = p.order ? p.order[tid] : tid;
     d3 o, end;
     bool hit;
     if (!point_ray(p, i, o, end, hit)) return;
@@ -326,6 +333,32 @@ __global__ void __launch_bounds__(256) k_depth_points(const float* __restrict__ 
     out[3 * i] = x;
     out[3 * i + 1] = y;
     out[3 * i + 2] = zz;
+}
+
+// Visit order: the ray's cell count estimate (L1 voxel distance origin -> end, the DDA
+// visits about that many cells) as a descending sort key, so that the 32 rays of a warp
+// have similar lengths (lanes do not idle behind one long ray) and the longest rays start
+// first (the grid's tail is short rays). Dropped points sort last. Only the schedule
+// changes: the result does not depend on which thread handles which ray.
+__global__ void __launch_bounds__(256) k_occ_ray_keys(OccParams p, uint32_t* __restrict__ key,
+                                                      uint32_t* __restrict__ idx) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= p.n) return;
+    d3 o, end;
+    bool hit;
+    uint32_t len = 0;
+    if (point_ray(p, i, o, end, hit)) {
+        int32_t a[3], b[3];
+        world_to_voxel(o, p.inv_nu, a);
+        world_to_voxel(end, p.inv_nu, b);
+        const uint32_t l = p.carve ? uint32_t(abs(b[0] - a[0])) + uint32_t(abs(b[1] - a[1])) +
+                                         uint32_t(abs(b[2] - a[2])) + 1u
+                                   : 1u;
+        len = l > 0xFFFEu ? 0xFFFEu : l;
+        len += 1;
+    }
+    key[i] = 0xFFFFu - len;
+    idx[i] = uint32_t(i);
 }
 
 // Labelled hits -> class histograms, once the scan is accepted (the adds cannot be
@@ -516,6 +549,8 @@ struct svx_occ {
     svx::DevBuf<uint16_t> lbl;
     svx::DevBuf<float> conf;
     svx::DevBuf<float> dep;  // staged depth images
+    svx::DevBuf<uint32_t> ray_key, ray_idx;  // visit order (sort keys / point indices, x2)
+    svx::DevBuf<uint8_t> sort_tmp;
 };
 
 namespace svx {
@@ -540,6 +575,9 @@ void free_occ(svx_occ* m) {
     m->lbl.release();
     m->conf.release();
     m->dep.release();
+    m->ray_key.release();
+    m->ray_idx.release();
+    m->sort_tmp.release();
     if (m->stream) cudaStreamDestroy(m->stream);
     delete m;
 }
@@ -613,6 +651,21 @@ void occ_scan(svx_occ* m, const float* d_pts, const uint16_t* d_lbl, const float
     OccDev d = occ_dev(m);
     d.rep = rep_slot;
     if (n) {
+#if SVX_OCC_SORT
+        if (n >= 4096 && n < (1ull << 32)) {
+            m->ray_key.alloc(2 * n);
+            m->ray_idx.alloc(2 * n);
+            k_occ_ray_keys<<<grid256(n), 256, 0, st>>>(p, m->ray_key.p, m->ray_idx.p);
+            size_t bytes = 0;
+            SVX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, m->ray_key.p, m->ray_key.p + n,
+                                                     m->ray_idx.p, m->ray_idx.p + n, int(n), 0, 16, st));
+            m->sort_tmp.alloc(bytes);
+            SVX_CUDA(cub::DeviceRadixSort::SortPairs(m->sort_tmp.p, bytes, m->ray_key.p, m->ray_key.p + n,
+                                                     m->ray_idx.p, m->ray_idx.p + n, int(n), 0, 16, st));
+            p.order = m->ray_idx.p + n;
+            count_launch(2);
+        }
+#endif
         k_occ_visit<<<grid256(n), 256, 0, st>>>(p, d);
         count_launch();
     }
