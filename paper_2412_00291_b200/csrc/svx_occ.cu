@@ -241,8 +241,12 @@ struct TagBatch {
 // touched, so a hit needs neither the global probe nor the mark; a reader that sees
 // the key before the index falls back to the global path.
 constexpr int kBlockCache = 2048;
+#ifndef SVX_OCC_VB
+#define SVX_OCC_VB 256
+#endif
+constexpr int kVisitThreads = SVX_OCC_VB;  // rays per CTA
 
-__global__ void __launch_bounds__(256) k_occ_visit(OccParams p, OccDev d) {
+__global__ void __launch_bounds__(kVisitThreads) k_occ_visit(OccParams p, OccDev d) {
     __shared__ unsigned long long ckey[kBlockCache];
     __shared__ uint32_t cidx[kBlockCache];
     for (int j = threadIdx.x; j < kBlockCache; j += blockDim.x) {
@@ -666,7 +670,7 @@ void occ_scan(svx_occ* m, const float* d_pts, const uint16_t* d_lbl, const float
             count_launch(2);
         }
 #endif
-        k_occ_visit<<<grid256(n), 256, 0, st>>>(p, d);
+        k_occ_visit<<<unsigned((n + kVisitThreads - 1) / kVisitThreads), kVisitThreads, 0, st>>>(p, d);
         count_launch();
     }
     SVX_CUDA(cudaMemcpyAsync(m->h_ctr, m->d_ctr, 4 * O_COUNT, cudaMemcpyDeviceToHost, st));
@@ -701,7 +705,7 @@ void occ_scan(svx_occ* m, const float* d_pts, const uint16_t* d_lbl, const float
         p.redo = 1;
         p.prev_blocks = p.mapped_blocks;
         p.mapped_blocks = uint32_t(m->mapped_blocks);
-        k_occ_visit<<<grid256(n), 256, 0, st>>>(p, d);
+        k_occ_visit<<<unsigned((n + kVisitThreads - 1) / kVisitThreads), kVisitThreads, 0, st>>>(p, d);
         count_launch();
         // it may claim histogram layers for the blocks it completes
         SVX_CUDA(cudaMemcpyAsync(&m->h_ctr[O_LAYERS], &m->d_ctr[O_LAYERS], 4, cudaMemcpyDeviceToHost, st));
