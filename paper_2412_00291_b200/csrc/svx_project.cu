@@ -40,19 +40,26 @@ k_project_points(const T* __restrict__ pts, uint64_t n, int stride, Model m,
                  unsigned long long* __restrict__ pixkey, uint8_t* __restrict__ tie,
                  unsigned long long* __restrict__ ties, uint32_t tie_cap,
                  uint32_t* __restrict__ ctr) {
+    // The point loads and the pixel computation read only this frame's input (never
+    // written by the frame kernels before it), so they run before the dependency wait
+    // and overlap the previous frame's last kernels; every write comes after it.
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    double x = 0.0, y = 0.0, z = 0.0, r = 0.0;
+    uint32_t pix = kInvalid;
+    if (i < n) {
+        x = pts[i * stride];
+        y = pts[i * stride + 1];
+        z = pts[i * stride + 2];
+        r = sqrt(dot3(mk(x, y, z), mk(x, y, z)));
+        if (isfinite(r) && !(r < m.min_range)) {
+            pix = pixel_fast(float(x), float(y), float(z), m, m.r2_lo, m.r2_hi);
+            if (pix == kNeedFp64) pix = pixel_fp64(mk(x, y, z), m);
+        }
+    }
     pdl_wait();
     pdl_trigger();
     if (ctr[C_ABORT]) return;
-    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const double x = pts[i * stride], y = pts[i * stride + 1], z = pts[i * stride + 2];
-    const d3 p = mk(x, y, z);
-    const double r = sqrt(dot3(p, p));
-    uint32_t pix = kInvalid;
-    if (isfinite(r) && !(r < m.min_range)) {
-        pix = pixel_fast(float(x), float(y), float(z), m, m.r2_lo, m.r2_hi);
-        if (pix == kNeedFp64) pix = pixel_fp64(p, m);
-    }
     if (pix == kInvalid) {
         warp_agg_inc(&ctr[C_DROPPED]);
         return;

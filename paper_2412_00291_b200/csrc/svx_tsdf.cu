@@ -950,8 +950,10 @@ __global__ void k_fb_fold_sorted(HashView h, svx_tsdf_voxel* __restrict__ pool, 
 }
 
 __global__ void k_frame_end(FrameOut* __restrict__ out, uint32_t* __restrict__ ctr) {
-    pdl_wait();
+    // trigger first: the next frame's projection may launch (its pre-wait part reads
+    // only its own points) while this frame's last kernel drains
     pdl_trigger();
+    pdl_wait();
     if (ctr[C_ABORT]) return;
     write_frame_end(out, ctr);
 }
