@@ -366,3 +366,26 @@ def test_gpu_depth_images_equal_oracle():
     assert g2.save_bytes() == ref
     g.close()
     g2.close()
+
+
+# ------------------------------------------------------- C++ host API (drop-in)
+DROPIN_TEST = svx.LIB_PATH.replace("libsvx_b200.so", "test_occupancy_dropin")
+
+
+def test_cpp_occupancy_api_is_built():
+    """semvox/occupancy_map.hpp is compiled into libsemvox_b200.so and its check
+    program is built in-tree (make -C paper_2412_00291_b200/csrc)."""
+    import os
+    assert os.access(DROPIN_TEST, os.X_OK), DROPIN_TEST
+    import ctypes
+    lib = ctypes.CDLL(svx.LIB_PATH.replace("libsvx_b200.so", "libsemvox_b200.so"))
+    assert hasattr(lib, "_ZN6semvox12OccupancyMap15integrate_depthERKSt6vectorINS_10DepthImageESaIS2_EE")
+
+
+@pytest.mark.gpu
+def test_gpu_cpp_occupancy_api():
+    """The C++ OccupancyMap reproduces the contract's known answers on the device."""
+    import subprocess
+    r = subprocess.run([DROPIN_TEST], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "all checks passed" in r.stdout
