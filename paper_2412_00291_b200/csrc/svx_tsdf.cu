@@ -438,7 +438,10 @@ __device__ void visit_global(const FrameParams& f, HashView h, uint64_t* __restr
 // voxel masks (smem atomics). Global work is then one hash find-or-insert per
 // distinct block (in parallel across threads) and one RED.OR per non-empty mask
 // word, instead of serialized global round trips per ray.
-constexpr int kTileU = 32, kTileV = 8;
+#ifndef SVX_TILE_U
+#define SVX_TILE_U 32
+#endif
+constexpr int kTileU = SVX_TILE_U, kTileV = 256 / SVX_TILE_U;
 constexpr int kLocalKeys = 256;
 constexpr int kTileFb = 1024;  // staged fallback visits per tile
 
@@ -1086,7 +1089,7 @@ void launch_stages(svx_map* m, svx_scan* s, const FrameParams& f, int from, Fram
             count_launch();
             s->rowdist_fresh = true;
         }
-        const unsigned tiles = unsigned(((s->dm.W + 31) / 32) * ((s->dm.H + 7) / 8));
+        const unsigned tiles = unsigned(((s->dm.W + kTileU - 1) / kTileU) * ((s->dm.H + kTileV - 1) / kTileV));
         launch_pdl(k_raycast_band, tiles, 256, m->stream, f, s->depth.p, s->normals.p, s->valid.p,
                    s->dirs.p, s->rowdist.p, s->validbits.p, reinterpret_cast<PixCache*>(s->pixcache.p), hv,
                    m->block_keys,
