@@ -443,7 +443,10 @@ __device__ void visit_global(const FrameParams& f, HashView h, uint64_t* __restr
 #endif
 constexpr int kTileU = SVX_TILE_U, kTileV = 256 / SVX_TILE_U;
 constexpr int kLocalKeys = 256;
-constexpr int kTileFb = 1024;  // staged fallback visits per tile
+#ifndef SVX_TILE_FB
+#define SVX_TILE_FB 1024
+#endif
+constexpr int kTileFb = SVX_TILE_FB;  // staged fallback visits per tile
 
 __global__ void __launch_bounds__(kTileU * kTileV, 4)
 k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __restrict__ normals,
