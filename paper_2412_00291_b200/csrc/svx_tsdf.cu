@@ -586,6 +586,9 @@ k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __re
                 fb = own == kInvalid || !pixel_has_return(validbits, own);
             }
             if (cur_li < 0) {  // local table full: straight to global state
+#ifdef SVX_DIAG_NOGLOBAL
+                return;  // diagnostic build only: drop table-overflow visits
+#endif
                 visit_global(f, h, block_keys, stamp, touched, vmask, fbcnt, rec, pool, cache, dirty,
                              vlist, blocks_before, ctr, key, lin, fb, p);
                 return;
