@@ -10,6 +10,7 @@
 #include <cstring>
 #include <fstream>
 #include <numeric>
+#include <unordered_map>
 #include <string>
 #include <thread>
 #include <vector>
@@ -270,25 +271,41 @@ svx_map* load_svox1(const std::vector<uint8_t>& buf, int device, uint32_t max_bl
         std::vector<svx_tsdf_voxel> tsdf;
         std::vector<float> sem;
         uint32_t layers = 0;
+        // a repeated block coordinate is the SAME block (get_or_allocate_block,
+        // voxel_store.cpp:145): its TSDF is overwritten by the later record, its
+        // semantic layer by a later record that has one and kept otherwise; the
+        // capacity check counts distinct blocks only
+        std::unordered_map<uint64_t, uint32_t> seen;
+        seen.reserve(size_t(std::min<uint64_t>(nb, cfg.max_blocks)) * 2);
         for (uint64_t i = 0; i < nb; ++i) {
             int32_t b[3];
             get(b, 12);
-            if (keys.size() >= cfg.max_blocks)
-                throw Error(SVX_CAPACITY, "block budget exhausted (max_blocks = " +
-                                              std::to_string(cfg.max_blocks) + ")");
-            keys.push_back(key_of(b));
-            tsdf.resize(tsdf.size() + kBlockVoxels);
-            get(&tsdf[tsdf.size() - kBlockVoxels], m->block_bytes);
+            const uint64_t key = key_of(b);
+            auto it = seen.find(key);
+            uint32_t at;
+            if (it == seen.end()) {
+                if (keys.size() >= cfg.max_blocks)
+                    throw Error(SVX_CAPACITY, "block budget exhausted (max_blocks = " +
+                                                  std::to_string(cfg.max_blocks) + ")");
+                at = uint32_t(keys.size());
+                seen.emplace(key, at);
+                keys.push_back(key);
+                tsdf.resize(tsdf.size() + kBlockVoxels);
+                sid.push_back(kInvalid);
+            } else {
+                at = it->second;
+            }
+            get(&tsdf[uint64_t(at) * kBlockVoxels], m->block_bytes);
             uint8_t hs = 0;
             get(&hs, 1);
             if (hs) {
-                sem.resize(sem.size() + size_t(kBlockVoxels) * K);
+                if (sid[at] == kInvalid) {
+                    sem.resize(sem.size() + size_t(kBlockVoxels) * K);
+                    sid[at] = layers++;
+                }
                 if (off + m->layer_bytes > buf.size())
                     throw Error(SVX_DATA, "truncated semantic section: " + origin);
-                get(&sem[sem.size() - size_t(kBlockVoxels) * K], m->layer_bytes);
-                sid.push_back(layers++);
-            } else {
-                sid.push_back(kInvalid);
+                get(&sem[uint64_t(sid[at]) * kBlockVoxels * K], m->layer_bytes);
             }
         }
         const uint64_t n = keys.size();

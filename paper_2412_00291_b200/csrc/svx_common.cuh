@@ -138,7 +138,12 @@ __device__ inline uint32_t pixel_fast(float px, float py, float pz, const Model&
     const float r2 = px * px + py * py + pz * pz;
     if (r2 < r2_lo) return kInvalid;  // range < min_range for sure
     if (!(r2 > r2_hi)) return kNeedFp64;
-    const float rxy = sqrtf(px * px + py * py);
+    // The azimuth error of an input with absolute error ~3e-7 |p| is ~3e-7 |p| / rxy:
+    // the fixed margin_u budget only covers rxy >= 0.05 |p| (polar angle >= ~2.9 deg
+    // from either pole); closer to the pole the FP64 reference formula decides.
+    const float rxy2 = px * px + py * py;
+    if (!(rxy2 >= 0.0025f * r2)) return kNeedFp64;
+    const float rxy = sqrtf(rxy2);
     const float uf = (3.14159274f - fast_atan2f(py, px)) * m.inv_dphi_f;
     const float vf = (fast_atan2f(rxy, pz) - m.theta0_f) * m.inv_dtheta_f;
     const float fu = uf - floorf(uf), fv = vf - floorf(vf);
@@ -334,6 +339,7 @@ enum Counter : int {
     C_DONE = 24,        // CTAs of k_fb_fold finished (last one writes the report)
     C_TOUCHED_PREV = 25,  // blocks touched by the previous frame (their mask words get cleared)
     C_ABORT_FRAME = 26, // frame serial that raised a pool / big-bucket abort (set before the bit)
+    C_CONF_MAYBE = 27,  // the current label image may read a confidence outside [0, 1]
     kNumCounters = 32
 };
 

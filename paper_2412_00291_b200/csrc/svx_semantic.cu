@@ -250,11 +250,17 @@ k_sem_update(SemParams sp, HashView h, const uint64_t* __restrict__ block_keys,
              uint32_t* __restrict__ sem_idx, const uint32_t* __restrict__ cand,
              const uint16_t* __restrict__ labels, const float* __restrict__ conf,
              const float* __restrict__ tensor, uint8_t* __restrict__ dirty_sem,
-             uint32_t* __restrict__ ctr) {
+             int check, uint32_t* __restrict__ ctr) {
     const int lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    if (ctr[C_ERR_CONF]) return;  // invalid confidence: no voxel is touched
+    // an image that throws (a voxel passing every test reads a confidence outside
+    // [0, 1], label_to_likelihood, semantic_integrator.cpp:24-27,140-142) updates
+    // nothing, and no later image of the batch runs
+    if (ctr[C_ERR_CONF]) return;
+    // check pass: runs only when the image holds such a confidence (or the default is
+    // one); evaluates the reference's test sequence and flags, writes nothing else
+    if (check && !ctr[C_CONF_MAYBE]) return;
     const uint32_t n_cand = ctr[C_CAND];
     const int K = KC > 0 ? KC : sp.K;
     uint32_t n_upd = 0;
@@ -287,6 +293,17 @@ k_sem_update(SemParams sp, HashView h, const uint64_t* __restrict__ block_keys,
             pass |= 1u << j;
         }
         if (!__any_sync(0xFFFFFFFFu, pass != 0)) continue;
+        if (check) {
+            if (!sp.has_tensor) {
+#pragma unroll
+                for (int j = 0; j < kPer; ++j) {
+                    if (!((pass >> j) & 1u)) continue;
+                    const float cf = sp.has_conf ? conf[pix[j]] : sp.default_conf;
+                    if (cf < 0.f || cf > 1.f) atomicOr(&ctr[C_ERR_CONF], 1u);
+                }
+            }
+            continue;
+        }
         // the block's semantic layer (ensure_semantics): the first part to need it
         // claims it, fills it with 1/K and publishes its index; other parts wait
         uint32_t sid = __ldcg(&sem_idx[idx]);
@@ -349,11 +366,14 @@ k_sem_update(SemParams sp, HashView h, const uint64_t* __restrict__ block_keys,
     if (lane == 0 && n_upd) atomicAdd(&ctr[C_SEM_UPDATED], n_upd);
 }
 
+// Flags an image whose confidence image holds a value outside [0, 1] (NaN passes,
+// as in the reference's comparison); the check pass of k_sem_update then decides
+// whether a voxel actually reads one.
 __global__ void k_check_conf(const float* __restrict__ conf, uint64_t n, uint32_t* __restrict__ ctr) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const float c = conf[i];
-    if (c < 0.f || c > 1.f) atomicAdd(&ctr[C_ERR_CONF], 1u);
+    if (c < 0.f || c > 1.f) ctr[C_CONF_MAYBE] = 1u;
 }
 
 }  // namespace
@@ -371,10 +391,8 @@ void run_integrate_labels_batch(svx_map* m, const svx_label_image* imgs, int n, 
         reps[i].updated_voxels = reps[i].new_blocks = 0;
         if (imgs[i].width <= 0 || imgs[i].height <= 0 || !imgs[i].labels)
             throw Error(SVX_INVALID_ARGUMENT, "label image is empty");
-        if (!imgs[i].prob_tensor && !imgs[i].confidence &&
-            (cfg.default_confidence < 0.f || cfg.default_confidence > 1.f))
-            throw Error(SVX_INVALID_ARGUMENT, "confidence must be in [0, 1]");
     }
+    const bool bad_default = cfg.default_confidence < 0.f || cfg.default_confidence > 1.f;
     if (n <= 0) return;
     // staging for host images: every image of the batch gets its own slice
     uint64_t lbl_n = 0, conf_n = 0, ten_n = 0;
@@ -390,7 +408,7 @@ void run_integrate_labels_batch(svx_map* m, const svx_label_image* imgs, int n, 
         if (ten_n) m->tensor.alloc(ten_n);
     }
     m->cand.alloc(std::max<uint64_t>(m->n_blocks, 1));
-    m->sem_out.alloc(2ull * n);
+    m->sem_out.alloc(3ull * n);
     // a block owns at most one layer: map as many layers as there are blocks, so the
     // update kernel never outgrows the pool and no mid-pass synchronisation is needed
     ensure_layers(m, m->n_blocks);
@@ -441,9 +459,16 @@ void run_integrate_labels_batch(svx_map* m, const svx_label_image* imgs, int n, 
                 to += P * K;
             }
         }
-        if (conf && !ten) {
-            k_check_conf<<<grid_for(P), kThreads, 0, m->stream>>>(conf, P, m->d_ctr);
-            count_launch();
+        // confidence validity: only a voxel that passes every test reads one
+        const bool conf_check = !ten && (conf || bad_default);
+        if (conf_check) {
+            if (conf) {
+                SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_CONF_MAYBE, 0, 4, m->stream));
+                k_check_conf<<<grid_for(P), kThreads, 0, m->stream>>>(conf, P, m->d_ctr);
+                count_launch();
+            } else {
+                SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_CONF_MAYBE, 0x01, 1, m->stream));
+            }
         }
         SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_CAND, 0, 4, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_SEM_UPDATED, 0, 4, m->stream));
@@ -472,34 +497,48 @@ void run_integrate_labels_batch(svx_map* m, const svx_label_image* imgs, int n, 
                 int per_sm = 0;
                 SVX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0));
                 const unsigned grid = std::max(1u, unsigned(per_sm)) * (persistent_grid(m->device) / 8);
-                kern<<<grid, kThreads, 0, m->stream>>>(
-                    sp, hash_view(m), m->block_keys, tsdf_base(m), sem_base(m), m->sem_idx, m->cand.p, lbl,
-                    conf, ten, m->dirty + m->cfg.max_blocks, m->d_ctr);
-                count_launch();
+                for (int check = conf_check ? 1 : 0; check >= 0; --check) {
+                    kern<<<grid, kThreads, 0, m->stream>>>(
+                        sp, hash_view(m), m->block_keys, tsdf_base(m), sem_base(m), m->sem_idx, m->cand.p,
+                        lbl, conf, ten, m->dirty + m->cfg.max_blocks, check, m->d_ctr);
+                    count_launch();
+                }
             }
             SVX_CUDA(cudaGetLastError());
         }
         // per-image results: candidates and updated voxels
-        SVX_CUDA(cudaMemcpyAsync(m->sem_out.p + 2 * i, m->d_ctr + C_CAND, 4, cudaMemcpyDeviceToDevice,
+        SVX_CUDA(cudaMemcpyAsync(m->sem_out.p + 3 * i, m->d_ctr + C_CAND, 4, cudaMemcpyDeviceToDevice,
                                  m->stream));
-        SVX_CUDA(cudaMemcpyAsync(m->sem_out.p + 2 * i + 1, m->d_ctr + C_SEM_UPDATED, 4,
+        SVX_CUDA(cudaMemcpyAsync(m->sem_out.p + 3 * i + 1, m->d_ctr + C_SEM_UPDATED, 4,
+                                 cudaMemcpyDeviceToDevice, m->stream));
+        SVX_CUDA(cudaMemcpyAsync(m->sem_out.p + 3 * i + 2, m->d_ctr + C_ERR_CONF, 4,
                                  cudaMemcpyDeviceToDevice, m->stream));
     }
-    std::vector<uint32_t> outs(2ull * n);
-    SVX_CUDA(cudaMemcpyAsync(outs.data(), m->sem_out.p, 8ull * n, cudaMemcpyDeviceToHost, m->stream));
+    std::vector<uint32_t> outs(3ull * n);
+    SVX_CUDA(cudaMemcpyAsync(outs.data(), m->sem_out.p, 12ull * n, cudaMemcpyDeviceToHost, m->stream));
     sync_counters(m);
     if (m->h_ctr[C_ERR_CONF]) {
-        // the reference numbers a frame before it can throw (semantic_integrator.cpp:93-94)
-        m->sem_frames += n;
+        // images before the failing one are complete; the failing one is numbered (the
+        // reference numbers a frame before it can throw, semantic_integrator.cpp:93-94)
+        // and updated nothing; later images did not run
+        int fail = 0;
+        while (fail < n && !outs[3 * fail + 2]) ++fail;
+        for (int i = 0; i < fail && i < n; ++i) {
+            reps[i].frame = m->sem_frames++;
+            reps[i].updated_voxels = outs[3 * i + 1];
+        }
+        m->sem_frames++;
         m->n_layers = m->h_ctr[C_SEM];
+        SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_ERR_CONF, 0, 4, m->stream));
+        SVX_CUDA(cudaStreamSynchronize(m->stream));
         throw Error(SVX_INVALID_ARGUMENT, "confidence must be in [0, 1]");
     }
     for (int i = 0; i < n; ++i) {
         reps[i].frame = m->sem_frames++;
-        reps[i].updated_voxels = outs[2 * i + 1];
+        reps[i].updated_voxels = outs[3 * i + 1];
         m->prof_acc.sem_images += 1;
-        m->prof_acc.sem_candidates += outs[2 * i];
-        m->prof_acc.sem_updated += outs[2 * i + 1];
+        m->prof_acc.sem_candidates += outs[3 * i];
+        m->prof_acc.sem_updated += outs[3 * i + 1];
     }
     m->prof_acc.sem_new_layers += m->h_ctr[C_SEM] - m->n_layers;
     m->n_layers = m->h_ctr[C_SEM];

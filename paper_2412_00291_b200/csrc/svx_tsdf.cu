@@ -1313,6 +1313,21 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
             SVX_CUDA(cudaEventRecord(m->ingest_used[r], m->stream));
         }
     }
+    // fills the report of completed frame i (its FrameOut is final) and numbers it
+    auto commit = [&](int i) {
+        const FrameOut& o = m->h_outs[i];
+        reps[i].frame = m->tsdf_frames++;
+        reps[i].updated_voxels = o.updated;
+        reps[i].new_blocks = o.new_blocks;
+        m->new_ema = m->new_ema == 0.0 ? double(o.new_blocks) : 0.9 * m->new_ema + 0.1 * double(o.new_blocks);
+        jobs[i].scan->dropped = o.dropped;
+        m->prof_acc.frames += 1;
+        m->prof_acc.rays += o.rays;
+        m->prof_acc.touched_blocks += o.touched;
+        m->prof_acc.new_blocks += o.new_blocks;
+        m->prof_acc.updated_voxels += o.updated;
+        m->prof_acc.fallback_voxels += o.fb_voxels;
+    };
     int f0 = 0, stage0 = 0;
     for (;;) {
         const auto te0 = std::chrono::steady_clock::now();
@@ -1370,14 +1385,23 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
         svx_scan* s = jobs[fa].scan;
         const uint32_t before = m->h_ctr[C_BLOCKS_BEFORE];
         if (abort & kAbortKey) {
-            m->n_blocks = std::min<uint64_t>(m->h_ctr[C_BLOCKS], m->cfg.max_blocks);
+            // like the capacity path: the frames before the failing one are complete
+            // (reported and numbered); the failing frame is numbered (the reference
+            // numbers a frame before it can throw) and leaves no block behind: its
+            // partially inserted blocks (possibly beyond the mapped, zero-filled pool)
+            // are dropped and their dirty flags cleared
+            for (int i = 0; i < fa; ++i) commit(i);
+            m->tsdf_frames++;
+            const uint64_t hi = std::min<uint64_t>(m->h_ctr[C_BLOCKS], m->cfg.max_blocks);
+            if (hi > before) SVX_CUDA(cudaMemsetAsync(m->dirty + before, 0, hi - before, m->stream));
+            m->n_blocks = before;
             rebuild_hash(m);
             reset_frame_state(m);
             throw Error(SVX_INVALID_ARGUMENT,
                         "block coordinate outside the device key range [-2^20, 2^20)");
         }
         if (abort & (kAbortCapacity | kAbortHash)) {
-            for (int i = 0; i < fa; ++i) reps[i].frame = m->tsdf_frames++;
+            for (int i = 0; i < fa; ++i) commit(i);
             m->tsdf_frames++;
             m->n_blocks = before;
             capacity_path(m, fps[fa], s, before);
@@ -1427,21 +1451,7 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
         m->prof_acc.host_resume_ms +=
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tr0).count();
     }
-    for (int i = 0; i < n; ++i) {
-        const FrameOut& o = m->h_outs[i];
-        reps[i].frame = m->tsdf_frames++;
-        reps[i].updated_voxels = o.updated;
-        reps[i].new_blocks = o.new_blocks;
-        m->new_ema = m->new_ema == 0.0 ? double(o.new_blocks)
-                                       : 0.9 * m->new_ema + 0.1 * double(o.new_blocks);
-        jobs[i].scan->dropped = o.dropped;
-        m->prof_acc.frames += 1;
-        m->prof_acc.rays += o.rays;
-        m->prof_acc.touched_blocks += o.touched;
-        m->prof_acc.new_blocks += o.new_blocks;
-        m->prof_acc.updated_voxels += o.updated;
-        m->prof_acc.fallback_voxels += o.fb_voxels;
-    }
+    for (int i = 0; i < n; ++i) commit(i);
     m->n_blocks = m->h_ctr[C_BLOCKS];
 }
 

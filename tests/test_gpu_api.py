@@ -365,6 +365,118 @@ def test_invalid_confidence_rejected():
         svx.SemanticIntegrator(s).integrate_labels(img)
 
 
+def test_invalid_confidence_only_where_read():
+    """label_to_likelihood throws only for a pixel that a voxel passing every test
+    reads (semantic_integrator.cpp:24-27,140-142): an invalid confidence elsewhere,
+    or an invalid default on a frame no voxel passes, integrates normally."""
+    cfg = svx.MapConfig(0.25, 1.25, 2)
+    s, vc = store_with_voxel(cfg, (0, 0, 2.0))
+    si = svx.SemanticIntegrator(s)
+    img = simple_image(0)
+    img.confidence = np.full(64, 0.8, np.float32)
+    img.confidence[0] = 7.0                  # no voxel projects to pixel (0, 0)
+    r = si.integrate_labels(img)
+    assert r.updated_voxels == 1 and r.frame == 0
+    assert s.lookup_voxel(vc)[1][0] == pytest.approx(0.8)
+    img.confidence[4 * 8 + 4] = -0.5         # the voxel's own pixel: throws, updates nothing
+    before = s.save_bytes()
+    with pytest.raises(svx.InvalidArgument):
+        si.integrate_labels(img)
+    assert s.save_bytes() == before
+    img.confidence[4 * 8 + 4] = np.nan       # NaN passes the reference's comparison
+    assert si.integrate_labels(img).frame == 2
+    # invalid default confidence: fine while no voxel passes, throws once one does
+    bad = svx.SemanticIntegrator(svx.VoxelStore(cfg), svx.SemanticConfig(default_confidence=1.5))
+    assert bad.integrate_labels(simple_image(0)).updated_voxels == 0
+    s2, _ = store_with_voxel(cfg, (0, 0, 2.0))
+    with pytest.raises(svx.InvalidArgument):
+        svx.SemanticIntegrator(s2, svx.SemanticConfig(default_confidence=1.5)).integrate_labels(
+            simple_image(0))
+
+
+def test_invalid_confidence_batch_stops_at_failing_image():
+    cfg = svx.MapConfig(0.25, 1.25, 2)
+    s, vc = store_with_voxel(cfg, (0, 0, 2.0))
+    imgs = [simple_image(0), simple_image(1), simple_image(0)]
+    for im in imgs:
+        im.confidence = np.full(64, 0.7, np.float32)
+    imgs[1].confidence[36] = 2.0
+    si = svx.SemanticIntegrator(s)
+    with pytest.raises(svx.InvalidArgument):
+        si.integrate_labels_batch(imgs)
+    # only image 0 was applied; images 0 and 1 are numbered
+    assert s.lookup_voxel(vc)[1][0] == pytest.approx(0.7)
+    assert si.integrate_labels(simple_image(0)).frame == 2
+
+
+def test_key_range_abort_leaves_no_partial_blocks():
+    """A frame whose band leaves the device key range [-2^20, 2^20) blocks raises
+    InvalidArgument after the frames before it completed; it leaves no block behind
+    (even with a tiny pool headroom, so its band also exhausted the mapped pool), and
+    the map keeps integrating afterwards exactly like one that never saw it."""
+    m = svx.ProjectionModel.spinning(256, 32, 25, 25)
+    cfg = svx.MapConfig(0.1, 0.5, 2, 1 << 18)
+    far = (2 ** 20) * 8 * float(np.float32(0.1)) - 3.0  # some band blocks out of range
+    scans = [plane_scan(m, (0.0, 0.0, 1.2), 0.0), plane_scan(m, (far, 0.0, 1.2), 0.0),
+             plane_scan(m, (0.3, 0.0, 1.2), 0.0)]
+    os.environ["SVX_TEST_POOL_HEAD"] = "16"
+    try:
+        s = svx.VoxelStore(cfg)
+    finally:
+        os.environ.pop("SVX_TEST_POOL_HEAD", None)
+    ref = svx.VoxelStore(cfg)
+    ti, tr = svx.TsdfIntegrator(s), svx.TsdfIntegrator(ref)
+    import torch
+    pts = np.concatenate([p for p, _ in scans[:2]]).astype(np.float32)
+    offs = np.array([0, len(scans[0][0]), len(pts)], np.uint64)
+    dev = torch.from_numpy(pts).cuda()
+    with pytest.raises(svx.InvalidArgument):
+        s.integrate_clouds_device(m, dev.data_ptr(), offs, 3, [scans[0][1], scans[1][1]],
+                                  svx.IntegratorConfig())
+    tr.integrate_cloud(*scans[0], m)
+    assert s.block_count() == ref.block_count()
+    assert s.save_bytes() == ref.save_bytes()
+    r = ti.integrate_cloud(*scans[2], m)
+    r2 = tr.integrate_cloud(*scans[2], m)
+    assert r.frame == 2 and r2.frame == 1
+    assert (r.updated_voxels, r.new_blocks) == (r2.updated_voxels, r2.new_blocks)
+    assert s.save_bytes() == ref.save_bytes()
+    assert np.array_equal(s.take_dirty_blocks(0), ref.take_dirty_blocks(0))
+
+
+def test_load_merges_repeated_block_records(tmp_path):
+    """A snapshot that repeats a block coordinate loads as ONE block
+    (VoxelStore::load calls get_or_allocate_block, voxel_store.cpp:145): the later
+    TSDF wins, semantics are taken from the later record that has them; the same
+    file loaded by the reference's own reader gives the same map."""
+    import struct
+    K = 2
+    rng = np.random.default_rng(4)
+
+    def rec(b, sem):
+        t = np.zeros(512, TSDF_DTYPE)
+        t["distance"] = rng.uniform(-1, 1, 512)
+        t["weight"] = rng.uniform(0, 2, 512)
+        out = struct.pack("<3i", *b) + t.tobytes()
+        if sem is None:
+            return out + b"\x00"
+        return out + b"\x01" + np.full(512 * K, sem, np.float32).tobytes()
+
+    recs = [rec((0, 0, 0), 0.25), rec((1, 0, 0), None), rec((0, 0, 0), None),
+            rec((2, 0, 0), None), rec((1, 0, 0), 0.75), rec((0, 0, 0), None)]
+    blob = b"SVOX1" + struct.pack("<ffIQ", 0.1, 0.5, K, len(recs)) + b"".join(recs)
+    p = tmp_path / "dup.svox"
+    p.write_bytes(blob)
+    g = svx.VoxelStore.load(str(p), max_blocks=3)      # 3 distinct blocks fit
+    assert g.block_count() == 3
+    from oracle.bindings import RefMap, ref_available
+    if ref_available():
+        r = RefMap.load(str(p), svx.MapConfig(0.1, 0.5, K))
+        assert g.save_bytes() == r.save_bytes()
+    assert g.lookup_voxel((0, 0, 0))[1][0] == np.float32(0.25)
+    assert g.lookup_voxel((8, 0, 0))[1][0] == np.float32(0.75)
+
+
 def test_kernel_launch_counter_moves():
     s = svx.VoxelStore(svx.MapConfig(0.1, 0.5))
     m = svx.ProjectionModel.spinning(256, 32, 25, 25)
