@@ -197,7 +197,7 @@ def test_exact_boundary_atan2_acos_device_vs_glibc():
                 img = svx.project_cloud(np.array([[x, y, z]], np.float32), svx.pose_c(np.eye(3), [0, 0, 0]),
                                         m, _store())
                 nz = np.nonzero(img.depth)[0]
-                if 0 <= v < 128:
+                if r >= m.min_range and 0 <= v < 128:
                     assert list(nz) == [v * width + u], (x, y, z, width, nz, v * width + u)
                 else:
                     assert len(nz) == 0
