@@ -96,15 +96,16 @@ void free_map(svx_map* m) {
     cudaSetDevice(m->device);
     if (m->stream) cudaStreamSynchronize(m->stream);
     for (void* p : {(void*)m->keys, (void*)m->vals, (void*)m->block_keys, (void*)m->sem_idx,
-                    (void*)m->dirty, (void*)m->stamp, (void*)m->touched, (void*)m->vmask,
+                    (void*)m->dirty, (void*)m->stamp, (void*)m->touched, (void*)m->fctr,
                     (void*)m->d_ctr, (void*)m->fbcnt, (void*)m->fbstart, (void*)m->fbfill,
-                    (void*)m->fbslots, (void*)m->bigslots, (void*)m->fbclaim})
+                    (void*)m->fbslots, (void*)m->fbclaim})
         if (p) cudaFree(p);
     if (m->h_ctr) cudaFreeHost(m->h_ctr);
     if (m->h_outs) cudaFreeHost(m->h_outs);
     m->outs.release();
     m->bucket.release();
-    m->vlist.release();
+    m->bucket2.release();
+    m->wlist.release();
     prof_resolve(m);
     for (cudaEvent_t e : m->prof_free) cudaEventDestroy(e);
     m->records.release();
@@ -145,14 +146,14 @@ svx_map* create_map(const svx_map_cfg& cfg, int device) {
         uint64_t want = std::max<uint64_t>(2ull * cfg.max_blocks, 1024);
         m->log2cap = 0;
         while ((1ull << m->log2cap) < want) ++m->log2cap;
-        // slot * 32 mask words must fit in u32 (svx_tsdf.cu)
-        require(m->log2cap <= 26, SVX_INVALID_ARGUMENT, "max_blocks too large for the device hash");
+        // a fallback record holds a slot in 23 bits (svx_tsdf.cu): max_blocks <= 2^22
+        require(m->log2cap <= 23, SVX_INVALID_ARGUMENT, "max_blocks too large for the device hash (<= 2^22)");
         m->cap = uint32_t(1u << m->log2cap);
         m->keys = dmalloc<uint64_t>(m->cap);
         m->vals = dmalloc<uint32_t>(m->cap);
         m->stamp = dmalloc<uint32_t>(m->cap);
-        m->touched = dmalloc<uint32_t>(2ull * m->cap);
-        m->vmask = dmalloc<uint32_t>(32ull * m->cap);
+        m->touched = dmalloc<uint32_t>(m->cap);
+        m->fctr = dmalloc<uint32_t>(kMaxG * kFC);
         m->block_keys = dmalloc<uint64_t>(cfg.max_blocks);
         m->sem_idx = dmalloc<uint32_t>(cfg.max_blocks);
         m->dirty = dmalloc<uint8_t>(2ull * cfg.max_blocks);
@@ -162,19 +163,19 @@ svx_map* create_map(const svx_map_cfg& cfg, int device) {
         m->fbfill = dmalloc<uint32_t>(m->cap);
         m->fbclaim = dmalloc<uint32_t>(m->cap);
         m->fbslots = dmalloc<uint32_t>(m->cap);
-        m->bigslots = dmalloc<uint32_t>(m->cap);
         m->rec_cap = 1u << 20;
         // test hook: tiny buffers exercise the abort-and-resume paths
         if (const char* e = std::getenv("SVX_TEST_REC_CAP")) m->rec_cap = uint32_t(std::max(1L, std::atol(e)));
         if (const char* e = std::getenv("SVX_TEST_POOL_HEAD")) m->test_pool_head = uint64_t(std::max(1L, std::atol(e)));
-        m->records.alloc(2ull * m->rec_cap);  // 32-byte records: 2 x uint4
-        m->bucket.alloc(2ull * m->rec_cap);
+        m->records.alloc(m->rec_cap);
+        m->bucket.alloc(m->rec_cap);
+        m->bucket2.alloc(m->rec_cap);
         SVX_CUDA(cudaMallocHost(&m->h_ctr, sizeof(uint32_t) * kNumCounters));
         std::memset(m->h_ctr, 0, sizeof(uint32_t) * kNumCounters);
         SVX_CUDA(cudaMemsetAsync(m->keys, 0xFF, 8ull * m->cap, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->vals, 0xFF, 4ull * m->cap, m->stream));  // kInvalid: no block yet
         SVX_CUDA(cudaMemsetAsync(m->stamp, 0, 4ull * m->cap, m->stream));
-        SVX_CUDA(cudaMemsetAsync(m->vmask, 0, 128ull * m->cap, m->stream));
+        SVX_CUDA(cudaMemsetAsync(m->fctr, 0, 4ull * kMaxG * kFC, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->fbcnt, 0, 4ull * m->cap, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->fbfill, 0, 4ull * m->cap, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->fbclaim, 0, 4ull * m->cap, m->stream));
@@ -185,6 +186,7 @@ svx_map* create_map(const svx_map_cfg& cfg, int device) {
         m->block_bytes = sizeof(svx_tsdf_voxel) * kBlockVoxels;
         m->layer_bytes = sizeof(float) * kBlockVoxels * size_t(cfg.num_labels);
         m->tsdf_pool.reserve(device, size_t(cfg.max_blocks) * m->block_bytes);
+        m->mask_pool.reserve(device, size_t(cfg.max_blocks) * 4 * kMaskWords);
         m->sem_pool.reserve(device, size_t(cfg.max_blocks) * m->layer_bytes);
         SVX_CUDA(cudaStreamSynchronize(m->stream));
     } catch (...) {
@@ -858,24 +860,8 @@ svx_status svx_scan_create(svx_map* m, const svx_lidar_model* model, svx_scan** 
                 }
             s->dirs.alloc(3 * P);
             SVX_CUDA(cudaMemcpy(s->dirs.p, dirs.data(), 8 * 3 * P, cudaMemcpyHostToDevice));
-            s->depth.alloc(P);
-            s->height.alloc(P);
-            s->normals.alloc(3 * P);
-            s->valid.alloc(P);
-            s->tie.alloc(P);
-            s->pixkey.alloc(2 * P);
-            s->lexkey.alloc(3 * P);
-            s->pixcache.alloc(48 * P);
-            s->rowdist.alloc(P);
-            s->validbits.alloc((P + 31) / 32);
-            SVX_CUDA(cudaMemset(s->validbits.p, 0, 4 * ((P + 31) / 32)));
-            SVX_CUDA(cudaMemset(s->pixkey.p, 0xFF, 16 * P));
-            SVX_CUDA(cudaMemset(s->pixcache.p, 0, 48 * P));
-            SVX_CUDA(cudaMemset(s->depth.p, 0, 4 * P));
-            SVX_CUDA(cudaMemset(s->height.p, 0, 4 * P));
-            SVX_CUDA(cudaMemset(s->normals.p, 0, 12 * P));
-            SVX_CUDA(cudaMemset(s->valid.p, 0, P));
-            SVX_CUDA(cudaMemset(s->tie.p, 0, P));
+            s->VW = int((P + 31) / 32);
+            ensure_scan_slots(s, 1, 0);
         } catch (...) {
             delete s;
             throw;
@@ -901,13 +887,23 @@ svx_status svx_scan_destroy(svx_scan* s) {
         s->validbits.release();
         s->points64.release();
         s->tie.release();
-        s->pix_of_pt.release();
         s->points.release();
         delete s;
     });
 }
 
 namespace {
+// A standalone projection (slot 0): read its dropped count, clear the per-frame counters
+// it used (a TSDF group resets them itself).
+void finish_projection(svx_scan* s) {
+    svx_map* m = s->map;
+    uint32_t fc[kFC];
+    SVX_CUDA(cudaMemcpyAsync(fc, m->fctr, sizeof fc, cudaMemcpyDeviceToHost, m->stream));
+    SVX_CUDA(cudaMemsetAsync(m->fctr, 0, sizeof fc, m->stream));
+    sync_counters(m);
+    s->dropped = fc[FC_DROPPED];
+}
+
 const float* stage_points(svx_scan* s, const float* pts, uint64_t n, int32_t stride, int32_t is_dev) {
     require(stride >= 3, SVX_INVALID_ARGUMENT, "point stride must be >= 3");
     require(n < (1ull << 32), SVX_INVALID_ARGUMENT, "too many points in one cloud");
@@ -926,11 +922,7 @@ svx_status svx_project(svx_scan* s, const float* pts, uint64_t n, int32_t stride
         validate_pose(*pose);
         const float* d = stage_points(s, pts, n, stride, is_dev);
         launch_project(s, d, n, stride, to_pose(*pose));
-        sync_counters(s->map);
-        s->dropped = s->map->h_ctr[C_DROPPED];
-        SVX_CUDA(cudaMemsetAsync(s->map->d_ctr + C_TIES, 0, 4, s->map->stream));
-        SVX_CUDA(cudaMemsetAsync(s->map->d_ctr + C_DROPPED, 0, 4, s->map->stream));
-        SVX_CUDA(cudaStreamSynchronize(s->map->stream));
+        finish_projection(s);
     });
 }
 
@@ -949,11 +941,7 @@ svx_status svx_project_f64(svx_scan* s, const double* pts, uint64_t n, int32_t s
             d = s->points64.p;
         }
         launch_project(s, d, n, stride, to_pose(*pose));
-        sync_counters(s->map);
-        s->dropped = s->map->h_ctr[C_DROPPED];
-        SVX_CUDA(cudaMemsetAsync(s->map->d_ctr + C_TIES, 0, 4, s->map->stream));
-        SVX_CUDA(cudaMemsetAsync(s->map->d_ctr + C_DROPPED, 0, 4, s->map->stream));
-        SVX_CUDA(cudaStreamSynchronize(s->map->stream));
+        finish_projection(s);
     });
 }
 
@@ -971,6 +959,7 @@ svx_status svx_scan_upload(svx_scan* s, const float* depth, const float* height,
         DeviceGuard g(s->map->device);
         const size_t P = size_t(s->P);
         require(depth != nullptr, SVX_INVALID_ARGUMENT, "depth image required");
+        s->last_slot = 0;
         SVX_CUDA(cudaMemcpy(s->depth.p, depth, 4 * P, cudaMemcpyHostToDevice));
         if (height) SVX_CUDA(cudaMemcpy(s->height.p, height, 4 * P, cudaMemcpyHostToDevice));
         s->has_normals = normals != nullptr;
@@ -988,11 +977,11 @@ svx_status svx_scan_download(svx_scan* s, float* depth, float* height, float* no
     return guarded([&] {
         DeviceGuard g(s->map->device);
         SVX_CUDA(cudaStreamSynchronize(s->map->stream));
-        const size_t P = size_t(s->P);
-        if (depth) SVX_CUDA(cudaMemcpy(depth, s->depth.p, 4 * P, cudaMemcpyDeviceToHost));
-        if (height) SVX_CUDA(cudaMemcpy(height, s->height.p, 4 * P, cudaMemcpyDeviceToHost));
-        if (normals) SVX_CUDA(cudaMemcpy(normals, s->normals.p, 12 * P, cudaMemcpyDeviceToHost));
-        if (valid) SVX_CUDA(cudaMemcpy(valid, s->valid.p, P, cudaMemcpyDeviceToHost));
+        const size_t P = size_t(s->P), o = size_t(s->last_slot) * P;
+        if (depth) SVX_CUDA(cudaMemcpy(depth, s->depth.p + o, 4 * P, cudaMemcpyDeviceToHost));
+        if (height) SVX_CUDA(cudaMemcpy(height, s->height.p + o, 4 * P, cudaMemcpyDeviceToHost));
+        if (normals) SVX_CUDA(cudaMemcpy(normals, s->normals.p + 3 * o, 12 * P, cudaMemcpyDeviceToHost));
+        if (valid) SVX_CUDA(cudaMemcpy(valid, s->valid.p + o, P, cudaMemcpyDeviceToHost));
         if (dropped) *dropped = s->dropped;
         if (has_normals) *has_normals = s->has_normals;
     });

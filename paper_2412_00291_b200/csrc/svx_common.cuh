@@ -19,6 +19,15 @@ namespace svx {
 
 constexpr int kBlockSide = 8;
 constexpr int kBlockVoxels = 512;
+// TSDF frames integrated together by one group of kernel launches (svx_tsdf.cu)
+constexpr int kMaxG = 16;
+// Per-block visit masks of a frame group (svx_tsdf.cu), 16 words (512 voxel bits) per row:
+// row 0 = voxels visited by any frame of the group, row 1 + g = visited by frame g,
+// row kHdrRow word 0 = frames that touched the block (bit g). Cleared after each group.
+constexpr int kHdrRow = 1 + kMaxG;
+constexpr int kMaskWords = (kHdrRow + 1) * 16;
+// per-frame counters of a group: fctr[g * kFC + FC_*]
+enum FrameCounter : int { FC_UPD = 0, FC_RAYS, FC_DROPPED, FC_TIES, FC_TOUCH, FC_NEW, FC_FBV, kFC = 8 };
 constexpr double kPi = 3.14159265358979323846;
 
 // Packed block key: 21 bits per axis, biased by 2^20 so that unsigned order of
@@ -314,7 +323,7 @@ __device__ inline uint32_t hash_insert(const HashView& h, uint64_t key, int* ins
 enum Counter : int {
     C_BLOCKS = 0,       // allocated blocks (pool high-water mark)
     C_SEM = 1,          // allocated semantic layers
-    C_TOUCHED = 2,      // blocks touched by the current frame
+    C_TOUCHED = 2,      // blocks touched by the current frame group
     C_UPDATED = 3,      // voxels updated by the current pass
     C_FALLBACK = 4,     // voxels that need the multi-ray fallback
     C_RECORDS = 5,      // fallback visit records
@@ -329,28 +338,27 @@ enum Counter : int {
     C_REC_OVERFLOW = 14,
     C_RAYS = 15,        // band rays cast this frame
     C_ABORT = 16,       // bitmask of abort reasons (kAbort*); every frame kernel no-ops while set
-    C_BLOCKS_BEFORE = 17,  // C_BLOCKS at the start of the current frame
+    C_BLOCKS_BEFORE = 17,  // C_BLOCKS at the start of the current frame group
     C_MAPPED = 18,      // blocks of TSDF pool currently mapped (host-written)
     C_FB_BLOCKS = 19,   // blocks holding fallback records this frame
     C_FB_VOXELS = 20,   // voxels folded by the fallback path
     C_FB_BIG = 21,      // blocks whose fallback bucket exceeds the warp sort
-    C_VOXLIST = 22,     // touched voxels listed by the band kernel
+    C_WORDS = 22,       // visit-mask words listed by the band kernel (group)
     C_BUCKET_TOP = 23,  // fallback bucket space handed out this frame
-    C_DONE = 24,        // CTAs of k_fb_fold finished (last one writes the report)
-    C_TOUCHED_PREV = 25,  // blocks touched by the previous frame (their mask words get cleared)
-    C_ABORT_FRAME = 26, // frame serial that raised a pool / big-bucket abort (set before the bit)
+    C_DONE = 24,        // CTAs of k_fold finished (the last one writes the group's reports)
     C_CONF_MAYBE = 27,  // the current label image may read a confidence outside [0, 1]
     kNumCounters = 32
 };
 
+// Any abort stops the rest of the batch; the host rolls the aborted frame group back
+// (svx_tsdf.cu, rollback_group) and retries it.
 enum AbortBits : uint32_t {
-    kAbortPool = 1,      // pool mapping exhausted: map more, resume
-    kAbortCapacity = 2,  // max_blocks exceeded: CapacityError path
+    kAbortPool = 1,      // pool mapping exhausted: map more, retry the group
+    kAbortCapacity = 2,  // max_blocks exceeded: frame by frame, then the CapacityError path
     kAbortKey = 4,       // block coordinate outside the key range
     kAbortHash = 8,      // hash table full (implies capacity)
-    kAbortRecords = 16,  // fallback record buffer too small: grow, re-run band
-    kAbortBigBucket = 32, // a fallback bucket needs the host-sorted path
-    kAbortVoxList = 64    // touched-voxel list too small: grow, re-run band
+    kAbortRecords = 16,  // fallback record buffer too small: grow, retry
+    kAbortWords = 64     // visit-mask word list too small: grow, retry
 };
 
 // Per-frame results written by k_frame_end (device), read back per batch.
@@ -407,25 +415,6 @@ __device__ __forceinline__ bool pixel_has_return(const uint32_t* __restrict__ bi
 // not let their threads disagree about it (another CTA may set it meanwhile).
 __device__ inline bool cta_aborted(const uint32_t* ctr, uint32_t mask = 0xFFFFFFFFu) {
     return __syncthreads_or(threadIdx.x == 0 ? int((ctr[C_ABORT] & mask) != 0) : 0) != 0;
-}
-
-// Raises abort `bit` for the frame `serial` (the frame itself may finish the kernel
-// that raised it; later frames must not run): the frame id is published first.
-__device__ inline void raise_frame_abort(uint32_t* ctr, uint32_t bit, uint32_t serial) {
-    atomicExch(&ctr[C_ABORT_FRAME], serial);
-    __threadfence();
-    atomicOr(&ctr[C_ABORT], bit);
-}
-
-// CTA-uniform abort test that lets the frame that raised `own_bit` continue.
-__device__ inline bool cta_aborted_for(const uint32_t* ctr, uint32_t own_bit, uint32_t serial) {
-    int stop = 0;
-    if (threadIdx.x == 0) {
-        const uint32_t a = __ldcg(&ctr[C_ABORT]);
-        __threadfence();
-        stop = (a & ~own_bit) != 0 || ((a & own_bit) && __ldcg(&ctr[C_ABORT_FRAME]) != serial);
-    }
-    return __syncthreads_or(stop) != 0;
 }
 
 // CTA-wide reservation of n entries per thread in a list whose length lives in

@@ -9,9 +9,10 @@
 //                                      mapped on demand (CUDA VMM) so addresses are stable
 //   sem pool    [layers][512][K] f32   lazily allocated semantic layers (VMM as above)
 //   block_keys[idx], sem_idx[idx], dirty flags[idx]   per pool block
-//   frame scratch: stamp[cap] u32, touched[2][cap] u32 (slots touched by a frame),
-//                  vmask[cap][2][16] u32 (touched-voxel bits, two halves used by
-//                  alternate frames so each frame's half is cleared by the next one)
+//   mask pool  [blocks][kMaskWords] u32  per-block visit masks of the current frame group
+//                                      (VMM, parallel to the TSDF pool, 1152 B per block)
+//   group scratch: stamp[cap] u32 (first touch per group), touched[cap] u32, fallback
+//                  records and their per-block buckets, the visit-mask word list
 #pragma once
 
 #include <cuda.h>
@@ -142,27 +143,33 @@ struct MeshState {
 
 }  // namespace svx
 
+// Device ScanImages of up to `slots` frames of one ProjectionModel (one frame group,
+// svx_tsdf.cu): frame slot g of an image array starts at g * P (normals at 3 g P, pixel
+// cache at g P entries, valid bits at g * VW words).
 struct svx_scan {
     svx_map* map = nullptr;
     svx_lidar_model model{};
     svx::Model dm{};
     int P = 0;
+    int VW = 0;                   // valid-bit words per frame slot
+    int slots = 0;                // frame slots allocated
     svx::DevBuf<double> dirs;     // P x 3 back_project directions (host libm, bit-exact)
-    svx::DevBuf<float> depth;     // P
-    svx::DevBuf<float> height;    // P
-    svx::DevBuf<float> normals;   // 3P (sensor frame)
-    svx::DevBuf<uint8_t> valid;   // P
-    svx::DevBuf<unsigned long long> pixkey;  // 2P: double-buffered (range bits << 32) | point index
-    int parity = 0;                           // which pixkey half the next projection uses
-    svx::DevBuf<uint8_t> pixcache;           // P x 48 B: ray, range, world normal, flags
-    svx::DevBuf<uint8_t> rowdist;            // P: row distance to the nearest empty pixel
-    svx::DevBuf<uint32_t> validbits;         // P/32: pixel has a return (bit per pixel)
-    bool rowdist_fresh = false;              // rowdist matches depth (set by projection)
-    svx::DevBuf<unsigned long long> lexkey;  // P: tie-break scratch
-    svx::DevBuf<uint8_t> tie;     // P: possible exact-range tie
-    svx::DevBuf<uint32_t> pix_of_pt;  // per input point: pixel index or kInvalid
+    svx::DevBuf<float> depth;     // slots x P
+    svx::DevBuf<float> height;    // slots x P
+    svx::DevBuf<float> normals;   // slots x 3P (sensor frame)
+    svx::DevBuf<uint8_t> valid;   // slots x P
+    svx::DevBuf<unsigned long long> pixkey;  // slots x 2P: double-buffered (range bits << 32) | point index
+    int parity[svx::kMaxG] = {};             // which pixkey half a slot's next projection uses
+    svx::DevBuf<uint8_t> pixcache;           // slots x P x 48 B: ray, range, world normal, flags
+    svx::DevBuf<uint8_t> rowdist;            // slots x P: row distance to the nearest empty pixel
+    svx::DevBuf<uint32_t> validbits;         // slots x VW: pixel has a return (bit per pixel)
+    bool rowdist_fresh = false;              // slot 0's rowdist matches its depth (user images)
+    svx::DevBuf<unsigned long long> lexkey;  // slots x tie_cap: tie lists
+    uint64_t tie_cap = 0;                    // tie-list entries per slot
+    svx::DevBuf<uint8_t> tie;     // slots x P: possible exact-range tie
     svx::DevBuf<float> points;    // staging for host points
     svx::DevBuf<double> points64; // staging for host FP64 points
+    int last_slot = 0;            // slot holding the most recent ScanImages
     bool has_normals = false;
     uint64_t dropped = 0;
     uint64_t n_points = 0;
@@ -187,25 +194,26 @@ struct svx_map {
     uint64_t* block_keys = nullptr;  // [max_blocks]
     uint32_t* sem_idx = nullptr;     // [max_blocks]
     uint8_t* dirty = nullptr;        // [2][max_blocks]
-    // frame scratch
-    uint32_t* stamp = nullptr;
-    uint32_t* touched = nullptr;     // [2][cap]: blocks touched by the frame, per mask parity
-    uint32_t* vmask = nullptr;       // [cap][32]
-    svx::DevBuf<uint4> records;      // fallback records of the frame (32 B each: 2 x uint4)
+    // frame-group scratch (svx_tsdf.cu)
+    uint32_t* stamp = nullptr;       // [cap] group serial of a slot's first touch
+    uint32_t* touched = nullptr;     // [cap] slots touched by the current group
+    svx::VmmArray mask_pool;         // [blocks][kMaskWords] u32 visit masks, parallel to the pool
+    uint64_t mask_zeroed = 0;        // blocks of mask_pool zero-filled so far
+    uint32_t* fctr = nullptr;        // [kMaxG][kFC] per-frame counters of the current group
+    svx::DevBuf<unsigned long long> records;  // fallback visit records: slot<<41|lin<<32|g<<28|pixel
     svx::DevBuf<unsigned long long> records_alt;  // capacity path: visited block keys
     svx::DevBuf<uint8_t> sort_tmp;
-    // fallback stage (voxels whose own pixel has no return): per-slot record
-    // counts / bucket offsets, the frame's record list and the bucketed keys
+    // fallback stage (voxels whose own pixel has no return in some frame): per-slot record
+    // counts / bucket offsets / claims, the blocks holding records, the bucketed records
     uint32_t* fbcnt = nullptr;       // [cap]
     uint32_t* fbstart = nullptr;     // [cap]
     uint32_t* fbfill = nullptr;      // [cap]
     uint32_t* fbclaim = nullptr;     // [cap] bucket allocation claim flags
     uint32_t* fbslots = nullptr;     // [cap]
-    uint32_t* bigslots = nullptr;    // [cap] buckets too large for the warp sort
-    svx::DevBuf<uint4> bucket;       // the records grouped by block (32 B each)
+    svx::DevBuf<unsigned long long> bucket, bucket2;  // records grouped by block (+ sort scratch)
     uint32_t rec_cap = 0;
-    svx::DevBuf<unsigned long long> vlist;  // touched voxels of the frame: (pool idx << 9) | linear
-    uint32_t vox_cap = 0;
+    svx::DevBuf<unsigned long long> wlist;  // visit-mask words of the group: (pool idx << 4) | word
+    uint32_t word_cap = 0;
     // per-frame results of a batch
     svx::DevBuf<svx::FrameOut> outs;
     svx::FrameOut* h_outs = nullptr;
@@ -213,9 +221,9 @@ struct svx_map {
     uint64_t mapped_blocks = 0;      // host mirror of C_MAPPED
     double new_ema = 0.0;            // moving average of new blocks per frame
     uint64_t test_pool_head = 0;     // test hook (SVX_TEST_POOL_HEAD): fixed pool headroom
-    // host ingest ring (svx_integrate_clouds): the points of the next frames are
-    // copied on `copy_stream` while the current frame integrates
-    static constexpr int kIngestSlots = 4;
+    // host ingest ring (svx_integrate_clouds): the points of the next frame group are
+    // copied on `copy_stream` while the current group integrates
+    static constexpr int kIngestSlots = 2;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ingest_ready[kIngestSlots] = {}, ingest_used[kIngestSlots] = {};
     svx::DevBuf<float> ingest[kIngestSlots];
@@ -297,16 +305,22 @@ inline svx_tsdf_voxel* tsdf_base(svx_map* m) {
 }
 inline float* sem_base(svx_map* m) { return static_cast<float*>(m->sem_pool.base()); }
 inline HashView hash_view(svx_map* m) { return HashView{m->keys, m->vals, m->log2cap, m->cap - 1}; }
+inline uint32_t* mask_base(svx_map* m) { return static_cast<uint32_t*>(m->mask_pool.base()); }
 
 Model make_model(const svx_lidar_model& lm);
 Pose to_pose(const svx_pose& p);
 void validate_pose(const svx_pose& p);
 
 // kernels' host launchers (svx_project.cu, svx_tsdf.cu, svx_semantic.cu, svx_store.cu)
+// Projection of a frame group: frame g's points (device) go to scan slot g.
+void launch_project_group(svx_scan* s, const void* const* d_pts, const uint64_t* n, int G, int stride,
+                          bool fp64, const Pose* poses);
 void launch_project(svx_scan* s, const float* d_pts, uint64_t n, int stride, const Pose& pose);
 void launch_project(svx_scan* s, const double* d_pts, uint64_t n, int stride, const Pose& pose);
 void launch_normals(svx_scan* s);
-// One TSDF frame of a batch: project (optional) + integrate_frame.
+// Frame slots of a scan for groups of G frames of up to max_points points each.
+void ensure_scan_slots(svx_scan* s, int G, uint64_t max_points);
+// One TSDF frame: project (optional) + integrate_frame.
 struct FrameJob {
     svx_scan* scan;
     Pose pose;
@@ -316,8 +330,8 @@ struct FrameJob {
     bool project;
     bool host_ingest = false;  // pts are in host memory: staged through the ingest ring
 };
-// Runs the frames back to back on the map stream, synchronising once at the end
-// (plus once per abort/resume, rare). Fills one report per frame.
+// Runs the frames in groups of up to kMaxG on the map stream, synchronising once at
+// the end (plus once per abort + retry, rare). Fills one report per frame.
 void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cfg& cfg,
                 svx_frame_report* reps);
 void reset_frame_state(svx_map* m);

@@ -159,17 +159,32 @@ VmmArray::~VmmArray() {
     drv().addr_free(base_, reserved_);
 }
 
+// Maps TSDF pool and visit-mask memory (svx_tsdf.cu) for `blocks` blocks now and `ahead`
+// more in the background. C_MAPPED (what kernels may allocate into) counts blocks whose
+// pool and zero-filled masks are both mapped; the mask zero-fill is stream-ordered before
+// the new count is published.
 void ensure_blocks(svx_map* m, uint64_t blocks, uint64_t ahead) {
     if (blocks > m->cfg.max_blocks) blocks = m->cfg.max_blocks;
-    if (blocks * m->block_bytes > m->tsdf_pool.mapped()) {
+    const uint64_t mask_bytes = 4ull * kMaskWords;
+    if (blocks * m->block_bytes > m->tsdf_pool.mapped() || blocks * mask_bytes > m->mask_pool.mapped()) {
         const auto t0 = std::chrono::steady_clock::now();
         m->tsdf_pool.ensure(blocks * m->block_bytes);
+        m->mask_pool.ensure(blocks * mask_bytes);
         m->prof_acc.host_map_ms +=
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     }
     // keep the next growth off the critical path: map ahead in the background
-    m->tsdf_pool.prefetch(std::min<uint64_t>(m->cfg.max_blocks, blocks + ahead) * m->block_bytes);
-    const uint64_t mapped = std::min<uint64_t>(m->tsdf_pool.mapped() / m->block_bytes, m->cfg.max_blocks);
+    const uint64_t target = std::min<uint64_t>(m->cfg.max_blocks, blocks + ahead);
+    m->tsdf_pool.prefetch(target * m->block_bytes);
+    m->mask_pool.prefetch(target * mask_bytes);
+    const uint64_t mapped = std::min<uint64_t>(
+        std::min<uint64_t>(m->tsdf_pool.mapped() / m->block_bytes, m->mask_pool.mapped() / mask_bytes),
+        m->cfg.max_blocks);
+    if (mapped > m->mask_zeroed) {
+        SVX_CUDA(cudaMemsetAsync(mask_base(m) + m->mask_zeroed * kMaskWords, 0,
+                                 (mapped - m->mask_zeroed) * mask_bytes, m->stream));
+        m->mask_zeroed = mapped;
+    }
     if (mapped != m->mapped_blocks) {
         m->mapped_blocks = mapped;
         m->h_ctr[C_MAPPED] = uint32_t(mapped);

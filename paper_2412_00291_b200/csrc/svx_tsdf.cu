@@ -1,52 +1,60 @@
-// K3-K5: TsdfIntegrator::integrate_frame on the device (tsdf_integrator.cpp:97-258).
+// K3-K5: TsdfIntegrator::integrate_frame on the device (tsdf_integrator.cpp:97-258),
+// for GROUPS of up to kMaxG consecutive frames per launch sequence.
 //
-// Three kernels per frame on the map stream, no host synchronisation (a batch of
-// frames is synchronised once at its end):
-//   k_raycast_band  K3+K4. CTA = 32 x 8 pixel tile, one thread per pixel. Writes the
-//                   pixel cache (ray, range, world normal: the measurement inputs of
-//                   tsdf_integrator.cpp:178-186, once per pixel instead of once per
-//                   (pixel, voxel)). Band [q - tau r^, q + tau r^], amortised DDA
-//                   (tsdf_integrator.hpp:93-135) into a shared-memory table of the
-//                   tile's blocks and their 512-bit voxel masks. Per visit, the
-//                   own-pixel test of the voxel (FP32, sensor-frame offset updated
-//                   incrementally along the DDA, exact decision via error margins): a
-//                   voxel whose own pixel has no return is measured by every visiting
-//                   ray in the reference (.cpp:232-238), so the visit becomes a
-//                   fallback record, measured right away. Tile epilogue: one hash
-//                   find-or-insert per distinct block (new block => next pool index,
-//                   zero-filled by the tile), dirty flag, touched list; the masks are
-//                   ORed into the frame's half of the global mask words and the bits a
-//                   tile sets first become the frame's touched-voxel list (each voxel
-//                   exactly once).
-//   k_fold          K5, one thread per touched voxel (flat, load-balanced): own pixel,
-//                   measure, accumulate-then-merge fold (Eq. 4-5, .cpp:170-248). Also
-//                   clears the previous frame's half of the mask words and moves the
-//                   fallback records into per-block buckets.
-//   k_fb_fold       CTA per block with fallback records: orders its bucket by (voxel,
-//                   pixel) => per-voxel visits in ascending (v, u) order, exactly the
-//                   reference's order after its chunk-order merge + stable_sort; sums
-//                   the terms strictly in that order; fold. Its last CTA writes the
-//                   frame report and resets the per-frame counters.
-// Every kernel first checks the abort word: after an abort (pool growth, buffer
-// growth, capacity) the rest of the batch no-ops and the host resumes it.
+// What the reference does per frame, and what is independent across frames:
+//   * phase 1 (.cpp:112-139) casts the band of every valid pixel: pure geometry of the
+//     frame's images and pose, so every frame of a group runs its band in ONE launch;
+//   * which voxels a frame updates, their own pixel (.cpp:232) and whether a visiting
+//     ray's pixel is measurable (.cpp:172-181) are geometry too;
+//   * only the VALUES depend on the voxel's state: the non-projective distance reads the
+//     voxel's pre-update gradient (.cpp:190-196), and the fold reads W and D (.cpp:239-247).
+// So a group is integrated as: project all frames; band DDA of all frames (visit masks per
+// frame); then ONE thread per distinct visited voxel applies the group's frames to it in
+// frame order, with the voxel in registers - exactly the sequence of the reference's
+// consecutive integrate_frame calls for that voxel.
+//
+// Kernels per group (one stream, programmatic dependent launch, no host synchronisation):
+//   k_band       CTA = (frame g, 32 x 8 pixel tile), thread = pixel: pixel cache (ray, range,
+//                world normal; the measurement inputs of .cpp:173-186, once per pixel),
+//                amortised band DDA (tsdf_integrator.hpp:93-135) into a shared-memory table
+//                of the tile's blocks and 512-bit voxel masks; per visit the own-pixel test
+//                of the voxel (FP32 with an exact-decision margin): a voxel whose own pixel
+//                has no return is measured by every visiting ray in the reference
+//                (.cpp:232-238), so such a visit becomes a fallback record (slot, voxel,
+//                frame, pixel). Epilogue: one hash find-or-insert per distinct block (new
+//                block -> next pool index, zero-filled by the tile), the group's touched
+//                list, the frame's visit-mask row (RED.OR) and the union row (ATOM.OR: the
+//                words a tile sets first become the group's word list).
+//   k_fb_bucket  the fallback records into per-block buckets.
+//   k_fb_fold    CTA per block with fallback records: orders its records by (voxel, frame,
+//                pixel) - per frame the reference's ascending (v, u) visit order after its
+//                chunk-order merge + stable_sort (.cpp:141-146,215-216) - and applies every
+//                frame of the group to each of those voxels (own pixel where it has a
+//                return, else the ordered sum over the frame's visiting rays).
+//   k_fold       warp per 32 listed mask words, lane per visited voxel: applies the group's
+//                frames in order (own-pixel measurement, accumulate-then-merge fold, Eq.
+//                4-5); voxels with a fallback frame are left to k_fb_fold. Clears the mask
+//                words, marks dirty blocks, counts per-frame touched / new blocks; the last
+//                CTA writes the frames' reports.
+// Any abort (pool growth, buffer growth, capacity, key range) stops the batch; the host
+// rolls the aborted group back (its blocks, hash entries and masks) and retries it
+// (CapacityError and key-range errors: frame by frame, reproducing the reference's
+// per-frame behaviour).
 #include <cub/block/block_scan.cuh>
-#include <cub/device/device_radix_sort.cuh>
 #include <math_constants.h>
 
 #include <algorithm>
-#include <cstdio>
 #include <chrono>
+#include <cstdio>
 #include <vector>
 
 #include "svx_map.hpp"
 
 namespace svx {
 
-struct FrameParams {
+// Constants shared by every frame of a group (same model, same integrator config).
+struct GroupConsts {
     Model m;
-    Pose pose, w2s;
-    d3 origin;
-    float col[3][3];  // nu * (R^T e_m): sensor-frame step of +1 voxel along world axis m
     double tau, max_range, alpha_eps, nu, inv_nu;
     double ca_hi, ca_lo;  // cos(alpha_eps) +- 1e-12: margins of the alpha < eps branch
     float min_clamp;
@@ -55,10 +63,35 @@ struct FrameParams {
     float delta, min_range_safe, sin_min, dphi_f, dtheta_f;
     int nonproj, drop_unreliable, has_normals;
     int32_t shard_rank, shard_world;
-    uint32_t frame_serial;
-    uint32_t parity;  // which half of each block's 32 mask words this frame uses
-    uint32_t max_blocks;
-    uint32_t rec_cap, vox_cap;
+    uint32_t serial;    // group serial (touched stamps)
+    uint32_t G, P, VW;  // frames, pixels per frame, valid-bit words per frame
+    uint32_t tiles;     // band tiles per frame
+    uint32_t max_blocks, rec_cap, word_cap;
+};
+
+// Per-frame pose data.
+struct FramePose {
+    Pose pose, w2s;
+    d3 origin;
+    float col[3][3];  // nu * (R^T e_m): sensor-frame step of +1 voxel along world axis m
+    float pad;
+};
+static_assert(sizeof(FramePose) % 8 == 0, "FramePose layout");
+
+struct GroupParams {
+    GroupConsts c;
+    FramePose f[kMaxG];
+};
+
+// Device images of the group's frames (frame g at slot g of the scan).
+struct ScanSlots {
+    const float* depth;
+    const float* normals;
+    const uint8_t* valid;
+    const double* dirs;
+    const uint8_t* rowdist;
+    const uint32_t* validbits;
+    uint8_t* cache;  // PixCache[slots][P]
 };
 
 struct PixCache {
@@ -69,7 +102,7 @@ struct PixCache {
 };
 static_assert(sizeof(PixCache) == 48, "PixCache layout");
 
-struct Term {  // one (pixel, voxel) measurement of the fallback path
+struct Term {  // one (pixel, voxel) measurement
     float wg, w, nx, ny, nz;
     uint32_t flags;  // bit0: measured, bit1: has normal
 };
@@ -77,8 +110,6 @@ struct Term {  // one (pixel, voxel) measurement of the fallback path
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kFbThreads = 256;
-constexpr int kFbMax = 4096;  // fallback records of one block ordered in shared memory
 
 __device__ inline d3 dir_at(const double* __restrict__ dirs, uint32_t p) {
     return mk(__ldg(&dirs[3 * p]), __ldg(&dirs[3 * p + 1]), __ldg(&dirs[3 * p + 2]));
@@ -96,15 +127,38 @@ __device__ inline d3 center_of(uint64_t key, int linear, double nu) {
                         bz * kBlockSide + linear / (kBlockSide * kBlockSide), nu);
 }
 
-// Own pixel of a voxel centre c: project_point(world_to_sensor * c)
-// (tsdf_integrator.cpp:232). pc is world_to_sensor * c in FP64 (reference formula).
-__device__ inline uint32_t own_pixel(const FrameParams& f, d3 pc) {
-    const uint32_t q = pixel_fast(float(pc.x), float(pc.y), float(pc.z), f.m, f.m.r2_lo, f.m.r2_hi);
-    return q == kNeedFp64 ? pixel_fp64(pc, f.m) : q;
+__device__ inline const PixCache* cache_of(const ScanSlots& sc, const GroupConsts& c, uint32_t g) {
+    return reinterpret_cast<const PixCache*>(sc.cache) + uint64_t(g) * c.P;
 }
 
-// Row distance (columns, azimuth wraps) from each pixel to the nearest pixel of
-// its row without a return, capped at kRmax + 1.
+// Position of the r-th (0-based) set bit of x (r < popc(x)).
+__device__ inline uint32_t select_bit(uint32_t x, uint32_t r) {
+    uint32_t pos = 0;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        const uint32_t low = x & ((1u << s) - 1u);
+        const uint32_t n = __popc(low);
+        if (r >= n) {
+            r -= n;
+            x >>= s;
+            pos += uint32_t(s);
+        } else {
+            x = low;
+        }
+    }
+    return pos;
+}
+
+// Own pixel of a voxel centre: project_point(world_to_sensor * c) (tsdf_integrator.cpp:232);
+// pc is world_to_sensor * c in FP64 (reference formula).
+__device__ inline uint32_t own_pixel(const Model& m, d3 pc) {
+    const uint32_t q = pixel_fast(float(pc.x), float(pc.y), float(pc.z), m, m.r2_lo, m.r2_hi);
+    return q == kNeedFp64 ? pixel_fp64(pc, m) : q;
+}
+
+// Row distance (columns, azimuth wraps) from each pixel to the nearest pixel of its row
+// without a return, capped at kRmax + 1; plus the valid bits. For images the caller
+// uploaded (the projection builds both itself).
 constexpr int kRmax = kRowDistMax;
 __global__ void __launch_bounds__(kThreads)
 k_row_dist(const float* __restrict__ depth, int W, int H, uint8_t* __restrict__ hd,
@@ -129,9 +183,8 @@ k_row_dist(const float* __restrict__ depth, int W, int H, uint8_t* __restrict__ 
     hd[p] = uint8_t(d);
 }
 
-// Chebyshev distance from pixel p to the nearest pixel without a return or to
-// the top/bottom image edge, capped at kRmax + 1: every pixel closer than that
-// holds a return.
+// Chebyshev distance from pixel p to the nearest pixel without a return or to the
+// top/bottom image edge, capped at kRmax + 1: every pixel closer than that holds a return.
 __device__ inline int valid_radius(const uint8_t* __restrict__ hd, int W, int H, uint32_t p) {
     const int u = int(p % W), v = int(p / W);
     int r = kRmax + 1;
@@ -145,25 +198,25 @@ __device__ inline int valid_radius(const uint8_t* __restrict__ hd, int W, int H,
     return r;
 }
 
-// True when no voxel visited by the band of this ray can have its own pixel
-// without a return: the voxel centre lies within delta = sqrt(3)/2 nu of the ray,
-// so its direction is within angle a <= 1.1 delta / d_min of the pixel-centre
-// direction, i.e. within k pixels; every pixel within k of p holds a return.
-__device__ inline bool band_all_own(const FrameParams& f, const uint8_t* __restrict__ hd,
+// True when no voxel visited by the band of this ray can have its own pixel without a
+// return: the voxel centre lies within delta = sqrt(3)/2 nu of the ray, so its direction is
+// within angle a <= 1.1 delta / d_min of the pixel-centre direction, i.e. within k pixels;
+// every pixel within k of p holds a return.
+__device__ inline bool band_all_own(const GroupConsts& c, const uint8_t* __restrict__ hd,
                                     uint32_t p, float r) {
-    const float dmin = r - float(f.tau) - f.delta;
-    if (!(dmin > f.min_range_safe)) return false;
-    const float x = f.delta / dmin;
+    const float dmin = r - float(c.tau) - c.delta;
+    if (!(dmin > c.min_range_safe)) return false;
+    const float x = c.delta / dmin;
     if (x > 0.3f) return false;
     const float a = 1.1f * x;  // asin(x) <= 1.1 x for x <= 0.3
-    const float s = f.sin_min - a;
+    const float s = c.sin_min - a;
     if (s < 0.1f || a > s * (1.f / 3.f)) return false;
     // azimuth offset <= 2 asin(sin(a/2) / s) <= 1.05 a / s for a / s <= 1/3
-    const int ku = int(floorf(1.05f * a / (s * f.dphi_f) + 0.5f)) + 1;
-    const int kv = int(floorf(a / f.dtheta_f + 0.5f)) + 1;
+    const int ku = int(floorf(1.05f * a / (s * c.dphi_f) + 0.5f)) + 1;
+    const int kv = int(floorf(a / c.dtheta_f + 0.5f)) + 1;
     const int k = max(ku, kv);
     if (k > kRmax) return false;
-    return valid_radius(hd, f.m.W, f.m.H, p) > k;
+    return valid_radius(hd, c.m.W, c.m.H, p) > k;
 }
 
 struct Accum {
@@ -171,8 +224,7 @@ struct Accum {
 };
 
 // nonprojective_distance (tsdf_integrator.cpp:39-46)
-__device__ inline double nonprojective_distance(double psi, double theta, double alpha,
-                                                double eps) {
+__device__ inline double nonprojective_distance(double psi, double theta, double alpha, double eps) {
     double st, ct;
     sincos(theta, &st, &ct);  // same values as sin()/cos(), one shared range reduction
     if (alpha < eps) return fabs(ct) * psi;
@@ -187,26 +239,25 @@ __device__ inline float truncate_f(double d, double tau) {
     return float(d >= 0.0 ? (tau < d ? tau : d) : (d < -tau ? -tau : d));
 }
 
-// Gamma(d) of the non-projective distance from the clamped cosines ct = cos(theta)
-// and ca = cos(alpha). The reference evaluates theta = acos(ct), alpha = acos(ca)
-// and then cos/sin of both with libm (tsdf_integrator.cpp:39-46,195-196).
-// Fast path without transcendentals: cos(acos(x)) = x and sin(acos(x)) =
-// sqrt((1-x)(1+x)) up to |err| <= 2e-15 (1-ulp libm acos/cos/sin: pi * 2^-52 + 2^-52),
-// an absolute bound E on the resulting d, and the f32 value the reference stores,
-// float(clamp(d, +-tau)), accepted only when all of [d - E, d + E] rounds to it.
-// The branch alpha < eps is decided on ca against cos(eps) with a 1e-12 margin
-// (acos is strictly decreasing). Otherwise (ca near cos(eps), sin(alpha) < 1e-6,
-// or an interval straddling a float boundary: ~1e-4 of the voxels) the reference
-// formula is evaluated with CUDA's FP64 acos/sincos.
-__device__ inline float gamma_nonprojective(const FrameParams& f, double psi, double ct, double ca) {
+// Gamma(d) of the non-projective distance from the clamped cosines ct = cos(theta) and
+// ca = cos(alpha). The reference evaluates theta = acos(ct), alpha = acos(ca) and then
+// cos/sin of both with libm (tsdf_integrator.cpp:39-46,195-196). Fast path without
+// transcendentals: cos(acos(x)) = x and sin(acos(x)) = sqrt((1-x)(1+x)) up to
+// |err| <= 2e-15 (1-ulp libm acos/cos/sin: pi * 2^-52 + 2^-52), an absolute bound E on the
+// resulting d, and the f32 value the reference stores, float(clamp(d, +-tau)), accepted
+// only when all of [d - E, d + E] rounds to it. The branch alpha < eps is decided on ca
+// against cos(eps) with a 1e-12 margin (acos is strictly decreasing). Otherwise (ca near
+// cos(eps), sin(alpha) < 1e-6, or an interval straddling a float boundary: ~1e-4 of the
+// voxels) the reference formula is evaluated with CUDA's FP64 acos/sincos.
+__device__ inline float gamma_nonprojective(const GroupConsts& c, double psi, double ct, double ca) {
     constexpr double kAbs = 2e-15, kRel = 2e-15;
     bool fast = false;
     double d = 0.0, e = 0.0;
-    if (ca > f.ca_hi) {  // alpha < eps: |cos theta| * psi
+    if (ca > c.ca_hi) {  // alpha < eps: |cos theta| * psi
         d = fabs(ct) * psi;
         e = fabs(psi) * (kAbs + kRel * fabs(ct)) + 1e-15 * fabs(d);
         fast = true;
-    } else if (ca < f.ca_lo) {
+    } else if (ca < c.ca_lo) {
         const double st = sqrt((1.0 - ct) * (1.0 + ct));
         const double sa = sqrt((1.0 - ca) * (1.0 + ca));
         if (sa > 1e-6) {
@@ -215,22 +266,22 @@ __device__ inline float gamma_nonprojective(const FrameParams& f, double psi, do
             const double mag = t1 + t2;
             d = psi >= 0.0 ? mag : -mag;
             const double da = kAbs + kRel * fabs(a), dst = kAbs + kRel * st, dsa = kAbs + kRel * sa;
-            e = 1.01 * ((fabs(a) * dst + st * da) / sa + t1 * dsa / sa +
-                        fabs(psi) * (kAbs + kRel * fabs(ct))) +
+            e = 1.01 * ((fabs(a) * dst + st * da) / sa + t1 * dsa / sa + fabs(psi) * (kAbs + kRel * fabs(ct))) +
                 1e-15 * mag;
             fast = true;
         }
     }
     if (fast) {
-        const float lo = truncate_f(d - e, f.tau), hi = truncate_f(d + e, f.tau);
+        const float lo = truncate_f(d - e, c.tau), hi = truncate_f(d + e, c.tau);
         if (lo == hi && __float_as_uint(lo) == __float_as_uint(hi)) return lo;
     }
-    return truncate_f(nonprojective_distance(psi, acos(ct), acos(ca), f.alpha_eps), f.tau);
+    return truncate_f(nonprojective_distance(psi, acos(ct), acos(ca), c.alpha_eps), c.tau);
 }
 
-// measure lambda (tsdf_integrator.cpp:172-205) for pixel p, from the pixel cache:
-// the contribution (w * Gamma(d), w, w * n) as the reference forms it, in f32.
-__device__ inline Term measure_term(const FrameParams& f, const PixCache* __restrict__ cache,
+// measure lambda (tsdf_integrator.cpp:172-205) for pixel p of a frame, from its pixel
+// cache: the contribution (w * Gamma(d), w, w * n) as the reference forms it, in f32.
+// vox is the voxel's state before this frame (the pre-update gradient).
+__device__ inline Term measure_term(const GroupConsts& c, d3 origin, const PixCache* __restrict__ cache,
                                     uint32_t p, d3 center, const svx_tsdf_voxel& vox) {
     Term t{0.f, 0.f, 0.f, 0.f, 0.f, 0u};
     const PixCache& pc = cache[p];
@@ -238,14 +289,14 @@ __device__ inline Term measure_term(const FrameParams& f, const PixCache* __rest
     if (!(flags & 1u)) return t;
     const bool have_normal = flags & 2u;
     const d3 ray = mk(pc.ray[0], pc.ray[1], pc.ray[2]);
-    const double psi = pc.range - dot3(sub3(center, f.origin), ray);
-    if (fabs(psi) > f.tau) return t;
+    const double psi = pc.range - dot3(sub3(center, origin), ray);
+    if (fabs(psi) > c.tau) return t;
     const float nw[3] = {pc.n[0], pc.n[1], pc.n[2]};
     float gamma;
-    if (f.nonproj && have_normal) {
+    if (c.nonproj && have_normal) {
         float g[3] = {nw[0], nw[1], nw[2]};
-        const float gsq = (vox.gradient[0] * vox.gradient[0] + vox.gradient[1] * vox.gradient[1]) +
-                          vox.gradient[2] * vox.gradient[2];
+        const float gsq =
+            (vox.gradient[0] * vox.gradient[0] + vox.gradient[1] * vox.gradient[1]) + vox.gradient[2] * vox.gradient[2];
         if (vox.weight > 0.f && gsq > 1e-12f) {
             g[0] = vox.gradient[0];
             g[1] = vox.gradient[1];
@@ -258,13 +309,13 @@ __device__ inline Term measure_term(const FrameParams& f, const PixCache* __rest
         ct = ct < -1.0 ? -1.0 : (1.0 < ct ? 1.0 : ct);
         double ca = dot3(gd, mk(nw[0], nw[1], nw[2]));
         ca = ca < -1.0 ? -1.0 : (1.0 < ca ? 1.0 : ca);
-        gamma = gamma_nonprojective(f, psi, ct, ca);
+        gamma = gamma_nonprojective(c, psi, ct, ca);
     } else {
-        gamma = truncate_f(psi, f.tau);
+        gamma = truncate_f(psi, c.tau);
     }
     // observation_weight (tsdf_integrator.cpp:48-51)
-    double wr = (psi + f.tau) / (2.0 * f.tau);
-    const double lo = double(f.min_clamp);
+    double wr = (psi + c.tau) / (2.0 * c.tau);
+    const double lo = double(c.min_clamp);
     wr = wr < lo ? lo : (1.0 < wr ? 1.0 : wr);
     const float w_obs = float(wr);
     t.wg = w_obs * gamma;
@@ -323,16 +374,72 @@ __device__ inline void store_voxel(svx_tsdf_voxel* p, const svx_tsdf_voxel& v) {
     d[4] = v.gradient[2];
 }
 
-// A fallback record: one (visiting ray, voxel) measurement of a voxel whose own
-// pixel has no return, measured where the visit is found (band kernel) and
-// summed later in pixel order (k_fb_fold). The voxel's state cannot change in
-// between: fallback voxels are only written by k_fb_fold.
-struct FbRec {
-    uint32_t key;   // linear << 23 | pixel
-    uint32_t slot;  // hash slot of the block
-    Term t;
-};
-static_assert(sizeof(FbRec) == 32, "FbRec layout");
+// Fallback visit record: bits 41.. hash slot, 32..40 voxel, 28..31 frame of the group,
+// 0..27 pixel. Within a block, the low 41 bits order by (voxel, frame, pixel).
+__device__ inline unsigned long long make_record(uint32_t slot, int lin, uint32_t g, uint32_t p) {
+    return (static_cast<unsigned long long>(slot) << 41) | (static_cast<unsigned long long>(lin) << 32) |
+           (static_cast<unsigned long long>(g) << 28) | p;
+}
+__device__ inline uint32_t rec_frame(unsigned long long r) { return uint32_t(r >> 28) & 15u; }
+__device__ inline uint32_t rec_pixel(unsigned long long r) { return uint32_t(r) & 0x0FFFFFFFu; }
+__device__ inline int rec_lin(unsigned long long r) { return int(uint32_t(r >> 32) & 511u); }
+
+// Bit g = frame g of the group visited voxel lin of block idx.
+__device__ inline uint32_t voxel_frames(const uint32_t* __restrict__ fm, uint32_t idx, int lin, uint32_t G) {
+    const uint32_t* row = fm + uint64_t(idx) * kMaskWords + 16 + (lin >> 5);
+    const int b = lin & 31;
+    uint32_t f = 0;
+#pragma unroll 4
+    for (uint32_t g = 0; g < G; ++g) f |= ((row[16 * g] >> b) & 1u) << g;
+    return f;
+}
+
+// Applies the group's frames that visited the voxel (bit g of `frames`, ascending = the
+// order of the reference's consecutive integrate_frame calls) to the voxel at vp, whose
+// state lives in registers meanwhile. Per frame: the own pixel of the voxel centre if it
+// holds a return (.cpp:232-233), else every visiting ray of that frame in ascending pixel
+// order (.cpp:235-236), taken from `recs` (sorted by (frame, pixel)). Without records
+// (kRec = false), a frame of the second kind returns kFallback and stores nothing: the
+// voxel belongs to k_fb_fold. Returns the frames that updated the voxel.
+constexpr uint32_t kFallback = 0xFFFFFFFFu;
+template <bool kRec>
+__device__ uint32_t fold_voxel(const GroupConsts& c, const FramePose* __restrict__ fp, uint32_t frames,
+                               svx_tsdf_voxel* vp, d3 center, const ScanSlots& sc,
+                               const unsigned long long* __restrict__ recs, uint32_t nrec) {
+    svx_tsdf_voxel vox = load_voxel(vp);
+    uint32_t j = 0, upd = 0;
+    for (uint32_t fr = frames; fr; fr &= fr - 1) {
+        const uint32_t g = uint32_t(__ffs(fr) - 1);
+        const FramePose& f = fp[g];
+        const PixCache* cache = cache_of(sc, c, g);
+        const uint32_t own = own_pixel(c.m, xform(f.w2s, center));
+        Accum acc{0.0, 0.0, 0.0, 0.0, 0.0};
+        bool measured = false;
+        if (own != kInvalid && pixel_has_return(sc.validbits + uint64_t(g) * c.VW, own)) {
+            const Term t = measure_term(c, f.origin, cache, own, center, vox);
+            if (t.flags & 1u) {
+                accumulate(acc, t);
+                measured = true;
+            }
+        } else {
+            if constexpr (!kRec) return kFallback;
+            while (j < nrec && rec_frame(recs[j]) < g) ++j;
+            for (; j < nrec && rec_frame(recs[j]) == g; ++j) {
+                const Term t = measure_term(c, f.origin, cache, rec_pixel(recs[j]), center, vox);
+                if (t.flags & 1u) {
+                    accumulate(acc, t);
+                    measured = true;
+                }
+            }
+        }
+        if (measured) {
+            fold(vox, acc);
+            upd |= 1u << g;
+        }
+    }
+    if (upd) store_voxel(vp, vox);
+    return upd;
+}
 
 // Hash find-or-insert of a block key; a new block takes the next pool index.
 struct SlotRef {
@@ -340,8 +447,8 @@ struct SlotRef {
     bool inserted;
 };
 
-// Pool index of an existing slot. A slot inserted concurrently by another CTA
-// gets its index right after the key (find_or_insert): wait for it.
+// Pool index of an existing slot. A slot inserted concurrently by another CTA gets its
+// index right after the key (find_or_insert): wait for it.
 __device__ inline uint32_t block_index(HashView h, uint32_t slot) {
     uint32_t idx = __ldcg(&h.vals[slot]);
     while (idx == kInvalid) {
@@ -351,27 +458,37 @@ __device__ inline uint32_t block_index(HashView h, uint32_t slot) {
     return idx;
 }
 
-__device__ inline SlotRef find_or_insert(const FrameParams& f, HashView h,
-                                         uint64_t* __restrict__ block_keys,
+// Returns slot kInvalid when the block cannot be used by this group (hash full, capacity,
+// pool not mapped); the matching abort bit is raised and the group is rolled back.
+__device__ inline SlotRef find_or_insert(const GroupConsts& c, HashView h, uint64_t* __restrict__ block_keys,
                                          uint32_t* __restrict__ ctr, uint64_t key) {
     SlotRef r{kInvalid, kInvalid, false};
     int ins = 0;
-    r.slot = hash_insert(h, key, &ins);
-    if (r.slot == kInvalid) {
+    const uint32_t slot = hash_insert(h, key, &ins);
+    if (slot == kInvalid) {
         atomicOr(&ctr[C_ABORT], kAbortHash | kAbortCapacity);
         return r;
     }
+    uint32_t idx;
     if (ins) {
-        r.inserted = true;
-        r.idx = atomicAdd(&ctr[C_BLOCKS], 1u);
-        if (r.idx < f.max_blocks) block_keys[r.idx] = key;
+        idx = atomicAdd(&ctr[C_BLOCKS], 1u);
+        if (idx < c.max_blocks) block_keys[idx] = key;
         __threadfence();
-        atomicExch(&h.vals[r.slot], r.idx);
-        if (r.idx >= f.max_blocks) atomicOr(&ctr[C_ABORT], kAbortCapacity);
-        else if (r.idx >= ctr[C_MAPPED]) raise_frame_abort(ctr, kAbortPool, f.frame_serial);
+        atomicExch(&h.vals[slot], idx);
     } else {
-        r.idx = block_index(h, r.slot);
+        idx = block_index(h, slot);
     }
+    if (idx >= c.max_blocks) {
+        atomicOr(&ctr[C_ABORT], kAbortCapacity);
+        return r;
+    }
+    if (idx >= __ldcg(&ctr[C_MAPPED])) {  // pool / mask memory not mapped yet: map, retry
+        atomicOr(&ctr[C_ABORT], kAbortPool);
+        return r;
+    }
+    r.slot = slot;
+    r.idx = idx;
+    r.inserted = ins != 0;
     return r;
 }
 
@@ -380,64 +497,40 @@ __device__ inline void zero_block(svx_tsdf_voxel* __restrict__ pool, uint32_t id
     for (int i = lane; i < kBlockVoxels * 5 / 4; i += lanes) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
-// Measurement of fallback visit (slot, lin) by the ray of pixel p. A block
-// created in this frame (pool index unset yet or >= the frame's first new index)
-// is all-zero; its pool memory may not be zero-filled yet (tile epilogues).
-__device__ inline Term fallback_term(const FrameParams& f, HashView h,
-                                     const svx_tsdf_voxel* __restrict__ pool,
-                                     const PixCache* __restrict__ cache, uint32_t blocks_before,
-                                     uint32_t slot, uint64_t key, int lin, uint32_t p) {
-    const uint32_t idx = __ldcg(&h.vals[slot]);
-    svx_tsdf_voxel vox{0.f, 0.f, {0.f, 0.f, 0.f}};
-    if (idx != kInvalid && idx < blocks_before) vox = load_voxel(pool + uint64_t(idx) * kBlockVoxels + lin);
-    return measure_term(f, cache, p, center_of(key, lin, f.nu), vox);
-}
-
-__device__ inline void store_record(FbRec* __restrict__ rec, uint32_t pos, const FbRec& r) {
-    uint4* d = reinterpret_cast<uint4*>(rec + pos);
-    const uint4* s = reinterpret_cast<const uint4*>(&r);
-    d[0] = s[0];
-    d[1] = s[1];
-}
-
-// Per-visit work on global state (no tile staging): the path a visit takes when
-// its tile's shared tables are full. Same effect as the staged path.
-__device__ void visit_global(const FrameParams& f, HashView h, uint64_t* __restrict__ block_keys,
+// Per-visit work on global state (no tile staging): the path a visit takes when its tile's
+// shared tables are full. Same effect as the staged path.
+__device__ void visit_global(const GroupConsts& c, uint32_t g, HashView h, uint64_t* __restrict__ block_keys,
                              uint32_t* __restrict__ stamp, uint32_t* __restrict__ touched,
-                             uint32_t* __restrict__ vmask, uint32_t* __restrict__ fbcnt,
-                             FbRec* __restrict__ rec, svx_tsdf_voxel* __restrict__ pool,
-                             const PixCache* __restrict__ cache, uint8_t* __restrict__ dirty,
-                             unsigned long long* __restrict__ vlist, uint32_t blocks_before,
-                             uint32_t* __restrict__ ctr, uint64_t key, int lin, bool fb, uint32_t p) {
-    const SlotRef r = find_or_insert(f, h, block_keys, ctr, key);
+                             uint32_t* __restrict__ fm, uint32_t* __restrict__ fbcnt,
+                             unsigned long long* __restrict__ rec, svx_tsdf_voxel* __restrict__ pool,
+                             unsigned long long* __restrict__ wlist, uint32_t* __restrict__ ctr, uint64_t key,
+                             int lin, bool fb, uint32_t p) {
+    const SlotRef r = find_or_insert(c, h, block_keys, ctr, key);
     if (r.slot == kInvalid) return;
-    if (atomicExch(&stamp[r.slot], f.frame_serial) != f.frame_serial)
-        touched[atomicAdd(&ctr[C_TOUCHED], 1u)] = r.slot;
-    if (r.idx >= f.max_blocks) return;
-    if (r.inserted && r.idx < ctr[C_MAPPED]) zero_block(pool, r.idx, 0, 1);
-    dirty[r.idx] = 1;
+    if (atomicExch(&stamp[r.slot], c.serial) != c.serial) touched[atomicAdd(&ctr[C_TOUCHED], 1u)] = r.slot;
+    if (r.inserted) zero_block(pool, r.idx, 0, 1);
+    uint32_t* bm = fm + uint64_t(r.idx) * kMaskWords;
+    atomicOr(&bm[kHdrRow * 16], 1u << g);
     const uint32_t bit = 1u << (lin & 31);
-    if (!(atomicOr(&vmask[uint64_t(r.slot) * 32 + f.parity * 16 + (lin >> 5)], bit) & bit)) {
-        const uint32_t pos = atomicAdd(&ctr[C_VOXLIST], 1u);
-        if (pos < f.vox_cap) vlist[pos] = (static_cast<unsigned long long>(r.idx) << 9) | uint32_t(lin);
-        else atomicOr(&ctr[C_ABORT], kAbortVoxList);
+    const int w = lin >> 5;
+    atomicOr(&bm[(1 + g) * 16 + w], bit);
+    if (atomicOr(&bm[w], bit) == 0u) {
+        const uint32_t pos = atomicAdd(&ctr[C_WORDS], 1u);
+        if (pos < c.word_cap) wlist[pos] = (static_cast<unsigned long long>(r.idx) << 4) | uint32_t(w);
+        else atomicOr(&ctr[C_ABORT], kAbortWords);
     }
     if (!fb) return;
-    const Term t = fallback_term(f, h, pool, cache, blocks_before, r.slot, key, lin, p);
-    if (!(t.flags & 1u)) return;  // no contribution
     atomicAdd(&fbcnt[r.slot], 1u);
     const uint32_t pos = atomicAdd(&ctr[C_RECORDS], 1u);
-    if (pos < f.rec_cap)
-        store_record(rec, pos, FbRec{(uint32_t(lin) << 23) | p, r.slot, t});
-    else
-        atomicOr(&ctr[C_ABORT], kAbortRecords);
+    if (pos < c.rec_cap) rec[pos] = make_record(r.slot, lin, g, p);
+    else atomicOr(&ctr[C_ABORT], kAbortRecords);
 }
 
-// CTA = 32 x 8 pixel tile. The tile's rays run their DDA into shared memory: a
-// local table of the distinct blocks they visit, the visit records and per-block
-// voxel masks (smem atomics). Global work is then one hash find-or-insert per
-// distinct block (in parallel across threads) and one RED.OR per non-empty mask
-// word, instead of serialized global round trips per ray.
+// CTA = one 32 x 8 pixel tile of frame g. The tile's rays run their DDA into shared memory:
+// a local table of the distinct blocks they visit, per-block voxel masks (smem atomics) and
+// the staged fallback visits. Global work is then one hash find-or-insert per distinct block
+// (in parallel across threads) and two atomics per non-empty mask word, instead of global
+// round trips per visit.
 #ifndef SVX_TILE_U
 #define SVX_TILE_U 32
 #endif
@@ -449,30 +542,32 @@ constexpr int kLocalKeys = 256;
 constexpr int kTileFb = SVX_TILE_FB;  // staged fallback visits per tile
 
 __global__ void __launch_bounds__(kTileU * kTileV, 4)
-k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __restrict__ normals,
-               const uint8_t* __restrict__ valid, const double* __restrict__ dirs,
-               const uint8_t* __restrict__ hd, const uint32_t* __restrict__ validbits,
-               PixCache* __restrict__ cache, HashView h,
-               uint64_t* __restrict__ block_keys, uint32_t* __restrict__ stamp,
-               uint32_t* __restrict__ touched, uint32_t* __restrict__ vmask,
-               uint32_t* __restrict__ fbcnt, FbRec* __restrict__ rec,
-               svx_tsdf_voxel* __restrict__ pool, uint8_t* __restrict__ dirty,
-               unsigned long long* __restrict__ vlist, uint32_t* __restrict__ ctr) {
+k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
+       uint64_t* __restrict__ block_keys, uint32_t* __restrict__ stamp, uint32_t* __restrict__ touched,
+       uint32_t* __restrict__ fm, uint32_t* __restrict__ fbcnt, unsigned long long* __restrict__ rec,
+       svx_tsdf_voxel* __restrict__ pool, unsigned long long* __restrict__ wlist,
+       uint32_t* __restrict__ fctr, uint32_t* __restrict__ ctr) {
     pdl_wait();
     pdl_trigger();
-    // pool exhaustion raised by this frame does not stop its band: the frame
-    // resumes after its band
-    if (cta_aborted_for(ctr, kAbortPool, f.frame_serial)) return;
+    if (cta_aborted(ctr)) return;  // the group is rolled back and retried: stop early
+    const GroupConsts& c = gp.c;
+    __shared__ FramePose s_f;
     __shared__ unsigned long long lkey[kLocalKeys];
     __shared__ uint32_t lslot[kLocalKeys];
     __shared__ uint32_t lidx[kLocalKeys];
     __shared__ uint32_t lmask[kLocalKeys][16];
     __shared__ uint32_t lfb[kTileFb];
-    __shared__ uint32_t lcnt[kLocalKeys];  // kept fallback records per local block
+    __shared__ uint32_t lcnt[kLocalKeys];  // fallback records per local block
     __shared__ uint32_t lnew[kLocalKeys];  // pool indices of blocks this tile created
     __shared__ uint32_t nfb, nnew;
     const int tid = threadIdx.x;
-    const uint32_t blocks_before = ctr[C_BLOCKS_BEFORE];
+    const uint32_t g = blockIdx.x / c.tiles;
+    const uint32_t tile = blockIdx.x - g * c.tiles;
+    {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(&gp.f[g]);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(&s_f);
+        for (int i = tid; i < int(sizeof(FramePose) / 4); i += kTileU * kTileV) dst[i] = src[i];
+    }
     lkey[tid] = kEmptyKey;
     lcnt[tid] = 0u;
 #pragma unroll
@@ -480,23 +575,28 @@ k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __re
     if (tid == 0) nfb = nnew = 0;
     __syncthreads();
 
-    const int tiles_u = (f.m.W + kTileU - 1) / kTileU;
-    const int tu = int(blockIdx.x) % tiles_u, tv = int(blockIdx.x) / tiles_u;
+    const uint64_t pg = uint64_t(g) * c.P;
+    const float* depth = sc.depth + pg;
+    const uint8_t* hd = sc.rowdist + pg;
+    const uint32_t* validbits = sc.validbits + uint64_t(g) * c.VW;
+    PixCache* cache = reinterpret_cast<PixCache*>(sc.cache) + pg;
+    const int tiles_u = (c.m.W + kTileU - 1) / kTileU;
+    const int tu = int(tile) % tiles_u, tv = int(tile) / tiles_u;
     const int u = tu * kTileU + (tid % kTileU);
     const int v = tv * kTileV + (tid / kTileU);
-    const uint32_t tile_p0 = uint32_t(tv * kTileV) * uint32_t(f.m.W) + uint32_t(tu * kTileU);
-    const bool has_pix = u < f.m.W && v < f.m.H;
-    const uint32_t p = has_pix ? uint32_t(v) * uint32_t(f.m.W) + uint32_t(u) : 0u;
+    const uint32_t tile_p0 = uint32_t(tv * kTileV) * uint32_t(c.m.W) + uint32_t(tu * kTileU);
+    const bool has_pix = u < c.m.W && v < c.m.H;
+    const uint32_t p = has_pix ? uint32_t(v) * uint32_t(c.m.W) + uint32_t(u) : 0u;
     const float r = has_pix ? depth[p] : 0.f;
-    const bool in_range = has_pix && !(r == 0.f || double(r) > f.max_range);
-    const bool have_normal = has_pix && f.has_normals && valid[p];
+    const bool in_range = has_pix && !(r == 0.f || double(r) > c.max_range);
+    const bool have_normal = has_pix && c.has_normals && sc.valid[pg + p];
     // pixel cache (measure lambda inputs, tsdf_integrator.cpp:173-186)
     d3 q = mk(0, 0, 0), ray = mk(0, 0, 0);
     if (has_pix) {
         PixCache pc{};
         if (in_range) {
-            q = xform(f.pose, scale3(double(r), dir_at(dirs, p)));
-            const d3 dq = sub3(q, f.origin);
+            q = xform(s_f.pose, scale3(double(r), dir_at(sc.dirs, p)));
+            const d3 dq = sub3(q, s_f.origin);
             const double range = sqrt(dot3(dq, dq));
             ray = div3(dq, range);
             pc.ray[0] = ray.x;
@@ -504,27 +604,21 @@ k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __re
             pc.ray[2] = ray.z;
             pc.range = range;
             if (have_normal) {
-                const d3 n = matvec(f.pose.R, mk(normals[3 * p], normals[3 * p + 1], normals[3 * p + 2]));
+                const float* nn = sc.normals + 3 * (pg + p);
+                const d3 n = matvec(s_f.pose.R, mk(nn[0], nn[1], nn[2]));
                 pc.n[0] = float(n.x);
                 pc.n[1] = float(n.y);
                 pc.n[2] = float(n.z);
             }
-            pc.flags = ((have_normal || !f.drop_unreliable) ? 1u : 0u) | (have_normal ? 2u : 0u);
+            pc.flags = ((have_normal || !c.drop_unreliable) ? 1u : 0u) | (have_normal ? 2u : 0u);
         }
         cache[p] = pc;
     }
     // band ray (tsdf_integrator.cpp:123-131)
-#ifdef SVX_DIAG_NODDA  // timing diagnostic builds only (results invalid)
-    const bool cast = false;
-#else
-    const bool cast = in_range && !(f.drop_unreliable && f.has_normals && !valid[p]);
-#endif
-#ifdef SVX_DIAG_NOVISIT
-    uint32_t diag_sink = 0;
-#endif
+    const bool cast = in_range && !(c.drop_unreliable && c.has_normals && !sc.valid[pg + p]);
     if (cast) {
-        warp_agg_inc(&ctr[C_RAYS]);
-        const d3 tr = scale3(f.tau, ray);  // (q - o).normalized() == (q - o) / range
+        warp_agg_inc(&fctr[g * kFC + FC_RAYS]);
+        const d3 tr = scale3(c.tau, ray);  // (q - o).normalized() == (q - o) / range
         const d3 a = sub3(q, tr), b = add3(q, tr);
         uint64_t cur_key = kEmptyKey;
         int cur_li = -1;
@@ -534,12 +628,8 @@ k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __re
         int32_t x0 = 0, y0 = 0, z0 = 0;
         float p0x = 0.f, p0y = 0.f, p0z = 0.f;
         bool first = true;
-        const bool all_own = band_all_own(f, hd, p, r);
-        traverse_segment<true>(a, b, f.nu, f.inv_nu, [&](int32_t x, int32_t y, int32_t z) {
-#ifdef SVX_DIAG_NOVISIT
-            diag_sink += uint32_t(x ^ y ^ z);
-            return;
-#endif
+        const bool all_own = band_all_own(c, hd, p, r);
+        traverse_segment<true>(a, b, c.nu, c.inv_nu, [&](int32_t x, int32_t y, int32_t z) {
             const int32_t bx = block_coord(x), by = block_coord(y), bz = block_coord(z);
             if (!key_in_range(bx) || !key_in_range(by) || !key_in_range(bz)) {
                 atomicOr(&ctr[C_ABORT], kAbortKey);
@@ -548,7 +638,7 @@ k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __re
             const uint64_t key = pack_key(bx, by, bz);
             if (key != cur_key) {
                 cur_key = key;
-                cur_own = !(f.shard_world > 1 && owner_of(key, f.shard_world) != f.shard_rank);
+                cur_own = !(c.shard_world > 1 && owner_of(key, c.shard_world) != c.shard_rank);
                 cur_li = -1;
                 if (cur_own) {  // local table insert (open addressing in smem)
                     uint32_t s = hash_slot(key, 8);
@@ -568,7 +658,7 @@ k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __re
             bool fb = false;
             if (!all_own) {
                 if (first) {
-                    const d3 pc0 = xform(f.w2s, voxel_center(x, y, z, f.nu));
+                    const d3 pc0 = xform(s_f.w2s, voxel_center(x, y, z, c.nu));
                     p0x = float(pc0.x);
                     p0y = float(pc0.y);
                     p0z = float(pc0.z);
@@ -578,19 +668,15 @@ k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __re
                     first = false;
                 }
                 const float kx = float(x - x0), ky = float(y - y0), kz = float(z - z0);
-                const float px = p0x + kx * f.col[0][0] + ky * f.col[1][0] + kz * f.col[2][0];
-                const float py = p0y + kx * f.col[0][1] + ky * f.col[1][1] + kz * f.col[2][1];
-                const float pz = p0z + kx * f.col[0][2] + ky * f.col[1][2] + kz * f.col[2][2];
-                uint32_t own = pixel_fast(px, py, pz, f.m, f.m.r2_lo, f.m.r2_hi);
-                if (own == kNeedFp64) own = pixel_fp64(xform(f.w2s, voxel_center(x, y, z, f.nu)), f.m);
+                const float px = p0x + kx * s_f.col[0][0] + ky * s_f.col[1][0] + kz * s_f.col[2][0];
+                const float py = p0y + kx * s_f.col[0][1] + ky * s_f.col[1][1] + kz * s_f.col[2][1];
+                const float pz = p0z + kx * s_f.col[0][2] + ky * s_f.col[1][2] + kz * s_f.col[2][2];
+                uint32_t own = pixel_fast(px, py, pz, c.m, c.m.r2_lo, c.m.r2_hi);
+                if (own == kNeedFp64) own = pixel_fp64(xform(s_f.w2s, voxel_center(x, y, z, c.nu)), c.m);
                 fb = own == kInvalid || !pixel_has_return(validbits, own);
             }
             if (cur_li < 0) {  // local table full: straight to global state
-#ifdef SVX_DIAG_NOGLOBAL
-                return;  // diagnostic build only: drop table-overflow visits
-#endif
-                visit_global(f, h, block_keys, stamp, touched, vmask, fbcnt, rec, pool, cache, dirty,
-                             vlist, blocks_before, ctr, key, lin, fb, p);
+                visit_global(c, g, h, block_keys, stamp, touched, fm, fbcnt, rec, pool, wlist, ctr, key, lin, fb, p);
                 return;
             }
             const int word = cur_li * 16 + (lin >> 5);
@@ -605,149 +691,91 @@ k_raycast_band(FrameParams f, const float* __restrict__ depth, const float* __re
                 if (pos < uint32_t(kTileFb))
                     lfb[pos] = (uint32_t(cur_li) << 24) | (uint32_t(lin) << 15) | uint32_t(tid);
                 else
-                    visit_global(f, h, block_keys, stamp, touched, vmask, fbcnt, rec, pool, cache,
-                                 dirty, vlist, blocks_before, ctr, key, lin, true, p);
+                    visit_global(c, g, h, block_keys, stamp, touched, fm, fbcnt, rec, pool, wlist, ctr, key, lin,
+                                 true, p);
             }
         });
         if (pend_word >= 0) atomicOr(&lmask[0][0] + pend_word, pend_bits);
-#ifdef SVX_DIAG_NOVISIT
-        if (diag_sink == 0xFFFFFFFFu) atomicOr(&ctr[C_ABORT], 0u);
-#endif
     }
     __syncthreads();
-    // one global hash operation per distinct block of the tile; first touches of
-    // the frame are appended to the touched list with one atomic per tile
+    // one global hash operation per distinct block of the tile; first touches of the
+    // group are appended to the touched list with one atomic per tile
     constexpr int kW = kTileU * kTileV / 32;
     __shared__ uint32_t s_w[2 * kW];
-    uint32_t slot = kInvalid;
+    uint32_t slot = kInvalid, idx = kInvalid;
     bool first_touch = false;
     if (lkey[tid] != kEmptyKey) {
-        const SlotRef r = find_or_insert(f, h, block_keys, ctr, lkey[tid]);
-        slot = r.slot;
-        if (slot != kInvalid) {
-            first_touch = atomicExch(&stamp[slot], f.frame_serial) != f.frame_serial;
-            lidx[tid] = r.idx;
-            if (r.idx < f.max_blocks) {
-                dirty[r.idx] = 1;
-                if (r.inserted && r.idx < ctr[C_MAPPED]) lnew[atomicAdd(&nnew, 1u)] = r.idx;
-            } else {
-                slot = kInvalid;  // capacity abort is set; nothing below may touch the pool
-                first_touch = false;
-            }
+        const SlotRef sr = find_or_insert(c, h, block_keys, ctr, lkey[tid]);
+        if (sr.slot != kInvalid) {
+            slot = sr.slot;
+            idx = sr.idx;
+            first_touch = atomicExch(&stamp[slot], c.serial) != c.serial;
+            atomicOr(&fm[uint64_t(idx) * kMaskWords + kHdrRow * 16], 1u << g);
+            if (sr.inserted) lnew[atomicAdd(&nnew, 1u)] = idx;
         }
     }
     lslot[tid] = slot;
+    lidx[tid] = idx;
     const uint32_t tpos = cta_append<kW>(first_touch, &ctr[C_TOUCHED], s_w);
     if (first_touch) touched[tpos] = slot;
-    // zero-fill the blocks this tile created (read from the next kernel on)
+    // zero-fill the blocks this tile created (read from the fold on)
     for (uint32_t j = 0; j < nnew; ++j) zero_block(pool, lnew[j], tid, kTileU * kTileV);
-    // fallback visits: measured here (the rays' pixel cache entries were written
-    // above by this CTA); records that contribute are appended with one atomic per
-    // round, and counted per block with one atomic per block
+    // staged fallback visits -> records (slot, voxel, frame, pixel), counted per block
     const uint32_t nf = min(nfb, uint32_t(kTileFb));
-    for (uint32_t i0 = 0; i0 < nf; i0 += kTileU * kTileV) {
-        const uint32_t i = i0 + uint32_t(tid);
-        FbRec r{};
-        bool keep = false;
-        uint32_t li = 0;
-        if (i < nf) {
-            const uint32_t e = lfb[i];
-            li = e >> 24;
-            r.slot = lslot[li];
-            if (r.slot != kInvalid) {
-                const uint32_t t = e & 255u;
-                const uint32_t px = tile_p0 + (t / kTileU) * uint32_t(f.m.W) + (t % kTileU);
-                const int lin = int((e >> 15) & 511u);
-                r.t = fallback_term(f, h, pool, cache, blocks_before, r.slot, lkey[li], lin, px);
-                r.key = (uint32_t(lin) << 23) | px;
-                keep = r.t.flags & 1u;
-            }
-        }
-        const uint32_t pos = cta_append<kW>(keep, &ctr[C_RECORDS], s_w);
-        if (keep) {
-            atomicAdd(&lcnt[li], 1u);
-            if (pos < f.rec_cap) store_record(rec, pos, r);
-            else atomicOr(&ctr[C_ABORT], kAbortRecords);
-        }
+    uint32_t nrec = 0;
+    for (uint32_t i = tid; i < nf; i += kTileU * kTileV) nrec += lslot[lfb[i] >> 24] != kInvalid ? 1u : 0u;
+    uint32_t rpos = cta_reserve<kW>(nrec, &ctr[C_RECORDS], s_w);
+    if (nrec && rpos + nrec > c.rec_cap) atomicOr(&ctr[C_ABORT], kAbortRecords);
+    for (uint32_t i = tid; i < nf; i += kTileU * kTileV) {
+        const uint32_t e = lfb[i], li = e >> 24;
+        const uint32_t sl = lslot[li];
+        if (sl == kInvalid) continue;
+        const uint32_t t = e & 255u;
+        const uint32_t px = tile_p0 + (t / kTileU) * uint32_t(c.m.W) + (t % kTileU);
+        if (rpos < c.rec_cap) rec[rpos] = make_record(sl, int((e >> 15) & 511u), g, px);
+        ++rpos;
+        atomicAdd(&lcnt[li], 1u);
     }
-    // voxel masks -> this frame's half of the global mask words; the bits a tile
-    // sets first (atomicOr returns them clear) are its voxels' single entries in
-    // the frame's touched-voxel list
-    uint32_t nv = 0;
+    // voxel masks -> the frame's row and the union row of each block; the union words a
+    // tile sets first (the atomic returns them clear) are the group's word list
+    uint32_t nw = 0;
     for (int i = tid; i < kLocalKeys * 16; i += kTileU * kTileV) {
         const int li = i >> 4, w = i & 15;
-        uint32_t bits = lmask[li][w];
-        if (bits && lslot[li] != kInvalid) {
-            const uint32_t old = atomicOr(&vmask[uint64_t(lslot[li]) * 32 + f.parity * 16 + w], bits);
-            bits &= ~old;
-        } else {
-            bits = 0u;
+        const uint32_t bits = lmask[li][w];
+        uint32_t take = 0;
+        if (bits && lidx[li] != kInvalid) {
+            uint32_t* bm = fm + uint64_t(lidx[li]) * kMaskWords;
+            atomicOr(&bm[(1 + g) * 16 + w], bits);
+            take = atomicOr(&bm[w], bits) == 0u ? 1u : 0u;
         }
-        lmask[li][w] = bits;
-        nv += __popc(bits);
+        lmask[li][w] = take;
+        nw += take;
     }
-    uint32_t pos = cta_reserve<kW>(nv, &ctr[C_VOXLIST], s_w);
-    if (nv && pos + nv > f.vox_cap) atomicOr(&ctr[C_ABORT], kAbortVoxList);
-    for (int i = tid; i < kLocalKeys * 16 && nv; i += kTileU * kTileV) {
+    uint32_t pos = cta_reserve<kW>(nw, &ctr[C_WORDS], s_w);
+    if (nw && pos + nw > c.word_cap) atomicOr(&ctr[C_ABORT], kAbortWords);
+    for (int i = tid; i < kLocalKeys * 16 && nw; i += kTileU * kTileV) {
         const int li = i >> 4, w = i & 15;
-        const unsigned long long hi = static_cast<unsigned long long>(lidx[li]) << 9;
-        for (uint32_t bits = lmask[li][w]; bits; bits &= bits - 1, ++pos)
-            if (pos < f.vox_cap) vlist[pos] = hi | (uint32_t(w) * 32u + uint32_t(__ffs(bits) - 1));
+        if (!lmask[li][w]) continue;
+        if (pos < c.word_cap) wlist[pos] = (static_cast<unsigned long long>(lidx[li]) << 4) | uint32_t(w);
+        ++pos;
     }
     __syncthreads();  // lcnt complete
     if (lcnt[tid]) atomicAdd(&fbcnt[lslot[tid]], lcnt[tid]);
 }
 
-// One thread per touched voxel: own pixel, measure, fold. A list entry holds the
-// pool index and the voxel, so the voxel and its block key load in parallel.
-// The same kernel clears the previous frame's half of the mask words (the next
-// frame uses it) and moves the fallback records into per-block buckets; a
-// block's bucket is allocated by the first of its records to arrive.
+// Fallback records into per-block buckets; a block's bucket is allocated by the first of
+// its records to arrive.
 __global__ void __launch_bounds__(kThreads)
-k_fold(FrameParams f, const uint32_t* __restrict__ validbits, const PixCache* __restrict__ cache,
-       const uint64_t* __restrict__ block_keys, svx_tsdf_voxel* __restrict__ pool,
-       const unsigned long long* __restrict__ vlist, const uint32_t* __restrict__ touched_prev,
-       uint32_t* __restrict__ vmask, const FbRec* __restrict__ rec,
-       const uint32_t* __restrict__ fbcnt, uint32_t* __restrict__ fbstart,
-       uint32_t* __restrict__ fbclaim, uint32_t* __restrict__ fbfill,
-       uint32_t* __restrict__ fbslots, FbRec* __restrict__ bucket, uint32_t* __restrict__ ctr) {
+k_fb_bucket(const unsigned long long* __restrict__ rec, uint32_t rec_cap, const uint32_t* __restrict__ fbcnt,
+            uint32_t* __restrict__ fbstart, uint32_t* __restrict__ fbclaim, uint32_t* __restrict__ fbfill,
+            uint32_t* __restrict__ fbslots, unsigned long long* __restrict__ bucket, uint32_t* __restrict__ ctr) {
     pdl_wait();
     pdl_trigger();
     if (ctr[C_ABORT]) return;
-    const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    {
-        const uint32_t n_prev = ctr[C_TOUCHED_PREV];
-        const uint32_t other = (f.parity ^ 1u) * 16u;
-        for (uint32_t i = gtid; i < n_prev * 16u; i += stride)
-            vmask[uint64_t(touched_prev[i >> 4]) * 32 + other + (i & 15u)] = 0u;
-    }
-    const uint32_t nv = min(ctr[C_VOXLIST], f.vox_cap);
-    uint32_t n_upd = 0;
-    for (uint32_t i = gtid; i < nv; i += stride) {
-        const unsigned long long v = vlist[i];
-        const uint64_t idx = v >> 9;
-        const int linear = int(v & 511u);
-        svx_tsdf_voxel* vp = pool + idx * kBlockVoxels + linear;
-        const uint64_t key = block_keys[idx];
-        svx_tsdf_voxel vox = load_voxel(vp);
-        const d3 c = center_of(key, linear, f.nu);
-        const uint32_t own = own_pixel(f, xform(f.w2s, c));
-        if (own == kInvalid || !pixel_has_return(validbits, own)) continue;  // fallback path
-        const Term t = measure_term(f, cache, own, c, vox);
-        if (t.flags & 1u) {
-            Accum acc{0.0, 0.0, 0.0, 0.0, 0.0};
-            accumulate(acc, t);
-            fold(vox, acc);
-            store_voxel(vp, vox);
-            ++n_upd;
-        }
-    }
-    const uint32_t nr = min(ctr[C_RECORDS], f.rec_cap);
-    for (uint32_t i = gtid; i < nr; i += stride) {
-        const uint4* src = reinterpret_cast<const uint4*>(rec + i);
-        const uint4 a = src[0], b = src[1];
-        const uint32_t slot = a.y;
+    const uint32_t nr = min(ctr[C_RECORDS], rec_cap);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += gridDim.x * blockDim.x) {
+        const unsigned long long r = rec[i];
+        const uint32_t slot = uint32_t(r >> 41);
         uint32_t start = __ldcg(&fbstart[slot]);
         if (start == kInvalid) {
             if (atomicCAS(&fbclaim[slot], 0u, 1u) == 0u) {  // this record allocates the bucket
@@ -755,158 +783,95 @@ k_fold(FrameParams f, const uint32_t* __restrict__ validbits, const PixCache* __
                 fbslots[atomicAdd(&ctr[C_FB_BLOCKS], 1u)] = slot;
                 atomicExch(&fbstart[slot], start);
             } else {
-                while ((start = *reinterpret_cast<volatile uint32_t*>(&fbstart[slot])) == kInvalid)
-                    __nanosleep(32);
+                while ((start = *reinterpret_cast<volatile uint32_t*>(&fbstart[slot])) == kInvalid) __nanosleep(32);
             }
         }
-        const uint32_t pos = start + atomicAdd(&fbfill[slot], 1u);
-        uint4* dst = reinterpret_cast<uint4*>(bucket + pos);
-        dst[0] = a;
-        dst[1] = b;
+        bucket[start + atomicAdd(&fbfill[slot], 1u)] = r;
     }
-    for (int o = 16; o; o >>= 1) n_upd += __shfl_xor_sync(0xFFFFFFFFu, n_upd, o);
-    if ((threadIdx.x & 31) == 0 && n_upd) atomicAdd(&ctr[C_UPDATED], n_upd);
 }
 
-__device__ void write_frame_end(FrameOut* __restrict__ out, uint32_t* __restrict__ ctr) {
-    FrameOut o;
-    o.updated = ctr[C_UPDATED];
-    o.new_blocks = ctr[C_BLOCKS] - ctr[C_BLOCKS_BEFORE];
-    o.touched = ctr[C_TOUCHED];
-    o.records = ctr[C_RECORDS];
-    o.rays = ctr[C_RAYS];
-    o.dropped = ctr[C_DROPPED];
-    o.fb_voxels = ctr[C_FB_VOXELS];
-    o.ok = 1;
-    *out = o;
-    ctr[C_TOUCHED_PREV] = ctr[C_TOUCHED];
-    ctr[C_TOUCHED] = ctr[C_UPDATED] = ctr[C_RECORDS] = ctr[C_RAYS] = 0;
-    ctr[C_DROPPED] = ctr[C_TIES] = ctr[C_FB_BLOCKS] = ctr[C_FB_VOXELS] = ctr[C_FB_BIG] = 0;
-    ctr[C_VOXLIST] = ctr[C_BUCKET_TOP] = 0;
-    ctr[C_BLOCKS_BEFORE] = ctr[C_BLOCKS];
+template <int kThr>
+__device__ inline void load_poses(const GroupParams& gp, FramePose* s_f) {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(&gp.f[0]);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(s_f);
+    const int n = int(gp.c.G * (sizeof(FramePose) / 4));
+    for (int i = threadIdx.x; i < n; i += kThr) dst[i] = src[i];
 }
 
-__device__ inline Term record_term(const FbRec* __restrict__ r) {
-    const uint4* q = reinterpret_cast<const uint4*>(r);
-    const uint4 a = q[0], b = q[1];
-    Term t;
-    t.wg = __uint_as_float(a.z);
-    t.w = __uint_as_float(a.w);
-    t.nx = __uint_as_float(b.x);
-    t.ny = __uint_as_float(b.y);
-    t.nz = __uint_as_float(b.z);
-    t.flags = b.w;
-    return t;
-}
-
-// Ordered fold of one fallback voxel: the terms of records bucket[src[i..end)],
-// summed in that order (ascending pixel). Loads are issued four at a time so the
-// sequential sum does not pay one L2 round trip per record.
-template <typename Src>
-__device__ inline bool fold_records(svx_tsdf_voxel* vp, const FbRec* __restrict__ bucket,
-                                    const Src* __restrict__ src, uint32_t i, uint32_t end) {
-    if (i == end) return false;
-    Accum acc{0.0, 0.0, 0.0, 0.0, 0.0};
-    uint32_t j = i;
-    for (; j + 4 <= end; j += 4) {
-        const Term t0 = record_term(bucket + src[j]), t1 = record_term(bucket + src[j + 1]);
-        const Term t2 = record_term(bucket + src[j + 2]), t3 = record_term(bucket + src[j + 3]);
-        accumulate(acc, t0);
-        accumulate(acc, t1);
-        accumulate(acc, t2);
-        accumulate(acc, t3);
-    }
-    for (; j < end; ++j) accumulate(acc, record_term(bucket + src[j]));
-    svx_tsdf_voxel vox = load_voxel(vp);
-    fold(vox, acc);
-    store_voxel(vp, vox);
-    return true;
-}
-
-// CTA per block with fallback records (the records cluster on few blocks, e.g. on
-// the ring where the lowest beam meets the ground). Records arrive measured; the
-// bucket is ordered by (voxel, pixel) in shared memory: counting sort by voxel
-// (histogram, scan, scatter), then inside each voxel's segment a rank sort (the
-// rank of a record is the number of smaller keys in its segment; keys are unique,
-// a ray visits a voxel once), all in parallel. One thread per voxel then folds it
-// with the terms summed strictly in that order.
-__global__ void __launch_bounds__(kFbThreads)
-k_fb_fold(HashView h, svx_tsdf_voxel* __restrict__ pool, const uint32_t* __restrict__ fbslots,
-          uint32_t* __restrict__ fbcnt, uint32_t* __restrict__ fbstart,
-          uint32_t* __restrict__ fbclaim, uint32_t* __restrict__ fbfill,
-          const FbRec* __restrict__ bucket, uint32_t* __restrict__ bigslots,
-          FrameOut* __restrict__ out, uint32_t serial, uint32_t* __restrict__ ctr) {
+// CTA per block with fallback records. The bucket is ordered by (voxel, frame, pixel):
+// counting sort by voxel (histogram, scan, scatter to the sort scratch), then inside each
+// voxel's segment a rank sort (keys are unique: a ray visits a voxel once per frame), in
+// parallel. One thread per such voxel then applies every frame of the group to it, the
+// fallback frames with their visiting rays summed strictly in ascending pixel order.
+__global__ void __launch_bounds__(kThreads)
+k_fb_fold(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
+          const uint64_t* __restrict__ block_keys, svx_tsdf_voxel* __restrict__ pool,
+          const uint32_t* __restrict__ fm, const uint32_t* __restrict__ fbslots, uint32_t* __restrict__ fbcnt,
+          uint32_t* __restrict__ fbstart, uint32_t* __restrict__ fbclaim, uint32_t* __restrict__ fbfill,
+          unsigned long long* __restrict__ bucket, unsigned long long* __restrict__ bucket2,
+          uint32_t* __restrict__ fctr, uint32_t* __restrict__ ctr) {
     pdl_wait();
     pdl_trigger();
-    // a big bucket (host-sorted afterwards) of this frame must not stop its other buckets
-    if (cta_aborted_for(ctr, kAbortBigBucket, serial)) return;
-    using Scan = cub::BlockScan<uint32_t, kFbThreads>;
-    constexpr int kPer = kBlockVoxels / kFbThreads;  // voxels per thread in the scan
+    if (cta_aborted(ctr)) return;
+    const GroupConsts& c = gp.c;
+    using Scan = cub::BlockScan<uint32_t, kThreads>;
+    constexpr int kPer = kBlockVoxels / kThreads;  // voxels per thread in the scan
     __shared__ typename Scan::TempStorage scan_tmp;
-    __shared__ uint32_t keys[kFbMax];   // grouped by voxel
-    __shared__ uint16_t src1[kFbMax];   // record index of keys[i]
-    __shared__ uint16_t src2[kFbMax];   // record indices in (voxel, pixel) order
+    __shared__ FramePose s_f[kMaxG];
     __shared__ uint32_t seg_start[kBlockVoxels], seg_cnt[kBlockVoxels], cursor[kBlockVoxels];
-    __shared__ bool last;
+    __shared__ uint32_t s_upd[kMaxG], s_fbv[kMaxG];
+    load_poses<kThreads>(gp, s_f);
+    if (threadIdx.x < kMaxG) s_upd[threadIdx.x] = s_fbv[threadIdx.x] = 0u;
     const uint32_t nb = ctr[C_FB_BLOCKS];
-    uint32_t n_upd = 0;
     for (uint32_t t = blockIdx.x; t < nb; t += gridDim.x) {
         const uint32_t slot = fbslots[t];
         const uint32_t cnt = fbcnt[slot];
         const uint32_t start = fbstart[slot];
-        if (cnt > uint32_t(kFbMax)) {
-            if (threadIdx.x == 0) {
-                bigslots[atomicAdd(&ctr[C_FB_BIG], 1u)] = slot;
-                raise_frame_abort(ctr, kAbortBigBucket, serial);
-            }
-            continue;
-        }
-#ifdef SVX_DEBUG_CHECKS
-        if (threadIdx.x == 0 && (start == kInvalid || slot > h.mask || start + cnt > ctr[C_BUCKET_TOP] ||
-                                 h.vals[slot] == kInvalid)) {
-            printf("k_fb_fold: t %u/%u slot %u cnt %u start %u top %u val %u serial %u\n", t, nb, slot, cnt,
-                   start, ctr[C_BUCKET_TOP], h.vals[slot], serial);
-            __trap();
-        }
-#endif
-        const FbRec* bk = bucket + start;
-        for (int v = threadIdx.x; v < kBlockVoxels; v += kFbThreads) seg_cnt[v] = 0u;
+        const uint32_t idx = h.vals[slot];
+        unsigned long long* bk = bucket + start;
+        unsigned long long* tmp = bucket2 + start;
+        for (int v = threadIdx.x; v < kBlockVoxels; v += kThreads) seg_cnt[v] = 0u;
         __syncthreads();
-        for (uint32_t i = threadIdx.x; i < cnt; i += kFbThreads) atomicAdd(&seg_cnt[bk[i].key >> 23], 1u);
+        for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) atomicAdd(&seg_cnt[rec_lin(bk[i])], 1u);
         __syncthreads();
         {   // exclusive scan of the per-voxel counts -> segment starts
-            uint32_t c[kPer];
+            uint32_t cc[kPer];
 #pragma unroll
-            for (int j = 0; j < kPer; ++j) c[j] = seg_cnt[threadIdx.x * kPer + j];
-            Scan(scan_tmp).ExclusiveSum(c, c);
+            for (int j = 0; j < kPer; ++j) cc[j] = seg_cnt[threadIdx.x * kPer + j];
+            Scan(scan_tmp).ExclusiveSum(cc, cc);
 #pragma unroll
             for (int j = 0; j < kPer; ++j) {
-                seg_start[threadIdx.x * kPer + j] = c[j];
-                cursor[threadIdx.x * kPer + j] = c[j];
+                seg_start[threadIdx.x * kPer + j] = cc[j];
+                cursor[threadIdx.x * kPer + j] = cc[j];
             }
         }
         __syncthreads();
-        for (uint32_t i = threadIdx.x; i < cnt; i += kFbThreads) {
-            const uint32_t k = bk[i].key;
-            const uint32_t d = atomicAdd(&cursor[k >> 23], 1u);
-            keys[d] = k;
-            src1[d] = uint16_t(i);
+        for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
+            const unsigned long long k = bk[i];
+            tmp[atomicAdd(&cursor[rec_lin(k)], 1u)] = k;
         }
         __syncthreads();
-        for (uint32_t i = threadIdx.x; i < cnt; i += kFbThreads) {
-            const uint32_t k = keys[i], v = k >> 23;
+        for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
+            const unsigned long long k = tmp[i];
+            const int v = rec_lin(k);
             const uint32_t b = seg_start[v], e = b + seg_cnt[v];
+            const uint32_t lo = uint32_t(k);  // (frame, pixel)
             uint32_t r = 0;
-            for (uint32_t j = b; j < e; ++j) r += keys[j] < k ? 1u : 0u;
-            src2[b + r] = src1[i];
+            for (uint32_t j = b; j < e; ++j) r += uint32_t(tmp[j]) < lo ? 1u : 0u;
+            bk[b + r] = k;
         }
         __syncthreads();
-        svx_tsdf_voxel* blk = pool + uint64_t(h.vals[slot]) * kBlockVoxels;
-        for (int v = threadIdx.x; v < kBlockVoxels; v += kFbThreads) {
-            const uint32_t b = seg_start[v];
-            n_upd += fold_records(blk + v, bk, src2, b, b + seg_cnt[v]) ? 1u : 0u;
+        const uint64_t key = block_keys[idx];
+        svx_tsdf_voxel* blk = pool + uint64_t(idx) * kBlockVoxels;
+        for (int v = threadIdx.x; v < kBlockVoxels; v += kThreads) {
+            if (!seg_cnt[v]) continue;
+            const uint32_t frames = voxel_frames(fm, idx, v, c.G);
+            const uint32_t upd = fold_voxel<true>(c, s_f, frames, blk + v, center_of(key, v, c.nu), sc,
+                                                  bk + seg_start[v], seg_cnt[v]);
+            for (uint32_t u = upd; u; u &= u - 1) atomicAdd(&s_upd[__ffs(u) - 1], 1u);
+            for (uint32_t u = frames; u; u &= u - 1) atomicAdd(&s_fbv[__ffs(u) - 1], 1u);
         }
-        if (threadIdx.x == 0) {  // per-slot fallback state, clean for the next frame
+        if (threadIdx.x == 0) {  // per-slot fallback state, clean for the next group
             fbcnt[slot] = 0u;
             fbstart[slot] = kInvalid;
             fbclaim[slot] = 0u;
@@ -914,93 +879,157 @@ k_fb_fold(HashView h, svx_tsdf_voxel* __restrict__ pool, const uint32_t* __restr
         }
         __syncthreads();  // shared arrays are reused by the next bucket
     }
-    for (int o = 16; o; o >>= 1) n_upd += __shfl_xor_sync(0xFFFFFFFFu, n_upd, o);
-    if ((threadIdx.x & 31) == 0 && n_upd) {
-        atomicAdd(&ctr[C_UPDATED], n_upd);
-        atomicAdd(&ctr[C_FB_VOXELS], n_upd);
+    __syncthreads();
+    if (threadIdx.x < c.G) {
+        if (s_upd[threadIdx.x]) atomicAdd(&fctr[threadIdx.x * kFC + FC_UPD], s_upd[threadIdx.x]);
+        if (s_fbv[threadIdx.x]) atomicAdd(&fctr[threadIdx.x * kFC + FC_FBV], s_fbv[threadIdx.x]);
     }
-    // the last CTA to finish writes the frame report
+}
+
+// Warp per 32 listed mask words, lane per visited voxel (the words' set bits expanded
+// across the warp with a shuffle search). Then the group's end: dirty flags and per-frame
+// touched / new block counts over the touched list; the last CTA writes the reports.
+__global__ void __launch_bounds__(kThreads)
+k_fold(const __grid_constant__ GroupParams gp, const ScanSlots sc, const uint32_t* __restrict__ vals,
+       const uint64_t* __restrict__ block_keys, svx_tsdf_voxel* __restrict__ pool, uint32_t* __restrict__ fm,
+       const unsigned long long* __restrict__ wlist, const uint32_t* __restrict__ touched,
+       uint8_t* __restrict__ dirty, uint32_t* __restrict__ fctr, FrameOut* __restrict__ outs,
+       uint32_t* __restrict__ ctr) {
+    pdl_wait();
+    pdl_trigger();
+    if (cta_aborted(ctr)) return;
+    const GroupConsts& c = gp.c;
+    __shared__ FramePose s_f[kMaxG];
+    __shared__ uint32_t s_upd[kMaxG], s_touch[kMaxG], s_new[kMaxG];
+    __shared__ bool last;
+    load_poses<kThreads>(gp, s_f);
+    if (threadIdx.x < kMaxG) s_upd[threadIdx.x] = s_touch[threadIdx.x] = s_new[threadIdx.x] = 0u;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t nw = min(ctr[C_WORDS], c.word_cap);
+    for (uint32_t base = warp * 32; base < nw; base += nwarps * 32) {
+        const uint32_t i = base + lane;
+        const bool valid = i < nw;
+        const unsigned long long e = valid ? wlist[i] : 0ull;
+        const uint32_t idx = uint32_t(e >> 4), w = uint32_t(e) & 15u;
+        const uint32_t bits = valid ? fm[uint64_t(idx) * kMaskWords + w] : 0u;
+        const uint32_t cnt = __popc(bits);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        for (uint32_t k0 = 0; k0 < total; k0 += 32) {
+            const uint32_t k = k0 + uint32_t(lane);
+            // owner lane of voxel k: the first lane whose inclusive count exceeds k
+            int o = 0;
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1) {
+                const uint32_t y = __shfl_sync(0xFFFFFFFFu, incl, o + s - 1);
+                if (y <= k) o += s;
+            }
+            const uint32_t ob = __shfl_sync(0xFFFFFFFFu, bits, o);
+            const uint32_t obase = __shfl_sync(0xFFFFFFFFu, incl - cnt, o);
+            const unsigned long long oe = __shfl_sync(0xFFFFFFFFu, e, o);
+            uint32_t upd = 0;
+            if (k < total) {
+                const uint32_t oidx = uint32_t(oe >> 4);
+                const int lin = int((uint32_t(oe) & 15u) * 32u + select_bit(ob, k - obase));
+                const uint32_t frames = voxel_frames(fm, oidx, lin, c.G);
+                upd = fold_voxel<false>(c, s_f, frames, pool + uint64_t(oidx) * kBlockVoxels + lin,
+                                        center_of(block_keys[oidx], lin, c.nu), sc, nullptr, 0);
+                if (upd == kFallback) upd = 0;  // k_fb_fold applied this voxel
+            }
+            for (uint32_t gg = 0; gg < c.G; ++gg) {
+                const uint32_t n = __popc(__ballot_sync(0xFFFFFFFFu, (upd >> gg) & 1u));
+                if (lane == 0 && n) atomicAdd(&s_upd[gg], n);
+            }
+        }
+        __syncwarp();
+        if (valid) {  // this warp's words are done: clean for the next group
+            uint32_t* bm = fm + uint64_t(idx) * kMaskWords + w;
+            bm[0] = 0u;
+            for (uint32_t gg = 0; gg < c.G; ++gg) bm[16 * (1 + gg)] = 0u;
+        }
+    }
+    // group end: dirty blocks (tsdf_integrator.cpp:160-168 pushes every visited block),
+    // per-frame touched blocks and new blocks (a block new to the map is new in the first
+    // frame of the group that visits it)
+    const uint32_t nt = ctr[C_TOUCHED];
+    const uint32_t before = ctr[C_BLOCKS_BEFORE];
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+        const uint32_t idx = vals[touched[t]];
+        dirty[idx] = 1;
+        uint32_t* hdr = fm + uint64_t(idx) * kMaskWords + kHdrRow * 16;
+        const uint32_t ft = *hdr;
+        *hdr = 0u;
+        for (uint32_t u = ft; u; u &= u - 1) atomicAdd(&s_touch[__ffs(u) - 1], 1u);
+        if (idx >= before && ft) atomicAdd(&s_new[__ffs(ft) - 1], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < c.G) {
+        const uint32_t g = threadIdx.x;
+        if (s_upd[g]) atomicAdd(&fctr[g * kFC + FC_UPD], s_upd[g]);
+        if (s_touch[g]) atomicAdd(&fctr[g * kFC + FC_TOUCH], s_touch[g]);
+        if (s_new[g]) atomicAdd(&fctr[g * kFC + FC_NEW], s_new[g]);
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
         last = atomicAdd(&ctr[C_DONE], 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (last && threadIdx.x == 0) {
-        __threadfence();
+    if (!last) return;
+    __threadfence();
+    if (threadIdx.x < c.G) {
+        const uint32_t g = threadIdx.x;
+        uint32_t* fc = fctr + g * kFC;
+        FrameOut o;
+        o.updated = __ldcg(&fc[FC_UPD]);
+        o.new_blocks = __ldcg(&fc[FC_NEW]);
+        o.touched = __ldcg(&fc[FC_TOUCH]);
+        o.records = ctr[C_RECORDS];
+        o.rays = __ldcg(&fc[FC_RAYS]);
+        o.dropped = __ldcg(&fc[FC_DROPPED]);
+        o.fb_voxels = __ldcg(&fc[FC_FBV]);
+        o.ok = 1;
+        outs[g] = o;
+        for (int k = 0; k < kFC; ++k) fc[k] = 0u;
+    }
+    if (threadIdx.x == 0) {
         ctr[C_DONE] = 0;
-        if (!atomicAdd(&ctr[C_ABORT], 0u)) write_frame_end(out, ctr);
+        ctr[C_TOUCHED] = ctr[C_RECORDS] = ctr[C_WORDS] = ctr[C_FB_BLOCKS] = ctr[C_BUCKET_TOP] = 0;
+        ctr[C_BLOCKS_BEFORE] = ctr[C_BLOCKS];
     }
 }
 
-// Big buckets (more records than k_fb_fold orders in shared memory): keys and
-// record indices sorted by CUB on the device, then one thread per voxel segment.
-__global__ void k_fb_extract(const FbRec* __restrict__ bk, uint32_t cnt, uint32_t* __restrict__ keys,
-                             uint32_t* __restrict__ idx) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= cnt) return;
-    keys[i] = bk[i].key;
-    idx[i] = i;
-}
-
-__global__ void k_fb_fold_sorted(HashView h, svx_tsdf_voxel* __restrict__ pool, uint32_t slot,
-                                 const FbRec* __restrict__ bk, const uint32_t* __restrict__ keys,
-                                 const uint32_t* __restrict__ idx, uint32_t cnt,
-                                 uint32_t* __restrict__ ctr) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= cnt || !(i == 0 || (keys[i] >> 23) != (keys[i - 1] >> 23))) return;
-    uint32_t end = i + 1;
-    while (end < cnt && (keys[end] >> 23) == (keys[i] >> 23)) ++end;
-    svx_tsdf_voxel* blk = pool + uint64_t(h.vals[slot]) * kBlockVoxels;
-    if (fold_records(blk + (keys[i] >> 23), bk, idx, i, end)) {
-        atomicAdd(&ctr[C_UPDATED], 1u);
-        atomicAdd(&ctr[C_FB_VOXELS], 1u);
-    }
-}
-
-__global__ void k_frame_end(FrameOut* __restrict__ out, uint32_t* __restrict__ ctr) {
-    // trigger first: the next frame's projection may launch (its pre-wait part reads
-    // only its own points) while this frame's last kernel drains
-    pdl_trigger();
-    pdl_wait();
-    if (ctr[C_ABORT]) return;
-    write_frame_end(out, ctr);
-}
-
-// Undo the per-frame record state before re-running the band kernel of a frame.
-// (fallback counts and this frame's half of the mask words of its touched blocks)
-__global__ void k_reset_fb(const uint32_t* __restrict__ touched, uint32_t* __restrict__ fbcnt,
-                           uint32_t* __restrict__ vmask, uint32_t parity, uint32_t* __restrict__ ctr) {
-    const uint32_t n = ctr[C_TOUCHED];
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n * 16u; i += gridDim.x * blockDim.x) {
-        const uint32_t slot = touched[i >> 4];
-        if ((i & 15u) == 0) fbcnt[slot] = 0;
-        vmask[uint64_t(slot) * 32 + parity * 16 + (i & 15u)] = 0u;
-    }
-}
-
-// Capacity path: every visited block key of the frame (duplicates allowed).
+// Capacity path: every visited block key of frame slot 0 (duplicates allowed).
 __global__ void __launch_bounds__(kThreads)
-k_collect_keys(FrameParams f, const float* __restrict__ depth, const uint8_t* __restrict__ valid,
-               const double* __restrict__ dirs, unsigned long long* __restrict__ out,
+k_collect_keys(const __grid_constant__ GroupParams gp, const ScanSlots sc, unsigned long long* __restrict__ out,
                uint32_t cap, uint32_t* __restrict__ ctr) {
+    const GroupConsts& c = gp.c;
+    const FramePose& f = gp.f[0];
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= uint32_t(f.m.W) * uint32_t(f.m.H)) return;
-    const float r = depth[p];
-    if (r == 0.f || double(r) > f.max_range) return;
-    if (f.drop_unreliable && f.has_normals && !valid[p]) return;
-    const d3 q = xform(f.pose, scale3(double(r), dir_at(dirs, p)));
+    if (p >= uint32_t(c.m.W) * uint32_t(c.m.H)) return;
+    const float r = sc.depth[p];
+    if (r == 0.f || double(r) > c.max_range) return;
+    if (c.drop_unreliable && c.has_normals && !sc.valid[p]) return;
+    const d3 q = xform(f.pose, scale3(double(r), dir_at(sc.dirs, p)));
     const d3 dq = sub3(q, f.origin);
     const d3 ray = div3(dq, sqrt(dot3(dq, dq)));
-    const d3 tr = scale3(f.tau, ray);
+    const d3 tr = scale3(c.tau, ray);
     uint64_t cur_key = kEmptyKey;
-    traverse_segment(sub3(q, tr), add3(q, tr), f.nu, f.inv_nu, [&](int32_t x, int32_t y, int32_t z) {
+    traverse_segment(sub3(q, tr), add3(q, tr), c.nu, c.inv_nu, [&](int32_t x, int32_t y, int32_t z) {
         const int32_t bx = block_coord(x), by = block_coord(y), bz = block_coord(z);
         if (!key_in_range(bx) || !key_in_range(by) || !key_in_range(bz)) return;
         const uint64_t key = pack_key(bx, by, bz);
         if (key == cur_key) return;
         cur_key = key;
-        if (f.shard_world > 1 && owner_of(key, f.shard_world) != f.shard_rank) return;
+        if (c.shard_world > 1 && owner_of(key, c.shard_world) != c.shard_rank) return;
         const uint32_t pos = atomicAdd(&ctr[C_RECORDS], 1u);
         if (pos < cap) out[pos] = key;
     });
@@ -1016,59 +1045,66 @@ __global__ void k_mark_dirty(const uint64_t* __restrict__ keys_sorted, uint32_t 
 
 inline unsigned grid_for(uint64_t n) { return unsigned((n + kThreads - 1) / kThreads); }
 
-FrameParams make_params(svx_map* m, svx_scan* s, const Pose& pose, const svx_integrator_cfg& cfg,
-                        uint32_t parity) {
-    FrameParams f{};
-    f.parity = parity & 1u;
-    f.m = s->dm;
+GroupConsts make_consts(svx_map* m, svx_scan* s, const svx_integrator_cfg& cfg, uint32_t G, bool has_normals) {
+    GroupConsts c{};
+    c.m = s->dm;
+    const double nu = double(m->cfg.voxel_size);
+    c.tau = cfg.truncation > 0.f ? double(cfg.truncation) : double(m->cfg.truncation);
+    c.max_range = cfg.max_range;
+    c.alpha_eps = cfg.alpha_epsilon;
+    if (!(cfg.alpha_epsilon > 0.0)) {  // alpha < eps never holds
+        c.ca_hi = c.ca_lo = 2.0;
+    } else if (cfg.alpha_epsilon > kPi) {  // always holds (alpha <= pi)
+        c.ca_hi = c.ca_lo = -2.0;
+    } else {
+        c.ca_hi = std::cos(cfg.alpha_epsilon) + 1e-12;
+        c.ca_lo = std::cos(cfg.alpha_epsilon) - 1e-12;
+    }
+    c.min_clamp = cfg.min_weight_clamp;
+    c.nonproj = cfg.mode == SVX_NON_PROJECTIVE;
+    c.drop_unreliable = cfg.drop_unreliable != 0;
+    c.has_normals = has_normals;
+    c.nu = nu;
+    c.inv_nu = 1.0 / nu;
+    c.delta = float(0.8660254037844386 * nu * (1.0 + 1e-6)) + 1e-6f;
+    c.min_range_safe = float(s->model.min_range * (1.0 + 1e-4)) + 1e-4f;
+    {
+        const double t0 = s->model.theta0, t1 = s->model.theta0 + s->model.height_px * s->model.delta_theta;
+        // polar range inside (0, pi): sin is smallest at an end of the range
+        c.sin_min = (t0 > 0.0 && t1 < kPi) ? float(std::min(std::sin(t0), std::sin(t1)) - 1e-6) : 0.f;
+    }
+    c.dphi_f = float(s->model.delta_phi * (1.0 - 1e-6));
+    c.dtheta_f = float(s->model.delta_theta * (1.0 - 1e-6));
+    c.shard_rank = m->shard_rank;
+    c.shard_world = m->shard_world;
+    c.serial = ++m->frame_serial;
+    c.G = G;
+    c.P = uint32_t(s->P);
+    c.VW = uint32_t(s->VW);
+    c.tiles = uint32_t(((s->dm.W + kTileU - 1) / kTileU) * ((s->dm.H + kTileV - 1) / kTileV));
+    c.max_blocks = m->cfg.max_blocks;
+    c.rec_cap = m->rec_cap;
+    c.word_cap = m->word_cap;
+    return c;
+}
+
+FramePose make_pose(svx_map* m, const Pose& pose) {
+    FramePose f{};
     f.pose = pose;
     f.w2s = inverse_pose(pose);
     f.origin = mk(pose.t[0], pose.t[1], pose.t[2]);
     const double nu = double(m->cfg.voxel_size);
-    for (int a = 0; a < 3; ++a)        // world axis
-        for (int i = 0; i < 3; ++i)    // sensor component: (R^T)_{i a} = R_{a i}
+    for (int a = 0; a < 3; ++a)      // world axis
+        for (int i = 0; i < 3; ++i)  // sensor component: (R^T)_{i a} = R_{a i}
             f.col[a][i] = float(nu * pose.R[3 * a + i]);
-    f.tau = cfg.truncation > 0.f ? double(cfg.truncation) : double(m->cfg.truncation);
-    f.max_range = cfg.max_range;
-    f.alpha_eps = cfg.alpha_epsilon;
-    if (!(cfg.alpha_epsilon > 0.0)) {  // alpha < eps never holds
-        f.ca_hi = f.ca_lo = 2.0;
-    } else if (cfg.alpha_epsilon > kPi) {  // always holds (alpha <= pi)
-        f.ca_hi = f.ca_lo = -2.0;
-    } else {
-        f.ca_hi = std::cos(cfg.alpha_epsilon) + 1e-12;
-        f.ca_lo = std::cos(cfg.alpha_epsilon) - 1e-12;
-    }
-    f.min_clamp = cfg.min_weight_clamp;
-    f.nonproj = cfg.mode == SVX_NON_PROJECTIVE;
-    f.drop_unreliable = cfg.drop_unreliable != 0;
-    f.has_normals = s->has_normals;
-    f.nu = nu;
-    f.inv_nu = 1.0 / nu;
-    f.delta = float(0.8660254037844386 * nu * (1.0 + 1e-6)) + 1e-6f;
-    f.min_range_safe = float(s->model.min_range * (1.0 + 1e-4)) + 1e-4f;
-    {
-        const double t0 = s->model.theta0, t1 = s->model.theta0 + s->model.height_px * s->model.delta_theta;
-        // polar range inside (0, pi): sin is smallest at an end of the range
-        f.sin_min = (t0 > 0.0 && t1 < kPi) ? float(std::min(std::sin(t0), std::sin(t1)) - 1e-6) : 0.f;
-    }
-    f.dphi_f = float(s->model.delta_phi * (1.0 - 1e-6));
-    f.dtheta_f = float(s->model.delta_theta * (1.0 - 1e-6));
-    f.shard_rank = m->shard_rank;
-    f.shard_world = m->shard_world;
-    f.frame_serial = ++m->frame_serial;
-    f.max_blocks = m->cfg.max_blocks;
-    f.rec_cap = m->rec_cap;
-    f.vox_cap = m->vox_cap;
     return f;
 }
 
-// Stages of one frame: 0 band, 1 fold, 2 fallback (+ report), 3 report only.
-enum { kStageBand = 0, kStageFold = 1, kStageFallback = 2, kStageReport = 3 };
+ScanSlots scan_slots(svx_scan* s) {
+    return ScanSlots{s->depth.p, s->normals.p, s->valid.p, s->dirs.p, s->rowdist.p, s->validbits.p, s->pixcache.p};
+}
 
-// k_fold's grid: exactly one wave of resident CTAs (register-limited to 4 per SM),
-// each thread striding over ~4 listed voxels. Measured on cfg2: 41 -> 37 us per frame
-// against two waves (persistent_grid), 43 us at 2/3 of a wave, 49 us at half a wave.
+// k_fold's grid: one wave of resident CTAs.
 unsigned fold_grid(int device) {
     static int grid[64] = {0};
     if (!grid[device]) {
@@ -1080,63 +1116,47 @@ unsigned fold_grid(int device) {
     return unsigned(grid[device]);
 }
 
-void launch_stages(svx_map* m, svx_scan* s, const FrameParams& f, int from, FrameOut* out) {
-    const uint32_t P = uint32_t(s->P);
+// Enqueues the TSDF kernels of one group (the frames' images are in the scan's slots).
+void launch_group_kernels(svx_map* m, svx_scan* s, const GroupParams& gp, FrameOut* outs) {
+    const GroupConsts& c = gp.c;
     HashView hv = hash_view(m);
-    const PixCache* cache = reinterpret_cast<const PixCache*>(s->pixcache.p);
+    const ScanSlots sc = scan_slots(s);
     const unsigned pg = persistent_grid(m->device);
-    uint32_t* touched_cur = m->touched + uint64_t(f.parity) * m->cap;
-    uint32_t* touched_prev = m->touched + uint64_t(f.parity ^ 1u) * m->cap;
-    if (from <= kStageBand) {
+    uint32_t* fm = mask_base(m);
+    {
         ProfMark pm(m, SVX_K_RAYCAST);
-        if (!s->rowdist_fresh) {  // host-provided depth: the projection did not build it
-            launch_pdl(k_row_dist, grid_for(P), kThreads, m->stream, s->depth.p, s->dm.W, s->dm.H,
-                       s->rowdist.p, s->validbits.p, m->d_ctr);
-            count_launch();
-            s->rowdist_fresh = true;
-        }
-        const unsigned tiles = unsigned(((s->dm.W + kTileU - 1) / kTileU) * ((s->dm.H + kTileV - 1) / kTileV));
-        launch_pdl(k_raycast_band, tiles, 256, m->stream, f, s->depth.p, s->normals.p, s->valid.p,
-                   s->dirs.p, s->rowdist.p, s->validbits.p, reinterpret_cast<PixCache*>(s->pixcache.p), hv,
-                   m->block_keys,
-                   m->stamp, touched_cur, m->vmask, m->fbcnt, reinterpret_cast<FbRec*>(m->records.p),
-                   tsdf_base(m), m->dirty, m->vlist.p, m->d_ctr);
+        launch_pdl(k_band, c.G * c.tiles, kTileU * kTileV, m->stream, gp, sc, hv, m->block_keys, m->stamp,
+                   m->touched, fm, m->fbcnt, m->records.p, tsdf_base(m), m->wlist.p, m->fctr, m->d_ctr);
         count_launch();
     }
-    if (from <= kStageFold) {
-        ProfMark pm(m, SVX_K_FOLD);
-        launch_pdl(k_fold, fold_grid(m->device), kThreads, m->stream, f, s->validbits.p, cache,
-                   m->block_keys, tsdf_base(m),
-                   m->vlist.p, touched_prev, m->vmask, reinterpret_cast<const FbRec*>(m->records.p),
-                   m->fbcnt, m->fbstart, m->fbclaim, m->fbfill, m->fbslots,
-                   reinterpret_cast<FbRec*>(m->bucket.p), m->d_ctr);
-        count_launch();
-    }
-    if (from <= kStageFallback) {
+    {
         ProfMark pm(m, SVX_K_FALLBACK);
-        // pg / 2 CTAs: measured on cfg2, pg / 4 is equal, pg, pg / 8 and pg / 16 are slower
-        launch_pdl(k_fb_fold, pg / 2, kFbThreads, m->stream, hv, tsdf_base(m), m->fbslots, m->fbcnt,
-                   m->fbstart, m->fbclaim, m->fbfill, reinterpret_cast<const FbRec*>(m->bucket.p),
-                   m->bigslots, out, f.frame_serial, m->d_ctr);
-        count_launch();
-    } else {
-        launch_pdl(k_frame_end, 1, 1, m->stream, out, m->d_ctr);
+        launch_pdl(k_fb_bucket, pg / 4, kThreads, m->stream, m->records.p, m->rec_cap, m->fbcnt, m->fbstart,
+                   m->fbclaim, m->fbfill, m->fbslots, m->bucket.p, m->d_ctr);
+        launch_pdl(k_fb_fold, pg / 2, kThreads, m->stream, gp, sc, hv, m->block_keys, tsdf_base(m), fm,
+                   m->fbslots, m->fbcnt, m->fbstart, m->fbclaim, m->fbfill, m->bucket.p, m->bucket2.p, m->fctr,
+                   m->d_ctr);
+        count_launch(2);
+    }
+    {
+        ProfMark pm(m, SVX_K_FOLD);
+        launch_pdl(k_fold, fold_grid(m->device), kThreads, m->stream, gp, sc, m->vals, m->block_keys, tsdf_base(m),
+                   fm, m->wlist.p, m->touched, m->dirty, m->fctr, outs, m->d_ctr);
         count_launch();
     }
     SVX_CUDA(cudaGetLastError());
 }
 
-// CapacityError path (tsdf_integrator.cpp:160-168 + voxel_store.cpp:18-20):
-// blocks are allocated in sorted key order until max_blocks is reached; every
-// block before the failing one is marked dirty; no voxel is updated.
-[[noreturn]] void capacity_path(svx_map* m, const FrameParams& f, svx_scan* s, uint32_t before) {
+// CapacityError path (tsdf_integrator.cpp:160-168 + voxel_store.cpp:18-20) for the single
+// frame in slot 0: blocks are allocated in sorted key order until max_blocks is reached;
+// every block before the failing one is marked dirty; no voxel is updated.
+[[noreturn]] void capacity_path(svx_map* m, svx_scan* s, const GroupParams& gp, uint32_t before) {
     uint32_t cap = uint32_t(std::min<uint64_t>(uint64_t(s->P) * 64, 1u << 30));
     for (;;) {
         m->records_alt.alloc(cap);
         SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_RECORDS, 0, 4, m->stream));
-        k_collect_keys<<<grid_for(s->P), kThreads, 0, m->stream>>>(f, s->depth.p, s->valid.p,
-                                                                   s->dirs.p, m->records_alt.p,
-                                                                   cap, m->d_ctr);
+        k_collect_keys<<<grid_for(s->P), kThreads, 0, m->stream>>>(gp, scan_slots(s), m->records_alt.p, cap,
+                                                                   m->d_ctr);
         count_launch();
         sync_counters(m);
         if (m->h_ctr[C_RECORDS] <= cap) break;
@@ -1144,8 +1164,7 @@ void launch_stages(svx_map* m, svx_scan* s, const FrameParams& f, int from, Fram
     }
     const uint32_t n = m->h_ctr[C_RECORDS];
     std::vector<unsigned long long> keys(n);
-    SVX_CUDA(cudaMemcpy(keys.data(), m->records_alt.p, sizeof(unsigned long long) * n,
-                        cudaMemcpyDeviceToHost));
+    SVX_CUDA(cudaMemcpy(keys.data(), m->records_alt.p, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost));
     std::sort(keys.begin(), keys.end());
     keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
     std::vector<unsigned long long> existing(before);
@@ -1166,59 +1185,23 @@ void launch_stages(svx_map* m, svx_scan* s, const FrameParams& f, int from, Fram
     const uint64_t total = before + alloc_new.size();
     ensure_blocks(m, total);
     if (!alloc_new.empty())
-        SVX_CUDA(cudaMemcpy(m->block_keys + before, alloc_new.data(),
-                            sizeof(unsigned long long) * alloc_new.size(), cudaMemcpyHostToDevice));
+        SVX_CUDA(cudaMemcpy(m->block_keys + before, alloc_new.data(), sizeof(unsigned long long) * alloc_new.size(),
+                            cudaMemcpyHostToDevice));
     m->n_blocks = total;
     rebuild_hash(m);
     launch_zero_blocks(m, before, alloc_new.size());
     reset_frame_state(m);
     if (!dirty_keys.empty()) {
         m->records_alt.alloc(dirty_keys.size());
-        SVX_CUDA(cudaMemcpy(m->records_alt.p, dirty_keys.data(),
-                            sizeof(unsigned long long) * dirty_keys.size(), cudaMemcpyHostToDevice));
+        SVX_CUDA(cudaMemcpy(m->records_alt.p, dirty_keys.data(), sizeof(unsigned long long) * dirty_keys.size(),
+                            cudaMemcpyHostToDevice));
         k_mark_dirty<<<grid_for(dirty_keys.size()), kThreads, 0, m->stream>>>(
-            reinterpret_cast<const uint64_t*>(m->records_alt.p), uint32_t(dirty_keys.size()),
-            hash_view(m), m->dirty);
+            reinterpret_cast<const uint64_t*>(m->records_alt.p), uint32_t(dirty_keys.size()), hash_view(m),
+            m->dirty);
         count_launch();
     }
     SVX_CUDA(cudaStreamSynchronize(m->stream));
-    throw Error(SVX_CAPACITY, "block budget exhausted (max_blocks = " +
-                                  std::to_string(m->cfg.max_blocks) + ")");
-}
-
-// Host side of kAbortBigBucket: each oversized bucket is ordered by a CUB pair
-// sort (key, record index) on the device and folded per voxel segment.
-void big_buckets(svx_map* m) {
-    const uint32_t nbig = m->h_ctr[C_FB_BIG];
-    std::vector<uint32_t> slots(nbig), cnt(nbig), start(nbig);
-    SVX_CUDA(cudaMemcpy(slots.data(), m->bigslots, 4 * nbig, cudaMemcpyDeviceToHost));
-    for (uint32_t i = 0; i < nbig; ++i) {
-        SVX_CUDA(cudaMemcpy(&cnt[i], m->fbcnt + slots[i], 4, cudaMemcpyDeviceToHost));
-        SVX_CUDA(cudaMemcpy(&start[i], m->fbstart + slots[i], 4, cudaMemcpyDeviceToHost));
-    }
-    const FbRec* bucket = reinterpret_cast<const FbRec*>(m->bucket.p);
-    DevBuf<uint32_t> buf;
-    for (uint32_t i = 0; i < nbig; ++i) {
-        const uint32_t n = cnt[i];
-        buf.alloc(4ull * n);
-        uint32_t *k_in = buf.p, *k_out = buf.p + n, *i_in = buf.p + 2ull * n, *i_out = buf.p + 3ull * n;
-        k_fb_extract<<<grid_for(n), kThreads, 0, m->stream>>>(bucket + start[i], n, k_in, i_in);
-        size_t bytes = 0;
-        SVX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k_in, k_out, i_in, i_out, int(n), 0, 32,
-                                                 m->stream));
-        m->sort_tmp.alloc(bytes ? bytes : 1);
-        SVX_CUDA(cub::DeviceRadixSort::SortPairs(m->sort_tmp.p, bytes, k_in, k_out, i_in, i_out, int(n),
-                                                 0, 32, m->stream));
-        k_fb_fold_sorted<<<grid_for(n), kThreads, 0, m->stream>>>(
-            hash_view(m), tsdf_base(m), slots[i], bucket + start[i], k_out, i_out, n, m->d_ctr);
-        count_launch(2);
-        SVX_CUDA(cudaMemsetAsync(m->fbcnt + slots[i], 0, 4, m->stream));
-        SVX_CUDA(cudaMemsetAsync(m->fbclaim + slots[i], 0, 4, m->stream));
-        SVX_CUDA(cudaMemsetAsync(m->fbfill + slots[i], 0, 4, m->stream));
-        SVX_CUDA(cudaMemsetAsync(m->fbstart + slots[i], 0xFF, 4, m->stream));
-    }
-    SVX_CUDA(cudaStreamSynchronize(m->stream));
-    buf.release();
+    throw Error(SVX_CAPACITY, "block budget exhausted (max_blocks = " + std::to_string(m->cfg.max_blocks) + ")");
 }
 
 }  // namespace
@@ -1229,75 +1212,95 @@ unsigned persistent_grid(int device) {
     return unsigned(sms[device] * 8);  // 8 CTAs x 8 warps per SM
 }
 
-// Clears the frame scratch (masks, fallback counts, per-frame counters) after a
+// Clears the group scratch (masks of the mapped blocks, fallback state, counters) after a
 // host-side intervention, and re-arms the device block counters.
 void reset_frame_state(svx_map* m) {
-    SVX_CUDA(cudaMemsetAsync(m->vmask, 0, sizeof(uint32_t) * 32ull * m->cap, m->stream));
+    if (m->mapped_blocks)
+        SVX_CUDA(cudaMemsetAsync(mask_base(m), 0, 4ull * kMaskWords * m->mapped_blocks, m->stream));
     SVX_CUDA(cudaMemsetAsync(m->fbcnt, 0, sizeof(uint32_t) * m->cap, m->stream));
     SVX_CUDA(cudaMemsetAsync(m->fbclaim, 0, sizeof(uint32_t) * m->cap, m->stream));
     SVX_CUDA(cudaMemsetAsync(m->fbfill, 0, sizeof(uint32_t) * m->cap, m->stream));
     SVX_CUDA(cudaMemsetAsync(m->fbstart, 0xFF, sizeof(uint32_t) * m->cap, m->stream));
-    for (int c : {C_TOUCHED, C_UPDATED, C_RECORDS, C_RAYS, C_DROPPED, C_TIES, C_FB_BLOCKS,
-                  C_FB_VOXELS, C_FB_BIG, C_ABORT, C_VOXLIST, C_BUCKET_TOP, C_DONE, C_TOUCHED_PREV})
+    SVX_CUDA(cudaMemsetAsync(m->fctr, 0, sizeof(uint32_t) * kMaxG * kFC, m->stream));
+    for (int c : {C_TOUCHED, C_UPDATED, C_RECORDS, C_RAYS, C_DROPPED, C_TIES, C_FB_BLOCKS, C_FB_VOXELS, C_FB_BIG,
+                  C_ABORT, C_WORDS, C_BUCKET_TOP, C_DONE})
         m->h_ctr[c] = 0;
     m->h_ctr[C_BLOCKS] = m->h_ctr[C_BLOCKS_BEFORE] = uint32_t(m->n_blocks);
     m->h_ctr[C_MAPPED] = uint32_t(m->mapped_blocks);
-    SVX_CUDA(cudaMemcpyAsync(m->d_ctr, m->h_ctr, sizeof(uint32_t) * kNumCounters,
-                             cudaMemcpyHostToDevice, m->stream));
+    SVX_CUDA(cudaMemcpyAsync(m->d_ctr, m->h_ctr, sizeof(uint32_t) * kNumCounters, cudaMemcpyHostToDevice,
+                             m->stream));
     SVX_CUDA(cudaStreamSynchronize(m->stream));
 }
 
 namespace {
-void put_ctr(svx_map* m, int c, uint32_t v) {
-    m->h_ctr[c] = v;
-    SVX_CUDA(cudaMemcpyAsync(m->d_ctr + c, &m->h_ctr[c], 4, cudaMemcpyHostToDevice, m->stream));
+
+// Undoes an aborted group: its new blocks (and their hash entries, dirty flags), the visit
+// masks and the rest of the group scratch (reset_frame_state); the scans' pixel keys are
+// reset (later groups of the batch did not run). The frames before it are complete.
+void rollback_group(svx_map* m, svx_scan* s, uint32_t before) {
+    const uint64_t hi = std::min<uint64_t>(m->h_ctr[C_BLOCKS], m->cfg.max_blocks);
+    if (hi > before) SVX_CUDA(cudaMemsetAsync(m->dirty + before, 0, hi - before, m->stream));
+    m->n_blocks = before;
+    rebuild_hash(m);
+    if (s->slots) {
+        SVX_CUDA(cudaMemsetAsync(s->pixkey.p, 0xFF, 16ull * s->P * s->slots, m->stream));
+        for (int g = 0; g < kMaxG; ++g) s->parity[g] = 0;
+    }
+    reset_frame_state(m);
 }
+
+// Frames per group: up to kMaxG, with at most ~4M pixels of frame slots.
+int group_cap(const svx_scan* s) {
+    const uint64_t by_mem = std::max<uint64_t>(1, (uint64_t(1) << 22) / uint64_t(std::max(1, s->P)));
+    return int(std::min<uint64_t>(kMaxG, by_mem));
+}
+
 }  // namespace
 
-void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cfg& cfg,
-                svx_frame_report* reps) {
+void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cfg& cfg, svx_frame_report* reps) {
     if (!(cfg.alpha_epsilon > 0.0)) throw Error(SVX_INVALID_ARGUMENT, "alpha_epsilon must be > 0");
     if (n <= 0) return;
+    svx_scan* s = jobs[0].scan;
     for (int i = 0; i < n; ++i) {
         reps[i].frame = -1;
         reps[i].updated_voxels = reps[i].new_blocks = 0;
-        if (!jobs[i].project && !jobs[i].scan->has_normals && cfg.mode == SVX_NON_PROJECTIVE)
+        if (jobs[i].scan != s) throw Error(SVX_INVALID_ARGUMENT, "a batch integrates the frames of one scan model");
+        if (!jobs[i].project && n != 1) throw Error(SVX_INVALID_ARGUMENT, "image frames are integrated one at a time");
+        if (!jobs[i].project && !s->has_normals && cfg.mode == SVX_NON_PROJECTIVE)
             throw Error(SVX_INVALID_ARGUMENT, "non-projective mode needs a normal image");
     }
+    if (uint64_t(s->P) >= (1ull << 28)) throw Error(SVX_INVALID_ARGUMENT, "scan image too large (>= 2^28 pixels)");
+    const bool project = jobs[0].project;
+    const bool ingest = jobs[0].host_ingest;
+    const int gcap = project ? group_cap(s) : 1;
+    const int gmax = std::min(gcap, n);
+    uint64_t nmax = 1, most = 1;
+    for (int i = 0; i < n; ++i) {
+        nmax = std::max<uint64_t>(nmax, jobs[i].n);
+        most = std::max<uint64_t>(most, jobs[i].n * uint64_t(jobs[i].stride));
+    }
+    ensure_scan_slots(s, gmax, project ? nmax : 0);
     m->outs.alloc(size_t(n));
-    // frame reports start "not done": the resume logic finds the aborted frame as the
-    // first report without ok (stale reports of an earlier batch must not count)
     SVX_CUDA(cudaMemsetAsync(m->outs.p, 0, sizeof(FrameOut) * size_t(n), m->stream));
     if (m->h_outs_n < size_t(n)) {
         if (m->h_outs) cudaFreeHost(m->h_outs);
         SVX_CUDA(cudaMallocHost(&m->h_outs, sizeof(FrameOut) * n));
         m->h_outs_n = size_t(n);
     }
-    // per-frame buffers sized for the largest scan of the batch
-    uint64_t pmax = 0, nmax = 0;
-    for (int i = 0; i < n; ++i) {
-        pmax = std::max<uint64_t>(pmax, uint64_t(jobs[i].scan->P));
-        nmax = std::max<uint64_t>(nmax, jobs[i].n);
-        if (jobs[i].project) jobs[i].scan->lexkey.alloc(std::min<uint64_t>(2 * jobs[i].n + 2, 0xFFFFFFF0ull));
+    // the word list of a group: at most one entry per 32-voxel word a ray visits
+    const uint64_t want_words = std::min<uint64_t>(uint64_t(s->P) * uint64_t(gmax) + 4096, 0xFFFFFFF0ull);
+    if (m->word_cap < want_words) {
+        m->word_cap = uint32_t(want_words);
+        m->wlist.alloc(m->word_cap);
     }
-    if (m->vox_cap < 16 * pmax) {
-        m->vox_cap = uint32_t(std::min<uint64_t>(16 * pmax, 0xFFFFFFF0ull));
-        m->vlist.alloc(m->vox_cap);
-    }
-    // pool headroom for the whole batch (an overflow aborts and resumes below)
-    // (an exhausted headroom costs one abort + resume; over-mapping costs physical
-    // memory and cuMemCreate time, so size it from the recent new-block rate)
-    const uint64_t head = m->test_pool_head ? m->test_pool_head
-                                            : std::max<uint64_t>(32768, uint64_t(2.0 * m->new_ema * n));
+    // pool headroom for the batch (an exhausted headroom costs one rollback + retry; over-
+    // mapping costs physical memory and cuMemCreate time, so size it from the recent rate)
+    const uint64_t head =
+        m->test_pool_head ? m->test_pool_head : std::max<uint64_t>(32768, uint64_t(2.0 * m->new_ema * n));
     ensure_blocks(m, m->n_blocks + head, 4 * head);
-    std::vector<FrameParams> fps(n);
-    std::vector<int> parity(n, 0);
-    std::vector<char> launched(n, 0);
-    // host ingest ring: frame i's points go to slot i % R on the copy stream, at most
-    // R - 1 frames ahead of the frame being launched; a slot is refilled only after
-    // the projection of the frame that used it (event ingest_used)
+    // host ingest ring: group k's points are copied to staging slot k % R on the copy stream
+    // while group k - 1 integrates
     constexpr int R = svx_map::kIngestSlots;
-    const bool ingest = jobs[0].host_ingest;
     if (ingest) {
         if (!m->copy_stream) {
             SVX_CUDA(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking));
@@ -1306,21 +1309,18 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
                 SVX_CUDA(cudaEventCreateWithFlags(&m->ingest_used[r], cudaEventDisableTiming));
             }
         }
-        uint64_t most = 1;
-        for (int i = 0; i < n; ++i) most = std::max<uint64_t>(most, jobs[i].n * uint64_t(jobs[i].stride));
         for (int r = 0; r < R; ++r) {
-            m->ingest[r].alloc(most);
+            m->ingest[r].alloc(most * uint64_t(gmax));
             SVX_CUDA(cudaEventRecord(m->ingest_used[r], m->stream));
         }
     }
-    // fills the report of completed frame i (its FrameOut is final) and numbers it
     auto commit = [&](int i) {
         const FrameOut& o = m->h_outs[i];
         reps[i].frame = m->tsdf_frames++;
         reps[i].updated_voxels = o.updated;
         reps[i].new_blocks = o.new_blocks;
         m->new_ema = m->new_ema == 0.0 ? double(o.new_blocks) : 0.9 * m->new_ema + 0.1 * double(o.new_blocks);
-        jobs[i].scan->dropped = o.dropped;
+        s->dropped = o.dropped;
         m->prof_acc.frames += 1;
         m->prof_acc.rays += o.rays;
         m->prof_acc.touched_blocks += o.touched;
@@ -1328,130 +1328,109 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
         m->prof_acc.updated_voxels += o.updated;
         m->prof_acc.fallback_voxels += o.fb_voxels;
     };
-    int f0 = 0, stage0 = 0;
+    int f0 = 0;
+    int single_lo = 0, single_hi = 0;  // frames run one per group (after a capacity / key abort)
     for (;;) {
         const auto te0 = std::chrono::steady_clock::now();
-        int next_copy = f0;
-        for (int i = f0; i < n; ++i) {
-            const FrameJob& j = jobs[i];
-            const int from = i == f0 ? stage0 : 0;
-            const float* pts = j.pts;
-            if (ingest) {
-                for (; next_copy < n && next_copy < i + R; ++next_copy) {
-                    const FrameJob& c = jobs[next_copy];
-                    const int r = next_copy % R;
+        std::vector<int> starts;
+        GroupParams gp{};
+        int k = 0;
+        for (int a = f0; a < n; ++k) {
+            const int G = (a >= single_lo && a < single_hi) ? 1 : std::min(gcap, n - a);
+            starts.push_back(a);
+            gp.c = make_consts(m, s, cfg, uint32_t(G), project ? true : s->has_normals);
+            for (int g = 0; g < G; ++g) gp.f[g] = make_pose(m, jobs[a + g].pose);
+            if (project) {
+                const void* pts[kMaxG];
+                uint64_t cnt[kMaxG];
+                Pose poses[kMaxG];
+                const int r = k % R;
+                if (ingest) {  // stage the group's points (pinned host -> device) on the copy stream
                     SVX_CUDA(cudaStreamWaitEvent(m->copy_stream, m->ingest_used[r], 0));
-                    if (c.n)
-                        SVX_CUDA(cudaMemcpyAsync(m->ingest[r].p, c.pts, 4ull * c.n * c.stride,
-                                                 cudaMemcpyHostToDevice, m->copy_stream));
+                    uint64_t off = 0;
+                    for (int g = 0; g < G; ++g) {
+                        const FrameJob& j = jobs[a + g];
+                        if (j.n)
+                            SVX_CUDA(cudaMemcpyAsync(m->ingest[r].p + off, j.pts, 4ull * j.n * j.stride,
+                                                     cudaMemcpyHostToDevice, m->copy_stream));
+                        pts[g] = m->ingest[r].p + off;
+                        off += j.n * uint64_t(j.stride);
+                    }
                     SVX_CUDA(cudaEventRecord(m->ingest_ready[r], m->copy_stream));
+                    SVX_CUDA(cudaStreamWaitEvent(m->stream, m->ingest_ready[r], 0));
+                } else {
+                    for (int g = 0; g < G; ++g) pts[g] = jobs[a + g].pts;
                 }
-                SVX_CUDA(cudaStreamWaitEvent(m->stream, m->ingest_ready[i % R], 0));
-                pts = m->ingest[i % R].p;
-            }
-            if (!launched[i] || (i > f0)) {
-                if (j.project) {
-                    if (launched[i]) j.scan->parity = parity[i];
-                    parity[i] = j.scan->parity;
-                    launch_project(j.scan, pts, j.n, j.stride, j.pose);
-                    if (ingest) SVX_CUDA(cudaEventRecord(m->ingest_used[i % R], m->stream));
+                for (int g = 0; g < G; ++g) {
+                    cnt[g] = jobs[a + g].n;
+                    poses[g] = jobs[a + g].pose;
                 }
-                fps[i] = make_params(m, j.scan, j.pose, cfg, uint32_t(m->tsdf_frames + i));
-                launched[i] = 1;
+                launch_project_group(s, pts, cnt, G, jobs[a].stride, false, poses);
+                if (ingest) SVX_CUDA(cudaEventRecord(m->ingest_used[r], m->stream));
+            } else if (!s->rowdist_fresh) {  // images the caller uploaded into slot 0
+                launch_pdl(k_row_dist, grid_for(s->P), kThreads, m->stream, s->depth.p, s->dm.W, s->dm.H,
+                           s->rowdist.p, s->validbits.p, m->d_ctr);
+                count_launch();
+                s->rowdist_fresh = true;
             }
-            launch_stages(m, j.scan, fps[i], from, m->outs.p + i);
+            launch_group_kernels(m, s, gp, m->outs.p + a);
+            a += G;
         }
         if (m->prof)
             m->prof_acc.host_enqueue_ms +=
                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - te0).count();
-        SVX_CUDA(cudaMemcpyAsync(m->h_outs, m->outs.p, sizeof(FrameOut) * n,
-                                 cudaMemcpyDeviceToHost, m->stream));
+        SVX_CUDA(cudaMemcpyAsync(m->h_outs, m->outs.p, sizeof(FrameOut) * n, cudaMemcpyDeviceToHost, m->stream));
         sync_counters(m);
         if (ingest) SVX_CUDA(cudaStreamSynchronize(m->copy_stream));
         const uint32_t abort = m->h_ctr[C_ABORT];
         if (!abort) break;
         const auto tr0 = std::chrono::steady_clock::now();
         for (int b = 0; b < 8; ++b) m->prof_acc.aborts[b] += (abort >> b) & 1u;
-#ifdef SVX_DEBUG_CHECKS
-        std::fprintf(stderr, "abort %#x f0 %d blocks %u before %u mapped %u records %u rec_cap %u touched %u fbb %u top %u\n",
-                     abort, f0, m->h_ctr[C_BLOCKS], m->h_ctr[C_BLOCKS_BEFORE], m->h_ctr[C_MAPPED],
-                     m->h_ctr[C_RECORDS], m->rec_cap, m->h_ctr[C_TOUCHED], m->h_ctr[C_FB_BLOCKS],
-                     m->h_ctr[C_BUCKET_TOP]);
-#endif
-        // the first frame of this pass without a report is the one that aborted
-        int fa = f0;
-        while (fa < n && m->h_outs[fa].ok) ++fa;
-        if (fa >= n) fa = n - 1;
-        svx_scan* s = jobs[fa].scan;
+        // the first group whose frames have no report is the one that aborted
+        int ga = 0;
+        while (ga + 1 < int(starts.size()) && m->h_outs[starts[ga + 1] - 1].ok) ++ga;
+        const int fa = starts[ga];
+        const int fb = ga + 1 < int(starts.size()) ? starts[ga + 1] : n;
+        for (int i = f0; i < fa; ++i) commit(i);
         const uint32_t before = m->h_ctr[C_BLOCKS_BEFORE];
-        if (abort & kAbortKey) {
-            // like the capacity path: the frames before the failing one are complete
-            // (reported and numbered); the failing frame is numbered (the reference
-            // numbers a frame before it can throw) and leaves no block behind: its
-            // partially inserted blocks (possibly beyond the mapped, zero-filled pool)
-            // are dropped and their dirty flags cleared
-            for (int i = 0; i < fa; ++i) commit(i);
-            m->tsdf_frames++;
-            const uint64_t hi = std::min<uint64_t>(m->h_ctr[C_BLOCKS], m->cfg.max_blocks);
-            if (hi > before) SVX_CUDA(cudaMemsetAsync(m->dirty + before, 0, hi - before, m->stream));
-            m->n_blocks = before;
-            rebuild_hash(m);
-            reset_frame_state(m);
-            throw Error(SVX_INVALID_ARGUMENT,
-                        "block coordinate outside the device key range [-2^20, 2^20)");
-        }
-        if (abort & (kAbortCapacity | kAbortHash)) {
-            for (int i = 0; i < fa; ++i) commit(i);
-            m->tsdf_frames++;
-            m->n_blocks = before;
-            capacity_path(m, fps[fa], s, before);
-        }
-        int stage = kStageReport;
-        const uint32_t par = fps[fa].parity;
-        if (abort & (kAbortRecords | kAbortVoxList)) {
-            // grow the buffer and re-run the band kernel of this frame with a fresh
-            // stamp, after clearing what its first run left: this frame's mask
-            // words (so every voxel is listed again), fallback counts, counters
-            ensure_blocks(m, uint64_t(m->h_ctr[C_BLOCKS]) + head);
-            if (abort & kAbortRecords) {
-                m->rec_cap = std::max<uint32_t>(m->h_ctr[C_RECORDS] + (m->h_ctr[C_RECORDS] >> 1),
-                                                m->rec_cap * 2);
-                m->records.alloc(2ull * m->rec_cap);
-                m->bucket.alloc(2ull * m->rec_cap);
-                fps[fa].rec_cap = m->rec_cap;
-            }
-            if (abort & kAbortVoxList) {
-                m->vox_cap = uint32_t(std::min<uint64_t>(uint64_t(m->h_ctr[C_VOXLIST]) * 2, 0xFFFFFFF0ull));
-                m->vlist.alloc(m->vox_cap);
-                fps[fa].vox_cap = m->vox_cap;
-            }
-            k_reset_fb<<<256, kThreads, 0, m->stream>>>(m->touched + uint64_t(par) * m->cap, m->fbcnt,
-                                                        m->vmask, par, m->d_ctr);
-            count_launch();
-            // blocks created by the first run are found again (not created): zero them all here
-            launch_zero_blocks(m, before, uint64_t(m->h_ctr[C_BLOCKS]) - before);
-            fps[fa].frame_serial = ++m->frame_serial;
-            for (int c : {C_RECORDS, C_TOUCHED, C_VOXLIST}) put_ctr(m, c, 0);
-            stage = kStageBand;
-        } else if (abort & kAbortPool) {
-            // the band ran to completion; blocks beyond the mapped pool were not
-            // zero-filled: map more, zero all of the frame's new blocks, fold
-            ensure_blocks(m, uint64_t(m->h_ctr[C_BLOCKS]) + head);
-            launch_zero_blocks(m, before, uint64_t(m->h_ctr[C_BLOCKS]) - before);
-            stage = kStageFold;
-        } else if (abort & kAbortBigBucket) {
-            big_buckets(m);
-            put_ctr(m, C_DONE, 0);
-            stage = kStageReport;
-        }
-        put_ctr(m, C_ABORT, 0);
-        put_ctr(m, C_MAPPED, uint32_t(m->mapped_blocks));
+        const uint32_t blocks_seen = m->h_ctr[C_BLOCKS], recs_seen = m->h_ctr[C_RECORDS],
+                       words_seen = m->h_ctr[C_WORDS];
+        rollback_group(m, s, before);
         f0 = fa;
-        stage0 = stage;
+        if (abort & (kAbortCapacity | kAbortHash | kAbortKey)) {
+            if (fb - fa > 1) {  // find the failing frame: the group again, one frame at a time
+                single_lo = fa;
+                single_hi = fb;
+            } else if (abort & kAbortKey) {
+                // the failing frame is numbered (the reference numbers a frame before it can
+                // throw) and leaves no block behind (rolled back above)
+                m->tsdf_frames++;
+                throw Error(SVX_INVALID_ARGUMENT, "block coordinate outside the device key range [-2^20, 2^20)");
+            } else {
+                // the failing frame's images are in slot 0 (a group of one; its projection ran)
+                m->tsdf_frames++;
+                GroupParams g1{};
+                g1.c = make_consts(m, s, cfg, 1, project ? true : s->has_normals);
+                g1.f[0] = make_pose(m, jobs[fa].pose);
+                capacity_path(m, s, g1, before);
+            }
+        }
+        if (abort & kAbortPool) ensure_blocks(m, uint64_t(m->n_blocks) + 2 * head + (blocks_seen - before));
+        if (abort & kAbortRecords) {
+            m->rec_cap = std::max<uint32_t>(recs_seen + (recs_seen >> 1), m->rec_cap * 2);
+            m->records.alloc(m->rec_cap);
+            m->bucket.alloc(m->rec_cap);
+            m->bucket2.alloc(m->rec_cap);
+        }
+        if (abort & kAbortWords) {
+            m->word_cap = uint32_t(std::min<uint64_t>(uint64_t(words_seen) * 2, 0xFFFFFFF0ull));
+            m->wlist.alloc(m->word_cap);
+        }
+        SVX_CUDA(cudaMemsetAsync(m->outs.p, 0, sizeof(FrameOut) * size_t(n), m->stream));
         m->prof_acc.host_resume_ms +=
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tr0).count();
     }
-    for (int i = 0; i < n; ++i) commit(i);
+    for (int i = f0; i < n; ++i) commit(i);
     m->n_blocks = m->h_ctr[C_BLOCKS];
 }
 
