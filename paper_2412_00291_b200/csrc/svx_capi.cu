@@ -105,7 +105,8 @@ void free_map(svx_map* m) {
     m->outs.release();
     m->bucket.release();
     m->bucket2.release();
-    m->wlist.release();
+    m->fbdesc.release();
+    m->vlist.release();
     prof_resolve(m);
     for (cudaEvent_t e : m->prof_free) cudaEventDestroy(e);
     m->records.release();
@@ -170,6 +171,7 @@ svx_map* create_map(const svx_map_cfg& cfg, int device) {
         m->records.alloc(m->rec_cap);
         m->bucket.alloc(m->rec_cap);
         m->bucket2.alloc(m->rec_cap);
+        m->fbdesc.alloc(m->rec_cap);
         SVX_CUDA(cudaMallocHost(&m->h_ctr, sizeof(uint32_t) * kNumCounters));
         std::memset(m->h_ctr, 0, sizeof(uint32_t) * kNumCounters);
         SVX_CUDA(cudaMemsetAsync(m->keys, 0xFF, 8ull * m->cap, m->stream));

@@ -22,12 +22,22 @@ constexpr int kBlockVoxels = 512;
 // TSDF frames integrated together by one group of kernel launches (svx_tsdf.cu)
 constexpr int kMaxG = 16;
 // Per-block visit masks of a frame group (svx_tsdf.cu), 16 words (512 voxel bits) per row:
-// row 0 = voxels visited by any frame of the group, row 1 + g = visited by frame g,
-// row kHdrRow word 0 = frames that touched the block (bit g). Cleared after each group.
-constexpr int kHdrRow = 1 + kMaxG;
+// row g = voxels visited by frame g, row kHdrRow word 0 = frames that touched the block
+// (bit g). Cleared as the group is folded.
+constexpr int kHdrRow = kMaxG;
 constexpr int kMaskWords = (kHdrRow + 1) * 16;
-// per-frame counters of a group: fctr[g * kFC + FC_*]
-enum FrameCounter : int { FC_UPD = 0, FC_RAYS, FC_DROPPED, FC_TIES, FC_TOUCH, FC_NEW, FC_FBV, kFC = 8 };
+enum FrameCounter : int {
+    FC_UPD = 0,  // voxels updated
+    FC_RAYS,     // band rays cast
+    FC_DROPPED,  // points dropped by project_point
+    FC_TIES,     // tie-list entries (projection)
+    FC_TOUCH,    // blocks touched
+    FC_NEW,      // blocks new to the map
+    FC_FBV,      // voxels measured by their visiting rays (own pixel without a return)
+    FC_VOX,      // visited voxels listed (the frame's fold work)
+    FC_VQ,       // k_fold work queue position (visited voxels)
+    kFC = 16
+};
 constexpr double kPi = 3.14159265358979323846;
 
 // Packed block key: 21 bits per axis, biased by 2^20 so that unsigned order of
@@ -324,27 +334,16 @@ enum Counter : int {
     C_BLOCKS = 0,       // allocated blocks (pool high-water mark)
     C_SEM = 1,          // allocated semantic layers
     C_TOUCHED = 2,      // blocks touched by the current frame group
-    C_UPDATED = 3,      // voxels updated by the current pass
-    C_FALLBACK = 4,     // voxels that need the multi-ray fallback
-    C_RECORDS = 5,      // fallback visit records
-    C_ERR_KEY = 6,      // block coordinate out of key range
-    C_ERR_HASH = 7,     // hash table full
-    C_TIES = 8,         // pixels with a possible exact range tie
-    C_DROPPED = 9,      // points dropped by project_point
+    C_RECORDS = 5,      // fallback visit records of the group
+    C_FB_VOXELS = 6,    // fallback (voxel, frame) descriptors written by k_fb_sort
     C_CAND = 10,        // semantic candidate blocks
     C_ERR_CONF = 11,    // confidence outside [0, 1]
     C_SEM_UPDATED = 12,
-    C_FRAME = 13,       // frame serial (stamp for touched detection)
-    C_REC_OVERFLOW = 14,
-    C_RAYS = 15,        // band rays cast this frame
     C_ABORT = 16,       // bitmask of abort reasons (kAbort*); every frame kernel no-ops while set
     C_BLOCKS_BEFORE = 17,  // C_BLOCKS at the start of the current frame group
-    C_MAPPED = 18,      // blocks of TSDF pool currently mapped (host-written)
-    C_FB_BLOCKS = 19,   // blocks holding fallback records this frame
-    C_FB_VOXELS = 20,   // voxels folded by the fallback path
-    C_FB_BIG = 21,      // blocks whose fallback bucket exceeds the warp sort
-    C_WORDS = 22,       // visit-mask words listed by the band kernel (group)
-    C_BUCKET_TOP = 23,  // fallback bucket space handed out this frame
+    C_MAPPED = 18,      // blocks with pool + visit-mask memory mapped (host-written)
+    C_FB_BLOCKS = 19,   // blocks holding fallback records this group
+    C_BUCKET_TOP = 23,  // fallback bucket space handed out this group
     C_DONE = 24,        // CTAs of k_fold finished (the last one writes the group's reports)
     C_CONF_MAYBE = 27,  // the current label image may read a confidence outside [0, 1]
     kNumCounters = 32
@@ -358,7 +357,7 @@ enum AbortBits : uint32_t {
     kAbortKey = 4,       // block coordinate outside the key range
     kAbortHash = 8,      // hash table full (implies capacity)
     kAbortRecords = 16,  // fallback record buffer too small: grow, retry
-    kAbortWords = 64     // visit-mask word list too small: grow, retry
+    kAbortVox = 64       // visited-voxel list too small: grow, retry
 };
 
 // Per-frame results written by k_frame_end (device), read back per batch.

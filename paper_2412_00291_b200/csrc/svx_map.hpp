@@ -211,9 +211,10 @@ struct svx_map {
     uint32_t* fbclaim = nullptr;     // [cap] bucket allocation claim flags
     uint32_t* fbslots = nullptr;     // [cap]
     svx::DevBuf<unsigned long long> bucket, bucket2;  // records grouped by block (+ sort scratch)
+    svx::DevBuf<uint4> fbdesc;       // fallback voxels: pool idx, voxel | frames << 16, records start, count
     uint32_t rec_cap = 0;
-    svx::DevBuf<unsigned long long> wlist;  // visit-mask words of the group: (pool idx << 4) | word
-    uint32_t word_cap = 0;
+    svx::DevBuf<uint32_t> vlist;     // per frame of the group: its visited voxels, (pool idx << 9) | voxel
+    uint32_t vox_cap = 0;            // entries per frame
     // per-frame results of a batch
     svx::DevBuf<svx::FrameOut> outs;
     svx::FrameOut* h_outs = nullptr;

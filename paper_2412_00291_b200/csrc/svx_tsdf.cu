@@ -26,16 +26,17 @@
 //                list, the frame's visit-mask row (RED.OR) and the union row (ATOM.OR: the
 //                words a tile sets first become the group's word list).
 //   k_fb_bucket  the fallback records into per-block buckets.
-//   k_fb_fold    CTA per block with fallback records: orders its records by (voxel, frame,
+//   k_fb_sort    CTA per block with fallback records: orders its records by (voxel, frame,
 //                pixel) - per frame the reference's ascending (v, u) visit order after its
-//                chunk-order merge + stable_sort (.cpp:141-146,215-216) - and applies every
-//                frame of the group to each of those voxels (own pixel where it has a
-//                return, else the ordered sum over the frame's visiting rays).
-//   k_fold       warp per 32 listed mask words, lane per visited voxel: applies the group's
-//                frames in order (own-pixel measurement, accumulate-then-merge fold, Eq.
-//                4-5); voxels with a fallback frame are left to k_fb_fold. Clears the mask
-//                words, marks dirty blocks, counts per-frame touched / new blocks; the last
-//                CTA writes the frames' reports.
+//                chunk-order merge + stable_sort (.cpp:141-146,215-216) - and emits one
+//                descriptor per such voxel.
+//   k_fold       warps pull chunks of 32 listed mask words (lane per visited voxel) and then
+//                chunks of fallback-voxel descriptors from two queues, and apply the
+//                group's frames to each voxel in order (own-pixel measurement where the own
+//                pixel has a return, else the frame's visiting rays in ascending pixel
+//                order; accumulate-then-merge fold, Eq. 4-5). Clears the mask words, marks
+//                dirty blocks, counts per-frame touched / new blocks; the last CTA writes
+//                the frames' reports.
 // Any abort (pool growth, buffer growth, capacity, key range) stops the batch; the host
 // rolls the aborted group back (its blocks, hash entries and masks) and retries it
 // (CapacityError and key-range errors: frame by frame, reproducing the reference's
@@ -66,7 +67,7 @@ struct GroupConsts {
     uint32_t serial;    // group serial (touched stamps)
     uint32_t G, P, VW;  // frames, pixels per frame, valid-bit words per frame
     uint32_t tiles;     // band tiles per frame
-    uint32_t max_blocks, rec_cap, word_cap;
+    uint32_t max_blocks, rec_cap, vox_cap;
 };
 
 // Per-frame pose data.
@@ -384,61 +385,41 @@ __device__ inline uint32_t rec_frame(unsigned long long r) { return uint32_t(r >
 __device__ inline uint32_t rec_pixel(unsigned long long r) { return uint32_t(r) & 0x0FFFFFFFu; }
 __device__ inline int rec_lin(unsigned long long r) { return int(uint32_t(r >> 32) & 511u); }
 
-// Bit g = frame g of the group visited voxel lin of block idx.
-__device__ inline uint32_t voxel_frames(const uint32_t* __restrict__ fm, uint32_t idx, int lin, uint32_t G) {
-    const uint32_t* row = fm + uint64_t(idx) * kMaskWords + 16 + (lin >> 5);
-    const int b = lin & 31;
-    uint32_t f = 0;
-#pragma unroll 4
-    for (uint32_t g = 0; g < G; ++g) f |= ((row[16 * g] >> b) & 1u) << g;
-    return f;
-}
-
-// Applies the group's frames that visited the voxel (bit g of `frames`, ascending = the
-// order of the reference's consecutive integrate_frame calls) to the voxel at vp, whose
-// state lives in registers meanwhile. Per frame: the own pixel of the voxel centre if it
-// holds a return (.cpp:232-233), else every visiting ray of that frame in ascending pixel
-// order (.cpp:235-236), taken from `recs` (sorted by (frame, pixel)). Without records
-// (kRec = false), a frame of the second kind returns kFallback and stores nothing: the
-// voxel belongs to k_fb_fold. Returns the frames that updated the voxel.
+// Applies frame g to the voxel at vp (tsdf_integrator.cpp:224-248): the own pixel of the
+// voxel centre if it holds a return (.cpp:232-233), else every visiting ray of the frame
+// in ascending pixel order (.cpp:235-236), given as `recs` (its fallback records, sorted
+// by pixel). Without records (kRec = false), a voxel whose own pixel has no return returns
+// kFallback and is left alone: a fallback descriptor (k_fb_sort) applies it. Returns 1 when
+// the voxel was updated.
 constexpr uint32_t kFallback = 0xFFFFFFFFu;
 template <bool kRec>
-__device__ uint32_t fold_voxel(const GroupConsts& c, const FramePose* __restrict__ fp, uint32_t frames,
-                               svx_tsdf_voxel* vp, d3 center, const ScanSlots& sc,
-                               const unsigned long long* __restrict__ recs, uint32_t nrec) {
-    svx_tsdf_voxel vox = load_voxel(vp);
-    uint32_t j = 0, upd = 0;
-    for (uint32_t fr = frames; fr; fr &= fr - 1) {
-        const uint32_t g = uint32_t(__ffs(fr) - 1);
-        const FramePose& f = fp[g];
-        const PixCache* cache = cache_of(sc, c, g);
+__device__ __forceinline__ uint32_t fold_one(const GroupConsts& c, const FramePose& f, uint32_t g, svx_tsdf_voxel* vp, d3 center,
+                             const ScanSlots& sc, const unsigned long long* __restrict__ recs, uint32_t nrec) {
+    const PixCache* cache = cache_of(sc, c, g);
+    Accum acc{0.0, 0.0, 0.0, 0.0, 0.0};
+    bool measured = false;
+    svx_tsdf_voxel vox = load_voxel(vp);  // in flight while the own pixel is computed
+    if constexpr (!kRec) {
         const uint32_t own = own_pixel(c.m, xform(f.w2s, center));
-        Accum acc{0.0, 0.0, 0.0, 0.0, 0.0};
-        bool measured = false;
-        if (own != kInvalid && pixel_has_return(sc.validbits + uint64_t(g) * c.VW, own)) {
-            const Term t = measure_term(c, f.origin, cache, own, center, vox);
+        if (own == kInvalid || !pixel_has_return(sc.validbits + uint64_t(g) * c.VW, own)) return kFallback;
+        const Term t = measure_term(c, f.origin, cache, own, center, vox);
+        if (t.flags & 1u) {
+            accumulate(acc, t);
+            measured = true;
+        }
+    } else {
+        for (uint32_t j = 0; j < nrec; ++j) {
+            const Term t = measure_term(c, f.origin, cache, rec_pixel(recs[j]), center, vox);
             if (t.flags & 1u) {
                 accumulate(acc, t);
                 measured = true;
             }
-        } else {
-            if constexpr (!kRec) return kFallback;
-            while (j < nrec && rec_frame(recs[j]) < g) ++j;
-            for (; j < nrec && rec_frame(recs[j]) == g; ++j) {
-                const Term t = measure_term(c, f.origin, cache, rec_pixel(recs[j]), center, vox);
-                if (t.flags & 1u) {
-                    accumulate(acc, t);
-                    measured = true;
-                }
-            }
-        }
-        if (measured) {
-            fold(vox, acc);
-            upd |= 1u << g;
         }
     }
-    if (upd) store_voxel(vp, vox);
-    return upd;
+    if (!measured) return 0;
+    fold(vox, acc);
+    store_voxel(vp, vox);
+    return 1;
 }
 
 // Hash find-or-insert of a block key; a new block takes the next pool index.
@@ -503,8 +484,8 @@ __device__ void visit_global(const GroupConsts& c, uint32_t g, HashView h, uint6
                              uint32_t* __restrict__ stamp, uint32_t* __restrict__ touched,
                              uint32_t* __restrict__ fm, uint32_t* __restrict__ fbcnt,
                              unsigned long long* __restrict__ rec, svx_tsdf_voxel* __restrict__ pool,
-                             unsigned long long* __restrict__ wlist, uint32_t* __restrict__ ctr, uint64_t key,
-                             int lin, bool fb, uint32_t p) {
+                             uint32_t* __restrict__ vlist, uint32_t* __restrict__ fctr,
+                             uint32_t* __restrict__ ctr, uint64_t key, int lin, bool fb, uint32_t p) {
     const SlotRef r = find_or_insert(c, h, block_keys, ctr, key);
     if (r.slot == kInvalid) return;
     if (atomicExch(&stamp[r.slot], c.serial) != c.serial) touched[atomicAdd(&ctr[C_TOUCHED], 1u)] = r.slot;
@@ -512,12 +493,10 @@ __device__ void visit_global(const GroupConsts& c, uint32_t g, HashView h, uint6
     uint32_t* bm = fm + uint64_t(r.idx) * kMaskWords;
     atomicOr(&bm[kHdrRow * 16], 1u << g);
     const uint32_t bit = 1u << (lin & 31);
-    const int w = lin >> 5;
-    atomicOr(&bm[(1 + g) * 16 + w], bit);
-    if (atomicOr(&bm[w], bit) == 0u) {
-        const uint32_t pos = atomicAdd(&ctr[C_WORDS], 1u);
-        if (pos < c.word_cap) wlist[pos] = (static_cast<unsigned long long>(r.idx) << 4) | uint32_t(w);
-        else atomicOr(&ctr[C_ABORT], kAbortWords);
+    if (!(atomicOr(&bm[g * 16 + (lin >> 5)], bit) & bit)) {  // the frame's first visit of the voxel
+        const uint32_t pos = atomicAdd(&fctr[g * kFC + FC_VOX], 1u);
+        if (pos < c.vox_cap) vlist[uint64_t(g) * c.vox_cap + pos] = (r.idx << 9) | uint32_t(lin);
+        else atomicOr(&ctr[C_ABORT], kAbortVox);
     }
     if (!fb) return;
     atomicAdd(&fbcnt[r.slot], 1u);
@@ -545,7 +524,7 @@ __global__ void __launch_bounds__(kTileU * kTileV, 4)
 k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
        uint64_t* __restrict__ block_keys, uint32_t* __restrict__ stamp, uint32_t* __restrict__ touched,
        uint32_t* __restrict__ fm, uint32_t* __restrict__ fbcnt, unsigned long long* __restrict__ rec,
-       svx_tsdf_voxel* __restrict__ pool, unsigned long long* __restrict__ wlist,
+       svx_tsdf_voxel* __restrict__ pool, uint32_t* __restrict__ vlist,
        uint32_t* __restrict__ fctr, uint32_t* __restrict__ ctr) {
     pdl_wait();
     pdl_trigger();
@@ -676,7 +655,7 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
                 fb = own == kInvalid || !pixel_has_return(validbits, own);
             }
             if (cur_li < 0) {  // local table full: straight to global state
-                visit_global(c, g, h, block_keys, stamp, touched, fm, fbcnt, rec, pool, wlist, ctr, key, lin, fb, p);
+                visit_global(c, g, h, block_keys, stamp, touched, fm, fbcnt, rec, pool, vlist, fctr, ctr, key, lin, fb, p);
                 return;
             }
             const int word = cur_li * 16 + (lin >> 5);
@@ -691,8 +670,8 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
                 if (pos < uint32_t(kTileFb))
                     lfb[pos] = (uint32_t(cur_li) << 24) | (uint32_t(lin) << 15) | uint32_t(tid);
                 else
-                    visit_global(c, g, h, block_keys, stamp, touched, fm, fbcnt, rec, pool, wlist, ctr, key, lin,
-                                 true, p);
+                    visit_global(c, g, h, block_keys, stamp, touched, fm, fbcnt, rec, pool, vlist, fctr, ctr, key,
+                                 lin, true, p);
             }
         });
         if (pend_word >= 0) atomicOr(&lmask[0][0] + pend_word, pend_bits);
@@ -736,28 +715,25 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
         ++rpos;
         atomicAdd(&lcnt[li], 1u);
     }
-    // voxel masks -> the frame's row and the union row of each block; the union words a
-    // tile sets first (the atomic returns them clear) are the group's word list
-    uint32_t nw = 0;
+    // voxel masks -> the frame's row of each block; the bits a tile sets first (the atomic
+    // returns them clear) are those voxels' single entries in the frame's voxel list
+    uint32_t nv = 0;
     for (int i = tid; i < kLocalKeys * 16; i += kTileU * kTileV) {
         const int li = i >> 4, w = i & 15;
-        const uint32_t bits = lmask[li][w];
-        uint32_t take = 0;
-        if (bits && lidx[li] != kInvalid) {
-            uint32_t* bm = fm + uint64_t(lidx[li]) * kMaskWords;
-            atomicOr(&bm[(1 + g) * 16 + w], bits);
-            take = atomicOr(&bm[w], bits) == 0u ? 1u : 0u;
-        }
-        lmask[li][w] = take;
-        nw += take;
+        uint32_t bits = lmask[li][w];
+        if (bits && lidx[li] != kInvalid) bits &= ~atomicOr(&fm[uint64_t(lidx[li]) * kMaskWords + g * 16 + w], bits);
+        else bits = 0u;
+        lmask[li][w] = bits;
+        nv += __popc(bits);
     }
-    uint32_t pos = cta_reserve<kW>(nw, &ctr[C_WORDS], s_w);
-    if (nw && pos + nw > c.word_cap) atomicOr(&ctr[C_ABORT], kAbortWords);
-    for (int i = tid; i < kLocalKeys * 16 && nw; i += kTileU * kTileV) {
+    uint32_t pos = cta_reserve<kW>(nv, &fctr[g * kFC + FC_VOX], s_w);
+    if (nv && pos + nv > c.vox_cap) atomicOr(&ctr[C_ABORT], kAbortVox);
+    uint32_t* vl = vlist + uint64_t(g) * c.vox_cap;
+    for (int i = tid; i < kLocalKeys * 16 && nv; i += kTileU * kTileV) {
         const int li = i >> 4, w = i & 15;
-        if (!lmask[li][w]) continue;
-        if (pos < c.word_cap) wlist[pos] = (static_cast<unsigned long long>(lidx[li]) << 4) | uint32_t(w);
-        ++pos;
+        const uint32_t hi = lidx[li] << 9;
+        for (uint32_t bits = lmask[li][w]; bits; bits &= bits - 1, ++pos)
+            if (pos < c.vox_cap) vl[pos] = hi | (uint32_t(w) * 32u + uint32_t(__ffs(bits) - 1));
     }
     __syncthreads();  // lcnt complete
     if (lcnt[tid]) atomicAdd(&fbcnt[lslot[tid]], lcnt[tid]);
@@ -801,27 +777,24 @@ __device__ inline void load_poses(const GroupParams& gp, FramePose* s_f) {
 // CTA per block with fallback records. The bucket is ordered by (voxel, frame, pixel):
 // counting sort by voxel (histogram, scan, scatter to the sort scratch), then inside each
 // voxel's segment a rank sort (keys are unique: a ray visits a voxel once per frame), in
-// parallel. One thread per such voxel then applies every frame of the group to it, the
-// fallback frames with their visiting rays summed strictly in ascending pixel order.
+// parallel. Each (voxel, frame) run of records becomes one descriptor (pool index, voxel,
+// frame, its records, sorted by pixel) that the frame's fold applies.
 __global__ void __launch_bounds__(kThreads)
-k_fb_fold(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
-          const uint64_t* __restrict__ block_keys, svx_tsdf_voxel* __restrict__ pool,
-          const uint32_t* __restrict__ fm, const uint32_t* __restrict__ fbslots, uint32_t* __restrict__ fbcnt,
+k_fb_sort(const uint32_t G, HashView h, const uint32_t* __restrict__ fbslots, uint32_t* __restrict__ fbcnt,
           uint32_t* __restrict__ fbstart, uint32_t* __restrict__ fbclaim, uint32_t* __restrict__ fbfill,
           unsigned long long* __restrict__ bucket, unsigned long long* __restrict__ bucket2,
-          uint32_t* __restrict__ fctr, uint32_t* __restrict__ ctr) {
+          uint4* __restrict__ fbdesc, uint32_t* __restrict__ fctr, uint32_t* __restrict__ ctr) {
     pdl_wait();
     pdl_trigger();
     if (cta_aborted(ctr)) return;
-    const GroupConsts& c = gp.c;
     using Scan = cub::BlockScan<uint32_t, kThreads>;
-    constexpr int kPer = kBlockVoxels / kThreads;  // voxels per thread in the scan
+    constexpr int kPer = kBlockVoxels / kThreads;  // voxels per thread
+    constexpr int kW = kThreads / 32;
     __shared__ typename Scan::TempStorage scan_tmp;
-    __shared__ FramePose s_f[kMaxG];
     __shared__ uint32_t seg_start[kBlockVoxels], seg_cnt[kBlockVoxels], cursor[kBlockVoxels];
-    __shared__ uint32_t s_upd[kMaxG], s_fbv[kMaxG];
-    load_poses<kThreads>(gp, s_f);
-    if (threadIdx.x < kMaxG) s_upd[threadIdx.x] = s_fbv[threadIdx.x] = 0u;
+    __shared__ uint32_t s_fbv[kMaxG];
+    __shared__ uint32_t s_w[2 * kW];
+    if (threadIdx.x < kMaxG) s_fbv[threadIdx.x] = 0u;
     const uint32_t nb = ctr[C_FB_BLOCKS];
     for (uint32_t t = blockIdx.x; t < nb; t += gridDim.x) {
         const uint32_t slot = fbslots[t];
@@ -861,15 +834,27 @@ k_fb_fold(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h
             bk[b + r] = k;
         }
         __syncthreads();
-        const uint64_t key = block_keys[idx];
-        svx_tsdf_voxel* blk = pool + uint64_t(idx) * kBlockVoxels;
-        for (int v = threadIdx.x; v < kBlockVoxels; v += kThreads) {
-            if (!seg_cnt[v]) continue;
-            const uint32_t frames = voxel_frames(fm, idx, v, c.G);
-            const uint32_t upd = fold_voxel<true>(c, s_f, frames, blk + v, center_of(key, v, c.nu), sc,
-                                                  bk + seg_start[v], seg_cnt[v]);
-            for (uint32_t u = upd; u; u &= u - 1) atomicAdd(&s_upd[__ffs(u) - 1], 1u);
-            for (uint32_t u = frames; u; u &= u - 1) atomicAdd(&s_fbv[__ffs(u) - 1], 1u);
+        // one descriptor per (voxel, frame) run of the sorted segments
+        uint32_t nd = 0;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            const int v = threadIdx.x * kPer + j;
+            const uint32_t b = seg_start[v], e = b + seg_cnt[v];
+            for (uint32_t q = b; q < e; ++q) nd += (q == b || rec_frame(bk[q]) != rec_frame(bk[q - 1])) ? 1u : 0u;
+        }
+        uint32_t pos = cta_reserve<kW>(nd, &ctr[C_FB_VOXELS], s_w);
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            const int v = threadIdx.x * kPer + j;
+            const uint32_t b = seg_start[v], e = b + seg_cnt[v];
+            for (uint32_t q = b; q < e;) {
+                const uint32_t g = rec_frame(bk[q]);
+                uint32_t q2 = q + 1;
+                while (q2 < e && rec_frame(bk[q2]) == g) ++q2;
+                fbdesc[pos++] = make_uint4(idx, uint32_t(v) | (g << 16), start + q, q2 - q);
+                atomicAdd(&s_fbv[g], 1u);
+                q = q2;
+            }
         }
         if (threadIdx.x == 0) {  // per-slot fallback state, clean for the next group
             fbcnt[slot] = 0u;
@@ -880,82 +865,63 @@ k_fb_fold(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h
         __syncthreads();  // shared arrays are reused by the next bucket
     }
     __syncthreads();
-    if (threadIdx.x < c.G) {
-        if (s_upd[threadIdx.x]) atomicAdd(&fctr[threadIdx.x * kFC + FC_UPD], s_upd[threadIdx.x]);
-        if (s_fbv[threadIdx.x]) atomicAdd(&fctr[threadIdx.x * kFC + FC_FBV], s_fbv[threadIdx.x]);
-    }
+    if (threadIdx.x < G && s_fbv[threadIdx.x]) atomicAdd(&fctr[threadIdx.x * kFC + FC_FBV], s_fbv[threadIdx.x]);
 }
 
-// Warp per 32 listed mask words, lane per visited voxel (the words' set bits expanded
-// across the warp with a shuffle search). Then the group's end: dirty flags and per-frame
-// touched / new block counts over the touched list; the last CTA writes the reports.
-__global__ void __launch_bounds__(kThreads)
-k_fold(const __grid_constant__ GroupParams gp, const ScanSlots sc, const uint32_t* __restrict__ vals,
-       const uint64_t* __restrict__ block_keys, svx_tsdf_voxel* __restrict__ pool, uint32_t* __restrict__ fm,
-       const unsigned long long* __restrict__ wlist, const uint32_t* __restrict__ touched,
+// Frame g of the group: one thread per listed visited voxel of the frame (grid-stride, one
+// wave of CTAs), then the group's fallback descriptors of frame g; each applies frame g to
+// its voxel, whose state then holds frames 0..g, as after the reference's g + 1
+// consecutive integrate_frame calls. The last frame's launch ends the group: dirty flags,
+// per-frame touched / new block counts and the mask rows over the touched list; its last
+// CTA writes the frames' reports.
+__global__ void __launch_bounds__(kThreads, 4)
+k_fold(const GroupConsts c, const FramePose f, const uint32_t g, const ScanSlots sc,
+       const uint32_t* __restrict__ vals, const uint64_t* __restrict__ block_keys, svx_tsdf_voxel* __restrict__ pool,
+       uint32_t* __restrict__ fm, const uint32_t* __restrict__ vlist, const uint4* __restrict__ fbdesc,
+       const unsigned long long* __restrict__ bucket, const uint32_t* __restrict__ touched,
        uint8_t* __restrict__ dirty, uint32_t* __restrict__ fctr, FrameOut* __restrict__ outs,
        uint32_t* __restrict__ ctr) {
     pdl_wait();
     pdl_trigger();
     if (cta_aborted(ctr)) return;
-    const GroupConsts& c = gp.c;
-    __shared__ FramePose s_f[kMaxG];
-    __shared__ uint32_t s_upd[kMaxG], s_touch[kMaxG], s_new[kMaxG];
+    __shared__ uint32_t s_touch[kMaxG], s_new[kMaxG];
     __shared__ bool last;
-    load_poses<kThreads>(gp, s_f);
-    if (threadIdx.x < kMaxG) s_upd[threadIdx.x] = s_touch[threadIdx.x] = s_new[threadIdx.x] = 0u;
-    __syncthreads();
     const int lane = threadIdx.x & 31;
-    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    const uint32_t nw = min(ctr[C_WORDS], c.word_cap);
-    for (uint32_t base = warp * 32; base < nw; base += nwarps * 32) {
-        const uint32_t i = base + lane;
-        const bool valid = i < nw;
-        const unsigned long long e = valid ? wlist[i] : 0ull;
-        const uint32_t idx = uint32_t(e >> 4), w = uint32_t(e) & 15u;
-        const uint32_t bits = valid ? fm[uint64_t(idx) * kMaskWords + w] : 0u;
-        const uint32_t cnt = __popc(bits);
-        uint32_t incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-        for (uint32_t k0 = 0; k0 < total; k0 += 32) {
-            const uint32_t k = k0 + uint32_t(lane);
-            // owner lane of voxel k: the first lane whose inclusive count exceeds k
-            int o = 0;
-#pragma unroll
-            for (int s = 16; s > 0; s >>= 1) {
-                const uint32_t y = __shfl_sync(0xFFFFFFFFu, incl, o + s - 1);
-                if (y <= k) o += s;
-            }
-            const uint32_t ob = __shfl_sync(0xFFFFFFFFu, bits, o);
-            const uint32_t obase = __shfl_sync(0xFFFFFFFFu, incl - cnt, o);
-            const unsigned long long oe = __shfl_sync(0xFFFFFFFFu, e, o);
-            uint32_t upd = 0;
-            if (k < total) {
-                const uint32_t oidx = uint32_t(oe >> 4);
-                const int lin = int((uint32_t(oe) & 15u) * 32u + select_bit(ob, k - obase));
-                const uint32_t frames = voxel_frames(fm, oidx, lin, c.G);
-                upd = fold_voxel<false>(c, s_f, frames, pool + uint64_t(oidx) * kBlockVoxels + lin,
-                                        center_of(block_keys[oidx], lin, c.nu), sc, nullptr, 0);
-                if (upd == kFallback) upd = 0;  // k_fb_fold applied this voxel
-            }
-            for (uint32_t gg = 0; gg < c.G; ++gg) {
-                const uint32_t n = __popc(__ballot_sync(0xFFFFFFFFu, (upd >> gg) & 1u));
-                if (lane == 0 && n) atomicAdd(&s_upd[gg], n);
-            }
-        }
-        __syncwarp();
-        if (valid) {  // this warp's words are done: clean for the next group
-            uint32_t* bm = fm + uint64_t(idx) * kMaskWords + w;
-            bm[0] = 0u;
-            for (uint32_t gg = 0; gg < c.G; ++gg) bm[16 * (1 + gg)] = 0u;
-        }
+    const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+    uint32_t* fc = fctr + g * kFC;
+    const uint32_t nv = min(fc[FC_VOX], c.vox_cap);
+    const uint32_t* vl = vlist + uint64_t(g) * c.vox_cap;
+    uint32_t n_upd = 0;
+    // fallback descriptors first: a long record chain starts early instead of in the tail
+    const uint32_t nfv = ctr[C_FB_VOXELS];
+    for (uint32_t i = gtid; i < nfv; i += stride) {
+        const uint4 d = fbdesc[i];
+        if ((d.y >> 16) != g) continue;
+        const int lin = int(d.y & 511u);
+        n_upd += fold_one<true>(c, f, g, pool + uint64_t(d.x) * kBlockVoxels + lin,
+                                center_of(block_keys[d.x], lin, c.nu), sc, bucket + d.z, d.w);
     }
+    // the visited voxels, 32 per warp from a queue (threads that took a long fallback
+    // chain take fewer of them)
+    for (;;) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&fc[FC_VQ], 32u);
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        if (base >= nv) break;
+        const uint32_t i = base + uint32_t(lane);
+        if (i >= nv) continue;
+        const uint32_t e = vl[i];
+        const uint32_t idx = e >> 9;
+        const int lin = int(e & 511u);
+        const uint32_t u = fold_one<false>(c, f, g, pool + uint64_t(idx) * kBlockVoxels + lin,
+                                           center_of(block_keys[idx], lin, c.nu), sc, nullptr, 0);
+        n_upd += u == 1u ? 1u : 0u;  // kFallback: a fallback descriptor applies it
+    }
+    for (int o = 16; o; o >>= 1) n_upd += __shfl_xor_sync(0xFFFFFFFFu, n_upd, o);
+    if (lane == 0 && n_upd) atomicAdd(&fc[FC_UPD], n_upd);
+    if (g + 1 < c.G) return;  // (no barrier: warps leave as soon as their voxels are done)
+    if (threadIdx.x < kMaxG) s_touch[threadIdx.x] = s_new[threadIdx.x] = 0u;
+    __syncthreads();
     // group end: dirty blocks (tsdf_integrator.cpp:160-168 pushes every visited block),
     // per-frame touched blocks and new blocks (a block new to the map is new in the first
     // frame of the group that visits it)
@@ -964,18 +930,22 @@ k_fold(const __grid_constant__ GroupParams gp, const ScanSlots sc, const uint32_
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
         const uint32_t idx = vals[touched[t]];
         dirty[idx] = 1;
-        uint32_t* hdr = fm + uint64_t(idx) * kMaskWords + kHdrRow * 16;
-        const uint32_t ft = *hdr;
-        *hdr = 0u;
-        for (uint32_t u = ft; u; u &= u - 1) atomicAdd(&s_touch[__ffs(u) - 1], 1u);
+        uint32_t* bm = fm + uint64_t(idx) * kMaskWords;
+        const uint32_t ft = bm[kHdrRow * 16];
+        bm[kHdrRow * 16] = 0u;
+        for (uint32_t u = ft; u; u &= u - 1) {  // the rows of the frames that touched the block
+            const int gg = __ffs(u) - 1;
+            uint4* row = reinterpret_cast<uint4*>(bm + gg * 16);
+            row[0] = row[1] = row[2] = row[3] = make_uint4(0u, 0u, 0u, 0u);
+            atomicAdd(&s_touch[gg], 1u);
+        }
         if (idx >= before && ft) atomicAdd(&s_new[__ffs(ft) - 1], 1u);
     }
     __syncthreads();
     if (threadIdx.x < c.G) {
-        const uint32_t g = threadIdx.x;
-        if (s_upd[g]) atomicAdd(&fctr[g * kFC + FC_UPD], s_upd[g]);
-        if (s_touch[g]) atomicAdd(&fctr[g * kFC + FC_TOUCH], s_touch[g]);
-        if (s_new[g]) atomicAdd(&fctr[g * kFC + FC_NEW], s_new[g]);
+        const uint32_t gg = threadIdx.x;
+        if (s_touch[gg]) atomicAdd(&fctr[gg * kFC + FC_TOUCH], s_touch[gg]);
+        if (s_new[gg]) atomicAdd(&fctr[gg * kFC + FC_NEW], s_new[gg]);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -986,23 +956,22 @@ k_fold(const __grid_constant__ GroupParams gp, const ScanSlots sc, const uint32_
     if (!last) return;
     __threadfence();
     if (threadIdx.x < c.G) {
-        const uint32_t g = threadIdx.x;
-        uint32_t* fc = fctr + g * kFC;
+        uint32_t* f = fctr + threadIdx.x * kFC;
         FrameOut o;
-        o.updated = __ldcg(&fc[FC_UPD]);
-        o.new_blocks = __ldcg(&fc[FC_NEW]);
-        o.touched = __ldcg(&fc[FC_TOUCH]);
+        o.updated = __ldcg(&f[FC_UPD]);
+        o.new_blocks = __ldcg(&f[FC_NEW]);
+        o.touched = __ldcg(&f[FC_TOUCH]);
         o.records = ctr[C_RECORDS];
-        o.rays = __ldcg(&fc[FC_RAYS]);
-        o.dropped = __ldcg(&fc[FC_DROPPED]);
-        o.fb_voxels = __ldcg(&fc[FC_FBV]);
+        o.rays = __ldcg(&f[FC_RAYS]);
+        o.dropped = __ldcg(&f[FC_DROPPED]);
+        o.fb_voxels = __ldcg(&f[FC_FBV]);
         o.ok = 1;
-        outs[g] = o;
-        for (int k = 0; k < kFC; ++k) fc[k] = 0u;
+        outs[threadIdx.x] = o;
+        for (int k = 0; k < kFC; ++k) f[k] = 0u;
     }
     if (threadIdx.x == 0) {
         ctr[C_DONE] = 0;
-        ctr[C_TOUCHED] = ctr[C_RECORDS] = ctr[C_WORDS] = ctr[C_FB_BLOCKS] = ctr[C_BUCKET_TOP] = 0;
+        ctr[C_TOUCHED] = ctr[C_RECORDS] = ctr[C_FB_BLOCKS] = ctr[C_BUCKET_TOP] = ctr[C_FB_VOXELS] = 0;
         ctr[C_BLOCKS_BEFORE] = ctr[C_BLOCKS];
     }
 }
@@ -1084,7 +1053,7 @@ GroupConsts make_consts(svx_map* m, svx_scan* s, const svx_integrator_cfg& cfg, 
     c.tiles = uint32_t(((s->dm.W + kTileU - 1) / kTileU) * ((s->dm.H + kTileV - 1) / kTileV));
     c.max_blocks = m->cfg.max_blocks;
     c.rec_cap = m->rec_cap;
-    c.word_cap = m->word_cap;
+    c.vox_cap = m->vox_cap;
     return c;
 }
 
@@ -1126,23 +1095,25 @@ void launch_group_kernels(svx_map* m, svx_scan* s, const GroupParams& gp, FrameO
     {
         ProfMark pm(m, SVX_K_RAYCAST);
         launch_pdl(k_band, c.G * c.tiles, kTileU * kTileV, m->stream, gp, sc, hv, m->block_keys, m->stamp,
-                   m->touched, fm, m->fbcnt, m->records.p, tsdf_base(m), m->wlist.p, m->fctr, m->d_ctr);
+                   m->touched, fm, m->fbcnt, m->records.p, tsdf_base(m), m->vlist.p, m->fctr, m->d_ctr);
         count_launch();
     }
     {
         ProfMark pm(m, SVX_K_FALLBACK);
         launch_pdl(k_fb_bucket, pg / 4, kThreads, m->stream, m->records.p, m->rec_cap, m->fbcnt, m->fbstart,
                    m->fbclaim, m->fbfill, m->fbslots, m->bucket.p, m->d_ctr);
-        launch_pdl(k_fb_fold, pg / 2, kThreads, m->stream, gp, sc, hv, m->block_keys, tsdf_base(m), fm,
-                   m->fbslots, m->fbcnt, m->fbstart, m->fbclaim, m->fbfill, m->bucket.p, m->bucket2.p, m->fctr,
-                   m->d_ctr);
+        launch_pdl(k_fb_sort, pg / 2, kThreads, m->stream, c.G, hv, m->fbslots, m->fbcnt, m->fbstart, m->fbclaim,
+                   m->fbfill, m->bucket.p, m->bucket2.p, m->fbdesc.p, m->fctr, m->d_ctr);
         count_launch(2);
     }
     {
         ProfMark pm(m, SVX_K_FOLD);
-        launch_pdl(k_fold, fold_grid(m->device), kThreads, m->stream, gp, sc, m->vals, m->block_keys, tsdf_base(m),
-                   fm, m->wlist.p, m->touched, m->dirty, m->fctr, outs, m->d_ctr);
-        count_launch();
+        for (uint32_t g = 0; g < c.G; ++g) {
+            launch_pdl(k_fold, fold_grid(m->device), kThreads, m->stream, c, gp.f[g], g, sc, m->vals, m->block_keys,
+                       tsdf_base(m), fm, m->vlist.p, m->fbdesc.p, m->bucket.p, m->touched, m->dirty, m->fctr, outs,
+                       m->d_ctr);
+            count_launch();
+        }
     }
     SVX_CUDA(cudaGetLastError());
 }
@@ -1222,8 +1193,7 @@ void reset_frame_state(svx_map* m) {
     SVX_CUDA(cudaMemsetAsync(m->fbfill, 0, sizeof(uint32_t) * m->cap, m->stream));
     SVX_CUDA(cudaMemsetAsync(m->fbstart, 0xFF, sizeof(uint32_t) * m->cap, m->stream));
     SVX_CUDA(cudaMemsetAsync(m->fctr, 0, sizeof(uint32_t) * kMaxG * kFC, m->stream));
-    for (int c : {C_TOUCHED, C_UPDATED, C_RECORDS, C_RAYS, C_DROPPED, C_TIES, C_FB_BLOCKS, C_FB_VOXELS, C_FB_BIG,
-                  C_ABORT, C_WORDS, C_BUCKET_TOP, C_DONE})
+    for (int c : {C_TOUCHED, C_RECORDS, C_FB_VOXELS, C_FB_BLOCKS, C_ABORT, C_BUCKET_TOP, C_DONE})
         m->h_ctr[c] = 0;
     m->h_ctr[C_BLOCKS] = m->h_ctr[C_BLOCKS_BEFORE] = uint32_t(m->n_blocks);
     m->h_ctr[C_MAPPED] = uint32_t(m->mapped_blocks);
@@ -1251,8 +1221,12 @@ void rollback_group(svx_map* m, svx_scan* s, uint32_t before) {
 
 // Frames per group: up to kMaxG, with at most ~4M pixels of frame slots.
 int group_cap(const svx_scan* s) {
+    static const int knob = [] {  // experiment knob: SVX_GROUP=<frames per group>
+        const char* e = std::getenv("SVX_GROUP");
+        return e ? std::max(1, std::min(kMaxG, std::atoi(e))) : kMaxG;
+    }();
     const uint64_t by_mem = std::max<uint64_t>(1, (uint64_t(1) << 22) / uint64_t(std::max(1, s->P)));
-    return int(std::min<uint64_t>(kMaxG, by_mem));
+    return int(std::min<uint64_t>(uint64_t(knob), by_mem));
 }
 
 }  // namespace
@@ -1287,12 +1261,10 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
         SVX_CUDA(cudaMallocHost(&m->h_outs, sizeof(FrameOut) * n));
         m->h_outs_n = size_t(n);
     }
-    // the word list of a group: at most one entry per 32-voxel word a ray visits
-    const uint64_t want_words = std::min<uint64_t>(uint64_t(s->P) * uint64_t(gmax) + 4096, 0xFFFFFFF0ull);
-    if (m->word_cap < want_words) {
-        m->word_cap = uint32_t(want_words);
-        m->wlist.alloc(m->word_cap);
-    }
+    // per-frame visited-voxel lists (~5 per pixel at cfg2): 8 per pixel, grown on overflow
+    const uint64_t want_vox = std::min<uint64_t>(8ull * uint64_t(s->P) + 4096, 0x7FFFFFFFull);
+    if (m->vox_cap < want_vox) m->vox_cap = uint32_t(want_vox);
+    m->vlist.alloc(uint64_t(m->vox_cap) * uint64_t(gmax));
     // pool headroom for the batch (an exhausted headroom costs one rollback + retry; over-
     // mapping costs physical memory and cuMemCreate time, so size it from the recent rate)
     const uint64_t head =
@@ -1393,8 +1365,7 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
         const int fb = ga + 1 < int(starts.size()) ? starts[ga + 1] : n;
         for (int i = f0; i < fa; ++i) commit(i);
         const uint32_t before = m->h_ctr[C_BLOCKS_BEFORE];
-        const uint32_t blocks_seen = m->h_ctr[C_BLOCKS], recs_seen = m->h_ctr[C_RECORDS],
-                       words_seen = m->h_ctr[C_WORDS];
+        const uint32_t blocks_seen = m->h_ctr[C_BLOCKS], recs_seen = m->h_ctr[C_RECORDS];
         rollback_group(m, s, before);
         f0 = fa;
         if (abort & (kAbortCapacity | kAbortHash | kAbortKey)) {
@@ -1421,10 +1392,11 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
             m->records.alloc(m->rec_cap);
             m->bucket.alloc(m->rec_cap);
             m->bucket2.alloc(m->rec_cap);
+            m->fbdesc.alloc(m->rec_cap);
         }
-        if (abort & kAbortWords) {
-            m->word_cap = uint32_t(std::min<uint64_t>(uint64_t(words_seen) * 2, 0xFFFFFFF0ull));
-            m->wlist.alloc(m->word_cap);
+        if (abort & kAbortVox) {
+            m->vox_cap = uint32_t(std::min<uint64_t>(uint64_t(m->vox_cap) * 2, 0x7FFFFFFFull));
+            m->vlist.alloc(uint64_t(m->vox_cap) * uint64_t(gmax));
         }
         SVX_CUDA(cudaMemsetAsync(m->outs.p, 0, sizeof(FrameOut) * size_t(n), m->stream));
         m->prof_acc.host_resume_ms +=
