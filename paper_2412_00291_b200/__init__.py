@@ -123,7 +123,7 @@ class ProfileC(C.Structure):
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("ms", "launches", "aborts")}
-        names = ["pool", "capacity", "key", "hash", "records", "big_bucket", "voxel_list", "b7"]
+        names = ["pool", "capacity", "key", "hash", "records", "b5", "voxel_list", "b7"]
         d["aborts"] = {names[i]: self.aborts[i] for i in range(8) if self.aborts[i]}
         d["ms"] = {K_NAMES[i]: self.ms[i] for i in range(8) if self.launches[i]}
         d["launches"] = {K_NAMES[i]: self.launches[i] for i in range(8) if self.launches[i]}
@@ -980,15 +980,27 @@ class OccupancyMap:
     def integrate_batch_device(self, d_points_ptr: int, offsets: np.ndarray, stride: int, poses,
                                d_labels_ptr: int = 0, d_conf_ptr: int = 0) -> list:
         """Scans already in HBM (device pointers, e.g. torch tensor .data_ptr())."""
+        return self._batch(d_points_ptr, offsets, stride, poses, d_labels_ptr, d_conf_ptr, 1)
+
+    def integrate_batch_host(self, points_ptr: int, offsets: np.ndarray, stride: int, poses,
+                             labels_ptr: int = 0, conf_ptr: int = 0) -> list:
+        """Scans in host memory (pinned for overlap): copied inside the call."""
+        return self._batch(points_ptr, offsets, stride, poses, labels_ptr, conf_ptr, 0)
+
+    def _batch(self, pts, offsets, stride, poses, labels, conf, on_device) -> list:
         offs = np.ascontiguousarray(offsets, np.uint64)
         nf = len(offs) - 1
         pa = (PoseC * nf)(*poses)
         reps = (OccReportC * nf)()
-        _check(lib().svx_occ_integrate_batch(self._h, C.c_void_p(d_points_ptr),
-                                             C.c_void_p(d_labels_ptr or None),
-                                             C.c_void_p(d_conf_ptr or None), _ptr(offs), stride, 1,
+        _check(lib().svx_occ_integrate_batch(self._h, C.c_void_p(pts), C.c_void_p(labels or None),
+                                             C.c_void_p(conf or None), _ptr(offs), stride, on_device,
                                              pa, nf, reps))
         return list(reps)
+
+    def stream_ptr(self) -> int:
+        p = C.c_void_p()
+        _check(lib().svx_occ_get_stream(self._h, C.byref(p)))
+        return p.value or 0
 
     def lookup(self, coords) -> dict:
         v = np.ascontiguousarray(np.asarray(coords, np.int32).reshape(-1, 3))

@@ -38,6 +38,7 @@ class Scene:
     labels: list = field(default_factory=list)
     strips: list = field(default_factory=list)    # (x0, x1, y0, y1, label) on hplanes
     unlabeled: int = 19
+    cull: float = 0.0  # > 0: a ray only sees primitives within this distance (large scenes)
 
     def add_hplane(self, z, x0, x1, y0, y1, label):
         self.kinds.append(HPLANE)
@@ -88,6 +89,62 @@ def street_canyon(length: float = 560.0, seed: int = 1) -> Scene:
     return s
 
 
+def city(extent: float = 1100.0, seed: int = 7) -> Scene:
+    """A street grid (20 m streets, 80 m blocks) of buildings, parked cars and poles over
+    [-60, extent]^2, for the 2 km cfg4 trajectory (east along the street y = 50, then north
+    along the street x = 1050). Rays see primitives within 120 m."""
+    rng = np.random.default_rng(seed)
+    s = Scene(cull=120.0)
+    s.add_hplane(0.0, -100.0, extent + 100.0, -100.0, extent + 100.0, 0)
+    pitch, street = 100.0, 20.0
+    n = int((extent + 60.0) // pitch) + 1
+    for i in range(n):
+        for j in range(n):
+            x0, y0 = -50.0 + i * pitch + street / 2, -50.0 + j * pitch + street / 2
+            blk = pitch - street
+            # 2-4 buildings per block along its edges
+            x = x0
+            while x < x0 + blk - 6:
+                w = float(rng.uniform(12, 30))
+                w = min(w, x0 + blk - x)
+                d = float(rng.uniform(10, 20))
+                h = float(rng.uniform(8, 45))
+                s.add_box((x, y0, 0.0), (x + w, y0 + d, h), 2 if rng.uniform() < 0.8 else 3)
+                s.add_box((x, y0 + blk - d, 0.0), (x + w, y0 + blk, float(rng.uniform(8, 45))),
+                          2 if rng.uniform() < 0.8 else 3)
+                x += w + float(rng.uniform(2, 8))
+            for side in (0, 1):  # parked cars and poles along the block's x edges
+                yy = y0 - 3.0 if side == 0 else y0 + blk + 1.2
+                xc = x0 + float(rng.uniform(0, 10))
+                while xc < x0 + blk - 5:
+                    L = float(rng.uniform(3.8, 5.2))
+                    s.add_box((xc, yy, 0.0), (xc + L, yy + 1.8, float(rng.uniform(1.4, 1.9))),
+                              13 if rng.uniform() < 0.8 else 14)
+                    xc += L + float(rng.uniform(6, 25))
+                s.add_box((x0 + blk / 2 - 0.1, yy - 1.5, 0.0), (x0 + blk / 2 + 0.1, yy - 1.3,
+                                                                  float(rng.uniform(3, 7))), 5)
+    return s
+
+
+def city_trajectory(n: int, spacing: float = 0.5, z: float = 1.73):
+    """East along the street y = 50 to x = 1040, a 10 m-radius corner, then north along the
+    street x = 1050 (4000 poses at 0.5 m = 2 km)."""
+    poses = []
+    x_turn, y0, r = 1040.0, 50.0, 10.0
+    arc = 0.5 * math.pi * r
+    for i in range(n):
+        d = spacing * i
+        if d <= x_turn:
+            x, y, yaw = d, y0, 0.0
+        elif d <= x_turn + arc:  # quarter circle
+            a = (d - x_turn) / r
+            x, y, yaw = x_turn + r * math.sin(a), y0 + r - r * math.cos(a), a
+        else:
+            x, y, yaw = x_turn + r, y0 + r + d - (x_turn + arc), 0.5 * math.pi
+        poses.append(yaw_pose(x, y, z, yaw))
+    return poses
+
+
 def closed_room(seed: int = 3) -> Scene:
     rng = np.random.default_rng(seed)
     s = Scene()
@@ -107,12 +164,18 @@ def closed_room(seed: int = 3) -> Scene:
     return s
 
 
+_PRIM_CACHE = {}
+
+
 def _prim_tensors(scene: Scene, device):
-    k = torch.tensor(scene.kinds, dtype=torch.int64, device=device)
-    lo = torch.tensor(scene.lo, dtype=torch.float64, device=device)
-    hi = torch.tensor(scene.hi, dtype=torch.float64, device=device)
-    lab = torch.tensor(scene.labels, dtype=torch.int64, device=device)
-    return k, lo, hi, lab
+    key = (id(scene), len(scene.kinds), str(device))
+    if key not in _PRIM_CACHE:
+        k = torch.tensor(scene.kinds, dtype=torch.int64, device=device)
+        lo = torch.tensor(scene.lo, dtype=torch.float64, device=device)
+        hi = torch.tensor(scene.hi, dtype=torch.float64, device=device)
+        lab = torch.tensor(scene.labels, dtype=torch.int64, device=device)
+        _PRIM_CACHE[key] = (k, lo, hi, lab)
+    return _PRIM_CACHE[key]
 
 
 def raycast(scene: Scene, origin, dirs: torch.Tensor, t_min: float = 1e-6, chunk: int = 1 << 17):
@@ -121,6 +184,11 @@ def raycast(scene: Scene, origin, dirs: torch.Tensor, t_min: float = 1e-6, chunk
     device = dirs.device
     k, lo, hi, _ = _prim_tensors(scene, device)
     o = torch.as_tensor(np.asarray(origin, np.float64), device=device)
+    keep = None
+    if scene.cull > 0:  # primitives whose box lies within `cull` of the origin
+        dist = torch.linalg.norm(torch.clamp(torch.maximum(lo - o, o - hi), min=0.0), dim=1)
+        keep = torch.nonzero(dist <= scene.cull).squeeze(1)
+        k, lo, hi = k[keep], lo[keep], hi[keep]
     ts, ps = [], []
     is_h = (k == HPLANE)
     for c0 in range(0, dirs.shape[0], chunk):
@@ -167,6 +235,9 @@ def raycast(scene: Scene, origin, dirs: torch.Tensor, t_min: float = 1e-6, chunk
             upd = tbx < best
             best = torch.where(upd, tbx, best)
             prim = torch.where(upd, idx[ibx], prim)
+        if scene.cull > 0:
+            best = torch.where(best <= scene.cull, best, torch.full_like(best, math.inf))
+            prim = torch.where(prim >= 0, keep[prim.clamp(min=0)], prim)
         ts.append(best)
         ps.append(prim)
     return torch.cat(ts), torch.cat(ps)
@@ -328,6 +399,11 @@ def make(name: str, n_frames: int = None) -> Workload:
                 for k in range(6)]
         return Workload("cfg3-6cam-0.05m", m, 0.05, 0.25, 20, trajectory(n, 0.5, 1.73),
                         street_canyon(), cams=cams)
+    if name == "cfg4":  # city scale: 2 km, 4000 scans at 0.5 m, 0.1 m voxels (key-sharded 2/4/8)
+        n = n_frames or 4000
+        m = ProjectionModel.spinning(1024, 128, 22.5, 22.5)
+        return Workload("cfg4-city-2km-0.1m", m, 0.1, 0.5, 20, city_trajectory(n), city(),
+                        cams=[(_forward_cam(0), np.zeros(3), 1280, 720, 640.0, 640.0, 640.0, 360.0)])
     if name.startswith("cfg5"):  # points-per-scan sweep in a closed room: cfg5-<W>
         W = int(name.split("-")[1]) if "-" in name else 1024
         n = n_frames or 50

@@ -1,7 +1,8 @@
 """Summarise an ncu report: per-kernel duration, throughput, occupancy, pipes, stalls, DRAM bytes.
 
-usage: ncu_summary.py REPORT [JSON_OUT]   (JSON_OUT: per-kernel mean duration and DRAM
-bytes per launch, read by bench.py for the roofline `traffic` field)"""
+usage: ncu_summary.py REPORT [JSON_OUT] [G]   (JSON_OUT: per-kernel mean duration and DRAM
+bytes per launch, read by bench.py for the roofline `traffic` field; G = frames per launch
+of the frame-group kernels (k_fold runs once per frame))"""
 import csv
 import json
 import subprocess
@@ -10,6 +11,7 @@ from collections import defaultdict
 
 rep = sys.argv[1]
 json_out = sys.argv[2] if len(sys.argv) > 2 else None
+group = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(raw.splitlines()))
 hdr, units = rows[0], rows[1]
@@ -65,5 +67,6 @@ for r in rows[2:]:
 
 if json_out:
     res = {k: {"launches": v["launches"], "us_per_launch": v["us"] / v["launches"],
-               "dram_bytes_per_launch": v["dram_bytes"] / v["launches"]} for k, v in agg.items()}
+               "dram_bytes_per_launch": v["dram_bytes"] / v["launches"],
+               "frames_per_launch": 1 if k == "k_fold" else group} for k, v in agg.items()}
     json.dump({"report": rep.split("/")[-1], "kernels": res}, open(json_out, "w"), indent=1)
