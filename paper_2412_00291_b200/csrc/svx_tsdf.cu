@@ -57,6 +57,7 @@ namespace svx {
 struct GroupConsts {
     Model m;
     double tau, max_range, alpha_eps, nu, inv_nu;
+    double inv_2tau;      // 1 / (2 tau), rounded: the weight's quotient estimate
     double ca_hi, ca_lo;  // cos(alpha_eps) +- 1e-12: margins of the alpha < eps branch
     float min_clamp;
     // band_all_own(): half voxel diagonal, safe min range, min sin(polar) over the
@@ -224,6 +225,35 @@ struct Accum {
     double wd, w, wx, wy, wz;
 };
 
+// ---- exact f32 results from one-reciprocal estimates
+// The reference stores float(x / y) (or float(clamp(x / y))) of a correctly rounded double
+// quotient. An estimate q with |q - fl(x / y)| <= kQuotTol |q| decides that float whenever
+// both ends of [q - kQuotTol |q|, q + kQuotTol |q|] round to the same float (rounding is
+// monotonic); otherwise the exact division is used. The estimates below are within ~5 ulp
+// (2^-52 relative each): kQuotTol = 4e-15 is ~18 ulp. Undecided cases need the exact
+// double to lie within 4e-15 of a float rounding boundary (relative spacing 6e-8).
+constexpr double kQuotTol = 4e-15;
+
+// 1 / b for 1e-300 < b < 1e300: hardware estimate + two Newton steps (rel. error ~2^-52).
+__device__ __forceinline__ double rcp_est(double b) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+    double e = __fma_rn(-b, r, 1.0);
+    r = __fma_rn(r, e, r);
+    e = __fma_rn(-b, r, 1.0);
+    return __fma_rn(r, e, r);
+}
+
+// float(x / y) for y > 0.
+__device__ __forceinline__ float f32_div(double x, double y) {
+    if (y > 1e-300 && y < 1e300) {
+        const double q = x * rcp_est(y), d = fabs(q) * kQuotTol;
+        const float lo = float(q - d), hi = float(q + d);
+        if (__float_as_uint(lo) == __float_as_uint(hi)) return lo;
+    }
+    return float(x / y);
+}
+
 // nonprojective_distance (tsdf_integrator.cpp:39-46)
 __device__ inline double nonprojective_distance(double psi, double theta, double alpha, double eps) {
     double st, ct;
@@ -263,12 +293,13 @@ __device__ inline float gamma_nonprojective(const GroupConsts& c, double psi, do
         const double sa = sqrt((1.0 - ca) * (1.0 + ca));
         if (sa > 1e-6) {
             const double a = ca - 1.0;
-            const double t1 = fabs(a * st / sa), t2 = fabs(ct * psi);
+            const double inv_sa = rcp_est(sa);  // (a st / sa within ~4 ulp: in the 2e-15 term)
+            const double t1 = fabs(a * st * inv_sa), t2 = fabs(ct * psi);
             const double mag = t1 + t2;
             d = psi >= 0.0 ? mag : -mag;
             const double da = kAbs + kRel * fabs(a), dst = kAbs + kRel * st, dsa = kAbs + kRel * sa;
-            e = 1.01 * ((fabs(a) * dst + st * da) / sa + t1 * dsa / sa + fabs(psi) * (kAbs + kRel * fabs(ct))) +
-                1e-15 * mag;
+            e = 1.01 * ((fabs(a) * dst + st * da + t1 * dsa) * inv_sa + fabs(psi) * (kAbs + kRel * fabs(ct))) +
+                2e-15 * mag;
             fast = true;
         }
     }
@@ -314,11 +345,23 @@ __device__ inline Term measure_term(const GroupConsts& c, d3 origin, const PixCa
     } else {
         gamma = truncate_f(psi, c.tau);
     }
-    // observation_weight (tsdf_integrator.cpp:48-51)
-    double wr = (psi + c.tau) / (2.0 * c.tau);
+    // observation_weight (tsdf_integrator.cpp:48-51): float(clamp((psi + tau) / 2 tau)),
+    // from the quotient estimate when that decides the float, else the exact division
     const double lo = double(c.min_clamp);
-    wr = wr < lo ? lo : (1.0 < wr ? 1.0 : wr);
-    const float w_obs = float(wr);
+    float w_obs;
+    {
+        const double q = (psi + c.tau) * c.inv_2tau, dq = fabs(q) * kQuotTol;
+        const double q0 = q - dq, q1 = q + dq;
+        const float f0 = float(q0 < lo ? lo : (1.0 < q0 ? 1.0 : q0));
+        const float f1 = float(q1 < lo ? lo : (1.0 < q1 ? 1.0 : q1));
+        if (__float_as_uint(f0) == __float_as_uint(f1)) {
+            w_obs = f0;
+        } else {
+            double wr = (psi + c.tau) / (2.0 * c.tau);
+            wr = wr < lo ? lo : (1.0 < wr ? 1.0 : wr);
+            w_obs = float(wr);
+        }
+    }
     t.wg = w_obs * gamma;
     t.w = w_obs;
     if (have_normal) {
@@ -342,17 +385,35 @@ __device__ inline void accumulate(Accum& acc, const Term& t) {
 }
 
 // accumulate-then-merge fold (tsdf_integrator.cpp:239-247)
+// (the f32 quotients through f32_div / the rsqrt estimate: the same floats, fewer FP64
+// divisions and square roots)
 __device__ inline void fold(svx_tsdf_voxel& vox, const Accum& acc) {
     const double w_old = double(vox.weight);
-    vox.distance = float((w_old * double(vox.distance) + acc.wd) / (w_old + acc.w));
+    vox.distance = f32_div(w_old * double(vox.distance) + acc.wd, w_old + acc.w);
     vox.weight = float(w_old + acc.w);
     const d3 bl = mk(w_old * double(vox.gradient[0]) + acc.wx, w_old * double(vox.gradient[1]) + acc.wy,
                      w_old * double(vox.gradient[2]) + acc.wz);
-    const double nrm = sqrt(dot3(bl, bl));
-    if (nrm > 1e-12) {
-        vox.gradient[0] = float(bl.x / nrm);
-        vox.gradient[1] = float(bl.y / nrm);
-        vox.gradient[2] = float(bl.z / nrm);
+    const double s2 = dot3(bl, bl);
+    // norm > 1e-12 decided on s2 away from 1e-24; float(bl_i / norm) from bl_i * rsqrt(s2)
+    // (within ~3 ulp of bl_i / fl(sqrt(s2))) when that decides the float
+    bool upd;
+    if (s2 > 1.0000001e-24) upd = true;
+    else if (s2 < 0.9999999e-24) upd = false;
+    else upd = sqrt(s2) > 1e-12;
+    if (!upd) return;
+    const double r = s2 < 1e300 ? rsqrt(s2) : 0.0;
+    const double b[3] = {bl.x, bl.y, bl.z};
+    double nrm = 0.0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const double q = b[i] * r, d = fabs(q) * kQuotTol;
+        const float f0 = float(q - d), f1 = float(q + d);
+        if (r > 0.0 && __float_as_uint(f0) == __float_as_uint(f1)) {
+            vox.gradient[i] = f0;
+        } else {
+            if (nrm == 0.0) nrm = sqrt(s2);
+            vox.gradient[i] = float(b[i] / nrm);
+        }
     }
 }
 
@@ -1019,6 +1080,7 @@ GroupConsts make_consts(svx_map* m, svx_scan* s, const svx_integrator_cfg& cfg, 
     c.m = s->dm;
     const double nu = double(m->cfg.voxel_size);
     c.tau = cfg.truncation > 0.f ? double(cfg.truncation) : double(m->cfg.truncation);
+    c.inv_2tau = 1.0 / (2.0 * c.tau);
     c.max_range = cfg.max_range;
     c.alpha_eps = cfg.alpha_epsilon;
     if (!(cfg.alpha_epsilon > 0.0)) {  // alpha < eps never holds
