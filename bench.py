@@ -275,6 +275,7 @@ def run_tsdf(args, world, rank, local):
     import torch.distributed as dist
 
     import paper_2412_00291_b200 as svx
+    from paper_2412_00291_b200 import dist as sdist
     from paper_2412_00291_b200 import workload as W
 
     torch.cuda.set_device(local)
@@ -314,12 +315,8 @@ def run_tsdf(args, world, rank, local):
 
     def make_store():
         st = svx.VoxelStore(cfg, device=local)
-        st.set_shard(rank, world)
-        # diagnostic: one rank's share of an N-way key shard on a single GPU
-        # (SVX_SIM_SHARD="r,N"), for per-rank cost estimates without N GPUs
-        sim = os.environ.get("SVX_SIM_SHARD")
-        if sim and world == 1:
-            st.set_shard(*[int(x) for x in sim.split(",")])
+        if world > 1:
+            st.set_shard(rank, world)
         return st
 
     def run_leg(store, host_pts=None, clocks=None):
@@ -355,7 +352,12 @@ def run_tsdf(args, world, rank, local):
                     pts_all[a:b].copy_(host_pts[a:b], non_blocking=True)
                 dist.broadcast(pts_all[a:b], 0)
                 torch.cuda.current_stream().synchronize()
-            if host_pts is not None and world == 1:
+            if world > 1:
+                # exchange mode: each rank casts its share of the rays, one all-to-all of
+                # the visits per frame group, each rank folds the blocks it owns
+                reps = sdist.integrate_sharded(store, wl.model, pts_all.data_ptr() + a * 12, rel, 3,
+                                               poses[f0:f1], icfg)
+            elif host_pts is not None:
                 reps = store.integrate_clouds_host(wl.model, host_pts.data_ptr() + a * 12, rel, 3,
                                                    poses[f0:f1], icfg)
             else:
@@ -477,7 +479,8 @@ def run_tsdf(args, world, rank, local):
                "config": {"workload": describe(args.workload, n_frames), "frames_total": n_frames,
                           "scans_per_step": spp, "points_per_step": pts_t / args.steps,
                           "l2": "inputs > L2: ~150 MB of fresh scans per step; map state > 1 GB",
-                          "parallelism": f"key-sharded map x{world}" if world > 1 else "1 GPU",
+                          "parallelism": (f"key-sharded map x{world}, ray tiles round robin, one NCCL "
+                                          f"all-to-all of visits per 16-frame group") if world > 1 else "1 GPU",
                           "map_blocks": blocks_final},
                "voxel_updates_per_s": upd_t / total_s,
                "rays_per_s": prof.rays / total_s,
@@ -768,6 +771,85 @@ def run_carve(args, world, rank, local):
     return 0
 
 
+# ------------------------------------------------------------------ multi-GPU emulation
+
+def run_emulated(args):
+    """The multi-GPU data plane with N ranks emulated on ONE GPU (dist.emulate_sharded: the
+    ranks' calls run one after another, the all-to-all is a device copy). Per frame group
+    the cost of rank r is its xbegin + xend time; an N-GPU step would take the max over
+    ranks plus the all-to-all of the visit entries (estimated at the measured 770 GB/s
+    NVLink peer bandwidth, B200_PROFILING.md). Not a measured multi-GPU number: the
+    per-rank cost model behind DESIGN.md section 6's scaling estimate."""
+    import torch
+
+    import paper_2412_00291_b200 as svx
+    from paper_2412_00291_b200 import dist as sdist
+    from paper_2412_00291_b200 import workload as W
+    dev = torch.device("cuda", 0)
+    spp = args.scans_per_step
+    n_frames = (args.warmup + args.steps) * spp
+    wl = W.make(args.workload, n_frames)
+    if args.workload == "cfg2" and n_frames * 0.5 + 60 > 560:
+        wl.scene = W.street_canyon(length=n_frames * 0.5 + 60)
+    chunks = [p for p, _ in wl.scans(device=dev)]
+    offs = np.zeros(n_frames + 1, np.uint64)
+    offs[1:] = np.cumsum([c.shape[0] for c in chunks])
+    pts = torch.cat(chunks).contiguous()
+    del chunks
+    poses = [wl.pose(i) for i in range(n_frames)]
+    cfg = svx.MapConfig(wl.voxel_size, wl.truncation, wl.num_labels, 1 << 21)
+    icfg = svx.IntegratorConfig()
+    out = {"emulated": True, "workload": describe(args.workload, n_frames), "scans_per_step": spp, "ranks": {}}
+    for N in args.emulate_ranks:
+        stores = []
+        for r in range(N):
+            st = svx.VoxelStore(cfg, 0)
+            if N > 1:
+                st.set_shard(r, N)
+            stores.append(st)
+        step_max, step_sum, xbytes, pts_t = [], [], [], 0
+        for s in range(args.warmup + args.steps):
+            f0, f1 = s * spp, (s + 1) * spp
+            rel = offs[f0:f1 + 1] - offs[f0]
+            timers = []
+            if N > 1:
+                sdist.emulate_sharded(stores, wl.model, pts.data_ptr() + int(offs[f0]) * 12, rel, 3, poses[f0:f1],
+                                      icfg, timers=timers)
+                tmax = sum(max(b + e for b, e in zip(t["xbegin_ms"], t["xend_ms"])) for t in timers)
+                tsum = sum(sum(t["xbegin_ms"]) + sum(t["xend_ms"]) for t in timers)
+                ent = sum(sum(t["entries"]) for t in timers)
+            else:
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                stores[0].integrate_clouds_device(wl.model, pts.data_ptr() + int(offs[f0]) * 12, rel, 3,
+                                                  poses[f0:f1], icfg)
+                tmax = tsum = (time.perf_counter() - t0) * 1e3
+                ent = 0
+            if s >= args.warmup:
+                step_max.append(tmax)
+                step_sum.append(tsum)
+                xbytes.append(16 * ent)
+                pts_t += int(offs[f1] - offs[f0])
+        # all-to-all: each rank sends/receives ~1/N of the entries; time at 770 GB/s per
+        # direction per GPU (measured peer copy), per step
+        xchg_ms = [b / N / 770e9 * 1e3 for b in xbytes]
+        t_step = [a + x for a, x in zip(step_max, xchg_ms)]
+        out["ranks"][N] = {"max_rank_ms_per_step": float(np.mean(step_max)),
+                           "all_ranks_ms_per_step": float(np.mean(step_sum)),
+                           "exchange_bytes_per_step": float(np.mean(xbytes)),
+                           "exchange_ms_per_step_est": float(np.mean(xchg_ms)),
+                           "points_per_s_est": pts_t / (sum(t_step) / 1e3),
+                           "blocks_per_rank": [st.block_count() for st in stores]}
+        for st in stores:
+            st.close()
+    base = out["ranks"].get(1, {}).get("points_per_s_est")
+    if base:
+        for N, r in out["ranks"].items():
+            r["speedup_vs_1"] = r["points_per_s_est"] / base
+    print(json.dumps(out))
+    return 0
+
+
 # ------------------------------------------------------------------ cfg5 sweep
 
 def run_sweep(args):
@@ -864,6 +946,8 @@ def main():
     ap.add_argument("--sweep-widths", type=int, nargs="*",
                     default=[80, 160, 320, 640, 1280, 2560, 5120, 10240, 16384])
     ap.add_argument("--sweep-scans", type=int, default=64)
+    ap.add_argument("--emulate-ranks", type=int, nargs="*", default=None,
+                    help="emulate the multi-GPU data plane with these rank counts on one GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-json", default="")
@@ -880,6 +964,8 @@ def main():
         return run_reference(args, world, rank)
     if args.sweep:
         return run_sweep(args) if rank == 0 else 0
+    if args.emulate_ranks:
+        return run_emulated(args) if rank == 0 else 0
     if args.carve:
         return run_carve(args, world, rank, local)
     if args.workload == "cfg3":

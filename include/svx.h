@@ -223,20 +223,45 @@ svx_status svx_integrate_cloud(svx_map* map, svx_scan* scan, const float* points
                                int32_t stride, int32_t ptr_is_device, const svx_pose* pose,
                                const svx_integrator_cfg* cfg, svx_frame_report* report);
 /* A sequence of posed clouds already resident in HBM: frame f uses points
- * [offsets[f], offsets[f+1]) and poses[f]. No host synchronisation between
- * frames unless pool growth is needed; reports[f] filled at the end. */
+ * [offsets[f], offsets[f+1]) and poses[f]. Frames are integrated in groups of up to
+ * 16 (one launch sequence per group: results identical to one integrate_frame call per
+ * frame); no host synchronisation inside the call unless a buffer or the pool must
+ * grow; reports[f] filled at the end. */
 svx_status svx_integrate_clouds_device(svx_map* map, svx_scan* scan, const float* d_points,
                                        const uint64_t* offsets, int32_t stride,
                                        const svx_pose* poses, int32_t n_frames,
                                        const svx_integrator_cfg* cfg, svx_frame_report* reports);
 /* The same sequence with the points in HOST memory (pinned for full overlap): the
- * points of the next frames are copied to the device on a copy stream while the
- * current frame integrates (a ring of 4 staged frames) — the per-frame body of
- * cmd_integrate with its prefetcher (semvox_main.cpp:30-76,121-124) in one call. */
+ * points of the next frame group are copied to the device on a copy stream while the
+ * current group integrates — the per-frame body of cmd_integrate with its prefetcher
+ * (semvox_main.cpp:30-76,121-124) in one call. */
 svx_status svx_integrate_clouds(svx_map* map, svx_scan* scan, const float* points,
                                 const uint64_t* offsets, int32_t stride, const svx_pose* poses,
                                 int32_t n_frames, const svx_integrator_cfg* cfg,
                                 svx_frame_report* reports);
+/* Multi-GPU data plane (exchange mode, SURVEY.md 8(e) "ray-partitioned DDA + one
+ * all-to-all visit exchange"; no reference analogue: the reference is single-process).
+ * On a key-sharded map (svx_map_set_shard, world >= 2) one group of n_frames <= 16
+ * clouds (device pointers; every rank passes the same clouds) is integrated in two calls
+ * around the caller's all-to-all (NCCL):
+ *   xbegin  projects the group and casts this rank's share of the rays (round robin over
+ *           pixel tiles); visits of blocks another rank owns are returned as 16-byte
+ *           entries packed by destination rank (*d_send: a device buffer valid until the
+ *           next xbegin). send_meta[world][17]: per destination, the number of entries,
+ *           then per frame of the group the number of voxel bits sent (sizes the
+ *           receiver's lists without a synchronisation).
+ *   xend    applies the entries received from all ranks (d_recv, device memory, in source
+ *           rank order; recv_meta[world][17] = what each source's send_meta held for this
+ *           rank) and folds this rank's blocks; reports[f] hold this rank's share
+ *           (updated_voxels / new_blocks summed over ranks = the unsharded values).
+ * The union of the ranks' maps equals the map one rank builds alone, byte for byte. */
+svx_status svx_integrate_clouds_xbegin(svx_map* map, svx_scan* scan, const float* d_points,
+                                       const uint64_t* offsets, int32_t stride,
+                                       const svx_pose* poses, int32_t n_frames,
+                                       const svx_integrator_cfg* cfg, uint64_t* send_meta,
+                                       const void** d_send);
+svx_status svx_integrate_clouds_xend(svx_map* map, const void* d_recv,
+                                     const uint64_t* recv_meta, svx_frame_report* reports);
 /* SemanticIntegrator::integrate_labels — semantic_integrator.cpp:91-165, with
  * exact block-level frustum culling (results identical to the O(map) sweep). */
 svx_status svx_integrate_labels(svx_map* map, const svx_label_image* img,

@@ -130,6 +130,7 @@ class ProfileC(C.Structure):
         return d
 
 
+XMETA = 17  # exchange-mode metadata per destination: entries, voxel bits of frames 0..15
 TSDF_DTYPE = np.dtype([("distance", "<f4"), ("weight", "<f4"), ("gradient", "<f4", (3,))])
 BLOCK_VOXELS = 512
 
@@ -199,6 +200,9 @@ def _sig(lib: C.CDLL) -> None:
                                             C.POINTER(IntegratorCfg), P]),
         "svx_integrate_clouds": (S, [P, P, P, P, C.c_int32, P, C.c_int32,
                                      C.POINTER(IntegratorCfg), P]),
+        "svx_integrate_clouds_xbegin": (S, [P, P, P, P, C.c_int32, P, C.c_int32, C.POINTER(IntegratorCfg),
+                                            P, C.POINTER(P)]),
+        "svx_integrate_clouds_xend": (S, [P, P, P, P]),
         "svx_integrate_labels_batch": (S, [P, P, C.c_int32, C.c_int32, C.POINTER(SemanticCfg), P]),
         "svx_integrate_labels": (S, [P, C.POINTER(LabelImageC), C.POINTER(SemanticCfg),
                                      C.POINTER(FrameReportC)]),
@@ -420,6 +424,7 @@ class VoxelStore:
             _check(lib().svx_map_create(C.byref(self.cfg.c()), device, C.byref(self._h)))
         self.device = device
         self._scans: dict = {}
+        self._world = 1
 
     def close(self) -> None:
         if getattr(self, "_h", None) and self._h.value:
@@ -458,6 +463,7 @@ class VoxelStore:
 
     def set_shard(self, rank: int, world: int) -> None:
         _check(lib().svx_map_set_shard(self._h, rank, world))
+        self._world = world
 
     def profile_enable(self, on: bool = True) -> None:
         _check(lib().svx_profile_enable(self._h, int(on)))
@@ -491,6 +497,32 @@ class VoxelStore:
         _check(lib().svx_integrate_clouds(self._h, self.scan(model), C.c_void_p(points_ptr), _ptr(offs),
                                           stride, C.cast(parr, C.c_void_p), n, C.byref(cfg.c()),
                                           C.cast(reps, C.c_void_p)))
+        return [FrameReport.of(r) for r in reps]
+
+    # ---- multi-GPU data plane (exchange mode): see paper_2412_00291_b200.dist
+    def xbegin(self, model: ProjectionModel, d_points_ptr: int, offsets: np.ndarray, stride: int,
+               poses: list, cfg: "IntegratorConfig"):
+        """svx_integrate_clouds_xbegin: one group (<= 16 clouds in HBM) on a key-sharded map.
+        Returns (send_meta[world][17]: entries, then voxel bits per frame, per destination;
+        device pointer of the 16-byte entries packed by destination)."""
+        n = len(poses)
+        offs = np.ascontiguousarray(np.asarray(offsets, np.uint64))
+        parr = (PoseC * n)(*poses)
+        meta = np.zeros((self._world, XMETA), np.uint64)
+        ptr = C.c_void_p()
+        _check(lib().svx_integrate_clouds_xbegin(self._h, self.scan(model), C.c_void_p(d_points_ptr), _ptr(offs),
+                                                 stride, C.cast(parr, C.c_void_p), n, C.byref(cfg.c()),
+                                                 _ptr(meta), C.byref(ptr)))
+        self._xn = n
+        return meta, int(ptr.value or 0)
+
+    def xend(self, d_recv_ptr: int, recv_meta: np.ndarray) -> list:
+        """svx_integrate_clouds_xend: the entries received from all ranks (device pointer,
+        source-rank order) and their senders' metadata rows for this rank ([world][17])."""
+        rm = np.ascontiguousarray(np.asarray(recv_meta, np.uint64).reshape(self._world, XMETA))
+        reps = (FrameReportC * self._xn)()
+        _check(lib().svx_integrate_clouds_xend(self._h, C.c_void_p(d_recv_ptr or None), _ptr(rm),
+                                               C.cast(reps, C.c_void_p)))
         return [FrameReport.of(r) for r in reps]
 
     def get_or_allocate_block(self, bc) -> bool:

@@ -101,11 +101,17 @@ void free_map(svx_map* m) {
                     (void*)m->fbslots, (void*)m->fbclaim})
         if (p) cudaFree(p);
     if (m->h_ctr) cudaFreeHost(m->h_ctr);
+    if (m->h_fctr) cudaFreeHost(m->h_fctr);
     if (m->h_outs) cudaFreeHost(m->h_outs);
     m->outs.release();
     m->bucket.release();
     m->bucket2.release();
     m->fbdesc.release();
+    m->xsend.release();
+    m->xpack.release();
+    m->xaux.release();
+    m->xcnt.release();
+    if (m->xstate && m->xstate_free) m->xstate_free(m->xstate);
     m->vlist.release();
     prof_resolve(m);
     for (cudaEvent_t e : m->prof_free) cudaEventDestroy(e);
@@ -173,6 +179,7 @@ svx_map* create_map(const svx_map_cfg& cfg, int device) {
         m->bucket2.alloc(m->rec_cap);
         m->fbdesc.alloc(m->rec_cap);
         SVX_CUDA(cudaMallocHost(&m->h_ctr, sizeof(uint32_t) * kNumCounters));
+        SVX_CUDA(cudaMallocHost(&m->h_fctr, sizeof(uint32_t) * kMaxG * kFC));
         std::memset(m->h_ctr, 0, sizeof(uint32_t) * kNumCounters);
         SVX_CUDA(cudaMemsetAsync(m->keys, 0xFF, 8ull * m->cap, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->vals, 0xFF, 4ull * m->cap, m->stream));  // kInvalid: no block yet
@@ -1065,6 +1072,35 @@ svx_status svx_integrate_clouds(svx_map* m, svx_scan* s, const float* points, co
         const double ms =
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         for (int32_t f = 0; f < n_frames; ++f) reports[f].elapsed_ms = ms / n_frames;
+    });
+}
+
+svx_status svx_integrate_clouds_xbegin(svx_map* m, svx_scan* s, const float* d_points, const uint64_t* offsets,
+                                       int32_t stride, const svx_pose* poses, int32_t n_frames,
+                                       const svx_integrator_cfg* cfg, uint64_t* send_meta, const void** d_send) {
+    return guarded([&] {
+        require(m && s && cfg && send_meta && d_send && poses && offsets, SVX_INVALID_ARGUMENT, "null argument");
+        require(s->map == m, SVX_INVALID_ARGUMENT, "scan belongs to another map");
+        require(stride >= 3, SVX_INVALID_ARGUMENT, "point stride must be >= 3");
+        DeviceGuard g(m->device);
+        std::vector<FrameJob> jobs(size_t(std::max(n_frames, 0)));
+        for (int32_t f = 0; f < n_frames; ++f) {
+            validate_pose(poses[f]);
+            require(offsets[f + 1] >= offsets[f], SVX_INVALID_ARGUMENT, "offsets must not decrease");
+            require(offsets[f + 1] - offsets[f] < (1ull << 32), SVX_INVALID_ARGUMENT, "too many points in one cloud");
+            jobs[f] = FrameJob{s, to_pose(poses[f]), d_points + offsets[f] * stride, offsets[f + 1] - offsets[f],
+                               stride, true};
+        }
+        run_group_xbegin(m, jobs.data(), n_frames, *cfg, send_meta, d_send);
+    });
+}
+
+svx_status svx_integrate_clouds_xend(svx_map* m, const void* d_recv, const uint64_t* recv_meta,
+                                     svx_frame_report* reports) {
+    return guarded([&] {
+        require(m && reports && recv_meta, SVX_INVALID_ARGUMENT, "null argument");
+        DeviceGuard g(m->device);
+        run_group_xend(m, d_recv, recv_meta, reports);
     });
 }
 

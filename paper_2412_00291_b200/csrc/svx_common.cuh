@@ -357,6 +357,7 @@ enum AbortBits : uint32_t {
     kAbortKey = 4,       // block coordinate outside the key range
     kAbortHash = 8,      // hash table full (implies capacity)
     kAbortRecords = 16,  // fallback record buffer too small: grow, retry
+    kAbortXchg = 32,     // exchange send list too small (multi-GPU data plane): grow, retry
     kAbortVox = 64       // visited-voxel list too small: grow, retry
 };
 

@@ -200,6 +200,7 @@ struct svx_map {
     svx::VmmArray mask_pool;         // [blocks][kMaskWords] u32 visit masks, parallel to the pool
     uint64_t mask_zeroed = 0;        // blocks of mask_pool zero-filled so far
     uint32_t* fctr = nullptr;        // [kMaxG][kFC] per-frame counters of the current group
+    uint32_t* h_fctr = nullptr;      // pinned mirror (exchange mode)
     svx::DevBuf<unsigned long long> records;  // fallback visit records: slot<<41|lin<<32|g<<28|pixel
     svx::DevBuf<unsigned long long> records_alt;  // capacity path: visited block keys
     svx::DevBuf<uint8_t> sort_tmp;
@@ -215,6 +216,13 @@ struct svx_map {
     uint32_t rec_cap = 0;
     svx::DevBuf<uint32_t> vlist;     // per frame of the group: its visited voxels, (pool idx << 9) | voxel
     uint32_t vox_cap = 0;            // entries per frame
+    // exchange mode (multi-GPU data plane, svx_tsdf.cu): per-destination send lists of
+    // 16-byte visit entries, the packed send buffer, the received entries' ingest scratch
+    svx::DevBuf<uint4> xsend, xpack, xaux;
+    svx::DevBuf<uint32_t> xcnt;      // [world] entries per destination
+    uint32_t xcap = 0;               // send-list entries per destination
+    void* xstate = nullptr;          // the group between svx_integrate_clouds_xbegin and _xend
+    void (*xstate_free)(void*) = nullptr;
     // per-frame results of a batch
     svx::DevBuf<svx::FrameOut> outs;
     svx::FrameOut* h_outs = nullptr;
@@ -335,6 +343,14 @@ struct FrameJob {
 // the end (plus once per abort + retry, rare). Fills one report per frame.
 void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cfg& cfg,
                 svx_frame_report* reps);
+// Exchange mode (multi-GPU data plane): one frame group in two halves around
+// the caller's all-to-all. xbegin projects the group and casts this rank's share of its
+// rays; visits of blocks other ranks own are returned packed by destination (16-byte
+// entries, send_counts[world]). xend applies the entries received from all ranks and folds
+// this rank's blocks.
+void run_group_xbegin(svx_map* m, const FrameJob* jobs, int G, const svx_integrator_cfg& cfg,
+                      uint64_t* send_meta, const void** d_send);
+void run_group_xend(svx_map* m, const void* d_recv, const uint64_t* recv_meta, svx_frame_report* reps);
 void reset_frame_state(svx_map* m);
 // Writes the host's block/layer/mapping counts into the device counters.
 void push_block_counters(svx_map* m);

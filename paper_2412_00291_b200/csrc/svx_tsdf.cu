@@ -47,6 +47,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <memory>
 #include <vector>
 
 #include "svx_map.hpp"
@@ -65,6 +66,10 @@ struct GroupConsts {
     float delta, min_range_safe, sin_min, dphi_f, dtheta_f;
     int nonproj, drop_unreliable, has_normals;
     int32_t shard_rank, shard_world;
+    // exchange mode (multi-GPU data plane): this rank casts the rays of its
+    // share of the tiles and sends the visits of blocks other ranks own to them
+    int exchange;
+    uint32_t xcap;  // send-list entries per destination rank
     uint32_t serial;    // group serial (touched stamps)
     uint32_t G, P, VW;  // frames, pixels per frame, valid-bit words per frame
     uint32_t tiles;     // band tiles per frame
@@ -539,6 +544,30 @@ __device__ inline void zero_block(svx_tsdf_voxel* __restrict__ pool, uint32_t id
     for (int i = lane; i < kBlockVoxels * 5 / 4; i += lanes) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
+// Send metadata per destination rank: [0] entries, [1 + g] voxel bits of frame g (a bound
+// on the receiver's new voxel-list entries of frame g).
+constexpr int kXMeta = 1 + kMaxG;
+constexpr int kMaxXWorld = 16;  // ranks supported by exchange mode
+
+// ---- exchange mode: visits of blocks another rank owns go to that rank as 16-byte
+// entries (x, y = packed block key; z bit 31 = fallback record; word entry: z = g << 4 | w,
+// w = the voxel bits of mask word w in frame g; record entry: z = g << 9 | voxel,
+// w = pixel). The owner applies them with k_ingest exactly as its own band would have.
+__device__ inline void send_remote(const GroupConsts& c, uint4* __restrict__ xsend, uint32_t* __restrict__ xcnt,
+                                   uint32_t* __restrict__ ctr, uint64_t key, uint32_t z, uint32_t w) {
+    const int32_t dest = owner_of(key, c.shard_world);
+    uint32_t* meta = xcnt + dest * kXMeta;
+    const uint32_t pos = atomicAdd(&meta[0], 1u);
+    if (!(z & 0x80000000u)) atomicAdd(&meta[1 + (z >> 4)], uint32_t(__popc(w)));  // voxel bits per frame
+    if (pos < c.xcap)
+        xsend[uint64_t(dest) * c.xcap + pos] = make_uint4(uint32_t(key), uint32_t(key >> 32), z, w);
+    else
+        atomicOr(&ctr[C_ABORT], kAbortXchg);
+}
+__device__ inline bool is_remote(const GroupConsts& c, uint64_t key) {
+    return c.exchange && owner_of(key, c.shard_world) != c.shard_rank;
+}
+
 // Per-visit work on global state (no tile staging): the path a visit takes when its tile's
 // shared tables are full. Same effect as the staged path.
 __device__ void visit_global(const GroupConsts& c, uint32_t g, HashView h, uint64_t* __restrict__ block_keys,
@@ -546,7 +575,13 @@ __device__ void visit_global(const GroupConsts& c, uint32_t g, HashView h, uint6
                              uint32_t* __restrict__ fm, uint32_t* __restrict__ fbcnt,
                              unsigned long long* __restrict__ rec, svx_tsdf_voxel* __restrict__ pool,
                              uint32_t* __restrict__ vlist, uint32_t* __restrict__ fctr,
+                             uint4* __restrict__ xsend, uint32_t* __restrict__ xcnt,
                              uint32_t* __restrict__ ctr, uint64_t key, int lin, bool fb, uint32_t p) {
+    if (is_remote(c, key)) {
+        send_remote(c, xsend, xcnt, ctr, key, (g << 4) | uint32_t(lin >> 5), 1u << (lin & 31));
+        if (fb) send_remote(c, xsend, xcnt, ctr, key, 0x80000000u | (g << 9) | uint32_t(lin), p);
+        return;
+    }
     const SlotRef r = find_or_insert(c, h, block_keys, ctr, key);
     if (r.slot == kInvalid) return;
     if (atomicExch(&stamp[r.slot], c.serial) != c.serial) touched[atomicAdd(&ctr[C_TOUCHED], 1u)] = r.slot;
@@ -586,7 +621,8 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
        uint64_t* __restrict__ block_keys, uint32_t* __restrict__ stamp, uint32_t* __restrict__ touched,
        uint32_t* __restrict__ fm, uint32_t* __restrict__ fbcnt, unsigned long long* __restrict__ rec,
        svx_tsdf_voxel* __restrict__ pool, uint32_t* __restrict__ vlist,
-       uint32_t* __restrict__ fctr, uint32_t* __restrict__ ctr) {
+       uint32_t* __restrict__ fctr, uint4* __restrict__ xsend, uint32_t* __restrict__ xcnt,
+       uint32_t* __restrict__ ctr) {
     pdl_wait();
     pdl_trigger();
     if (cta_aborted(ctr)) return;  // the group is rolled back and retried: stop early
@@ -654,8 +690,11 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
         }
         cache[p] = pc;
     }
-    // band ray (tsdf_integrator.cpp:123-131)
-    const bool cast = in_range && !(c.drop_unreliable && c.has_normals && !sc.valid[pg + p]);
+    // band ray (tsdf_integrator.cpp:123-131); in exchange mode only the rays of this rank's
+    // tiles (round robin over the group's tiles); every rank still writes the whole pixel
+    // cache, which the folds of its own blocks read
+    const bool my_tile = !c.exchange || int(blockIdx.x % uint32_t(c.shard_world)) == c.shard_rank;
+    const bool cast = my_tile && in_range && !(c.drop_unreliable && c.has_normals && !sc.valid[pg + p]);
     if (cast) {
         warp_agg_inc(&fctr[g * kFC + FC_RAYS]);
         const d3 tr = scale3(c.tau, ray);  // (q - o).normalized() == (q - o) / range
@@ -678,7 +717,9 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
             const uint64_t key = pack_key(bx, by, bz);
             if (key != cur_key) {
                 cur_key = key;
-                cur_own = !(c.shard_world > 1 && owner_of(key, c.shard_world) != c.shard_rank);
+                // key sharding without exchange: this rank's blocks only (its band is redundant);
+                // with exchange: every block is staged, the epilogue routes the remote ones
+                cur_own = c.exchange || !(c.shard_world > 1 && owner_of(key, c.shard_world) != c.shard_rank);
                 cur_li = -1;
                 if (cur_own) {  // local table insert (open addressing in smem)
                     uint32_t s = hash_slot(key, 8);
@@ -716,7 +757,8 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
                 fb = own == kInvalid || !pixel_has_return(validbits, own);
             }
             if (cur_li < 0) {  // local table full: straight to global state
-                visit_global(c, g, h, block_keys, stamp, touched, fm, fbcnt, rec, pool, vlist, fctr, ctr, key, lin, fb, p);
+                visit_global(c, g, h, block_keys, stamp, touched, fm, fbcnt, rec, pool, vlist, fctr, xsend, xcnt, ctr, key,
+                             lin, fb, p);
                 return;
             }
             const int word = cur_li * 16 + (lin >> 5);
@@ -731,8 +773,8 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
                 if (pos < uint32_t(kTileFb))
                     lfb[pos] = (uint32_t(cur_li) << 24) | (uint32_t(lin) << 15) | uint32_t(tid);
                 else
-                    visit_global(c, g, h, block_keys, stamp, touched, fm, fbcnt, rec, pool, vlist, fctr, ctr, key,
-                                 lin, true, p);
+                    visit_global(c, g, h, block_keys, stamp, touched, fm, fbcnt, rec, pool, vlist, fctr, xsend,
+                                 xcnt, ctr, key, lin, true, p);
             }
         });
         if (pend_word >= 0) atomicOr(&lmask[0][0] + pend_word, pend_bits);
@@ -744,7 +786,7 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
     __shared__ uint32_t s_w[2 * kW];
     uint32_t slot = kInvalid, idx = kInvalid;
     bool first_touch = false;
-    if (lkey[tid] != kEmptyKey) {
+    if (lkey[tid] != kEmptyKey && !is_remote(c, lkey[tid])) {
         const SlotRef sr = find_or_insert(c, h, block_keys, ctr, lkey[tid]);
         if (sr.slot != kInvalid) {
             slot = sr.slot;
@@ -760,8 +802,44 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
     if (first_touch) touched[tpos] = slot;
     // zero-fill the blocks this tile created (read from the fold on)
     for (uint32_t j = 0; j < nnew; ++j) zero_block(pool, lnew[j], tid, kTileU * kTileV);
-    // staged fallback visits -> records (slot, voxel, frame, pixel), counted per block
     const uint32_t nf = min(nfb, uint32_t(kTileFb));
+    // exchange mode: the tile's entries for other ranks are counted per destination in
+    // shared memory and reserved with one global atomic per (tile, destination)
+    __shared__ uint32_t s_xn[kMaxXWorld], s_xb[kMaxXWorld], s_xbase[kMaxXWorld];
+    __shared__ uint8_t lown[kLocalKeys];
+    if (c.exchange) {
+        if (tid < kMaxXWorld) s_xn[tid] = s_xb[tid] = 0u;
+        lown[tid] = (lkey[tid] != kEmptyKey) ? uint8_t(owner_of(lkey[tid], c.shard_world)) : uint8_t(255);
+        __syncthreads();
+        for (uint32_t i = tid; i < nf; i += kTileU * kTileV) {
+            const uint32_t li = lfb[i] >> 24;
+            if (lown[li] != c.shard_rank) atomicAdd(&s_xn[lown[li]], 1u);
+        }
+        for (int i = tid; i < kLocalKeys * 16; i += kTileU * kTileV) {
+            const int li = i >> 4;
+            const uint32_t bits = lmask[li][i & 15];
+            if (bits && lown[li] != c.shard_rank) {
+                atomicAdd(&s_xn[lown[li]], 1u);
+                atomicAdd(&s_xb[lown[li]], uint32_t(__popc(bits)));
+            }
+        }
+        __syncthreads();
+        if (tid < c.shard_world) {
+            uint32_t* meta = xcnt + tid * kXMeta;
+            s_xbase[tid] = s_xn[tid] ? atomicAdd(&meta[0], s_xn[tid]) : 0u;
+            if (s_xb[tid]) atomicAdd(&meta[1 + g], s_xb[tid]);
+            if (s_xn[tid] && s_xbase[tid] + s_xn[tid] > c.xcap) atomicOr(&ctr[C_ABORT], kAbortXchg);
+            s_xn[tid] = 0u;  // now the write cursor
+        }
+        __syncthreads();
+    }
+    auto xput = [&](uint32_t li, uint32_t z, uint32_t w) {
+        const uint32_t d = lown[li];
+        const uint32_t pos = s_xbase[d] + atomicAdd(&s_xn[d], 1u);
+        if (pos < c.xcap)
+            xsend[uint64_t(d) * c.xcap + pos] = make_uint4(uint32_t(lkey[li]), uint32_t(lkey[li] >> 32), z, w);
+    };
+    // staged fallback visits -> records (slot, voxel, frame, pixel), counted per block
     uint32_t nrec = 0;
     for (uint32_t i = tid; i < nf; i += kTileU * kTileV) nrec += lslot[lfb[i] >> 24] != kInvalid ? 1u : 0u;
     uint32_t rpos = cta_reserve<kW>(nrec, &ctr[C_RECORDS], s_w);
@@ -769,9 +847,12 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
     for (uint32_t i = tid; i < nf; i += kTileU * kTileV) {
         const uint32_t e = lfb[i], li = e >> 24;
         const uint32_t sl = lslot[li];
-        if (sl == kInvalid) continue;
         const uint32_t t = e & 255u;
         const uint32_t px = tile_p0 + (t / kTileU) * uint32_t(c.m.W) + (t % kTileU);
+        if (sl == kInvalid) {
+            if (c.exchange && lown[li] != c.shard_rank) xput(li, 0x80000000u | (g << 9) | ((e >> 15) & 511u), px);
+            continue;
+        }
         if (rpos < c.rec_cap) rec[rpos] = make_record(sl, int((e >> 15) & 511u), g, px);
         ++rpos;
         atomicAdd(&lcnt[li], 1u);
@@ -782,8 +863,12 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
     for (int i = tid; i < kLocalKeys * 16; i += kTileU * kTileV) {
         const int li = i >> 4, w = i & 15;
         uint32_t bits = lmask[li][w];
-        if (bits && lidx[li] != kInvalid) bits &= ~atomicOr(&fm[uint64_t(lidx[li]) * kMaskWords + g * 16 + w], bits);
-        else bits = 0u;
+        if (bits && lidx[li] != kInvalid) {
+            bits &= ~atomicOr(&fm[uint64_t(lidx[li]) * kMaskWords + g * 16 + w], bits);
+        } else {
+            if (bits && c.exchange && lown[li] != c.shard_rank) xput(uint32_t(li), (g << 4) | uint32_t(w), bits);
+            bits = 0u;
+        }
         lmask[li][w] = bits;
         nv += __popc(bits);
     }
@@ -1037,6 +1122,79 @@ k_fold(const GroupConsts c, const FramePose f, const uint32_t g, const ScanSlots
     }
 }
 
+// Exchange mode, owner side, phase 1: the visit entries other ranks sent (send_remote),
+// applied as this rank's band applies its own visits: block find-or-insert (new blocks
+// zero-filled), the group's touched list, the block's frame header, the frame's mask row
+// (the bits set first are the voxels' single entries in the frame's voxel list: their
+// positions are reserved here and written by phase 2, after the host has grown the lists
+// if needed) and the fallback records.
+__global__ void __launch_bounds__(kThreads)
+k_ingest(const GroupConsts c, const uint4* __restrict__ recv, uint32_t n, HashView h,
+         uint64_t* __restrict__ block_keys, uint32_t* __restrict__ stamp, uint32_t* __restrict__ touched,
+         uint32_t* __restrict__ fm, uint32_t* __restrict__ fbcnt, unsigned long long* __restrict__ rec,
+         svx_tsdf_voxel* __restrict__ pool, uint4* __restrict__ xaux, uint32_t* __restrict__ fctr,
+         uint32_t* __restrict__ ctr) {
+    pdl_wait();
+    pdl_trigger();
+    if (ctr[C_ABORT]) return;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint4 e = recv[i];
+        xaux[i] = make_uint4(0u, 0u, 0u, 0u);
+        const uint64_t key = uint64_t(e.x) | (uint64_t(e.y) << 32);
+        const SlotRef r = find_or_insert(c, h, block_keys, ctr, key);
+        if (r.slot == kInvalid) continue;
+        if (atomicExch(&stamp[r.slot], c.serial) != c.serial) touched[atomicAdd(&ctr[C_TOUCHED], 1u)] = r.slot;
+        if (r.inserted) zero_block(pool, r.idx, 0, 1);
+        uint32_t* bm = fm + uint64_t(r.idx) * kMaskWords;
+        if (e.z & 0x80000000u) {  // fallback record
+            const uint32_t g = (e.z >> 9) & 15u;
+            atomicOr(&bm[kHdrRow * 16], 1u << g);
+            atomicAdd(&fbcnt[r.slot], 1u);
+            const uint32_t pos = atomicAdd(&ctr[C_RECORDS], 1u);
+            if (pos < c.rec_cap) rec[pos] = make_record(r.slot, int(e.z & 511u), g, e.w);
+            else atomicOr(&ctr[C_ABORT], kAbortRecords);
+        } else {
+            const uint32_t g = (e.z >> 4) & 15u, w = e.z & 15u;
+            atomicOr(&bm[kHdrRow * 16], 1u << g);
+            const uint32_t nb = e.w & ~atomicOr(&bm[g * 16 + w], e.w);
+            if (nb) xaux[i] = make_uint4(atomicAdd(&fctr[g * kFC + FC_VOX], uint32_t(__popc(nb))), nb, r.idx,
+                                         (g << 4) | w);
+        }
+    }
+}
+
+// Exchange mode, owner side, phase 2: the reserved voxel-list entries.
+__global__ void __launch_bounds__(kThreads)
+k_ingest_list(const GroupConsts c, const uint4* __restrict__ xaux, uint32_t n, uint32_t* __restrict__ vlist,
+              const uint32_t* __restrict__ ctr) {
+    pdl_wait();
+    pdl_trigger();
+    if (ctr[C_ABORT]) return;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint4 a = xaux[i];
+        if (!a.y) continue;
+        const uint32_t g = a.w >> 4, w = a.w & 15u;
+        uint32_t* vl = vlist + uint64_t(g) * c.vox_cap;
+        uint32_t pos = a.x;
+        for (uint32_t bits = a.y; bits; bits &= bits - 1, ++pos)
+            vl[pos] = (a.z << 9) | (w * 32u + uint32_t(__ffs(bits) - 1));
+    }
+}
+
+// Exchange mode, sender side: the per-destination send lists packed back to back in
+// destination order (blockIdx.y = destination).
+__global__ void k_xpack(const uint4* __restrict__ xsend, uint32_t xcap, const uint32_t* __restrict__ xmeta,
+                        uint4* __restrict__ out) {
+    pdl_wait();  // the band's lists and counts are complete
+    pdl_trigger();
+    const uint32_t d = blockIdx.y;
+    uint64_t off = 0;
+    for (uint32_t k = 0; k < d; ++k) off += min(xmeta[k * kXMeta], xcap);
+    const uint32_t n = min(xmeta[d * kXMeta], xcap);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[off + i] = xsend[uint64_t(d) * xcap + i];
+}
+
 // Capacity path: every visited block key of frame slot 0 (duplicates allowed).
 __global__ void __launch_bounds__(kThreads)
 k_collect_keys(const __grid_constant__ GroupParams gp, const ScanSlots sc, unsigned long long* __restrict__ out,
@@ -1108,6 +1266,8 @@ GroupConsts make_consts(svx_map* m, svx_scan* s, const svx_integrator_cfg& cfg, 
     c.dtheta_f = float(s->model.delta_theta * (1.0 - 1e-6));
     c.shard_rank = m->shard_rank;
     c.shard_world = m->shard_world;
+    c.exchange = 0;
+    c.xcap = m->xcap;
     c.serial = ++m->frame_serial;
     c.G = G;
     c.P = uint32_t(s->P);
@@ -1147,19 +1307,32 @@ unsigned fold_grid(int device) {
     return unsigned(grid[device]);
 }
 
+void launch_fold_kernels(svx_map* m, svx_scan* s, const GroupParams& gp, FrameOut* outs);
+
 // Enqueues the TSDF kernels of one group (the frames' images are in the scan's slots).
 void launch_group_kernels(svx_map* m, svx_scan* s, const GroupParams& gp, FrameOut* outs) {
     const GroupConsts& c = gp.c;
     HashView hv = hash_view(m);
     const ScanSlots sc = scan_slots(s);
-    const unsigned pg = persistent_grid(m->device);
     uint32_t* fm = mask_base(m);
     {
         ProfMark pm(m, SVX_K_RAYCAST);
         launch_pdl(k_band, c.G * c.tiles, kTileU * kTileV, m->stream, gp, sc, hv, m->block_keys, m->stamp,
-                   m->touched, fm, m->fbcnt, m->records.p, tsdf_base(m), m->vlist.p, m->fctr, m->d_ctr);
+                   m->touched, fm, m->fbcnt, m->records.p, tsdf_base(m), m->vlist.p, m->fctr, m->xsend.p,
+                   m->xcnt.p, m->d_ctr);
         count_launch();
     }
+    if (c.exchange) return;  // the rest runs after the exchange (run_group_xend)
+    launch_fold_kernels(m, s, gp, outs);
+}
+
+// The group's kernels after the band (and, in exchange mode, after the ingest).
+void launch_fold_kernels(svx_map* m, svx_scan* s, const GroupParams& gp, FrameOut* outs) {
+    const GroupConsts& c = gp.c;
+    HashView hv = hash_view(m);
+    const ScanSlots sc = scan_slots(s);
+    const unsigned pg = persistent_grid(m->device);
+    uint32_t* fm = mask_base(m);
     {
         ProfMark pm(m, SVX_K_FALLBACK);
         launch_pdl(k_fb_bucket, pg / 4, kThreads, m->stream, m->records.p, m->rec_cap, m->fbcnt, m->fbstart,
@@ -1293,6 +1466,35 @@ int group_cap(const svx_scan* s) {
 
 }  // namespace
 
+namespace {
+// The report of a completed frame (its FrameOut is final); numbers the frame.
+void commit_frame(svx_map* m, svx_scan* s, const FrameOut& o, svx_frame_report& rep) {
+    rep.frame = m->tsdf_frames++;
+    rep.updated_voxels = o.updated;
+    rep.new_blocks = o.new_blocks;
+    m->new_ema = m->new_ema == 0.0 ? double(o.new_blocks) : 0.9 * m->new_ema + 0.1 * double(o.new_blocks);
+    s->dropped = o.dropped;
+    m->prof_acc.frames += 1;
+    m->prof_acc.rays += o.rays;
+    m->prof_acc.touched_blocks += o.touched;
+    m->prof_acc.new_blocks += o.new_blocks;
+    m->prof_acc.updated_voxels += o.updated;
+    m->prof_acc.fallback_voxels += o.fb_voxels;
+}
+
+// DevBuf growth that keeps the first `keep` elements.
+template <typename T>
+void grow_keep(DevBuf<T>& b, size_t count, size_t keep, cudaStream_t stream) {
+    if (count <= b.n) return;
+    DevBuf<T> nb;
+    nb.alloc(count);
+    if (keep) SVX_CUDA(cudaMemcpyAsync(nb.p, b.p, sizeof(T) * keep, cudaMemcpyDeviceToDevice, stream));
+    SVX_CUDA(cudaStreamSynchronize(stream));
+    b.release();
+    b = nb;
+}
+}  // namespace
+
 void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cfg& cfg, svx_frame_report* reps) {
     if (!(cfg.alpha_epsilon > 0.0)) throw Error(SVX_INVALID_ARGUMENT, "alpha_epsilon must be > 0");
     if (n <= 0) return;
@@ -1348,20 +1550,7 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
             SVX_CUDA(cudaEventRecord(m->ingest_used[r], m->stream));
         }
     }
-    auto commit = [&](int i) {
-        const FrameOut& o = m->h_outs[i];
-        reps[i].frame = m->tsdf_frames++;
-        reps[i].updated_voxels = o.updated;
-        reps[i].new_blocks = o.new_blocks;
-        m->new_ema = m->new_ema == 0.0 ? double(o.new_blocks) : 0.9 * m->new_ema + 0.1 * double(o.new_blocks);
-        s->dropped = o.dropped;
-        m->prof_acc.frames += 1;
-        m->prof_acc.rays += o.rays;
-        m->prof_acc.touched_blocks += o.touched;
-        m->prof_acc.new_blocks += o.new_blocks;
-        m->prof_acc.updated_voxels += o.updated;
-        m->prof_acc.fallback_voxels += o.fb_voxels;
-    };
+    auto commit = [&](int i) { commit_frame(m, s, m->h_outs[i], reps[i]); };
     int f0 = 0;
     int single_lo = 0, single_hi = 0;  // frames run one per group (after a capacity / key abort)
     for (;;) {
@@ -1465,6 +1654,181 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tr0).count();
     }
     for (int i = f0; i < n; ++i) commit(i);
+    m->n_blocks = m->h_ctr[C_BLOCKS];
+}
+
+namespace {
+struct XState {  // a frame group between run_group_xbegin and run_group_xend
+    GroupParams gp;
+    svx_scan* s;
+};
+void free_xstate(void* p) { delete static_cast<XState*>(p); }
+}  // namespace
+
+void run_group_xbegin(svx_map* m, const FrameJob* jobs, int G, const svx_integrator_cfg& cfg,
+                      uint64_t* send_meta, const void** d_send) {
+    if (!(cfg.alpha_epsilon > 0.0)) throw Error(SVX_INVALID_ARGUMENT, "alpha_epsilon must be > 0");
+    if (m->shard_world < 2 || m->shard_world > kMaxXWorld)
+        throw Error(SVX_INVALID_ARGUMENT, "exchange mode needs a key-sharded map with 2..16 ranks");
+    if (m->xstate) throw Error(SVX_INVALID_ARGUMENT, "xbegin: the previous group was not finished (xend)");
+    if (G < 1 || G > kMaxG) throw Error(SVX_INVALID_ARGUMENT, "xbegin: 1..16 frames per group");
+    svx_scan* s = jobs[0].scan;
+    for (int i = 0; i < G; ++i)
+        if (jobs[i].scan != s || !jobs[i].project)
+            throw Error(SVX_INVALID_ARGUMENT, "xbegin: point clouds of one scan model");
+    if (G > group_cap(s)) throw Error(SVX_INVALID_ARGUMENT, "xbegin: group too large for this scan size");
+    const int world = m->shard_world;
+    uint64_t nmax = 1;
+    for (int i = 0; i < G; ++i) nmax = std::max<uint64_t>(nmax, jobs[i].n);
+    ensure_scan_slots(s, G, nmax);
+    m->outs.alloc(size_t(G));
+    SVX_CUDA(cudaMemsetAsync(m->outs.p, 0, sizeof(FrameOut) * size_t(G), m->stream));
+    if (m->h_outs_n < size_t(G)) {
+        if (m->h_outs) cudaFreeHost(m->h_outs);
+        SVX_CUDA(cudaMallocHost(&m->h_outs, sizeof(FrameOut) * G));
+        m->h_outs_n = size_t(G);
+    }
+    const uint64_t want_vox = std::min<uint64_t>(8ull * uint64_t(s->P) + 4096, 0x7FFFFFFFull);
+    if (m->vox_cap < want_vox) m->vox_cap = uint32_t(want_vox);
+    m->vlist.alloc(uint64_t(m->vox_cap) * uint64_t(G));
+    const uint64_t head = m->test_pool_head ? m->test_pool_head : std::max<uint64_t>(32768, uint64_t(2.0 * m->new_ema * G));
+    ensure_blocks(m, m->n_blocks + head, 4 * head);
+    if (!m->xcap) m->xcap = uint32_t(std::max<uint64_t>(1u << 16, 2ull * uint64_t(s->P) * uint64_t(G) / uint64_t(world)));
+    m->xcnt.alloc(size_t(world) * kXMeta);
+    m->xsend.alloc(uint64_t(world) * m->xcap);
+    m->xpack.alloc(uint64_t(world) * m->xcap);
+    std::vector<uint32_t> meta(size_t(world) * kXMeta);
+    auto xs = std::make_unique<XState>();
+    xs->s = s;
+    for (;;) {
+        SVX_CUDA(cudaMemsetAsync(m->xcnt.p, 0, 4ull * world * kXMeta, m->stream));
+        GroupParams& gp = xs->gp;
+        gp.c = make_consts(m, s, cfg, uint32_t(G), true);
+        gp.c.exchange = 1;
+        gp.c.xcap = m->xcap;
+        const void* pts[kMaxG];
+        uint64_t n[kMaxG];
+        Pose poses[kMaxG];
+        for (int g = 0; g < G; ++g) {
+            gp.f[g] = make_pose(m, jobs[g].pose);
+            pts[g] = jobs[g].pts;
+            n[g] = jobs[g].n;
+            poses[g] = jobs[g].pose;
+        }
+        launch_project_group(s, pts, n, G, jobs[0].stride, false, poses);
+        launch_group_kernels(m, s, gp, m->outs.p);  // exchange mode: the band only
+        launch_pdl(k_xpack, dim3(64, unsigned(world)), kThreads, m->stream, static_cast<const uint4*>(m->xsend.p),
+                   m->xcap, static_cast<const uint32_t*>(m->xcnt.p), m->xpack.p);
+        count_launch();
+        SVX_CUDA(cudaMemcpyAsync(meta.data(), m->xcnt.p, 4ull * world * kXMeta, cudaMemcpyDeviceToHost, m->stream));
+        SVX_CUDA(cudaMemcpyAsync(m->h_fctr, m->fctr, 4ull * kMaxG * kFC, cudaMemcpyDeviceToHost, m->stream));
+        sync_counters(m);
+        const uint32_t abort = m->h_ctr[C_ABORT];
+        if (!abort) break;
+        for (int b = 0; b < 8; ++b) m->prof_acc.aborts[b] += (abort >> b) & 1u;
+        const uint32_t before = m->h_ctr[C_BLOCKS_BEFORE], blocks_seen = m->h_ctr[C_BLOCKS],
+                       recs_seen = m->h_ctr[C_RECORDS];
+        rollback_group(m, s, before);
+        if (abort & kAbortKey)
+            throw Error(SVX_INVALID_ARGUMENT, "block coordinate outside the device key range [-2^20, 2^20)");
+        if (abort & (kAbortCapacity | kAbortHash))
+            throw Error(SVX_CAPACITY, "block budget of this shard exhausted (max_blocks = " +
+                                          std::to_string(m->cfg.max_blocks) + ")");
+        if (abort & kAbortPool) ensure_blocks(m, uint64_t(m->n_blocks) + 2 * head + (blocks_seen - before));
+        if (abort & kAbortRecords) {
+            m->rec_cap = std::max<uint32_t>(recs_seen + (recs_seen >> 1), m->rec_cap * 2);
+            m->records.alloc(m->rec_cap);
+            m->bucket.alloc(m->rec_cap);
+            m->bucket2.alloc(m->rec_cap);
+            m->fbdesc.alloc(m->rec_cap);
+        }
+        if (abort & kAbortVox) {
+            m->vox_cap = uint32_t(std::min<uint64_t>(uint64_t(m->vox_cap) * 2, 0x7FFFFFFFull));
+            m->vlist.alloc(uint64_t(m->vox_cap) * uint64_t(G));
+        }
+        if (abort & kAbortXchg) {
+            uint32_t most = 0;
+            for (int d = 0; d < world; ++d) most = std::max(most, meta[size_t(d) * kXMeta]);
+            m->xcap = std::max<uint32_t>(m->xcap * 2, most + most / 2);
+            m->xsend.alloc(uint64_t(world) * m->xcap);
+            m->xpack.alloc(uint64_t(world) * m->xcap);
+        }
+        SVX_CUDA(cudaMemsetAsync(m->outs.p, 0, sizeof(FrameOut) * size_t(G), m->stream));
+    }
+    // (the lists were packed destination-major on the device by k_xpack)
+    for (size_t i = 0; i < meta.size(); ++i) send_meta[i] = meta[i];
+    *d_send = m->xpack.p;
+    m->xstate = xs.release();
+    m->xstate_free = free_xstate;
+}
+
+void run_group_xend(svx_map* m, const void* d_recv, const uint64_t* recv_meta, svx_frame_report* reps) {
+    XState* xs = static_cast<XState*>(m->xstate);
+    if (!xs) throw Error(SVX_INVALID_ARGUMENT, "xend without xbegin");
+    std::unique_ptr<XState> hold(xs);
+    m->xstate = nullptr;
+    GroupParams& gp = xs->gp;
+    svx_scan* s = xs->s;
+    const int G = int(gp.c.G);
+    for (int i = 0; i < G; ++i) {
+        reps[i].frame = -1;
+        reps[i].updated_voxels = reps[i].new_blocks = 0;
+    }
+    const int world = m->shard_world;
+    uint64_t n_recv = 0;
+    uint64_t add[kMaxG] = {};  // bound on the received new voxels per frame
+    for (int r = 0; r < world; ++r) {
+        n_recv += recv_meta[size_t(r) * kXMeta];
+        for (int g = 0; g < G; ++g) add[g] += recv_meta[size_t(r) * kXMeta + 1 + g];
+    }
+    if (n_recv >= (1ull << 31)) throw Error(SVX_INVALID_ARGUMENT, "xend: too many entries");
+    // room for the received entries: each may add one block and one record
+    ensure_blocks(m, uint64_t(m->h_ctr[C_BLOCKS]) + n_recv + 1);
+    const uint64_t recs = m->h_ctr[C_RECORDS];
+    if (recs + n_recv > m->rec_cap) {
+        m->rec_cap = uint32_t(std::min<uint64_t>((recs + n_recv) * 3 / 2 + 1024, 0xFFFFFFF0ull));
+        grow_keep(m->records, m->rec_cap, recs, m->stream);
+        m->bucket.alloc(m->rec_cap);
+        m->bucket2.alloc(m->rec_cap);
+        m->fbdesc.alloc(m->rec_cap);
+    }
+    gp.c.rec_cap = m->rec_cap;
+    // the voxel lists: this rank's entries (xbegin) + at most the received voxel bits per
+    // frame; grown here (keeping each frame's entries) before the ingest reserves positions
+    uint64_t most = 0;
+    for (int g = 0; g < G; ++g) most = std::max<uint64_t>(most, uint64_t(m->h_fctr[g * kFC + FC_VOX]) + add[g]);
+    if (most > m->vox_cap) {
+        const uint32_t ncap = uint32_t(std::min<uint64_t>(most * 5 / 4 + 1024, 0x7FFFFFFFull));
+        DevBuf<uint32_t> nb;
+        nb.alloc(uint64_t(ncap) * G);
+        for (int g = 0; g < G; ++g) {
+            const uint32_t keep = std::min(m->h_fctr[g * kFC + FC_VOX], m->vox_cap);
+            if (keep)
+                SVX_CUDA(cudaMemcpyAsync(nb.p + uint64_t(g) * ncap, m->vlist.p + uint64_t(g) * m->vox_cap, 4ull * keep,
+                                         cudaMemcpyDeviceToDevice, m->stream));
+        }
+        SVX_CUDA(cudaStreamSynchronize(m->stream));
+        m->vlist.release();
+        m->vlist = nb;
+        m->vox_cap = ncap;
+    }
+    gp.c.vox_cap = m->vox_cap;
+    const unsigned grid = persistent_grid(m->device);
+    if (n_recv) {
+        m->xaux.alloc(n_recv);
+        launch_pdl(k_ingest, grid, kThreads, m->stream, gp.c, static_cast<const uint4*>(d_recv), uint32_t(n_recv),
+                   hash_view(m), m->block_keys, m->stamp, m->touched, mask_base(m), m->fbcnt, m->records.p,
+                   tsdf_base(m), m->xaux.p, m->fctr, m->d_ctr);
+        count_launch();
+        launch_pdl(k_ingest_list, grid, kThreads, m->stream, gp.c, static_cast<const uint4*>(m->xaux.p),
+                   uint32_t(n_recv), m->vlist.p, m->d_ctr);
+        count_launch();
+    }
+    launch_fold_kernels(m, s, gp, m->outs.p);
+    SVX_CUDA(cudaMemcpyAsync(m->h_outs, m->outs.p, sizeof(FrameOut) * G, cudaMemcpyDeviceToHost, m->stream));
+    sync_counters(m);
+    if (m->h_ctr[C_ABORT]) throw Error(SVX_CUDA, "xend: fold aborted");
+    for (int i = 0; i < G; ++i) commit_frame(m, s, m->h_outs[i], reps[i]);
     m->n_blocks = m->h_ctr[C_BLOCKS];
 }
 

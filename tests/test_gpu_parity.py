@@ -309,3 +309,46 @@ def test_key_sharded_maps_union_equals_unsharded():
         assert np.array_equal(sems[idx[j]], sf[sorted(sf)[n_full]])
     for g, _ in maps:
         g.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_exchange_sharded_union_equals_unsharded(world):
+    """The multi-GPU data plane (exchange mode, paper_2412_00291_b200.dist), every rank
+    emulated in one process on one GPU: each rank casts its share of the rays, visits of
+    other ranks' blocks are exchanged, each rank folds its own blocks. The ranks' block
+    sets are disjoint, their reports sum to the unsharded map's, and their union is the
+    unsharded map byte for byte (24 cfg2 frames: two groups)."""
+    import torch
+    from oracle.bindings import parse_svox1
+    from paper_2412_00291_b200 import dist as sdist
+    wl = W.make("cfg2", 24)
+    scans = [p for p, _ in wl.scans(device=torch.device("cuda", 0))]
+    offs = np.zeros(len(scans) + 1, np.uint64)
+    offs[1:] = np.cumsum([s.shape[0] for s in scans])
+    pts = torch.cat(scans).contiguous()
+    poses = [wl.pose(i) for i in range(len(scans))]
+    cfg = svx.MapConfig(wl.voxel_size, wl.truncation, wl.num_labels, 1 << 20)
+    icfg = svx.IntegratorConfig()
+    full = svx.VoxelStore(cfg, 0)
+    want = full.integrate_clouds_device(wl.model, pts.data_ptr(), offs, 3, poses, icfg)
+    stores = []
+    for r in range(world):
+        st = svx.VoxelStore(cfg, 0)
+        st.set_shard(r, world)
+        stores.append(st)
+    reps = sdist.emulate_sharded(stores, wl.model, pts.data_ptr(), offs, 3, poses, icfg)
+    for f in range(len(poses)):
+        assert sum(reps[r][f].updated_voxels for r in range(world)) == want[f].updated_voxels
+        assert sum(reps[r][f].new_blocks for r in range(world)) == want[f].new_blocks
+        assert all(reps[r][f].frame == want[f].frame for r in range(world))
+    _, kf, tf, _ = parse_svox1(full.save_bytes())
+    parts = [parse_svox1(st.save_bytes()) for st in stores]
+    assert all(len(p[1]) > 0 for p in parts)
+    keys = np.concatenate([p[1] for p in parts])
+    tsdf = np.concatenate([p[2] for p in parts])
+    order = np.lexsort((keys[:, 2], keys[:, 1], keys[:, 0]))
+    assert len(keys) == len(kf)
+    assert np.array_equal(keys[order], kf)
+    assert tsdf[order].tobytes() == tf.tobytes()
+    for st in stores + [full]:
+        st.close()

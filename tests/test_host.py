@@ -100,3 +100,54 @@ def test_key_sharding_gloo_world2():
     keys = {tuple(k) for k in rng.integers(-3000, 3000, size=(5000, 3))}
     assert shards[0] | shards[1] == keys
     assert out[0][1] == out[1][1]  # both ranks received the identical scan
+
+
+def _exchange_worker(rank, world, port, q):
+    """dist.exchange (the all-to-all of the multi-GPU data plane) with gloo on the CPU:
+    16-byte entries packed by destination; each rank must receive exactly the entries
+    addressed to it, in source-rank order."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2412_00291_b200 import dist as sdist
+    rng = np.random.default_rng(100 + rank)
+    # visit entries of random blocks: (key lo, key hi, src << 16 | seq, dest), routed by owner
+    keys = rng.integers(-3000, 3000, size=(int(rng.integers(0, 400)), 3))
+    dests = np.array([svx.block_owner(k, world) for k in keys], np.int64)
+    order = np.argsort(dests, kind="stable")
+    ent = np.zeros((len(keys), 4), np.uint32)
+    ent[:, 0] = keys[order, 0].astype(np.uint32)
+    ent[:, 1] = keys[order, 1].astype(np.uint32)
+    ent[:, 2] = (rank << 16) | np.arange(len(keys), dtype=np.uint32)
+    ent[:, 3] = dests[order].astype(np.uint32)
+    counts = np.bincount(dests, minlength=world)
+    meta = np.zeros((world, 17), np.int64)
+    meta[:, 0] = counts
+    meta[:, 1] = rank * 1000 + np.arange(world)  # per-frame voxel bits ride along
+    send = torch.from_numpy(ent.view(np.uint8).reshape(-1).copy())
+    recv, rmeta = sdist.exchange(send, meta)
+    got = recv.numpy().view(np.uint32).reshape(-1, 4)
+    assert np.array_equal(rmeta[:, 1], np.arange(world) * 1000 + rank)
+    out = [None] * world
+    dist.all_gather_object(out, (ent, got))
+    if rank == 0:
+        q.put(out)
+    dist.destroy_process_group()
+
+
+def test_exchange_all_to_all_gloo():
+    for world in (2, 3):
+        ctx = mp.get_context("spawn")
+        q = ctx.Queue()
+        port = _free_port()
+        procs = [ctx.Process(target=_exchange_worker, args=(r, world, port, q)) for r in range(world)]
+        for p in procs:
+            p.start()
+        out = q.get(timeout=240)
+        for p in procs:
+            p.join(timeout=60)
+        sent = [o[0] for o in out]
+        for d in range(world):
+            got = out[d][1]
+            want = np.concatenate([s[s[:, 3] == d] for s in sent]) if sent else np.zeros((0, 4), np.uint32)
+            assert np.array_equal(got, want), (world, d)
+            assert np.all(got[:, 3] == d)
