@@ -694,7 +694,8 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
     // tiles (round robin over the group's tiles); every rank still writes the whole pixel
     // cache, which the folds of its own blocks read
     const bool my_tile = !c.exchange || int(blockIdx.x % uint32_t(c.shard_world)) == c.shard_rank;
-    const bool cast = my_tile && in_range && !(c.drop_unreliable && c.has_normals && !sc.valid[pg + p]);
+    if (!my_tile) return;  // (CTA-uniform) another rank casts this tile's rays
+    const bool cast = in_range && !(c.drop_unreliable && c.has_normals && !sc.valid[pg + p]);
     if (cast) {
         warp_agg_inc(&fctr[g * kFC + FC_RAYS]);
         const d3 tr = scale3(c.tau, ray);  // (q - o).normalized() == (q - o) / range
