@@ -345,7 +345,6 @@ enum Counter : int {
     C_FB_BLOCKS = 19,   // blocks holding fallback records this group
     C_BUCKET_TOP = 23,  // fallback bucket space handed out this group
     C_DONE = 24,        // CTAs of k_fold finished (the last one writes the group's reports)
-    C_CONF_MAYBE = 27,  // the current label image may read a confidence outside [0, 1]
     kNumCounters = 32
 };
 

@@ -1,22 +1,30 @@
 // K6: SemanticIntegrator::integrate_labels on the device
-// (semantic_integrator.cpp:91-165).
+// (semantic_integrator.cpp:91-165), for a BATCH of label images (e.g. the 6 cameras of a
+// cfg3 frame) fused into one pass over the map.
 //
-// The reference sweeps EVERY allocated block per image (O(map)). Here:
-//   k_sem_cull    one thread per allocated block: the block's voxel-centre box is
-//                 tested against the camera's half-spaces (z > 0, z <= max_depth,
-//                 0 <= u < W, 0 <= v < H, each as an affine function of the
-//                 centre) with a conservative margin. A block is dropped only if
-//                 all 8 corners are outside one half-space, so no voxel the
-//                 reference would update is lost: results are identical.
-//   k_sem_update  persistent warps (grid = the resident CTAs), one eighth of a
-//                 candidate block per task (2 voxels per lane: short chains of
-//                 dependent loads), lane = voxel. Per voxel exactly the reference test sequence (observed,
-//                 D >= -tau/2, 0 < z <= max_depth, pixel in bounds, optional
-//                 raycast occlusion), then likelihood (tensor or label +
-//                 confidence, floored and renormalised in f32) and the Bayes
-//                 step (f32 products, f64 normaliser, f32 inverse) or the
-//                 latest-argmax ablation. The semantic layer of a block is
-//                 allocated on first update (ensure_semantics) and filled 1/K.
+// The reference sweeps every allocated block once per image and, per voxel, multiplies
+// the image's likelihood into the voxel's class probabilities. A voxel's result depends
+// only on its own state (W, D read, probabilities updated) and the images in their order,
+// so a batch of images is applied voxel by voxel: each voxel's TSDF state is read once,
+// tested against every image of the batch (the reference's test sequence per image),
+// and its probabilities are loaded once, multiplied by the passing images' likelihoods in
+// image order and stored once - identical to successive integrate_labels calls.
+//   k_sem_cull    one thread per allocated block (the device block count): the block's
+//                 voxel-centre box is tested against each image's half-spaces (z > 0,
+//                 z <= max_depth, 0 <= u < W, 0 <= v < H, each as an affine function of
+//                 the centre) with a conservative margin; a block is a candidate for the
+//                 images whose frustum it may touch (bit mask), dropped only when all 8
+//                 corners are outside one half-space of every image.
+//   k_sem_update  persistent warps, one sixteenth of a candidate block per task, lane =
+//                 voxel: observed and D >= -tau/2 (surrogate occlusion), then per image of
+//                 the mask: 0 < z <= max_depth, pixel in bounds, optional raycast
+//                 occlusion; then the layer (ensure_semantics: allocated on first update
+//                 and filled 1/K) and the Bayes steps (f32 products, f64 normaliser, f32
+//                 inverse) or the latest-argmax ablation, image by image.
+//                 A check pass (same kernel) runs first when an image may read a
+//                 confidence outside [0, 1]: label_to_likelihood throws only for a pixel a
+//                 passing voxel reads (semantic_integrator.cpp:24-27,140-142), so the pass
+//                 flags the first such image; images from it on are not applied.
 #include <algorithm>
 #include <chrono>
 
@@ -29,16 +37,28 @@ namespace {
 constexpr int kThreads = 256;
 inline unsigned grid_for(uint64_t n) { return unsigned((n + kThreads - 1) / kThreads); }
 
-struct SemParams {
+constexpr int kMaxImg = 8;  // label images fused in one pass
+
+// One label image (LabelImage, semantic_integrator.hpp:14-26) of a pass.
+struct ImgParams {
     Pose w2c;
     d3 cam_o;
     double fx, fy, cx, cy, max_depth;
     int32_t W, H;
+    const uint16_t* labels;
+    const float* conf;
+    const float* tensor;
+    int has_tensor, has_conf, conf_maybe;  // conf_maybe: may read a confidence outside [0, 1]
+};
+
+struct SemBatch {
+    ImgParams img[kMaxImg];
+    int n;  // images in this pass
     int K;
     double nu, inv_nu, occ_floor;
-    int use_bayes, raycast, has_tensor, has_conf;
+    int use_bayes, raycast, any_check;
     float floor_v, default_conf;
-    uint32_t n_blocks;
+    uint32_t pass_id;  // 1-based index of this pass in the batch (confidence errors)
 };
 
 __device__ inline d3 center_of(uint64_t key, int linear, double nu) {
@@ -49,52 +69,58 @@ __device__ inline d3 center_of(uint64_t key, int linear, double nu) {
               nu * (bz * kBlockSide + linear / (kBlockSide * kBlockSide)));
 }
 
-__global__ void k_sem_cull(SemParams sp, const uint64_t* __restrict__ block_keys,
-                           uint32_t* __restrict__ cand, uint32_t* __restrict__ ctr) {
-    const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= sp.n_blocks) return;
-    const uint64_t key = block_keys[idx];
-    int32_t bx, by, bz;
-    unpack_key(key, bx, by, bz);
-    // half-space values at the 8 corners of the voxel-centre box
-    bool out_zlo = true, out_zhi = true, out_ulo = true, out_uhi = true, out_vlo = true,
-         out_vhi = true;
-    const bool planes = sp.fx > 0.0 && sp.fy > 0.0;
-    for (int c = 0; c < 8; ++c) {
-        const int32_t vx = bx * 8 + ((c & 1) ? 7 : 0);
-        const int32_t vy = by * 8 + ((c & 2) ? 7 : 0);
-        const int32_t vz = bz * 8 + ((c & 4) ? 7 : 0);
-        const d3 p = xform(sp.w2c, mk(sp.nu * vx, sp.nu * vy, sp.nu * vz));
-        const double mag = fabs(p.x) + fabs(p.y) + fabs(p.z) + 1.0;
-        const double eps = 1e-9 * mag;
-        if (!(p.z < -eps)) out_zlo = false;
-        if (!(p.z > sp.max_depth + eps)) out_zhi = false;
-        if (planes) {
-            const double su = sp.fx * p.x + sp.cx * p.z;          // u >= 0  <=>  su >= 0
-            const double tu = sp.fx * p.x + (sp.cx - sp.W) * p.z;  // u < W   <=>  tu < 0
-            const double sv = sp.fy * p.y + sp.cy * p.z;
-            const double tv = sp.fy * p.y + (sp.cy - sp.H) * p.z;
-            const double e2 = 1e-9 * (fabs(sp.fx * p.x) + (fabs(sp.cx) + sp.W) * fabs(p.z) +
-                                      fabs(sp.fy * p.y) + (fabs(sp.cy) + sp.H) * fabs(p.z) + 1.0);
-            if (!(su < -e2)) out_ulo = false;
-            if (!(tu > e2)) out_uhi = false;
-            if (!(sv < -e2)) out_vlo = false;
-            if (!(tv > e2)) out_vhi = false;
-        } else {
-            out_ulo = out_uhi = out_vlo = out_vhi = false;
+// Per block: bit i set when the block may hold a voxel image i can update.
+__global__ void __launch_bounds__(kThreads)
+k_sem_cull(const __grid_constant__ SemBatch sb, const uint64_t* __restrict__ block_keys, uint2* __restrict__ cand,
+           uint32_t* __restrict__ ctr) {
+    const uint32_t nb = ctr[C_BLOCKS];
+    for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nb; idx += gridDim.x * blockDim.x) {
+        const uint64_t key = block_keys[idx];
+        int32_t bx, by, bz;
+        unpack_key(key, bx, by, bz);
+        uint32_t mask = 0;
+        for (int i = 0; i < sb.n; ++i) {
+            const ImgParams& ip = sb.img[i];
+            // half-space values at the 8 corners of the voxel-centre box
+            bool out_zlo = true, out_zhi = true, out_ulo = true, out_uhi = true, out_vlo = true, out_vhi = true;
+            const bool planes = ip.fx > 0.0 && ip.fy > 0.0;
+            for (int c = 0; c < 8; ++c) {
+                const int32_t vx = bx * 8 + ((c & 1) ? 7 : 0);
+                const int32_t vy = by * 8 + ((c & 2) ? 7 : 0);
+                const int32_t vz = bz * 8 + ((c & 4) ? 7 : 0);
+                const d3 p = xform(ip.w2c, mk(sb.nu * vx, sb.nu * vy, sb.nu * vz));
+                const double mag = fabs(p.x) + fabs(p.y) + fabs(p.z) + 1.0;
+                const double eps = 1e-9 * mag;
+                if (!(p.z < -eps)) out_zlo = false;
+                if (!(p.z > ip.max_depth + eps)) out_zhi = false;
+                if (planes) {
+                    const double su = ip.fx * p.x + ip.cx * p.z;          // u >= 0  <=>  su >= 0
+                    const double tu = ip.fx * p.x + (ip.cx - ip.W) * p.z;  // u < W   <=>  tu < 0
+                    const double sv = ip.fy * p.y + ip.cy * p.z;
+                    const double tv = ip.fy * p.y + (ip.cy - ip.H) * p.z;
+                    const double e2 = 1e-9 * (fabs(ip.fx * p.x) + (fabs(ip.cx) + ip.W) * fabs(p.z) +
+                                              fabs(ip.fy * p.y) + (fabs(ip.cy) + ip.H) * fabs(p.z) + 1.0);
+                    if (!(su < -e2)) out_ulo = false;
+                    if (!(tu > e2)) out_uhi = false;
+                    if (!(sv < -e2)) out_vlo = false;
+                    if (!(tv > e2)) out_vhi = false;
+                } else {
+                    out_ulo = out_uhi = out_vlo = out_vhi = false;
+                }
+            }
+            if (!(out_zlo || out_zhi || out_ulo || out_uhi || out_vlo || out_vhi)) mask |= 1u << i;
         }
+        if (mask) cand[warp_agg_inc(&ctr[C_CAND])] = make_uint2(idx, mask);
     }
-    if (out_zlo || out_zhi || out_ulo || out_uhi || out_vlo || out_vhi) return;
-    cand[warp_agg_inc(&ctr[C_CAND])] = idx;
 }
 
 // occluded_along_ray (semantic_integrator.cpp:64-84), TSDF read through the hash.
-__device__ bool occluded_along_ray(const SemParams& sp, HashView h,
-                                   const svx_tsdf_voxel* __restrict__ pool, d3 center) {
-    const d3 dc = sub3(center, sp.cam_o);
+__device__ bool occluded_along_ray(const SemBatch& sb, d3 cam_o, HashView h, const svx_tsdf_voxel* __restrict__ pool,
+                                   d3 center) {
+    const d3 dc = sub3(center, cam_o);
     const double voxel_depth = sqrt(dot3(dc, dc));
-    const double step = sp.nu;
-    const double stop = voxel_depth - 2.5 * sp.nu;
+    const double step = sb.nu;
+    const double stop = voxel_depth - 2.5 * sb.nu;
     if (stop <= 2.0 * step) return false;
     const double z = dot3(dc, dc);
     const d3 ray = z > 0.0 ? div3(dc, sqrt(z)) : dc;
@@ -102,17 +128,15 @@ __device__ bool occluded_along_ray(const SemParams& sp, HashView h,
     bool prev_valid = false;
     for (double t = 2.0 * step; t < stop; t += step) {
         int32_t vc[3];
-        world_to_voxel(add3(sp.cam_o, scale3(t, ray)), sp.inv_nu, vc);
+        world_to_voxel(add3(cam_o, scale3(t, ray)), sb.inv_nu, vc);
         const int32_t bx = block_coord(vc[0]), by = block_coord(vc[1]), bz = block_coord(vc[2]);
         uint32_t s = kInvalid;
-        if (key_in_range(bx) && key_in_range(by) && key_in_range(bz))
-            s = hash_find(h, pack_key(bx, by, bz));
+        if (key_in_range(bx) && key_in_range(by) && key_in_range(bz)) s = hash_find(h, pack_key(bx, by, bz));
         if (s == kInvalid) {
             prev_valid = false;
             continue;
         }
-        const svx_tsdf_voxel& vox =
-            pool[uint64_t(h.vals[s]) * kBlockVoxels + local_linear(vc[0], vc[1], vc[2])];
+        const svx_tsdf_voxel& vox = pool[uint64_t(h.vals[s]) * kBlockVoxels + local_linear(vc[0], vc[1], vc[2])];
         if (!(vox.weight > 0.f)) {
             prev_valid = false;
             continue;
@@ -124,7 +148,7 @@ __device__ bool occluded_along_ray(const SemParams& sp, HashView h,
     return false;
 }
 
-// The voxel's K class probabilities in registers (compile-time K) or in place.
+// The voxel's K class probabilities in registers (compile-time K).
 template <int KC>
 struct Probs {
     float v[KC];
@@ -166,12 +190,11 @@ struct Probs {
 };
 
 // Likelihood of class k for one pixel (label_to_likelihood / the floored tensor,
-// semantic_integrator.cpp:24-39,130-145), divided by its f32 sum as the
-// reference does. A label likelihood has two distinct values, so two divisions
-// replace K (same quotients).
+// semantic_integrator.cpp:24-39,130-145), divided by its f32 sum as the reference does.
+// A label likelihood has two distinct values, so two divisions replace K (same quotients).
 struct Like {
     const float* tp;  // tensor row or nullptr
-    float floor_v, inv_src, lb, lt;
+    float floor_v, lb, lt;
     int label;
     float sum;
     __device__ inline float operator()(int k) const {
@@ -183,129 +206,166 @@ struct Like {
     }
 };
 
-template <int KC>
-__device__ inline void bayes_step(float* probs, const Like& like, int K, bool use_bayes) {
-    if constexpr (KC > 0) {
-        Probs<KC> p;
-        p.load(probs);
-        if (use_bayes) {  // apply_likelihood (semantic_integrator.cpp:44-52)
-            double z = 0.0;
-#pragma unroll
-            for (int k = 0; k < KC; ++k) {
-                p.v[k] = p.v[k] * like(k);
-                z += double(p.v[k]);
-            }
-            const float inv = float(1.0 / z);
-#pragma unroll
-            for (int k = 0; k < KC; ++k) p.v[k] = p.v[k] * inv;
-        } else {  // apply_latest_argmax (semantic_integrator.cpp:54-59)
-            int best = 0;
-            float bl = like(0);
-            for (int k = 1; k < KC; ++k) {
-                const float lk = like(k);
-                if (lk > bl) {  // tie -> lower id
-                    best = k;
-                    bl = lk;
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < KC; ++k) p.v[k] = k == best ? 1.f : 0.f;
+__device__ inline Like make_like(const SemBatch& sb, const ImgParams& ip, uint32_t px, int K) {
+    Like like{nullptr, sb.floor_v, 0.f, 0.f, -1, 0.f};
+    if (ip.has_tensor) {
+        like.tp = ip.tensor + uint64_t(px) * K;
+        for (int k = 0; k < K; ++k) {
+            const float tk = like.tp[k];
+            like.sum += tk < sb.floor_v ? sb.floor_v : tk;
         }
-        p.store(probs);
     } else {
-        if (use_bayes) {
-            double z = 0.0;
-            for (int k = 0; k < K; ++k) {
-                const float pk = probs[k] * like(k);
-                probs[k] = pk;
-                z += double(pk);
-            }
-            const float inv = float(1.0 / z);
-            for (int k = 0; k < K; ++k) probs[k] = probs[k] * inv;
-        } else {
-            int best = 0;
-            float bl = like(0);
-            for (int k = 1; k < K; ++k) {
-                const float lk = like(k);
-                if (lk > bl) {
-                    best = k;
-                    bl = lk;
-                }
-            }
-            for (int k = 0; k < K; ++k) probs[k] = k == best ? 1.f : 0.f;
+        // label_to_likelihood (semantic_integrator.cpp:24-39): floored, f32 sum in k order
+        const float cf = ip.has_conf ? ip.conf[px] : sb.default_conf;
+        int label = int(ip.labels[px]);
+        float base = K > 1 ? (1.f - cf) / float(K - 1) : 1.f;
+        float top = K > 1 ? cf : 1.f;
+        if (!(label >= 0 && label < K)) label = -1;
+        base = base < sb.floor_v ? sb.floor_v : base;
+        top = top < sb.floor_v ? sb.floor_v : top;
+        for (int k = 0; k < K; ++k) like.sum += (k == label) ? top : base;
+        like.label = label;
+        like.lb = base / like.sum;
+        like.lt = top / like.sum;
+    }
+    return like;
+}
+
+// apply_likelihood / apply_latest_argmax (semantic_integrator.cpp:44-59) on registers
+template <int KC>
+__device__ inline void bayes_regs(Probs<KC>& p, const Like& like, bool use_bayes) {
+    if (use_bayes) {
+        double z = 0.0;
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            p.v[k] = p.v[k] * like(k);
+            z += double(p.v[k]);
         }
+        const float inv = float(1.0 / z);
+#pragma unroll
+        for (int k = 0; k < KC; ++k) p.v[k] = p.v[k] * inv;
+    } else {
+        int best = 0;
+        float bl = like(0);
+        for (int k = 1; k < KC; ++k) {
+            const float lk = like(k);
+            if (lk > bl) {  // tie -> lower id
+                best = k;
+                bl = lk;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < KC; ++k) p.v[k] = k == best ? 1.f : 0.f;
     }
 }
 
-#ifndef SVX_SEM_PARTS
-#define SVX_SEM_PARTS 8
-#endif
-constexpr int kParts = SVX_SEM_PARTS;  // warp tasks per candidate block
+// the same in place (class counts without a compile-time specialisation)
+__device__ inline void bayes_mem(float* probs, const Like& like, int K, bool use_bayes) {
+    if (use_bayes) {
+        double z = 0.0;
+        for (int k = 0; k < K; ++k) {
+            const float pk = probs[k] * like(k);
+            probs[k] = pk;
+            z += double(pk);
+        }
+        const float inv = float(1.0 / z);
+        for (int k = 0; k < K; ++k) probs[k] = probs[k] * inv;
+    } else {
+        int best = 0;
+        float bl = like(0);
+        for (int k = 1; k < K; ++k) {
+            const float lk = like(k);
+            if (lk > bl) {
+                best = k;
+                bl = lk;
+            }
+        }
+        for (int k = 0; k < K; ++k) probs[k] = k == best ? 1.f : 0.f;
+    }
+}
+
+constexpr int kParts = 16;  // warp tasks per candidate block: lane = voxel
 constexpr uint32_t kLayerClaim = 0xFFFFFFFEu;  // semantic layer being allocated
 
+// Whether the check pass must evaluate image i: it may read an invalid confidence (an
+// invalid default without a map, or a map k_check_conf flagged).
+__device__ inline bool needs_check(const ImgParams& ip, const uint32_t* xconf, int i) {
+    return ip.conf_maybe && (!ip.has_conf || xconf[i]);
+}
+
+// xconf[i]: image i's confidence map holds an invalid value; xerr[i]: image i reads one
+// (check pass); xupd[i]: voxels image i updated.
 template <int KC>
 __global__ void __launch_bounds__(kThreads)
-k_sem_update(SemParams sp, HashView h, const uint64_t* __restrict__ block_keys,
-             const svx_tsdf_voxel* __restrict__ pool, float* __restrict__ sem,
-             uint32_t* __restrict__ sem_idx, const uint32_t* __restrict__ cand,
-             const uint16_t* __restrict__ labels, const float* __restrict__ conf,
-             const float* __restrict__ tensor, uint8_t* __restrict__ dirty_sem,
-             int check, uint32_t* __restrict__ ctr) {
+k_sem_update(const __grid_constant__ SemBatch sb, HashView h, const uint64_t* __restrict__ block_keys,
+             const svx_tsdf_voxel* __restrict__ pool, float* __restrict__ sem, uint32_t* __restrict__ sem_idx,
+             const uint2* __restrict__ cand, uint8_t* __restrict__ dirty_sem, int check,
+             const uint32_t* __restrict__ xconf, uint32_t* __restrict__ xerr, uint32_t* __restrict__ xupd,
+             uint32_t* __restrict__ ctr) {
     const int lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    // an image that throws (a voxel passing every test reads a confidence outside
-    // [0, 1], label_to_likelihood, semantic_integrator.cpp:24-27,140-142) updates
-    // nothing, and no later image of the batch runs
-    if (ctr[C_ERR_CONF]) return;
-    // check pass: runs only when the image holds such a confidence (or the default is
-    // one); evaluates the reference's test sequence and flags, writes nothing else
-    if (check && !ctr[C_CONF_MAYBE]) return;
+    // a confidence error of an earlier pass of the batch: nothing more is applied
+    const uint32_t err = ctr[C_ERR_CONF];
+    if (err && err != sb.pass_id) return;
+    int n_apply = sb.n;
+    if (check) {
+        bool any = false;
+        for (int i = 0; i < sb.n; ++i) any |= needs_check(sb.img[i], xconf, i);
+        if (!any) return;
+    } else {
+        // images applied: up to the first one whose check failed (the reference throws in it)
+        for (int i = 0; i < sb.n; ++i)
+            if (xerr[i]) {
+                n_apply = i;
+                break;
+            }
+        if (n_apply == 0) return;
+    }
     const uint32_t n_cand = ctr[C_CAND];
-    const int K = KC > 0 ? KC : sp.K;
-    uint32_t n_upd = 0;
-    // task = (candidate block, quarter): 4 voxels per lane keeps each warp's chain of
-    // dependent loads short; the grid is sized to the resident CTAs
+    const int K = KC > 0 ? KC : sb.K;
+    // the pixel of each (image, voxel) of a warp's task in shared memory: the image loops
+    // stay rolled (one copy of the likelihood / Bayes code: unrolled over 8 images the
+    // kernel outgrows the instruction cache)
+    __shared__ uint32_t s_pix[kThreads / 32][kMaxImg][32];
+    uint32_t (*pix)[32] = s_pix[threadIdx.x >> 5];
+    uint32_t n_upd = 0;  // lane i < n_apply: voxels image i updated
     for (uint32_t t = warp; t < kParts * n_cand; t += nwarps) {
-        const uint32_t idx = cand[t / kParts];
-        const int part = int(t % kParts);
+        const uint2 cd = cand[t / kParts];
+        const uint32_t idx = cd.x;
+        const int linear = int(t % kParts) * 32 + lane;
         const uint64_t key = block_keys[idx];
-        const svx_tsdf_voxel* blk = pool + uint64_t(idx) * kBlockVoxels;
-        constexpr int kPer = kBlockVoxels / 32 / kParts;
-        uint32_t pix[kPer];
+        const svx_tsdf_voxel* v = pool + uint64_t(idx) * kBlockVoxels + linear;
+        const float w = v->weight, dist = v->distance;
         uint32_t pass = 0;
-#pragma unroll
-        for (int j = 0; j < kPer; ++j) {
-            pix[j] = 0;
-            const int linear = (part * kPer + j) * 32 + lane;
-            const float w = blk[linear].weight;
-            const float dist = blk[linear].distance;
-            if (!(w > 0.f)) continue;
-            if (double(dist) < sp.occ_floor) continue;
-            const d3 c = center_of(key, linear, sp.nu);
-            const d3 pc = xform(sp.w2c, c);
-            if (pc.z <= 0.0 || pc.z > sp.max_depth) continue;
-            const int u = int(floor(sp.fx * pc.x / pc.z + sp.cx));
-            const int v = int(floor(sp.fy * pc.y / pc.z + sp.cy));
-            if (u < 0 || u >= sp.W || v < 0 || v >= sp.H) continue;
-            if (sp.raycast && occluded_along_ray(sp, h, pool, c)) continue;
-            pix[j] = uint32_t(v) * uint32_t(sp.W) + uint32_t(u);
-            pass |= 1u << j;
+        if (w > 0.f && !(double(dist) < sb.occ_floor)) {
+            const d3 c = center_of(key, linear, sb.nu);
+#pragma unroll 1
+            for (int i = 0; i < n_apply; ++i) {
+                if (!((cd.y >> i) & 1u)) continue;
+                const ImgParams& ip = sb.img[i];
+                const d3 pc = xform(ip.w2c, c);
+                if (pc.z <= 0.0 || pc.z > ip.max_depth) continue;
+                const int u = int(floor(ip.fx * pc.x / pc.z + ip.cx));
+                const int vv = int(floor(ip.fy * pc.y / pc.z + ip.cy));
+                if (u < 0 || u >= ip.W || vv < 0 || vv >= ip.H) continue;
+                if (sb.raycast && occluded_along_ray(sb, ip.cam_o, h, pool, c)) continue;
+                pix[i][lane] = uint32_t(vv) * uint32_t(ip.W) + uint32_t(u);
+                pass |= 1u << i;
+            }
         }
         if (!__any_sync(0xFFFFFFFFu, pass != 0)) continue;
-        if (check) {
-            if (!sp.has_tensor) {
-#pragma unroll
-                for (int j = 0; j < kPer; ++j) {
-                    if (!((pass >> j) & 1u)) continue;
-                    const float cf = sp.has_conf ? conf[pix[j]] : sp.default_conf;
-                    if (cf < 0.f || cf > 1.f) atomicOr(&ctr[C_ERR_CONF], 1u);
-                }
+        if (check) {  // flag images whose passing voxels read an invalid confidence
+#pragma unroll 1
+            for (int i = 0; i < n_apply; ++i) {
+                if (!((pass >> i) & 1u) || !needs_check(sb.img[i], xconf, i) || sb.img[i].has_tensor) continue;
+                const float cf = sb.img[i].has_conf ? sb.img[i].conf[pix[i][lane]] : sb.default_conf;
+                if (cf < 0.f || cf > 1.f) atomicOr(&xerr[i], 1u);
             }
             continue;
         }
-        // the block's semantic layer (ensure_semantics): the first part to need it
-        // claims it, fills it with 1/K and publishes its index; other parts wait
+        // the block's semantic layer (ensure_semantics): the first task to need it claims
+        // it, fills it with 1/K and publishes its index; other tasks wait
         uint32_t sid = __ldcg(&sem_idx[idx]);
         if (sid == kInvalid || sid == kLayerClaim) {
             uint32_t claimed = 0;
@@ -331,58 +391,74 @@ k_sem_update(SemParams sp, HashView h, const uint64_t* __restrict__ block_keys,
                 if (lane == 0) atomicExch(&sem_idx[idx], sid);
             }
         }
+        if (pass) {  // the passing images in order, the probabilities in registers meanwhile
+            float* probs = sem + (uint64_t(sid) * kBlockVoxels + linear) * K;
+            if constexpr (KC > 0) {
+                Probs<KC> p;
+                p.load(probs);
 #pragma unroll 1
-        for (int j = 0; j < kPer; ++j) {
-            if (!((pass >> j) & 1u)) continue;
-            const int linear = (part * kPer + j) * 32 + lane;
-            const uint32_t px = pix[j];
-            Like like{nullptr, sp.floor_v, 0.f, 0.f, 0.f, -1, 0.f};
-            if (sp.has_tensor) {
-                like.tp = tensor + uint64_t(px) * K;
-                for (int k = 0; k < K; ++k) {
-                    const float tk = like.tp[k];
-                    like.sum += tk < sp.floor_v ? sp.floor_v : tk;
+                for (uint32_t r = pass; r; r &= r - 1) {
+                    const int i = __ffs(r) - 1;
+                    bayes_regs<KC>(p, make_like(sb, sb.img[i], pix[i][lane], K), sb.use_bayes != 0);
                 }
+                p.store(probs);
             } else {
-                // label_to_likelihood (semantic_integrator.cpp:24-39): floored, f32 sum in k order
-                const float cf = sp.has_conf ? conf[px] : sp.default_conf;
-                int label = int(labels[px]);
-                float base = K > 1 ? (1.f - cf) / float(K - 1) : 1.f;
-                float top = K > 1 ? cf : 1.f;
-                if (!(label >= 0 && label < K)) label = -1;
-                base = base < sp.floor_v ? sp.floor_v : base;
-                top = top < sp.floor_v ? sp.floor_v : top;
-                for (int k = 0; k < K; ++k) like.sum += (k == label) ? top : base;
-                like.label = label;
-                like.lb = base / like.sum;
-                like.lt = top / like.sum;
+#pragma unroll 1
+                for (uint32_t r = pass; r; r &= r - 1) {
+                    const int i = __ffs(r) - 1;
+                    bayes_mem(probs, make_like(sb, sb.img[i], pix[i][lane], K), K, sb.use_bayes != 0);
+                }
             }
-            bayes_step<KC>(sem + (uint64_t(sid) * kBlockVoxels + linear) * K, like, K, sp.use_bayes != 0);
-            ++n_upd;
+        }
+        __syncwarp();
+        // per image, the warp's updated voxels: lane i keeps image i's count
+        for (int i = 0; i < n_apply; ++i) {
+            const uint32_t nu = __popc(__ballot_sync(0xFFFFFFFFu, (pass >> i) & 1u));
+            if (lane == i) n_upd += nu;
         }
         if (lane == 0) dirty_sem[idx] = 1;
     }
-    for (int o = 16; o; o >>= 1) n_upd += __shfl_xor_sync(0xFFFFFFFFu, n_upd, o);
-    if (lane == 0 && n_upd) atomicAdd(&ctr[C_SEM_UPDATED], n_upd);
+    if (lane < n_apply && n_upd) atomicAdd(&xupd[lane], n_upd);
 }
 
-// Flags an image whose confidence image holds a value outside [0, 1] (NaN passes,
-// as in the reference's comparison); the check pass of k_sem_update then decides
-// whether a voxel actually reads one.
-__global__ void k_check_conf(const float* __restrict__ conf, uint64_t n, uint32_t* __restrict__ ctr) {
+// Flags an image whose confidence map holds a value outside [0, 1] (NaN passes, as in the
+// reference's comparison); the check pass of k_sem_update then decides whether a voxel
+// actually reads one.
+__global__ void k_check_conf(const float* __restrict__ conf, uint64_t n, uint32_t* __restrict__ flag) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const float c = conf[i];
-    if (c < 0.f || c > 1.f) ctr[C_CONF_MAYBE] = 1u;
+    if (c < 0.f || c > 1.f) *flag = 1u;
+}
+
+// A check pass that found a failing image makes its error sticky for the batch.
+__global__ void k_conf_verdict(const uint32_t* __restrict__ xerr, int n, uint32_t pass_id, uint32_t* __restrict__ ctr) {
+    for (int i = 0; i < n; ++i)
+        if (xerr[i]) {
+            atomicCAS(&ctr[C_ERR_CONF], 0u, pass_id);
+            return;
+        }
+}
+
+template <int KC>
+void launch_update(const SemBatch& sb, svx_map* m, const uint2* cand, int check, const uint32_t* xconf,
+                   uint32_t* xerr, uint32_t* xupd) {
+    static int per_sm = 0;
+    if (!per_sm) SVX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sem_update<KC>, kThreads, 0));
+    const unsigned grid = std::max(1u, unsigned(per_sm)) * (persistent_grid(m->device) / 8);
+    k_sem_update<KC><<<grid, kThreads, 0, m->stream>>>(sb, hash_view(m), m->block_keys, tsdf_base(m), sem_base(m),
+                                                       m->sem_idx, cand, m->dirty + m->cfg.max_blocks, check, xconf,
+                                                       xerr, xupd, m->d_ctr);
+    count_launch();
 }
 
 }  // namespace
 
-// A sequence of label images, enqueued back to back on the map stream with one
-// synchronisation at the end (images are applied in order, each seeing the
-// previous ones' updates, exactly as successive integrate_labels calls).
-// Labels / confidences / tensors are read from device memory when on_device,
-// else copied from the host (asynchronously; pinned memory overlaps).
+// A sequence of label images, applied in passes of up to kMaxImg images (one map sweep
+// per pass) with one synchronisation at the end: the result equals successive
+// integrate_labels calls (each voxel sees the images in order). Labels / confidences /
+// tensors are read from device memory when on_device, else copied from the host
+// (asynchronously; pinned memory overlaps).
 void run_integrate_labels_batch(svx_map* m, const svx_label_image* imgs, int n, bool on_device,
                                 const svx_semantic_cfg& cfg, svx_frame_report* reps) {
     const int K = m->cfg.num_labels;
@@ -407,141 +483,136 @@ void run_integrate_labels_batch(svx_map* m, const svx_label_image* imgs, int n, 
         if (conf_n) m->conf.alloc(conf_n);
         if (ten_n) m->tensor.alloc(ten_n);
     }
-    m->cand.alloc(std::max<uint64_t>(m->n_blocks, 1));
-    m->sem_out.alloc(3ull * n);
+    const int passes = (n + kMaxImg - 1) / kMaxImg;
+    // per pass: confidence-map flags, error flags and updates per image, then candidates
+    constexpr int kOut = 3 * kMaxImg + 1;
+    m->sem_out.alloc(uint64_t(kOut) * passes);
+    SVX_CUDA(cudaMemsetAsync(m->sem_out.p, 0, 4ull * kOut * passes, m->stream));
+    m->cand.alloc(2 * std::max<uint64_t>(m->n_blocks, 1));  // uint2 per candidate block
     // a block owns at most one layer: map as many layers as there are blocks, so the
     // update kernel never outgrows the pool and no mid-pass synchronisation is needed
     ensure_layers(m, m->n_blocks);
     SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_ERR_CONF, 0, 4, m->stream));
+    uint2* cand = reinterpret_cast<uint2*>(m->cand.p);
     uint64_t lo = 0, co = 0, to = 0;
-    for (int i = 0; i < n; ++i) {
-        const svx_label_image& img = imgs[i];
-        const uint64_t P = uint64_t(img.width) * uint64_t(img.height);
-        SemParams sp{};
-        const Pose cp = to_pose(img.pose);
-        sp.w2c = inverse_pose(cp);
-        sp.cam_o = mk(cp.t[0], cp.t[1], cp.t[2]);
-        sp.fx = img.fx;
-        sp.fy = img.fy;
-        sp.cx = img.cx;
-        sp.cy = img.cy;
-        sp.max_depth = img.max_depth;
-        sp.W = img.width;
-        sp.H = img.height;
-        sp.K = K;
-        sp.nu = double(m->cfg.voxel_size);
-        sp.inv_nu = 1.0 / double(m->cfg.voxel_size);
-        sp.occ_floor = -0.5 * double(m->cfg.truncation);
-        sp.use_bayes = cfg.use_bayes != 0;
-        sp.raycast = cfg.occlusion == SVX_OCCLUSION_RAYCAST;
-        sp.has_tensor = img.prob_tensor != nullptr;
-        sp.has_conf = img.confidence != nullptr;
-        sp.floor_v = cfg.likelihood_floor;
-        sp.default_conf = cfg.default_confidence;
-        sp.n_blocks = uint32_t(m->n_blocks);
-        const uint16_t* lbl = img.labels;
-        const float* conf = img.confidence;
-        const float* ten = img.prob_tensor;
-        if (!on_device) {
-            SVX_CUDA(cudaMemcpyAsync(m->lbl.p + lo, img.labels, 2 * P, cudaMemcpyHostToDevice, m->stream));
-            lbl = m->lbl.p + lo;
-            lo += P;
-            if (conf) {
-                SVX_CUDA(cudaMemcpyAsync(m->conf.p + co, img.confidence, 4 * P, cudaMemcpyHostToDevice,
-                                         m->stream));
-                conf = m->conf.p + co;
-                co += P;
+    for (int ps = 0; ps < passes; ++ps) {
+        const int i0 = ps * kMaxImg, ni = std::min(kMaxImg, n - i0);
+        uint32_t* out = m->sem_out.p + uint64_t(kOut) * ps;
+        uint32_t *xconf = out, *xerr = out + kMaxImg, *xupd = out + 2 * kMaxImg;
+        SemBatch sb{};
+        sb.n = ni;
+        sb.K = K;
+        sb.nu = double(m->cfg.voxel_size);
+        sb.inv_nu = 1.0 / double(m->cfg.voxel_size);
+        sb.occ_floor = -0.5 * double(m->cfg.truncation);
+        sb.use_bayes = cfg.use_bayes != 0;
+        sb.raycast = cfg.occlusion == SVX_OCCLUSION_RAYCAST;
+        sb.floor_v = cfg.likelihood_floor;
+        sb.default_conf = cfg.default_confidence;
+        sb.pass_id = uint32_t(ps + 1);
+        for (int k = 0; k < ni; ++k) {
+            const svx_label_image& img = imgs[i0 + k];
+            const uint64_t P = uint64_t(img.width) * uint64_t(img.height);
+            ImgParams& ip = sb.img[k];
+            const Pose cp = to_pose(img.pose);
+            ip.w2c = inverse_pose(cp);
+            ip.cam_o = mk(cp.t[0], cp.t[1], cp.t[2]);
+            ip.fx = img.fx;
+            ip.fy = img.fy;
+            ip.cx = img.cx;
+            ip.cy = img.cy;
+            ip.max_depth = img.max_depth;
+            ip.W = img.width;
+            ip.H = img.height;
+            ip.has_tensor = img.prob_tensor != nullptr;
+            ip.has_conf = img.confidence != nullptr;
+            ip.labels = img.labels;
+            ip.conf = img.confidence;
+            ip.tensor = img.prob_tensor;
+            if (!on_device) {
+                SVX_CUDA(cudaMemcpyAsync(m->lbl.p + lo, img.labels, 2 * P, cudaMemcpyHostToDevice, m->stream));
+                ip.labels = m->lbl.p + lo;
+                lo += P;
+                if (ip.conf) {
+                    SVX_CUDA(cudaMemcpyAsync(m->conf.p + co, img.confidence, 4 * P, cudaMemcpyHostToDevice,
+                                             m->stream));
+                    ip.conf = m->conf.p + co;
+                    co += P;
+                }
+                if (ip.tensor) {
+                    SVX_CUDA(cudaMemcpyAsync(m->tensor.p + to, img.prob_tensor, 4 * P * K, cudaMemcpyHostToDevice,
+                                             m->stream));
+                    ip.tensor = m->tensor.p + to;
+                    to += P * K;
+                }
             }
-            if (ten) {
-                SVX_CUDA(cudaMemcpyAsync(m->tensor.p + to, img.prob_tensor, 4 * P * K,
-                                         cudaMemcpyHostToDevice, m->stream));
-                ten = m->tensor.p + to;
-                to += P * K;
-            }
-        }
-        // confidence validity: only a voxel that passes every test reads one
-        const bool conf_check = !ten && (conf || bad_default);
-        if (conf_check) {
-            if (conf) {
-                SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_CONF_MAYBE, 0, 4, m->stream));
-                k_check_conf<<<grid_for(P), kThreads, 0, m->stream>>>(conf, P, m->d_ctr);
-                count_launch();
-            } else {
-                SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_CONF_MAYBE, 0x01, 1, m->stream));
-            }
+            // confidence validity: only a voxel that passes every test reads one
+            ip.conf_maybe = !ip.has_tensor && (ip.has_conf || bad_default);
+            if (ip.conf_maybe) sb.any_check = 1;
         }
         SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_CAND, 0, 4, m->stream));
-        SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_SEM_UPDATED, 0, 4, m->stream));
-        if (m->n_blocks) {
-            {
-                ProfMark pm(m, SVX_K_SEM_CULL);
-                k_sem_cull<<<grid_for(m->n_blocks), kThreads, 0, m->stream>>>(sp, m->block_keys, m->cand.p,
-                                                                              m->d_ctr);
-                count_launch();
-            }
-            {
-                ProfMark pm(m, SVX_K_SEM_UPDATE);
-                // compile-time class counts keep a voxel's probabilities in registers
-                auto kern = &k_sem_update<0>;
-                switch (K) {
-                    case 2: kern = &k_sem_update<2>; break;
-                    case 4: kern = &k_sem_update<4>; break;
-                    case 8: kern = &k_sem_update<8>; break;
-                    case 10: kern = &k_sem_update<10>; break;
-                    case 16: kern = &k_sem_update<16>; break;
-                    case 19: kern = &k_sem_update<19>; break;
-                    case 20: kern = &k_sem_update<20>; break;
-                    case 32: kern = &k_sem_update<32>; break;
-                    default: break;
+        if (!m->n_blocks) continue;
+        {
+            ProfMark pm(m, SVX_K_SEM_CULL);
+            k_sem_cull<<<std::min<unsigned>(grid_for(m->n_blocks), persistent_grid(m->device)), kThreads, 0,
+                         m->stream>>>(sb, m->block_keys, cand, m->d_ctr);
+            count_launch();
+        }
+        SVX_CUDA(cudaMemcpyAsync(out + 3 * kMaxImg, m->d_ctr + C_CAND, 4, cudaMemcpyDeviceToDevice, m->stream));
+        {
+            ProfMark pm(m, SVX_K_SEM_UPDATE);
+            for (int check = sb.any_check ? 1 : 0; check >= 0; --check) {
+                if (check)
+                    for (int k = 0; k < ni; ++k)
+                        if (sb.img[k].conf_maybe && sb.img[k].has_conf) {
+                            const uint64_t P = uint64_t(sb.img[k].W) * uint64_t(sb.img[k].H);
+                            k_check_conf<<<grid_for(P), kThreads, 0, m->stream>>>(sb.img[k].conf, P, xconf + k);
+                            count_launch();
+                        }
+                switch (K) {  // compile-time class counts keep a voxel's probabilities in registers
+                    case 2: launch_update<2>(sb, m, cand, check, xconf, xerr, xupd); break;
+                    case 4: launch_update<4>(sb, m, cand, check, xconf, xerr, xupd); break;
+                    case 8: launch_update<8>(sb, m, cand, check, xconf, xerr, xupd); break;
+                    case 10: launch_update<10>(sb, m, cand, check, xconf, xerr, xupd); break;
+                    case 16: launch_update<16>(sb, m, cand, check, xconf, xerr, xupd); break;
+                    case 19: launch_update<19>(sb, m, cand, check, xconf, xerr, xupd); break;
+                    case 20: launch_update<20>(sb, m, cand, check, xconf, xerr, xupd); break;
+                    case 32: launch_update<32>(sb, m, cand, check, xconf, xerr, xupd); break;
+                    default: launch_update<0>(sb, m, cand, check, xconf, xerr, xupd); break;
                 }
-                int per_sm = 0;
-                SVX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0));
-                const unsigned grid = std::max(1u, unsigned(per_sm)) * (persistent_grid(m->device) / 8);
-                for (int check = conf_check ? 1 : 0; check >= 0; --check) {
-                    kern<<<grid, kThreads, 0, m->stream>>>(
-                        sp, hash_view(m), m->block_keys, tsdf_base(m), sem_base(m), m->sem_idx, m->cand.p,
-                        lbl, conf, ten, m->dirty + m->cfg.max_blocks, check, m->d_ctr);
+                if (check) {
+                    k_conf_verdict<<<1, 1, 0, m->stream>>>(xerr, ni, sb.pass_id, m->d_ctr);
                     count_launch();
                 }
             }
-            SVX_CUDA(cudaGetLastError());
         }
-        // per-image results: candidates and updated voxels
-        SVX_CUDA(cudaMemcpyAsync(m->sem_out.p + 3 * i, m->d_ctr + C_CAND, 4, cudaMemcpyDeviceToDevice,
-                                 m->stream));
-        SVX_CUDA(cudaMemcpyAsync(m->sem_out.p + 3 * i + 1, m->d_ctr + C_SEM_UPDATED, 4,
-                                 cudaMemcpyDeviceToDevice, m->stream));
-        SVX_CUDA(cudaMemcpyAsync(m->sem_out.p + 3 * i + 2, m->d_ctr + C_ERR_CONF, 4,
-                                 cudaMemcpyDeviceToDevice, m->stream));
+        SVX_CUDA(cudaGetLastError());
     }
-    std::vector<uint32_t> outs(3ull * n);
-    SVX_CUDA(cudaMemcpyAsync(outs.data(), m->sem_out.p, 12ull * n, cudaMemcpyDeviceToHost, m->stream));
+    std::vector<uint32_t> outs(size_t(kOut) * passes);
+    SVX_CUDA(cudaMemcpyAsync(outs.data(), m->sem_out.p, 4ull * kOut * passes, cudaMemcpyDeviceToHost, m->stream));
     sync_counters(m);
-    if (m->h_ctr[C_ERR_CONF]) {
+    int fail = n;  // the first image that reads an invalid confidence
+    for (int i = 0; i < n && fail == n; ++i)
+        if (outs[size_t(kOut) * (i / kMaxImg) + kMaxImg + (i % kMaxImg)]) fail = i;
+    for (int i = 0; i < fail; ++i) {
+        const size_t ps = size_t(i / kMaxImg);
+        reps[i].frame = m->sem_frames++;
+        reps[i].updated_voxels = outs[kOut * ps + 2 * kMaxImg + (i % kMaxImg)];
+        m->prof_acc.sem_images += 1;
+        m->prof_acc.sem_updated += reps[i].updated_voxels;
+    }
+    for (int ps = 0; ps < passes; ++ps) m->prof_acc.sem_candidates += outs[size_t(kOut) * ps + 3 * kMaxImg];
+    m->prof_acc.sem_new_layers += m->h_ctr[C_SEM] - m->n_layers;
+    m->n_layers = m->h_ctr[C_SEM];
+    if (fail < n) {
         // images before the failing one are complete; the failing one is numbered (the
         // reference numbers a frame before it can throw, semantic_integrator.cpp:93-94)
         // and updated nothing; later images did not run
-        int fail = 0;
-        while (fail < n && !outs[3 * fail + 2]) ++fail;
-        for (int i = 0; i < fail && i < n; ++i) {
-            reps[i].frame = m->sem_frames++;
-            reps[i].updated_voxels = outs[3 * i + 1];
-        }
         m->sem_frames++;
-        m->n_layers = m->h_ctr[C_SEM];
         SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_ERR_CONF, 0, 4, m->stream));
         SVX_CUDA(cudaStreamSynchronize(m->stream));
         throw Error(SVX_INVALID_ARGUMENT, "confidence must be in [0, 1]");
     }
-    for (int i = 0; i < n; ++i) {
-        reps[i].frame = m->sem_frames++;
-        reps[i].updated_voxels = outs[3 * i + 1];
-        m->prof_acc.sem_images += 1;
-        m->prof_acc.sem_candidates += outs[3 * i];
-        m->prof_acc.sem_updated += outs[3 * i + 1];
-    }
-    m->prof_acc.sem_new_layers += m->h_ctr[C_SEM] - m->n_layers;
-    m->n_layers = m->h_ctr[C_SEM];
 }
 
 void run_integrate_labels(svx_map* m, const svx_label_image& img, const svx_semantic_cfg& cfg,
