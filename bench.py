@@ -539,9 +539,10 @@ def run_cfg3(args, world, rank, local):
     icfg = svx.IntegratorConfig()
     torch.cuda.synchronize()
 
+    scfg = svx.SemanticConfig()
+
     def leg(device_resident, clocks=None):
         st = svx.VoxelStore(cfg, local)
-        si = svx.SemanticIntegrator(st)
         ext = torch.cuda.ExternalStream(st.stream_ptr(), device=dev)
         step_ms, pts, upd = [], 0, 0
         launches0 = 0
@@ -555,18 +556,17 @@ def run_cfg3(args, world, rank, local):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(ext)
-            su = sp = 0
-            for i in range(s * spp, (s + 1) * spp):
-                a = int(offs[i])
-                rel = offs[i:i + 2] - offs[i]
-                if device_resident:
-                    r = st.integrate_clouds_device(wl.model, pts_dev.data_ptr() + 12 * a, rel, 3, [wl.pose(i)], icfg)
-                    ls = si.integrate_labels_batch(lab_dev[i], on_device=True)
-                else:
-                    r = st.integrate_clouds_host(wl.model, pts_host.data_ptr() + 12 * a, rel, 3, [wl.pose(i)], icfg)
-                    ls = si.integrate_labels_batch(lab_pin[i])
-                su += r[0].updated_voxels + sum(x.updated_voxels for x in ls)
-                sp += len(scans[i])
+            # the whole step in one call: TSDF frame groups, each frame's 6 label images
+            # right after its fold (svx_integrate_clouds_labels)
+            f0, f1 = s * spp, (s + 1) * spp
+            rel = offs[f0:f1 + 1] - offs[f0]
+            src = pts_dev if device_resident else pts_host
+            tr, lr = svx.integrate_clouds_labels(
+                st, wl.model, src.data_ptr() + 12 * int(offs[f0]), rel, 3, [wl.pose(i) for i in range(f0, f1)],
+                icfg, [lab_dev[i] if device_resident else lab_pin[i] for i in range(f0, f1)], scfg,
+                points_on_device=device_resident, labels_on_device=device_resident)
+            su = sum(r.updated_voxels for r in tr) + sum(r.updated_voxels for r in lr)
+            sp = int(offs[f1] - offs[f0])
             e1.record(ext)
             e1.synchronize()
             if clocks and s >= args.warmup:
@@ -592,7 +592,7 @@ def run_cfg3(args, world, rank, local):
                "h2d_bytes_per_step": int(12 * p2 / args.steps + spp * sum(2 * li.width * li.height
                                                                            for li in labels[0])),
                "d2h_bytes_per_step": int(spp * 7 * 32),
-               "api": "svx_integrate_clouds + svx_integrate_labels_batch (pinned host points and labels)"}
+               "api": "svx_integrate_clouds_labels (pinned host points and label images)"}
     peak, peak_src = peaks()
     nf = max(prof["frames"], 1)
     # SURVEY 8(d) bytes: geometry terms + semantic terms (2 B/label pixel, 8 B per frustum
@@ -955,7 +955,7 @@ def main():
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
     if args.scans_per_step is None:
-        args.scans_per_step = {"cfg3": 10, "cfg4": 400}.get(args.workload, 100)
+        args.scans_per_step = {"cfg3": 16, "cfg4": 400}.get(args.workload, 100)
     relaunch_if_needed(args)
     world, rank, local = dist_env()
     if world > 1:

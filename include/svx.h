@@ -239,6 +239,22 @@ svx_status svx_integrate_clouds(svx_map* map, svx_scan* scan, const float* point
                                 const uint64_t* offsets, int32_t stride, const svx_pose* poses,
                                 int32_t n_frames, const svx_integrator_cfg* cfg,
                                 svx_frame_report* reports);
+/* cmd_integrate's per-frame body over a sequence (semvox_main.cpp:121-146):
+ * project_cloud + compute_normal_image + integrate_frame of cloud f, then
+ * integrate_labels of its label images imgs[img_offsets[f] .. img_offsets[f+1]) (one
+ * SemanticIntegrator: frame numbers continue across the images). Clouds in device
+ * memory (points_on_device) or pinned host memory; label images in device memory
+ * (imgs_on_device) or host memory. Frames run in groups of up to 16 with each frame's
+ * label pass right after its fold, so the result equals the per-frame calls; a batch whose
+ * label images may throw (confidence maps, or an invalid default confidence) alternates
+ * frame by frame instead. reports[n_frames], label_reports[img_offsets[n_frames]]. */
+svx_status svx_integrate_clouds_labels(svx_map* map, svx_scan* scan, const float* points,
+                                       const uint64_t* offsets, int32_t stride,
+                                       int32_t points_on_device, const svx_pose* poses,
+                                       int32_t n_frames, const svx_integrator_cfg* cfg,
+                                       const svx_label_image* imgs, const int32_t* img_offsets,
+                                       int32_t imgs_on_device, const svx_semantic_cfg* scfg,
+                                       svx_frame_report* reports, svx_frame_report* label_reports);
 /* Multi-GPU data plane (exchange mode, SURVEY.md 8(e) "ray-partitioned DDA + one
  * all-to-all visit exchange"; no reference analogue: the reference is single-process).
  * On a key-sharded map (svx_map_set_shard, world >= 2) one group of n_frames <= 16

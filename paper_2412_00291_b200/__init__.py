@@ -200,6 +200,9 @@ def _sig(lib: C.CDLL) -> None:
                                             C.POINTER(IntegratorCfg), P]),
         "svx_integrate_clouds": (S, [P, P, P, P, C.c_int32, P, C.c_int32,
                                      C.POINTER(IntegratorCfg), P]),
+        "svx_integrate_clouds_labels": (S, [P, P, P, P, C.c_int32, C.c_int32, P, C.c_int32,
+                                            C.POINTER(IntegratorCfg), P, P, C.c_int32, C.POINTER(SemanticCfg),
+                                            P, P]),
         "svx_integrate_clouds_xbegin": (S, [P, P, P, P, C.c_int32, P, C.c_int32, C.POINTER(IntegratorCfg),
                                             P, C.POINTER(P)]),
         "svx_integrate_clouds_xend": (S, [P, P, P, P]),
@@ -820,6 +823,63 @@ class SemanticIntegrator:
                                                 int(on_device), C.byref(self.cfg.c()),
                                                 C.cast(reps, C.c_void_p)))
         return [FrameReport.of(r) for r in reps]
+
+    def label_array(self, imgs: list, on_device: bool = False):
+        """(LabelImageC array, buffers to keep alive) for the C-ABI."""
+        K = self.store.cfg.num_labels
+        n = len(imgs)
+        arr = (LabelImageC * max(n, 1))()
+        keep = []
+
+        def addr(x, dtype):
+            if x is None:
+                return None
+            if on_device:
+                return C.c_void_p(x if isinstance(x, int) else x.data_ptr())
+            a = np.ascontiguousarray(np.asarray(x, dtype).reshape(-1))
+            keep.append(a)
+            return C.c_void_p(a.ctypes.data)
+
+        for i, img in enumerate(imgs):
+            P = img.width * img.height
+            conf = img.confidence if (img.confidence is not None and (
+                on_device or np.asarray(img.confidence).size == P)) else None
+            ten = img.prob_tensor if (img.prob_tensor is not None and (
+                on_device or np.asarray(img.prob_tensor).size == P * K)) else None
+            pc = img.pose if isinstance(img.pose, PoseC) else (
+                img.pose.c() if isinstance(img.pose, Pose) else pose_c(img.pose))
+            arr[i] = LabelImageC(img.width, img.height,
+                                 C.cast(addr(img.labels, np.uint16), C.POINTER(C.c_uint16)),
+                                 C.cast(addr(conf, np.float32), C.POINTER(C.c_float)),
+                                 C.cast(addr(ten, np.float32), C.POINTER(C.c_float)),
+                                 img.fx, img.fy, img.cx, img.cy, pc, img.max_depth)
+        return arr, keep
+
+
+def integrate_clouds_labels(store: "VoxelStore", model: ProjectionModel, points_ptr: int, offsets,
+                            stride: int, poses: list, icfg: "IntegratorConfig", frame_images: list,
+                            scfg: "SemanticConfig" = None, points_on_device: bool = True,
+                            labels_on_device: bool = False):
+    """svx_integrate_clouds_labels: cmd_integrate's per-frame body over a sequence (the
+    TSDF frame, then its label images frame_images[f]) in frame groups. Returns (TSDF
+    reports, label reports)."""
+    scfg = scfg or SemanticConfig()
+    n = len(poses)
+    imgs = [li for f in frame_images for li in f]
+    img_off = np.zeros(n + 1, np.int32)
+    img_off[1:] = np.cumsum([len(f) for f in frame_images])
+    arr, keep = SemanticIntegrator(store, scfg).label_array(imgs, labels_on_device)
+    offs = np.ascontiguousarray(np.asarray(offsets, np.uint64))
+    parr = (PoseC * n)(*poses)
+    reps = (FrameReportC * n)()
+    lreps = (FrameReportC * max(len(imgs), 1))()
+    _check(lib().svx_integrate_clouds_labels(store.handle, store.scan(model), C.c_void_p(points_ptr), _ptr(offs),
+                                             stride, int(points_on_device), C.cast(parr, C.c_void_p), n,
+                                             C.byref(icfg.c()), C.cast(arr, C.c_void_p), _ptr(img_off),
+                                             int(labels_on_device), C.byref(scfg.c()), C.cast(reps, C.c_void_p),
+                                             C.cast(lreps, C.c_void_p)))
+    del keep
+    return [FrameReport.of(r) for r in reps], [FrameReport.of(lreps[i]) for i in range(len(imgs))]
 
     def take_dirty_blocks(self) -> np.ndarray:
         return self.store.take_dirty_blocks(1)

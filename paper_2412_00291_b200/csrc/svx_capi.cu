@@ -1075,6 +1075,58 @@ svx_status svx_integrate_clouds(svx_map* m, svx_scan* s, const float* points, co
     });
 }
 
+svx_status svx_integrate_clouds_labels(svx_map* m, svx_scan* s, const float* points, const uint64_t* offsets,
+                                       int32_t stride, int32_t points_on_device, const svx_pose* poses,
+                                       int32_t n_frames, const svx_integrator_cfg* cfg, const svx_label_image* imgs,
+                                       const int32_t* img_offsets, int32_t imgs_on_device,
+                                       const svx_semantic_cfg* scfg, svx_frame_report* reports,
+                                       svx_frame_report* label_reports) {
+    return guarded([&] {
+        require(m && s && cfg && scfg && reports && offsets && img_offsets && (points || n_frames <= 0),
+                SVX_INVALID_ARGUMENT, "null argument");
+        require(s->map == m, SVX_INVALID_ARGUMENT, "scan belongs to another map");
+        require(stride >= 3, SVX_INVALID_ARGUMENT, "point stride must be >= 3");
+        DeviceGuard g(m->device);
+        const auto t0 = std::chrono::steady_clock::now();
+        const int n_img = n_frames > 0 ? img_offsets[n_frames] : 0;
+        require(n_frames <= 0 || img_offsets[0] == 0, SVX_INVALID_ARGUMENT, "img_offsets[0] must be 0");
+        require(n_img == 0 || (imgs && label_reports), SVX_INVALID_ARGUMENT, "null label images");
+        std::vector<FrameJob> jobs(size_t(std::max(n_frames, 0)));
+        for (int32_t f = 0; f < n_frames; ++f) {
+            validate_pose(poses[f]);
+            require(offsets[f + 1] >= offsets[f] && img_offsets[f + 1] >= img_offsets[f], SVX_INVALID_ARGUMENT,
+                    "offsets must not decrease");
+            require(offsets[f + 1] - offsets[f] < (1ull << 32), SVX_INVALID_ARGUMENT, "too many points in one cloud");
+            jobs[f] = FrameJob{s, to_pose(poses[f]), points + offsets[f] * stride, offsets[f + 1] - offsets[f],
+                               stride, true, points_on_device == 0};
+        }
+        // a label pass that may throw (a confidence map, or an invalid default confidence)
+        // must stop the sequence at its frame: those batches alternate frame by frame
+        bool may_throw = scfg->default_confidence < 0.f || scfg->default_confidence > 1.f;
+        for (int i = 0; i < n_img; ++i) may_throw |= imgs[i].confidence != nullptr;
+        if (may_throw) {
+            for (int32_t f = 0; f < n_frames; ++f) {
+                run_frames(m, &jobs[size_t(f)], 1, *cfg, &reports[f]);
+                const int a = img_offsets[f], b = img_offsets[f + 1];
+                if (b > a) run_integrate_labels_batch(m, imgs + a, b - a, imgs_on_device != 0, *scfg, label_reports + a);
+            }
+        } else {
+            // every block the batch can allocate lies below the mapped pool (the band aborts
+            // otherwise): size the label passes' candidate list and layers for it
+            const uint64_t head = std::max<uint64_t>(32768, uint64_t(2.0 * m->new_ema * n_frames));
+            ensure_blocks(m, m->n_blocks + head, 4 * head);
+            LabelBatch lb = labels_begin(m, imgs, n_img, imgs_on_device != 0, *scfg,
+                                         std::max<uint64_t>(m->mapped_blocks, m->n_blocks + head));
+            LabelHook hook{&lb, img_offsets};
+            run_frames(m, jobs.data(), n_frames, *cfg, reports, &hook);
+            labels_finish(m, lb, label_reports);
+        }
+        const double ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        for (int32_t f = 0; f < n_frames; ++f) reports[f].elapsed_ms = ms / n_frames;
+    });
+}
+
 svx_status svx_integrate_clouds_xbegin(svx_map* m, svx_scan* s, const float* d_points, const uint64_t* offsets,
                                        int32_t stride, const svx_pose* poses, int32_t n_frames,
                                        const svx_integrator_cfg* cfg, uint64_t* send_meta, const void** d_send) {

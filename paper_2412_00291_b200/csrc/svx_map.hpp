@@ -341,8 +341,16 @@ struct FrameJob {
 };
 // Runs the frames in groups of up to kMaxG on the map stream, synchronising once at
 // the end (plus once per abort + retry, rare). Fills one report per frame.
+struct LabelBatch;
+// Label images interleaved with a TSDF batch: the images [img_off[f], img_off[f + 1]) of
+// frame f run right after frame f's fold (cmd_integrate's integrate_frame +
+// integrate_labels, semvox_main.cpp:122-143).
+struct LabelHook {
+    LabelBatch* lb;
+    const int* img_off;  // [n_frames + 1]
+};
 void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cfg& cfg,
-                svx_frame_report* reps);
+                svx_frame_report* reps, LabelHook* labels = nullptr);
 // Exchange mode (multi-GPU data plane): one frame group in two halves around
 // the caller's all-to-all. xbegin projects the group and casts this rank's share of its
 // rays; visits of blocks other ranks own are returned packed by destination (16-byte
@@ -359,6 +367,25 @@ void run_integrate_labels(svx_map* m, const svx_label_image& img, const svx_sema
                           svx_frame_report* rep);
 void run_integrate_labels_batch(svx_map* m, const svx_label_image* imgs, int n, bool on_device,
                                 const svx_semantic_cfg& cfg, svx_frame_report* reps);
+// The same split in three (svx_semantic.cu): stage a batch, enqueue the label passes of
+// images [i0, i1) without synchronising (TSDF frame groups interleave them with their
+// folds), read the reports after the stream synchronised.
+constexpr int kMaxLabelImages = 8;  // label images fused in one pass over the map
+struct LabelBatch {
+    const svx_label_image* imgs = nullptr;
+    int n = 0;
+    bool on_device = false;
+    svx_semantic_cfg cfg{};
+    int passes = 0, max_passes = 0;
+    std::vector<int> pass_first, pass_count;
+    uint64_t lo = 0, co = 0, to = 0;  // host staging offsets
+    std::vector<const uint16_t*> staged_lbl;  // per image: its staged device copy
+    std::vector<const float*> staged_conf, staged_ten;
+};
+LabelBatch labels_begin(svx_map* m, const svx_label_image* imgs, int n, bool on_device,
+                        const svx_semantic_cfg& cfg, uint64_t max_blocks_seen);
+void labels_enqueue(svx_map* m, LabelBatch& lb, int i0, int i1, uint32_t group_frame);
+void labels_finish(svx_map* m, const LabelBatch& lb, svx_frame_report* reps);
 uint64_t count_observed(svx_map* m);
 void launch_zero_blocks(svx_map* m, uint64_t first, uint64_t count);
 void rebuild_hash(svx_map* m);

@@ -27,6 +27,7 @@
 //                 flags the first such image; images from it on are not applied.
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 
 #include "svx_map.hpp"
 
@@ -37,7 +38,8 @@ namespace {
 constexpr int kThreads = 256;
 inline unsigned grid_for(uint64_t n) { return unsigned((n + kThreads - 1) / kThreads); }
 
-constexpr int kMaxImg = 8;  // label images fused in one pass
+constexpr int kMaxImg = kMaxLabelImages;  // label images fused in one pass
+constexpr int kSemOut = 3 * kMaxImg + 1;    // per pass: confidence-map flags, errors, updates; candidates
 
 // One label image (LabelImage, semantic_integrator.hpp:14-26) of a pass.
 struct ImgParams {
@@ -49,6 +51,7 @@ struct ImgParams {
     const float* conf;
     const float* tensor;
     int has_tensor, has_conf, conf_maybe;  // conf_maybe: may read a confidence outside [0, 1]
+    float reach;  // no voxel farther from the camera than this can pass 0 < z <= max_depth and the bounds
 };
 
 struct SemBatch {
@@ -59,6 +62,7 @@ struct SemBatch {
     int use_bayes, raycast, any_check;
     float floor_v, default_conf;
     uint32_t pass_id;  // 1-based index of this pass in the batch (confidence errors)
+    uint32_t group_frame;  // inside a TSDF frame group: the frame this pass follows, else ~0
 };
 
 __device__ inline d3 center_of(uint64_t key, int linear, double nu) {
@@ -71,16 +75,34 @@ __device__ inline d3 center_of(uint64_t key, int linear, double nu) {
 
 // Per block: bit i set when the block may hold a voxel image i can update.
 __global__ void __launch_bounds__(kThreads)
-k_sem_cull(const __grid_constant__ SemBatch sb, const uint64_t* __restrict__ block_keys, uint2* __restrict__ cand,
-           uint32_t* __restrict__ ctr) {
+k_sem_cull(const __grid_constant__ SemBatch sb, const uint64_t* __restrict__ block_keys,
+           const uint32_t* __restrict__ fm, uint2* __restrict__ cand, uint32_t* __restrict__ ctr) {
+    if (ctr[C_ABORT]) return;  // the frame group these images follow is rolled back
     const uint32_t nb = ctr[C_BLOCKS];
+    // inside a frame group, blocks its later frames allocated do not exist yet for this pass
+    // (their voxels are unobserved anyway): skipped without reading them
+    const uint32_t before = sb.group_frame == ~0u ? nb : ctr[C_BLOCKS_BEFORE];
+    const uint32_t seen = sb.group_frame == ~0u ? 0u : (2u << sb.group_frame) - 1u;
     for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nb; idx += gridDim.x * blockDim.x) {
+        if (idx >= before && !(fm[uint64_t(idx) * kMaskWords + kHdrRow * 16] & seen)) continue;
         const uint64_t key = block_keys[idx];
         int32_t bx, by, bz;
         unpack_key(key, bx, by, bz);
+        // block centre and half diagonal (of the voxel-centre box): a block farther than
+        // the image's reach (a passing voxel has 0 < z <= max_depth and |x / z|, |y / z|
+        // within the image, so distance <= max_depth sqrt(1 + ax^2 + ay^2)) cannot hold a
+        // voxel it updates: most of the map costs one distance test per image
+        const float bcx = float(sb.nu * (bx * 8 + 3.5)), bcy = float(sb.nu * (by * 8 + 3.5)),
+                    bcz = float(sb.nu * (bz * 8 + 3.5));
+        const float rad = float(sb.nu * 6.07) + 1e-3f;  // sqrt(3) * 3.5 voxels + slack
         uint32_t mask = 0;
         for (int i = 0; i < sb.n; ++i) {
             const ImgParams& ip = sb.img[i];
+            {
+                const float dx = bcx - float(ip.cam_o.x), dy = bcy - float(ip.cam_o.y), dz = bcz - float(ip.cam_o.z);
+                const float reach = ip.reach + rad;
+                if (dx * dx + dy * dy + dz * dz > reach * reach) continue;
+            }
             // half-space values at the 8 corners of the voxel-centre box
             bool out_zlo = true, out_zhi = true, out_ulo = true, out_uhi = true, out_vlo = true, out_vhi = true;
             const bool planes = ip.fx > 0.0 && ip.fy > 0.0;
@@ -305,6 +327,7 @@ k_sem_update(const __grid_constant__ SemBatch sb, HashView h, const uint64_t* __
     const int lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    if (ctr[C_ABORT]) return;  // the frame group these images follow is rolled back
     // a confidence error of an earlier pass of the batch: nothing more is applied
     const uint32_t err = ctr[C_ERR_CONF];
     if (err && err != sb.pass_id) return;
@@ -455,21 +478,24 @@ void launch_update(const SemBatch& sb, svx_map* m, const uint2* cand, int check,
 }  // namespace
 
 // A sequence of label images, applied in passes of up to kMaxImg images (one map sweep
-// per pass) with one synchronisation at the end: the result equals successive
-// integrate_labels calls (each voxel sees the images in order). Labels / confidences /
-// tensors are read from device memory when on_device, else copied from the host
-// (asynchronously; pinned memory overlaps).
-void run_integrate_labels_batch(svx_map* m, const svx_label_image* imgs, int n, bool on_device,
-                                const svx_semantic_cfg& cfg, svx_frame_report* reps) {
+// per pass): the result equals successive integrate_labels calls (each voxel sees the
+// images in order). Labels / confidences / tensors are read from device memory when
+// on_device, else copied from the host (asynchronously; pinned memory overlaps).
+// labels_begin stages the batch, labels_enqueue launches the passes of images [i0, i1)
+// on the map stream (no synchronisation: a TSDF frame group interleaves them with its
+// folds), labels_finish reads the per-image results after the stream synchronised.
+LabelBatch labels_begin(svx_map* m, const svx_label_image* imgs, int n, bool on_device,
+                        const svx_semantic_cfg& cfg, uint64_t max_blocks_seen) {
     const int K = m->cfg.num_labels;
-    for (int i = 0; i < n; ++i) {
-        reps[i].frame = -1;
-        reps[i].updated_voxels = reps[i].new_blocks = 0;
+    for (int i = 0; i < n; ++i)
         if (imgs[i].width <= 0 || imgs[i].height <= 0 || !imgs[i].labels)
             throw Error(SVX_INVALID_ARGUMENT, "label image is empty");
-    }
-    const bool bad_default = cfg.default_confidence < 0.f || cfg.default_confidence > 1.f;
-    if (n <= 0) return;
+    LabelBatch lb;
+    lb.imgs = imgs;
+    lb.n = n;
+    lb.on_device = on_device;
+    lb.cfg = cfg;
+    if (n <= 0) return lb;
     // staging for host images: every image of the batch gets its own slice
     uint64_t lbl_n = 0, conf_n = 0, ten_n = 0;
     for (int i = 0; i < n; ++i) {
@@ -482,22 +508,35 @@ void run_integrate_labels_batch(svx_map* m, const svx_label_image* imgs, int n, 
         m->lbl.alloc(lbl_n);
         if (conf_n) m->conf.alloc(conf_n);
         if (ten_n) m->tensor.alloc(ten_n);
+        lb.staged_lbl.assign(size_t(n), nullptr);
+        lb.staged_conf.assign(size_t(n), nullptr);
+        lb.staged_ten.assign(size_t(n), nullptr);
     }
-    const int passes = (n + kMaxImg - 1) / kMaxImg;
-    // per pass: confidence-map flags, error flags and updates per image, then candidates
-    constexpr int kOut = 3 * kMaxImg + 1;
-    m->sem_out.alloc(uint64_t(kOut) * passes);
-    SVX_CUDA(cudaMemsetAsync(m->sem_out.p, 0, 4ull * kOut * passes, m->stream));
-    m->cand.alloc(2 * std::max<uint64_t>(m->n_blocks, 1));  // uint2 per candidate block
-    // a block owns at most one layer: map as many layers as there are blocks, so the
+    // passes: at most one per image (ranges may split the batch anywhere), and a frame
+    // group that is rolled back and retried enqueues its images' passes again
+    lb.max_passes = 3 * n + 16;
+    m->sem_out.alloc(uint64_t(kSemOut) * lb.max_passes);
+    SVX_CUDA(cudaMemsetAsync(m->sem_out.p, 0, 4ull * kSemOut * lb.max_passes, m->stream));
+    m->cand.alloc(2 * std::max<uint64_t>(max_blocks_seen, 1));  // uint2 per candidate block
+    // a block owns at most one layer: map as many layers as there can be blocks, so the
     // update kernel never outgrows the pool and no mid-pass synchronisation is needed
-    ensure_layers(m, m->n_blocks);
+    ensure_layers(m, max_blocks_seen);
     SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_ERR_CONF, 0, 4, m->stream));
+    return lb;
+}
+
+void labels_enqueue(svx_map* m, LabelBatch& lb, int i0, int i1, uint32_t group_frame) {
+    const int K = m->cfg.num_labels;
+    const svx_semantic_cfg& cfg = lb.cfg;
+    const bool bad_default = cfg.default_confidence < 0.f || cfg.default_confidence > 1.f;
     uint2* cand = reinterpret_cast<uint2*>(m->cand.p);
-    uint64_t lo = 0, co = 0, to = 0;
-    for (int ps = 0; ps < passes; ++ps) {
-        const int i0 = ps * kMaxImg, ni = std::min(kMaxImg, n - i0);
-        uint32_t* out = m->sem_out.p + uint64_t(kOut) * ps;
+    for (int a = i0; a < i1; a += kMaxImg) {
+        if (lb.passes >= lb.max_passes) throw Error(SVX_DATA, "label passes: too many retries");
+        const int ps = lb.passes++;
+        const int ni = std::min(kMaxImg, i1 - a);
+        lb.pass_first.push_back(a);
+        lb.pass_count.push_back(ni);
+        uint32_t* out = m->sem_out.p + uint64_t(kSemOut) * ps;
         uint32_t *xconf = out, *xerr = out + kMaxImg, *xupd = out + 2 * kMaxImg;
         SemBatch sb{};
         sb.n = ni;
@@ -510,8 +549,9 @@ void run_integrate_labels_batch(svx_map* m, const svx_label_image* imgs, int n, 
         sb.floor_v = cfg.likelihood_floor;
         sb.default_conf = cfg.default_confidence;
         sb.pass_id = uint32_t(ps + 1);
+        sb.group_frame = group_frame;
         for (int k = 0; k < ni; ++k) {
-            const svx_label_image& img = imgs[i0 + k];
+            const svx_label_image& img = lb.imgs[a + k];
             const uint64_t P = uint64_t(img.width) * uint64_t(img.height);
             ImgParams& ip = sb.img[k];
             const Pose cp = to_pose(img.pose);
@@ -529,33 +569,45 @@ void run_integrate_labels_batch(svx_map* m, const svx_label_image* imgs, int n, 
             ip.labels = img.labels;
             ip.conf = img.confidence;
             ip.tensor = img.prob_tensor;
-            if (!on_device) {
-                SVX_CUDA(cudaMemcpyAsync(m->lbl.p + lo, img.labels, 2 * P, cudaMemcpyHostToDevice, m->stream));
-                ip.labels = m->lbl.p + lo;
-                lo += P;
-                if (ip.conf) {
-                    SVX_CUDA(cudaMemcpyAsync(m->conf.p + co, img.confidence, 4 * P, cudaMemcpyHostToDevice,
-                                             m->stream));
-                    ip.conf = m->conf.p + co;
-                    co += P;
+            if (!lb.on_device) {  // staged once (a retried frame group reuses the copy)
+                const size_t ii = size_t(a + k);
+                if (!lb.staged_lbl[ii]) {
+                    SVX_CUDA(cudaMemcpyAsync(m->lbl.p + lb.lo, img.labels, 2 * P, cudaMemcpyHostToDevice, m->stream));
+                    lb.staged_lbl[ii] = m->lbl.p + lb.lo;
+                    lb.lo += P;
+                    if (img.confidence) {
+                        SVX_CUDA(cudaMemcpyAsync(m->conf.p + lb.co, img.confidence, 4 * P, cudaMemcpyHostToDevice,
+                                                 m->stream));
+                        lb.staged_conf[ii] = m->conf.p + lb.co;
+                        lb.co += P;
+                    }
+                    if (img.prob_tensor) {
+                        SVX_CUDA(cudaMemcpyAsync(m->tensor.p + lb.to, img.prob_tensor, 4 * P * K,
+                                                 cudaMemcpyHostToDevice, m->stream));
+                        lb.staged_ten[ii] = m->tensor.p + lb.to;
+                        lb.to += P * K;
+                    }
                 }
-                if (ip.tensor) {
-                    SVX_CUDA(cudaMemcpyAsync(m->tensor.p + to, img.prob_tensor, 4 * P * K, cudaMemcpyHostToDevice,
-                                             m->stream));
-                    ip.tensor = m->tensor.p + to;
-                    to += P * K;
-                }
+                ip.labels = lb.staged_lbl[ii];
+                ip.conf = lb.staged_conf[ii];
+                ip.tensor = lb.staged_ten[ii];
+            }
+            if (img.fx > 0.0 && img.fy > 0.0 && img.max_depth < 1e30) {
+                const double ax = std::max(std::fabs(img.cx), std::fabs(img.width - img.cx)) / img.fx;
+                const double ay = std::max(std::fabs(img.cy), std::fabs(img.height - img.cy)) / img.fy;
+                ip.reach = float(img.max_depth * std::sqrt(1.0 + ax * ax + ay * ay) * (1.0 + 1e-5) + 1e-3);
+            } else {
+                ip.reach = 3e38f;  // no finite bound: the half-space tests decide
             }
             // confidence validity: only a voxel that passes every test reads one
             ip.conf_maybe = !ip.has_tensor && (ip.has_conf || bad_default);
             if (ip.conf_maybe) sb.any_check = 1;
         }
         SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_CAND, 0, 4, m->stream));
-        if (!m->n_blocks) continue;
         {
             ProfMark pm(m, SVX_K_SEM_CULL);
-            k_sem_cull<<<std::min<unsigned>(grid_for(m->n_blocks), persistent_grid(m->device)), kThreads, 0,
-                         m->stream>>>(sb, m->block_keys, cand, m->d_ctr);
+            k_sem_cull<<<persistent_grid(m->device), kThreads, 0, m->stream>>>(sb, m->block_keys, mask_base(m), cand,
+                                                                              m->d_ctr);
             count_launch();
         }
         SVX_CUDA(cudaMemcpyAsync(out + 3 * kMaxImg, m->d_ctr + C_CAND, 4, cudaMemcpyDeviceToDevice, m->stream));
@@ -588,23 +640,37 @@ void run_integrate_labels_batch(svx_map* m, const svx_label_image* imgs, int n, 
         }
         SVX_CUDA(cudaGetLastError());
     }
-    std::vector<uint32_t> outs(size_t(kOut) * passes);
-    SVX_CUDA(cudaMemcpyAsync(outs.data(), m->sem_out.p, 4ull * kOut * passes, cudaMemcpyDeviceToHost, m->stream));
-    sync_counters(m);
-    int fail = n;  // the first image that reads an invalid confidence
-    for (int i = 0; i < n && fail == n; ++i)
-        if (outs[size_t(kOut) * (i / kMaxImg) + kMaxImg + (i % kMaxImg)]) fail = i;
-    for (int i = 0; i < fail; ++i) {
-        const size_t ps = size_t(i / kMaxImg);
-        reps[i].frame = m->sem_frames++;
-        reps[i].updated_voxels = outs[kOut * ps + 2 * kMaxImg + (i % kMaxImg)];
-        m->prof_acc.sem_images += 1;
-        m->prof_acc.sem_updated += reps[i].updated_voxels;
+}
+
+// After the stream synchronised (sync_counters): reports of images [0, lb.n) in order.
+void labels_finish(svx_map* m, const LabelBatch& lb, svx_frame_report* reps) {
+    for (int i = 0; i < lb.n; ++i) {
+        reps[i].frame = -1;
+        reps[i].updated_voxels = reps[i].new_blocks = 0;
     }
-    for (int ps = 0; ps < passes; ++ps) m->prof_acc.sem_candidates += outs[size_t(kOut) * ps + 3 * kMaxImg];
+    std::vector<uint32_t> outs(size_t(kSemOut) * lb.passes);
+    if (lb.passes)
+        SVX_CUDA(cudaMemcpy(outs.data(), m->sem_out.p, 4ull * kSemOut * lb.passes, cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> upd(lb.n, 0), err(lb.n, 0);
+    for (int ps = 0; ps < lb.passes; ++ps) {
+        for (int k = 0; k < lb.pass_count[ps]; ++k) {
+            upd[lb.pass_first[ps] + k] = outs[size_t(kSemOut) * ps + 2 * kMaxImg + k];
+            err[lb.pass_first[ps] + k] = outs[size_t(kSemOut) * ps + kMaxImg + k];
+        }
+        m->prof_acc.sem_candidates += outs[size_t(kSemOut) * ps + 3 * kMaxImg];
+    }
+    int fail = lb.n;  // the first image that reads an invalid confidence
+    for (int i = 0; i < lb.n && fail == lb.n; ++i)
+        if (err[i]) fail = i;
+    for (int i = 0; i < fail; ++i) {
+        reps[i].frame = m->sem_frames++;
+        reps[i].updated_voxels = upd[i];
+        m->prof_acc.sem_images += 1;
+        m->prof_acc.sem_updated += upd[i];
+    }
     m->prof_acc.sem_new_layers += m->h_ctr[C_SEM] - m->n_layers;
     m->n_layers = m->h_ctr[C_SEM];
-    if (fail < n) {
+    if (fail < lb.n) {
         // images before the failing one are complete; the failing one is numbered (the
         // reference numbers a frame before it can throw, semantic_integrator.cpp:93-94)
         // and updated nothing; later images did not run
@@ -613,6 +679,19 @@ void run_integrate_labels_batch(svx_map* m, const svx_label_image* imgs, int n, 
         SVX_CUDA(cudaStreamSynchronize(m->stream));
         throw Error(SVX_INVALID_ARGUMENT, "confidence must be in [0, 1]");
     }
+}
+
+void run_integrate_labels_batch(svx_map* m, const svx_label_image* imgs, int n, bool on_device,
+                                const svx_semantic_cfg& cfg, svx_frame_report* reps) {
+    for (int i = 0; i < n; ++i) {
+        reps[i].frame = -1;
+        reps[i].updated_voxels = reps[i].new_blocks = 0;
+    }
+    if (n <= 0) return;
+    LabelBatch lb = labels_begin(m, imgs, n, on_device, cfg, m->n_blocks);
+    if (m->n_blocks) labels_enqueue(m, lb, 0, n, ~0u);
+    sync_counters(m);
+    labels_finish(m, lb, reps);
 }
 
 void run_integrate_labels(svx_map* m, const svx_label_image& img, const svx_semantic_cfg& cfg,

@@ -1308,10 +1308,12 @@ unsigned fold_grid(int device) {
     return unsigned(grid[device]);
 }
 
-void launch_fold_kernels(svx_map* m, svx_scan* s, const GroupParams& gp, FrameOut* outs);
+void launch_fold_kernels(svx_map* m, svx_scan* s, const GroupParams& gp, FrameOut* outs, LabelHook* labels,
+                         int first);
 
 // Enqueues the TSDF kernels of one group (the frames' images are in the scan's slots).
-void launch_group_kernels(svx_map* m, svx_scan* s, const GroupParams& gp, FrameOut* outs) {
+void launch_group_kernels(svx_map* m, svx_scan* s, const GroupParams& gp, FrameOut* outs, LabelHook* labels = nullptr,
+                          int first = 0) {
     const GroupConsts& c = gp.c;
     HashView hv = hash_view(m);
     const ScanSlots sc = scan_slots(s);
@@ -1324,11 +1326,13 @@ void launch_group_kernels(svx_map* m, svx_scan* s, const GroupParams& gp, FrameO
         count_launch();
     }
     if (c.exchange) return;  // the rest runs after the exchange (run_group_xend)
-    launch_fold_kernels(m, s, gp, outs);
+    launch_fold_kernels(m, s, gp, outs, labels, first);
 }
 
-// The group's kernels after the band (and, in exchange mode, after the ingest).
-void launch_fold_kernels(svx_map* m, svx_scan* s, const GroupParams& gp, FrameOut* outs) {
+// The group's kernels after the band (and, in exchange mode, after the ingest); with
+// `labels`, frame g's label images (frame first + g of the batch) follow its fold.
+void launch_fold_kernels(svx_map* m, svx_scan* s, const GroupParams& gp, FrameOut* outs, LabelHook* labels,
+                         int first) {
     const GroupConsts& c = gp.c;
     HashView hv = hash_view(m);
     const ScanSlots sc = scan_slots(s);
@@ -1342,13 +1346,18 @@ void launch_fold_kernels(svx_map* m, svx_scan* s, const GroupParams& gp, FrameOu
                    m->fbfill, m->bucket.p, m->bucket2.p, m->fbdesc.p, m->fctr, m->d_ctr);
         count_launch(2);
     }
-    {
-        ProfMark pm(m, SVX_K_FOLD);
-        for (uint32_t g = 0; g < c.G; ++g) {
+    for (uint32_t g = 0; g < c.G; ++g) {
+        {
+            ProfMark pm(m, SVX_K_FOLD);  // per launch: label passes may follow each fold
             launch_pdl(k_fold, fold_grid(m->device), kThreads, m->stream, c, gp.f[g], g, sc, m->vals, m->block_keys,
                        tsdf_base(m), fm, m->vlist.p, m->fbdesc.p, m->bucket.p, m->touched, m->dirty, m->fctr, outs,
                        m->d_ctr);
             count_launch();
+        }
+        if (labels) {  // frame first + g's label images, after its fold, before the next
+            const int f = first + int(g);
+            if (labels->img_off[f + 1] > labels->img_off[f])
+                labels_enqueue(m, *labels->lb, labels->img_off[f], labels->img_off[f + 1], g);
         }
     }
     SVX_CUDA(cudaGetLastError());
@@ -1496,7 +1505,8 @@ void grow_keep(DevBuf<T>& b, size_t count, size_t keep, cudaStream_t stream) {
 }
 }  // namespace
 
-void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cfg& cfg, svx_frame_report* reps) {
+void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cfg& cfg, svx_frame_report* reps,
+                LabelHook* labels) {
     if (!(cfg.alpha_epsilon > 0.0)) throw Error(SVX_INVALID_ARGUMENT, "alpha_epsilon must be > 0");
     if (n <= 0) return;
     svx_scan* s = jobs[0].scan;
@@ -1597,7 +1607,7 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
                 count_launch();
                 s->rowdist_fresh = true;
             }
-            launch_group_kernels(m, s, gp, m->outs.p + a);
+            launch_group_kernels(m, s, gp, m->outs.p + a, labels, a);
             a += G;
         }
         if (m->prof)
@@ -1825,7 +1835,7 @@ void run_group_xend(svx_map* m, const void* d_recv, const uint64_t* recv_meta, s
                    uint32_t(n_recv), m->vlist.p, m->d_ctr);
         count_launch();
     }
-    launch_fold_kernels(m, s, gp, m->outs.p);
+    launch_fold_kernels(m, s, gp, m->outs.p, nullptr, 0);
     SVX_CUDA(cudaMemcpyAsync(m->h_outs, m->outs.p, sizeof(FrameOut) * G, cudaMemcpyDeviceToHost, m->stream));
     sync_counters(m);
     if (m->h_ctr[C_ABORT]) throw Error(SVX_CUDA, "xend: fold aborted");

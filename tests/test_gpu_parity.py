@@ -352,3 +352,54 @@ def test_exchange_sharded_union_equals_unsharded(world):
     assert tsdf[order].tobytes() == tf.tobytes()
     for st in stores + [full]:
         st.close()
+
+
+@pytest.mark.parametrize("how", ["device", "host", "confidence"])
+def test_clouds_labels_batch_matches_per_frame(how):
+    """svx_integrate_clouds_labels (frame groups with each frame's label pass right after
+    its fold) == one integrate_cloud + one integrate_labels batch per frame: same TSDF and
+    label reports, same map bytes (cfg3 geometry, 6 cameras, 20 frames = two groups).
+    With confidence maps the batch alternates frame by frame."""
+    import torch
+    wl = W.make("cfg3", 20)
+    dev = torch.device("cuda", 0)
+    scans = [p for p, _ in wl.scans(device=dev)]
+    offs = np.zeros(len(scans) + 1, np.uint64)
+    offs[1:] = np.cumsum([s.shape[0] for s in scans])
+    pts = torch.cat(scans).contiguous()
+    poses = [wl.pose(i) for i in range(len(scans))]
+    frame_imgs = [wl.label_images(i, device=dev) for i in range(len(scans))]
+    if how == "confidence":
+        rng = np.random.default_rng(3)
+        for f in frame_imgs:
+            for li in f:
+                li.confidence = rng.uniform(0.2, 1.0, li.width * li.height).astype(np.float32)
+    cfg = svx.MapConfig(wl.voxel_size, wl.truncation, wl.num_labels, 1 << 20)
+    icfg, scfg = svx.IntegratorConfig(), svx.SemanticConfig()
+    ref = svx.VoxelStore(cfg, 0)
+    ti, si = svx.TsdfIntegrator(ref, icfg), svx.SemanticIntegrator(ref, scfg)
+    want_t, want_l = [], []
+    for i, s in enumerate(scans):
+        want_t.append(ti.integrate_cloud(s.cpu().numpy(), poses[i], wl.model))
+        want_l += si.integrate_labels_batch(frame_imgs[i])
+    st = svx.VoxelStore(cfg, 0)
+    if how == "device":
+        dimgs = [[svx.LabelImage(li.width, li.height,
+                                 torch.from_numpy(np.asarray(li.labels).view(np.int16).copy()).to(dev),
+                                 li.fx, li.fy, li.cx, li.cy, li.pose, max_depth=li.max_depth) for li in f]
+                 for f in frame_imgs]
+        torch.cuda.synchronize()
+        got_t, got_l = svx.integrate_clouds_labels(st, wl.model, pts.data_ptr(), offs, 3, poses, icfg, dimgs,
+                                                   scfg, points_on_device=True, labels_on_device=True)
+    else:
+        host = pts.cpu().pin_memory()
+        got_t, got_l = svx.integrate_clouds_labels(st, wl.model, host.data_ptr(), offs, 3, poses, icfg,
+                                                   frame_imgs, scfg, points_on_device=False)
+    assert [(r.frame, r.updated_voxels, r.new_blocks) for r in got_t] == \
+        [(r.frame, r.updated_voxels, r.new_blocks) for r in want_t]
+    assert [(r.frame, r.updated_voxels) for r in got_l] == [(r.frame, r.updated_voxels) for r in want_l]
+    assert sum(r.updated_voxels for r in got_l) > 100000
+    assert st.save_bytes() == ref.save_bytes()
+    assert np.array_equal(st.take_dirty_blocks(1), ref.take_dirty_blocks(1))
+    st.close()
+    ref.close()
