@@ -865,7 +865,7 @@ def run_sweep(args):
     rows = []
     for Wd in args.sweep_widths:
         n = args.sweep_scans
-        wl = W.make(f"cfg5-{Wd}", 2 * n + 8)
+        wl = W.make(f"cfg5-{Wd}", 3 * n + 8)
         wl.cams = [(W._forward_cam(0), np.zeros(3), 1280, 720, 640.0, 640.0, 640.0, 360.0)]
         chunks = [p for p, _ in wl.scans(device=dev)]
         offs = np.zeros(len(chunks) + 1, np.uint64)
@@ -878,40 +878,44 @@ def run_sweep(args):
                     for li in wl.label_images(i, device=dev)] for i in range(len(chunks))}
         for sem in (False, True):
             st = svx.VoxelStore(svx.MapConfig(wl.voxel_size, wl.truncation, wl.num_labels, 1 << 21), 0)
-            si = svx.SemanticIntegrator(st)
             ext = torch.cuda.ExternalStream(st.stream_ptr(), device=dev)
             icfg = svx.IntegratorConfig()
             # warm-up: the first 8 scans
             rel = offs[:9] - offs[0]
             st.integrate_clouds_device(wl.model, pts.data_ptr(), rel, 3, poses[:8], icfg)
             def one_pass(first):
-                """Scans first..first + n (frame groups; with semantics frame by frame, each
-                TSDF frame followed by its label image); device time of the pass."""
+                """Scans first..first + n in one call (frame groups; with semantics each TSDF
+                frame's label image right after its fold, svx_integrate_clouds_labels);
+                device time of the pass."""
                 torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(ext)
+                rel = offs[first:first + n + 1] - offs[first]
                 if sem:
-                    for i in range(first, first + n):
-                        st.integrate_clouds_device(wl.model, pts.data_ptr() + 12 * int(offs[i]),
-                                                   offs[i:i + 2] - offs[i], 3, [poses[i]], icfg)
-                        si.integrate_labels_batch(labs[i], on_device=True)
+                    svx.integrate_clouds_labels(st, wl.model, pts.data_ptr() + 12 * int(offs[first]), rel, 3,
+                                                poses[first:first + n], icfg,
+                                                [labs[i] for i in range(first, first + n)],
+                                                labels_on_device=True)
                 else:
-                    rel = offs[first:first + n + 1] - offs[first]
                     st.integrate_clouds_device(wl.model, pts.data_ptr() + 12 * int(offs[first]), rel, 3,
                                                poses[first:first + n], icfg)
                 e1.record(ext)
                 e1.synchronize()
                 return e0.elapsed_time(e1)
-            ms = one_pass(8)                      # timed: no profiling marks (PDL chains intact)
-            st.profile_enable(True)               # kernel breakdown: a second, profiled pass
-            one_pass(8 + n)
+            one_pass(8)                           # warm-up pass: buffers sized, pool mapped ahead
+            ms = one_pass(8 + n)                  # timed: no profiling marks (PDL chains intact)
+            st.profile_enable(True)               # kernel breakdown: a third, profiled pass
+            one_pass(8 + 2 * n)
             p = st.profile_read().as_dict()
-            npts = int(offs[8 + n] - offs[8])
-            B = 12.0 * npts + 16.0 * p["touched_blocks"] + 10240.0 * p["new_blocks"] + \
+            npts = int(offs[8 + 2 * n] - offs[8 + n])
+            # SURVEY 8(d) bytes of the profiled pass, scaled to the timed pass's points
+            npts_prof = int(offs[8 + 3 * n] - offs[8 + 2 * n])
+            B = 12.0 * npts_prof + 16.0 * p["touched_blocks"] + 10240.0 * p["new_blocks"] + \
                 40.0 * p["updated_voxels"]
             if sem:
                 B += 2.0 * 1280 * 720 * p["sem_images"] + 8.0 * 512 * p["sem_candidates"] + \
                     8.0 * 20 * p["sem_updated"]
+            B *= npts / max(npts_prof, 1)
             row = {"sweep": "cfg5", "W": Wd, "points_per_scan": npts / n, "semantics": sem, "scans": n,
                    "points_per_s": npts / (ms / 1e3), "ms_per_scan": ms / n,
                    "pipeline_frac": B / (ms / 1e3) / 1e9 / peak,

@@ -855,6 +855,9 @@ class SemanticIntegrator:
                                  img.fx, img.fy, img.cx, img.cy, pc, img.max_depth)
         return arr, keep
 
+    def take_dirty_blocks(self) -> np.ndarray:
+        return self.store.take_dirty_blocks(1)
+
 
 def integrate_clouds_labels(store: "VoxelStore", model: ProjectionModel, points_ptr: int, offsets,
                             stride: int, poses: list, icfg: "IntegratorConfig", frame_images: list,
@@ -880,9 +883,6 @@ def integrate_clouds_labels(store: "VoxelStore", model: ProjectionModel, points_
                                              C.cast(lreps, C.c_void_p)))
     del keep
     return [FrameReport.of(r) for r in reps], [FrameReport.of(lreps[i]) for i in range(len(imgs))]
-
-    def take_dirty_blocks(self) -> np.ndarray:
-        return self.store.take_dirty_blocks(1)
 
 
 # ------------------------------------------------------------------ mesh

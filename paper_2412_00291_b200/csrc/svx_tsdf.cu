@@ -259,6 +259,19 @@ __device__ __forceinline__ float f32_div(double x, double y) {
     return float(x / y);
 }
 
+// float(x) from an estimate q with |q - x| <= kQuotTol |q| (<= 36 ulps of q), decided with
+// one conversion: x and q round to the same float unless a rounding midpoint between two
+// floats lies within the error interval. Within q's binade those midpoints are exactly the
+// doubles whose 29 low mantissa bits equal 2^28 (the midpoint below a power of two included),
+// so q decides when its low bits are more than 64 ulps away from that pattern. Normal-range
+// results only (|q| in [1.2e-38, 1e38]), and q = 0 (an exact zero numerator).
+__device__ __forceinline__ bool f32_of_est(double q, float& f) {
+    const int32_t dist = int32_t(uint32_t(__double2loint(q)) & 0x1FFFFFFFu) - 0x10000000;
+    const double aq = fabs(q);
+    f = float(q);
+    return (q == 0.0) || (aq > 1.2e-38 && aq < 1e38 && (dist > 64 || dist < -64));
+}
+
 // nonprojective_distance (tsdf_integrator.cpp:39-46)
 __device__ inline double nonprojective_distance(double psi, double theta, double alpha, double eps) {
     double st, ct;
@@ -285,33 +298,59 @@ __device__ inline float truncate_f(double d, double tau) {
 // against cos(eps) with a 1e-12 margin (acos is strictly decreasing). Otherwise (ca near
 // cos(eps), sin(alpha) < 1e-6, or an interval straddling a float boundary: ~1e-4 of the
 // voxels) the reference formula is evaluated with CUDA's FP64 acos/sincos.
-__device__ inline float gamma_nonprojective(const GroupConsts& c, double psi, double ct, double ca) {
-    constexpr double kAbs = 2e-15, kRel = 2e-15;
-    bool fast = false;
-    double d = 0.0, e = 0.0;
+//
+// ct and ca may carry an input error: the fast path forms them from g * rsqrt(|g|^2) instead
+// of the reference's g / sqrt(|g|^2) (measure_term), within kDot of the reference's values.
+// That error enters the bound additively (cosines) and through sqrt(1 - x^2), whose change
+// is at most |x'^2 - x^2| / sqrt(1 - x'^2) <= 2.1 kDot / sqrt(1 - x'^2).
+// Returns false when undecided; the caller then evaluates the reference formula from the
+// reference's own ct, ca (gamma_reference).
+constexpr double kDot = 2e-15;
+__device__ __forceinline__ bool gamma_fast(const GroupConsts& c, double psi, double ct, double ca, float& out) {
+    constexpr double kAbs = 2e-15 + kDot, kRel = 4e-15;  // kRel: libm + our rsqrt-based roots
+    double d, e;
     if (ca > c.ca_hi) {  // alpha < eps: |cos theta| * psi
         d = fabs(ct) * psi;
         e = fabs(psi) * (kAbs + kRel * fabs(ct)) + 1e-15 * fabs(d);
-        fast = true;
     } else if (ca < c.ca_lo) {
-        const double st = sqrt((1.0 - ct) * (1.0 + ct));
-        const double sa = sqrt((1.0 - ca) * (1.0 + ca));
-        if (sa > 1e-6) {
-            const double a = ca - 1.0;
-            const double inv_sa = rcp_est(sa);  // (a st / sa within ~4 ulp: in the 2e-15 term)
-            const double t1 = fabs(a * st * inv_sa), t2 = fabs(ct * psi);
-            const double mag = t1 + t2;
-            d = psi >= 0.0 ? mag : -mag;
-            const double da = kAbs + kRel * fabs(a), dst = kAbs + kRel * st, dsa = kAbs + kRel * sa;
-            e = 1.01 * ((fabs(a) * dst + st * da + t1 * dsa) * inv_sa + fabs(psi) * (kAbs + kRel * fabs(ct))) +
-                2e-15 * mag;
-            fast = true;
-        }
+        const double tt = (1.0 - ct) * (1.0 + ct), ss = (1.0 - ca) * (1.0 + ca);
+        if (!(tt > 1e-14 && ss > 1e-12)) return false;  // sin theta < 1e-7 or sin alpha < 1e-6
+        const double rt = rsqrt(tt), inv_sa = rsqrt(ss);  // (<= 1 ulp each)
+        const double st = tt * rt, sa = ss * inv_sa;
+        const double a = ca - 1.0;
+        const double t1 = fabs(a * st * inv_sa), t2 = fabs(ct * psi);
+        const double mag = t1 + t2;
+        d = psi >= 0.0 ? mag : -mag;
+        const double da = kAbs + kRel * fabs(a);
+        const double dst = kAbs + kRel * st + 2.1 * kDot * rt;
+        const double dsa = kAbs + kRel * sa + 2.1 * kDot * inv_sa;
+        e = 1.01 * ((fabs(a) * dst + st * da + t1 * dsa) * inv_sa + fabs(psi) * (kAbs + kRel * fabs(ct))) +
+            4e-15 * mag;
+    } else {
+        return false;
     }
-    if (fast) {
-        const float lo = truncate_f(d - e, c.tau), hi = truncate_f(d + e, c.tau);
-        if (lo == hi && __float_as_uint(lo) == __float_as_uint(hi)) return lo;
+    // float(clamp(x, +-tau)) is monotonic in x: [d - e, d + e] decides it when both ends agree
+    const double lo = d - e, hi = d + e;
+    if (lo > -c.tau && hi < c.tau) {
+        const float flo = float(lo), fhi = float(hi);
+        if (__float_as_uint(flo) != __float_as_uint(fhi)) return false;
+        out = flo;
+        return true;
     }
+    const float flo = truncate_f(lo, c.tau), fhi = truncate_f(hi, c.tau);
+    if (!(flo == fhi && __float_as_uint(flo) == __float_as_uint(fhi))) return false;
+    out = flo;
+    return true;
+}
+
+// The reference's own evaluation (the undecided cases).
+__device__ inline float gamma_reference(const GroupConsts& c, double psi, d3 ray, d3 g, const float nw[3]) {
+    const double gz = dot3(g, g);
+    if (gz > 0.0) g = div3(g, sqrt(gz));
+    double ct = dot3(neg3(ray), g);
+    ct = ct < -1.0 ? -1.0 : (1.0 < ct ? 1.0 : ct);
+    double ca = dot3(g, mk(nw[0], nw[1], nw[2]));
+    ca = ca < -1.0 ? -1.0 : (1.0 < ca ? 1.0 : ca);
     return truncate_f(nonprojective_distance(psi, acos(ct), acos(ca), c.alpha_eps), c.tau);
 }
 
@@ -339,14 +378,16 @@ __device__ inline Term measure_term(const GroupConsts& c, d3 origin, const PixCa
             g[1] = vox.gradient[1];
             g[2] = vox.gradient[2];
         }
-        d3 gd = mk(g[0], g[1], g[2]);
-        const double gz = dot3(gd, gd);
-        if (gz > 0.0) gd = div3(gd, sqrt(gz));
+        // g.normalized() (g / sqrt(|g|^2)) as g * rsqrt(|g|^2): each component within 3 ulp,
+        // so ct and ca within kDot of the reference's (|ray| = 1, |nw| = 1 + O(1e-7))
+        const d3 g0 = mk(g[0], g[1], g[2]);
+        const double gz = dot3(g0, g0);
+        const d3 gd = gz > 0.0 ? scale3(rsqrt(gz), g0) : g0;
         double ct = dot3(neg3(ray), gd);
         ct = ct < -1.0 ? -1.0 : (1.0 < ct ? 1.0 : ct);
         double ca = dot3(gd, mk(nw[0], nw[1], nw[2]));
         ca = ca < -1.0 ? -1.0 : (1.0 < ca ? 1.0 : ca);
-        gamma = gamma_nonprojective(c, psi, ct, ca);
+        if (!gamma_fast(c, psi, ct, ca, gamma)) gamma = gamma_reference(c, psi, ray, g0, nw);
     } else {
         gamma = truncate_f(psi, c.tau);
     }
@@ -458,6 +499,106 @@ __device__ inline int rec_lin(unsigned long long r) { return int(uint32_t(r >> 3
 // kFallback and is left alone: a fallback descriptor (k_fb_sort) applies it. Returns 1 when
 // the voxel was updated.
 constexpr uint32_t kFallback = 0xFFFFFFFFu;
+
+// The own-pixel measurement and fold of one voxel through the generic code (each quotient
+// decided separately, exact divisions where undecided): the rare voxels fold_own_fast
+// cannot decide.
+__device__ __noinline__ uint32_t fold_own_exact(const GroupConsts& c, d3 origin, const PixCache* __restrict__ cache,
+                                                uint32_t own, d3 center, svx_tsdf_voxel* vp) {
+    svx_tsdf_voxel vox = load_voxel(vp);
+    const Term t = measure_term(c, origin, cache, own, center, vox);
+    if (!(t.flags & 1u)) return 0;
+    Accum acc{0.0, 0.0, 0.0, 0.0, 0.0};
+    accumulate(acc, t);
+    fold(vox, acc);
+    store_voxel(vp, vox);
+    return 1;
+}
+
+// Own-pixel measurement + fold (one term: tsdf_integrator.cpp:172-205,232-247) as ONE
+// branch-free decision chain: every f32 result (Gamma, weight, D, gradient) comes from an
+// estimate with an error bound, and the chain reports whether all of them were decided.
+// Only an undecided voxel takes the generic path (fold_own_exact), so the common case pays
+// one reconvergence point instead of one per quotient.
+__device__ __forceinline__ uint32_t fold_own_fast(const GroupConsts& c, d3 origin, const PixCache* __restrict__ cache,
+                                                  uint32_t own, d3 center, svx_tsdf_voxel* vp, svx_tsdf_voxel vox) {
+    const PixCache& pc = cache[own];
+    const uint32_t flags = pc.flags;
+    if (!(flags & 1u)) return 0;
+    const bool have_normal = flags & 2u;
+    const d3 ray = mk(pc.ray[0], pc.ray[1], pc.ray[2]);
+    const double psi = pc.range - dot3(sub3(center, origin), ray);
+    if (fabs(psi) > c.tau) return 0;
+    const float nw0 = pc.n[0], nw1 = pc.n[1], nw2 = pc.n[2];
+    bool ok = true;
+    float gamma;
+    if (c.nonproj && have_normal) {
+        const float gsq =
+            (vox.gradient[0] * vox.gradient[0] + vox.gradient[1] * vox.gradient[1]) + vox.gradient[2] * vox.gradient[2];
+        const bool use_g = vox.weight > 0.f && gsq > 1e-12f;
+        const d3 g0 = mk(use_g ? vox.gradient[0] : nw0, use_g ? vox.gradient[1] : nw1, use_g ? vox.gradient[2] : nw2);
+        const double gz = dot3(g0, g0);
+        const d3 gd = gz > 0.0 ? scale3(rsqrt(gz), g0) : g0;  // within kDot (gamma_fast)
+        double ct = dot3(neg3(ray), gd);
+        ct = fmin(fmax(ct, -1.0), 1.0);
+        double ca = dot3(gd, mk(nw0, nw1, nw2));
+        ca = fmin(fmax(ca, -1.0), 1.0);
+        ok = gamma_fast(c, psi, ct, ca, gamma);
+    } else {
+        gamma = truncate_f(psi, c.tau);
+    }
+    // observation_weight: float(clamp((psi + tau) / 2 tau, min_clamp, 1))
+    float w_obs;
+    {
+        const double lo = double(c.min_clamp);
+        const double q = (psi + c.tau) * c.inv_2tau, dq = fabs(q) * kQuotTol;
+        bool wok;
+        if (q + dq < lo) {
+            w_obs = c.min_clamp;
+            wok = true;
+        } else if (q - dq > 1.0) {
+            w_obs = 1.f;
+            wok = true;
+        } else {
+            wok = q - dq > lo && q + dq < 1.0 && f32_of_est(q, w_obs);
+        }
+        ok = ok && wok;
+    }
+    // the term and the accumulate-then-merge fold, in the reference's operation order
+    const double wd = 0.0 + double(w_obs * gamma), w = 0.0 + double(w_obs);
+    const double wx = have_normal ? 0.0 + double(w_obs * nw0) : 0.0;
+    const double wy = have_normal ? 0.0 + double(w_obs * nw1) : 0.0;
+    const double wz = have_normal ? 0.0 + double(w_obs * nw2) : 0.0;
+    const double w_old = double(vox.weight);
+    svx_tsdf_voxel out;
+    {
+        const double num = w_old * double(vox.distance) + wd, den = w_old + w;
+        ok = ok && den > 1e-300 && den < 1e300 && f32_of_est(num * rcp_est(den), out.distance);
+        out.weight = float(den);
+    }
+    const double bx = w_old * double(vox.gradient[0]) + wx, by = w_old * double(vox.gradient[1]) + wy,
+                 bz = w_old * double(vox.gradient[2]) + wz;
+    const double s2 = (bx * bx + by * by) + bz * bz;
+    // norm > 1e-12 decided on s2 away from 1e-24 (else undecided); float(b_i / norm) from
+    // b_i * rsqrt(s2) when that decides the float
+    const bool upd = s2 > 1.0000001e-24;
+    ok = ok && (upd || s2 < 0.9999999e-24) && s2 < 1e300;
+    if (upd) {
+        const double r = rsqrt(s2);
+        const bool g0 = f32_of_est(bx * r, out.gradient[0]);
+        const bool g1 = f32_of_est(by * r, out.gradient[1]);
+        const bool g2 = f32_of_est(bz * r, out.gradient[2]);
+        ok = ok && g0 && g1 && g2;
+    } else {
+        out.gradient[0] = vox.gradient[0];
+        out.gradient[1] = vox.gradient[1];
+        out.gradient[2] = vox.gradient[2];
+    }
+    if (!ok) return fold_own_exact(c, origin, cache, own, center, vp);
+    store_voxel(vp, out);
+    return 1;
+}
+
 template <bool kRec>
 __device__ __forceinline__ uint32_t fold_one(const GroupConsts& c, const FramePose& f, uint32_t g, svx_tsdf_voxel* vp, d3 center,
                              const ScanSlots& sc, const unsigned long long* __restrict__ recs, uint32_t nrec) {
@@ -468,11 +609,7 @@ __device__ __forceinline__ uint32_t fold_one(const GroupConsts& c, const FramePo
     if constexpr (!kRec) {
         const uint32_t own = own_pixel(c.m, xform(f.w2s, center));
         if (own == kInvalid || !pixel_has_return(sc.validbits + uint64_t(g) * c.VW, own)) return kFallback;
-        const Term t = measure_term(c, f.origin, cache, own, center, vox);
-        if (t.flags & 1u) {
-            accumulate(acc, t);
-            measured = true;
-        }
+        return fold_own_fast(c, f.origin, cache, own, center, vp, vox);
     } else {
         for (uint32_t j = 0; j < nrec; ++j) {
             const Term t = measure_term(c, f.origin, cache, rec_pixel(recs[j]), center, vox);
@@ -635,7 +772,8 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
     __shared__ uint32_t lfb[kTileFb];
     __shared__ uint32_t lcnt[kLocalKeys];  // fallback records per local block
     __shared__ uint32_t lnew[kLocalKeys];  // pool indices of blocks this tile created
-    __shared__ uint32_t nfb, nnew;
+    __shared__ uint8_t s_occ[kLocalKeys];
+    __shared__ uint32_t nfb, nnew, nocc;
     const int tid = threadIdx.x;
     const uint32_t g = blockIdx.x / c.tiles;
     const uint32_t tile = blockIdx.x - g * c.tiles;
@@ -648,7 +786,7 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
     lcnt[tid] = 0u;
 #pragma unroll
     for (int w = 0; w < 16; ++w) lmask[tid][w] = 0u;
-    if (tid == 0) nfb = nnew = 0;
+    if (tid == 0) nfb = nnew = nocc = 0;
     __syncthreads();
 
     const uint64_t pg = uint64_t(g) * c.P;
@@ -709,23 +847,30 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
         float p0x = 0.f, p0y = 0.f, p0z = 0.f;
         bool first = true;
         const bool all_own = band_all_own(c, hd, p, r);
+        int32_t cbx = INT32_MIN, cby = 0, cbz = 0;  // block of the previous visit
         traverse_segment<true>(a, b, c.nu, c.inv_nu, [&](int32_t x, int32_t y, int32_t z) {
             const int32_t bx = block_coord(x), by = block_coord(y), bz = block_coord(z);
-            if (!key_in_range(bx) || !key_in_range(by) || !key_in_range(bz)) {
-                atomicOr(&ctr[C_ABORT], kAbortKey);
-                return;
-            }
-            const uint64_t key = pack_key(bx, by, bz);
-            if (key != cur_key) {
+            if (bx != cbx || by != cby || bz != cbz) {  // block change: key, range, local slot
+                cbx = bx;
+                cby = by;
+                cbz = bz;
+                cur_li = -1;
+                if (!key_in_range(bx) || !key_in_range(by) || !key_in_range(bz)) {
+                    atomicOr(&ctr[C_ABORT], kAbortKey);  // (the group is rolled back)
+                    cur_own = false;
+                    return;
+                }
+                const uint64_t key = pack_key(bx, by, bz);
                 cur_key = key;
                 // key sharding without exchange: this rank's blocks only (its band is redundant);
                 // with exchange: every block is staged, the epilogue routes the remote ones
                 cur_own = c.exchange || !(c.shard_world > 1 && owner_of(key, c.shard_world) != c.shard_rank);
-                cur_li = -1;
                 if (cur_own) {  // local table insert (open addressing in smem)
                     uint32_t s = hash_slot(key, 8);
                     for (int probe = 0; probe < kLocalKeys; ++probe) {
-                        const unsigned long long old = atomicCAS(&lkey[s], kEmptyKey, key);
+                        // plain load first: most blocks are already in the table (neighbour rays)
+                        unsigned long long old = lkey[s];
+                        if (old == kEmptyKey) old = atomicCAS(&lkey[s], kEmptyKey, key);
                         if (old == kEmptyKey || old == key) {
                             cur_li = int(s);
                             break;
@@ -758,7 +903,7 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
                 fb = own == kInvalid || !pixel_has_return(validbits, own);
             }
             if (cur_li < 0) {  // local table full: straight to global state
-                visit_global(c, g, h, block_keys, stamp, touched, fm, fbcnt, rec, pool, vlist, fctr, xsend, xcnt, ctr, key,
+                visit_global(c, g, h, block_keys, stamp, touched, fm, fbcnt, rec, pool, vlist, fctr, xsend, xcnt, ctr, cur_key,
                              lin, fb, p);
                 return;
             }
@@ -775,7 +920,7 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
                     lfb[pos] = (uint32_t(cur_li) << 24) | (uint32_t(lin) << 15) | uint32_t(tid);
                 else
                     visit_global(c, g, h, block_keys, stamp, touched, fm, fbcnt, rec, pool, vlist, fctr, xsend,
-                                 xcnt, ctr, key, lin, true, p);
+                                 xcnt, ctr, cur_key, lin, true, p);
             }
         });
         if (pend_word >= 0) atomicOr(&lmask[0][0] + pend_word, pend_bits);
@@ -799,11 +944,14 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
     }
     lslot[tid] = slot;
     lidx[tid] = idx;
-    const uint32_t tpos = cta_append<kW>(first_touch, &ctr[C_TOUCHED], s_w);
+    // occupied local slots (the epilogue's loops run over their 16 mask words only)
+    if (lkey[tid] != kEmptyKey) s_occ[atomicAdd(&nocc, 1u)] = uint8_t(tid);
+    const uint32_t tpos = cta_append<kW>(first_touch, &ctr[C_TOUCHED], s_w);  // (barriers)
     if (first_touch) touched[tpos] = slot;
     // zero-fill the blocks this tile created (read from the fold on)
     for (uint32_t j = 0; j < nnew; ++j) zero_block(pool, lnew[j], tid, kTileU * kTileV);
     const uint32_t nf = min(nfb, uint32_t(kTileFb));
+    const uint32_t nwords = nocc * 16u;
     // exchange mode: the tile's entries for other ranks are counted per destination in
     // shared memory and reserved with one global atomic per (tile, destination)
     __shared__ uint32_t s_xn[kMaxXWorld], s_xb[kMaxXWorld], s_xbase[kMaxXWorld];
@@ -816,8 +964,8 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
             const uint32_t li = lfb[i] >> 24;
             if (lown[li] != c.shard_rank) atomicAdd(&s_xn[lown[li]], 1u);
         }
-        for (int i = tid; i < kLocalKeys * 16; i += kTileU * kTileV) {
-            const int li = i >> 4;
+        for (uint32_t i = tid; i < nwords; i += kTileU * kTileV) {
+            const int li = s_occ[i >> 4];
             const uint32_t bits = lmask[li][i & 15];
             if (bits && lown[li] != c.shard_rank) {
                 atomicAdd(&s_xn[lown[li]], 1u);
@@ -861,8 +1009,8 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
     // voxel masks -> the frame's row of each block; the bits a tile sets first (the atomic
     // returns them clear) are those voxels' single entries in the frame's voxel list
     uint32_t nv = 0;
-    for (int i = tid; i < kLocalKeys * 16; i += kTileU * kTileV) {
-        const int li = i >> 4, w = i & 15;
+    for (uint32_t i = tid; i < nwords; i += kTileU * kTileV) {
+        const int li = s_occ[i >> 4], w = i & 15;
         uint32_t bits = lmask[li][w];
         if (bits && lidx[li] != kInvalid) {
             bits &= ~atomicOr(&fm[uint64_t(lidx[li]) * kMaskWords + g * 16 + w], bits);
@@ -875,12 +1023,45 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
     }
     uint32_t pos = cta_reserve<kW>(nv, &fctr[g * kFC + FC_VOX], s_w);
     if (nv && pos + nv > c.vox_cap) atomicOr(&ctr[C_ABORT], kAbortVox);
+    // the list entries, written warp-cooperatively: per 32 words (one per lane), entry j of
+    // the warp goes to the lane whose bit range holds j (binary search over the inclusive
+    // popcount scan) and takes that lane's (j - excl)-th set bit; each lane's entries land
+    // at its own running position, as a per-lane loop over its bits would place them
     uint32_t* vl = vlist + uint64_t(g) * c.vox_cap;
-    for (int i = tid; i < kLocalKeys * 16 && nv; i += kTileU * kTileV) {
-        const int li = i >> 4, w = i & 15;
-        const uint32_t hi = lidx[li] << 9;
-        for (uint32_t bits = lmask[li][w]; bits; bits &= bits - 1, ++pos)
-            if (pos < c.vox_cap) vl[pos] = hi | (uint32_t(w) * 32u + uint32_t(__ffs(bits) - 1));
+    const int lane = tid & 31;
+    for (uint32_t base = uint32_t(tid & ~31); base < nwords; base += kTileU * kTileV) {  // warp-uniform
+        const uint32_t i = base + uint32_t(lane);
+        uint32_t bits = 0u, hi = 0u;
+        if (i < nwords) {
+            const int li = s_occ[i >> 4], w = int(i & 15u);
+            bits = lmask[li][w];
+            hi = (lidx[li] << 9) | (uint32_t(w) * 32u);
+        }
+        const uint32_t n = uint32_t(__popc(bits));
+        uint32_t incl = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        const uint32_t start = pos - (incl - n);  // this lane's entry k goes to start + excl + k
+        pos += n;
+        for (uint32_t jb = 0; jb < total; jb += 32u) {
+            const uint32_t j = jb + uint32_t(lane);
+            int l = 0;
+#pragma unroll
+            for (int s = 16; s; s >>= 1)
+                if (__shfl_sync(0xFFFFFFFFu, incl, l + s - 1) <= j) l += s;
+            const uint32_t bl = __shfl_sync(0xFFFFFFFFu, bits, l);
+            const uint32_t hl = __shfl_sync(0xFFFFFFFFu, hi, l);
+            const uint32_t sl = __shfl_sync(0xFFFFFFFFu, start, l);
+            const uint32_t el = __shfl_sync(0xFFFFFFFFu, incl, l) - uint32_t(__popc(bl));
+            if (j < total) {
+                const uint32_t at = sl + j;
+                if (at < c.vox_cap) vl[at] = hl | select_bit(bl, j - el);
+            }
+        }
     }
     __syncthreads();  // lcnt complete
     if (lcnt[tid]) atomicAdd(&fbcnt[lslot[tid]], lcnt[tid]);
@@ -1021,8 +1202,11 @@ k_fb_sort(const uint32_t G, HashView h, const uint32_t* __restrict__ fbslots, ui
 // consecutive integrate_frame calls. The last frame's launch ends the group: dirty flags,
 // per-frame touched / new block counts and the mask rows over the touched list; its last
 // CTA writes the frames' reports.
-__global__ void __launch_bounds__(kThreads, 4)
-k_fold(const GroupConsts c, const FramePose f, const uint32_t g, const ScanSlots sc,
+#ifndef SVX_FOLD_MINB
+#define SVX_FOLD_MINB 4
+#endif
+__global__ void __launch_bounds__(kThreads, SVX_FOLD_MINB)
+k_fold(const __grid_constant__ GroupConsts c, const __grid_constant__ FramePose f, const uint32_t g, const ScanSlots sc,
        const uint32_t* __restrict__ vals, const uint64_t* __restrict__ block_keys, svx_tsdf_voxel* __restrict__ pool,
        uint32_t* __restrict__ fm, const uint32_t* __restrict__ vlist, const uint4* __restrict__ fbdesc,
        const unsigned long long* __restrict__ bucket, const uint32_t* __restrict__ touched,
@@ -1048,21 +1232,23 @@ k_fold(const GroupConsts c, const FramePose f, const uint32_t g, const ScanSlots
         n_upd += fold_one<true>(c, f, g, pool + uint64_t(d.x) * kBlockVoxels + lin,
                                 center_of(block_keys[d.x], lin, c.nu), sc, bucket + d.z, d.w);
     }
-    // the visited voxels, 32 per warp from a queue (threads that took a long fallback
-    // chain take fewer of them)
-    for (;;) {
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(&fc[FC_VQ], 32u);
-        base = __shfl_sync(0xFFFFFFFFu, base, 0);
-        if (base >= nv) break;
+    // the visited voxels, 32 per warp: each warp's first chunk is its own (no atomic), the
+    // rest come from a queue (threads that took a long fallback chain take fewer of them;
+    // the queue atomics are spread over the kernel instead of all arriving at its start)
+    const uint32_t nwarps = gridDim.x * (blockDim.x / 32u);
+    uint32_t base = (blockIdx.x * (blockDim.x / 32u) + (threadIdx.x >> 5)) * 32u;
+    while (base < nv) {
         const uint32_t i = base + uint32_t(lane);
-        if (i >= nv) continue;
-        const uint32_t e = vl[i];
-        const uint32_t idx = e >> 9;
-        const int lin = int(e & 511u);
-        const uint32_t u = fold_one<false>(c, f, g, pool + uint64_t(idx) * kBlockVoxels + lin,
-                                           center_of(block_keys[idx], lin, c.nu), sc, nullptr, 0);
-        n_upd += u == 1u ? 1u : 0u;  // kFallback: a fallback descriptor applies it
+        if (i < nv) {
+            const uint32_t e = vl[i];
+            const uint32_t idx = e >> 9;
+            const int lin = int(e & 511u);
+            const uint32_t u = fold_one<false>(c, f, g, pool + uint64_t(idx) * kBlockVoxels + lin,
+                                               center_of(block_keys[idx], lin, c.nu), sc, nullptr, 0);
+            n_upd += u == 1u ? 1u : 0u;  // kFallback: a fallback descriptor applies it
+        }
+        if (lane == 0) base = nwarps * 32u + atomicAdd(&fc[FC_VQ], 32u);
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
     }
     for (int o = 16; o; o >>= 1) n_upd += __shfl_xor_sync(0xFFFFFFFFu, n_upd, o);
     if (lane == 0 && n_upd) atomicAdd(&fc[FC_UPD], n_upd);

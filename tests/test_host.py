@@ -151,3 +151,13 @@ def test_exchange_all_to_all_gloo():
             want = np.concatenate([s[s[:, 3] == d] for s in sent]) if sent else np.zeros((0, 4), np.uint32)
             assert np.array_equal(got, want), (world, d)
             assert np.all(got[:, 3] == d)
+
+
+def test_integrators_mirror_the_reference_methods():
+    # both integrators expose the reference's take_dirty_blocks (tsdf_integrator.hpp:84,
+    # semantic_integrator.hpp:59) plus their integrate entry points
+    for cls, names in ((svx.TsdfIntegrator, ("integrate_frame", "take_dirty_blocks")),
+                       (svx.SemanticIntegrator, ("integrate_labels", "integrate_labels_batch",
+                                                 "take_dirty_blocks"))):
+        for n in names:
+            assert callable(getattr(cls, n, None)), (cls.__name__, n)
