@@ -97,15 +97,14 @@ void free_map(svx_map* m) {
     if (m->stream) cudaStreamSynchronize(m->stream);
     for (void* p : {(void*)m->keys, (void*)m->vals, (void*)m->block_keys, (void*)m->sem_idx,
                     (void*)m->dirty, (void*)m->stamp, (void*)m->touched, (void*)m->fctr,
-                    (void*)m->d_ctr, (void*)m->fbcnt, (void*)m->fbstart, (void*)m->fbfill,
-                    (void*)m->fbslots, (void*)m->fbclaim})
+                    (void*)m->d_ctr})
         if (p) cudaFree(p);
     if (m->h_ctr) cudaFreeHost(m->h_ctr);
     if (m->h_fctr) cudaFreeHost(m->h_fctr);
     if (m->h_outs) cudaFreeHost(m->h_outs);
     m->outs.release();
     m->bucket.release();
-    m->bucket2.release();
+    m->fb_tmp.release();
     m->fbdesc.release();
     m->xsend.release();
     m->xpack.release();
@@ -153,7 +152,7 @@ svx_map* create_map(const svx_map_cfg& cfg, int device) {
         uint64_t want = std::max<uint64_t>(2ull * cfg.max_blocks, 1024);
         m->log2cap = 0;
         while ((1ull << m->log2cap) < want) ++m->log2cap;
-        // a fallback record holds a slot in 23 bits (svx_tsdf.cu): max_blocks <= 2^22
+        // a fallback record holds a pool index in 22 bits (svx_tsdf.cu): max_blocks <= 2^22
         require(m->log2cap <= 23, SVX_INVALID_ARGUMENT, "max_blocks too large for the device hash (<= 2^22)");
         m->cap = uint32_t(1u << m->log2cap);
         m->keys = dmalloc<uint64_t>(m->cap);
@@ -165,19 +164,13 @@ svx_map* create_map(const svx_map_cfg& cfg, int device) {
         m->sem_idx = dmalloc<uint32_t>(cfg.max_blocks);
         m->dirty = dmalloc<uint8_t>(2ull * cfg.max_blocks);
         m->d_ctr = dmalloc<uint32_t>(kNumCounters);
-        m->fbcnt = dmalloc<uint32_t>(m->cap);
-        m->fbstart = dmalloc<uint32_t>(m->cap);
-        m->fbfill = dmalloc<uint32_t>(m->cap);
-        m->fbclaim = dmalloc<uint32_t>(m->cap);
-        m->fbslots = dmalloc<uint32_t>(m->cap);
-        m->rec_cap = 1u << 20;
+        // fallback records per group: sized by use (grown on overflow, the group retried);
+        // the per-group sort covers the whole buffer
+        uint32_t rec_cap = 1u << 18;
         // test hook: tiny buffers exercise the abort-and-resume paths
-        if (const char* e = std::getenv("SVX_TEST_REC_CAP")) m->rec_cap = uint32_t(std::max(1L, std::atol(e)));
+        if (const char* e = std::getenv("SVX_TEST_REC_CAP")) rec_cap = uint32_t(std::max(1L, std::atol(e)));
         if (const char* e = std::getenv("SVX_TEST_POOL_HEAD")) m->test_pool_head = uint64_t(std::max(1L, std::atol(e)));
-        m->records.alloc(m->rec_cap);
-        m->bucket.alloc(m->rec_cap);
-        m->bucket2.alloc(m->rec_cap);
-        m->fbdesc.alloc(m->rec_cap);
+        set_rec_cap(m, rec_cap);
         SVX_CUDA(cudaMallocHost(&m->h_ctr, sizeof(uint32_t) * kNumCounters));
         SVX_CUDA(cudaMallocHost(&m->h_fctr, sizeof(uint32_t) * kMaxG * kFC));
         std::memset(m->h_ctr, 0, sizeof(uint32_t) * kNumCounters);
@@ -185,10 +178,6 @@ svx_map* create_map(const svx_map_cfg& cfg, int device) {
         SVX_CUDA(cudaMemsetAsync(m->vals, 0xFF, 4ull * m->cap, m->stream));  // kInvalid: no block yet
         SVX_CUDA(cudaMemsetAsync(m->stamp, 0, 4ull * m->cap, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->fctr, 0, 4ull * kMaxG * kFC, m->stream));
-        SVX_CUDA(cudaMemsetAsync(m->fbcnt, 0, 4ull * m->cap, m->stream));
-        SVX_CUDA(cudaMemsetAsync(m->fbfill, 0, 4ull * m->cap, m->stream));
-        SVX_CUDA(cudaMemsetAsync(m->fbclaim, 0, 4ull * m->cap, m->stream));
-        SVX_CUDA(cudaMemsetAsync(m->fbstart, 0xFF, 4ull * m->cap, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->sem_idx, 0xFF, 4ull * cfg.max_blocks, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->dirty, 0, 2ull * cfg.max_blocks, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->d_ctr, 0, sizeof(uint32_t) * kNumCounters, m->stream));

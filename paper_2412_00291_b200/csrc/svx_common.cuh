@@ -335,15 +335,13 @@ enum Counter : int {
     C_SEM = 1,          // allocated semantic layers
     C_TOUCHED = 2,      // blocks touched by the current frame group
     C_RECORDS = 5,      // fallback visit records of the group
-    C_FB_VOXELS = 6,    // fallback (voxel, frame) descriptors written by k_fb_sort
+    C_FB_VOXELS = 6,    // fallback (voxel, frame) descriptors written by k_fb_runs
     C_CAND = 10,        // semantic candidate blocks
     C_ERR_CONF = 11,    // confidence outside [0, 1]
     C_SEM_UPDATED = 12,
     C_ABORT = 16,       // bitmask of abort reasons (kAbort*); every frame kernel no-ops while set
     C_BLOCKS_BEFORE = 17,  // C_BLOCKS at the start of the current frame group
     C_MAPPED = 18,      // blocks with pool + visit-mask memory mapped (host-written)
-    C_FB_BLOCKS = 19,   // blocks holding fallback records this group
-    C_BUCKET_TOP = 23,  // fallback bucket space handed out this group
     C_DONE = 24,        // CTAs of k_fold finished (the last one writes the group's reports)
     kNumCounters = 32
 };

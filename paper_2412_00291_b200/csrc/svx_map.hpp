@@ -12,7 +12,7 @@
 //   mask pool  [blocks][kMaskWords] u32  per-block visit masks of the current frame group
 //                                      (VMM, parallel to the TSDF pool, 1152 B per block)
 //   group scratch: stamp[cap] u32 (first touch per group), touched[cap] u32, fallback
-//                  records and their per-block buckets, the visit-mask word list
+//                  records (sorted per group), the per-frame visited-voxel lists
 #pragma once
 
 #include <cuda.h>
@@ -201,18 +201,15 @@ struct svx_map {
     uint64_t mask_zeroed = 0;        // blocks of mask_pool zero-filled so far
     uint32_t* fctr = nullptr;        // [kMaxG][kFC] per-frame counters of the current group
     uint32_t* h_fctr = nullptr;      // pinned mirror (exchange mode)
-    svx::DevBuf<unsigned long long> records;  // fallback visit records: slot<<41|lin<<32|g<<28|pixel
+    // fallback stage (voxels whose own pixel has no return in some frame): the group's visit
+    // records (block, voxel, frame, pixel; the unused tail holds ~0, the sort's padding key),
+    // their sorted copy, the radix sort's scratch, one descriptor per (voxel, frame) run
+    svx::DevBuf<unsigned long long> records;
     svx::DevBuf<unsigned long long> records_alt;  // capacity path: visited block keys
     svx::DevBuf<uint8_t> sort_tmp;
-    // fallback stage (voxels whose own pixel has no return in some frame): per-slot record
-    // counts / bucket offsets / claims, the blocks holding records, the bucketed records
-    uint32_t* fbcnt = nullptr;       // [cap]
-    uint32_t* fbstart = nullptr;     // [cap]
-    uint32_t* fbfill = nullptr;      // [cap]
-    uint32_t* fbclaim = nullptr;     // [cap] bucket allocation claim flags
-    uint32_t* fbslots = nullptr;     // [cap]
-    svx::DevBuf<unsigned long long> bucket, bucket2;  // records grouped by block (+ sort scratch)
-    svx::DevBuf<uint4> fbdesc;       // fallback voxels: pool idx, voxel | frames << 16, records start, count
+    svx::DevBuf<unsigned long long> bucket;  // the records, sorted
+    svx::DevBuf<uint8_t> fb_tmp;
+    svx::DevBuf<uint4> fbdesc;       // fallback voxels: pool idx, voxel | frame << 16, records start, count
     uint32_t rec_cap = 0;
     svx::DevBuf<uint32_t> vlist;     // per frame of the group: its visited voxels, (pool idx << 9) | voxel
     uint32_t vox_cap = 0;            // entries per frame
@@ -277,8 +274,9 @@ void count_launch(uint64_t n = 1);
 struct ProfMark {
     svx_map* m;
     int kid;
+    int launches;  // kernel launches the mark spans
     cudaEvent_t a = nullptr;
-    ProfMark(svx_map* map, int k);
+    ProfMark(svx_map* map, int k, int n_launches = 1);
     ~ProfMark();
 };
 void prof_resolve(svx_map* m);
@@ -360,6 +358,8 @@ void run_group_xbegin(svx_map* m, const FrameJob* jobs, int G, const svx_integra
                       uint64_t* send_meta, const void** d_send);
 void run_group_xend(svx_map* m, const void* d_recv, const uint64_t* recv_meta, svx_frame_report* reps);
 void reset_frame_state(svx_map* m);
+// Fallback record capacity per frame group (buffers sized, padding key written).
+void set_rec_cap(svx_map* m, uint32_t cap);
 // Writes the host's block/layer/mapping counts into the device counters.
 void push_block_counters(svx_map* m);
 unsigned persistent_grid(int device);

@@ -233,7 +233,7 @@ cudaEvent_t take_event(svx_map* m) {
 }
 }  // namespace
 
-ProfMark::ProfMark(svx_map* map, int k) : m(map), kid(k) {
+ProfMark::ProfMark(svx_map* map, int k, int n_launches) : m(map), kid(k), launches(n_launches) {
     if (!m->prof || !((m->prof_mask >> k) & 1u)) return;
     a = take_event(m);
     SVX_CUDA(cudaEventRecord(a, m->stream));
@@ -244,7 +244,7 @@ ProfMark::~ProfMark() {
     cudaEvent_t b = take_event(m);
     cudaEventRecord(b, m->stream);
     m->prof_pending.push_back({kid, a, b});
-    m->prof_acc.launches[kid] += 1;
+    m->prof_acc.launches[kid] += uint64_t(launches);
 }
 
 void prof_resolve(svx_map* m) {

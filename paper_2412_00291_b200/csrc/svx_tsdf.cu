@@ -20,28 +20,28 @@
 //                of the tile's blocks and 512-bit voxel masks; per visit the own-pixel test
 //                of the voxel (FP32 with an exact-decision margin): a voxel whose own pixel
 //                has no return is measured by every visiting ray in the reference
-//                (.cpp:232-238), so such a visit becomes a fallback record (slot, voxel,
+//                (.cpp:232-238), so such a visit becomes a fallback record (block, voxel,
 //                frame, pixel). Epilogue: one hash find-or-insert per distinct block (new
 //                block -> next pool index, zero-filled by the tile), the group's touched
 //                list, the frame's visit-mask row (RED.OR) and the union row (ATOM.OR: the
 //                words a tile sets first become the group's word list).
-//   k_fb_bucket  the fallback records into per-block buckets.
-//   k_fb_sort    CTA per block with fallback records: orders its records by (voxel, frame,
-//                pixel) - per frame the reference's ascending (v, u) visit order after its
-//                chunk-order merge + stable_sort (.cpp:141-146,215-216) - and emits one
-//                descriptor per such voxel.
-//   k_fold       warps pull chunks of 32 listed mask words (lane per visited voxel) and then
-//                chunks of fallback-voxel descriptors from two queues, and apply the
-//                group's frames to each voxel in order (own-pixel measurement where the own
-//                pixel has a return, else the frame's visiting rays in ascending pixel
-//                order; accumulate-then-merge fold, Eq. 4-5). Clears the mask words, marks
-//                dirty blocks, counts per-frame touched / new blocks; the last CTA writes
-//                the frames' reports.
+//   (sort)       the group's fallback records, radix-sorted on their (block, voxel,
+//                frame, pixel) bits (cub::DeviceRadixSort over the record buffer; O(records)
+//                however many rays visit a voxel).
+//   k_fb_runs    one descriptor per (voxel, frame) run of the sorted records: per frame
+//                the reference's ascending (v, u) visit order (.cpp:141-146,215-216).
+//   k_fold       one launch per frame g of the group: thread per fallback descriptor of
+//                frame g (its records in pixel order), then the frame's visited-voxel list,
+//                32 per warp (own pixel, measurement, accumulate-then-merge fold, Eq. 4-5);
+//                each voxel then holds frames 0..g. The last frame's launch marks dirty
+//                blocks, counts per-frame touched / new blocks, clears the masks, and its
+//                last CTA writes the frames' reports.
 // Any abort (pool growth, buffer growth, capacity, key range) stops the batch; the host
 // rolls the aborted group back (its blocks, hash entries and masks) and retries it
 // (CapacityError and key-range errors: frame by frame, reproducing the reference's
 // per-frame behaviour).
 #include <cub/block/block_scan.cuh>
+#include <cub/device/device_radix_sort.cuh>
 #include <math_constants.h>
 
 #include <algorithm>
@@ -74,6 +74,7 @@ struct GroupConsts {
     uint32_t G, P, VW;  // frames, pixels per frame, valid-bit words per frame
     uint32_t tiles;     // band tiles per frame
     uint32_t max_blocks, rec_cap, vox_cap;
+    uint32_t pbits;  // pixel bits of a fallback record (make_record)
 };
 
 // Per-frame pose data.
@@ -482,21 +483,21 @@ __device__ inline void store_voxel(svx_tsdf_voxel* p, const svx_tsdf_voxel& v) {
     d[4] = v.gradient[2];
 }
 
-// Fallback visit record: bits 41.. hash slot, 32..40 voxel, 28..31 frame of the group,
-// 0..27 pixel. Within a block, the low 41 bits order by (voxel, frame, pixel).
-__device__ inline unsigned long long make_record(uint32_t slot, int lin, uint32_t g, uint32_t p) {
-    return (static_cast<unsigned long long>(slot) << 41) | (static_cast<unsigned long long>(lin) << 32) |
-           (static_cast<unsigned long long>(g) << 28) | p;
+// Fallback visit record: (pool index, voxel, frame of the group, pixel), packed so that the
+// unsigned order is (block, voxel, frame, pixel): pixel in the low pb bits (pb = bits of the
+// scan's pixel count), frame in the next 4, voxel in the next 9, pool index above. The
+// group's records are sorted on those bits (k_fb_runs).
+__device__ inline unsigned long long make_record(uint32_t idx, int lin, uint32_t g, uint32_t p, uint32_t pb) {
+    return (((static_cast<unsigned long long>(idx) << 9 | static_cast<unsigned long long>(lin)) << 4 |
+             static_cast<unsigned long long>(g)) << pb) | p;
 }
-__device__ inline uint32_t rec_frame(unsigned long long r) { return uint32_t(r >> 28) & 15u; }
-__device__ inline uint32_t rec_pixel(unsigned long long r) { return uint32_t(r) & 0x0FFFFFFFu; }
-__device__ inline int rec_lin(unsigned long long r) { return int(uint32_t(r >> 32) & 511u); }
+__device__ inline uint32_t rec_pixel(unsigned long long r, uint32_t pb) { return uint32_t(r & ((1ull << pb) - 1)); }
 
 // Applies frame g to the voxel at vp (tsdf_integrator.cpp:224-248): the own pixel of the
 // voxel centre if it holds a return (.cpp:232-233), else every visiting ray of the frame
 // in ascending pixel order (.cpp:235-236), given as `recs` (its fallback records, sorted
 // by pixel). Without records (kRec = false), a voxel whose own pixel has no return returns
-// kFallback and is left alone: a fallback descriptor (k_fb_sort) applies it. Returns 1 when
+// kFallback and is left alone: a fallback descriptor (k_fb_runs) applies it. Returns 1 when
 // the voxel was updated.
 constexpr uint32_t kFallback = 0xFFFFFFFFu;
 
@@ -612,7 +613,7 @@ __device__ __forceinline__ uint32_t fold_one(const GroupConsts& c, const FramePo
         return fold_own_fast(c, f.origin, cache, own, center, vp, vox);
     } else {
         for (uint32_t j = 0; j < nrec; ++j) {
-            const Term t = measure_term(c, f.origin, cache, rec_pixel(recs[j]), center, vox);
+            const Term t = measure_term(c, f.origin, cache, rec_pixel(recs[j], c.pbits), center, vox);
             if (t.flags & 1u) {
                 accumulate(acc, t);
                 measured = true;
@@ -709,8 +710,7 @@ __device__ inline bool is_remote(const GroupConsts& c, uint64_t key) {
 // shared tables are full. Same effect as the staged path.
 __device__ void visit_global(const GroupConsts& c, uint32_t g, HashView h, uint64_t* __restrict__ block_keys,
                              uint32_t* __restrict__ stamp, uint32_t* __restrict__ touched,
-                             uint32_t* __restrict__ fm, uint32_t* __restrict__ fbcnt,
-                             unsigned long long* __restrict__ rec, svx_tsdf_voxel* __restrict__ pool,
+                             uint32_t* __restrict__ fm, unsigned long long* __restrict__ rec, svx_tsdf_voxel* __restrict__ pool,
                              uint32_t* __restrict__ vlist, uint32_t* __restrict__ fctr,
                              uint4* __restrict__ xsend, uint32_t* __restrict__ xcnt,
                              uint32_t* __restrict__ ctr, uint64_t key, int lin, bool fb, uint32_t p) {
@@ -732,9 +732,8 @@ __device__ void visit_global(const GroupConsts& c, uint32_t g, HashView h, uint6
         else atomicOr(&ctr[C_ABORT], kAbortVox);
     }
     if (!fb) return;
-    atomicAdd(&fbcnt[r.slot], 1u);
     const uint32_t pos = atomicAdd(&ctr[C_RECORDS], 1u);
-    if (pos < c.rec_cap) rec[pos] = make_record(r.slot, lin, g, p);
+    if (pos < c.rec_cap) rec[pos] = make_record(r.idx, lin, g, p, c.pbits);
     else atomicOr(&ctr[C_ABORT], kAbortRecords);
 }
 
@@ -756,7 +755,7 @@ constexpr int kTileFb = SVX_TILE_FB;  // staged fallback visits per tile
 __global__ void __launch_bounds__(kTileU * kTileV, 4)
 k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
        uint64_t* __restrict__ block_keys, uint32_t* __restrict__ stamp, uint32_t* __restrict__ touched,
-       uint32_t* __restrict__ fm, uint32_t* __restrict__ fbcnt, unsigned long long* __restrict__ rec,
+       uint32_t* __restrict__ fm, unsigned long long* __restrict__ rec,
        svx_tsdf_voxel* __restrict__ pool, uint32_t* __restrict__ vlist,
        uint32_t* __restrict__ fctr, uint4* __restrict__ xsend, uint32_t* __restrict__ xcnt,
        uint32_t* __restrict__ ctr) {
@@ -770,7 +769,6 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
     __shared__ uint32_t lidx[kLocalKeys];
     __shared__ uint32_t lmask[kLocalKeys][16];
     __shared__ uint32_t lfb[kTileFb];
-    __shared__ uint32_t lcnt[kLocalKeys];  // fallback records per local block
     __shared__ uint32_t lnew[kLocalKeys];  // pool indices of blocks this tile created
     __shared__ uint8_t s_occ[kLocalKeys];
     __shared__ uint32_t nfb, nnew, nocc;
@@ -783,7 +781,6 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
         for (int i = tid; i < int(sizeof(FramePose) / 4); i += kTileU * kTileV) dst[i] = src[i];
     }
     lkey[tid] = kEmptyKey;
-    lcnt[tid] = 0u;
 #pragma unroll
     for (int w = 0; w < 16; ++w) lmask[tid][w] = 0u;
     if (tid == 0) nfb = nnew = nocc = 0;
@@ -903,7 +900,7 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
                 fb = own == kInvalid || !pixel_has_return(validbits, own);
             }
             if (cur_li < 0) {  // local table full: straight to global state
-                visit_global(c, g, h, block_keys, stamp, touched, fm, fbcnt, rec, pool, vlist, fctr, xsend, xcnt, ctr, cur_key,
+                visit_global(c, g, h, block_keys, stamp, touched, fm, rec, pool, vlist, fctr, xsend, xcnt, ctr, cur_key,
                              lin, fb, p);
                 return;
             }
@@ -919,7 +916,7 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
                 if (pos < uint32_t(kTileFb))
                     lfb[pos] = (uint32_t(cur_li) << 24) | (uint32_t(lin) << 15) | uint32_t(tid);
                 else
-                    visit_global(c, g, h, block_keys, stamp, touched, fm, fbcnt, rec, pool, vlist, fctr, xsend,
+                    visit_global(c, g, h, block_keys, stamp, touched, fm, rec, pool, vlist, fctr, xsend,
                                  xcnt, ctr, cur_key, lin, true, p);
             }
         });
@@ -988,23 +985,22 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
         if (pos < c.xcap)
             xsend[uint64_t(d) * c.xcap + pos] = make_uint4(uint32_t(lkey[li]), uint32_t(lkey[li] >> 32), z, w);
     };
-    // staged fallback visits -> records (slot, voxel, frame, pixel), counted per block
+    // staged fallback visits -> records (block, voxel, frame, pixel)
     uint32_t nrec = 0;
-    for (uint32_t i = tid; i < nf; i += kTileU * kTileV) nrec += lslot[lfb[i] >> 24] != kInvalid ? 1u : 0u;
+    for (uint32_t i = tid; i < nf; i += kTileU * kTileV) nrec += lidx[lfb[i] >> 24] != kInvalid ? 1u : 0u;
     uint32_t rpos = cta_reserve<kW>(nrec, &ctr[C_RECORDS], s_w);
     if (nrec && rpos + nrec > c.rec_cap) atomicOr(&ctr[C_ABORT], kAbortRecords);
     for (uint32_t i = tid; i < nf; i += kTileU * kTileV) {
         const uint32_t e = lfb[i], li = e >> 24;
-        const uint32_t sl = lslot[li];
+        const uint32_t bi = lidx[li];
         const uint32_t t = e & 255u;
         const uint32_t px = tile_p0 + (t / kTileU) * uint32_t(c.m.W) + (t % kTileU);
-        if (sl == kInvalid) {
+        if (bi == kInvalid) {
             if (c.exchange && lown[li] != c.shard_rank) xput(li, 0x80000000u | (g << 9) | ((e >> 15) & 511u), px);
             continue;
         }
-        if (rpos < c.rec_cap) rec[rpos] = make_record(sl, int((e >> 15) & 511u), g, px);
+        if (rpos < c.rec_cap) rec[rpos] = make_record(bi, int((e >> 15) & 511u), g, px, c.pbits);
         ++rpos;
-        atomicAdd(&lcnt[li], 1u);
     }
     // voxel masks -> the frame's row of each block; the bits a tile sets first (the atomic
     // returns them clear) are those voxels' single entries in the frame's voxel list
@@ -1063,137 +1059,32 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
             }
         }
     }
-    __syncthreads();  // lcnt complete
-    if (lcnt[tid]) atomicAdd(&fbcnt[lslot[tid]], lcnt[tid]);
 }
 
-// Fallback records into per-block buckets; a block's bucket is allocated by the first of
-// its records to arrive.
+// The group's fallback records, sorted by (block, voxel, frame, pixel) (a device radix sort
+// over the record bits precedes this kernel: O(records) whatever the number of rays per
+// voxel), cut into (voxel, frame) runs: one descriptor per run (pool index, voxel | frame
+// << 16, first record, count) - per frame the reference's ascending (v, u) visit order
+// after its chunk-order merge + stable_sort (tsdf_integrator.cpp:141-146,215-216). The
+// unsorted input is reset to the sort's padding key for the next group.
 __global__ void __launch_bounds__(kThreads)
-k_fb_bucket(const unsigned long long* __restrict__ rec, uint32_t rec_cap, const uint32_t* __restrict__ fbcnt,
-            uint32_t* __restrict__ fbstart, uint32_t* __restrict__ fbclaim, uint32_t* __restrict__ fbfill,
-            uint32_t* __restrict__ fbslots, unsigned long long* __restrict__ bucket, uint32_t* __restrict__ ctr) {
+k_fb_runs(const unsigned long long* __restrict__ sorted, unsigned long long* __restrict__ rec, uint32_t rec_cap,
+          uint32_t pb, uint4* __restrict__ fbdesc, uint32_t* __restrict__ fctr, uint32_t* __restrict__ ctr) {
     pdl_wait();
     pdl_trigger();
     if (ctr[C_ABORT]) return;
-    const uint32_t nr = min(ctr[C_RECORDS], rec_cap);
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += gridDim.x * blockDim.x) {
-        const unsigned long long r = rec[i];
-        const uint32_t slot = uint32_t(r >> 41);
-        uint32_t start = __ldcg(&fbstart[slot]);
-        if (start == kInvalid) {
-            if (atomicCAS(&fbclaim[slot], 0u, 1u) == 0u) {  // this record allocates the bucket
-                start = atomicAdd(&ctr[C_BUCKET_TOP], fbcnt[slot]);
-                fbslots[atomicAdd(&ctr[C_FB_BLOCKS], 1u)] = slot;
-                atomicExch(&fbstart[slot], start);
-            } else {
-                while ((start = *reinterpret_cast<volatile uint32_t*>(&fbstart[slot])) == kInvalid) __nanosleep(32);
-            }
-        }
-        bucket[start + atomicAdd(&fbfill[slot], 1u)] = r;
+    const uint32_t n = min(ctr[C_RECORDS], rec_cap);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        rec[i] = ~0ull;
+        const unsigned long long k = sorted[i];
+        const unsigned long long run = k >> pb;  // (block, voxel, frame)
+        if (i > 0 && (sorted[i - 1] >> pb) == run) continue;
+        uint32_t j = i + 1;
+        while (j < n && (sorted[j] >> pb) == run) ++j;
+        const uint32_t g = uint32_t(run) & 15u, lin = uint32_t(run >> 4) & 511u, idx = uint32_t(run >> 13);
+        fbdesc[atomicAdd(&ctr[C_FB_VOXELS], 1u)] = make_uint4(idx, lin | (g << 16), i, j - i);
+        atomicAdd(&fctr[g * kFC + FC_FBV], 1u);
     }
-}
-
-template <int kThr>
-__device__ inline void load_poses(const GroupParams& gp, FramePose* s_f) {
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(&gp.f[0]);
-    uint32_t* dst = reinterpret_cast<uint32_t*>(s_f);
-    const int n = int(gp.c.G * (sizeof(FramePose) / 4));
-    for (int i = threadIdx.x; i < n; i += kThr) dst[i] = src[i];
-}
-
-// CTA per block with fallback records. The bucket is ordered by (voxel, frame, pixel):
-// counting sort by voxel (histogram, scan, scatter to the sort scratch), then inside each
-// voxel's segment a rank sort (keys are unique: a ray visits a voxel once per frame), in
-// parallel. Each (voxel, frame) run of records becomes one descriptor (pool index, voxel,
-// frame, its records, sorted by pixel) that the frame's fold applies.
-__global__ void __launch_bounds__(kThreads)
-k_fb_sort(const uint32_t G, HashView h, const uint32_t* __restrict__ fbslots, uint32_t* __restrict__ fbcnt,
-          uint32_t* __restrict__ fbstart, uint32_t* __restrict__ fbclaim, uint32_t* __restrict__ fbfill,
-          unsigned long long* __restrict__ bucket, unsigned long long* __restrict__ bucket2,
-          uint4* __restrict__ fbdesc, uint32_t* __restrict__ fctr, uint32_t* __restrict__ ctr) {
-    pdl_wait();
-    pdl_trigger();
-    if (cta_aborted(ctr)) return;
-    using Scan = cub::BlockScan<uint32_t, kThreads>;
-    constexpr int kPer = kBlockVoxels / kThreads;  // voxels per thread
-    constexpr int kW = kThreads / 32;
-    __shared__ typename Scan::TempStorage scan_tmp;
-    __shared__ uint32_t seg_start[kBlockVoxels], seg_cnt[kBlockVoxels], cursor[kBlockVoxels];
-    __shared__ uint32_t s_fbv[kMaxG];
-    __shared__ uint32_t s_w[2 * kW];
-    if (threadIdx.x < kMaxG) s_fbv[threadIdx.x] = 0u;
-    const uint32_t nb = ctr[C_FB_BLOCKS];
-    for (uint32_t t = blockIdx.x; t < nb; t += gridDim.x) {
-        const uint32_t slot = fbslots[t];
-        const uint32_t cnt = fbcnt[slot];
-        const uint32_t start = fbstart[slot];
-        const uint32_t idx = h.vals[slot];
-        unsigned long long* bk = bucket + start;
-        unsigned long long* tmp = bucket2 + start;
-        for (int v = threadIdx.x; v < kBlockVoxels; v += kThreads) seg_cnt[v] = 0u;
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) atomicAdd(&seg_cnt[rec_lin(bk[i])], 1u);
-        __syncthreads();
-        {   // exclusive scan of the per-voxel counts -> segment starts
-            uint32_t cc[kPer];
-#pragma unroll
-            for (int j = 0; j < kPer; ++j) cc[j] = seg_cnt[threadIdx.x * kPer + j];
-            Scan(scan_tmp).ExclusiveSum(cc, cc);
-#pragma unroll
-            for (int j = 0; j < kPer; ++j) {
-                seg_start[threadIdx.x * kPer + j] = cc[j];
-                cursor[threadIdx.x * kPer + j] = cc[j];
-            }
-        }
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
-            const unsigned long long k = bk[i];
-            tmp[atomicAdd(&cursor[rec_lin(k)], 1u)] = k;
-        }
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
-            const unsigned long long k = tmp[i];
-            const int v = rec_lin(k);
-            const uint32_t b = seg_start[v], e = b + seg_cnt[v];
-            const uint32_t lo = uint32_t(k);  // (frame, pixel)
-            uint32_t r = 0;
-            for (uint32_t j = b; j < e; ++j) r += uint32_t(tmp[j]) < lo ? 1u : 0u;
-            bk[b + r] = k;
-        }
-        __syncthreads();
-        // one descriptor per (voxel, frame) run of the sorted segments
-        uint32_t nd = 0;
-#pragma unroll
-        for (int j = 0; j < kPer; ++j) {
-            const int v = threadIdx.x * kPer + j;
-            const uint32_t b = seg_start[v], e = b + seg_cnt[v];
-            for (uint32_t q = b; q < e; ++q) nd += (q == b || rec_frame(bk[q]) != rec_frame(bk[q - 1])) ? 1u : 0u;
-        }
-        uint32_t pos = cta_reserve<kW>(nd, &ctr[C_FB_VOXELS], s_w);
-#pragma unroll
-        for (int j = 0; j < kPer; ++j) {
-            const int v = threadIdx.x * kPer + j;
-            const uint32_t b = seg_start[v], e = b + seg_cnt[v];
-            for (uint32_t q = b; q < e;) {
-                const uint32_t g = rec_frame(bk[q]);
-                uint32_t q2 = q + 1;
-                while (q2 < e && rec_frame(bk[q2]) == g) ++q2;
-                fbdesc[pos++] = make_uint4(idx, uint32_t(v) | (g << 16), start + q, q2 - q);
-                atomicAdd(&s_fbv[g], 1u);
-                q = q2;
-            }
-        }
-        if (threadIdx.x == 0) {  // per-slot fallback state, clean for the next group
-            fbcnt[slot] = 0u;
-            fbstart[slot] = kInvalid;
-            fbclaim[slot] = 0u;
-            fbfill[slot] = 0u;
-        }
-        __syncthreads();  // shared arrays are reused by the next bucket
-    }
-    __syncthreads();
-    if (threadIdx.x < G && s_fbv[threadIdx.x]) atomicAdd(&fctr[threadIdx.x * kFC + FC_FBV], s_fbv[threadIdx.x]);
 }
 
 // Frame g of the group: one thread per listed visited voxel of the frame (grid-stride, one
@@ -1304,7 +1195,7 @@ k_fold(const __grid_constant__ GroupConsts c, const __grid_constant__ FramePose 
     }
     if (threadIdx.x == 0) {
         ctr[C_DONE] = 0;
-        ctr[C_TOUCHED] = ctr[C_RECORDS] = ctr[C_FB_BLOCKS] = ctr[C_BUCKET_TOP] = ctr[C_FB_VOXELS] = 0;
+        ctr[C_TOUCHED] = ctr[C_RECORDS] = ctr[C_FB_VOXELS] = 0;
         ctr[C_BLOCKS_BEFORE] = ctr[C_BLOCKS];
     }
 }
@@ -1318,7 +1209,7 @@ k_fold(const __grid_constant__ GroupConsts c, const __grid_constant__ FramePose 
 __global__ void __launch_bounds__(kThreads)
 k_ingest(const GroupConsts c, const uint4* __restrict__ recv, uint32_t n, HashView h,
          uint64_t* __restrict__ block_keys, uint32_t* __restrict__ stamp, uint32_t* __restrict__ touched,
-         uint32_t* __restrict__ fm, uint32_t* __restrict__ fbcnt, unsigned long long* __restrict__ rec,
+         uint32_t* __restrict__ fm, unsigned long long* __restrict__ rec,
          svx_tsdf_voxel* __restrict__ pool, uint4* __restrict__ xaux, uint32_t* __restrict__ fctr,
          uint32_t* __restrict__ ctr) {
     pdl_wait();
@@ -1336,9 +1227,8 @@ k_ingest(const GroupConsts c, const uint4* __restrict__ recv, uint32_t n, HashVi
         if (e.z & 0x80000000u) {  // fallback record
             const uint32_t g = (e.z >> 9) & 15u;
             atomicOr(&bm[kHdrRow * 16], 1u << g);
-            atomicAdd(&fbcnt[r.slot], 1u);
             const uint32_t pos = atomicAdd(&ctr[C_RECORDS], 1u);
-            if (pos < c.rec_cap) rec[pos] = make_record(r.slot, int(e.z & 511u), g, e.w);
+            if (pos < c.rec_cap) rec[pos] = make_record(r.idx, int(e.z & 511u), g, e.w, c.pbits);
             else atomicOr(&ctr[C_ABORT], kAbortRecords);
         } else {
             const uint32_t g = (e.z >> 4) & 15u, w = e.z & 15u;
@@ -1463,6 +1353,8 @@ GroupConsts make_consts(svx_map* m, svx_scan* s, const svx_integrator_cfg& cfg, 
     c.max_blocks = m->cfg.max_blocks;
     c.rec_cap = m->rec_cap;
     c.vox_cap = m->vox_cap;
+    c.pbits = 1;
+    while ((1ull << c.pbits) < s->P) ++c.pbits;
     return c;
 }
 
@@ -1507,7 +1399,7 @@ void launch_group_kernels(svx_map* m, svx_scan* s, const GroupParams& gp, FrameO
     {
         ProfMark pm(m, SVX_K_RAYCAST);
         launch_pdl(k_band, c.G * c.tiles, kTileU * kTileV, m->stream, gp, sc, hv, m->block_keys, m->stamp,
-                   m->touched, fm, m->fbcnt, m->records.p, tsdf_base(m), m->vlist.p, m->fctr, m->xsend.p,
+                   m->touched, fm, m->records.p, tsdf_base(m), m->vlist.p, m->fctr, m->xsend.p,
                    m->xcnt.p, m->d_ctr);
         count_launch();
     }
@@ -1526,15 +1418,29 @@ void launch_fold_kernels(svx_map* m, svx_scan* s, const GroupParams& gp, FrameOu
     uint32_t* fm = mask_base(m);
     {
         ProfMark pm(m, SVX_K_FALLBACK);
-        launch_pdl(k_fb_bucket, pg / 4, kThreads, m->stream, m->records.p, m->rec_cap, m->fbcnt, m->fbstart,
-                   m->fbclaim, m->fbfill, m->fbslots, m->bucket.p, m->d_ctr);
-        launch_pdl(k_fb_sort, pg / 2, kThreads, m->stream, c.G, hv, m->fbslots, m->fbcnt, m->fbstart, m->fbclaim,
-                   m->fbfill, m->bucket.p, m->bucket2.p, m->fbdesc.p, m->fctr, m->d_ctr);
-        count_launch(2);
+        // the group's records sorted on their (block, voxel, frame, pixel) bits: the whole
+        // buffer (the unused tail holds the padding key ~0, which sorts last)
+        int end_bit = int(c.pbits) + 13, ib = 1;
+        while ((1ull << ib) < m->cfg.max_blocks) ++ib;
+        end_bit += ib;
+        size_t bytes = 0;
+        SVX_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, m->records.p, m->bucket.p, int(c.rec_cap), 0, end_bit,
+                                                m->stream));
+        if (bytes > m->fb_tmp.n) m->fb_tmp.alloc(bytes);  // (set_rec_cap sized it for any bit range)
+        SVX_CUDA(cub::DeviceRadixSort::SortKeys(m->fb_tmp.p, bytes, m->records.p, m->bucket.p, int(c.rec_cap), 0,
+                                                end_bit, m->stream));
+        launch_pdl(k_fb_runs, pg, kThreads, m->stream, m->bucket.p, m->records.p, c.rec_cap, c.pbits, m->fbdesc.p,
+                   m->fctr, m->d_ctr);
+        count_launch(1);
     }
+    // one profiling mark spans the group's folds when nothing runs between them (marks
+    // between PDL launches cost their overlap), else one per fold
+    std::unique_ptr<ProfMark> all_folds;
+    if (!labels) all_folds = std::make_unique<ProfMark>(m, SVX_K_FOLD, c.G);
     for (uint32_t g = 0; g < c.G; ++g) {
         {
-            ProfMark pm(m, SVX_K_FOLD);  // per launch: label passes may follow each fold
+            std::unique_ptr<ProfMark> pm;
+            if (labels) pm = std::make_unique<ProfMark>(m, SVX_K_FOLD);
             launch_pdl(k_fold, fold_grid(m->device), kThreads, m->stream, c, gp.f[g], g, sc, m->vals, m->block_keys,
                        tsdf_base(m), fm, m->vlist.p, m->fbdesc.p, m->bucket.p, m->touched, m->dirty, m->fctr, outs,
                        m->d_ctr);
@@ -1546,6 +1452,7 @@ void launch_fold_kernels(svx_map* m, svx_scan* s, const GroupParams& gp, FrameOu
                 labels_enqueue(m, *labels->lb, labels->img_off[f], labels->img_off[f + 1], g);
         }
     }
+    all_folds.reset();
     SVX_CUDA(cudaGetLastError());
 }
 
@@ -1614,17 +1521,29 @@ unsigned persistent_grid(int device) {
     return unsigned(sms[device] * 8);  // 8 CTAs x 8 warps per SM
 }
 
+// Fallback record buffers for `cap` records per group: the records (all ~0, the sort's
+// padding key, outside a group's entries), their sorted copy and the run descriptors.
+void set_rec_cap(svx_map* m, uint32_t cap) {
+    const uint64_t had = m->records.n;
+    m->records.alloc(cap);
+    if (m->records.n != had)  // (re)allocated: contents undefined
+        SVX_CUDA(cudaMemsetAsync(m->records.p, 0xFF, 8ull * m->records.n, m->stream));
+    m->bucket.alloc(cap);
+    m->fbdesc.alloc(cap);
+    m->rec_cap = cap;
+    size_t bytes = 0;  // the radix sort's scratch for every bit range (allocated here, not per group)
+    SVX_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, m->records.p, m->bucket.p, int(cap), 0, 64, m->stream));
+    m->fb_tmp.alloc(bytes);
+}
+
 // Clears the group scratch (masks of the mapped blocks, fallback state, counters) after a
 // host-side intervention, and re-arms the device block counters.
 void reset_frame_state(svx_map* m) {
     if (m->mapped_blocks)
         SVX_CUDA(cudaMemsetAsync(mask_base(m), 0, 4ull * kMaskWords * m->mapped_blocks, m->stream));
-    SVX_CUDA(cudaMemsetAsync(m->fbcnt, 0, sizeof(uint32_t) * m->cap, m->stream));
-    SVX_CUDA(cudaMemsetAsync(m->fbclaim, 0, sizeof(uint32_t) * m->cap, m->stream));
-    SVX_CUDA(cudaMemsetAsync(m->fbfill, 0, sizeof(uint32_t) * m->cap, m->stream));
-    SVX_CUDA(cudaMemsetAsync(m->fbstart, 0xFF, sizeof(uint32_t) * m->cap, m->stream));
+    SVX_CUDA(cudaMemsetAsync(m->records.p, 0xFF, 8ull * m->records.n, m->stream));  // the sort's padding
     SVX_CUDA(cudaMemsetAsync(m->fctr, 0, sizeof(uint32_t) * kMaxG * kFC, m->stream));
-    for (int c : {C_TOUCHED, C_RECORDS, C_FB_VOXELS, C_FB_BLOCKS, C_ABORT, C_BUCKET_TOP, C_DONE})
+    for (int c : {C_TOUCHED, C_RECORDS, C_FB_VOXELS, C_ABORT, C_DONE})
         m->h_ctr[c] = 0;
     m->h_ctr[C_BLOCKS] = m->h_ctr[C_BLOCKS_BEFORE] = uint32_t(m->n_blocks);
     m->h_ctr[C_MAPPED] = uint32_t(m->mapped_blocks);
@@ -1836,11 +1755,7 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
         }
         if (abort & kAbortPool) ensure_blocks(m, uint64_t(m->n_blocks) + 2 * head + (blocks_seen - before));
         if (abort & kAbortRecords) {
-            m->rec_cap = std::max<uint32_t>(recs_seen + (recs_seen >> 1), m->rec_cap * 2);
-            m->records.alloc(m->rec_cap);
-            m->bucket.alloc(m->rec_cap);
-            m->bucket2.alloc(m->rec_cap);
-            m->fbdesc.alloc(m->rec_cap);
+            set_rec_cap(m, std::max<uint32_t>(recs_seen + (recs_seen >> 1), m->rec_cap * 2));
         }
         if (abort & kAbortVox) {
             m->vox_cap = uint32_t(std::min<uint64_t>(uint64_t(m->vox_cap) * 2, 0x7FFFFFFFull));
@@ -1933,11 +1848,7 @@ void run_group_xbegin(svx_map* m, const FrameJob* jobs, int G, const svx_integra
                                           std::to_string(m->cfg.max_blocks) + ")");
         if (abort & kAbortPool) ensure_blocks(m, uint64_t(m->n_blocks) + 2 * head + (blocks_seen - before));
         if (abort & kAbortRecords) {
-            m->rec_cap = std::max<uint32_t>(recs_seen + (recs_seen >> 1), m->rec_cap * 2);
-            m->records.alloc(m->rec_cap);
-            m->bucket.alloc(m->rec_cap);
-            m->bucket2.alloc(m->rec_cap);
-            m->fbdesc.alloc(m->rec_cap);
+            set_rec_cap(m, std::max<uint32_t>(recs_seen + (recs_seen >> 1), m->rec_cap * 2));
         }
         if (abort & kAbortVox) {
             m->vox_cap = uint32_t(std::min<uint64_t>(uint64_t(m->vox_cap) * 2, 0x7FFFFFFFull));
@@ -1983,11 +1894,11 @@ void run_group_xend(svx_map* m, const void* d_recv, const uint64_t* recv_meta, s
     ensure_blocks(m, uint64_t(m->h_ctr[C_BLOCKS]) + n_recv + 1);
     const uint64_t recs = m->h_ctr[C_RECORDS];
     if (recs + n_recv > m->rec_cap) {
-        m->rec_cap = uint32_t(std::min<uint64_t>((recs + n_recv) * 3 / 2 + 1024, 0xFFFFFFF0ull));
-        grow_keep(m->records, m->rec_cap, recs, m->stream);
-        m->bucket.alloc(m->rec_cap);
-        m->bucket2.alloc(m->rec_cap);
-        m->fbdesc.alloc(m->rec_cap);
+        const uint32_t cap = uint32_t(std::min<uint64_t>((recs + n_recv) * 3 / 2 + 1024, 0xFFFFFFF0ull));
+        grow_keep(m->records, cap, recs, m->stream);
+        // the new tail holds the sort's padding key
+        SVX_CUDA(cudaMemsetAsync(m->records.p + recs, 0xFF, 8ull * (m->records.n - recs), m->stream));
+        set_rec_cap(m, cap);
     }
     gp.c.rec_cap = m->rec_cap;
     // the voxel lists: this rank's entries (xbegin) + at most the received voxel bits per
@@ -2014,7 +1925,7 @@ void run_group_xend(svx_map* m, const void* d_recv, const uint64_t* recv_meta, s
     if (n_recv) {
         m->xaux.alloc(n_recv);
         launch_pdl(k_ingest, grid, kThreads, m->stream, gp.c, static_cast<const uint4*>(d_recv), uint32_t(n_recv),
-                   hash_view(m), m->block_keys, m->stamp, m->touched, mask_base(m), m->fbcnt, m->records.p,
+                   hash_view(m), m->block_keys, m->stamp, m->touched, mask_base(m), m->records.p,
                    tsdf_base(m), m->xaux.p, m->fctr, m->d_ctr);
         count_launch();
         launch_pdl(k_ingest_list, grid, kThreads, m->stream, gp.c, static_cast<const uint4*>(m->xaux.p),

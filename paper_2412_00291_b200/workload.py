@@ -408,7 +408,10 @@ def make(name: str, n_frames: int = None) -> Workload:
         W = int(name.split("-")[1]) if "-" in name else 1024
         n = n_frames or 50
         m = ProjectionModel.spinning(W, 128, 22.5, 22.5)
-        poses = [yaw_pose(-6 + 0.25 * i, 0.0, 0.5, 0.0) for i in range(n)]
+        # back and forth along x in [-6, 10] (0.25 m steps): any number of scans stays
+        # inside the room, clear of its walls (+-15 m)
+        poses = [yaw_pose(-6 + 0.25 * (i % 128 if i % 128 < 64 else 128 - i % 128), 0.0, 0.5, 0.0)
+                 for i in range(n)]
         return Workload(f"cfg5-W{W}", m, 0.1, 0.5, 20, poses, closed_room())
     if name == "tiny":  # unit-test sized
         n = n_frames or 4

@@ -167,6 +167,27 @@ def test_sweep_max_size_cfg5():
     assert st["blocks"] > 1000
 
 
+def test_sensor_next_to_a_wall_many_rays_per_voxel():
+    """Returns at 0.4-2 m (a sensor 0.5 m from a wall, a 4096-column scan): thousands of rays
+    visit the same voxels and many own pixels fall outside the vertical field of view, so
+    the fallback path orders long visit lists (sorted records, O(records)). One call per
+    frame and one batched call both equal the oracle."""
+    import torch
+    wl = W.make("cfg5-4096", 3)
+    wl.poses = [W.yaw_pose(14.5, 0.0, 0.5, 0.0), W.yaw_pose(14.4, 0.2, 0.6, 0.4), W.yaw_pose(14.45, -0.3, 0.4, -0.3)]
+    g, o = _run_pair(wl, svx.IntegratorConfig(), labels=False)
+    compare_maps(g.save_bytes(), o.save_bytes())
+    b = svx.VoxelStore(svx.MapConfig(wl.voxel_size, wl.truncation, wl.num_labels, 1 << 20), 0)
+    chunks = [p for p, _ in wl.scans()]
+    offs = np.zeros(len(chunks) + 1, np.uint64)
+    offs[1:] = np.cumsum([c.shape[0] for c in chunks])
+    pts = torch.cat(chunks).contiguous().cuda()
+    reps = b.integrate_clouds_device(wl.model, pts.data_ptr(), offs, 3, [wl.pose(i) for i in range(3)],
+                                     svx.IntegratorConfig())
+    assert b.save_bytes() == g.save_bytes()
+    assert all(r.updated_voxels > 0 for r in reps)
+
+
 def test_batched_paths_match_per_frame():
     """The batched entry points (clouds resident in HBM; clouds in pinned host memory,
     staged through the ingest ring) produce the same map, reports and dirty lists as
