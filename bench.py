@@ -885,7 +885,7 @@ def run_sweep(args):
             st = svx.VoxelStore(svx.MapConfig(wl.voxel_size, wl.truncation, wl.num_labels, 1 << 21), 0)
             ext = torch.cuda.ExternalStream(st.stream_ptr(), device=dev)
             icfg = svx.IntegratorConfig()
-            st.reserve(1 << 18, (1 << 18) if sem else 0)  # pool mapped before the timed passes
+            st.reserve(1 << 20, (1 << 18) if sem else 0)  # pool mapped before the timed passes
             # warm-up: the first 8 scans
             rel = offs[:9] - offs[0]
             st.integrate_clouds_device(wl.model, pts.data_ptr(), rel, 3, poses[:8], icfg)

@@ -168,7 +168,10 @@ svx_map* create_map(const svx_map_cfg& cfg, int device) {
         // the per-group sort covers the whole buffer
         uint32_t rec_cap = 1u << 18;
         // test hook: tiny buffers exercise the abort-and-resume paths
-        if (const char* e = std::getenv("SVX_TEST_REC_CAP")) rec_cap = uint32_t(std::max(1L, std::atol(e)));
+        if (const char* e = std::getenv("SVX_TEST_REC_CAP")) {
+            rec_cap = uint32_t(std::max(1L, std::atol(e)));
+            m->test_rec_cap = true;
+        }
         if (const char* e = std::getenv("SVX_TEST_POOL_HEAD")) m->test_pool_head = uint64_t(std::max(1L, std::atol(e)));
         set_rec_cap(m, rec_cap);
         SVX_CUDA(cudaMallocHost(&m->h_ctr, sizeof(uint32_t) * kNumCounters));

@@ -210,7 +210,8 @@ struct svx_map {
     svx::DevBuf<unsigned long long> bucket;  // the records, sorted
     svx::DevBuf<uint8_t> fb_tmp;
     svx::DevBuf<uint4> fbdesc;       // fallback voxels: pool idx, voxel | frame << 16, records start, count
-    uint32_t rec_cap = 0;
+    uint32_t rec_cap = 0;            // fallback records per group (the sort's size)
+    bool test_rec_cap = false;       // SVX_TEST_REC_CAP: fixed (tests of the overflow path)
     svx::DevBuf<uint32_t> vlist;     // per frame of the group: its visited voxels, (pool idx << 9) | voxel
     uint32_t vox_cap = 0;            // entries per frame
     // exchange mode (multi-GPU data plane, svx_tsdf.cu): per-destination send lists of

@@ -626,6 +626,46 @@ __device__ __forceinline__ uint32_t fold_one(const GroupConsts& c, const FramePo
     return 1;
 }
 
+// A fallback voxel with many visiting rays in frame g: the lanes of one warp measure its
+// records in parallel (32 at a time), lane 0 then takes the terms by shuffle in record
+// (= ascending pixel) order and sums them as the reference does (tsdf_integrator.cpp:
+// 235-236): the serial part per record is the accumulation, not the measurement. Returns 1
+// on lane 0 when the voxel was updated.
+constexpr uint32_t kWarpRecs = 8;  // descriptors with more records than this take a warp
+__device__ __forceinline__ uint32_t fold_records_warp(const GroupConsts& c, const FramePose& f, uint32_t g,
+                                                      svx_tsdf_voxel* vp, d3 center, const ScanSlots& sc,
+                                                      const unsigned long long* __restrict__ recs, uint32_t nrec,
+                                                      int lane) {
+    const PixCache* cache = cache_of(sc, c, g);
+    svx_tsdf_voxel vox = load_voxel(vp);
+    Accum acc{0.0, 0.0, 0.0, 0.0, 0.0};
+    bool measured = false;
+    for (uint32_t j0 = 0; j0 < nrec; j0 += 32u) {  // (warp-uniform)
+        Term t{0.f, 0.f, 0.f, 0.f, 0.f, 0u};
+        if (j0 + uint32_t(lane) < nrec)
+            t = measure_term(c, f.origin, cache, rec_pixel(recs[j0 + lane], c.pbits), center, vox);
+        const uint32_t n = min(32u, nrec - j0);
+        for (uint32_t k = 0; k < n; ++k) {
+            Term tk;
+            tk.wg = __shfl_sync(0xFFFFFFFFu, t.wg, int(k));
+            tk.w = __shfl_sync(0xFFFFFFFFu, t.w, int(k));
+            tk.nx = __shfl_sync(0xFFFFFFFFu, t.nx, int(k));
+            tk.ny = __shfl_sync(0xFFFFFFFFu, t.ny, int(k));
+            tk.nz = __shfl_sync(0xFFFFFFFFu, t.nz, int(k));
+            tk.flags = __shfl_sync(0xFFFFFFFFu, t.flags, int(k));
+            if (tk.flags & 1u) {  // (every lane keeps the same sums; lane 0 stores)
+                accumulate(acc, tk);
+                measured = true;
+            }
+        }
+    }
+    if (!measured) return 0;
+    fold(vox, acc);
+    if (lane != 0) return 0;
+    store_voxel(vp, vox);
+    return 1;
+}
+
 // Hash find-or-insert of a block key; a new block takes the next pool index.
 struct SlotRef {
     uint32_t slot, idx;
@@ -1114,11 +1154,19 @@ k_fold(const __grid_constant__ GroupConsts c, const __grid_constant__ FramePose 
     const uint32_t nv = min(fc[FC_VOX], c.vox_cap);
     const uint32_t* vl = vlist + uint64_t(g) * c.vox_cap;
     uint32_t n_upd = 0;
-    // fallback descriptors first: a long record chain starts early instead of in the tail
+    // fallback descriptors first (a record chain starts early instead of in the tail): those
+    // with many records one per warp, the rest one per thread
     const uint32_t nfv = ctr[C_FB_VOXELS];
+    for (uint32_t i = gtid >> 5; i < nfv; i += stride >> 5) {  // (warp-uniform)
+        const uint4 d = fbdesc[i];
+        if ((d.y >> 16) != g || d.w <= kWarpRecs) continue;
+        const int lin = int(d.y & 511u);
+        n_upd += fold_records_warp(c, f, g, pool + uint64_t(d.x) * kBlockVoxels + lin,
+                                   center_of(block_keys[d.x], lin, c.nu), sc, bucket + d.z, d.w, lane);
+    }
     for (uint32_t i = gtid; i < nfv; i += stride) {
         const uint4 d = fbdesc[i];
-        if ((d.y >> 16) != g) continue;
+        if ((d.y >> 16) != g || d.w > kWarpRecs) continue;
         const int lin = int(d.y & 511u);
         n_upd += fold_one<true>(c, f, g, pool + uint64_t(d.x) * kBlockVoxels + lin,
                                 center_of(block_keys[d.x], lin, c.nu), sc, bucket + d.z, d.w);
@@ -1767,6 +1815,13 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
     }
     for (int i = f0; i < n; ++i) commit(i);
     m->n_blocks = m->h_ctr[C_BLOCKS];
+    // the record capacity follows use: the per-group sort covers all of it, so after a batch
+    // it shrinks to 1.25x the batch's largest group (+ slack); a larger group later costs
+    // one rollback and retry with a grown buffer (above)
+    uint32_t hwm = 0;
+    for (int i = 0; i < n; ++i) hwm = std::max(hwm, m->h_outs[i].records);
+    const uint64_t want = (uint64_t(hwm) + hwm / 4 + 8192 + 4095) & ~uint64_t(4095);
+    if (!m->test_rec_cap && want < m->rec_cap) m->rec_cap = uint32_t(want);
 }
 
 namespace {
