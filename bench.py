@@ -909,7 +909,7 @@ def run_sweep(args):
                 e1.synchronize()
                 return e0.elapsed_time(e1)
             one_pass(8)                           # warm-up pass: buffers sized, pool mapped ahead
-            st.profile_read()
+            st.profile_enable(False)              # (resets the counters; no kernel marks)
             ms = one_pass(8 + n)                  # timed: no profiling marks (PDL chains intact)
             hp = st.profile_read().as_dict()      # host-side work of the timed pass
             st.profile_enable(True)               # kernel breakdown: a third, profiled pass

@@ -335,7 +335,7 @@ enum Counter : int {
     C_SEM = 1,          // allocated semantic layers
     C_TOUCHED = 2,      // blocks touched by the current frame group
     C_RECORDS = 5,      // fallback visit records of the group
-    C_FB_VOXELS = 6,    // fallback (voxel, frame) descriptors written by k_fb_runs
+    C_FB_VOXELS = 6,    // (unused since the per-frame descriptor lists: FC_FBV counts them)
     C_CAND = 10,        // semantic candidate blocks
     C_ERR_CONF = 11,    // confidence outside [0, 1]
     C_SEM_UPDATED = 12,

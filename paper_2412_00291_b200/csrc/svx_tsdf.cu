@@ -1122,8 +1122,8 @@ k_fb_runs(const unsigned long long* __restrict__ sorted, unsigned long long* __r
         uint32_t j = i + 1;
         while (j < n && (sorted[j] >> pb) == run) ++j;
         const uint32_t g = uint32_t(run) & 15u, lin = uint32_t(run >> 4) & 511u, idx = uint32_t(run >> 13);
-        fbdesc[atomicAdd(&ctr[C_FB_VOXELS], 1u)] = make_uint4(idx, lin | (g << 16), i, j - i);
-        atomicAdd(&fctr[g * kFC + FC_FBV], 1u);
+        // frame g's list (its fold reads only its own descriptors)
+        fbdesc[uint64_t(g) * rec_cap + atomicAdd(&fctr[g * kFC + FC_FBV], 1u)] = make_uint4(idx, lin | (g << 16), i, j - i);
     }
 }
 
@@ -1156,17 +1156,18 @@ k_fold(const __grid_constant__ GroupConsts c, const __grid_constant__ FramePose 
     uint32_t n_upd = 0;
     // fallback descriptors first (a record chain starts early instead of in the tail): those
     // with many records one per warp, the rest one per thread
-    const uint32_t nfv = ctr[C_FB_VOXELS];
+    const uint32_t nfv = min(fc[FC_FBV], c.rec_cap);
+    const uint4* fd = fbdesc + uint64_t(g) * c.rec_cap;
     for (uint32_t i = gtid >> 5; i < nfv; i += stride >> 5) {  // (warp-uniform)
-        const uint4 d = fbdesc[i];
-        if ((d.y >> 16) != g || d.w <= kWarpRecs) continue;
+        const uint4 d = fd[i];
+        if (d.w <= kWarpRecs) continue;
         const int lin = int(d.y & 511u);
         n_upd += fold_records_warp(c, f, g, pool + uint64_t(d.x) * kBlockVoxels + lin,
                                    center_of(block_keys[d.x], lin, c.nu), sc, bucket + d.z, d.w, lane);
     }
     for (uint32_t i = gtid; i < nfv; i += stride) {
-        const uint4 d = fbdesc[i];
-        if ((d.y >> 16) != g || d.w > kWarpRecs) continue;
+        const uint4 d = fd[i];
+        if (d.w > kWarpRecs) continue;
         const int lin = int(d.y & 511u);
         n_upd += fold_one<true>(c, f, g, pool + uint64_t(d.x) * kBlockVoxels + lin,
                                 center_of(block_keys[d.x], lin, c.nu), sc, bucket + d.z, d.w);
@@ -1577,7 +1578,7 @@ void set_rec_cap(svx_map* m, uint32_t cap) {
     if (m->records.n != had)  // (re)allocated: contents undefined
         SVX_CUDA(cudaMemsetAsync(m->records.p, 0xFF, 8ull * m->records.n, m->stream));
     m->bucket.alloc(cap);
-    m->fbdesc.alloc(cap);
+    m->fbdesc.alloc(uint64_t(cap) * kMaxG);  // [frame of the group][cap]
     m->rec_cap = cap;
     size_t bytes = 0;  // the radix sort's scratch for every bit range (allocated here, not per group)
     SVX_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, m->records.p, m->bucket.p, int(cap), 0, 64, m->stream));
@@ -1816,12 +1817,12 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
     for (int i = f0; i < n; ++i) commit(i);
     m->n_blocks = m->h_ctr[C_BLOCKS];
     // the record capacity follows use: the per-group sort covers all of it, so after a batch
-    // it shrinks to 1.25x the batch's largest group (+ slack); a larger group later costs
-    // one rollback and retry with a grown buffer (above)
+    // whose largest group used less than a third of it, it shrinks to 1.5x that group
+    // (+ slack); a larger group later costs one rollback and retry with a grown buffer
     uint32_t hwm = 0;
     for (int i = 0; i < n; ++i) hwm = std::max(hwm, m->h_outs[i].records);
-    const uint64_t want = (uint64_t(hwm) + hwm / 4 + 8192 + 4095) & ~uint64_t(4095);
-    if (!m->test_rec_cap && want < m->rec_cap) m->rec_cap = uint32_t(want);
+    const uint64_t want = (uint64_t(hwm) + hwm / 2 + 16384 + 4095) & ~uint64_t(4095);
+    if (!m->test_rec_cap && 3 * uint64_t(hwm) < m->rec_cap && want < m->rec_cap) m->rec_cap = uint32_t(want);
 }
 
 namespace {
