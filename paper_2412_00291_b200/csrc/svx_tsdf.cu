@@ -631,7 +631,12 @@ __device__ __forceinline__ uint32_t fold_one(const GroupConsts& c, const FramePo
 // (= ascending pixel) order and sums them as the reference does (tsdf_integrator.cpp:
 // 235-236): the serial part per record is the accumulation, not the measurement. Returns 1
 // on lane 0 when the voxel was updated.
-constexpr uint32_t kWarpRecs = 8;  // descriptors with more records than this take a warp
+#ifndef SVX_WARP_RECS
+#define SVX_WARP_RECS 1
+#endif
+// descriptors with more records than this take a warp (A/B: 1 beats 3 and 8 at N = 1 and
+// removes most of the fold's per-frame floor at 8 emulated ranks)
+constexpr uint32_t kWarpRecs = SVX_WARP_RECS;
 __device__ __forceinline__ uint32_t fold_records_warp(const GroupConsts& c, const FramePose& f, uint32_t g,
                                                       svx_tsdf_voxel* vp, d3 center, const ScanSlots& sc,
                                                       const unsigned long long* __restrict__ recs, uint32_t nrec,

@@ -424,3 +424,41 @@ def test_clouds_labels_batch_matches_per_frame(how):
     assert np.array_equal(st.take_dirty_blocks(1), ref.take_dirty_blocks(1))
     st.close()
     ref.close()
+
+
+def test_semantic_eligibility_after_host_writes_and_load(tmp_path):
+    """The semantic pass's cached per-voxel pre-tests (W > 0, D >= -tau/2) stay exact
+    across TSDF writes from the host (block writes that flip voxels across both tests) and
+    an SVOX1 load: GPU and oracle apply the same writes and label images."""
+    wl = W.make("tiny", 4)
+    g, o = _run_pair(wl, svx.IntegratorConfig(), frames=[0, 1])
+    keys = np.asarray(g.block_keys_sorted())[:6]
+    rng = np.random.default_rng(7)
+    for b in keys:
+        b = tuple(int(x) for x in b)
+        t, _ = g.read_block(b)
+        t = t.copy()
+        sel = rng.random(512) < 0.3
+        t["weight"][sel] = np.where(rng.random(sel.sum()) < 0.5, 0.0, 2.0).astype(np.float32)
+        t["distance"][sel] = rng.uniform(-0.5, 0.5, sel.sum()).astype(np.float32)
+        g.write_block(b, t)
+        o.write_block(b, t)
+    si = svx.SemanticIntegrator(g)
+    for li in wl.label_images(2):
+        assert si.integrate_labels(li).updated_voxels == o.integrate_labels(li, svx.SemanticConfig()).updated_voxels
+    compare_maps(g.save_bytes(), o.save_bytes())
+    # round trip through SVOX1, then more TSDF frames and label images on the loaded map
+    path = tmp_path / "m.svox"
+    g.save(str(path))
+    h = svx.VoxelStore.load(str(path), 0)
+    ti, sh = svx.TsdfIntegrator(h, svx.IntegratorConfig()), svx.SemanticIntegrator(h)
+    oi = o
+    for p, i in wl.scans(frames=[2, 3]):
+        p = p.numpy()
+        ti.integrate_cloud(p, wl.pose(i), wl.model)
+        d, hh, n, v, _ = ob.OracleMap.project(wl.model, p, wl.pose(i))
+        oi.integrate(wl.model, d, n, v, wl.pose(i), svx.IntegratorConfig())
+        for li in wl.label_images(i):
+            assert sh.integrate_labels(li).updated_voxels == \
+                oi.integrate_labels(li, svx.SemanticConfig()).updated_voxels
+    compare_maps(h.save_bytes(), oi.save_bytes())
