@@ -288,6 +288,48 @@ __host__ __device__ inline int local_linear(int32_t x, int32_t y, int32_t z) {
     return (x & 7) + 8 * (y & 7) + 64 * (z & 7);
 }
 
+// ---- exact f32 results from one-reciprocal estimates
+// The reference stores float(x / y) (or float(clamp(x / y))) of a correctly rounded double
+// quotient. An estimate q with |q - fl(x / y)| <= kQuotTol |q| decides that float whenever
+// both ends of [q - kQuotTol |q|, q + kQuotTol |q|] round to the same float (rounding is
+// monotonic); otherwise the exact division is used. The estimates below are within ~5 ulp
+// (2^-52 relative each): kQuotTol = 4e-15 is ~18 ulp. Undecided cases need the exact
+// double to lie within 4e-15 of a float rounding boundary (relative spacing 6e-8).
+constexpr double kQuotTol = 4e-15;
+
+// 1 / b for 1e-300 < b < 1e300: hardware estimate + two Newton steps (rel. error ~2^-52).
+__device__ __forceinline__ double rcp_est(double b) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+    double e = __fma_rn(-b, r, 1.0);
+    r = __fma_rn(r, e, r);
+    e = __fma_rn(-b, r, 1.0);
+    return __fma_rn(r, e, r);
+}
+
+// float(x / y) for y > 0.
+__device__ __forceinline__ float f32_div(double x, double y) {
+    if (y > 1e-300 && y < 1e300) {
+        const double q = x * rcp_est(y), d = fabs(q) * kQuotTol;
+        const float lo = float(q - d), hi = float(q + d);
+        if (__float_as_uint(lo) == __float_as_uint(hi)) return lo;
+    }
+    return float(x / y);
+}
+
+// float(x) from an estimate q with |q - x| <= kQuotTol |q| (<= 36 ulps of q), decided with
+// one conversion: x and q round to the same float unless a rounding midpoint between two
+// floats lies within the error interval. Within q's binade those midpoints are exactly the
+// doubles whose 29 low mantissa bits equal 2^28 (the midpoint below a power of two included),
+// so q decides when its low bits are more than 64 ulps away from that pattern. Normal-range
+// results only (|q| in [1.2e-38, 1e38]), and q = 0 (an exact zero numerator).
+__device__ __forceinline__ bool f32_of_est(double q, float& f) {
+    const int32_t dist = int32_t(uint32_t(__double2loint(q)) & 0x1FFFFFFFu) - 0x10000000;
+    const double aq = fabs(q);
+    f = float(q);
+    return (q == 0.0) || (aq > 1.2e-38 && aq < 1e38 && (dist > 64 || dist < -64));
+}
+
 // ----------------------------------------------------------------- hash
 struct HashView {
     uint64_t* keys;  // kEmptyKey = free

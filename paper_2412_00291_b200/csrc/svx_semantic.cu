@@ -228,8 +228,32 @@ struct Like {
     }
 };
 
-__device__ inline Like make_like(const SemBatch& sb, const ImgParams& ip, uint32_t px, int K) {
+// label_to_likelihood's two quotients for every label of an image without a confidence
+// map or a tensor (they depend on the label only): lut[1 + l] = (lb, lt) for l in [-1, K),
+// l = -1 for a label outside [0, K). The same f32 operations as make_like.
+constexpr int kLutK = 32;  // classes covered by the shared-memory table
+__device__ inline float2 label_quotients(const SemBatch& sb, float cf, int label, int K) {
+    float base = K > 1 ? (1.f - cf) / float(K - 1) : 1.f;
+    float top = K > 1 ? cf : 1.f;
+    base = base < sb.floor_v ? sb.floor_v : base;
+    top = top < sb.floor_v ? sb.floor_v : top;
+    float sum = 0.f;
+    for (int k = 0; k < K; ++k) sum += (k == label) ? top : base;
+    return make_float2(base / sum, top / sum);
+}
+
+__device__ inline Like make_like(const SemBatch& sb, const ImgParams& ip, uint32_t px, int K,
+                                 const float2* __restrict__ lut) {
     Like like{nullptr, sb.floor_v, 0.f, 0.f, -1, 0.f};
+    if (lut) {
+        int label = int(ip.labels[px]);
+        if (!(label < K)) label = -1;
+        const float2 q = lut[1 + label];
+        like.label = label;
+        like.lb = q.x;
+        like.lt = q.y;
+        return like;
+    }
     if (ip.has_tensor) {
         like.tp = ip.tensor + uint64_t(px) * K;
         for (int k = 0; k < K; ++k) {
@@ -263,7 +287,9 @@ __device__ inline void bayes_regs(Probs<KC>& p, const Like& like, bool use_bayes
             p.v[k] = p.v[k] * like(k);
             z += double(p.v[k]);
         }
-        const float inv = float(1.0 / z);
+        // float(1 / z) from the reciprocal estimate when it decides the float
+        float inv;
+        if (!(z > 1e-300 && z < 1e300 && f32_of_est(rcp_est(z), inv))) inv = float(1.0 / z);
 #pragma unroll
         for (int k = 0; k < KC; ++k) p.v[k] = p.v[k] * inv;
     } else {
@@ -352,6 +378,16 @@ k_sem_update(const __grid_constant__ SemBatch sb, HashView h, const uint64_t* __
     // kernel outgrows the instruction cache)
     __shared__ uint32_t s_pix[kThreads / 32][kMaxImg][32];
     uint32_t (*pix)[32] = s_pix[threadIdx.x >> 5];
+    // label-only likelihood quotients per image (no confidence map, no tensor)
+    __shared__ float2 s_lut[kMaxImg][kLutK + 1];
+    const bool lut_ok = K <= kLutK;
+    if (lut_ok) {
+        for (int e = threadIdx.x; e < n_apply * (K + 1); e += blockDim.x) {
+            const int i = e / (K + 1), l = e % (K + 1) - 1;
+            s_lut[i][l + 1] = label_quotients(sb, sb.default_conf, l, K);
+        }
+    }
+    __syncthreads();
     uint32_t n_upd = 0;  // lane i < n_apply: voxels image i updated
     for (uint32_t t = warp; t < kParts * n_cand; t += nwarps) {
         const uint2 cd = cand[t / kParts];
@@ -369,8 +405,23 @@ k_sem_update(const __grid_constant__ SemBatch sb, HashView h, const uint64_t* __
                 const ImgParams& ip = sb.img[i];
                 const d3 pc = xform(ip.w2c, c);
                 if (pc.z <= 0.0 || pc.z > ip.max_depth) continue;
-                const int u = int(floor(ip.fx * pc.x / pc.z + ip.cx));
-                const int vv = int(floor(ip.fy * pc.y / pc.z + ip.cy));
+                // u = floor(fx x / z + cx), v = floor(fy y / z + cy) (semantic_integrator.cpp:
+                // 117-121) from one reciprocal of z: the estimates are within ~3 ulp of the
+                // reference's quotients, so floor() is decided unless an estimate lies within
+                // the bound of an integer; then the reference's divisions are evaluated
+                int u, vv;
+                {
+                    const double rz = rcp_est(pc.z);
+                    const double bu = ip.fx * pc.x * rz, bv = ip.fy * pc.y * rz;
+                    const double cu = bu + ip.cx, cv = bv + ip.cy;
+                    const double eu = 1e-15 * (fabs(bu) + fabs(cu)) + 1e-300;
+                    const double ev = 1e-15 * (fabs(bv) + fabs(cv)) + 1e-300;
+                    const double fu = floor(cu), fv = floor(cv);
+                    if (cu - eu >= fu && cu + eu < fu + 1.0) u = int(fu);
+                    else u = int(floor(ip.fx * pc.x / pc.z + ip.cx));
+                    if (cv - ev >= fv && cv + ev < fv + 1.0) vv = int(fv);
+                    else vv = int(floor(ip.fy * pc.y / pc.z + ip.cy));
+                }
                 if (u < 0 || u >= ip.W || vv < 0 || vv >= ip.H) continue;
                 if (sb.raycast && occluded_along_ray(sb, ip.cam_o, h, pool, c)) continue;
                 pix[i][lane] = uint32_t(vv) * uint32_t(ip.W) + uint32_t(u);
@@ -422,14 +473,18 @@ k_sem_update(const __grid_constant__ SemBatch sb, HashView h, const uint64_t* __
 #pragma unroll 1
                 for (uint32_t r = pass; r; r &= r - 1) {
                     const int i = __ffs(r) - 1;
-                    bayes_regs<KC>(p, make_like(sb, sb.img[i], pix[i][lane], K), sb.use_bayes != 0);
+                    const ImgParams& ip = sb.img[i];
+                    const float2* lut = (lut_ok && !ip.has_tensor && !ip.has_conf) ? s_lut[i] : nullptr;
+                    bayes_regs<KC>(p, make_like(sb, ip, pix[i][lane], K, lut), sb.use_bayes != 0);
                 }
                 p.store(probs);
             } else {
 #pragma unroll 1
                 for (uint32_t r = pass; r; r &= r - 1) {
                     const int i = __ffs(r) - 1;
-                    bayes_mem(probs, make_like(sb, sb.img[i], pix[i][lane], K), K, sb.use_bayes != 0);
+                    const ImgParams& ip = sb.img[i];
+                    const float2* lut = (lut_ok && !ip.has_tensor && !ip.has_conf) ? s_lut[i] : nullptr;
+                    bayes_mem(probs, make_like(sb, ip, pix[i][lane], K, lut), K, sb.use_bayes != 0);
                 }
             }
         }

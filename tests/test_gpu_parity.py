@@ -432,7 +432,7 @@ def test_semantic_eligibility_after_host_writes_and_load(tmp_path):
     an SVOX1 load: GPU and oracle apply the same writes and label images."""
     wl = W.make("tiny", 4)
     g, o = _run_pair(wl, svx.IntegratorConfig(), frames=[0, 1])
-    keys = np.asarray(g.block_keys_sorted())[:6]
+    keys = np.asarray(g.block_coords_sorted())[:6]
     rng = np.random.default_rng(7)
     for b in keys:
         b = tuple(int(x) for x in b)
