@@ -166,7 +166,7 @@ svx_map* create_map(const svx_map_cfg& cfg, int device) {
         m->d_ctr = dmalloc<uint32_t>(kNumCounters);
         // fallback records per group: sized by use (grown on overflow, the group retried);
         // the per-group sort covers the whole buffer
-        uint32_t rec_cap = 1u << 18;
+        uint32_t rec_cap = 1u << 16;
         // test hook: tiny buffers exercise the abort-and-resume paths
         if (const char* e = std::getenv("SVX_TEST_REC_CAP")) {
             rec_cap = uint32_t(std::max(1L, std::atol(e)));

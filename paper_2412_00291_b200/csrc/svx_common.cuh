@@ -307,6 +307,18 @@ __device__ __forceinline__ double rcp_est(double b) {
     return __fma_rn(r, e, r);
 }
 
+// 1 / sqrt(x) for 1e-300 < x < 1e300: hardware estimate + two Newton steps (rel. error
+// within ~3 ulp; no special-case handling: callers guarantee the range).
+__device__ __forceinline__ double rsqrt_est(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double hx = 0.5 * x;
+    double r = __fma_rn(-(hx * y), y, 0.5);
+    y = __fma_rn(y, r, y);
+    r = __fma_rn(-(hx * y), y, 0.5);
+    return __fma_rn(y, r, y);
+}
+
 // float(x / y) for y > 0.
 __device__ __forceinline__ float f32_div(double x, double y) {
     if (y > 1e-300 && y < 1e300) {
@@ -322,12 +334,16 @@ __device__ __forceinline__ float f32_div(double x, double y) {
 // floats lies within the error interval. Within q's binade those midpoints are exactly the
 // doubles whose 29 low mantissa bits equal 2^28 (the midpoint below a power of two included),
 // so q decides when its low bits are more than 64 ulps away from that pattern. Normal-range
-// results only (|q| in [1.2e-38, 1e38]), and q = 0 (an exact zero numerator).
+// results only (2^-126 <= |q| < 2^127, tested on the biased exponent), and q = 0 (an exact
+// zero numerator). Integer tests only: no FP64 compares.
 __device__ __forceinline__ bool f32_of_est(double q, float& f) {
-    const int32_t dist = int32_t(uint32_t(__double2loint(q)) & 0x1FFFFFFFu) - 0x10000000;
-    const double aq = fabs(q);
+    const uint32_t hi = uint32_t(__double2hiint(q)), lo = uint32_t(__double2loint(q));
+    const uint32_t e = (hi >> 20) & 0x7FFu;                 // 1023 + exponent
+    const bool normal = e - 897u <= 1149u - 897u;           // 2^-126 <= |q| < 2^127
+    const uint32_t dist = (lo & 0x1FFFFFFFu) - 0x10000000u;   // low bits - the midpoint pattern
+    const bool far = dist + 64u > 128u;                     // |dist| > 64 (two's complement)
     f = float(q);
-    return (q == 0.0) || (aq > 1.2e-38 && aq < 1e38 && (dist > 64 || dist < -64));
+    return (normal && far) || ((hi & 0x7FFFFFFFu) | lo) == 0u;
 }
 
 // ----------------------------------------------------------------- hash

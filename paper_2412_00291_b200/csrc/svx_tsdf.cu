@@ -264,7 +264,7 @@ __device__ inline float truncate_f(double d, double tau) {
 // is at most |x'^2 - x^2| / sqrt(1 - x'^2) <= 2.1 kDot / sqrt(1 - x'^2).
 // Returns false when undecided; the caller then evaluates the reference formula from the
 // reference's own ct, ca (gamma_reference).
-constexpr double kDot = 2e-15;
+constexpr double kDot = 3e-15;
 __device__ __forceinline__ bool gamma_fast(const GroupConsts& c, double psi, double ct, double ca, float& out) {
     constexpr double kAbs = 2e-15 + kDot, kRel = 4e-15;  // kRel: libm + our rsqrt-based roots
     double d, e;
@@ -274,7 +274,7 @@ __device__ __forceinline__ bool gamma_fast(const GroupConsts& c, double psi, dou
     } else if (ca < c.ca_lo) {
         const double tt = (1.0 - ct) * (1.0 + ct), ss = (1.0 - ca) * (1.0 + ca);
         if (!(tt > 1e-14 && ss > 1e-12)) return false;  // sin theta < 1e-7 or sin alpha < 1e-6
-        const double rt = rsqrt(tt), inv_sa = rsqrt(ss);  // (<= 1 ulp each)
+        const double rt = rsqrt_est(tt), inv_sa = rsqrt_est(ss);  // (<= 3 ulp each)
         const double st = tt * rt, sa = ss * inv_sa;
         const double a = ca - 1.0;
         const double t1 = fabs(a * st * inv_sa), t2 = fabs(ct * psi);
@@ -497,7 +497,7 @@ __device__ __forceinline__ uint32_t fold_own_fast(const GroupConsts& c, d3 origi
         const bool use_g = vox.weight > 0.f && gsq > 1e-12f;
         const d3 g0 = mk(use_g ? vox.gradient[0] : nw0, use_g ? vox.gradient[1] : nw1, use_g ? vox.gradient[2] : nw2);
         const double gz = dot3(g0, g0);
-        const d3 gd = gz > 0.0 ? scale3(rsqrt(gz), g0) : g0;  // within kDot (gamma_fast)
+        const d3 gd = gz > 1e-300 ? scale3(rsqrt_est(gz), g0) : (gz > 0.0 ? scale3(rsqrt(gz), g0) : g0);  // within kDot
         double ct = dot3(neg3(ray), gd);
         ct = fmin(fmax(ct, -1.0), 1.0);
         double ca = dot3(gd, mk(nw0, nw1, nw2));
@@ -543,7 +543,7 @@ __device__ __forceinline__ uint32_t fold_own_fast(const GroupConsts& c, d3 origi
     const bool upd = s2 > 1.0000001e-24;
     ok = ok && (upd || s2 < 0.9999999e-24) && s2 < 1e300;
     if (upd) {
-        const double r = rsqrt(s2);
+        const double r = rsqrt_est(s2);
         const bool g0 = f32_of_est(bx * r, out.gradient[0]);
         const bool g1 = f32_of_est(by * r, out.gradient[1]);
         const bool g2 = f32_of_est(bz * r, out.gradient[2]);
@@ -1780,12 +1780,12 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
     for (int i = f0; i < n; ++i) commit(i);
     m->n_blocks = m->h_ctr[C_BLOCKS];
     // the record capacity follows use: the per-group sort covers all of it, so after a batch
-    // whose largest group used less than a third of it, it shrinks to 1.5x that group
-    // (+ slack); a larger group later costs one rollback and retry with a grown buffer
+    // whose largest group used less than half of it, it shrinks to 1.5x that group (+ slack);
+    // a larger group later costs one rollback and retry with a grown buffer
     uint32_t hwm = 0;
     for (int i = 0; i < n; ++i) hwm = std::max(hwm, m->h_outs[i].records);
-    const uint64_t want = (uint64_t(hwm) + hwm / 2 + 16384 + 4095) & ~uint64_t(4095);
-    if (!m->test_rec_cap && 3 * uint64_t(hwm) < m->rec_cap && want < m->rec_cap) m->rec_cap = uint32_t(want);
+    const uint64_t want = (uint64_t(hwm) + hwm / 2 + 8192 + 4095) & ~uint64_t(4095);
+    if (!m->test_rec_cap && 2 * uint64_t(hwm) < m->rec_cap && want < m->rec_cap) m->rec_cap = uint32_t(want);
 }
 
 namespace {
