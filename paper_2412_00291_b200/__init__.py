@@ -123,7 +123,7 @@ class ProfileC(C.Structure):
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("ms", "launches", "aborts")}
-        names = ["pool", "capacity", "key", "hash", "records", "b5", "voxel_list", "b7"]
+        names = ["pool", "capacity", "key", "hash", "records", "exchange", "voxel_list", "b7"]
         d["aborts"] = {names[i]: self.aborts[i] for i in range(8) if self.aborts[i]}
         d["ms"] = {K_NAMES[i]: self.ms[i] for i in range(8) if self.launches[i]}
         d["launches"] = {K_NAMES[i]: self.launches[i] for i in range(8) if self.launches[i]}

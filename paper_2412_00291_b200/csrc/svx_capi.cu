@@ -96,7 +96,7 @@ void free_map(svx_map* m) {
     cudaSetDevice(m->device);
     if (m->stream) cudaStreamSynchronize(m->stream);
     for (void* p : {(void*)m->keys, (void*)m->vals, (void*)m->block_keys, (void*)m->sem_idx,
-                    (void*)m->dirty, (void*)m->stamp, (void*)m->touched, (void*)m->fctr,
+                    (void*)m->dirty, (void*)m->fbcnt, (void*)m->fbstart, (void*)m->fbfill, (void*)m->fbblocks, (void*)m->stamp, (void*)m->touched, (void*)m->fctr,
                     (void*)m->d_ctr})
         if (p) cudaFree(p);
     if (m->h_ctr) cudaFreeHost(m->h_ctr);
@@ -104,6 +104,7 @@ void free_map(svx_map* m) {
     if (m->h_outs) cudaFreeHost(m->h_outs);
     m->outs.release();
     m->bucket.release();
+    m->bucket2.release();
     m->fb_tmp.release();
     m->fbdesc.release();
     m->xsend.release();
@@ -163,6 +164,10 @@ svx_map* create_map(const svx_map_cfg& cfg, int device) {
         m->block_keys = dmalloc<uint64_t>(cfg.max_blocks);
         m->sem_idx = dmalloc<uint32_t>(cfg.max_blocks);
         m->dirty = dmalloc<uint8_t>(2ull * cfg.max_blocks);
+        m->fbcnt = dmalloc<uint32_t>(cfg.max_blocks);
+        m->fbstart = dmalloc<uint32_t>(cfg.max_blocks);
+        m->fbfill = dmalloc<uint32_t>(cfg.max_blocks);
+        m->fbblocks = dmalloc<uint32_t>(cfg.max_blocks);
         m->d_ctr = dmalloc<uint32_t>(kNumCounters);
         // fallback records per group: sized by use (grown on overflow, the group retried);
         // the per-group sort covers the whole buffer
@@ -174,6 +179,7 @@ svx_map* create_map(const svx_map_cfg& cfg, int device) {
         }
         if (const char* e = std::getenv("SVX_TEST_POOL_HEAD")) m->test_pool_head = uint64_t(std::max(1L, std::atol(e)));
         set_rec_cap(m, rec_cap);
+        m->fb_global = std::getenv("SVX_FB_GLOBAL") != nullptr;  // A/B: the global radix sort
         SVX_CUDA(cudaMallocHost(&m->h_ctr, sizeof(uint32_t) * kNumCounters));
         SVX_CUDA(cudaMallocHost(&m->h_fctr, sizeof(uint32_t) * kMaxG * kFC));
         std::memset(m->h_ctr, 0, sizeof(uint32_t) * kNumCounters);
@@ -183,6 +189,8 @@ svx_map* create_map(const svx_map_cfg& cfg, int device) {
         SVX_CUDA(cudaMemsetAsync(m->fctr, 0, 4ull * kMaxG * kFC, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->sem_idx, 0xFF, 4ull * cfg.max_blocks, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->dirty, 0, 2ull * cfg.max_blocks, m->stream));
+        SVX_CUDA(cudaMemsetAsync(m->fbcnt, 0, 4ull * cfg.max_blocks, m->stream));
+        SVX_CUDA(cudaMemsetAsync(m->fbfill, 0, 4ull * cfg.max_blocks, m->stream));
         SVX_CUDA(cudaMemsetAsync(m->d_ctr, 0, sizeof(uint32_t) * kNumCounters, m->stream));
         m->block_bytes = sizeof(svx_tsdf_voxel) * kBlockVoxels;
         m->layer_bytes = sizeof(float) * kBlockVoxels * size_t(cfg.num_labels);

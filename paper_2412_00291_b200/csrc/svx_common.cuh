@@ -401,6 +401,8 @@ enum Counter : int {
     C_BLOCKS_BEFORE = 17,  // C_BLOCKS at the start of the current frame group
     C_MAPPED = 18,      // blocks with pool + visit-mask memory mapped (host-written)
     C_DONE = 24,        // CTAs of k_fold finished (the last one writes the group's reports)
+    C_FB_BLOCKS = 25,   // blocks holding fallback records this group (per-block ordering)
+    C_BUCKET_TOP = 26,  // fallback bucket space handed out this group
     kNumCounters = 32
 };
 

@@ -207,7 +207,14 @@ struct svx_map {
     svx::DevBuf<unsigned long long> records;
     svx::DevBuf<unsigned long long> records_alt;  // capacity path: visited block keys
     svx::DevBuf<uint8_t> sort_tmp;
-    svx::DevBuf<unsigned long long> bucket;  // the records, sorted
+    svx::DevBuf<unsigned long long> bucket, bucket2;  // the records, sorted (+ merge scratch)
+    // per-block ordering (the default): per pool block its record count, bucket start and
+    // fill cursor, and the list of blocks holding records ([max_blocks] each)
+    uint32_t* fbcnt = nullptr;
+    uint32_t* fbstart = nullptr;
+    uint32_t* fbfill = nullptr;
+    uint32_t* fbblocks = nullptr;
+    bool fb_global = false;          // order the records with the global radix sort (SVX_FB_GLOBAL=1)
     svx::DevBuf<uint8_t> fb_tmp;
     svx::DevBuf<uint4> fbdesc;       // fallback voxels: pool idx, voxel | frame << 16, records start, count
     uint32_t rec_cap = 0;            // fallback records per group (the sort's size)

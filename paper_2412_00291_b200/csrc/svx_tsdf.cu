@@ -40,6 +40,7 @@
 // rolls the aborted group back (its blocks, hash entries and masks) and retries it
 // (CapacityError and key-range errors: frame by frame, reproducing the reference's
 // per-frame behaviour).
+#include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <math_constants.h>
@@ -1090,6 +1091,147 @@ k_fb_runs(const unsigned long long* __restrict__ sorted, unsigned long long* __r
     }
 }
 
+// ---- ordering of the fallback records: counted per block, bucketed per block, and each
+// bucket sorted by one CTA (k_fb_sort): four PDL-chained kernels, one pass over the records
+// each. (The global radix sort over the record buffer, CUB + k_fb_runs, is kept as an
+// alternative: SVX_FB_GLOBAL=1.)
+constexpr int kFbSortItems = 8;
+constexpr uint32_t kFbSortMax = kThreads * kFbSortItems;  // records per block one CTA sorts
+
+__global__ void __launch_bounds__(kThreads)
+k_fb_count(const unsigned long long* __restrict__ rec, uint32_t rec_cap, uint32_t pb, uint32_t* __restrict__ fbcnt,
+           uint32_t* __restrict__ fbblocks, uint32_t* __restrict__ ctr) {
+    pdl_wait();
+    pdl_trigger();
+    if (ctr[C_ABORT]) return;
+    const uint32_t n = min(ctr[C_RECORDS], rec_cap);
+    const int lane = threadIdx.x & 31;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t idx = uint32_t(rec[i] >> (pb + 13));
+        // one atomic per distinct block among the warp's lanes (a tile's records of a block
+        // are adjacent; a block many rays cross would serialise per-record atomics)
+        const unsigned grp = __match_any_sync(__activemask(), idx);
+        if (lane == __ffs(grp) - 1 && atomicAdd(&fbcnt[idx], uint32_t(__popc(grp))) == 0u)
+            fbblocks[atomicAdd(&ctr[C_FB_BLOCKS], 1u)] = idx;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_fb_alloc(const uint32_t* __restrict__ fbcnt, const uint32_t* __restrict__ fbblocks, uint32_t* __restrict__ fbstart,
+           uint32_t* __restrict__ ctr) {
+    pdl_wait();
+    pdl_trigger();
+    if (ctr[C_ABORT]) return;
+    const uint32_t nb = ctr[C_FB_BLOCKS];
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nb; t += gridDim.x * blockDim.x) {
+        const uint32_t idx = fbblocks[t], cnt = fbcnt[idx];
+        fbstart[idx] = atomicAdd(&ctr[C_BUCKET_TOP], cnt);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_fb_bucket(unsigned long long* __restrict__ rec, uint32_t rec_cap, uint32_t pb, const uint32_t* __restrict__ fbstart,
+            uint32_t* __restrict__ fbfill, unsigned long long* __restrict__ bucket, uint32_t* __restrict__ ctr) {
+    pdl_wait();
+    pdl_trigger();
+    if (ctr[C_ABORT]) return;
+    const uint32_t n = min(ctr[C_RECORDS], rec_cap);
+    const int lane = threadIdx.x & 31;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const unsigned long long r = rec[i];
+        rec[i] = ~0ull;  // the record buffer holds the padding key outside a group's entries
+        const uint32_t idx = uint32_t(r >> (pb + 13));
+        const unsigned grp = __match_any_sync(__activemask(), idx);
+        const int leader = __ffs(grp) - 1;
+        uint32_t base = 0;
+        if (lane == leader) base = fbstart[idx] + atomicAdd(&fbfill[idx], uint32_t(__popc(grp)));
+        base = __shfl_sync(grp, base, leader);
+        bucket[base + uint32_t(__popc(grp & ((1u << lane) - 1u)))] = r;
+    }
+}
+
+// CTA per block with records: its bucket sorted by (voxel, frame, pixel) - in shared memory
+// (cub::BlockRadixSort) when it holds at most kFbSortMax records, else as sorted 2048-record
+// tiles merged pairwise through the scratch buffer (each record's rank in the other run by
+// binary search: keys are unique, a ray visits a voxel once per frame) - then one
+// descriptor per (voxel, frame) run - per frame the reference's ascending (v, u) visit order
+// (.cpp:141-146,215-216) - into the frame's list.
+__global__ void __launch_bounds__(kThreads)
+k_fb_sort(const uint32_t* __restrict__ fbblocks, uint32_t* __restrict__ fbcnt, const uint32_t* __restrict__ fbstart,
+          uint32_t* __restrict__ fbfill, unsigned long long* __restrict__ bucket, unsigned long long* __restrict__ scratch,
+          uint32_t pb, uint32_t rec_cap, uint4* __restrict__ fbdesc, uint32_t* __restrict__ fctr,
+          uint32_t* __restrict__ ctr) {
+    pdl_wait();
+    pdl_trigger();
+    if (cta_aborted(ctr)) return;
+    using Sort = cub::BlockRadixSort<unsigned long long, kThreads, kFbSortItems>;
+    __shared__ typename Sort::TempStorage tmp;
+    const uint32_t nb = ctr[C_FB_BLOCKS];
+    const int end_bit = int(pb) + 13;
+    for (uint32_t t = blockIdx.x; t < nb; t += gridDim.x) {
+        const uint32_t idx = fbblocks[t];
+        const uint32_t cnt = fbcnt[idx], start = fbstart[idx];
+        unsigned long long* bk = bucket + start;
+        // sorted tiles of kFbSortMax records (one tile: the whole bucket)
+        for (uint32_t t0 = 0; t0 < cnt; t0 += kFbSortMax) {
+            unsigned long long k[kFbSortItems];
+#pragma unroll
+            for (int j = 0; j < kFbSortItems; ++j) {
+                const uint32_t pos = t0 + threadIdx.x * kFbSortItems + j;  // blocked arrangement
+                k[j] = pos < cnt ? bk[pos] : ~0ull;  // padding sorts last (the sort is stable)
+            }
+            Sort(tmp).Sort(k, 0, end_bit);
+#pragma unroll
+            for (int j = 0; j < kFbSortItems; ++j) {
+                const uint32_t pos = t0 + threadIdx.x * kFbSortItems + j;
+                if (pos < cnt) bk[pos] = k[j];
+            }
+            __syncthreads();  // tmp reused; the tile's writes visible to the CTA
+        }
+        // merge passes for a bucket of several tiles (rare: a block many rays cross)
+        if (cnt > kFbSortMax) {
+            unsigned long long* src = bk;
+            unsigned long long* dst = scratch + start;
+            for (uint32_t w = kFbSortMax; w < cnt; w *= 2) {
+                for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
+                    const uint32_t p0 = (i / (2 * w)) * (2 * w);
+                    const uint32_t a1 = min(p0 + w, cnt), b1 = min(p0 + 2 * w, cnt);
+                    const unsigned long long key = src[i];
+                    // rank of key in the other run: lower bound (unique keys)
+                    uint32_t lo, hi;
+                    if (i < a1) { lo = a1; hi = b1; } else { lo = p0; hi = a1; }
+                    const uint32_t base = lo;
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (src[mid] < key) lo = mid + 1; else hi = mid;
+                    }
+                    const uint32_t own = i < a1 ? i - p0 : i - a1;
+                    dst[p0 + own + (lo - base)] = key;
+                }
+                __syncthreads();
+                unsigned long long* x = src;
+                src = dst;
+                dst = x;
+            }
+            if (src != bk) {
+                for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) bk[i] = src[i];
+                __syncthreads();
+            }
+        }
+        for (uint32_t pos = threadIdx.x; pos < cnt; pos += kThreads) {
+            const unsigned long long run = bk[pos] >> pb;  // (block, voxel, frame)
+            if (pos > 0 && (bk[pos - 1] >> pb) == run) continue;
+            uint32_t e = pos + 1;
+            while (e < cnt && (bk[e] >> pb) == run) ++e;
+            const uint32_t g = uint32_t(run) & 15u, lin = uint32_t(run >> 4) & 511u;
+            fbdesc[uint64_t(g) * rec_cap + atomicAdd(&fctr[g * kFC + FC_FBV], 1u)] =
+                make_uint4(idx, lin | (g << 16), start + pos, e - pos);
+        }
+        if (threadIdx.x == 0) fbcnt[idx] = fbfill[idx] = 0u;  // clean for the next group
+        __syncthreads();
+    }
+}
+
 // Frame g of the group: one thread per listed visited voxel of the frame (grid-stride, one
 // wave of CTAs), then the group's fallback descriptors of frame g; each applies frame g to
 // its voxel, whose state then holds frames 0..g, as after the reference's g + 1
@@ -1207,7 +1349,7 @@ k_fold(const __grid_constant__ GroupConsts c, const __grid_constant__ FramePose 
     }
     if (threadIdx.x == 0) {
         ctr[C_DONE] = 0;
-        ctr[C_TOUCHED] = ctr[C_RECORDS] = ctr[C_FB_VOXELS] = 0;
+        ctr[C_TOUCHED] = ctr[C_RECORDS] = ctr[C_FB_VOXELS] = ctr[C_FB_BLOCKS] = ctr[C_BUCKET_TOP] = 0;
         ctr[C_BLOCKS_BEFORE] = ctr[C_BLOCKS];
     }
 }
@@ -1430,6 +1572,19 @@ void launch_fold_kernels(svx_map* m, svx_scan* s, const GroupParams& gp, FrameOu
     uint32_t* fm = mask_base(m);
     {
         ProfMark pm(m, SVX_K_FALLBACK);
+      if (!m->fb_global) {  // per-block ordering (the default)
+        const unsigned eg = pg / 2;
+        launch_pdl(k_fb_count, eg, kThreads, m->stream, static_cast<const unsigned long long*>(m->records.p),
+                   c.rec_cap, c.pbits, m->fbcnt, m->fbblocks, m->d_ctr);
+        launch_pdl(k_fb_alloc, 64u, kThreads, m->stream, static_cast<const uint32_t*>(m->fbcnt),
+                   static_cast<const uint32_t*>(m->fbblocks), m->fbstart, m->d_ctr);
+        launch_pdl(k_fb_bucket, eg, kThreads, m->stream, m->records.p, c.rec_cap, c.pbits,
+                   static_cast<const uint32_t*>(m->fbstart), m->fbfill, m->bucket.p, m->d_ctr);
+        launch_pdl(k_fb_sort, pg / 4, kThreads, m->stream, static_cast<const uint32_t*>(m->fbblocks), m->fbcnt,
+                   static_cast<const uint32_t*>(m->fbstart), m->fbfill, m->bucket.p, m->bucket2.p, c.pbits,
+                   c.rec_cap, m->fbdesc.p, m->fctr, m->d_ctr);
+        count_launch(4);
+      } else {
         // the group's records sorted on their (block, voxel, frame, pixel) bits: the whole
         // buffer (the unused tail holds the padding key ~0, which sorts last)
         int end_bit = int(c.pbits) + 13, ib = 1;
@@ -1444,6 +1599,7 @@ void launch_fold_kernels(svx_map* m, svx_scan* s, const GroupParams& gp, FrameOu
         launch_pdl(k_fb_runs, pg, kThreads, m->stream, m->bucket.p, m->records.p, c.rec_cap, c.pbits, m->fbdesc.p,
                    m->fctr, m->d_ctr);
         count_launch(1);
+      }
     }
     // one profiling mark spans the group's folds when nothing runs between them (marks
     // between PDL launches cost their overlap), else one per fold
@@ -1541,6 +1697,7 @@ void set_rec_cap(svx_map* m, uint32_t cap) {
     if (m->records.n != had)  // (re)allocated: contents undefined
         SVX_CUDA(cudaMemsetAsync(m->records.p, 0xFF, 8ull * m->records.n, m->stream));
     m->bucket.alloc(cap);
+    m->bucket2.alloc(cap);  // merge scratch of big buckets (k_fb_sort)
     m->fbdesc.alloc(uint64_t(cap) * kMaxG);  // [frame of the group][cap]
     m->rec_cap = cap;
     size_t bytes = 0;  // the radix sort's scratch for every bit range (allocated here, not per group)
@@ -1554,8 +1711,10 @@ void reset_frame_state(svx_map* m) {
     if (m->mapped_blocks)
         SVX_CUDA(cudaMemsetAsync(mask_base(m), 0, 4ull * kMaskWords * m->mapped_blocks, m->stream));
     SVX_CUDA(cudaMemsetAsync(m->records.p, 0xFF, 8ull * m->records.n, m->stream));  // the sort's padding
+    SVX_CUDA(cudaMemsetAsync(m->fbcnt, 0, 4ull * m->cfg.max_blocks, m->stream));
+    SVX_CUDA(cudaMemsetAsync(m->fbfill, 0, 4ull * m->cfg.max_blocks, m->stream));
     SVX_CUDA(cudaMemsetAsync(m->fctr, 0, sizeof(uint32_t) * kMaxG * kFC, m->stream));
-    for (int c : {C_TOUCHED, C_RECORDS, C_FB_VOXELS, C_ABORT, C_DONE})
+    for (int c : {C_TOUCHED, C_RECORDS, C_FB_VOXELS, C_FB_BLOCKS, C_BUCKET_TOP, C_ABORT, C_DONE})
         m->h_ctr[c] = 0;
     m->h_ctr[C_BLOCKS] = m->h_ctr[C_BLOCKS_BEFORE] = uint32_t(m->n_blocks);
     m->h_ctr[C_MAPPED] = uint32_t(m->mapped_blocks);
