@@ -1150,12 +1150,61 @@ k_fb_bucket(unsigned long long* __restrict__ rec, uint32_t rec_cap, uint32_t pb,
     }
 }
 
-// CTA per block with records: its bucket sorted by (voxel, frame, pixel) - in shared memory
-// (cub::BlockRadixSort) when it holds at most kFbSortMax records, else as sorted 2048-record
-// tiles merged pairwise through the scratch buffer (each record's rank in the other run by
-// binary search: keys are unique, a ray visits a voxel once per frame) - then one
+// Sorts n keys src[0..n) into dst[0..n) with the whole CTA (n arbitrary): sorted tiles of
+// kFbSortMax keys (cub::BlockRadixSort in shared memory), then pairwise merges of sorted runs
+// through the two buffers (each key's rank in the other run by binary search: the keys are
+// unique). Every thread of the CTA calls it with the same arguments.
+template <typename SortT>
+__device__ void cta_sort_range(typename SortT::TempStorage& tmp, unsigned long long* __restrict__ src,
+                               unsigned long long* __restrict__ dst, uint32_t n, int end_bit) {
+    for (uint32_t t0 = 0; t0 < n; t0 += kFbSortMax) {
+        unsigned long long k[kFbSortItems];
+#pragma unroll
+        for (int j = 0; j < kFbSortItems; ++j) {
+            const uint32_t pos = t0 + threadIdx.x * kFbSortItems + j;  // blocked arrangement
+            k[j] = pos < n ? src[pos] : ~0ull;  // padding sorts last (the sort is stable)
+        }
+        SortT(tmp).Sort(k, 0, end_bit);
+#pragma unroll
+        for (int j = 0; j < kFbSortItems; ++j) {
+            const uint32_t pos = t0 + threadIdx.x * kFbSortItems + j;
+            if (pos < n) dst[pos] = k[j];
+        }
+        __syncthreads();  // tmp reused; the tile visible to the CTA
+    }
+    unsigned long long* a = dst;
+    unsigned long long* b = src;
+    for (uint32_t w = kFbSortMax; w < n; w *= 2) {  // runs of w in a -> runs of 2w in b
+        for (uint32_t i = threadIdx.x; i < n; i += kThreads) {
+            const uint32_t p0 = (i / (2 * w)) * (2 * w);
+            const uint32_t a1 = min(p0 + w, n), b1 = min(p0 + 2 * w, n);
+            const unsigned long long key = a[i];
+            uint32_t lo = i < a1 ? a1 : p0, hi = i < a1 ? b1 : a1;
+            const uint32_t base = lo;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (a[mid] < key) lo = mid + 1;
+                else hi = mid;
+            }
+            b[p0 + (i < a1 ? i - p0 : i - a1) + (lo - base)] = key;
+        }
+        __syncthreads();
+        unsigned long long* x = a;
+        a = b;
+        b = x;
+    }
+    if (a != dst) {
+        for (uint32_t i = threadIdx.x; i < n; i += kThreads) dst[i] = a[i];
+        __syncthreads();
+    }
+}
+
+// CTA per block with records: its bucket sorted by (voxel, frame, pixel), then one
 // descriptor per (voxel, frame) run - per frame the reference's ascending (v, u) visit order
-// (.cpp:141-146,215-216) - into the frame's list.
+// (.cpp:141-146,215-216) - into the frame's list. A bucket of up to 256 records is ordered by
+// a rank count per record, one of up to kFbSortMax in shared memory; a larger one (a block many rays cross) is first counting-sorted
+// by voxel, then each voxel's records are ordered: up to 64 by a rank count per record, more
+// by cta_sort_range (the wall case: thousands of rays through one voxel).
 __global__ void __launch_bounds__(kThreads)
 k_fb_sort(const uint32_t* __restrict__ fbblocks, uint32_t* __restrict__ fbcnt, const uint32_t* __restrict__ fbstart,
           uint32_t* __restrict__ fbfill, unsigned long long* __restrict__ bucket, unsigned long long* __restrict__ scratch,
@@ -1165,58 +1214,64 @@ k_fb_sort(const uint32_t* __restrict__ fbblocks, uint32_t* __restrict__ fbcnt, c
     pdl_trigger();
     if (cta_aborted(ctr)) return;
     using Sort = cub::BlockRadixSort<unsigned long long, kThreads, kFbSortItems>;
-    __shared__ typename Sort::TempStorage tmp;
+    using Scan = cub::BlockScan<uint32_t, kThreads>;
+    __shared__ union {
+        typename Sort::TempStorage sort;
+        typename Scan::TempStorage scan;
+    } tmp;
+    __shared__ uint32_t seg_start[kBlockVoxels], seg_cnt[kBlockVoxels], cursor[kBlockVoxels];
     const uint32_t nb = ctr[C_FB_BLOCKS];
     const int end_bit = int(pb) + 13;
     for (uint32_t t = blockIdx.x; t < nb; t += gridDim.x) {
         const uint32_t idx = fbblocks[t];
         const uint32_t cnt = fbcnt[idx], start = fbstart[idx];
         unsigned long long* bk = bucket + start;
-        // sorted tiles of kFbSortMax records (one tile: the whole bucket)
-        for (uint32_t t0 = 0; t0 < cnt; t0 += kFbSortMax) {
-            unsigned long long k[kFbSortItems];
+        unsigned long long* sc = scratch + start;
+        if (cnt <= kThreads) {  // most buckets: a rank count per record (keys are unique)
+            unsigned long long k = 0;
+            uint32_t r = 0;
+            if (threadIdx.x < cnt) {
+                k = bk[threadIdx.x];
+                for (uint32_t j = 0; j < cnt; ++j) r += bk[j] < k ? 1u : 0u;
+            }
+            __syncthreads();
+            if (threadIdx.x < cnt) bk[r] = k;
+            __syncthreads();
+        } else if (cnt <= kFbSortMax) {
+            cta_sort_range<Sort>(tmp.sort, bk, bk, cnt, end_bit);
+        } else {
+            for (int v = threadIdx.x; v < kBlockVoxels; v += kThreads) seg_cnt[v] = 0u;
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) atomicAdd(&seg_cnt[(bk[i] >> (pb + 4)) & 511u], 1u);
+            __syncthreads();
+            {
+                constexpr int kPer = kBlockVoxels / kThreads;
+                uint32_t cc[kPer];
 #pragma unroll
-            for (int j = 0; j < kFbSortItems; ++j) {
-                const uint32_t pos = t0 + threadIdx.x * kFbSortItems + j;  // blocked arrangement
-                k[j] = pos < cnt ? bk[pos] : ~0ull;  // padding sorts last (the sort is stable)
-            }
-            Sort(tmp).Sort(k, 0, end_bit);
+                for (int j = 0; j < kPer; ++j) cc[j] = seg_cnt[threadIdx.x * kPer + j];
+                Scan(tmp.scan).ExclusiveSum(cc, cc);
 #pragma unroll
-            for (int j = 0; j < kFbSortItems; ++j) {
-                const uint32_t pos = t0 + threadIdx.x * kFbSortItems + j;
-                if (pos < cnt) bk[pos] = k[j];
+                for (int j = 0; j < kPer; ++j) seg_start[threadIdx.x * kPer + j] = cursor[threadIdx.x * kPer + j] = cc[j];
             }
-            __syncthreads();  // tmp reused; the tile's writes visible to the CTA
-        }
-        // merge passes for a bucket of several tiles (rare: a block many rays cross)
-        if (cnt > kFbSortMax) {
-            unsigned long long* src = bk;
-            unsigned long long* dst = scratch + start;
-            for (uint32_t w = kFbSortMax; w < cnt; w *= 2) {
-                for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
-                    const uint32_t p0 = (i / (2 * w)) * (2 * w);
-                    const uint32_t a1 = min(p0 + w, cnt), b1 = min(p0 + 2 * w, cnt);
-                    const unsigned long long key = src[i];
-                    // rank of key in the other run: lower bound (unique keys)
-                    uint32_t lo, hi;
-                    if (i < a1) { lo = a1; hi = b1; } else { lo = p0; hi = a1; }
-                    const uint32_t base = lo;
-                    while (lo < hi) {
-                        const uint32_t mid = (lo + hi) >> 1;
-                        if (src[mid] < key) lo = mid + 1; else hi = mid;
-                    }
-                    const uint32_t own = i < a1 ? i - p0 : i - a1;
-                    dst[p0 + own + (lo - base)] = key;
-                }
-                __syncthreads();
-                unsigned long long* x = src;
-                src = dst;
-                dst = x;
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
+                const unsigned long long k = bk[i];
+                sc[atomicAdd(&cursor[(k >> (pb + 4)) & 511u], 1u)] = k;
             }
-            if (src != bk) {
-                for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) bk[i] = src[i];
-                __syncthreads();
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {  // small voxel segments
+                const unsigned long long k = sc[i];
+                const uint32_t v = uint32_t(k >> (pb + 4)) & 511u;
+                const uint32_t b0 = seg_start[v], e0 = b0 + seg_cnt[v];
+                if (e0 - b0 > 64u) continue;
+                uint32_t r = 0;
+                for (uint32_t j = b0; j < e0; ++j) r += sc[j] < k ? 1u : 0u;
+                bk[b0 + r] = k;
             }
+            __syncthreads();
+            for (int v = 0; v < kBlockVoxels; ++v)  // large voxel segments (CTA-uniform loop)
+                if (seg_cnt[v] > 64u) cta_sort_range<Sort>(tmp.sort, sc + seg_start[v], bk + seg_start[v], seg_cnt[v], end_bit);
+            __syncthreads();
         }
         for (uint32_t pos = threadIdx.x; pos < cnt; pos += kThreads) {
             const unsigned long long run = bk[pos] >> pb;  // (block, voxel, frame)
