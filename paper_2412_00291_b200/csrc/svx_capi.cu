@@ -179,7 +179,7 @@ svx_map* create_map(const svx_map_cfg& cfg, int device) {
         }
         if (const char* e = std::getenv("SVX_TEST_POOL_HEAD")) m->test_pool_head = uint64_t(std::max(1L, std::atol(e)));
         set_rec_cap(m, rec_cap);
-        m->fb_global = std::getenv("SVX_FB_GLOBAL") != nullptr;  // A/B: the global radix sort
+        m->fb_global = m->fb_env = std::getenv("SVX_FB_GLOBAL") != nullptr;  // A/B: the global radix sort
         SVX_CUDA(cudaMallocHost(&m->h_ctr, sizeof(uint32_t) * kNumCounters));
         SVX_CUDA(cudaMallocHost(&m->h_fctr, sizeof(uint32_t) * kMaxG * kFC));
         std::memset(m->h_ctr, 0, sizeof(uint32_t) * kNumCounters);

@@ -403,6 +403,7 @@ enum Counter : int {
     C_DONE = 24,        // CTAs of k_fold finished (the last one writes the group's reports)
     C_FB_BLOCKS = 25,   // blocks holding fallback records this group (per-block ordering)
     C_BUCKET_TOP = 26,  // fallback bucket space handed out this group
+    C_FB_MAXB = 27,     // largest fallback bucket of the batch (the host picks the ordering)
     kNumCounters = 32
 };
 

@@ -1096,6 +1096,10 @@ k_fb_runs(const unsigned long long* __restrict__ sorted, unsigned long long* __r
 // each. (The global radix sort over the record buffer, CUB + k_fb_runs, is kept as an
 // alternative: SVX_FB_GLOBAL=1.)
 constexpr int kFbSortItems = 8;
+#ifndef SVX_FB_GLOBAL_BUCKET
+#define SVX_FB_GLOBAL_BUCKET 6144
+#endif
+constexpr uint32_t kFbGlobalBucket = SVX_FB_GLOBAL_BUCKET;  // a larger bucket: the next batch sorts globally
 constexpr uint32_t kFbSortMax = kThreads * kFbSortItems;  // records per block one CTA sorts
 
 __global__ void __launch_bounds__(kThreads)
@@ -1126,6 +1130,7 @@ k_fb_alloc(const uint32_t* __restrict__ fbcnt, const uint32_t* __restrict__ fbbl
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nb; t += gridDim.x * blockDim.x) {
         const uint32_t idx = fbblocks[t], cnt = fbcnt[idx];
         fbstart[idx] = atomicAdd(&ctr[C_BUCKET_TOP], cnt);
+        if (cnt > kFbSortMax) atomicMax(&ctr[C_FB_MAXB], cnt);
     }
 }
 
@@ -1993,6 +1998,16 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
     }
     for (int i = f0; i < n; ++i) commit(i);
     m->n_blocks = m->h_ctr[C_BLOCKS];
+    // fallback ordering for the next batch: one CTA per block is fastest unless some block
+    // holds very many records (thousands of rays through a few voxels: a long single-CTA
+    // tail), then the global radix sort over the record buffer
+    if (!m->fb_env) {
+        m->fb_global = m->h_ctr[C_FB_MAXB] > kFbGlobalBucket;
+        if (m->h_ctr[C_FB_MAXB]) {
+            m->h_ctr[C_FB_MAXB] = 0;
+            SVX_CUDA(cudaMemcpyAsync(m->d_ctr + C_FB_MAXB, &m->h_ctr[C_FB_MAXB], 4, cudaMemcpyHostToDevice, m->stream));
+        }
+    }
     // the record capacity follows use: the per-group sort covers all of it, so after a batch
     // whose largest group used less than half of it, it shrinks to 1.5x that group (+ slack);
     // a larger group later costs one rollback and retry with a grown buffer
@@ -2171,6 +2186,13 @@ void run_group_xend(svx_map* m, const void* d_recv, const uint64_t* recv_meta, s
     if (m->h_ctr[C_ABORT]) throw Error(SVX_CUDA, "xend: fold aborted");
     for (int i = 0; i < G; ++i) commit_frame(m, s, m->h_outs[i], reps[i]);
     m->n_blocks = m->h_ctr[C_BLOCKS];
+    if (!m->fb_env) {  // the fallback ordering of the next group (as after a batch in run_frames)
+        m->fb_global = m->h_ctr[C_FB_MAXB] > kFbGlobalBucket;
+        if (m->h_ctr[C_FB_MAXB]) {
+            m->h_ctr[C_FB_MAXB] = 0;
+            SVX_CUDA(cudaMemcpyAsync(m->d_ctr + C_FB_MAXB, &m->h_ctr[C_FB_MAXB], 4, cudaMemcpyHostToDevice, m->stream));
+        }
+    }
 }
 
 }  // namespace svx
