@@ -216,6 +216,7 @@ struct svx_map {
     uint32_t* fbblocks = nullptr;
     bool fb_global = false;          // order the records with the global radix sort (next batch)
     bool fb_env = false;             // SVX_FB_GLOBAL=1: always (A/B)
+    int fb_global_left = 0;          // batches left in the global ordering before a re-probe
     svx::DevBuf<uint8_t> fb_tmp;
     svx::DevBuf<uint4> fbdesc;       // fallback voxels: pool idx, voxel | frame << 16, records start, count
     uint32_t rec_cap = 0;            // fallback records per group (the sort's size)

@@ -1841,6 +1841,29 @@ void grow_keep(DevBuf<T>& b, size_t count, size_t keep, cudaStream_t stream) {
 }
 }  // namespace
 
+namespace {
+// Fallback ordering of the next batch: one CTA per block unless the per-block path just saw
+// a bucket of more than kFbGlobalBucket records (a long single-CTA tail), then the global
+// radix sort for kFbGlobalBatches batches before the per-block path is probed again (the
+// global path does not measure bucket sizes).
+constexpr int kFbGlobalBatches = 8;
+void pick_fb_ordering(svx_map* m) {
+    if (m->fb_env) return;
+    if (m->fb_global) {
+        if (--m->fb_global_left <= 0) m->fb_global = false;
+        return;
+    }
+    if (m->h_ctr[C_FB_MAXB] > kFbGlobalBucket) {
+        m->fb_global = true;
+        m->fb_global_left = kFbGlobalBatches;
+    }
+    if (m->h_ctr[C_FB_MAXB]) {
+        m->h_ctr[C_FB_MAXB] = 0;
+        SVX_CUDA(cudaMemcpyAsync(m->d_ctr + C_FB_MAXB, &m->h_ctr[C_FB_MAXB], 4, cudaMemcpyHostToDevice, m->stream));
+    }
+}
+}  // namespace
+
 void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cfg& cfg, svx_frame_report* reps,
                 LabelHook* labels) {
     if (!(cfg.alpha_epsilon > 0.0)) throw Error(SVX_INVALID_ARGUMENT, "alpha_epsilon must be > 0");
@@ -2001,13 +2024,7 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
     // fallback ordering for the next batch: one CTA per block is fastest unless some block
     // holds very many records (thousands of rays through a few voxels: a long single-CTA
     // tail), then the global radix sort over the record buffer
-    if (!m->fb_env) {
-        m->fb_global = m->h_ctr[C_FB_MAXB] > kFbGlobalBucket;
-        if (m->h_ctr[C_FB_MAXB]) {
-            m->h_ctr[C_FB_MAXB] = 0;
-            SVX_CUDA(cudaMemcpyAsync(m->d_ctr + C_FB_MAXB, &m->h_ctr[C_FB_MAXB], 4, cudaMemcpyHostToDevice, m->stream));
-        }
-    }
+    pick_fb_ordering(m);
     // the record capacity follows use: the per-group sort covers all of it, so after a batch
     // whose largest group used less than half of it, it shrinks to 1.5x that group (+ slack);
     // a larger group later costs one rollback and retry with a grown buffer
@@ -2186,13 +2203,7 @@ void run_group_xend(svx_map* m, const void* d_recv, const uint64_t* recv_meta, s
     if (m->h_ctr[C_ABORT]) throw Error(SVX_CUDA, "xend: fold aborted");
     for (int i = 0; i < G; ++i) commit_frame(m, s, m->h_outs[i], reps[i]);
     m->n_blocks = m->h_ctr[C_BLOCKS];
-    if (!m->fb_env) {  // the fallback ordering of the next group (as after a batch in run_frames)
-        m->fb_global = m->h_ctr[C_FB_MAXB] > kFbGlobalBucket;
-        if (m->h_ctr[C_FB_MAXB]) {
-            m->h_ctr[C_FB_MAXB] = 0;
-            SVX_CUDA(cudaMemcpyAsync(m->d_ctr + C_FB_MAXB, &m->h_ctr[C_FB_MAXB], 4, cudaMemcpyHostToDevice, m->stream));
-        }
-    }
+    pick_fb_ordering(m);  // for the next group (as after a batch in run_frames)
 }
 
 }  // namespace svx
