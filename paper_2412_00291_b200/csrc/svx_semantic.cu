@@ -282,10 +282,20 @@ template <int KC>
 __device__ inline void bayes_regs(Probs<KC>& p, const Like& like, bool use_bayes) {
     if (use_bayes) {
         double z = 0.0;
+        if (like.tp) {
 #pragma unroll
-        for (int k = 0; k < KC; ++k) {
-            p.v[k] = p.v[k] * like(k);
-            z += double(p.v[k]);
+            for (int k = 0; k < KC; ++k) {
+                p.v[k] = p.v[k] * like(k);
+                z += double(p.v[k]);
+            }
+        } else {  // a label likelihood: lt at the label, lb elsewhere (the same products)
+            const float lt = like.lt, lb = like.lb;
+            const int label = like.label;
+#pragma unroll
+            for (int k = 0; k < KC; ++k) {
+                p.v[k] = p.v[k] * (k == label ? lt : lb);
+                z += double(p.v[k]);
+            }
         }
         // float(1 / z) from the reciprocal estimate when it decides the float
         float inv;
@@ -491,7 +501,7 @@ k_sem_update(const __grid_constant__ SemBatch sb, HashView h, const uint64_t* __
         __syncwarp();
         // per image, the warp's updated voxels: lane i keeps image i's count
         for (int i = 0; i < n_apply; ++i) {
-            const uint32_t nu = __popc(__ballot_sync(0xFFFFFFFFu, (pass >> i) & 1u));
+            const uint32_t nu = __reduce_add_sync(0xFFFFFFFFu, (pass >> i) & 1u);
             if (lane == i) n_upd += nu;
         }
         if (lane == 0) dirty_sem[idx] = 1;
