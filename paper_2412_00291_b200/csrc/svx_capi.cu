@@ -134,6 +134,7 @@ void free_map(svx_map* m) {
         if (m->ingest_used[i]) cudaEventDestroy(m->ingest_used[i]);
         m->ingest[i].release();
     }
+    for (cudaEvent_t e : m->label_events) cudaEventDestroy(e);
     if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
     if (m->stream && m->own_stream) cudaStreamDestroy(m->stream);
     delete m;

@@ -242,6 +242,8 @@ struct svx_map {
     static constexpr int kIngestSlots = 2;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ingest_ready[kIngestSlots] = {}, ingest_used[kIngestSlots] = {};
+    // host label images staged on copy_stream ahead of their label passes (one event per pass)
+    std::vector<cudaEvent_t> label_events;
     svx::DevBuf<float> ingest[kIngestSlots];
     svx::DevBuf<uint64_t> q_keys;    // scratch of host block queries (find / insert)
     svx::DevBuf<uint32_t> q_idx;
@@ -389,6 +391,7 @@ struct LabelBatch {
     int passes = 0, max_passes = 0;
     std::vector<int> pass_first, pass_count;
     uint64_t lo = 0, co = 0, to = 0;  // host staging offsets
+    size_t events_used = 0;           // label_events of this batch
     std::vector<const uint16_t*> staged_lbl;  // per image: its staged device copy
     std::vector<const float*> staged_conf, staged_ten;
 };

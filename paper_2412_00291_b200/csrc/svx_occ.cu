@@ -246,7 +246,10 @@ constexpr int kBlockCache = 2048;
 #endif
 constexpr int kVisitThreads = SVX_OCC_VB;  // rays per CTA
 
-__global__ void __launch_bounds__(kVisitThreads) k_occ_visit(OccParams p, OccDev d) {
+#ifndef SVX_OCC_MINB
+#define SVX_OCC_MINB 1
+#endif
+__global__ void __launch_bounds__(kVisitThreads, SVX_OCC_MINB) k_occ_visit(OccParams p, OccDev d) {
     __shared__ unsigned long long ckey[kBlockCache];
     __shared__ uint32_t cidx[kBlockCache];
     for (int j = threadIdx.x; j < kBlockCache; j += blockDim.x) {

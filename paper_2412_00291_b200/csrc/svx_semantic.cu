@@ -615,6 +615,11 @@ void labels_enqueue(svx_map* m, LabelBatch& lb, int i0, int i1, uint32_t group_f
         sb.default_conf = cfg.default_confidence;
         sb.pass_id = uint32_t(ps + 1);
         sb.group_frame = group_frame;
+        // host images go up on the copy stream when there is one (the TSDF ingest ring's):
+        // they overlap the frame's TSDF kernels, and the map stream waits for them only
+        // before this pass
+        cudaStream_t cs = m->copy_stream ? m->copy_stream : m->stream;
+        bool staged_now = false;
         for (int k = 0; k < ni; ++k) {
             const svx_label_image& img = lb.imgs[a + k];
             const uint64_t P = uint64_t(img.width) * uint64_t(img.height);
@@ -637,18 +642,19 @@ void labels_enqueue(svx_map* m, LabelBatch& lb, int i0, int i1, uint32_t group_f
             if (!lb.on_device) {  // staged once (a retried frame group reuses the copy)
                 const size_t ii = size_t(a + k);
                 if (!lb.staged_lbl[ii]) {
-                    SVX_CUDA(cudaMemcpyAsync(m->lbl.p + lb.lo, img.labels, 2 * P, cudaMemcpyHostToDevice, m->stream));
+                    staged_now = true;
+                    SVX_CUDA(cudaMemcpyAsync(m->lbl.p + lb.lo, img.labels, 2 * P, cudaMemcpyHostToDevice, cs));
                     lb.staged_lbl[ii] = m->lbl.p + lb.lo;
                     lb.lo += P;
                     if (img.confidence) {
                         SVX_CUDA(cudaMemcpyAsync(m->conf.p + lb.co, img.confidence, 4 * P, cudaMemcpyHostToDevice,
-                                                 m->stream));
+                                                 cs));
                         lb.staged_conf[ii] = m->conf.p + lb.co;
                         lb.co += P;
                     }
                     if (img.prob_tensor) {
                         SVX_CUDA(cudaMemcpyAsync(m->tensor.p + lb.to, img.prob_tensor, 4 * P * K,
-                                                 cudaMemcpyHostToDevice, m->stream));
+                                                 cudaMemcpyHostToDevice, cs));
                         lb.staged_ten[ii] = m->tensor.p + lb.to;
                         lb.to += P * K;
                     }
@@ -667,6 +673,16 @@ void labels_enqueue(svx_map* m, LabelBatch& lb, int i0, int i1, uint32_t group_f
             // confidence validity: only a voxel that passes every test reads one
             ip.conf_maybe = !ip.has_tensor && (ip.has_conf || bad_default);
             if (ip.conf_maybe) sb.any_check = 1;
+        }
+        if (staged_now && cs != m->stream) {
+            if (lb.events_used == m->label_events.size()) {
+                cudaEvent_t e;
+                SVX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                m->label_events.push_back(e);
+            }
+            cudaEvent_t e = m->label_events[lb.events_used++];
+            SVX_CUDA(cudaEventRecord(e, cs));
+            SVX_CUDA(cudaStreamWaitEvent(m->stream, e, 0));
         }
         SVX_CUDA(cudaMemsetAsync(m->d_ctr + C_CAND, 0, 4, m->stream));
         {
