@@ -351,6 +351,37 @@ __device__ inline bool needs_check(const ImgParams& ip, const uint32_t* xconf, i
     return ip.conf_maybe && (!ip.has_conf || xconf[i]);
 }
 
+// The Bayes steps of one queued voxel (k_sem_update): its probabilities in registers (or in
+// place without a compile-time K), the passing images in order.
+constexpr uint32_t kQueue = 64;  // voxels per warp queue (a ring: < 32 waiting + one task's 32)
+template <int KC>
+__device__ inline void bayes_queued(const SemBatch& sb, float* __restrict__ sem, int K, const uint32_t* q_sid,
+                                    const uint32_t* q_lp, const uint32_t (*q_pix)[kQueue], uint32_t e, bool lut_ok,
+                                    const float2 (*s_lut)[kLutK + 1]) {
+    const uint32_t lp = q_lp[e], pass = lp & 0xFFu, linear = lp >> 8;
+    float* probs = sem + (uint64_t(q_sid[e]) * kBlockVoxels + linear) * K;
+    if constexpr (KC > 0) {
+        Probs<KC> p;
+        p.load(probs);
+#pragma unroll 1
+        for (uint32_t r = pass; r; r &= r - 1) {
+            const int i = __ffs(r) - 1;
+            const ImgParams& ip = sb.img[i];
+            const float2* lut = (lut_ok && !ip.has_tensor && !ip.has_conf) ? s_lut[i] : nullptr;
+            bayes_regs<KC>(p, make_like(sb, ip, q_pix[i][e], K, lut), sb.use_bayes != 0);
+        }
+        p.store(probs);
+    } else {
+#pragma unroll 1
+        for (uint32_t r = pass; r; r &= r - 1) {
+            const int i = __ffs(r) - 1;
+            const ImgParams& ip = sb.img[i];
+            const float2* lut = (lut_ok && !ip.has_tensor && !ip.has_conf) ? s_lut[i] : nullptr;
+            bayes_mem(probs, make_like(sb, ip, q_pix[i][e], K, lut), K, sb.use_bayes != 0);
+        }
+    }
+}
+
 // xconf[i]: image i's confidence map holds an invalid value; xerr[i]: image i reads one
 // (check pass); xupd[i]: voxels image i updated.
 template <int KC>
@@ -398,6 +429,11 @@ k_sem_update(const __grid_constant__ SemBatch sb, HashView h, const uint64_t* __
         }
     }
     __syncthreads();
+    // per warp: a ring of voxels waiting for their Bayes steps (layer, voxel | images, pixels)
+    __shared__ uint32_t q_sid[kThreads / 32][kQueue], q_lp[kThreads / 32][kQueue];
+    __shared__ uint32_t q_pix[kThreads / 32][kMaxImg][kQueue];
+    const int wq = threadIdx.x >> 5;
+    uint32_t q_head = 0, q_tail = 0;
     uint32_t n_upd = 0;  // lane i < n_apply: voxels image i updated
     for (uint32_t t = warp; t < kParts * n_cand; t += nwarps) {
         const uint2 cd = cand[t / kParts];
@@ -475,27 +511,26 @@ k_sem_update(const __grid_constant__ SemBatch sb, HashView h, const uint64_t* __
                 if (lane == 0) atomicExch(&sem_idx[idx], sid);
             }
         }
-        if (pass) {  // the passing images in order, the probabilities in registers meanwhile
-            float* probs = sem + (uint64_t(sid) * kBlockVoxels + linear) * K;
-            if constexpr (KC > 0) {
-                Probs<KC> p;
-                p.load(probs);
-#pragma unroll 1
+        // the passing voxels join the warp's queue; the Bayes steps run 32 queued voxels at
+        // a time on full warps (a task's voxels fail the W / D / frustum tests unevenly)
+        {
+            const uint32_t m = __ballot_sync(0xFFFFFFFFu, pass != 0u);
+            if (pass) {
+                const uint32_t e = (q_tail + uint32_t(__popc(m & ((1u << lane) - 1u)))) & (kQueue - 1u);
+                q_sid[wq][e] = sid;
+                q_lp[wq][e] = (uint32_t(linear) << 8) | pass;
                 for (uint32_t r = pass; r; r &= r - 1) {
                     const int i = __ffs(r) - 1;
-                    const ImgParams& ip = sb.img[i];
-                    const float2* lut = (lut_ok && !ip.has_tensor && !ip.has_conf) ? s_lut[i] : nullptr;
-                    bayes_regs<KC>(p, make_like(sb, ip, pix[i][lane], K, lut), sb.use_bayes != 0);
+                    q_pix[wq][i][e] = pix[i][lane];
                 }
-                p.store(probs);
-            } else {
-#pragma unroll 1
-                for (uint32_t r = pass; r; r &= r - 1) {
-                    const int i = __ffs(r) - 1;
-                    const ImgParams& ip = sb.img[i];
-                    const float2* lut = (lut_ok && !ip.has_tensor && !ip.has_conf) ? s_lut[i] : nullptr;
-                    bayes_mem(probs, make_like(sb, ip, pix[i][lane], K, lut), K, sb.use_bayes != 0);
-                }
+            }
+            q_tail += uint32_t(__popc(m));
+            __syncwarp();
+            if (q_tail - q_head >= 32u) {
+                bayes_queued<KC>(sb, sem, K, q_sid[wq], q_lp[wq], q_pix[wq], (q_head + lane) & (kQueue - 1u), lut_ok,
+                                 s_lut);
+                q_head += 32u;
+                __syncwarp();
             }
         }
         __syncwarp();
@@ -506,6 +541,8 @@ k_sem_update(const __grid_constant__ SemBatch sb, HashView h, const uint64_t* __
         }
         if (lane == 0) dirty_sem[idx] = 1;
     }
+    if (!check && q_tail > q_head && uint32_t(lane) < q_tail - q_head)  // the queue's rest
+        bayes_queued<KC>(sb, sem, K, q_sid[wq], q_lp[wq], q_pix[wq], (q_head + lane) & (kQueue - 1u), lut_ok, s_lut);
     if (lane < n_apply && n_upd) atomicAdd(&xupd[lane], n_upd);
 }
 
