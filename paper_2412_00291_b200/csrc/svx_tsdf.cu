@@ -1864,6 +1864,11 @@ void pick_fb_ordering(svx_map* m) {
 }
 }  // namespace
 
+#ifndef SVX_INGEST_FIRST
+#define SVX_INGEST_FIRST 4
+#endif
+constexpr int kIngestFirstGroup = SVX_INGEST_FIRST;
+
 void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cfg& cfg, svx_frame_report* reps,
                 LabelHook* labels) {
     if (!(cfg.alpha_epsilon > 0.0)) throw Error(SVX_INVALID_ARGUMENT, "alpha_epsilon must be > 0");
@@ -1929,7 +1934,10 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
         GroupParams gp{};
         int k = 0;
         for (int a = f0; a < n; ++k) {
-            const int G = (a >= single_lo && a < single_hi) ? 1 : std::min(gcap, n - a);
+            // host ingest: the batch's first group is short (its H2D copy is the only one not
+            // hidden behind a previous group's kernels)
+            const int gfirst = (ingest && a == 0 && k == 0) ? std::min(gcap, kIngestFirstGroup) : gcap;
+            const int G = (a >= single_lo && a < single_hi) ? 1 : std::min(gfirst, n - a);
             starts.push_back(a);
             gp.c = make_consts(m, s, cfg, uint32_t(G), project ? true : s->has_normals);
             for (int g = 0; g < G; ++g) gp.f[g] = make_pose(m, jobs[a + g].pose);
