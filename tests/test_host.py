@@ -161,3 +161,14 @@ def test_integrators_mirror_the_reference_methods():
                                                  "take_dirty_blocks"))):
         for n in names:
             assert callable(getattr(cls, n, None)), (cls.__name__, n)
+
+
+def test_cfg5_trajectory_stays_inside_the_room():
+    # the sweep runs 3 passes of up to 64 scans: every pose stays clear of the room's walls
+    # (|x|, |y| < 15 m), so no scan starts inside a wall
+    wl = W.make("cfg5-80", 400)
+    xs = np.array([wl.poses[i][1][0] for i in range(400)])
+    ys = np.array([wl.poses[i][1][1] for i in range(400)])
+    assert xs.min() >= -6.0 and xs.max() <= 10.0 and np.abs(ys).max() < 15.0
+    # the first scans are the ones the parity tests use
+    assert tuple(wl.poses[0][1][:2]) == (-6.0, 0.0) and tuple(wl.poses[1][1][:2]) == (-5.75, 0.0)
