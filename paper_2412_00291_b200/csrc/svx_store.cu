@@ -177,6 +177,10 @@ void ensure_blocks(svx_map* m, uint64_t blocks, uint64_t ahead) {
     const uint64_t target = std::min<uint64_t>(m->cfg.max_blocks, blocks + ahead);
     m->tsdf_pool.prefetch(target * m->block_bytes);
     m->mask_pool.prefetch(target * mask_bytes);
+    // a map with semantic layers needs a layer for every block a label pass may reach (the
+    // label passes map up to the mapped block count): keep the layers' mapping in step, in
+    // the background too
+    if (m->n_layers) m->sem_pool.prefetch(target * m->layer_bytes);
     const uint64_t mapped = std::min<uint64_t>(
         std::min<uint64_t>(m->tsdf_pool.mapped() / m->block_bytes, m->mask_pool.mapped() / mask_bytes),
         m->cfg.max_blocks);

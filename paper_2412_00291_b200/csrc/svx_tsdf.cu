@@ -1900,8 +1900,9 @@ void run_frames(svx_map* m, const FrameJob* jobs, int n, const svx_integrator_cf
         SVX_CUDA(cudaMallocHost(&m->h_outs, sizeof(FrameOut) * n));
         m->h_outs_n = size_t(n);
     }
-    // per-frame visited-voxel lists (~5 per pixel at cfg2): 8 per pixel, grown on overflow
-    const uint64_t want_vox = std::min<uint64_t>(8ull * uint64_t(s->P) + 4096, 0x7FFFFFFFull);
+    // per-frame visited-voxel lists (~5 per pixel at cfg2, more in dense scenes): 12 per
+    // pixel, grown on overflow (a growth costs a rollback and retry of the group)
+    const uint64_t want_vox = std::min<uint64_t>(12ull * uint64_t(s->P) + 4096, 0x7FFFFFFFull);
     if (m->vox_cap < want_vox) m->vox_cap = uint32_t(want_vox);
     m->vlist.alloc(uint64_t(m->vox_cap) * uint64_t(gmax));
     // pool headroom for the batch (an exhausted headroom costs one rollback + retry; over-
