@@ -824,6 +824,10 @@ def run_emulated(args):
                 sdist.emulate_sharded(stores, wl.model, pts.data_ptr() + int(offs[f0]) * 12, rel, 3, poses[f0:f1],
                                       icfg, timers=timers)
                 tmax = sum(max(b + e for b, e in zip(t["xbegin_ms"], t["xend_ms"])) for t in timers)
+                if os.environ.get("SVX_EMU_DEBUG"):
+                    print(json.dumps({"N": N, "step": s, "groups": [[round(b, 2) for b in t["xbegin_ms"]] +
+                                                                  [round(e, 2) for e in t["xend_ms"]] for t in timers]}),
+                          file=sys.stderr, flush=True)
                 tsum = sum(sum(t["xbegin_ms"]) + sum(t["xend_ms"]) for t in timers)
                 ent = sum(sum(t["entries"]) for t in timers)
             else:
@@ -842,11 +846,15 @@ def run_emulated(args):
         # direction per GPU (measured peer copy), per step
         xchg_ms = [b / N / 770e9 * 1e3 for b in xbytes]
         t_step = [a + x for a, x in zip(step_max, xchg_ms)]
-        out["ranks"][N] = {"max_rank_ms_per_step": float(np.mean(step_max)),
-                           "all_ranks_ms_per_step": float(np.mean(step_sum)),
+        # the median step: a rank's one-time buffer growth (a host synchronisation inside one
+        # call) lands in a single step; the mean keeps it for reference
+        n_t = len(t_step)
+        out["ranks"][N] = {"max_rank_ms_per_step": float(np.median(step_max)),
+                           "max_rank_ms_per_step_mean": float(np.mean(step_max)),
+                           "all_ranks_ms_per_step": float(np.median(step_sum)),
                            "exchange_bytes_per_step": float(np.mean(xbytes)),
                            "exchange_ms_per_step_est": float(np.mean(xchg_ms)),
-                           "points_per_s_est": pts_t / (sum(t_step) / 1e3),
+                           "points_per_s_est": (pts_t / n_t) / (float(np.median(t_step)) / 1e3),
                            "blocks_per_rank": [st.block_count() for st in stores]}
         for st in stores:
             st.close()

@@ -29,9 +29,11 @@ for N in [int(a) for a in sys.argv[1:]] or [1, 8]:
     stores = []
     for r in range(N):
         st = svx.VoxelStore(cfg, 0)
+        st.reserve(1 << 18)
         if N > 1:
             st.set_shard(r, N)
         stores.append(st)
+    step_ms = []
     for s in range(warm + steps):
         if s == warm:
             for st in stores:
@@ -40,6 +42,7 @@ for N in [int(a) for a in sys.argv[1:]] or [1, 8]:
         f0, f1 = s * spp, (s + 1) * spp
         rel = offs[f0:f1 + 1] - offs[f0]
         timers = []
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
         if N > 1:
             sdist.emulate_sharded(stores, wl.model, pts.data_ptr() + int(offs[f0]) * 12, rel, 3, poses[f0:f1], icfg,
@@ -47,10 +50,13 @@ for N in [int(a) for a in sys.argv[1:]] or [1, 8]:
         else:
             stores[0].integrate_clouds_device(wl.model, pts.data_ptr() + int(offs[f0]) * 12, rel, 3, poses[f0:f1], icfg)
         torch.cuda.synchronize()
+        step_ms.append(round((time.perf_counter() - t0) * 1e3, 2))
+    print(json.dumps({"N": N, "step_ms": step_ms}), flush=True)
     for r, st in enumerate(stores[:2]):
         p = st.profile_read().as_dict()
         print(json.dumps({"N": N, "rank": r, "us_per_frame": {k: round(1e3 * v / (steps * spp), 2) for k, v in p["ms"].items()},
                           "launches": p["launches"], "host_enqueue_ms": p["host_enqueue_ms"],
-                          "host_resume_ms": p["host_resume_ms"], "aborts": p["aborts"]}), flush=True)
+                          "host_resume_ms": p["host_resume_ms"], "host_map_ms": p["host_map_ms"],
+                          "aborts": p["aborts"]}), flush=True)
     for st in stores:
         st.close()
