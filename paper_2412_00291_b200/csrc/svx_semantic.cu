@@ -31,6 +31,13 @@
 
 #include "svx_map.hpp"
 
+#ifndef SVX_SEM_PREFETCH
+#define SVX_SEM_PREFETCH 2
+#endif
+#ifndef SVX_SEM_PF_LAYER
+#define SVX_SEM_PF_LAYER 1
+#endif
+
 namespace svx {
 
 namespace {
@@ -435,13 +442,47 @@ k_sem_update(const __grid_constant__ SemBatch sb, HashView h, const uint64_t* __
     const int wq = threadIdx.x >> 5;
     uint32_t q_head = 0, q_tail = 0;
     uint32_t n_upd = 0;  // lane i < n_apply: voxels image i updated
-    for (uint32_t t = warp; t < kParts * n_cand; t += nwarps) {
+    const uint32_t n_tasks = kParts * n_cand;
+#if SVX_SEM_PREFETCH == 1
+    // the next task's candidate, block key and TSDF weight / distance are loaded one
+    // iteration ahead (their dependent chain overlaps this task's projections)
+    uint2 cd_n = make_uint2(0u, 0u);
+    uint64_t key_n = 0;
+    float w_n = 0.f, dist_n = 0.f;
+    auto fetch = [&](uint32_t tt) {
+        if (tt >= n_tasks) return;
+        cd_n = cand[tt / kParts];
+        key_n = block_keys[cd_n.x];
+        const svx_tsdf_voxel* vn = pool + uint64_t(cd_n.x) * kBlockVoxels + int(tt % kParts) * 32 + lane;
+        w_n = vn->weight;
+        dist_n = vn->distance;
+    };
+    fetch(warp);
+#elif SVX_SEM_PREFETCH == 2
+    // the next task's candidate entry is loaded one iteration ahead, and its block key and
+    // TSDF voxel are prefetched into L2 once this task's projections are issued
+    uint2 cd_n = warp < n_tasks ? cand[warp / kParts] : make_uint2(0u, 0u);
+#endif
+    for (uint32_t t = warp; t < n_tasks; t += nwarps) {
+#if SVX_SEM_PREFETCH == 1
+        const uint2 cd = cd_n;
+        const uint64_t key = key_n;
+        const float w = w_n, dist = dist_n;
+        fetch(t + nwarps);
+#elif SVX_SEM_PREFETCH == 2
+        const uint2 cd = cd_n;
+        if (t + nwarps < n_tasks) cd_n = cand[(t + nwarps) / kParts];
+        const uint64_t key = block_keys[cd.x];
+        const svx_tsdf_voxel* v = pool + uint64_t(cd.x) * kBlockVoxels + int(t % kParts) * 32 + lane;
+        const float w = v->weight, dist = v->distance;
+#else
         const uint2 cd = cand[t / kParts];
+        const uint64_t key = block_keys[cd.x];
+        const svx_tsdf_voxel* v = pool + uint64_t(cd.x) * kBlockVoxels + int(t % kParts) * 32 + lane;
+        const float w = v->weight, dist = v->distance;
+#endif
         const uint32_t idx = cd.x;
         const int linear = int(t % kParts) * 32 + lane;
-        const uint64_t key = block_keys[idx];
-        const svx_tsdf_voxel* v = pool + uint64_t(idx) * kBlockVoxels + linear;
-        const float w = v->weight, dist = v->distance;
         uint32_t pass = 0;
         if (w > 0.f && !(double(dist) < sb.occ_floor)) {
             const d3 c = center_of(key, linear, sb.nu);
@@ -474,6 +515,13 @@ k_sem_update(const __grid_constant__ SemBatch sb, HashView h, const uint64_t* __
                 pass |= 1u << i;
             }
         }
+#if SVX_SEM_PREFETCH == 2
+        if (t + nwarps < n_tasks) {
+            const svx_tsdf_voxel* vn = pool + uint64_t(cd_n.x) * kBlockVoxels + int((t + nwarps) % kParts) * 32 + lane;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(vn));
+            if (lane == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(block_keys + cd_n.x));
+        }
+#endif
         if (!__any_sync(0xFFFFFFFFu, pass != 0)) continue;
         if (check) {  // flag images whose passing voxels read an invalid confidence
 #pragma unroll 1
@@ -519,6 +567,13 @@ k_sem_update(const __grid_constant__ SemBatch sb, HashView h, const uint64_t* __
                 const uint32_t e = (q_tail + uint32_t(__popc(m & ((1u << lane) - 1u)))) & (kQueue - 1u);
                 q_sid[wq][e] = sid;
                 q_lp[wq][e] = (uint32_t(linear) << 8) | pass;
+#if SVX_SEM_PF_LAYER
+                {  // the voxel's probabilities, read when the queue next runs its Bayes steps
+                    const char* pr = reinterpret_cast<const char*>(sem + (uint64_t(sid) * kBlockVoxels + linear) * K);
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(pr));
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(pr + 4 * K - 4));
+                }
+#endif
                 for (uint32_t r = pass; r; r &= r - 1) {
                     const int i = __ffs(r) - 1;
                     q_pix[wq][i][e] = pix[i][lane];
