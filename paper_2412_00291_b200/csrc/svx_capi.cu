@@ -102,6 +102,7 @@ void free_map(svx_map* m) {
     if (m->h_ctr) cudaFreeHost(m->h_ctr);
     if (m->h_fctr) cudaFreeHost(m->h_fctr);
     if (m->h_outs) cudaFreeHost(m->h_outs);
+    if (m->h_xmeta) cudaFreeHost(m->h_xmeta);
     m->outs.release();
     m->bucket.release();
     m->bucket2.release();

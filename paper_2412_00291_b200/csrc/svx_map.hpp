@@ -234,6 +234,7 @@ struct svx_map {
     svx::DevBuf<svx::FrameOut> outs;
     svx::FrameOut* h_outs = nullptr;
     size_t h_outs_n = 0;
+    uint32_t* h_xmeta = nullptr;     // pinned: exchange-mode send metadata (world x (1 + kMaxG))
     uint64_t mapped_blocks = 0;      // host mirror of C_MAPPED
     double new_ema = 0.0;            // moving average of new blocks per frame
     uint64_t test_pool_head = 0;     // test hook (SVX_TEST_POOL_HEAD): fixed pool headroom

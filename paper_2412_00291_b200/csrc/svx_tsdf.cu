@@ -2083,7 +2083,8 @@ void run_group_xbegin(svx_map* m, const FrameJob* jobs, int G, const svx_integra
     m->xcnt.alloc(size_t(world) * kXMeta);
     m->xsend.alloc(uint64_t(world) * m->xcap);
     m->xpack.alloc(uint64_t(world) * m->xcap);
-    std::vector<uint32_t> meta(size_t(world) * kXMeta);
+    if (!m->h_xmeta) SVX_CUDA(cudaMallocHost(&m->h_xmeta, 4ull * kMaxXWorld * kXMeta));
+    uint32_t* meta = m->h_xmeta;  // pinned: the copy below stays asynchronous (one sync per group)
     auto xs = std::make_unique<XState>();
     xs->s = s;
     for (;;) {
@@ -2106,7 +2107,7 @@ void run_group_xbegin(svx_map* m, const FrameJob* jobs, int G, const svx_integra
         launch_pdl(k_xpack, dim3(64, unsigned(world)), kThreads, m->stream, static_cast<const uint4*>(m->xsend.p),
                    m->xcap, static_cast<const uint32_t*>(m->xcnt.p), m->xpack.p);
         count_launch();
-        SVX_CUDA(cudaMemcpyAsync(meta.data(), m->xcnt.p, 4ull * world * kXMeta, cudaMemcpyDeviceToHost, m->stream));
+        SVX_CUDA(cudaMemcpyAsync(meta, m->xcnt.p, 4ull * world * kXMeta, cudaMemcpyDeviceToHost, m->stream));
         SVX_CUDA(cudaMemcpyAsync(m->h_fctr, m->fctr, 4ull * kMaxG * kFC, cudaMemcpyDeviceToHost, m->stream));
         sync_counters(m);
         const uint32_t abort = m->h_ctr[C_ABORT];
@@ -2138,7 +2139,7 @@ void run_group_xbegin(svx_map* m, const FrameJob* jobs, int G, const svx_integra
         SVX_CUDA(cudaMemsetAsync(m->outs.p, 0, sizeof(FrameOut) * size_t(G), m->stream));
     }
     // (the lists were packed destination-major on the device by k_xpack)
-    for (size_t i = 0; i < meta.size(); ++i) send_meta[i] = meta[i];
+    for (size_t i = 0; i < size_t(world) * kXMeta; ++i) send_meta[i] = meta[i];
     *d_send = m->xpack.p;
     m->xstate = xs.release();
     m->xstate_free = free_xstate;
