@@ -149,11 +149,31 @@ k_finish_pixels(const __grid_constant__ ProjGroup pg, const uint32_t* __restrict
     const uint64_t o = uint64_t(g) * pg.P;
     const uint32_t bits = __ballot_sync(0xFFFFFFFFu, k != ~0ull);  // pixels with a return
     if ((threadIdx.x & 31) == 0 && inside) pg.validbits[uint64_t(g) * pg.VW + (p >> 5)] = bits;
+    // row distance to the nearest pixel without a return (band kernel's valid radius), capped
+    // at kRowDistMax + 1, the row wrapping around (azimuth): when a row is whole 32-pixel
+    // words, from the no-return bits of this word and its two neighbours in the row
+    int rd = -1;
+    if (W % 32 == 0) {
+        const int lane = int(threadIdx.x & 31);
+        const uint32_t wpr = uint32_t(W) / 32u, word = (p / 32u) % wpr, row0 = p - (p % uint32_t(W));
+        const uint32_t wp = row0 + ((word + wpr - 1u) % wpr) * 32u + uint32_t(lane);
+        const uint32_t wn = row0 + ((word + 1u) % wpr) * 32u + uint32_t(lane);
+        const unsigned long long kp = inside ? pixkey[wp] : 0ull, kn = inside ? pixkey[wn] : 0ull;
+        const uint32_t ip = ~__ballot_sync(0xFFFFFFFFu, kp != ~0ull), is = ~bits,
+                       in = ~__ballot_sync(0xFFFFFFFFu, kn != ~0ull);
+        const unsigned long long right = (uint64_t(is) >> lane) | (uint64_t(in) << (32 - lane));
+        const unsigned long long left = ((uint64_t(is) << 32) | ip) & ((2ull << (32 + lane)) - 1ull);
+        const int dr = right ? __ffsll(static_cast<long long>(right)) - 1 : 64;
+        const int dl = left ? (32 + lane) - (63 - __clzll(static_cast<long long>(left))) : 64;
+        rd = min(min(dr, dl), kRowDistMax + 1);
+    }
     if (!inside) return;
     pg.nxt[g][p] = ~0ull;  // the other half is clean for the slot's next projection
     const float d0 = key_depth(k);
     pg.depth[o + p] = d0;
-    {   // row distance to the nearest pixel without a return (band kernel's valid radius)
+    if (rd >= 0) {
+        pg.rowdist[o + p] = uint8_t(rd);
+    } else {
         const int u = int(p % W);
         const unsigned long long* row = pixkey + (p - u);
         int d = 0;
