@@ -970,7 +970,9 @@ def main():
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--sweep-widths", type=int, nargs="*",
                     default=[80, 160, 320, 640, 1280, 2560, 5120, 10240, 16384])
-    ap.add_argument("--sweep-scans", type=int, default=64)
+    ap.add_argument("--sweep-scans", type=int, default=16,
+                    help="scans per timed pass (16: x in 0..4 m of the room; from 64 on the passes "
+                         "include the wall-adjacent stretch x ~ 8..10 m, fallback-bound)")
     ap.add_argument("--emulate-ranks", type=int, nargs="*", default=None,
                     help="emulate the multi-GPU data plane with these rank counts on one GPU")
     ap.add_argument("--no-e2e", action="store_true")
