@@ -596,6 +596,9 @@ __device__ __forceinline__ uint32_t fold_one(const GroupConsts& c, const FramePo
 // descriptors with more records than this take a warp (A/B: 1 beats 3 and 8 at N = 1 and
 // removes most of the fold's per-frame floor at 8 emulated ranks)
 constexpr uint32_t kWarpRecs = SVX_WARP_RECS;
+#ifndef SVX_FB_SERIAL_SMEM
+#define SVX_FB_SERIAL_SMEM 1
+#endif
 __device__ __forceinline__ uint32_t fold_records_warp(const GroupConsts& c, const FramePose& f, uint32_t g,
                                                       svx_tsdf_voxel* vp, d3 center, const ScanSlots& sc,
                                                       const unsigned long long* __restrict__ recs, uint32_t nrec,
@@ -604,6 +607,44 @@ __device__ __forceinline__ uint32_t fold_records_warp(const GroupConsts& c, cons
     svx_tsdf_voxel vox = load_voxel(vp);
     Accum acc{0.0, 0.0, 0.0, 0.0, 0.0};
     bool measured = false;
+#if SVX_FB_SERIAL_SMEM
+    // the lanes' terms through shared memory; lane 0 sums them in record order (the serial
+    // part is then the FP64 adds alone: a term not measured adds +0.0, the sums' identity,
+    // as they never hold -0.0)
+    __shared__ float4 s_ta[kThreads / 32][32];
+    __shared__ float2 s_tb[kThreads / 32][32];
+    const int wq = threadIdx.x >> 5;
+    unsigned any = 0;
+    for (uint32_t j0 = 0; j0 < nrec; j0 += 32u) {  // (warp-uniform)
+        Term t{0.f, 0.f, 0.f, 0.f, 0.f, 0u};
+        if (j0 + uint32_t(lane) < nrec)
+            t = measure_term(c, f.origin, cache, rec_pixel(recs[j0 + lane], c.pbits), center, vox);
+        s_ta[wq][lane] = make_float4(t.wg, t.w, t.nx, t.ny);
+        s_tb[wq][lane] = make_float2(t.nz, __uint_as_float(t.flags));
+        any |= __ballot_sync(0xFFFFFFFFu, (t.flags & 1u) != 0u);
+        __syncwarp();
+        if (lane == 0) {
+            const uint32_t n = min(32u, nrec - j0);
+#pragma unroll 4
+            for (uint32_t k = 0; k < n; ++k) {
+                const float4 a = s_ta[wq][k];
+                const float2 b = s_tb[wq][k];
+                const uint32_t fl = __float_as_uint(b.y);
+                const bool m1 = (fl & 1u) != 0u, m2 = (fl & 3u) == 3u;
+                acc.wd += m1 ? double(a.x) : 0.0;
+                acc.w += m1 ? double(a.y) : 0.0;
+                acc.wx += m2 ? double(a.z) : 0.0;
+                acc.wy += m2 ? double(a.w) : 0.0;
+                acc.wz += m2 ? double(b.x) : 0.0;
+            }
+        }
+        __syncwarp();
+    }
+    if (!any || lane != 0) return 0;
+    fold(vox, acc);
+    store_voxel(vp, vox);
+    return 1;
+#else
     for (uint32_t j0 = 0; j0 < nrec; j0 += 32u) {  // (warp-uniform)
         Term t{0.f, 0.f, 0.f, 0.f, 0.f, 0u};
         if (j0 + uint32_t(lane) < nrec)
@@ -628,6 +669,7 @@ __device__ __forceinline__ uint32_t fold_records_warp(const GroupConsts& c, cons
     if (lane != 0) return 0;
     store_voxel(vp, vox);
     return 1;
+#endif
 }
 
 // Hash find-or-insert of a block key; a new block takes the next pool index.
@@ -1065,6 +1107,27 @@ k_band(const __grid_constant__ GroupParams gp, const ScanSlots sc, HashView h,
     }
 }
 
+// End of the run of keys equal to `run` (on their bits above pb) that starts at pos in the
+// sorted a[0..n): galloping then binary search, O(log run) loads (a voxel thousands of rays
+// cross in one frame is one long run).
+__device__ inline uint32_t run_end(const unsigned long long* __restrict__ a, uint32_t pos, uint32_t n,
+                                   unsigned long long run, uint32_t pb) {
+    uint32_t lo = pos + 1, step = 1;  // a[lo - 1] is in the run
+    uint32_t hi = lo;
+    while (hi < n && (a[hi] >> pb) == run) {
+        lo = hi + 1;
+        hi = (n - hi > step) ? hi + step : n;
+        step *= 2;
+    }
+    // a[lo - 1] in the run; a[hi] (hi < n) past it, or hi = n
+    while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        if ((a[mid] >> pb) == run) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
 // The group's fallback records, sorted by (block, voxel, frame, pixel) (a device radix sort
 // over the record bits precedes this kernel: O(records) whatever the number of rays per
 // voxel), cut into (voxel, frame) runs: one descriptor per run (pool index, voxel | frame
@@ -1083,8 +1146,7 @@ k_fb_runs(const unsigned long long* __restrict__ sorted, unsigned long long* __r
         const unsigned long long k = sorted[i];
         const unsigned long long run = k >> pb;  // (block, voxel, frame)
         if (i > 0 && (sorted[i - 1] >> pb) == run) continue;
-        uint32_t j = i + 1;
-        while (j < n && (sorted[j] >> pb) == run) ++j;
+        const uint32_t j = run_end(sorted, i, n, run, pb);
         const uint32_t g = uint32_t(run) & 15u, lin = uint32_t(run >> 4) & 511u, idx = uint32_t(run >> 13);
         // frame g's list (its fold reads only its own descriptors)
         fbdesc[uint64_t(g) * rec_cap + atomicAdd(&fctr[g * kFC + FC_FBV], 1u)] = make_uint4(idx, lin | (g << 16), i, j - i);
@@ -1281,8 +1343,7 @@ k_fb_sort(const uint32_t* __restrict__ fbblocks, uint32_t* __restrict__ fbcnt, c
         for (uint32_t pos = threadIdx.x; pos < cnt; pos += kThreads) {
             const unsigned long long run = bk[pos] >> pb;  // (block, voxel, frame)
             if (pos > 0 && (bk[pos - 1] >> pb) == run) continue;
-            uint32_t e = pos + 1;
-            while (e < cnt && (bk[e] >> pb) == run) ++e;
+            const uint32_t e = run_end(bk, pos, cnt, run, pb);
             const uint32_t g = uint32_t(run) & 15u, lin = uint32_t(run >> 4) & 511u;
             fbdesc[uint64_t(g) * rec_cap + atomicAdd(&fctr[g * kFC + FC_FBV], 1u)] =
                 make_uint4(idx, lin | (g << 16), start + pos, e - pos);
